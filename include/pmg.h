@@ -1,0 +1,165 @@
+/*
+ * pmg.h -- C ABI of the B200-native p-multigrid hot path of arXiv 1808.03595
+ * ("Factorizing the factorization -- a spectral-element solver for elliptic equations with
+ * linear operation count", Huismann, Stiller, Froehlich).  Citations: P:n = line n of the
+ * paper's LaTeX source.
+ *
+ * Problem (Eq. helmholtz_equation):  lambda u - Laplace(u) = f on a box of
+ * k1 x k2 x k3 cuboidal spectral elements of degree p (widths per direction), with
+ * homogeneous Dirichlet conditions on the box boundary.  All arithmetic is FP64.
+ *
+ * Conventions shared by every call
+ *  - Every call returns pmg_status; PMG_OK = 0.  No C++ exception crosses the ABI.  On an
+ *    error the thread-local message of pmg_last_error() says what was wrong.
+ *  - Vector arguments are caller-owned DEVICE pointers (cudaMalloc / torch CUDA tensors),
+ *    unless the name ends in _host.  The library never frees or reallocates them.  All work
+ *    is enqueued on the stream given in pmg_options.stream (NULL = legacy default stream)
+ *    and is asynchronous unless stated otherwise.  The context owns its tables and
+ *    workspaces, allocated in pmg_setup; no other call allocates device memory.
+ *  - "grid" vectors hold one value per global GLL node: N_d = k_d p + 1 nodes per direction
+ *    (boundary included), flat index i1 + N1 (i2 + N2 i3), x1 fastest.
+ *  - "skeleton" (condensed, hat) vectors hold the element-boundary unknowns of one level in
+ *    the library's record layout: one record per mesh vertex
+ *    (v1, v2, v3), 0 <= v_d <= k_d, record index v1 + (k1+1)(v2 + (k2+1) v3); a record holds
+ *    the interiors of the three faces and three edges leaving the vertex in +x_d direction,
+ *    then the vertex itself: [f1: (p-1)^2][f2: (p-1)^2][f3: (p-1)^2][e1: p-1][e2][e3][vertex].
+ *    Length = (k1+1)(k2+1)(k3+1) * (3(p-1)^2 + 3(p-1) + 1) doubles (pmg_level_info).
+ *    Entries that are not free unknowns (on the Dirichlet boundary or outside the box) are
+ *    zero on input and are written as zero on output.
+ *  - Levels: l = 0 .. L with degrees p_l = p0 2^l (l < L), p_L = p, L = ceil(log2(p/p0))
+ *    (reading R10).  Level L is the finest.
+ */
+#ifndef PMG_H
+#define PMG_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pmg_ctx pmg_ctx; /* opaque; owns all tables and workspaces */
+
+typedef enum {
+  PMG_OK = 0,
+  PMG_EINVAL = -1,      /* invalid argument (message says which) */
+  PMG_ECUDA = -2,       /* a CUDA runtime call or kernel launch failed */
+  PMG_ENCCL = -3,       /* reserved for the multi-GPU path */
+  PMG_ENOCONV = -4,     /* pmg_solve: max_cycles reached before the tolerance (report filled) */
+  PMG_EBREAKDOWN = -5,  /* coarse CG: p^T H p <= 0 */
+  PMG_ENOMEM = -6       /* device allocation failed in pmg_setup */
+} pmg_status;
+
+typedef struct {
+  int p0;             /* coarse degree, default 2 */
+  int weight_degree;  /* degree of the weight polynomial, default 7; only 7 supported */
+  int schedule;       /* 0: nu_pre = nu_post = 1 ("MG"); 1: 2^(L-l) */
+  double coarse_rtol; /* coarse CG relative tolerance, default 1e-8 (reading R11) */
+  int coarse_maxit;   /* coarse CG iteration cap, default 10000 */
+  int coarse_check;   /* coarse CG: host convergence poll every this many iterations, default 8 */
+  int rank, nranks;   /* z-slab decomposition; only nranks = 1 is implemented in this version */
+  const void* nccl_id;/* reserved (128-byte ncclUniqueId) */
+  void* stream;       /* cudaStream_t; NULL = default stream */
+} pmg_options;
+
+typedef struct {
+  int cycles;         /* V-cycles performed (n_10 of P:636 when rtol = 1e-10) */
+  int converged;      /* 1 if ||r_n|| <= rtol ||r_0|| */
+  double r0, r_final; /* ||r_hat||_2 over free skeleton unknowns, before / after */
+  double rho;         /* (r_final / r0)^(1/cycles) */
+  int coarse_iters;   /* total coarse CG iterations over the whole solve */
+  double* history;    /* optional caller array (host) receiving ||r_n||, n = 0..cycles */
+  int history_cap;    /* its capacity */
+} pmg_report;
+
+/* Fill *opt with the defaults listed above. */
+void pmg_default_options(pmg_options* opt);
+
+/* Build the level hierarchy (host: GLL, 1-D mass/stiffness, element and star generalised
+ * eigenpairs with identity padding at the boundary, weights, interpolation matrices, coarse
+ * diagonal; device: tables and workspaces).  n_e[3] = (k1, k2, k3) >= 1; widths[d] is a HOST
+ * array of k_d positive finite element widths; p in [1, 32] (p >= p0 for pmg_vcycle /
+ * pmg_solve); lambda >= 0; opt may be NULL.  Errors: PMG_EINVAL, PMG_ENOMEM, PMG_ECUDA. */
+pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths[3], int p,
+                     double lambda, const pmg_options* opt);
+pmg_status pmg_destroy(pmg_ctx* ctx);
+
+int pmg_num_levels(const pmg_ctx* ctx); /* L + 1, or -1 if ctx is NULL */
+/* degree p_l, skeleton vector length (doubles, incl. padding records) and grid vector length */
+pmg_status pmg_level_info(const pmg_ctx* ctx, int level, int* degree, long long* n_skel,
+                          long long* n_grid);
+/* 1-D GLL node coordinates of level `level` along direction d (HOST array of k_d p_l + 1). */
+pmg_status pmg_grid_coords(const pmg_ctx* ctx, int level, int d, double* coords_host);
+
+/* r_hat = f_hat - H_hat_l u_hat  (H_hat_l = sum_e Q_e (H_BB - H_BI H_II^-1 H_IB) Q_e^T,
+ * P:117-123, evaluated matrix-free in O(p^3) per element: DESIGN.md "Residual kernel").
+ * f_hat may be NULL, then r_hat = H_hat_l u_hat (operator apply).  u_hat and r_hat must not alias. */
+pmg_status pmg_residual(pmg_ctx* ctx, int level, const double* u_hat, const double* f_hat,
+                        double* r_hat);
+
+/* u_hat += Smoother(r_hat): Alg. 2 with the star inverse of Alg. 1,
+ * weights W_i, 8 race-free vertex colours.  r_hat and u_hat must not alias. */
+pmg_status pmg_smooth(pmg_ctx* ctx, int level, const double* r_hat, double* u_hat);
+
+/* f_coarse = J_hat_l^T r_fine (restriction, P:439, P:464 read as J_hat_l^T); level = fine level >= 1;
+ * r_fine lives on level `level`, f_coarse on level-1 (overwritten). */
+pmg_status pmg_restrict(pmg_ctx* ctx, int level, const double* r_fine, double* f_coarse);
+
+/* u_fine += J_hat_l u_coarse (prolongation of the correction); level >= 1. */
+pmg_status pmg_prolong(pmg_ctx* ctx, int level, const double* u_coarse, double* u_fine);
+
+/* One V-cycle of Alg. 3 on the finest level: u_hat <- MultigridCycle(u_hat, f_hat).
+ * With L = 0 it is u_hat <- u_hat + CG(f_hat - H_hat_0 u_hat) (reading R10b). */
+pmg_status pmg_vcycle(pmg_ctx* ctx, double* u_hat, const double* f_hat);
+
+/* f_hat = F_B - H_BI H_II^-1 F_I on the finest level (Alg. 4 line 2).  F_full is the grid
+ * vector of the discrete weak right-hand side F = B f (pmg_weak_rhs); Dirichlet entries ignored. */
+pmg_status pmg_condense(pmg_ctx* ctx, const double* F_full, double* f_hat);
+
+/* u_full = (u_hat, H_II^-1 (F_I - H_IB u_hat)) on the finest level (Alg. 4 last line);
+ * Dirichlet entries of u_full are written as 0. */
+pmg_status pmg_recover(pmg_ctx* ctx, const double* u_hat, const double* F_full, double* u_full);
+
+/* Alg. 4: condense, V-cycles from u_hat = 0 until ||r_hat|| <= rtol ||r_hat_0|| (reading R12) or
+ * max_cycles, recover.  Synchronises the stream once per cycle to read the residual norm.
+ * rep may be NULL.  Returns PMG_ENOCONV (with rep filled and u_full written) if not converged. */
+pmg_status pmg_solve(pmg_ctx* ctx, const double* F_full, double* u_full, double rtol,
+                     int max_cycles, pmg_report* rep);
+
+/* Same as pmg_solve with HOST buffers: copies F_full_host (grid vector) to the device, solves,
+ * copies u_full back to u_full_host, and synchronises.  Host buffers may be pageable or pinned. */
+pmg_status pmg_solve_host(pmg_ctx* ctx, const double* F_full_host, double* u_full_host,
+                          double rtol, int max_cycles, pmg_report* rep);
+
+/* F = B f: GLL-lumped assembled mass times the nodal values f_nodal (grid vectors, finest level;
+ * reading R8).  Dirichlet entries of F are written as 0. */
+pmg_status pmg_weak_rhs(pmg_ctx* ctx, const double* f_nodal, double* F_full);
+
+/* Layout converters between grid vectors and skeleton vectors of level `level`.
+ * skel_from_grid copies free skeleton points (others 0); skel_to_grid writes the skeleton
+ * values at skeleton points and 0 at element-interior and Dirichlet points. */
+pmg_status pmg_skel_from_grid(pmg_ctx* ctx, int level, const double* grid, double* skel);
+pmg_status pmg_skel_to_grid(pmg_ctx* ctx, int level, const double* skel, double* grid);
+
+/* sqrt(sum of squares) of a skeleton vector of `level` (deterministic two-pass reduction);
+ * synchronises the stream and returns the value in *out_host. */
+pmg_status pmg_norm(pmg_ctx* ctx, int level, const double* x_hat, double* out_host);
+
+/* Number of kernels this context launched since setup (all streams), for the bench's
+ * gpu_launches count. */
+long long pmg_launch_count(const pmg_ctx* ctx);
+
+/* Kernel timing with CUDA events recorded on the context's stream (bench.py roofline).
+ * pmg_timing_enable(ctx, 1) resets and starts bracketing every smoother sweep (the 8 colour
+ * launches of the star kernel) and every residual evaluation (element kernel + gather) with
+ * events; 0 stops.  pmg_timing_read synchronises the stream and returns the summed elapsed
+ * milliseconds and the number of bracketed calls of `kind`:
+ *   0 smoother sweep on the finest level, 1 residual on the finest level,
+ *   2 smoother sweeps on all levels,      3 residuals on all levels (incl. coarse CG applies). */
+pmg_status pmg_timing_enable(pmg_ctx* ctx, int enable);
+pmg_status pmg_timing_read(pmg_ctx* ctx, int kind, double* total_ms, long long* count);
+
+const char* pmg_last_error(void); /* thread-local message of the last failing call */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PMG_H */

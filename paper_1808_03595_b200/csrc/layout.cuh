@@ -1,0 +1,75 @@
+// Device helpers for the skeleton record layout.
+#pragma once
+#include "pmg_internal.h"
+
+namespace pmg {
+
+__host__ __device__ inline int off_face(int m, int d) { return d * m * m; }
+__host__ __device__ inline int off_edge(int m, int d) { return 3 * m * m + d * m; }
+__host__ __device__ inline int off_vert(int m) { return 3 * m * m + 3 * m; }
+
+// Skeleton point (global GLL indices, 0 <= g_d <= k_d p, at least one g_d a multiple of p)
+// -> index into a skeleton vector.
+__device__ __forceinline__ long long skel_index(const LevelGeom& g, int g1, int g2, int g3) {
+  const int p = g.p, m = g.m;
+  const int r1 = g1 / p, t1 = g1 - r1 * p;
+  const int r2 = g2 / p, t2 = g2 - r2 * p;
+  const int r3 = g3 / p, t3 = g3 - r3 * p;
+  const long long rec = r1 + (long long)g.V1 * (r2 + (long long)g.V2 * r3);
+  int off;
+  if (t1 == 0) {
+    if (t2 == 0) off = (t3 == 0) ? off_vert(m) : off_edge(m, 2) + t3 - 1;
+    else if (t3 == 0) off = off_edge(m, 1) + t2 - 1;
+    else off = off_face(m, 0) + (t3 - 1) * m + (t2 - 1);
+  } else if (t2 == 0) {
+    off = (t3 == 0) ? off_edge(m, 0) + t1 - 1 : off_face(m, 1) + (t3 - 1) * m + (t1 - 1);
+  } else {
+    off = off_face(m, 2) + (t2 - 1) * m + (t1 - 1);
+  }
+  return rec * g.RS + off;
+}
+
+__device__ __forceinline__ bool inside(const LevelGeom& g, int g1, int g2, int g3) {
+  return g1 >= 0 && g2 >= 0 && g3 >= 0 && g1 <= g.k1 * g.p && g2 <= g.k2 * g.p && g3 <= g.k3 * g.p;
+}
+__device__ __forceinline__ bool is_free(const LevelGeom& g, int g1, int g2, int g3) {
+  return g1 > 0 && g2 > 0 && g3 > 0 && g1 < g.k1 * g.p && g2 < g.k2 * g.p && g3 < g.k3 * g.p;
+}
+
+// Skeleton-vector entry -> record vertex, entity type (0-2 faces, 3-5 edges, 6 vertex),
+// local indices (a = slow, b = fast for faces; a for edges) and global point.
+struct Entry {
+  int v1, v2, v3, type, a, b, g1, g2, g3;
+};
+
+__device__ __forceinline__ Entry decode_entry(const LevelGeom& g, long long idx) {
+  Entry E;
+  const int m = g.m, p = g.p;
+  long long rec = idx / g.RS;
+  int o = (int)(idx - rec * g.RS);
+  E.v1 = (int)(rec % g.V1);
+  long long r2 = rec / g.V1;
+  E.v2 = (int)(r2 % g.V2);
+  E.v3 = (int)(r2 / g.V2);
+  E.g1 = E.v1 * p; E.g2 = E.v2 * p; E.g3 = E.v3 * p;
+  E.a = 0; E.b = 0;
+  if (o < 3 * m * m) {
+    E.type = o / (m * m);
+    int r = o - E.type * m * m;
+    E.a = r / m; E.b = r - E.a * m;
+    if (E.type == 0) { E.g3 += E.a + 1; E.g2 += E.b + 1; }
+    else if (E.type == 1) { E.g3 += E.a + 1; E.g1 += E.b + 1; }
+    else { E.g2 += E.a + 1; E.g1 += E.b + 1; }
+  } else if (o < 3 * m * m + 3 * m) {
+    int r = o - 3 * m * m;
+    int d = r / m;
+    E.type = 3 + d;
+    E.a = r - d * m;
+    if (d == 0) E.g1 += E.a + 1; else if (d == 1) E.g2 += E.a + 1; else E.g3 += E.a + 1;
+  } else {
+    E.type = 6;
+  }
+  return E;
+}
+
+}  // namespace pmg

@@ -1,0 +1,676 @@
+// C-ABI entry points (include/pmg.h) and the host orchestration of Alg. 2-4:
+// smoother colour sweep, V-cycle, coarse CG driver, solve.  Citations: P:n = PAPER.md line n.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstddef>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/pmg.h"
+#include "kernels.cuh"
+#include "pmg_internal.h"
+
+using namespace pmg;
+
+namespace {
+thread_local std::string g_err;
+
+pmg_status fail(pmg_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+constexpr int kThreads = 256;
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs; fixed so reductions are deterministic
+
+int grid_for(long long n) {
+  long long b = (n + kThreads - 1) / kThreads;
+  return (int)std::max<long long>(1, std::min<long long>(b, 148LL * 16));
+}
+
+struct DevLevel {
+  LevelGeom g;
+  double* etab = nullptr;
+  double* stab = nullptr;
+  double* Jint = nullptr;
+  double* u = nullptr;
+  double* f = nullptr;
+  double* r = nullptr;
+};
+
+}  // namespace
+
+struct pmg_ctx {
+  pmg_options opt;
+  cudaStream_t st = nullptr;
+  double lam = 0.0;
+  int L = 0;
+  std::vector<HostLevel> H;
+  std::vector<DevLevel> D;
+  double* Y = nullptr;       // element workspace  max_l nelem * YS
+  double* Z = nullptr;       // restriction workspace
+  double* cube = nullptr;    // condense/recover cube scratch (large p)
+  int cube_blocks = 0;
+  bool cube_in_smem = true;
+  bool star_s_smem = true;
+  double* part = nullptr;    // reduction partials (2 x kRedBlocks)
+  double* dres = nullptr;    // device scalar results
+  PcgState* pcg = nullptr;
+  double *cx = nullptr, *cr = nullptr, *cz = nullptr, *cp = nullptr, *cq = nullptr, *dinv = nullptr;
+  double* bm[3] = {nullptr, nullptr, nullptr};
+  double* Fdev = nullptr;    // grid buffers for pmg_solve_host
+  double* Udev = nullptr;
+  long long n_grid = 0;
+  long long launches = 0;
+  int last_coarse_its = 0;
+  long long coarse_its_total = 0;
+  // event timing (pmg_timing_enable)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  struct Mark { int base; bool top; cudaEvent_t a, b; };   // base 0: smoother sweep, 1: residual
+  std::vector<Mark> ev_marks;
+};
+
+namespace {
+cudaEvent_t ev_get(pmg_ctx* c) {
+  if (!c->ev_pool.empty()) { cudaEvent_t e = c->ev_pool.back(); c->ev_pool.pop_back(); return e; }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+void ev_reset(pmg_ctx* c) {
+  for (auto& mk : c->ev_marks) { c->ev_pool.push_back(mk.a); c->ev_pool.push_back(mk.b); }
+  c->ev_marks.clear();
+}
+struct TimedRegion {  // brackets one call with events on the context stream when timing is on
+  pmg_ctx* c; int base; bool top; cudaEvent_t a = nullptr;
+  TimedRegion(pmg_ctx* c_, int base_, bool top_) : c(c_), base(base_), top(top_) {
+    if (c->timing) { a = ev_get(c); cudaEventRecord(a, c->st); }
+  }
+  ~TimedRegion() {
+    if (!a) return;
+    cudaEvent_t b = ev_get(c);
+    cudaEventRecord(b, c->st);
+    c->ev_marks.push_back({base, top, a, b});
+  }
+};
+}  // namespace
+
+#define LAUNCH_CHECK(ctx)                                                                   \
+  do {                                                                                      \
+    (ctx)->launches++;                                                                      \
+    cudaError_t e_ = cudaGetLastError();                                                    \
+    if (e_ != cudaSuccess) return fail(PMG_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CUDA_CHECK(call)                                                                    \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) return fail(PMG_ECUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+namespace {
+
+int* done_ptr(pmg_ctx* c) { return reinterpret_cast<int*>(reinterpret_cast<char*>(c->pcg) + offsetof(PcgState, done)); }
+
+// ---------------------------------------------------------------- level operators (device)
+pmg_status residual_dev(pmg_ctx* c, int l, const double* u, const double* f, double* r, const int* done = nullptr) {
+  const DevLevel& D = c->D[l];
+  TimedRegion tr(c, 1, l == c->L);
+  size_t sm = elem_apply_smem(D.g.p, D.g.ET);
+  k_elem_apply<<<(unsigned)D.g.nelem, kThreads, sm, c->st>>>(D.g, u, D.etab, c->lam, c->Y, done);
+  LAUNCH_CHECK(c);
+  k_gather_resid<<<grid_for(D.g.nskel), kThreads, 0, c->st>>>(D.g, c->Y, f, r, done);
+  LAUNCH_CHECK(c);
+  return PMG_OK;
+}
+
+pmg_status smooth_dev(pmg_ctx* c, int l, const double* r, double* u) {
+  const DevLevel& D = c->D[l];
+  const LevelGeom& g = D.g;
+  TimedRegion tr(c, 0, l == c->L);
+  size_t sm = star_smem(g.p, c->star_s_smem);
+  for (int col = 0; col < 8; ++col) {   // 8 vertex colours (parity), race-free
+    int c1 = col & 1, c2 = (col >> 1) & 1, c3 = (col >> 2) & 1;
+    int n1 = (g.k1 - c1) / 2 + 1, n2 = (g.k2 - c2) / 2 + 1, n3 = (g.k3 - c3) / 2 + 1;
+    long long nb = (long long)n1 * n2 * n3;
+    k_star<<<(unsigned)nb, kThreads, sm, c->st>>>(g, c1, c2, c3, n1, n2, r, u, D.stab, c->lam, c->star_s_smem ? 1 : 0);
+    LAUNCH_CHECK(c);
+  }
+  return PMG_OK;
+}
+
+int zs_of(int pc) { int qc = pc + 1; return 3 * qc * qc + 3 * qc + 1; }
+
+pmg_status restrict_dev(pmg_ctx* c, int l, const double* rf, double* fc) {
+  const DevLevel& F = c->D[l];
+  const DevLevel& C = c->D[l - 1];
+  k_restrict_local<<<(unsigned)F.g.nrec, kThreads, transfer_smem(F.g.p, C.g.p), c->st>>>(F.g, C.g.p, F.Jint, rf, c->Z);
+  LAUNCH_CHECK(c);
+  k_restrict_gather<<<grid_for(C.g.nskel), kThreads, 0, c->st>>>(C.g, c->Z, fc);
+  LAUNCH_CHECK(c);
+  return PMG_OK;
+}
+
+pmg_status prolong_dev(pmg_ctx* c, int l, const double* uc, double* uf) {
+  const DevLevel& F = c->D[l];
+  const DevLevel& C = c->D[l - 1];
+  k_prolong<<<(unsigned)F.g.nrec, kThreads, transfer_smem(F.g.p, C.g.p), c->st>>>(F.g, C.g, F.Jint, uc, uf);
+  LAUNCH_CHECK(c);
+  return PMG_OK;
+}
+
+pmg_status zero_dev(pmg_ctx* c, double* x, long long n) {
+  k_zero<<<grid_for(n), kThreads, 0, c->st>>>(x, n);
+  LAUNCH_CHECK(c);
+  return PMG_OK;
+}
+
+pmg_status dot_dev(pmg_ctx* c, const double* a, const double* b, long long n, double* out_dev) {
+  k_dot_partial<<<kRedBlocks, kThreads, 0, c->st>>>(a, b, n, c->part, nullptr);
+  LAUNCH_CHECK(c);
+  k_sum_final<<<1, 1024, 0, c->st>>>(c->part, kRedBlocks, out_dev);
+  LAUNCH_CHECK(c);
+  return PMG_OK;
+}
+
+pmg_status norm_host(pmg_ctx* c, const double* x, long long n, double* out) {
+  pmg_status s = dot_dev(c, x, x, n, c->dres);
+  if (s) return s;
+  double h = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&h, c->dres, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CUDA_CHECK(cudaStreamSynchronize(c->st));
+  *out = std::sqrt(h);
+  return PMG_OK;
+}
+
+// Jacobi-PCG on H_hat_0 x = b from x = 0 (reading R11); device-resident scalars, the host
+// polls the done flag every opt.coarse_check iterations.  Stops exactly at the first iteration
+// with ||r|| <= rtol ||b|| (or at coarse_maxit), like the oracle.
+pmg_status pcg_dev(pmg_ctx* c, const double* b, double* x) {
+  const DevLevel& D = c->D[0];
+  const long long n = D.g.nskel;
+  double* part2 = c->part + kRedBlocks;
+  int* done = done_ptr(c);
+  k_pcg_init<<<kRedBlocks, kThreads, 0, c->st>>>(b, c->dinv, x, c->cr, c->cz, c->cp, n, c->part, part2);
+  LAUNCH_CHECK(c);
+  k_pcg_init_final<<<1, 1024, 0, c->st>>>(c->part, part2, kRedBlocks, c->pcg);
+  LAUNCH_CHECK(c);
+  PcgState hs;
+  const int chk = std::max(1, c->opt.coarse_check);
+  for (;;) {
+    for (int k = 0; k < chk; ++k) {
+      pmg_status s = residual_dev(c, 0, c->cp, nullptr, c->cq, done);   // q = H p
+      if (s) return s;
+      k_dot_partial<<<kRedBlocks, kThreads, 0, c->st>>>(c->cp, c->cq, n, c->part, done);
+      LAUNCH_CHECK(c);
+      k_pcg_alpha<<<1, 1024, 0, c->st>>>(c->part, kRedBlocks, c->pcg);
+      LAUNCH_CHECK(c);
+      k_pcg_update<<<kRedBlocks, kThreads, 0, c->st>>>(x, c->cr, c->cp, c->cq, n, c->pcg, c->part);
+      LAUNCH_CHECK(c);
+      k_pcg_check<<<1, 1024, 0, c->st>>>(c->part, kRedBlocks, c->pcg, c->opt.coarse_rtol, c->opt.coarse_maxit);
+      LAUNCH_CHECK(c);
+      k_pcg_precond<<<kRedBlocks, kThreads, 0, c->st>>>(c->cr, c->dinv, c->cz, n, c->pcg, c->part);
+      LAUNCH_CHECK(c);
+      k_pcg_beta<<<1, 1024, 0, c->st>>>(c->part, kRedBlocks, c->pcg);
+      LAUNCH_CHECK(c);
+      k_pcg_pdir<<<kRedBlocks, kThreads, 0, c->st>>>(c->cp, c->cz, n, c->pcg);
+      LAUNCH_CHECK(c);
+    }
+    CUDA_CHECK(cudaMemcpyAsync(&hs, c->pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, c->st));
+    CUDA_CHECK(cudaStreamSynchronize(c->st));
+    if (hs.done) break;
+  }
+  c->last_coarse_its = hs.its;
+  c->coarse_its_total += hs.its;
+  if (hs.breakdown) return fail(PMG_EBREAKDOWN, "coarse CG breakdown: p^T H p <= 0");
+  return PMG_OK;
+}
+
+int nu_of(const pmg_ctx* c, int l) { return c->opt.schedule == 0 ? 1 : (1 << (c->L - l)); }
+
+// Alg. 3.  r_top_valid: D[L].r already holds f - H u (saves one residual).
+pmg_status vcycle_dev(pmg_ctx* c, double* u, const double* f, bool r_top_valid) {
+  const int L = c->L;
+  pmg_status s;
+  if (L == 0) {  // reading R10b: u <- u + CG(f - H_0 u)
+    DevLevel& D = c->D[0];
+    if (!r_top_valid && (s = residual_dev(c, 0, u, f, D.r))) return s;
+    if ((s = pcg_dev(c, D.r, c->cx))) return s;
+    k_axpy<<<grid_for(D.g.nskel), kThreads, 0, c->st>>>(u, c->cx, 1.0, D.g.nskel);
+    LAUNCH_CHECK(c);
+    return PMG_OK;
+  }
+  for (int l = L; l >= 1; --l) {
+    DevLevel& D = c->D[l];
+    double* ul = (l == L) ? u : D.u;
+    const double* fl = (l == L) ? f : D.f;
+    bool r_valid = (l == L) && r_top_valid;
+    bool u_zero = false;
+    if (l != L) {
+      if ((s = zero_dev(c, ul, D.g.nskel))) return s;
+      u_zero = true;
+    }
+    for (int i = 0; i < nu_of(c, l); ++i) {
+      const double* rin = D.r;
+      if (u_zero) rin = fl;                       // f - H 0 = f exactly
+      else if (!r_valid && (s = residual_dev(c, l, ul, fl, D.r))) return s;
+      if ((s = smooth_dev(c, l, rin, ul))) return s;
+      r_valid = false;
+      u_zero = false;
+    }
+    if ((s = residual_dev(c, l, ul, fl, D.r))) return s;
+    if ((s = restrict_dev(c, l, D.r, c->D[l - 1].f))) return s;
+  }
+  if ((s = pcg_dev(c, c->D[0].f, c->D[0].u))) return s;
+  for (int l = 1; l <= L; ++l) {
+    DevLevel& D = c->D[l];
+    double* ul = (l == L) ? u : D.u;
+    const double* fl = (l == L) ? f : D.f;
+    if ((s = prolong_dev(c, l, c->D[l - 1].u, ul))) return s;
+    for (int i = 0; i < nu_of(c, l); ++i) {
+      if ((s = residual_dev(c, l, ul, fl, D.r))) return s;
+      if ((s = smooth_dev(c, l, D.r, ul))) return s;
+    }
+  }
+  return PMG_OK;
+}
+
+pmg_status condense_dev(pmg_ctx* c, const double* F, double* fhat) {
+  const DevLevel& D = c->D[c->L];
+  size_t sm = condense_smem(D.g.p, D.g.ET, c->cube_in_smem);
+  int nb = c->cube_in_smem ? (int)std::min<long long>(D.g.nelem, 148LL * 8) : c->cube_blocks;
+  k_condense_elem<<<nb, kThreads, sm, c->st>>>(D.g, F, D.etab, c->lam, c->Y, c->cube_in_smem ? nullptr : c->cube);
+  LAUNCH_CHECK(c);
+  k_condense_gather<<<grid_for(D.g.nskel), kThreads, 0, c->st>>>(D.g, F, c->Y, fhat);
+  LAUNCH_CHECK(c);
+  return PMG_OK;
+}
+
+pmg_status recover_dev(pmg_ctx* c, const double* uhat, const double* F, double* ufull) {
+  const DevLevel& D = c->D[c->L];
+  k_skel_to_grid<<<grid_for(c->n_grid), kThreads, 0, c->st>>>(D.g, uhat, ufull);
+  LAUNCH_CHECK(c);
+  size_t sm = recover_smem(D.g.p, D.g.ET, c->cube_in_smem);
+  int nb = c->cube_in_smem ? (int)std::min<long long>(D.g.nelem, 148LL * 8) : c->cube_blocks;
+  k_recover_elem<<<nb, kThreads, sm, c->st>>>(D.g, F, uhat, D.etab, c->lam, ufull, c->cube_in_smem ? nullptr : c->cube);
+  LAUNCH_CHECK(c);
+  return PMG_OK;
+}
+
+pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, int max_cycles, pmg_report* rep) {
+  DevLevel& D = c->D[c->L];
+  pmg_status s;
+  c->coarse_its_total = 0;
+  if ((s = condense_dev(c, F, D.f))) return s;
+  if ((s = zero_dev(c, D.u, D.g.nskel))) return s;
+  if ((s = residual_dev(c, c->L, D.u, D.f, D.r))) return s;
+  double r0, rn;
+  if ((s = norm_host(c, D.r, D.g.nskel, &r0))) return s;
+  rn = r0;
+  int cycles = 0;
+  if (rep && rep->history && rep->history_cap > 0) rep->history[0] = r0;
+  while (rn > rtol * r0 && cycles < max_cycles) {
+    if ((s = vcycle_dev(c, D.u, D.f, true))) return s;
+    if ((s = residual_dev(c, c->L, D.u, D.f, D.r))) return s;
+    if ((s = norm_host(c, D.r, D.g.nskel, &rn))) return s;
+    ++cycles;
+    if (rep && rep->history && cycles < rep->history_cap) rep->history[cycles] = rn;
+  }
+  if ((s = recover_dev(c, D.u, F, ufull))) return s;
+  bool conv = rn <= rtol * r0;
+  if (rep) {
+    rep->cycles = cycles;
+    rep->converged = conv ? 1 : 0;
+    rep->r0 = r0;
+    rep->r_final = rn;
+    rep->rho = (cycles > 0 && r0 > 0) ? std::pow(rn / r0, 1.0 / cycles) : 0.0;
+    rep->coarse_iters = (int)c->coarse_its_total;
+  }
+  if (!conv) return fail(PMG_ENOCONV, "pmg_solve: max_cycles reached before rtol");
+  return PMG_OK;
+}
+
+void free_ctx(pmg_ctx* c) {
+  if (!c) return;
+  for (auto& D : c->D) {
+    cudaFree(D.etab); cudaFree(D.stab); cudaFree(D.Jint); cudaFree(D.u); cudaFree(D.f); cudaFree(D.r);
+  }
+  cudaFree(c->Y); cudaFree(c->Z); cudaFree(c->cube); cudaFree(c->part); cudaFree(c->dres); cudaFree(c->pcg);
+  cudaFree(c->cx); cudaFree(c->cr); cudaFree(c->cz); cudaFree(c->cp); cudaFree(c->cq); cudaFree(c->dinv);
+  for (int d = 0; d < 3; ++d) cudaFree(c->bm[d]);
+  cudaFree(c->Fdev); cudaFree(c->Udev);
+  ev_reset(c);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  delete c;
+}
+
+template <class T>
+cudaError_t dalloc(T** p, size_t count) {
+  return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(1, count) * sizeof(T));
+}
+
+pmg_status upload(double** dst, const std::vector<double>& v) {
+  if (dalloc(dst, v.size()) != cudaSuccess) return fail(PMG_ENOMEM, "cudaMalloc failed (tables)");
+  if (!v.empty()) CUDA_CHECK(cudaMemcpy(*dst, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
+  return PMG_OK;
+}
+
+pmg_status check_level(const pmg_ctx* c, int level) {
+  if (!c) return fail(PMG_EINVAL, "ctx is NULL");
+  if (level < 0 || level > c->L) return fail(PMG_EINVAL, "level out of range");
+  return PMG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void pmg_default_options(pmg_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->p0 = 2;
+  o->weight_degree = 7;
+  o->schedule = 0;
+  o->coarse_rtol = 1e-8;
+  o->coarse_maxit = 10000;
+  o->coarse_check = 8;
+  o->rank = 0;
+  o->nranks = 1;
+  o->nccl_id = nullptr;
+  o->stream = nullptr;
+}
+
+const char* pmg_last_error(void) { return g_err.c_str(); }
+
+pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths[3], int p, double lambda,
+                     const pmg_options* opt) {
+  if (!out) return fail(PMG_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!n_e || !widths) return fail(PMG_EINVAL, "n_e / widths is NULL");
+  for (int d = 0; d < 3; ++d) {
+    if (n_e[d] < 1) return fail(PMG_EINVAL, "n_e[d] must be >= 1");
+    if (!widths[d]) return fail(PMG_EINVAL, "widths[d] is NULL");
+    for (int e = 0; e < n_e[d]; ++e)
+      if (!(widths[d][e] > 0.0) || !std::isfinite(widths[d][e])) return fail(PMG_EINVAL, "element widths must be positive and finite");
+  }
+  if (!(lambda >= 0.0) || !std::isfinite(lambda)) return fail(PMG_EINVAL, "lambda must be >= 0 and finite");
+  pmg_options o;
+  pmg_default_options(&o);
+  if (opt) o = *opt;
+  if (o.p0 < 2) return fail(PMG_EINVAL, "p0 must be >= 2");
+  if (p < 2 || p > 32) return fail(PMG_EINVAL, "degree p must be in [2, 32]");
+  if (p < o.p0) return fail(PMG_EINVAL, "p must be >= p0");
+  if (o.weight_degree != 7) return fail(PMG_EINVAL, "only weight_degree = 7 is implemented (P:316)");
+  if (o.schedule != 0 && o.schedule != 1) return fail(PMG_EINVAL, "schedule must be 0 or 1");
+  if (o.nranks != 1) return fail(PMG_EINVAL, "only nranks = 1 is implemented in this version");
+  if (!(o.coarse_rtol > 0.0) || o.coarse_maxit < 1) return fail(PMG_EINVAL, "coarse_rtol > 0 and coarse_maxit >= 1 required");
+
+  pmg_ctx* c = new (std::nothrow) pmg_ctx();
+  if (!c) return fail(PMG_ENOMEM, "host allocation failed");
+  c->opt = o;
+  c->st = static_cast<cudaStream_t>(o.stream);
+  c->lam = lambda;
+  int L = 0;
+  while ((o.p0 << L) < p) ++L;
+  c->L = L;
+  std::vector<int> deg;
+  for (int l = 0; l < L; ++l) deg.push_back(o.p0 << l);
+  deg.push_back(p);
+  c->H.resize(L + 1);
+  c->D.resize(L + 1);
+  for (int l = 0; l <= L; ++l) {
+    std::string err = build_level(c->H[l], deg[l], n_e, widths, lambda, o.weight_degree);
+    if (!err.empty()) { free_ctx(c); return fail(PMG_EINVAL, err); }
+    if (l >= 1) build_interp(c->H[l], deg[l - 1]);
+  }
+  std::vector<double> diag;
+  coarse_diag(c->H[0], lambda, diag);
+  std::vector<double> dinv(diag.size());
+  for (size_t i = 0; i < diag.size(); ++i) dinv[i] = diag[i] != 0.0 ? 1.0 / diag[i] : 0.0;
+
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int smem_optin = 0;
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  size_t max_elem = 0, max_star = 0, max_tr = 0;
+  size_t Ylen = 0, Zlen = 0;
+  pmg_status s;
+  for (int l = 0; l <= L; ++l) {
+    DevLevel& D = c->D[l];
+    D.g = c->H[l].g;
+    if ((s = upload(&D.etab, c->H[l].etab)) || (s = upload(&D.stab, c->H[l].stab))) { free_ctx(c); return s; }
+    if (l >= 1 && (s = upload(&D.Jint, c->H[l].Jint))) { free_ctx(c); return s; }
+    if (dalloc(&D.u, D.g.nskel) || dalloc(&D.f, D.g.nskel) || dalloc(&D.r, D.g.nskel)) { free_ctx(c); return fail(PMG_ENOMEM, "cudaMalloc failed (level vectors)"); }
+    cudaMemset(D.u, 0, D.g.nskel * sizeof(double));
+    cudaMemset(D.f, 0, D.g.nskel * sizeof(double));
+    cudaMemset(D.r, 0, D.g.nskel * sizeof(double));
+    Ylen = std::max<size_t>(Ylen, (size_t)D.g.nelem * D.g.YS);
+    max_elem = std::max(max_elem, elem_apply_smem(D.g.p, D.g.ET));
+    if (l >= 1) {
+      Zlen = std::max<size_t>(Zlen, (size_t)D.g.nrec * zs_of(deg[l - 1]));
+      max_tr = std::max(max_tr, transfer_smem(D.g.p, deg[l - 1]));
+    }
+  }
+  const LevelGeom& gt = c->D[L].g;
+  c->star_s_smem = star_smem(p, true) <= (size_t)smem_optin;
+  for (int l = 0; l <= L; ++l) max_star = std::max(max_star, star_smem(c->D[l].g.p, c->star_s_smem && star_smem(c->D[l].g.p, true) <= (size_t)smem_optin));
+  if (!c->star_s_smem) {
+    // the top level decides; lower levels always fit, but one flag is used for all levels
+    max_star = 0;
+    for (int l = 0; l <= L; ++l) max_star = std::max(max_star, star_smem(c->D[l].g.p, false));
+  }
+  c->cube_in_smem = std::max(condense_smem(p, gt.ET, true), recover_smem(p, gt.ET, true)) <= (size_t)smem_optin;
+  size_t max_cond = condense_smem(p, gt.ET, c->cube_in_smem), max_rec = recover_smem(p, gt.ET, c->cube_in_smem);
+  Ylen = std::max<size_t>(Ylen, (size_t)gt.nelem * 6 * gt.m * gt.m);
+  if (max_elem > (size_t)smem_optin || max_star > (size_t)smem_optin || max_tr > (size_t)smem_optin ||
+      max_cond > (size_t)smem_optin || max_rec > (size_t)smem_optin) {
+    free_ctx(c);
+    return fail(PMG_EINVAL, "shared-memory plan exceeds the device limit for this p");
+  }
+  if (dalloc(&c->Y, Ylen) || dalloc(&c->Z, Zlen) || dalloc(&c->part, 2 * kRedBlocks) || dalloc(&c->dres, 8) ||
+      dalloc(&c->pcg, 1)) {
+    free_ctx(c);
+    return fail(PMG_ENOMEM, "cudaMalloc failed (workspaces)");
+  }
+  if (!c->cube_in_smem) {
+    c->cube_blocks = 296;
+    if (dalloc(&c->cube, (size_t)c->cube_blocks * gt.m * gt.m * gt.m)) { free_ctx(c); return fail(PMG_ENOMEM, "cudaMalloc failed (cube)"); }
+  }
+  long long n0 = c->D[0].g.nskel;
+  if (dalloc(&c->cx, n0) || dalloc(&c->cr, n0) || dalloc(&c->cz, n0) || dalloc(&c->cp, n0) || dalloc(&c->cq, n0)) {
+    free_ctx(c);
+    return fail(PMG_ENOMEM, "cudaMalloc failed (coarse CG vectors)");
+  }
+  if ((s = upload(&c->dinv, dinv))) { free_ctx(c); return s; }
+  for (int d = 0; d < 3; ++d) {
+    std::vector<double> xw, ww;
+    gll(p, xw, ww);
+    int kd = n_e[d];
+    std::vector<double> b(kd * p + 1, 0.0);
+    for (int e = 0; e < kd; ++e)
+      for (int t = 0; t <= p; ++t) b[e * p + t] += 0.5 * widths[d][e] * ww[t];
+    if ((s = upload(&c->bm[d], b))) { free_ctx(c); return s; }
+  }
+  c->n_grid = (long long)(n_e[0] * p + 1) * (n_e[1] * p + 1) * (n_e[2] * p + 1);
+  if (dalloc(&c->Fdev, c->n_grid) || dalloc(&c->Udev, c->n_grid)) { free_ctx(c); return fail(PMG_ENOMEM, "cudaMalloc failed (grid buffers)"); }
+  // the attribute is per function, not per context: always allow the device maximum so that
+  // several contexts with different degrees can coexist
+  cudaError_t e1 = cudaFuncSetAttribute(k_elem_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  cudaError_t e2 = cudaFuncSetAttribute(k_star, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  cudaError_t e3 = cudaFuncSetAttribute(k_restrict_local, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  cudaError_t e4 = cudaFuncSetAttribute(k_prolong, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  cudaError_t e5 = cudaFuncSetAttribute(k_condense_elem, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  cudaError_t e6 = cudaFuncSetAttribute(k_recover_elem, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  if (e1 || e2 || e3 || e4 || e5 || e6) { free_ctx(c); return fail(PMG_ECUDA, "cudaFuncSetAttribute failed"); }
+  cudaError_t es = cudaDeviceSynchronize();
+  if (es != cudaSuccess) { free_ctx(c); return fail(PMG_ECUDA, std::string("setup: ") + cudaGetErrorString(es)); }
+  *out = c;
+  return PMG_OK;
+}
+
+pmg_status pmg_destroy(pmg_ctx* c) {
+  if (!c) return fail(PMG_EINVAL, "ctx is NULL");
+  cudaStreamSynchronize(c->st);
+  free_ctx(c);
+  return PMG_OK;
+}
+
+int pmg_num_levels(const pmg_ctx* c) { return c ? c->L + 1 : -1; }
+
+pmg_status pmg_level_info(const pmg_ctx* c, int level, int* degree, long long* n_skel, long long* n_grid) {
+  pmg_status s = check_level(c, level);
+  if (s) return s;
+  const LevelGeom& g = c->D[level].g;
+  if (degree) *degree = g.p;
+  if (n_skel) *n_skel = g.nskel;
+  if (n_grid) *n_grid = (long long)(g.k1 * g.p + 1) * (g.k2 * g.p + 1) * (g.k3 * g.p + 1);
+  return PMG_OK;
+}
+
+pmg_status pmg_grid_coords(const pmg_ctx* c, int level, int d, double* coords_host) {
+  pmg_status s = check_level(c, level);
+  if (s) return s;
+  if (d < 0 || d > 2 || !coords_host) return fail(PMG_EINVAL, "bad direction or NULL output");
+  const auto& x = c->H[level].coords[d];
+  std::memcpy(coords_host, x.data(), x.size() * sizeof(double));
+  return PMG_OK;
+}
+
+pmg_status pmg_residual(pmg_ctx* c, int level, const double* u_hat, const double* f_hat, double* r_hat) {
+  pmg_status s = check_level(c, level);
+  if (s) return s;
+  if (!u_hat || !r_hat) return fail(PMG_EINVAL, "NULL vector");
+  if (u_hat == r_hat) return fail(PMG_EINVAL, "u_hat and r_hat must not alias");
+  return residual_dev(c, level, u_hat, f_hat, r_hat);
+}
+
+pmg_status pmg_smooth(pmg_ctx* c, int level, const double* r_hat, double* u_hat) {
+  pmg_status s = check_level(c, level);
+  if (s) return s;
+  if (!u_hat || !r_hat) return fail(PMG_EINVAL, "NULL vector");
+  if (u_hat == r_hat) return fail(PMG_EINVAL, "u_hat and r_hat must not alias");
+  return smooth_dev(c, level, r_hat, u_hat);
+}
+
+pmg_status pmg_restrict(pmg_ctx* c, int level, const double* r_fine, double* f_coarse) {
+  pmg_status s = check_level(c, level);
+  if (s) return s;
+  if (level < 1) return fail(PMG_EINVAL, "restrict needs a fine level >= 1");
+  if (!r_fine || !f_coarse) return fail(PMG_EINVAL, "NULL vector");
+  return restrict_dev(c, level, r_fine, f_coarse);
+}
+
+pmg_status pmg_prolong(pmg_ctx* c, int level, const double* u_coarse, double* u_fine) {
+  pmg_status s = check_level(c, level);
+  if (s) return s;
+  if (level < 1) return fail(PMG_EINVAL, "prolong needs a fine level >= 1");
+  if (!u_coarse || !u_fine) return fail(PMG_EINVAL, "NULL vector");
+  return prolong_dev(c, level, u_coarse, u_fine);
+}
+
+pmg_status pmg_vcycle(pmg_ctx* c, double* u_hat, const double* f_hat) {
+  if (!c) return fail(PMG_EINVAL, "ctx is NULL");
+  if (!u_hat || !f_hat) return fail(PMG_EINVAL, "NULL vector");
+  return vcycle_dev(c, u_hat, f_hat, false);
+}
+
+pmg_status pmg_condense(pmg_ctx* c, const double* F_full, double* f_hat) {
+  if (!c) return fail(PMG_EINVAL, "ctx is NULL");
+  if (!F_full || !f_hat) return fail(PMG_EINVAL, "NULL vector");
+  return condense_dev(c, F_full, f_hat);
+}
+
+pmg_status pmg_recover(pmg_ctx* c, const double* u_hat, const double* F_full, double* u_full) {
+  if (!c) return fail(PMG_EINVAL, "ctx is NULL");
+  if (!u_hat || !F_full || !u_full) return fail(PMG_EINVAL, "NULL vector");
+  return recover_dev(c, u_hat, F_full, u_full);
+}
+
+pmg_status pmg_solve(pmg_ctx* c, const double* F_full, double* u_full, double rtol, int max_cycles, pmg_report* rep) {
+  if (!c) return fail(PMG_EINVAL, "ctx is NULL");
+  if (!F_full || !u_full) return fail(PMG_EINVAL, "NULL vector");
+  if (!(rtol > 0.0) || max_cycles < 0) return fail(PMG_EINVAL, "rtol > 0 and max_cycles >= 0 required");
+  return solve_dev(c, F_full, u_full, rtol, max_cycles, rep);
+}
+
+pmg_status pmg_solve_host(pmg_ctx* c, const double* F_host, double* u_host, double rtol, int max_cycles, pmg_report* rep) {
+  if (!c) return fail(PMG_EINVAL, "ctx is NULL");
+  if (!F_host || !u_host) return fail(PMG_EINVAL, "NULL vector");
+  CUDA_CHECK(cudaMemcpyAsync(c->Fdev, F_host, c->n_grid * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  pmg_status s = pmg_solve(c, c->Fdev, c->Udev, rtol, max_cycles, rep);
+  if (s != PMG_OK && s != PMG_ENOCONV) return s;
+  CUDA_CHECK(cudaMemcpyAsync(u_host, c->Udev, c->n_grid * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CUDA_CHECK(cudaStreamSynchronize(c->st));
+  return s;
+}
+
+pmg_status pmg_weak_rhs(pmg_ctx* c, const double* f_nodal, double* F_full) {
+  if (!c) return fail(PMG_EINVAL, "ctx is NULL");
+  if (!f_nodal || !F_full) return fail(PMG_EINVAL, "NULL vector");
+  k_weak_rhs<<<grid_for(c->n_grid), kThreads, 0, c->st>>>(c->D[c->L].g, c->bm[0], c->bm[1], c->bm[2], f_nodal, F_full);
+  LAUNCH_CHECK(c);
+  return PMG_OK;
+}
+
+pmg_status pmg_skel_from_grid(pmg_ctx* c, int level, const double* grid, double* skel) {
+  pmg_status s = check_level(c, level);
+  if (s) return s;
+  if (!grid || !skel) return fail(PMG_EINVAL, "NULL vector");
+  k_skel_from_grid<<<grid_for(c->D[level].g.nskel), kThreads, 0, c->st>>>(c->D[level].g, grid, skel);
+  LAUNCH_CHECK(c);
+  return PMG_OK;
+}
+
+pmg_status pmg_skel_to_grid(pmg_ctx* c, int level, const double* skel, double* grid) {
+  pmg_status s = check_level(c, level);
+  if (s) return s;
+  if (!grid || !skel) return fail(PMG_EINVAL, "NULL vector");
+  const LevelGeom& g = c->D[level].g;
+  long long ng = (long long)(g.k1 * g.p + 1) * (g.k2 * g.p + 1) * (g.k3 * g.p + 1);
+  k_skel_to_grid<<<grid_for(ng), kThreads, 0, c->st>>>(g, skel, grid);
+  LAUNCH_CHECK(c);
+  return PMG_OK;
+}
+
+pmg_status pmg_norm(pmg_ctx* c, int level, const double* x_hat, double* out_host) {
+  pmg_status s = check_level(c, level);
+  if (s) return s;
+  if (!x_hat || !out_host) return fail(PMG_EINVAL, "NULL pointer");
+  return norm_host(c, x_hat, c->D[level].g.nskel, out_host);
+}
+
+long long pmg_launch_count(const pmg_ctx* c) { return c ? c->launches : -1; }
+
+pmg_status pmg_timing_enable(pmg_ctx* c, int enable) {
+  if (!c) return fail(PMG_EINVAL, "ctx is NULL");
+  CUDA_CHECK(cudaStreamSynchronize(c->st));
+  ev_reset(c);
+  c->timing = enable != 0;
+  return PMG_OK;
+}
+
+pmg_status pmg_timing_read(pmg_ctx* c, int kind, double* total_ms, long long* count) {
+  if (!c) return fail(PMG_EINVAL, "ctx is NULL");
+  if (kind < 0 || kind > 3 || !total_ms || !count) return fail(PMG_EINVAL, "bad kind or NULL output");
+  CUDA_CHECK(cudaStreamSynchronize(c->st));
+  double tot = 0.0;
+  long long n = 0;
+  for (auto& mk : c->ev_marks) {
+    if (mk.base != (kind & 1)) continue;
+    if (kind < 2 && !mk.top) continue;
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, mk.a, mk.b));
+    tot += ms;
+    ++n;
+  }
+  *total_ms = tot;
+  *count = n;
+  return PMG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,71 @@
+// Internal declarations shared by the host setup (setup_host.cpp) and the CUDA side.
+// Not part of the C ABI (see include/pmg.h).
+#pragma once
+#include <string>
+#include <vector>
+
+#if defined(__CUDACC__)
+#define PMG_HD __host__ __device__
+#else
+#define PMG_HD
+#endif
+
+namespace pmg {
+
+// Geometry of one level on the device (record layout).
+struct LevelGeom {
+  int p, m, n;          // degree, m = p - 1 (element interior), n = 2p - 1 (star extent n_S)
+  int k1, k2, k3;       // elements per direction
+  int V1, V2, V3;       // vertices per direction (k_d + 1)
+  int RS;               // record stride: 3m^2 + 3m + 1
+  int YS;               // element output stride: 6m^2 + 12m + 8
+  int ET;               // element table stride (per direction, per 1-D element)
+  int ST;               // star table stride (per direction, per vertex line)
+  long long nrec;       // V1 V2 V3
+  long long nskel;      // nrec * RS
+  long long nelem;      // k1 k2 k3
+};
+
+// Element table, per direction d and 1-D element e_d (width h), m = p - 1, q = p + 1:
+//   [0, m)            Lambda_d  (interior generalised eigenvalues, S^T K_II S = Lambda)
+//   [m, m+m^2)        P_d[b][i] = S[i][b] M[i]   (S^T M_II, forward face transform)
+//   [.., +m^2)        S_d[i][b]                  (interior eigenvectors, S^T M_II S = I)
+//   [.., +m)          a0[b] = sum_i S[i][b] K[i][0]   (expansion vector of the low face)
+//   [.., +m)          a1[b] = sum_i S[i][b] K[i][p]   (expansion vector of the high face)
+//   [.., +q)          M diag (h/2 w)
+//   [.., +q^2)        K[i][j] (2/h K_hat)
+PMG_HD inline int elem_table_stride(int p) { int m = p - 1, q = p + 1; return m + 2 * m * m + 2 * m + q + q * q; }
+PMG_HD inline int et_lam(int) { return 0; }
+PMG_HD inline int et_P(int p) { return p - 1; }
+PMG_HD inline int et_S(int p) { int m = p - 1; return m + m * m; }
+PMG_HD inline int et_a0(int p) { int m = p - 1; return m + 2 * m * m; }
+PMG_HD inline int et_a1(int p) { int m = p - 1; return 2 * m + 2 * m * m; }
+PMG_HD inline int et_M(int p) { int m = p - 1; return 3 * m + 2 * m * m; }
+PMG_HD inline int et_K(int p) { int m = p - 1; return 3 * m + 2 * m * m + p + 1; }
+
+// Star table, per direction d and vertex line v_d, n = 2p - 1, c = p - 1:
+//   [0, n^2)   S[j][a]  (padded generalised eigenvectors of the assembled 1-D star, S^T M S = I)
+//   [.., +n)   Lambda[a] (padded with 1 at decoupled points)
+//   [.., +n)   s[a] = S[c][a]  (the vertex row, "S_I0^T" of Alg. 1)
+//   [.., +n)   w[j]  weight polynomial at star point j (1 at the vertex)
+PMG_HD inline int star_table_stride(int p) { int n = 2 * p - 1; return n * n + 3 * n; }
+
+struct HostLevel {
+  int p;
+  LevelGeom g;
+  std::vector<double> etab;      // (k1 + k2 + k3) * ET
+  std::vector<double> stab;      // (V1 + V2 + V3) * ST
+  std::vector<double> Jint;      // (p - 1) x (p_c + 1): rows 1..p-1 of J (coarse -> this level)
+  std::vector<double> coords[3];
+};
+
+// Host setup; returns an empty string on success, else an error message.
+std::string build_level(HostLevel& L, int p, const int k[3], const double* const widths[3],
+                        double lambda, int weight_degree);
+std::string build_interp(HostLevel& fine, int p_coarse);
+// diag(H_hat) for the given level in skeleton record layout (free entries only, others 0).
+std::string coarse_diag(const HostLevel& L, double lambda, std::vector<double>& diag);
+// 1-D GLL nodes and weights (p >= 1)
+void gll(int p, std::vector<double>& x, std::vector<double>& w);
+
+}  // namespace pmg

@@ -1,0 +1,219 @@
+"""GPU-vs-oracle parity through the C ABI (north star: 1e-11 relative per operator application,
+1e-9 relative on the final solution), on seeded inputs at sizes the oracle finishes in seconds
+that still span several elements/stars per direction and ragged (non-power-of-two, odd p,
+stretched) meshes."""
+import numpy as np
+import pytest
+
+import pmg_inputs as pi
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+OP_TOL = 1e-11
+SOLVE_TOL = 1e-9
+
+CASES = {
+    "k323_p4_lam1.7_stretched": dict(k=(3, 2, 3), p=4, lam=1.7, stretch=1.6),
+    "k232_p5_lam0": dict(k=(2, 3, 2), p=5, lam=0.0, stretch=None),
+    "k333_p8_lam0": dict(k=(3, 3, 3), p=8, lam=0.0, stretch=None),
+    "k422_p3_lam0.5": dict(k=(4, 2, 2), p=3, lam=0.5, stretch=1.3),
+    "k332_p2_lam0": dict(k=(3, 3, 2), p=2, lam=0.0, stretch=None),
+    "k222_p6_lam2": dict(k=(2, 2, 2), p=6, lam=2.0, stretch=1.2),
+}
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+class Pair:
+    """Oracle hierarchy + GPU solver for the same problem."""
+
+    def __init__(self, k, p, lam, stretch, coarse_rtol=1e-13, schedule=0):
+        from oracle import mg
+        import paper_1808_03595_b200 as pmg
+        case = pi.small_case(k, p, lam, stretch=stretch)
+        self.case = case
+        self.orc = mg.Hierarchy(case.k, case.widths, p, lam, coarse_rtol=coarse_rtol, schedule=schedule)
+        self.gpu = pmg.Solver(case.k, case.widths, p, lam, coarse_rtol=coarse_rtol, schedule=schedule)
+        assert self.gpu.nlevels == len(self.orc.levels)
+        self.rng = np.random.default_rng(11)
+
+    def mesh(self, l):
+        return self.orc.levels[l].mesh
+
+    def to_skel(self, l, grid_np):
+        g = torch.from_numpy(np.ascontiguousarray(grid_np, dtype=np.float64)).cuda()
+        s = self.gpu.new_skel(l)
+        self.gpu.skel_from_grid(l, g, s)
+        return s
+
+    def to_grid(self, l, skel):
+        g = self.gpu.new_grid(l)
+        self.gpu.skel_to_grid(l, skel, g)
+        torch.cuda.synchronize()
+        return g.cpu().numpy()
+
+    def rand_skel(self, l):
+        m = self.mesh(l)
+        return self.rng.standard_normal(m.ntot) * m.free_skel
+
+
+_PAIRS = {}
+
+
+def pair(name):
+    if name not in _PAIRS:
+        _PAIRS[name] = Pair(**CASES[name])
+    return _PAIRS[name]
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_coords_and_converters(name):
+    P = pair(name)
+    for l in range(P.gpu.nlevels):
+        m = P.mesh(l)
+        for d in range(3):
+            assert np.abs(P.gpu.grid_coords(l, d) - m.coords[d]).max() < 1e-14 * max(1.0, m.coords[d].max())
+        x = P.rng.standard_normal(m.ntot)
+        back = P.to_grid(l, P.to_skel(l, x))
+        assert np.array_equal(back, x * m.free_skel)          # exact round trip on free skeleton points
+        deg, nskel, ngrid = P.gpu.level_info(l)
+        assert deg == m.p and ngrid == m.ntot
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_weak_rhs(name):
+    from oracle import condensed
+    P = pair(name)
+    m = P.mesh(P.gpu.nlevels - 1)
+    f = P.rng.standard_normal(m.ntot)
+    F = P.gpu.new_grid()
+    P.gpu.weak_rhs(torch.from_numpy(f).cuda(), F)
+    torch.cuda.synchronize()
+    assert rel(F.cpu().numpy(), condensed.weak_rhs(m, f)) < 1e-14
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_residual_parity(name):
+    P = pair(name)
+    for l in range(P.gpu.nlevels):
+        op = P.orc.levels[l].op
+        u, f = P.rand_skel(l), P.rand_skel(l)
+        r = P.gpu.new_skel(l)
+        P.gpu.residual(l, P.to_skel(l, u), P.to_skel(l, f), r)
+        assert rel(P.to_grid(l, r), op.residual(u, f)) < OP_TOL, l
+        q = P.gpu.new_skel(l)
+        P.gpu.residual(l, P.to_skel(l, u), None, q)              # operator apply
+        assert rel(P.to_grid(l, q), op.apply(u)) < OP_TOL, l
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_operator_symmetric_on_gpu(name):
+    P = pair(name)
+    l = P.gpu.nlevels - 1
+    a, b = P.to_skel(l, P.rand_skel(l)), P.to_skel(l, P.rand_skel(l))
+    Ha, Hb = P.gpu.new_skel(l), P.gpu.new_skel(l)
+    P.gpu.residual(l, a, None, Ha)
+    P.gpu.residual(l, b, None, Hb)
+    x, y = float((Ha * b).sum()), float((a * Hb).sum())
+    assert abs(x - y) <= 1e-12 * max(abs(x), 1.0)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_smooth_parity(name):
+    P = pair(name)
+    for l in range(P.gpu.nlevels):
+        sm = P.orc.levels[l].smoother
+        u0, r = P.rand_skel(l), P.rand_skel(l)
+        u = P.to_skel(l, u0)
+        P.gpu.smooth(l, P.to_skel(l, r), u)
+        want = u0 + sm.apply(r)
+        assert rel(P.to_grid(l, u) - u0, want - u0) < OP_TOL, l
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if CASES[n]["p"] > 2])
+def test_transfer_parity(name):
+    P = pair(name)
+    for l in range(1, P.gpu.nlevels):
+        T = P.orc.transfers[l]
+        rf = P.rand_skel(l)
+        fc = P.gpu.new_skel(l - 1)
+        P.gpu.restrict(l, P.to_skel(l, rf), fc)
+        assert rel(P.to_grid(l - 1, fc), T.restrict(rf)) < OP_TOL, l
+        uc, uf0 = P.rand_skel(l - 1), P.rand_skel(l)
+        uf = P.to_skel(l, uf0)
+        P.gpu.prolong(l, P.to_skel(l - 1, uc), uf)
+        assert rel(P.to_grid(l, uf), uf0 + T.prolong(uc)) < OP_TOL, l
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_condense_recover_parity(name):
+    P = pair(name)
+    L = P.gpu.nlevels - 1
+    m = P.mesh(L)
+    op = P.orc.levels[L].op
+    F = P.rng.standard_normal(m.ntot) * m.free
+    Fd = torch.from_numpy(F).cuda()
+    fh = P.gpu.new_skel(L)
+    P.gpu.condense(Fd, fh)
+    assert rel(P.to_grid(L, fh), op.condense(F)) < OP_TOL
+    uh = P.rand_skel(L)
+    ug = P.gpu.new_grid()
+    P.gpu.recover(P.to_skel(L, uh), Fd, ug)
+    torch.cuda.synchronize()
+    assert rel(ug.cpu().numpy(), op.recover(uh, F)) < OP_TOL
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_vcycle_parity(name):
+    P = pair(name)
+    L = P.gpu.nlevels - 1
+    u0, f = P.rand_skel(L), P.rand_skel(L)
+    u = P.to_skel(L, u0)
+    P.gpu.vcycle(u, P.to_skel(L, f))
+    want = P.orc.vcycle(u0, f)
+    assert rel(P.to_grid(L, u), want) < OP_TOL
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_solve_parity(name):
+    from oracle import condensed
+    P = pair(name)
+    L = P.gpu.nlevels - 1
+    m = P.mesh(L)
+    f = pi.uniform_pm1(5, np.arange(m.ntot))
+    F = condensed.weak_rhs(m, f)
+    u_orc, rep_o = P.orc.solve(F, 1e-10)
+    ug = P.gpu.new_grid()
+    rep = P.gpu.solve(torch.from_numpy(F).cuda(), ug, 1e-10)
+    torch.cuda.synchronize()
+    assert rep["converged"] and rep["cycles"] == rep_o["cycles"]
+    assert rel(ug.cpu().numpy(), u_orc) < SOLVE_TOL
+    assert abs(rep["r0"] - rep_o["r0"]) <= 1e-12 * rep_o["r0"]
+
+
+def test_smoother_deterministic():
+    P = pair("k333_p8_lam0")
+    l = P.gpu.nlevels - 1
+    r = P.to_skel(l, P.rand_skel(l))
+    u1, u2 = P.gpu.new_skel(l), P.gpu.new_skel(l)
+    P.gpu.smooth(l, r, u1)
+    P.gpu.smooth(l, r, u2)
+    torch.cuda.synchronize()
+    assert torch.equal(u1, u2)
+
+
+def test_invalid_arguments_fail_loudly():
+    import paper_1808_03595_b200 as pmg
+    with pytest.raises(pmg.PmgError):
+        pmg.Solver((2, 2, 2), [np.ones(2)] * 3, 1, 0.0)           # p < 2
+    with pytest.raises(pmg.PmgError):
+        pmg.Solver((2, 2, 2), [np.array([1.0, -1.0])] * 3, 4, 0.0)  # negative width
+    with pytest.raises(pmg.PmgError):
+        pmg.Solver((2, 2, 2), [np.ones(2)] * 3, 4, -1.0)          # lambda < 0
+    P = pair("k232_p5_lam0")
+    with pytest.raises(pmg.PmgError):
+        P.gpu.restrict(0, P.gpu.new_skel(0), P.gpu.new_skel(0))   # no level below 0
