@@ -1,0 +1,329 @@
+"""Benchmark: unknowns/s of a 1e-10 residual-drop pMG solve (FP64) on B200, BASELINE.json metric.
+
+One "step" = one full pmg_solve (Alg. 4: condense, V-cycles until ||r|| <= 1e-10 ||r_0||,
+recover) of the workload, inputs resident in HBM.  Default workload: BASELINE configs[1]
+(Poisson, 16^3 elements, p = 8, f ~ U[-1,1] seed 1, 2,097,152 unknowns).  L2 (126 MB) is
+flushed between timed steps by writing a 512 MB buffer (outside the per-step events).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config 2] [--p P] [--impl reference]
+
+--impl reference times the CPU oracle (oracle/, test infrastructure) on the same config: the
+deliberately slow, plain program the GPU path is checked against.  Under torchrun (N > 1) only
+rank 0 runs it.  N > 1 in this version runs one independent replica of the workload per GPU
+(the z-slab decomposition with NCCL halos is not implemented yet), scaling "weak".
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import pmg_inputs as pi  # noqa: E402
+
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2: 64 FP64 FMA/clk/SM x 148 SMs x 1.965 GHz
+METRIC = "unknowns/s for a 1e-10 residual-drop pMG solve (FP64); smoother % of HBM peak"
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def case_for(args, n_gpu):
+    if args.config == 5:
+        return pi.config(5, n_gpu=1)      # per-replica weak-scaling slab 64x64x8
+    return pi.config(args.config, p=args.p)
+
+
+def n_stars(case):
+    k = case.k
+    return (k[0] + 1) * (k[1] + 1) * (k[2] + 1) - 8
+
+
+def n_skel_free(case):
+    p, k = case.p, case.k
+    m = p - 1
+    full = (k[0] * p - 1) * (k[1] * p - 1) * (k[2] * p - 1)
+    return full - k[0] * k[1] * k[2] * m ** 3
+
+
+def oracle_solve_timer(case, reps, warm=0):
+    """Time full oracle solves (setup excluded) on the host cores; returns (seconds per solve, cycles)."""
+    from oracle import condensed, mg
+    H = mg.Hierarchy(case.k, case.widths, case.p, case.lam)
+    m = H.levels[-1].mesh
+    F = condensed.weak_rhs(m, case.f_nodal(m.coords))
+    for _ in range(warm):
+        H.solve(F, 1e-10)
+    ts, cyc = [], 0
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        _, rep = H.solve(F, 1e-10)
+        ts.append(time.perf_counter() - t0)
+        cyc = rep["cycles"]
+    return ts, cyc
+
+
+def cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return 0
+    case = case_for(args, ws)
+    ts, cyc = oracle_solve_timer(case, args.steps, warm=args.warmup)
+    t = statistics.mean(ts)
+    val = case.n_dof / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "unknowns/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": case.name, "n_dof": case.n_dof, "p": case.p, "k": list(case.k), "lambda": case.lam,
+                   "rtol": 1e-10, "cycles": cyc},
+        "cpu_baseline": {"value": val, "unit": "unknowns/s", "cores": cores(), "kind": "oracle",
+                         "sample": "%d full oracle solves (dense Schur / dense-LU stars; setup excluded) of %s"
+                                   % (args.steps, case.name)},
+        "e2e": {"value": val, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def load_traffic(case_name):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        d = json.load(open(path))
+        return d.get(case_name, {})
+    except Exception:
+        return {}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--p", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    ws, rank, local = dist_init()
+    if args.impl == "reference":
+        return run_reference(args, ws, rank)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1808_03595_b200 as pmg
+
+    case = case_for(args, ws)
+    s = pmg.Solver(case.k, case.widths, case.p, case.lam)
+    L = s.nlevels - 1
+    coords = [s.grid_coords(L, d) for d in range(3)]
+    f = torch.from_numpy(case.f_nodal(coords)).cuda()
+    F = s.new_grid()
+    s.weak_rhs(f, F)
+    u = s.new_grid()
+    stream = s.stream
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")   # 512 MB > 126 MB L2
+    for _ in range(args.warmup):
+        rep = s.solve(F, u, 1e-10)
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    s.timing_enable(True)
+    l0 = s.launch_count()
+    durs = []
+    reps = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        reps.append(s.solve(F, u, 1e-10))
+        e1.record(stream)
+        e1.synchronize()
+        durs.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    launches = s.launch_count() - l0
+    sm_ms, sm_n = s.timing_read(0)
+    rs_ms, rs_n = s.timing_read(1)
+    all_sm_ms, _ = s.timing_read(2)
+    all_rs_ms, _ = s.timing_read(3)
+    s.timing_enable(False)
+    if ws > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = statistics.mean(durs)
+    if ws > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = ws * case.n_dof / (ms / 1e3)
+
+    # e2e: through the C ABI with host buffers (pinned), H2D of F and D2H of u inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        Fh = F.cpu().pin_memory()
+        uh = torch.empty_like(Fh).pin_memory()
+        ed = []
+        for i in range(args.steps + 1):
+            flush.fill_(1.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            s.solve_host(Fh, uh, 1e-10)
+            e1.record(stream)
+            e1.synchronize()
+            if i > 0:
+                ed.append(e0.elapsed_time(e1))
+        ems = statistics.mean(ed)
+        if ws > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        nb = F.numel() * 8
+        e2e = {"value": ws * case.n_dof / (ems / 1e3), "unit": "unknowns/s", "ms_per_step": ems,
+               "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb}
+
+    # roofline of the dominant kernel: the star smoother (finest level), FP64-pipe bound
+    n = 2 * case.p - 1
+    sweep_ms = sm_ms / max(sm_n, 1)
+    flops = 37.0 * n ** 3 * n_stars(case)            # Alg. 1 count x stars per sweep
+    achieved = flops / (sweep_ms / 1e3) / 1e12
+    bytes_alg = 24.0 * n_skel_free(case)             # read r, read+write u
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6541.5)
+    tr = load_traffic(case.name)
+    traffic = tr.get("k_star_bytes_per_sweep")
+    roof = {"kernel": "k_star (8 colour launches = 1 smoother sweep, finest level)", "bound": "alu",
+            "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+            "traffic": traffic, "algorithmic_flops_per_sweep": flops, "sweep_ms": sweep_ms,
+            "peak_source": "derived: 64 FP64 FMA/clk/SM x 148 SMs x 1.965 GHz (no FP64 entry in MEASURED_PEAKS.json); "
+                           "measured DFMA microbenchmark 34.1 TFLOP/s (profiles/r01_step0_fp64_peaks.jsonl)",
+            "hbm_view": {"achieved_gbs": bytes_alg / (sweep_ms / 1e3) / 1e9, "peak_gbs": hbm,
+                         "frac": bytes_alg / (sweep_ms / 1e3) / 1e9 / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}}
+    res_ms = rs_ms / max(rs_n, 1)
+    m = case.p - 1
+    res_flops = (73.0 * m ** 3 + 24.0 * case.p * (case.p + 1) ** 2) * case.k[0] * case.k[1] * case.k[2]
+    residual = {"kernel": "k_elem_apply + k_gather_resid (finest level)", "ms": res_ms,
+                "achieved_tflops": res_flops / (res_ms / 1e3) / 1e12,
+                "achieved_gbs_alg": bytes_alg / (res_ms / 1e3) / 1e9}
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        ts, cyc = oracle_solve_timer(case, 3)
+        tcpu = statistics.mean(ts)
+        cpu = {"value": case.n_dof / tcpu, "unit": "unknowns/s", "cores": cores(), "kind": "oracle",
+               "sample": "3 full oracle solves of %s (setup excluded), %.2f s each, %d cycles" % (case.name, tcpu, cyc)}
+    r = reps[-1]
+    line = {
+        "metric": METRIC, "value": value, "unit": "unknowns/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": case.name, "n_dof": case.n_dof, "p": case.p, "k": list(case.k), "lambda": case.lam,
+                   "rtol": 1e-10, "cycles": r["cycles"], "rho": r["rho"], "coarse_iters": r["coarse_iters"],
+                   "l2": "flushed between steps (512 MB write, outside the timed events)",
+                   "parallelism": "single GPU" if ws == 1 else "replicas (one independent solve per GPU; z-slab NCCL decomposition not implemented)"},
+        "roofline": roof,
+        "residual_kernel": residual,
+        "time_split_ms_per_step": {"smoother_all_levels": all_sm_ms / args.steps, "residual_all_levels": all_rs_ms / args.steps},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    s.close()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,475 @@
+// Degree-specialised hot kernels (template on p): the condensed element operator and the star
+// smoother.  Same arithmetic as the runtime-p reference kernels in kernels.cu (and the same
+// citations: P:117-123 / reading R1 for the element operator; Alg. 1 + Alg. 2, for the
+// star), re-organised for throughput:
+//   - all six faces (three star planes) advance through each transform step together, so a
+//     CTA synchronises 6 times per element / star instead of ~20;
+//   - transform operands are laid out so that one operand is a warp broadcast and the other is
+//     read by consecutive lanes (conflict-free shared memory);
+//   - 1/D = 1/(lambda + L1 + L2 + L3) via rcp.approx + two Newton steps (no IEEE division slow path);
+//   - block size chosen per degree so small-p elements do not leave most threads idle.
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+#include "layout.cuh"
+
+namespace pmg {
+
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+template <int P> struct ElemCfg {
+  static constexpr int M = P - 1, Q = P + 1, MM = M * M, QQ = Q * Q;
+  static constexpr int NT = (P <= 4) ? 64 : (P <= 10 ? 128 : 256);
+  // shared layout (doubles)
+  // X aliases G in the forward transform and T in the back transform (G/T are dead there)
+  static constexpr int oUc = 0, oT = oUc + 6 * QQ, oG = oT + 6 * MM;
+  static constexpr int oTab = oG + 6 * MM;
+  // per-direction table block: Lam[M], P[M][M], Pt[M][M], a0[M], a1[M], Mq[Q], K[Q][Q]
+  static constexpr int tLam = 0, tP = M, tPt = M + MM, ta0 = M + 2 * MM, ta1 = 2 * M + 2 * MM,
+                       tM = 3 * M + 2 * MM, tK = 3 * M + 2 * MM + Q, TB = 3 * M + 2 * MM + Q + QQ;
+  static constexpr int total = oTab + 3 * TB;
+};
+
+template <int P>
+size_t elem_t_smem() { return sizeof(double) * ElemCfg<P>::total; }
+
+template <int P>
+__device__ __forceinline__ double getUc(const double* Uc, int t1, int t2, int t3) {
+  constexpr int Q = P + 1, QQ = Q * Q;
+  if (t1 == 0 || t1 == P) return Uc[((t1 == P) ? 1 : 0) * QQ + t3 * Q + t2];
+  if (t2 == 0 || t2 == P) return Uc[(2 + ((t2 == P) ? 1 : 0)) * QQ + t3 * Q + t1];
+  return Uc[(4 + ((t3 == P) ? 1 : 0)) * QQ + t2 * Q + t1];
+}
+
+template <int P>
+__global__ void __launch_bounds__(ElemCfg<P>::NT) k_elem_apply_t(LevelGeom g, const double* __restrict__ u,
+                                                                 const double* __restrict__ etab, double lam,
+                                                                 double* __restrict__ Y, const int* __restrict__ done) {
+  using C = ElemCfg<P>;
+  constexpr int M = C::M, Q = C::Q, MM = C::MM, QQ = C::QQ, NT = C::NT, TB = C::TB;
+  if (done && *done) return;
+  extern __shared__ double sm[];
+  double* Uc = sm + C::oUc;
+  double* T = sm + C::oT;
+  double* G = sm + C::oG;
+  double* tb = sm + C::oTab;
+  const long long e = blockIdx.x;
+  const int e1 = (int)(e % g.k1), e2 = (int)((e / g.k1) % g.k2), e3 = (int)(e / ((long long)g.k1 * g.k2));
+  const int tid = threadIdx.x;
+  const int ET = g.ET;
+  // tables: rebuild the per-direction block [Lam, P, Pt, a0, a1, M, K] from the global layout
+  {
+    const double* src[3] = {etab + (size_t)e1 * ET, etab + (size_t)(g.k1 + e2) * ET, etab + (size_t)(g.k1 + g.k2 + e3) * ET};
+    for (int i = tid; i < 3 * TB; i += NT) {
+      const int d = i / TB, o = i - d * TB;
+      const double* s = src[d];
+      double v;
+      if (o < C::tP) v = s[et_lam(P) + o];
+      else if (o < C::tPt) v = s[et_P(P) + (o - C::tP)];
+      else if (o < C::ta0) { int r = o - C::tPt, ia = r / M, b = r - ia * M; v = s[et_P(P) + b * M + ia]; }
+      else if (o < C::ta1) v = s[et_a0(P) + (o - C::ta0)];
+      else if (o < C::tM) v = s[et_a1(P) + (o - C::ta1)];
+      else if (o < C::tK) v = s[et_M(P) + (o - C::tM)];
+      else v = s[et_K(P) + (o - C::tK)];
+      tb[i] = v;
+    }
+  }
+  for (int i = tid; i < 6 * QQ; i += NT) {
+    const int f = i / QQ, r = i - f * QQ, A = r / Q, B = r - A * Q, d = f >> 1, s = f & 1;
+    int t1, t2, t3;
+    if (d == 0) { t1 = s * P; t3 = A; t2 = B; }
+    else if (d == 1) { t2 = s * P; t3 = A; t1 = B; }
+    else { t3 = s * P; t2 = A; t1 = B; }
+    Uc[i] = __ldg(&u[skel_index(g, e1 * P + t1, e2 * P + t2, e3 * P + t3)]);
+  }
+  __syncthreads();
+  // tangential directions of face f: a (fast) = x2 for d = 0 else x1; b (slow) = x3 for d < 2 else x2
+  // forward A: X_f[ib][ba] = sum_ia U_f[ib][ia] Pt_a[ia][ba]   (X in G's space)
+  double* X = G;
+  for (int i = tid; i < 6 * MM; i += NT) {
+    const int f = i / MM, r = i - f * MM, ib = r / M, ba = r - ib * M, d = f >> 1, da = (d == 0) ? 1 : 0;
+    const double* U = Uc + f * QQ + (ib + 1) * Q + 1;
+    const double* Pt = tb + da * TB + C::tPt;
+    double s = 0.0;
+#pragma unroll
+    for (int ia = 0; ia < M; ++ia) s = fma(U[ia], Pt[ia * M + ba], s);
+    X[i] = s;
+  }
+  __syncthreads();
+  // forward B: T_f[bb][ba] = sum_ib Pt_b[ib][bb] X_f[ib][ba]
+  for (int i = tid; i < 6 * MM; i += NT) {
+    const int f = i / MM, r = i - f * MM, bb = r / M, ba = r - bb * M, d = f >> 1, db = (d == 2) ? 1 : 2;
+    const double* Pt = tb + db * TB + C::tPt;
+    const double* Xf = X + f * MM;
+    double s = 0.0;
+#pragma unroll
+    for (int ib = 0; ib < M; ++ib) s = fma(Pt[ib * M + bb], Xf[ib * M + ba], s);
+    T[i] = s;
+  }
+  __syncthreads();
+  {
+    const double *L1 = tb + C::tLam, *L2 = tb + TB + C::tLam, *L3 = tb + 2 * TB + C::tLam;
+    const double *a10 = tb + C::ta0, *a11 = tb + C::ta1;
+    const double *a20 = tb + TB + C::ta0, *a21 = tb + TB + C::ta1;
+    const double *a30 = tb + 2 * TB + C::ta0, *a31 = tb + 2 * TB + C::ta1;
+    const double *T0 = T, *T1 = T + MM, *T2 = T + 2 * MM, *T3 = T + 3 * MM, *T4 = T + 4 * MM, *T5 = T + 5 * MM;
+    for (int i = tid; i < 3 * MM; i += NT) {
+      const int pass = i / MM, r = i - pass * MM, hi = r / M, lo = r - hi * M;
+      double g0 = 0.0, g1 = 0.0;
+      if (pass == 0) {          // (b3, b2), reduce over b1 -> faces 0, 1
+        const int b3 = hi, b2 = lo;
+        const double tA = T0[r], tB = T1[r], c2 = a20[b2], c2b = a21[b2], c3 = a30[b3], c3b = a31[b3];
+        const double base = lam + L2[b2] + L3[b3];
+#pragma unroll
+        for (int b1 = 0; b1 < M; ++b1) {
+          double E = a10[b1] * tA;
+          E = fma(a11[b1], tB, E);
+          E = fma(c2, T2[b3 * M + b1], E);
+          E = fma(c2b, T3[b3 * M + b1], E);
+          E = fma(c3, T4[b2 * M + b1], E);
+          E = fma(c3b, T5[b2 * M + b1], E);
+          const double V = E * rcp_nr(base + L1[b1]);
+          g0 = fma(a10[b1], V, g0);
+          g1 = fma(a11[b1], V, g1);
+        }
+      } else if (pass == 1) {   // (b3, b1), reduce over b2 -> faces 2, 3
+        const int b3 = hi, b1 = lo;
+        const double tA = T2[r], tB = T3[r], c1 = a10[b1], c1b = a11[b1], c3 = a30[b3], c3b = a31[b3];
+        const double base = lam + L1[b1] + L3[b3];
+#pragma unroll
+        for (int b2 = 0; b2 < M; ++b2) {
+          double E = c1 * T0[b3 * M + b2];
+          E = fma(c1b, T1[b3 * M + b2], E);
+          E = fma(a20[b2], tA, E);
+          E = fma(a21[b2], tB, E);
+          E = fma(c3, T4[b2 * M + b1], E);
+          E = fma(c3b, T5[b2 * M + b1], E);
+          const double V = E * rcp_nr(base + L2[b2]);
+          g0 = fma(a20[b2], V, g0);
+          g1 = fma(a21[b2], V, g1);
+        }
+      } else {                  // (b2, b1), reduce over b3 -> faces 4, 5
+        const int b2 = hi, b1 = lo;
+        const double tA = T4[r], tB = T5[r], c1 = a10[b1], c1b = a11[b1], c2 = a20[b2], c2b = a21[b2];
+        const double base = lam + L1[b1] + L2[b2];
+#pragma unroll
+        for (int b3 = 0; b3 < M; ++b3) {
+          double E = c1 * T0[b3 * M + b2];
+          E = fma(c1b, T1[b3 * M + b2], E);
+          E = fma(c2, T2[b3 * M + b1], E);
+          E = fma(c2b, T3[b3 * M + b1], E);
+          E = fma(a30[b3], tA, E);
+          E = fma(a31[b3], tB, E);
+          const double V = E * rcp_nr(base + L3[b3]);
+          g0 = fma(a30[b3], V, g0);
+          g1 = fma(a31[b3], V, g1);
+        }
+      }
+      G[(2 * pass) * MM + r] = g0;
+      G[(2 * pass + 1) * MM + r] = g1;
+    }
+  }
+  __syncthreads();
+  // back A: X_f[bb][ia] = sum_ba G_f[bb][ba] P_a[ba][ia]   (X in T's space)
+  X = T;
+  for (int i = tid; i < 6 * MM; i += NT) {
+    const int f = i / MM, r = i - f * MM, bb = r / M, ia = r - bb * M, d = f >> 1, da = (d == 0) ? 1 : 0;
+    const double* Pa = tb + da * TB + C::tP;
+    const double* Gf = G + f * MM + bb * M;
+    double s = 0.0;
+#pragma unroll
+    for (int ba = 0; ba < M; ++ba) s = fma(Gf[ba], Pa[ba * M + ia], s);
+    X[i] = s;
+  }
+  __syncthreads();
+  // back B: C_f[ib][ia] = sum_bb P_b[bb][ib] X_f[bb][ia]   (into G's space)
+  for (int i = tid; i < 6 * MM; i += NT) {
+    const int f = i / MM, r = i - f * MM, ib = r / M, ia = r - ib * M, d = f >> 1, db = (d == 2) ? 1 : 2;
+    const double* Pb = tb + db * TB + C::tP;
+    const double* Xf = X + f * MM;
+    double s = 0.0;
+#pragma unroll
+    for (int bb = 0; bb < M; ++bb) s = fma(Pb[bb * M + ib], Xf[bb * M + ia], s);
+    G[i] = s;
+  }
+  __syncthreads();
+  // outputs: H_BB u (line sums over the closed faces) minus the face corrections
+  const double *M1 = tb + C::tM, *M2 = tb + TB + C::tM, *M3 = tb + 2 * TB + C::tM;
+  const double *K1 = tb + C::tK, *K2 = tb + TB + C::tK, *K3 = tb + 2 * TB + C::tK;
+  double* Ye = Y + (size_t)e * g.YS;
+  constexpr int YS = 6 * MM + 12 * M + 8;
+  for (int o = tid; o < YS; o += NT) {
+    int t1, t2, t3;
+    double corr = 0.0;
+    if (o < 6 * MM) {
+      const int f = o / MM, r = o - f * MM, A = r / M, B = r - A * M, d = f >> 1, s = f & 1;
+      if (d == 0) { t1 = s * P; t3 = A + 1; t2 = B + 1; }
+      else if (d == 1) { t2 = s * P; t3 = A + 1; t1 = B + 1; }
+      else { t3 = s * P; t2 = A + 1; t1 = B + 1; }
+      corr = G[o];
+    } else if (o < 6 * MM + 12 * M) {
+      const int r = o - 6 * MM, qe = r / M, i = r - qe * M, d = qe >> 2, sA = qe & 1, sB = (qe >> 1) & 1;
+      if (d == 0) { t1 = i + 1; t2 = sA * P; t3 = sB * P; }
+      else if (d == 1) { t2 = i + 1; t1 = sA * P; t3 = sB * P; }
+      else { t3 = i + 1; t1 = sA * P; t2 = sB * P; }
+    } else {
+      const int qv = o - 6 * MM - 12 * M;
+      t1 = (qv & 1) * P; t2 = ((qv >> 1) & 1) * P; t3 = ((qv >> 2) & 1) * P;
+    }
+    const bool bd1 = (t1 == 0 || t1 == P), bd2 = (t2 == 0 || t2 == P), bd3 = (t3 == 0 || t3 == P);
+    double y = lam * M1[t1] * M2[t2] * M3[t3] * getUc<P>(Uc, t1, t2, t3);
+    double s = 0.0;
+    if (bd2 || bd3) {
+#pragma unroll
+      for (int t = 0; t <= P; ++t) s = fma(K1[t1 * Q + t], getUc<P>(Uc, t, t2, t3), s);
+    } else {
+      s = K1[t1 * Q] * getUc<P>(Uc, 0, t2, t3) + K1[t1 * Q + P] * getUc<P>(Uc, P, t2, t3);
+    }
+    y = fma(M2[t2] * M3[t3], s, y);
+    s = 0.0;
+    if (bd1 || bd3) {
+#pragma unroll
+      for (int t = 0; t <= P; ++t) s = fma(K2[t2 * Q + t], getUc<P>(Uc, t1, t, t3), s);
+    } else {
+      s = K2[t2 * Q] * getUc<P>(Uc, t1, 0, t3) + K2[t2 * Q + P] * getUc<P>(Uc, t1, P, t3);
+    }
+    y = fma(M1[t1] * M3[t3], s, y);
+    s = 0.0;
+    if (bd1 || bd2) {
+#pragma unroll
+      for (int t = 0; t <= P; ++t) s = fma(K3[t3 * Q + t], getUc<P>(Uc, t1, t2, t), s);
+    } else {
+      s = K3[t3 * Q] * getUc<P>(Uc, t1, t2, 0) + K3[t3 * Q + P] * getUc<P>(Uc, t1, t2, P);
+    }
+    y = fma(M1[t1] * M2[t2], s, y);
+    Ye[o] = y - corr;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// star smoother, one colour, degree P (n = 2P - 1, vertex index c = P - 1)
+// ------------------------------------------------------------------------------------------
+template <int P> struct StarCfg {
+  static constexpr int N = 2 * P - 1, NN = N * N, C = P - 1;
+  static constexpr int NT = (P <= 4) ? 64 : (P <= 8 ? 128 : 256);
+  static constexpr bool S_SMEM = (P <= 16);         // S and S^T staged in shared memory
+  static constexpr int XPL = 3;                      // planes per transform step
+  // X aliases G in the forward transform and FT in the back transform; U is written into G
+  static constexpr int oFT = 0, oG = 3 * NN, oVec = 6 * NN, oS = oVec + 9 * N;
+  static constexpr int total = oS + (S_SMEM ? 6 * NN : 0);
+};
+
+template <int P>
+size_t star_t_smem() { return sizeof(double) * StarCfg<P>::total; }
+
+// star table (global) per direction and vertex line: [S n^2][Lambda n][s n][w n]; S^T is built on the fly
+template <int P>
+__global__ void __launch_bounds__(StarCfg<P>::NT) k_star_t(LevelGeom g, int c1, int c2, int c3, int n1c, int n2c,
+                                                          const double* __restrict__ r, double* __restrict__ u,
+                                                          const double* __restrict__ stab, const double* __restrict__ stabT,
+                                                          double lam) {
+  using C = StarCfg<P>;
+  constexpr int N = C::N, NN = C::NN, c = C::C, NT = C::NT, XPL = C::XPL;
+  extern __shared__ double sm[];
+  const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
+  const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
+  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 == 0 || v3 == g.k3)) return;
+  const int tid = threadIdx.x, ST = g.ST;
+  const size_t row[3] = {(size_t)v1, (size_t)(g.V1 + v2), (size_t)(g.V1 + g.V2 + v3)};
+  double* FT = sm + C::oFT;
+  double* Gs = sm + C::oG;
+  double* X = Gs;
+  double* vec = sm + C::oVec;
+  const double* S[3];
+  const double* St[3];
+  if (C::S_SMEM) {
+    double* Ssm = sm + C::oS;
+    for (int i = tid; i < 6 * NN; i += NT) {
+      const int k = i / NN, o = i - k * NN;     // k = 0..2: S of direction k; 3..5: S^T
+      Ssm[i] = (k < 3) ? __ldg(&stab[row[k] * ST + o]) : __ldg(&stabT[row[k - 3] * NN + o]);
+    }
+    for (int d = 0; d < 3; ++d) { S[d] = Ssm + d * NN; St[d] = Ssm + (3 + d) * NN; }
+  } else {
+    for (int d = 0; d < 3; ++d) { S[d] = stab + row[d] * ST; St[d] = stabT + row[d] * NN; }
+  }
+  for (int i = tid; i < 9 * N; i += NT) { const int d = i / (3 * N); vec[i] = __ldg(&stab[row[d] * ST + NN + i - d * 3 * N]); }
+  const int o1 = (v1 - 1) * P + 1, o2 = (v2 - 1) * P + 1, o3 = (v3 - 1) * P + 1;
+  for (int i = tid; i < 3 * NN; i += NT) {
+    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
+    int j1, j2, j3;
+    if (d == 0) { j1 = c; j2 = B; j3 = A; } else if (d == 1) { j2 = c; j1 = B; j3 = A; } else { j3 = c; j1 = B; j2 = A; }
+    const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
+    const double val = inside(g, g1, g2, g3) ? __ldg(&r[skel_index(g, g1, g2, g3)]) : 0.0;
+    FT[i] = val * (1.0 / (double)(1 + (A == c) + (B == c)));   // inverse multiplicity
+  }
+  __syncthreads();
+  // forward: X_d[jb][aa] = sum_ja F_d[jb][ja] S_a[ja][aa];  T_d[ab][aa] = sum_jb S_b[jb][ab] X_d[jb][aa]
+  for (int d0 = 0; d0 < 3; d0 += XPL) {
+    for (int i = tid; i < XPL * NN; i += NT) {
+      const int dd = i / NN, rr = i - dd * NN, jb = rr / N, aa = rr - jb * N, d = d0 + dd;
+      const double* Sa = S[d == 0 ? 1 : 0];
+      const double* F = FT + d * NN + jb * N;
+      double s = 0.0;
+#pragma unroll
+      for (int ja = 0; ja < N; ++ja) s = fma(F[ja], Sa[ja * N + aa], s);
+      X[i] = s;
+    }
+    __syncthreads();
+    for (int i = tid; i < XPL * NN; i += NT) {
+      const int dd = i / NN, rr = i - dd * NN, ab = rr / N, aa = rr - ab * N, d = d0 + dd;
+      const double* Sb = S[d == 2 ? 1 : 2];
+      const double* Xd = X + dd * NN;
+      double s = 0.0;
+#pragma unroll
+      for (int jb = 0; jb < N; ++jb) s = fma(Sb[jb * N + ab], Xd[jb * N + aa], s);
+      FT[d * NN + rr] = s;
+    }
+    __syncthreads();
+  }
+  // fused core (expand / D^-1 / contract), three passes each reducing along one axis
+  {
+    const double *L1 = vec, *s1 = vec + N, *L2 = vec + 3 * N, *s2 = vec + 4 * N, *L3 = vec + 6 * N, *s3 = vec + 7 * N;
+    const double *T1 = FT, *T2 = FT + NN, *T3 = FT + 2 * NN;
+    for (int i = tid; i < 3 * NN; i += NT) {
+      const int pass = i / NN, rr = i - pass * NN, hi = rr / N, lo = rr - hi * N;
+      double acc = 0.0;
+      if (pass == 0) {          // G1[a3][a2] = sum_a1 s1[a1] E
+        const int a3 = hi, a2 = lo;
+        const double t1 = T1[rr], x2 = s2[a2], x3 = s3[a3], base = lam + L2[a2] + L3[a3];
+#pragma unroll
+        for (int a1 = 0; a1 < N; ++a1) {
+          double E = s1[a1] * t1;
+          E = fma(x2, T2[a3 * N + a1], E);
+          E = fma(x3, T3[a2 * N + a1], E);
+          acc = fma(s1[a1], E * rcp_nr(base + L1[a1]), acc);
+        }
+      } else if (pass == 1) {   // G2[a3][a1] = sum_a2 s2[a2] E
+        const int a3 = hi, a1 = lo;
+        const double t2 = T2[rr], x1 = s1[a1], x3 = s3[a3], base = lam + L1[a1] + L3[a3];
+#pragma unroll
+        for (int a2 = 0; a2 < N; ++a2) {
+          double E = x1 * T1[a3 * N + a2];
+          E = fma(s2[a2], t2, E);
+          E = fma(x3, T3[a2 * N + a1], E);
+          acc = fma(s2[a2], E * rcp_nr(base + L2[a2]), acc);
+        }
+      } else {                  // G3[a2][a1] = sum_a3 s3[a3] E
+        const int a2 = hi, a1 = lo;
+        const double t3 = T3[rr], x1 = s1[a1], x2 = s2[a2], base = lam + L1[a1] + L2[a2];
+#pragma unroll
+        for (int a3 = 0; a3 < N; ++a3) {
+          double E = x1 * T1[a3 * N + a2];
+          E = fma(x2, T2[a3 * N + a1], E);
+          E = fma(s3[a3], t3, E);
+          acc = fma(s3[a3], E * rcp_nr(base + L3[a3]), acc);
+        }
+      }
+      Gs[i] = acc;
+    }
+  }
+  __syncthreads();
+  // back: X_d[ab][ja] = sum_aa G_d[ab][aa] S_a^T[aa][ja]  (X in FT's space);
+  //       U_d[jb][ja] = sum_ab S_b[jb][ab] X_d[ab][ja]      (U in G's space)
+  X = FT;
+  for (int d0 = 0; d0 < 3; d0 += XPL) {
+    for (int i = tid; i < XPL * NN; i += NT) {
+      const int dd = i / NN, rr = i - dd * NN, ab = rr / N, ja = rr - ab * N, d = d0 + dd;
+      const double* Sta = St[d == 0 ? 1 : 0];
+      const double* Gd = Gs + d * NN + ab * N;
+      double s = 0.0;
+#pragma unroll
+      for (int aa = 0; aa < N; ++aa) s = fma(Gd[aa], Sta[aa * N + ja], s);
+      X[i] = s;
+    }
+    __syncthreads();
+    for (int i = tid; i < XPL * NN; i += NT) {
+      const int dd = i / NN, rr = i - dd * NN, jb = rr / N, ja = rr - jb * N, d = d0 + dd;
+      const double* Sb = S[d == 2 ? 1 : 2];
+      const double* Xd = X + dd * NN;
+      double s = 0.0;
+#pragma unroll
+      for (int ab = 0; ab < N; ++ab) s = fma(Sb[jb * N + ab], Xd[ab * N + ja], s);
+      Gs[d * NN + rr] = s;
+    }
+    __syncthreads();
+  }
+  const double *w1 = vec + 2 * N, *w2 = vec + 5 * N, *w3 = vec + 8 * N;
+  for (int i = tid; i < 3 * NN; i += NT) {
+    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
+    int j1, j2, j3;
+    if (d == 0) { j1 = c; j2 = B; j3 = A; }
+    else if (d == 1) { j2 = c; j1 = B; j3 = A; if (j1 == c) continue; }
+    else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
+    const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
+    if (!is_free(g, g1, g2, g3)) continue;
+    const long long idx = skel_index(g, g1, g2, g3);
+    u[idx] += w1[j1] * w2[j2] * w3[j3] * Gs[i];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// dispatch
+// ------------------------------------------------------------------------------------------
+#define PMG_DEGREES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) \
+  X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32)
+
+cudaError_t launch_elem_apply(const LevelGeom& g, const double* u, const double* etab, double lam, double* Y,
+                              const int* done, cudaStream_t st) {
+  switch (g.p) {
+#define CASE(P)                                                                                     \
+  case P:                                                                                           \
+    k_elem_apply_t<P><<<(unsigned)g.nelem, ElemCfg<P>::NT, elem_t_smem<P>(), st>>>(g, u, etab, lam, Y, done); \
+    break;
+    PMG_DEGREES(CASE)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_star(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c, long long nb, const double* r,
+                        double* u, const double* stab, const double* stabT, double lam, cudaStream_t st) {
+  switch (g.p) {
+#define CASE(P)                                                                                     \
+  case P:                                                                                           \
+    k_star_t<P><<<(unsigned)nb, StarCfg<P>::NT, star_t_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam); \
+    break;
+    PMG_DEGREES(CASE)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+size_t hot_smem(int p, int which) {
+  switch (p) {
+#define CASE(P) \
+  case P: return which == 0 ? elem_t_smem<P>() : star_t_smem<P>();
+    PMG_DEGREES(CASE)
+#undef CASE
+    default: return 0;
+  }
+}
+
+cudaError_t hot_set_smem_attr(int bytes) {
+  cudaError_t e = cudaSuccess;
+#define CASE(P)                                                                                        \
+  {                                                                                                    \
+    cudaError_t a = cudaFuncSetAttribute(k_elem_apply_t<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+    cudaError_t b = cudaFuncSetAttribute(k_star_t<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);       \
+    if (a != cudaSuccess) e = a;                                                                       \
+    if (b != cudaSuccess) e = b;                                                                       \
+  }
+  PMG_DEGREES(CASE)
+#undef CASE
+  return e;
+}
+
+}  // namespace pmg

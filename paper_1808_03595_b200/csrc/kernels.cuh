@@ -8,8 +8,20 @@ namespace pmg {
 
 struct PcgState {
   double rz, bb, pq, alpha, beta, rr;
-  int done, its, breakdown, pad;
+  int done, its, breakdown, its_sum;   // its_sum / breakdown accumulate over coarse solves (reset per pmg_solve)
 };
+
+// degree-specialised hot kernels (hot_kernels.cu)
+cudaError_t launch_elem_apply(const LevelGeom& g, const double* u, const double* etab, double lam, double* Y,
+                              const int* done, cudaStream_t st);
+cudaError_t launch_star(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c, long long nb, const double* r,
+                        double* u, const double* stab, const double* stabT, double lam, cudaStream_t st);
+size_t hot_smem(int p, int which);   // which: 0 element, 1 star
+cudaError_t hot_set_smem_attr(int bytes);
+
+__global__ void k_pcg_coop_p2(LevelGeom g, const double* b, double* x, double* r, double* z, double* pv, double* q,
+                              const double* dinv, const double* etab, double lam, double* Y, double* part,
+                              PcgState* st, double rtol, int maxit);
 
 size_t elem_apply_smem(int p, int ET);
 size_t star_smem(int p, bool s_in_smem);

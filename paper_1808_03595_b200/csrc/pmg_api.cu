@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstddef>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -36,6 +37,7 @@ struct DevLevel {
   LevelGeom g;
   double* etab = nullptr;
   double* stab = nullptr;
+  double* stabT = nullptr;
   double* Jint = nullptr;
   double* u = nullptr;
   double* f = nullptr;
@@ -68,6 +70,9 @@ struct pmg_ctx {
   long long launches = 0;
   int last_coarse_its = 0;
   long long coarse_its_total = 0;
+  bool ref_kernels = false;  // PMG_REFERENCE_KERNELS=1: runtime-p v1 kernels (A/B checks only)
+  bool use_coop = false;     // coarse CG as one persistent cooperative kernel (p0 = 2)
+  int coop_nb = 0;
   // event timing (pmg_timing_enable)
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -121,8 +126,12 @@ int* done_ptr(pmg_ctx* c) { return reinterpret_cast<int*>(reinterpret_cast<char*
 pmg_status residual_dev(pmg_ctx* c, int l, const double* u, const double* f, double* r, const int* done = nullptr) {
   const DevLevel& D = c->D[l];
   TimedRegion tr(c, 1, l == c->L);
-  size_t sm = elem_apply_smem(D.g.p, D.g.ET);
-  k_elem_apply<<<(unsigned)D.g.nelem, kThreads, sm, c->st>>>(D.g, u, D.etab, c->lam, c->Y, done);
+  if (c->ref_kernels) {
+    size_t sm = elem_apply_smem(D.g.p, D.g.ET);
+    k_elem_apply<<<(unsigned)D.g.nelem, kThreads, sm, c->st>>>(D.g, u, D.etab, c->lam, c->Y, done);
+  } else {
+    launch_elem_apply(D.g, u, D.etab, c->lam, c->Y, done, c->st);
+  }
   LAUNCH_CHECK(c);
   k_gather_resid<<<grid_for(D.g.nskel), kThreads, 0, c->st>>>(D.g, c->Y, f, r, done);
   LAUNCH_CHECK(c);
@@ -138,7 +147,10 @@ pmg_status smooth_dev(pmg_ctx* c, int l, const double* r, double* u) {
     int c1 = col & 1, c2 = (col >> 1) & 1, c3 = (col >> 2) & 1;
     int n1 = (g.k1 - c1) / 2 + 1, n2 = (g.k2 - c2) / 2 + 1, n3 = (g.k3 - c3) / 2 + 1;
     long long nb = (long long)n1 * n2 * n3;
-    k_star<<<(unsigned)nb, kThreads, sm, c->st>>>(g, c1, c2, c3, n1, n2, r, u, D.stab, c->lam, c->star_s_smem ? 1 : 0);
+    if (c->ref_kernels)
+      k_star<<<(unsigned)nb, kThreads, sm, c->st>>>(g, c1, c2, c3, n1, n2, r, u, D.stab, c->lam, c->star_s_smem ? 1 : 0);
+    else
+      launch_star(g, c1, c2, c3, n1, n2, nb, r, u, D.stab, D.stabT, c->lam, c->st);
     LAUNCH_CHECK(c);
   }
   return PMG_OK;
@@ -194,6 +206,21 @@ pmg_status norm_host(pmg_ctx* c, const double* x, long long n, double* out) {
 pmg_status pcg_dev(pmg_ctx* c, const double* b, double* x) {
   const DevLevel& D = c->D[0];
   const long long n = D.g.nskel;
+  if (c->use_coop) {   // one launch, no host synchronisation; statistics read at the end of solve
+    LevelGeom g0 = D.g;
+    double lam = c->lam, rtol = c->opt.coarse_rtol;
+    int maxit = c->opt.coarse_maxit;
+    double* Y = c->Y;
+    double* part = c->part;
+    PcgState* st = c->pcg;
+    const double* dinv = c->dinv;
+    const double* etab = D.etab;
+    void* args[] = {&g0, (void*)&b, &x, &c->cr, &c->cz, &c->cp, &c->cq, (void*)&dinv, (void*)&etab, &lam, &Y, &part,
+                    &st, &rtol, &maxit};
+    CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_pcg_coop_p2, dim3(c->coop_nb), dim3(kThreads), args, 0, c->st));
+    c->launches++;
+    return PMG_OK;
+  }
   double* part2 = c->part + kRedBlocks;
   int* done = done_ptr(c);
   k_pcg_init<<<kRedBlocks, kThreads, 0, c->st>>>(b, c->dinv, x, c->cr, c->cz, c->cp, n, c->part, part2);
@@ -306,6 +333,7 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
   DevLevel& D = c->D[c->L];
   pmg_status s;
   c->coarse_its_total = 0;
+  CUDA_CHECK(cudaMemsetAsync(c->pcg, 0, sizeof(PcgState), c->st));
   if ((s = condense_dev(c, F, D.f))) return s;
   if ((s = zero_dev(c, D.u, D.g.nskel))) return s;
   if ((s = residual_dev(c, c->L, D.u, D.f, D.r))) return s;
@@ -322,6 +350,13 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
     if (rep && rep->history && cycles < rep->history_cap) rep->history[cycles] = rn;
   }
   if ((s = recover_dev(c, D.u, F, ufull))) return s;
+  if (c->use_coop) {
+    PcgState hs;
+    CUDA_CHECK(cudaMemcpyAsync(&hs, c->pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, c->st));
+    CUDA_CHECK(cudaStreamSynchronize(c->st));
+    c->coarse_its_total = hs.its_sum;
+    if (hs.breakdown) return fail(PMG_EBREAKDOWN, "coarse CG breakdown: p^T H p <= 0");
+  }
   bool conv = rn <= rtol * r0;
   if (rep) {
     rep->cycles = cycles;
@@ -443,7 +478,10 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   for (int l = 0; l <= L; ++l) {
     DevLevel& D = c->D[l];
     D.g = c->H[l].g;
-    if ((s = upload(&D.etab, c->H[l].etab)) || (s = upload(&D.stab, c->H[l].stab))) { free_ctx(c); return s; }
+    if ((s = upload(&D.etab, c->H[l].etab)) || (s = upload(&D.stab, c->H[l].stab)) ||
+        (s = upload(&D.stabT, c->H[l].stabT))) { free_ctx(c); return s; }
+    max_elem = std::max(max_elem, hot_smem(D.g.p, 0));
+    max_star = std::max(max_star, hot_smem(D.g.p, 1));
     if (l >= 1 && (s = upload(&D.Jint, c->H[l].Jint))) { free_ctx(c); return s; }
     if (dalloc(&D.u, D.g.nskel) || dalloc(&D.f, D.g.nskel) || dalloc(&D.r, D.g.nskel)) { free_ctx(c); return fail(PMG_ENOMEM, "cudaMalloc failed (level vectors)"); }
     cudaMemset(D.u, 0, D.g.nskel * sizeof(double));
@@ -457,13 +495,14 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
     }
   }
   const LevelGeom& gt = c->D[L].g;
-  c->star_s_smem = star_smem(p, true) <= (size_t)smem_optin;
-  for (int l = 0; l <= L; ++l) max_star = std::max(max_star, star_smem(c->D[l].g.p, c->star_s_smem && star_smem(c->D[l].g.p, true) <= (size_t)smem_optin));
-  if (!c->star_s_smem) {
-    // the top level decides; lower levels always fit, but one flag is used for all levels
-    max_star = 0;
-    for (int l = 0; l <= L; ++l) max_star = std::max(max_star, star_smem(c->D[l].g.p, false));
+  {
+    const char* env = std::getenv("PMG_REFERENCE_KERNELS");
+    c->ref_kernels = env && env[0] == '1';
   }
+  // the v1 reference star kernel keeps S in shared memory when the top level allows it
+  c->star_s_smem = star_smem(p, true) <= (size_t)smem_optin;
+  if (c->ref_kernels)
+    for (int l = 0; l <= L; ++l) max_star = std::max(max_star, star_smem(c->D[l].g.p, c->star_s_smem));
   c->cube_in_smem = std::max(condense_smem(p, gt.ET, true), recover_smem(p, gt.ET, true)) <= (size_t)smem_optin;
   size_t max_cond = condense_smem(p, gt.ET, c->cube_in_smem), max_rec = recover_smem(p, gt.ET, c->cube_in_smem);
   Ylen = std::max<size_t>(Ylen, (size_t)gt.nelem * 6 * gt.m * gt.m);
@@ -472,7 +511,7 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
     free_ctx(c);
     return fail(PMG_EINVAL, "shared-memory plan exceeds the device limit for this p");
   }
-  if (dalloc(&c->Y, Ylen) || dalloc(&c->Z, Zlen) || dalloc(&c->part, 2 * kRedBlocks) || dalloc(&c->dres, 8) ||
+  if (dalloc(&c->Y, Ylen) || dalloc(&c->Z, Zlen) || dalloc(&c->part, 4096) || dalloc(&c->dres, 8) ||
       dalloc(&c->pcg, 1)) {
     free_ctx(c);
     return fail(PMG_ENOMEM, "cudaMalloc failed (workspaces)");
@@ -506,7 +545,22 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   cudaError_t e4 = cudaFuncSetAttribute(k_prolong, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
   cudaError_t e5 = cudaFuncSetAttribute(k_condense_elem, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
   cudaError_t e6 = cudaFuncSetAttribute(k_recover_elem, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  if (e6 == cudaSuccess) e6 = hot_set_smem_attr(smem_optin);
   if (e1 || e2 || e3 || e4 || e5 || e6) { free_ctx(c); return fail(PMG_ECUDA, "cudaFuncSetAttribute failed"); }
+  // persistent cooperative coarse CG when the coarse degree is 2 and the device supports it
+  {
+    int coop = 0, nsm = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_coop_p2, kThreads, 0);
+    const char* env = std::getenv("PMG_COARSE_MULTIKERNEL");
+    if (coop && per_sm > 0 && c->D[0].g.p == 2 && !(env && env[0] == '1')) {
+      long long want = (c->D[0].g.nskel + 4 * kThreads - 1) / (4 * kThreads);
+      long long cap = std::min<long long>((long long)per_sm * nsm, 1344);
+      c->coop_nb = (int)std::max<long long>(1, std::min(want, cap));
+      c->use_coop = true;
+    }
+  }
   cudaError_t es = cudaDeviceSynchronize();
   if (es != cudaSuccess) { free_ctx(c); return fail(PMG_ECUDA, std::string("setup: ") + cudaGetErrorString(es)); }
   *out = c;

@@ -55,6 +55,7 @@ struct HostLevel {
   LevelGeom g;
   std::vector<double> etab;      // (k1 + k2 + k3) * ET
   std::vector<double> stab;      // (V1 + V2 + V3) * ST
+  std::vector<double> stabT;     // (V1 + V2 + V3) * n^2: S^T of each star table row
   std::vector<double> Jint;      // (p - 1) x (p_c + 1): rows 1..p-1 of J (coarse -> this level)
   std::vector<double> coords[3];
 };
