@@ -1,14 +1,22 @@
 // Coarse-grid solver (reading R11): Jacobi-preconditioned CG on the condensed p0 = 2
 // system, as ONE persistent cooperative kernel (grid-wide barriers between the phases of an
 // iteration).  The coarse solve is latency bound: a multi-kernel CG spends
-// ~10 launches per iteration; here the whole solve is one launch.
+// ~10 launches per iteration; here the whole solve is one launch with 2 grid barriers per
+// iteration.
+//
+// Operator: at p = 2 every element has one interior point, so the element Schur complement is
+//   H_hat_e = H_BB,e - (1/D_e) c_e c_e^T,  c_e[f] = a_f P_b P_a on the 6 face centres,
+// (reading R1 with m = 1) and sum_e H_BB,e is the assembled tensor-product operator
+//   H = lam B3(x)B2(x)B1 + B3(x)B2(x)K1 + B3(x)K2(x)B1 + K3(x)B2(x)B1
+// restricted to the skeleton with zero element interiors (B_d / K_d the assembled 1-D lumped
+// mass / stiffness, 5-point along each grid line).  So q = H_hat p is a 13-point line stencil
+// minus rank-one element corrections, V_e = (c_e . p_e) / D_e, evaluated on the fly.
 //
 // Every block reduces the per-block partial sums itself in a fixed order, so all blocks take the
 // same (bitwise identical) decisions on alpha, beta and convergence without another barrier,
-// and the result is deterministic.  The iteration and stopping rule are those of the oracle's
-// pcg(): x = 0, r = b, z = D^-1 r, p = z; per iteration q = H p, alpha = r.z / p.q,
-// x += alpha p, r -= alpha q, stop when ||r|| <= rtol ||b||, z = D^-1 r, beta = r.z_new / r.z,
-// p = z + beta p.
+// and the result is deterministic.  Iteration and stopping rule as the oracle's pcg(): x = 0,
+// r = b, z = D^-1 r, p = z; q = H p, alpha = r.z / p.q, x += alpha p, r -= alpha q, stop when
+// ||r|| <= rtol ||b||, z = D^-1 r, beta = r.z_new / r.z, p = z + beta p.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -18,83 +26,6 @@
 namespace cg = cooperative_groups;
 
 namespace pmg {
-
-// y_e = H_hat_e u_B for one p = 2 element (26 boundary values, compact element-output order of
-// k_elem_apply): H_BB u_B = (H_e u~)_B with u~ = u_B extended by a zero interior, minus the face
-// corrections C_f = P_b P_a a_f V, V = (sum_f a_f P_b P_a u_f) / (lam + L1 + L2 + L3).
-__device__ void elem_apply_p2(const LevelGeom& g, long long e, const double* __restrict__ u,
-                              const double* __restrict__ etab, double lam, double* __restrict__ Ye) {
-  const int p = 2, ET = g.ET;
-  const int e1 = (int)(e % g.k1), e2 = (int)((e / g.k1) % g.k2), e3 = (int)(e / ((long long)g.k1 * g.k2));
-  const double* T[3] = {etab + (size_t)e1 * ET, etab + (size_t)(g.k1 + e2) * ET, etab + (size_t)(g.k1 + g.k2 + e3) * ET};
-  double c[27];
-#pragma unroll
-  for (int t3 = 0; t3 < 3; ++t3)
-#pragma unroll
-    for (int t2 = 0; t2 < 3; ++t2)
-#pragma unroll
-      for (int t1 = 0; t1 < 3; ++t1) {
-        const int i = (t3 * 3 + t2) * 3 + t1;
-        if (t1 == 1 && t2 == 1 && t3 == 1) { c[i] = 0.0; continue; }
-        c[i] = __ldcg(&u[skel_index(g, e1 * p + t1, e2 * p + t2, e3 * p + t3)]);   // u changes in-kernel: L2 path
-      }
-  double M[3][3], K[3][9];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-#pragma unroll
-    for (int i = 0; i < 3; ++i) M[d][i] = __ldg(&T[d][et_M(p) + i]);
-#pragma unroll
-    for (int i = 0; i < 9; ++i) K[d][i] = __ldg(&T[d][et_K(p) + i]);
-  }
-  // face corrections (m = 1): T_f = P_b P_a u_f ; E = sum a_f T_f ; V = E / D
-  double Pd[3], a0[3], a1[3], Ld[3];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    Pd[d] = __ldg(&T[d][et_P(p)]);
-    a0[d] = __ldg(&T[d][et_a0(p)]);
-    a1[d] = __ldg(&T[d][et_a1(p)]);
-    Ld[d] = __ldg(&T[d][et_lam(p)]);
-  }
-  // face centre values: x1 faces (t1 = 0, 2; t2 = t3 = 1), x2 faces, x3 faces
-  const double uf[6] = {c[(1 * 3 + 1) * 3 + 0], c[(1 * 3 + 1) * 3 + 2], c[(1 * 3 + 0) * 3 + 1],
-                        c[(1 * 3 + 2) * 3 + 1], c[(0 * 3 + 1) * 3 + 1], c[(2 * 3 + 1) * 3 + 1]};
-  const double PbPa[3] = {Pd[2] * Pd[1], Pd[2] * Pd[0], Pd[1] * Pd[0]};
-  double E = 0.0;
-#pragma unroll
-  for (int f = 0; f < 6; ++f) {
-    const int d = f >> 1;
-    E += ((f & 1) ? a1[d] : a0[d]) * PbPa[d] * uf[f];
-  }
-  const double V = E / (lam + Ld[0] + Ld[1] + Ld[2]);
-  // outputs in the compact order: faces (6), edges (12), vertices (8)
-  auto Hu = [&](int t1, int t2, int t3) -> double {
-    double y = lam * M[0][t1] * M[1][t2] * M[2][t3] * c[(t3 * 3 + t2) * 3 + t1];
-    double s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-    for (int s = 0; s < 3; ++s) {
-      s1 += K[0][t1 * 3 + s] * c[(t3 * 3 + t2) * 3 + s];
-      s2 += K[1][t2 * 3 + s] * c[(t3 * 3 + s) * 3 + t1];
-      s3 += K[2][t3 * 3 + s] * c[(s * 3 + t2) * 3 + t1];
-    }
-    return y + M[1][t2] * M[2][t3] * s1 + M[0][t1] * M[2][t3] * s2 + M[0][t1] * M[1][t2] * s3;
-  };
-#pragma unroll
-  for (int f = 0; f < 6; ++f) {
-    const int d = f >> 1, s = (f & 1) * 2;
-    int t1 = 1, t2 = 1, t3 = 1;
-    if (d == 0) t1 = s; else if (d == 1) t2 = s; else t3 = s;
-    Ye[f] = Hu(t1, t2, t3) - ((f & 1) ? a1[d] : a0[d]) * PbPa[d] * V;
-  }
-#pragma unroll
-  for (int qe = 0; qe < 12; ++qe) {
-    const int d = qe >> 2, sA = (qe & 1) * 2, sB = ((qe >> 1) & 1) * 2;
-    int t1, t2, t3;
-    if (d == 0) { t1 = 1; t2 = sA; t3 = sB; } else if (d == 1) { t2 = 1; t1 = sA; t3 = sB; } else { t3 = 1; t1 = sA; t2 = sB; }
-    Ye[6 + qe] = Hu(t1, t2, t3);
-  }
-#pragma unroll
-  for (int qv = 0; qv < 8; ++qv) Ye[18 + qv] = Hu((qv & 1) * 2, ((qv >> 1) & 1) * 2, ((qv >> 2) & 1) * 2);
-}
 
 // sum of the block's values -> thread 0
 __device__ __forceinline__ double block_reduce(double v, double* red) {
@@ -124,77 +55,172 @@ __device__ __forceinline__ double grid_total(const double* part, int nb, double*
   return t;
 }
 
-__global__ void __launch_bounds__(256) k_pcg_coop_p2(LevelGeom g, const double* __restrict__ b, double* __restrict__ x,
-                                                    double* __restrict__ r, double* __restrict__ z, double* __restrict__ pv,
-                                                    double* __restrict__ q, const double* __restrict__ dinv,
-                                                    const double* __restrict__ etab, double lam, double* __restrict__ Y,
+// Skeleton-vector index of a point, or -1 outside the box (no memory access here)
+// p = 2 specialisation of skel_index: shifts instead of divisions by p, 32-bit record math (the
+// coarse level has < 2^31 entries).  Record offset of the point from the parities (t1,t2,t3):
+// (0,1,1) f1 = 0, (1,0,1) f2 = 1, (1,1,0) f3 = 2, (1,0,0) e1 = 3, (0,1,0) e2 = 4, (0,0,1) e3 = 5,
+// (0,0,0) vertex = 6, packed as nibbles of 0xF0152436 indexed by t1 + 2 t2 + 4 t3.
+__device__ __forceinline__ long long sidx2(const LevelGeom& g, int g1, int g2, int g3) {
+  const int key = (g1 & 1) | ((g2 & 1) << 1) | ((g3 & 1) << 2);
+  const int off = (int)((0xF0152436u >> (4 * key)) & 0xFu);
+  const int rec = (g1 >> 1) + g.V1 * ((g2 >> 1) + g.V2 * (g3 >> 1));
+  return (long long)rec * 7 + off;
+}
+
+__device__ __forceinline__ long long sidx_or_neg(const LevelGeom& g, int g1, int g2, int g3) {
+  return inside(g, g1, g2, g3) ? sidx2(g, g1, g2, g3) : -1LL;
+}
+
+// p = 2 entry decode: record = idx / 7 (constant divisor), parities from the record offset
+__device__ __forceinline__ Entry decode2(const LevelGeom& g, long long idx) {
+  Entry E;
+  const int i = (int)idx;
+  const int rec = i / 7, o = i - rec * 7;
+  const int r2 = rec / g.V1;
+  E.v1 = rec - r2 * g.V1;
+  E.v3 = r2 / g.V2;
+  E.v2 = r2 - E.v3 * g.V2;
+  E.g1 = 2 * E.v1 + ((0x0E >> o) & 1);
+  E.g2 = 2 * E.v2 + ((0x15 >> o) & 1);
+  E.g3 = 2 * E.v3 + ((0x23 >> o) & 1);
+  E.type = o;            // 0-2 faces, 3-5 edges, 6 vertex (m = 1)
+  E.a = 0; E.b = 0;
+  return E;
+}
+
+// Branch-free gather: all loads are issued back to back (a predicated index, then a select), so an
+// entry costs one L2 round trip instead of a chain of dependent ones.  p is written inside the
+// kernel -> L2 path (__ldcg).
+__device__ __forceinline__ double ld_sel(const double* p, long long i) {
+  const double v = __ldcg(&p[i < 0 ? 0 : i]);
+  return i < 0 ? 0.0 : v;
+}
+
+// q = H_hat p at one skeleton entry (p = 2); the element corrections V_e(p) of the (at most two)
+// elements adjacent to a face centre are evaluated on the fly
+__device__ __forceinline__ double apply_entry(const LevelGeom& g, const CoarseTabs& ct, const double* p,
+                                              long long idx, double lam) {
+  Entry E = decode2(g, idx);
+  if (!is_free(g, E.g1, E.g2, E.g3)) return 0.0;
+  const int G[3] = {E.g1, E.g2, E.g3};
+  const int N[3] = {2 * g.k1, 2 * g.k2, 2 * g.k3};
+  // indices: centre, then per direction the offsets -2, -1, +1, +2 along the line
+  long long ix[13];
+  ix[0] = idx;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2;
+    const bool full = ((G[da] & 1) == 0) || ((G[db] & 1) == 0);   // the line lies on the skeleton
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int o = (j < 2) ? j - 2 : j - 1;
+      const int s = G[d] + o;
+      int h[3] = {G[0], G[1], G[2]};
+      h[d] = s;
+      const bool ok = s >= 0 && s <= N[d] && (full || (s & 1) == 0);   // element interiors are zero
+      ix[1 + 4 * d + j] = ok ? sidx2(g, h[0], h[1], h[2]) : -1LL;
+    }
+  }
+  // face centre: the two adjacent elements' face-centre indices
+  long long fx[12];
+  double cw[2][7];
+  const bool face = E.type < 3;
+  if (face) {
+    const int d = E.type;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      int e[3] = {E.v1, E.v2, E.v3};
+      if (side == 1) e[d] -= 1;
+      const long long el = e[0] + (long long)g.k1 * (e[1] + (long long)g.k2 * e[2]);
+#pragma unroll
+      for (int i = 0; i < 7; ++i) cw[side][i] = __ldg(&ct.ce[el * 7 + i]);
+      const int b1 = 2 * e[0], b2 = 2 * e[1], b3 = 2 * e[2];
+      fx[6 * side + 0] = sidx_or_neg(g, b1, b2 + 1, b3 + 1);
+      fx[6 * side + 1] = sidx_or_neg(g, b1 + 2, b2 + 1, b3 + 1);
+      fx[6 * side + 2] = sidx_or_neg(g, b1 + 1, b2, b3 + 1);
+      fx[6 * side + 3] = sidx_or_neg(g, b1 + 1, b2 + 2, b3 + 1);
+      fx[6 * side + 4] = sidx_or_neg(g, b1 + 1, b2 + 1, b3);
+      fx[6 * side + 5] = sidx_or_neg(g, b1 + 1, b2 + 1, b3 + 2);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 12; ++i) fx[i] = -1;
+  }
+  double v[13], fv[12];
+#pragma unroll
+  for (int i = 0; i < 13; ++i) v[i] = ld_sel(p, ix[i]);
+#pragma unroll
+  for (int i = 0; i < 12; ++i) fv[i] = ld_sel(p, fx[i]);
+  const double* B[3] = {ct.b1, ct.b2, ct.b3};
+  const double* K[3] = {ct.K1, ct.K2, ct.K3};
+  double q = lam * __ldg(&B[0][G[0]]) * __ldg(&B[1][G[1]]) * __ldg(&B[2][G[2]]) * v[0];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2;
+    const double* Kr = K[d] + (size_t)G[d] * 5;
+    double acc = __ldg(&Kr[2]) * v[0];
+    acc = fma(__ldg(&Kr[0]), v[1 + 4 * d], acc);
+    acc = fma(__ldg(&Kr[1]), v[2 + 4 * d], acc);
+    acc = fma(__ldg(&Kr[3]), v[3 + 4 * d], acc);
+    acc = fma(__ldg(&Kr[4]), v[4 + 4 * d], acc);
+    q = fma(__ldg(&B[da][G[da]]) * __ldg(&B[db][G[db]]), acc, q);
+  }
+  if (face) {
+    const int d = E.type;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) s = fma(cw[side][i], fv[6 * side + i], s);
+      q = fma(-cw[side][2 * d + side], s * cw[side][6], q);
+    }
+  }
+  return q;
+}
+
+// Two grid barriers per iteration: with p_new = z + beta p and q = H_hat p,
+//   q_new = H_hat z + beta q_old,
+// so the direction update, the operator application (on z, complete after the previous barrier)
+// and the partial p.q share one phase; the x / r / z update and the partials r.r, r.z the other.
+__global__ void __launch_bounds__(256) k_pcg_coop_p2(LevelGeom g, CoarseTabs ct, const double* __restrict__ b,
+                                                    double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
+                                                    double* __restrict__ pv, double* __restrict__ q,
+                                                    const double* __restrict__ dinv, double lam,
                                                     double* __restrict__ part, PcgState* st, double rtol, int maxit) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[32];
   __shared__ double bc;
   const int nb = gridDim.x;
-  double* part_a = part;           // p.q, then r.z at init
-  double* part_b = part + nb;      // r.r, then b.b at init
+  double* part_a = part;           // p.q
+  double* part_b = part + nb;      // r.r (b.b at init)
   double* part_c = part + 2 * nb;  // r.z
   const long long n = g.nskel;
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
-  // init
   double s1 = 0.0, s2 = 0.0;
   for (long long i = tid; i < n; i += nth) {
     const double bi = b[i], zi = dinv[i] * bi;
-    x[i] = 0.0; r[i] = bi; z[i] = zi; pv[i] = zi;
-    s1 += bi * zi; s2 += bi * bi;
+    x[i] = 0.0; r[i] = bi; z[i] = zi; pv[i] = 0.0; q[i] = 0.0;
+    s1 = fma(bi, zi, s1); s2 = fma(bi, bi, s2);
   }
   s1 = block_reduce(s1, red);
-  if (threadIdx.x == 0) part_a[blockIdx.x] = s1;
+  if (threadIdx.x == 0) part_c[blockIdx.x] = s1;
   s2 = block_reduce(s2, red);
   if (threadIdx.x == 0) part_b[blockIdx.x] = s2;
   grid.sync();
-  double rz = grid_total(part_a, nb, &bc);
+  double rz = grid_total(part_c, nb, &bc);
   const double bb = grid_total(part_b, nb, &bc);
+  double beta = 0.0;
   int its = 0, breakdown = 0;
   bool done = (bb == 0.0);
-  grid.sync();   // everyone has read the partials before they are overwritten
   while (!done) {
-    // q = H p : element phase
-    for (long long e = tid; e < g.nelem; e += nth) elem_apply_p2(g, e, pv, etab, lam, Y + e * g.YS);
-    grid.sync();
-    // gather phase + partial p.q
+    // phase 1: p = z + beta p ; q = H_hat z + beta q ; partial p.q
     double spq = 0.0;
-    {
-      const int m = 1, mm = 1, YS = g.YS;
-      for (long long idx = tid; idx < n; idx += nth) {
-        Entry E = decode_entry(g, idx);
-        double s = 0.0;
-        if (is_free(g, E.g1, E.g2, E.g3)) {
-          auto el = [&](int a1, int a2, int a3) -> size_t {
-            return ((size_t)a1 + (size_t)g.k1 * ((size_t)a2 + (size_t)g.k2 * a3)) * YS;
-          };
-          if (E.type < 3) {
-            const int d = E.type;
-            int w1 = E.v1, w2 = E.v2, w3 = E.v3;
-            if (d == 0) w1 -= 1; else if (d == 1) w2 -= 1; else w3 -= 1;
-            s = __ldcg(&Y[el(w1, w2, w3) + (2 * d + 1) * mm]) + __ldcg(&Y[el(E.v1, E.v2, E.v3) + (2 * d) * mm]);
-          } else if (E.type < 6) {
-            const int d = E.type - 3;
-            for (int bB = 0; bB < 2; ++bB)
-              for (int bA = 0; bA < 2; ++bA) {
-                int a1 = E.v1, a2 = E.v2, a3 = E.v3;
-                if (d == 0) { a2 += bA - 1; a3 += bB - 1; } else if (d == 1) { a1 += bA - 1; a3 += bB - 1; }
-                else { a1 += bA - 1; a2 += bB - 1; }
-                s += __ldcg(&Y[el(a1, a2, a3) + 6 * mm + (4 * d + (1 - bA) + 2 * (1 - bB)) * m]);
-              }
-          } else {
-            for (int c3 = 0; c3 < 2; ++c3)
-              for (int c2 = 0; c2 < 2; ++c2)
-                for (int c1 = 0; c1 < 2; ++c1)
-                  s += __ldcg(&Y[el(E.v1 - 1 + c1, E.v2 - 1 + c2, E.v3 - 1 + c3) + 6 * mm + 12 * m +
-                                 (1 - c1) + 2 * (1 - c2) + 4 * (1 - c3)]);
-          }
-        }
-        q[idx] = s;
-        spq += pv[idx] * s;
-      }
+    for (long long i = tid; i < n; i += nth) {
+      const double pi_ = fma(beta, pv[i], z[i]);
+      const double qi = fma(beta, q[i], apply_entry(g, ct, z, i, lam));
+      pv[i] = pi_;
+      q[i] = qi;
+      spq = fma(pi_, qi, spq);
     }
     spq = block_reduce(spq, red);
     if (threadIdx.x == 0) part_a[blockIdx.x] = spq;
@@ -202,16 +228,16 @@ __global__ void __launch_bounds__(256) k_pcg_coop_p2(LevelGeom g, const double* 
     const double pq = grid_total(part_a, nb, &bc);
     if (!(pq > 0.0)) { breakdown = 1; break; }
     const double alpha = rz / pq;
-    // x += alpha p ; r -= alpha q ; z = D^-1 r ; partials r.r and r.z
+    // phase 2: x += alpha p ; r -= alpha q ; z = D^-1 r ; partials r.r, r.z
     double srr = 0.0, srz = 0.0;
     for (long long i = tid; i < n; i += nth) {
-      x[i] += alpha * pv[i];
-      const double ri = r[i] - alpha * q[i];
+      x[i] = fma(alpha, pv[i], x[i]);
+      const double ri = fma(-alpha, q[i], r[i]);
       r[i] = ri;
       const double zi = dinv[i] * ri;
       z[i] = zi;
-      srr += ri * ri;
-      srz += ri * zi;
+      srr = fma(ri, ri, srr);
+      srz = fma(ri, zi, srz);
     }
     srr = block_reduce(srr, red);
     if (threadIdx.x == 0) part_b[blockIdx.x] = srr;
@@ -222,10 +248,8 @@ __global__ void __launch_bounds__(256) k_pcg_coop_p2(LevelGeom g, const double* 
     const double rzn = grid_total(part_c, nb, &bc);
     ++its;
     if (sqrt(rr) <= rtol * sqrt(bb) || its >= maxit) break;
-    const double beta = rzn / rz;
+    beta = rzn / rz;
     rz = rzn;
-    for (long long i = tid; i < n; i += nth) pv[i] = z[i] + beta * pv[i];
-    grid.sync();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->its = its;

@@ -415,8 +415,178 @@ __global__ void __launch_bounds__(StarCfg<P>::NT) k_star_t(LevelGeom g, int c1, 
 }
 
 // ------------------------------------------------------------------------------------------
+// star smoother with a single-pass core (P <= 8): every (a1, a2, a3) triple of the eigenspace is
+// visited once.  Lanes of a GS-lane group own a1, groups own a3 values, a2 runs in registers:
+//   G2[a3][a1] = sum_a2 s2 V   accumulates in a register,
+//   G1[a3][a2] = sum_a1 s1 V   is a shuffle reduction inside the group,
+//   G3[a2][a1] = sum_a3 s3 V   is a per-group register partial, summed over groups in a fixed
+//                              order through shared memory (deterministic).
+// Per triple: 3 FMA for E, 1 add + rcp (MUFU + 4 FMA), 1 mul, 3 accumulations, ~log2(GS)/GS
+// shuffles -- versus three recomputations of E and 1/D in the 3-pass core.
+// ------------------------------------------------------------------------------------------
+template <int P> struct StarSpCfg {
+  static constexpr int N = 2 * P - 1, NN = N * N, C = P - 1;
+  static constexpr int GS = (N <= 4) ? 4 : (N <= 8 ? 8 : (N <= 16 ? 16 : 32));
+  static constexpr int NW = (P <= 4) ? 2 : 4;
+  static constexpr int NT = 32 * NW, GPW = 32 / GS, NG = NW * GPW;
+  static constexpr int A3IT = (N + NG - 1) / NG;      // warp-uniform a3 trip count
+  static constexpr int oFT = 0, oG = 3 * NN, oP3 = 6 * NN, oS = oP3 + NG * NN, oVec = oS + 6 * NN;
+  static constexpr int total = oVec + 9 * N;
+};
+
+template <int P>
+size_t star_sp_smem() { return sizeof(double) * StarSpCfg<P>::total; }
+
+template <int P>
+__global__ void __launch_bounds__(StarSpCfg<P>::NT) k_star_sp(LevelGeom g, int c1, int c2, int c3, int n1c, int n2c,
+                                                             const double* __restrict__ r, double* __restrict__ u,
+                                                             const double* __restrict__ stab,
+                                                             const double* __restrict__ stabT, double lam) {
+  using C = StarSpCfg<P>;
+  constexpr int N = C::N, NN = C::NN, c = C::C, NT = C::NT, GS = C::GS, GPW = C::GPW, NG = C::NG;
+  extern __shared__ double sm[];
+  const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
+  const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
+  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 == 0 || v3 == g.k3)) return;
+  const int tid = threadIdx.x, ST = g.ST;
+  const size_t row[3] = {(size_t)v1, (size_t)(g.V1 + v2), (size_t)(g.V1 + g.V2 + v3)};
+  double* FT = sm + C::oFT;
+  double* Gs = sm + C::oG;
+  double* P3 = sm + C::oP3;
+  double* Ssm = sm + C::oS;
+  double* vec = sm + C::oVec;
+  for (int i = tid; i < 6 * NN; i += NT) {
+    const int k = i / NN, o = i - k * NN;
+    Ssm[i] = (k < 3) ? __ldg(&stab[row[k] * ST + o]) : __ldg(&stabT[row[k - 3] * NN + o]);
+  }
+  for (int i = tid; i < 9 * N; i += NT) { const int d = i / (3 * N); vec[i] = __ldg(&stab[row[d] * ST + NN + i - d * 3 * N]); }
+  const double* S[3] = {Ssm, Ssm + NN, Ssm + 2 * NN};
+  const double* St[3] = {Ssm + 3 * NN, Ssm + 4 * NN, Ssm + 5 * NN};
+  const int o1 = (v1 - 1) * P + 1, o2 = (v2 - 1) * P + 1, o3 = (v3 - 1) * P + 1;
+  for (int i = tid; i < 3 * NN; i += NT) {
+    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
+    int j1, j2, j3;
+    if (d == 0) { j1 = c; j2 = B; j3 = A; } else if (d == 1) { j2 = c; j1 = B; j3 = A; } else { j3 = c; j1 = B; j2 = A; }
+    const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
+    const double val = inside(g, g1, g2, g3) ? __ldg(&r[skel_index(g, g1, g2, g3)]) : 0.0;
+    FT[i] = val * (1.0 / (double)(1 + (A == c) + (B == c)));   // inverse multiplicity
+  }
+  __syncthreads();
+  double* X = Gs;
+  for (int i = tid; i < 3 * NN; i += NT) {      // X_d = F_d S_a
+    const int d = i / NN, rr = i - d * NN, jb = rr / N, aa = rr - jb * N;
+    const double* Sa = S[d == 0 ? 1 : 0];
+    const double* F = FT + d * NN + jb * N;
+    double s = 0.0;
+#pragma unroll
+    for (int ja = 0; ja < N; ++ja) s = fma(F[ja], Sa[ja * N + aa], s);
+    X[i] = s;
+  }
+  __syncthreads();
+  for (int i = tid; i < 3 * NN; i += NT) {      // T_d = S_b^T X_d
+    const int d = i / NN, rr = i - d * NN, ab = rr / N, aa = rr - ab * N;
+    const double* Sb = S[d == 2 ? 1 : 2];
+    const double* Xd = X + d * NN;
+    double s = 0.0;
+#pragma unroll
+    for (int jb = 0; jb < N; ++jb) s = fma(Sb[jb * N + ab], Xd[jb * N + aa], s);
+    FT[i] = s;
+  }
+  __syncthreads();
+  {
+    const double *L1 = vec, *s1 = vec + N, *L2 = vec + 3 * N, *s2 = vec + 4 * N, *L3 = vec + 6 * N, *s3 = vec + 7 * N;
+    const double *T1 = FT, *T2 = FT + NN, *T3 = FT + 2 * NN;
+    const int lane = tid & 31, w = tid >> 5, grp = w * GPW + lane / GS, a1 = lane % GS;
+    const bool va = a1 < N;
+    const int a1c = va ? a1 : 0;
+    const double s1a = va ? s1[a1c] : 0.0, L1a = L1[a1c];
+    double g3[N];
+#pragma unroll
+    for (int a2 = 0; a2 < N; ++a2) g3[a2] = 0.0;
+    for (int k = 0; k < C::A3IT; ++k) {
+      const int a3 = grp + k * NG;
+      const bool act = a3 < N;
+      const int a3c = act ? a3 : 0;
+      const double on = (act && va) ? 1.0 : 0.0;
+      const double t2 = on * T2[a3c * N + a1c], s3v = on * s3[a3c], base = lam + L1a + L3[a3c];
+      const double s1v = on * s1a;
+      double g2 = 0.0;
+#pragma unroll
+      for (int a2 = 0; a2 < N; ++a2) {
+        double E = s1v * T1[a3c * N + a2];
+        E = fma(s2[a2], t2, E);
+        E = fma(s3v, T3[a2 * N + a1c], E);
+        const double V = E * rcp_nr(base + L2[a2]);
+        g2 = fma(s2[a2], V, g2);
+        g3[a2] = fma(s3v, V, g3[a2]);
+        double v = s1v * V;
+#pragma unroll
+        for (int o = GS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (act && a1 == 0) Gs[a3 * N + a2] = v;              // G1[a3][a2]
+      }
+      if (act && va) Gs[NN + a3 * N + a1] = g2;               // G2[a3][a1]
+    }
+    if (va) {
+#pragma unroll
+      for (int a2 = 0; a2 < N; ++a2) P3[grp * NN + a2 * N + a1] = g3[a2];
+    }
+    __syncthreads();
+    for (int i = tid; i < NN; i += NT) {                       // G3[a2][a1] = sum over groups
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < NG; ++q) s += P3[q * NN + i];
+      Gs[2 * NN + i] = s;
+    }
+  }
+  __syncthreads();
+  X = FT;
+  for (int i = tid; i < 3 * NN; i += NT) {      // X_d = G_d S_a^T
+    const int d = i / NN, rr = i - d * NN, ab = rr / N, ja = rr - ab * N;
+    const double* Sta = St[d == 0 ? 1 : 0];
+    const double* Gd = Gs + d * NN + ab * N;
+    double s = 0.0;
+#pragma unroll
+    for (int aa = 0; aa < N; ++aa) s = fma(Gd[aa], Sta[aa * N + ja], s);
+    X[i] = s;
+  }
+  __syncthreads();
+  for (int i = tid; i < 3 * NN; i += NT) {      // U_d = S_b X_d
+    const int d = i / NN, rr = i - d * NN, jb = rr / N, ja = rr - jb * N;
+    const double* Sb = S[d == 2 ? 1 : 2];
+    const double* Xd = X + d * NN;
+    double s = 0.0;
+#pragma unroll
+    for (int ab = 0; ab < N; ++ab) s = fma(Sb[jb * N + ab], Xd[ab * N + ja], s);
+    Gs[i] = s;
+  }
+  __syncthreads();
+  const double *w1 = vec + 2 * N, *w2 = vec + 5 * N, *w3 = vec + 8 * N;
+  for (int i = tid; i < 3 * NN; i += NT) {
+    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
+    int j1, j2, j3;
+    if (d == 0) { j1 = c; j2 = B; j3 = A; }
+    else if (d == 1) { j2 = c; j1 = B; j3 = A; if (j1 == c) continue; }
+    else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
+    const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
+    if (!is_free(g, g1, g2, g3)) continue;
+    u[skel_index(g, g1, g2, g3)] += w1[j1] * w2[j2] * w3[j3] * Gs[i];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // dispatch
 // ------------------------------------------------------------------------------------------
+constexpr bool kStarSinglePass(int p) { return p <= 8; }
+
+template <int P>
+void launch_star_p(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c, long long nb, const double* r,
+                   double* u, const double* stab, const double* stabT, double lam, cudaStream_t st) {
+  if constexpr (kStarSinglePass(P)) {
+    k_star_sp<P><<<(unsigned)nb, StarSpCfg<P>::NT, star_sp_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
+  } else {
+    k_star_t<P><<<(unsigned)nb, StarCfg<P>::NT, star_t_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
+  }
+}
 #define PMG_DEGREES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) \
   X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32)
 
@@ -439,7 +609,7 @@ cudaError_t launch_star(const LevelGeom& g, int c1, int c2, int c3, int n1c, int
   switch (g.p) {
 #define CASE(P)                                                                                     \
   case P:                                                                                           \
-    k_star_t<P><<<(unsigned)nb, StarCfg<P>::NT, star_t_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam); \
+    launch_star_p<P>(g, c1, c2, c3, n1c, n2c, nb, r, u, stab, stabT, lam, st);                    \
     break;
     PMG_DEGREES(CASE)
 #undef CASE
@@ -451,7 +621,7 @@ cudaError_t launch_star(const LevelGeom& g, int c1, int c2, int c3, int n1c, int
 size_t hot_smem(int p, int which) {
   switch (p) {
 #define CASE(P) \
-  case P: return which == 0 ? elem_t_smem<P>() : star_t_smem<P>();
+  case P: return which == 0 ? elem_t_smem<P>() : (kStarSinglePass(P) ? star_sp_smem<P>() : star_t_smem<P>());
     PMG_DEGREES(CASE)
 #undef CASE
     default: return 0;
@@ -464,6 +634,8 @@ cudaError_t hot_set_smem_attr(int bytes) {
   {                                                                                                    \
     cudaError_t a = cudaFuncSetAttribute(k_elem_apply_t<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     cudaError_t b = cudaFuncSetAttribute(k_star_t<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);       \
+    if (b == cudaSuccess && kStarSinglePass(P))                                                        \
+      b = cudaFuncSetAttribute(k_star_sp<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (a != cudaSuccess) e = a;                                                                       \
     if (b != cudaSuccess) e = b;                                                                       \
   }

@@ -19,9 +19,15 @@ cudaError_t launch_star(const LevelGeom& g, int c1, int c2, int c3, int n1c, int
 size_t hot_smem(int p, int which);   // which: 0 element, 1 star
 cudaError_t hot_set_smem_attr(int bytes);
 
-__global__ void k_pcg_coop_p2(LevelGeom g, const double* b, double* x, double* r, double* z, double* pv, double* q,
-                              const double* dinv, const double* etab, double lam, double* Y, double* part,
-                              PcgState* st, double rtol, int maxit);
+// p = 2 coarse operator tables (coarse_cg.cu): assembled 1-D lumped masses b_d[2k_d+1], assembled
+// 1-D stiffness 5-point rows K_d[(2k_d+1) x 5] (offsets -2..2), per element c_e[6] and 1/D_e
+struct CoarseTabs {
+  const double *b1, *b2, *b3, *K1, *K2, *K3, *ce;
+};
+
+__global__ void k_pcg_coop_p2(LevelGeom g, CoarseTabs ct, const double* b, double* x, double* r, double* z,
+                              double* pv, double* q, const double* dinv, double lam, double* part, PcgState* st,
+                              double rtol, int maxit);
 
 size_t elem_apply_smem(int p, int ET);
 size_t star_smem(int p, bool s_in_smem);

@@ -73,6 +73,12 @@ struct pmg_ctx {
   bool ref_kernels = false;  // PMG_REFERENCE_KERNELS=1: runtime-p v1 kernels (A/B checks only)
   bool use_coop = false;     // coarse CG as one persistent cooperative kernel (p0 = 2)
   int coop_nb = 0;
+  double* ctab[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // CoarseTabs storage
+  double* cV = nullptr;      // (unused)
+  cudaGraphExec_t cycle_exec = nullptr;   // captured solve cycle (V-cycle + residual + norm^2)
+  long long launches_per_cycle = 0;
+  double* hres = nullptr;    // pinned host scalar
+  bool no_graph = false;     // PMG_NO_GRAPH=1
   // event timing (pmg_timing_enable)
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -158,10 +164,13 @@ pmg_status smooth_dev(pmg_ctx* c, int l, const double* r, double* u) {
 
 int zs_of(int pc) { int qc = pc + 1; return 3 * qc * qc + 3 * qc + 1; }
 
+// per-record transfer kernels do O(p^3) work on O(p^2) data: size the block to the face
+int transfer_threads(int pf) { return pf <= 8 ? 64 : (pf <= 16 ? 128 : 256); }
+
 pmg_status restrict_dev(pmg_ctx* c, int l, const double* rf, double* fc) {
   const DevLevel& F = c->D[l];
   const DevLevel& C = c->D[l - 1];
-  k_restrict_local<<<(unsigned)F.g.nrec, kThreads, transfer_smem(F.g.p, C.g.p), c->st>>>(F.g, C.g.p, F.Jint, rf, c->Z);
+  k_restrict_local<<<(unsigned)F.g.nrec, transfer_threads(F.g.p), transfer_smem(F.g.p, C.g.p), c->st>>>(F.g, C.g.p, F.Jint, rf, c->Z);
   LAUNCH_CHECK(c);
   k_restrict_gather<<<grid_for(C.g.nskel), kThreads, 0, c->st>>>(C.g, c->Z, fc);
   LAUNCH_CHECK(c);
@@ -171,7 +180,7 @@ pmg_status restrict_dev(pmg_ctx* c, int l, const double* rf, double* fc) {
 pmg_status prolong_dev(pmg_ctx* c, int l, const double* uc, double* uf) {
   const DevLevel& F = c->D[l];
   const DevLevel& C = c->D[l - 1];
-  k_prolong<<<(unsigned)F.g.nrec, kThreads, transfer_smem(F.g.p, C.g.p), c->st>>>(F.g, C.g, F.Jint, uc, uf);
+  k_prolong<<<(unsigned)F.g.nrec, transfer_threads(F.g.p), transfer_smem(F.g.p, C.g.p), c->st>>>(F.g, C.g, F.Jint, uc, uf);
   LAUNCH_CHECK(c);
   return PMG_OK;
 }
@@ -204,20 +213,30 @@ pmg_status norm_host(pmg_ctx* c, const double* x, long long n, double* out) {
 // polls the done flag every opt.coarse_check iterations.  Stops exactly at the first iteration
 // with ||r|| <= rtol ||b|| (or at coarse_maxit), like the oracle.
 pmg_status pcg_dev(pmg_ctx* c, const double* b, double* x) {
+  TimedRegion tr(c, 2, true);
   const DevLevel& D = c->D[0];
   const long long n = D.g.nskel;
   if (c->use_coop) {   // one launch, no host synchronisation; statistics read at the end of solve
     LevelGeom g0 = D.g;
     double lam = c->lam, rtol = c->opt.coarse_rtol;
     int maxit = c->opt.coarse_maxit;
-    double* Y = c->Y;
     double* part = c->part;
     PcgState* st = c->pcg;
     const double* dinv = c->dinv;
-    const double* etab = D.etab;
-    void* args[] = {&g0, (void*)&b, &x, &c->cr, &c->cz, &c->cp, &c->cq, (void*)&dinv, (void*)&etab, &lam, &Y, &part,
+    CoarseTabs ct{c->ctab[0], c->ctab[1], c->ctab[2], c->ctab[3], c->ctab[4], c->ctab[5], c->ctab[6]};
+    void* args[] = {&g0, &ct, (void*)&b, &x, &c->cr, &c->cz, &c->cp, &c->cq, (void*)&dinv, &lam, &part,
                     &st, &rtol, &maxit};
-    CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_pcg_coop_p2, dim3(c->coop_nb), dim3(kThreads), args, 0, c->st));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c->coop_nb);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = c->st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;   // capturable cooperative launch
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_CHECK(cudaLaunchKernelExC(&cfg, (const void*)k_pcg_coop_p2, args));
     c->launches++;
     return PMG_OK;
   }
@@ -342,10 +361,38 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
   rn = r0;
   int cycles = 0;
   if (rep && rep->history && rep->history_cap > 0) rep->history[0] = r0;
+  // One cycle = V-cycle + residual + ||r||^2 into dres.  When the whole cycle is free of host
+  // synchronisation (cooperative coarse CG) it is captured once into a CUDA graph and replayed:
+  // ~60 kernel launches per cycle become one graph launch.
+  const bool graph_ok = c->use_coop && c->st != nullptr && !c->timing && !c->no_graph;
+  if (graph_ok && !c->cycle_exec) {
+    long long l0 = c->launches;
+    cudaGraph_t gr = nullptr;
+    CUDA_CHECK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+    pmg_status cs = vcycle_dev(c, D.u, D.f, true);
+    if (!cs) cs = residual_dev(c, c->L, D.u, D.f, D.r);
+    if (!cs) cs = dot_dev(c, D.r, D.r, D.g.nskel, c->dres);
+    cudaError_t ce = cudaStreamEndCapture(c->st, &gr);
+    if (cs) { if (gr) cudaGraphDestroy(gr); return cs; }
+    if (ce != cudaSuccess) return fail(PMG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    ce = cudaGraphInstantiate(&c->cycle_exec, gr, 0);
+    cudaGraphDestroy(gr);
+    if (ce != cudaSuccess) { c->cycle_exec = nullptr; return fail(PMG_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce)); }
+    c->launches_per_cycle = c->launches - l0;
+    c->launches = l0;
+  }
   while (rn > rtol * r0 && cycles < max_cycles) {
-    if ((s = vcycle_dev(c, D.u, D.f, true))) return s;
-    if ((s = residual_dev(c, c->L, D.u, D.f, D.r))) return s;
-    if ((s = norm_host(c, D.r, D.g.nskel, &rn))) return s;
+    if (graph_ok) {
+      CUDA_CHECK(cudaGraphLaunch(c->cycle_exec, c->st));
+      c->launches += c->launches_per_cycle;
+      CUDA_CHECK(cudaMemcpyAsync(c->hres, c->dres, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      CUDA_CHECK(cudaStreamSynchronize(c->st));
+      rn = std::sqrt(*c->hres);
+    } else {
+      if ((s = vcycle_dev(c, D.u, D.f, true))) return s;
+      if ((s = residual_dev(c, c->L, D.u, D.f, D.r))) return s;
+      if ((s = norm_host(c, D.r, D.g.nskel, &rn))) return s;
+    }
     ++cycles;
     if (rep && rep->history && cycles < rep->history_cap) rep->history[cycles] = rn;
   }
@@ -379,6 +426,10 @@ void free_ctx(pmg_ctx* c) {
   cudaFree(c->cx); cudaFree(c->cr); cudaFree(c->cz); cudaFree(c->cp); cudaFree(c->cq); cudaFree(c->dinv);
   for (int d = 0; d < 3; ++d) cudaFree(c->bm[d]);
   cudaFree(c->Fdev); cudaFree(c->Udev);
+  for (int i = 0; i < 7; ++i) cudaFree(c->ctab[i]);
+  cudaFree(c->cV);
+  if (c->cycle_exec) cudaGraphExecDestroy(c->cycle_exec);
+  if (c->hres) cudaFreeHost(c->hres);
   ev_reset(c);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete c;
@@ -555,10 +606,22 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_coop_p2, kThreads, 0);
     const char* env = std::getenv("PMG_COARSE_MULTIKERNEL");
     if (coop && per_sm > 0 && c->D[0].g.p == 2 && !(env && env[0] == '1')) {
-      long long want = (c->D[0].g.nskel + 4 * kThreads - 1) / (4 * kThreads);
+      long long want = (c->D[0].g.nskel + kThreads - 1) / kThreads;
       long long cap = std::min<long long>((long long)per_sm * nsm, 1344);
       c->coop_nb = (int)std::max<long long>(1, std::min(want, cap));
       c->use_coop = true;
+      std::vector<double> tabs[7];
+      coarse_tables(c->H[0], lambda, tabs);
+      for (int i = 0; i < 7; ++i)
+        if ((s = upload(&c->ctab[i], tabs[i]))) { free_ctx(c); return s; }
+      const char* ng = std::getenv("PMG_NO_GRAPH");
+      c->no_graph = ng && ng[0] == '1';
+      if (cudaMallocHost(reinterpret_cast<void**>(&c->hres), sizeof(double)) != cudaSuccess) {
+        free_ctx(c);
+        return fail(PMG_ENOMEM, "cudaMallocHost failed");
+      }
+      const char* nbenv = std::getenv("PMG_COOP_BLOCKS");   // tuning experiments only
+      if (nbenv && std::atoi(nbenv) > 0) c->coop_nb = (int)std::min<long long>(std::atoi(nbenv), cap);
     }
   }
   cudaError_t es = cudaDeviceSynchronize();
@@ -710,13 +773,17 @@ pmg_status pmg_timing_enable(pmg_ctx* c, int enable) {
 
 pmg_status pmg_timing_read(pmg_ctx* c, int kind, double* total_ms, long long* count) {
   if (!c) return fail(PMG_EINVAL, "ctx is NULL");
-  if (kind < 0 || kind > 3 || !total_ms || !count) return fail(PMG_EINVAL, "bad kind or NULL output");
+  if (kind < 0 || kind > 4 || !total_ms || !count) return fail(PMG_EINVAL, "bad kind or NULL output");
   CUDA_CHECK(cudaStreamSynchronize(c->st));
   double tot = 0.0;
   long long n = 0;
   for (auto& mk : c->ev_marks) {
-    if (mk.base != (kind & 1)) continue;
-    if (kind < 2 && !mk.top) continue;
+    if (kind == 4) {
+      if (mk.base != 2) continue;
+    } else {
+      if (mk.base != (kind & 1)) continue;
+      if (kind < 2 && !mk.top) continue;
+    }
     float ms = 0.f;
     CUDA_CHECK(cudaEventElapsedTime(&ms, mk.a, mk.b));
     tot += ms;

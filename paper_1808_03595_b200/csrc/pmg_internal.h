@@ -66,6 +66,8 @@ std::string build_level(HostLevel& L, int p, const int k[3], const double* const
 std::string build_interp(HostLevel& fine, int p_coarse);
 // diag(H_hat) for the given level in skeleton record layout (free entries only, others 0).
 std::string coarse_diag(const HostLevel& L, double lambda, std::vector<double>& diag);
+// p = 2 coarse CG operator tables (coarse_cg.cu)
+std::string coarse_tables(const HostLevel& L, double lambda, std::vector<double> tabs[7]);
 // 1-D GLL nodes and weights (p >= 1)
 void gll(int p, std::vector<double>& x, std::vector<double>& w);
 

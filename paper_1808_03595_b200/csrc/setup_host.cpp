@@ -313,6 +313,47 @@ static long long host_skel_index(const LevelGeom& g, int g1, int g2, int g3) {
   return rec * g.RS + off;
 }
 
+// p = 2 coarse operator tables (see coarse_cg.cu): tabs[0..2] = assembled 1-D lumped masses b_d,
+// tabs[3..5] = assembled 1-D stiffness rows K_d[i][o + 2], o = -2..2, tabs[6] = per element
+// [c_e[0..5], 1 / D_e] with c_e[2d + s] = a_{d,s} P_b P_a and D_e = lambda + L1 + L2 + L3.
+std::string coarse_tables(const HostLevel& L, double lambda, std::vector<double> tabs[7]) {
+  const LevelGeom& g = L.g;
+  if (g.p != 2) return "coarse tables need p = 2";
+  const int p = 2, q = 3;
+  const int k[3] = {g.k1, g.k2, g.k3};
+  size_t base = 0;
+  for (int d = 0; d < 3; ++d) {
+    const int n = 2 * k[d] + 1;
+    tabs[d].assign(n, 0.0);
+    tabs[3 + d].assign((size_t)n * 5, 0.0);
+    for (int e = 0; e < k[d]; ++e) {
+      const double* T = &L.etab[(base + e) * g.ET];
+      for (int t = 0; t <= p; ++t) {
+        tabs[d][2 * e + t] += T[et_M(p) + t];
+        for (int s = 0; s <= p; ++s) tabs[3 + d][(size_t)(2 * e + t) * 5 + (s - t + 2)] += T[et_K(p) + t * q + s];
+      }
+    }
+    base += k[d];
+  }
+  tabs[6].assign((size_t)g.nelem * 7, 0.0);
+  for (int e3 = 0; e3 < g.k3; ++e3)
+    for (int e2 = 0; e2 < g.k2; ++e2)
+      for (int e1 = 0; e1 < g.k1; ++e1) {
+        const double* T[3] = {&L.etab[(size_t)e1 * g.ET], &L.etab[(size_t)(g.k1 + e2) * g.ET],
+                              &L.etab[(size_t)(g.k1 + g.k2 + e3) * g.ET]};
+        const long long el = e1 + (long long)g.k1 * (e2 + (long long)g.k2 * e3);
+        double* c = &tabs[6][(size_t)el * 7];
+        for (int d = 0; d < 3; ++d) {
+          const int da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2;
+          const double PbPa = T[db][et_P(p)] * T[da][et_P(p)];
+          c[2 * d] = T[d][et_a0(p)] * PbPa;
+          c[2 * d + 1] = T[d][et_a1(p)] * PbPa;
+        }
+        c[6] = 1.0 / (lambda + T[0][et_lam(p)] + T[1][et_lam(p)] + T[2][et_lam(p)]);
+      }
+  return "";
+}
+
 std::string coarse_diag(const HostLevel& L, double lambda, std::vector<double>& diag) {
   const LevelGeom& g = L.g;
   int p = g.p, m = g.m, q = p + 1;

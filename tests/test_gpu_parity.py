@@ -217,3 +217,30 @@ def test_invalid_arguments_fail_loudly():
     P = pair("k232_p5_lam0")
     with pytest.raises(pmg.PmgError):
         P.gpu.restrict(0, P.gpu.new_skel(0), P.gpu.new_skel(0))   # no level below 0
+
+
+@pytest.mark.parametrize("name", ["k333_p8_lam0", "k422_p3_lam0.5", "k332_p2_lam0"])
+def test_coarse_cg_paths_agree(name, monkeypatch):
+    """The persistent cooperative coarse CG (stencil + rank-one element corrections) and the
+    multi-kernel CG (element operator) are two evaluations of the same Jacobi-PCG iteration."""
+    import paper_1808_03595_b200 as pmg
+    P = pair(name)
+    case = P.case
+    L = P.gpu.nlevels - 1
+    f = P.rand_skel(L)
+    outs = []
+    for env in ("0", "1"):
+        monkeypatch.setenv("PMG_COARSE_MULTIKERNEL", env)
+        s = pmg.Solver(case.k, case.widths, case.p, case.lam, coarse_rtol=1e-13)
+        u = s.new_skel(L)
+        fs = torch.from_numpy(np.ascontiguousarray(f)).cuda()
+        fh = s.new_skel(L)
+        s.skel_from_grid(L, fs, fh)
+        s.vcycle(u, fh)
+        g = s.new_grid(L)
+        s.skel_to_grid(L, u, g)
+        torch.cuda.synchronize()
+        outs.append(g.cpu().numpy())
+        s.close()
+    assert rel(outs[0], outs[1]) < 1e-11
+    assert rel(outs[0], P.orc.vcycle(np.zeros_like(f), f)) < OP_TOL
