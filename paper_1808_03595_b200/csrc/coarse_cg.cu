@@ -40,19 +40,29 @@ __device__ __forceinline__ double block_reduce(double v, double* red) {
   return s;
 }
 
-// total of the per-block partials, identical in every block (fixed order: lane-strided sums, then a
-// shuffle tree), broadcast to all threads of the block
-__device__ __forceinline__ double grid_total(const double* part, int nb, double* bcast) {
-  if (threadIdx.x < 32) {
-    double s = 0.0;
-    for (int i = threadIdx.x; i < nb; i += 32) s += __ldcg(&part[i]);
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) *bcast = s;
+// totals of two per-block partial arrays, identical in every block: the whole block loads the
+// partials (one L2 round trip: every thread at most ceil(nb / blockDim) loads), warp xor-trees, then
+// the warp sums in fixed order -- the same partition and order in every block, so every block
+// gets bitwise the same totals (deterministic, no extra grid barrier).  `red` holds 2 x 32 doubles.
+__device__ __forceinline__ void grid_totals(const double* pa, const double* pb, int nb, double* red,
+                                            double& ta, double& tb) {
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    a += __ldcg(&pa[i]);
+    if (pb) b += __ldcg(&pb[i]);
   }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
   __syncthreads();
-  double t = *bcast;
+  if (lane == 0) { red[w] = a; red[32 + w] = b; }
   __syncthreads();
-  return t;
+  double sa = 0.0, sb = 0.0;
+  for (int i = 0; i < nw; ++i) { sa += red[i]; sb += red[32 + i]; }
+  ta = sa;
+  tb = sb;
 }
 
 // Skeleton-vector index of a point, or -1 outside the box (no memory access here)
@@ -188,8 +198,7 @@ __global__ void __launch_bounds__(256) k_pcg_coop_p2(LevelGeom g, CoarseTabs ct,
                                                     const double* __restrict__ dinv, double lam,
                                                     double* __restrict__ part, PcgState* st, double rtol, int maxit) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double red[32];
-  __shared__ double bc;
+  __shared__ double red[64];
   const int nb = gridDim.x;
   double* part_a = part;           // p.q
   double* part_b = part + nb;      // r.r (b.b at init)
@@ -207,8 +216,9 @@ __global__ void __launch_bounds__(256) k_pcg_coop_p2(LevelGeom g, CoarseTabs ct,
   s2 = block_reduce(s2, red);
   if (threadIdx.x == 0) part_b[blockIdx.x] = s2;
   grid.sync();
-  double rz = grid_total(part_c, nb, &bc);
-  const double bb = grid_total(part_b, nb, &bc);
+  double rz, bb, dummy;
+  grid_totals(part_c, part_b, nb, red, rz, bb);
+  (void)dummy;
   double beta = 0.0;
   int its = 0, breakdown = 0;
   bool done = (bb == 0.0);
@@ -225,7 +235,8 @@ __global__ void __launch_bounds__(256) k_pcg_coop_p2(LevelGeom g, CoarseTabs ct,
     spq = block_reduce(spq, red);
     if (threadIdx.x == 0) part_a[blockIdx.x] = spq;
     grid.sync();
-    const double pq = grid_total(part_a, nb, &bc);
+    double pq, unused;
+    grid_totals(part_a, nullptr, nb, red, pq, unused);
     if (!(pq > 0.0)) { breakdown = 1; break; }
     const double alpha = rz / pq;
     // phase 2: x += alpha p ; r -= alpha q ; z = D^-1 r ; partials r.r, r.z
@@ -244,8 +255,8 @@ __global__ void __launch_bounds__(256) k_pcg_coop_p2(LevelGeom g, CoarseTabs ct,
     srz = block_reduce(srz, red);
     if (threadIdx.x == 0) part_c[blockIdx.x] = srz;
     grid.sync();
-    const double rr = grid_total(part_b, nb, &bc);
-    const double rzn = grid_total(part_c, nb, &bc);
+    double rr, rzn;
+    grid_totals(part_b, part_c, nb, red, rr, rzn);
     ++its;
     if (sqrt(rr) <= rtol * sqrt(bb) || its >= maxit) break;
     beta = rzn / rz;

@@ -10,6 +10,9 @@
 //   - block size chosen per degree so small-p elements do not leave most threads idle.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "layout.cuh"
 
@@ -574,15 +577,189 @@ __global__ void __launch_bounds__(StarSpCfg<P>::NT) k_star_sp(LevelGeom g, int c
 }
 
 // ------------------------------------------------------------------------------------------
+// star smoother, P <= 8: the twelve n x n transforms per star (3 planes x 2 forward, 2 back) run
+// on the FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64; tcgen05 has no f64 kind).  n_S is padded to
+// NP = 8 or 16 with zero rows/columns (exact).  One DMMA = 256 FMA per warp from two shared-memory
+// operand loads per lane, instead of 32 FMA per two loads -- the transforms stop competing with the
+// core for load/issue slots.  Leading dimension LD = NP + 4 keeps the fragment loads at the
+// 2-wavefront minimum.  The core is the single-pass DFMA core of k_star_sp.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// C = A * B for NP x NP row-major shared-memory matrices (leading dimension LD); one warp, tile (mi, ni)
+template <int NP, int LD>
+__device__ __forceinline__ void dmma_tile(const double* A, const double* B, double* Cm, int mi, int ni, int lane) {
+  const int r = lane >> 2, q = lane & 3;
+  double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < NP / 4; ++kk) dmma884(c0, c1, A[(8 * mi + r) * LD + 4 * kk + q], B[(4 * kk + q) * LD + 8 * ni + r]);
+  Cm[(8 * mi + r) * LD + 8 * ni + 2 * q] = c0;
+  Cm[(8 * mi + r) * LD + 8 * ni + 2 * q + 1] = c1;
+}
+
+template <int P> struct StarDmCfg {
+  static constexpr int N = 2 * P - 1, NN = N * N, C = P - 1;
+  static constexpr int NP = (N <= 8) ? 8 : 16, LD = NP + 4, MS = NP * LD, TPP = (NP / 8) * (NP / 8);
+  static constexpr int NW = 4, NT = 128;
+  static constexpr int GS = NP, GPW = 32 / GS, NG = NW * GPW, A3IT = (N + NG - 1) / NG;
+  static constexpr int oFT = 0, oX = 3 * MS, oG = 6 * MS, oS = 9 * MS, oSt = 12 * MS, oP3 = 15 * MS,
+                       oVec = oP3 + NG * NN, total = oVec + 9 * N;
+};
+
+template <int P>
+size_t star_dm_smem() { return sizeof(double) * StarDmCfg<P>::total; }
+
+template <int P>
+__global__ void __launch_bounds__(StarDmCfg<P>::NT) k_star_dm(LevelGeom g, int c1, int c2, int c3, int n1c, int n2c,
+                                                             const double* __restrict__ r, double* __restrict__ u,
+                                                             const double* __restrict__ stab,
+                                                             const double* __restrict__ stabT, double lam) {
+  using C = StarDmCfg<P>;
+  constexpr int N = C::N, NN = C::NN, c = C::C, NT = C::NT, NP = C::NP, LD = C::LD, MS = C::MS;
+  constexpr int GS = C::GS, GPW = C::GPW, NG = C::NG;
+  extern __shared__ double sm[];
+  const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
+  const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
+  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 == 0 || v3 == g.k3)) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, ST = g.ST;
+  const size_t row[3] = {(size_t)v1, (size_t)(g.V1 + v2), (size_t)(g.V1 + g.V2 + v3)};
+  double* FT = sm + C::oFT;
+  double* X = sm + C::oX;
+  double* Gs = sm + C::oG;
+  double* Ssm = sm + C::oS;
+  double* Stm = sm + C::oSt;
+  double* P3 = sm + C::oP3;
+  double* vec = sm + C::oVec;
+  const int o1 = (v1 - 1) * P + 1, o2 = (v2 - 1) * P + 1, o3 = (v3 - 1) * P + 1;
+  // padded operands: S, S^T, the three faces (/ multiplicity), zeroed G
+  for (int i = tid; i < 3 * NP * NP; i += NT) {
+    const int d = i / (NP * NP), rr = i - d * NP * NP, A = rr / NP, B = rr - A * NP;
+    const bool in = A < N && B < N;
+    Ssm[d * MS + A * LD + B] = in ? __ldg(&stab[row[d] * ST + A * N + B]) : 0.0;
+    Stm[d * MS + A * LD + B] = in ? __ldg(&stabT[row[d] * NN + A * N + B]) : 0.0;
+    double val = 0.0;
+    if (in) {
+      int j1, j2, j3;
+      if (d == 0) { j1 = c; j2 = B; j3 = A; } else if (d == 1) { j2 = c; j1 = B; j3 = A; } else { j3 = c; j1 = B; j2 = A; }
+      const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
+      val = inside(g, g1, g2, g3) ? __ldg(&r[skel_index(g, g1, g2, g3)]) : 0.0;
+      val *= 1.0 / (double)(1 + (A == c) + (B == c));   // inverse multiplicity
+    }
+    FT[d * MS + A * LD + B] = val;
+    Gs[d * MS + A * LD + B] = 0.0;
+  }
+  for (int i = tid; i < 9 * N; i += NT) { const int d = i / (3 * N); vec[i] = __ldg(&stab[row[d] * ST + NN + i - d * 3 * N]); }
+  __syncthreads();
+  // forward: X_d = F_d S_a ; T_d = S_b^T X_d  (tile jobs: 3 planes x TPP tiles over the warps)
+  for (int job = warp; job < 3 * C::TPP; job += C::NW) {
+    const int d = job / C::TPP, t = job - d * C::TPP, mi = t / (NP / 8), ni = t - mi * (NP / 8);
+    dmma_tile<NP, LD>(FT + d * MS, Ssm + (d == 0 ? 1 : 0) * MS, X + d * MS, mi, ni, lane);
+  }
+  __syncthreads();
+  for (int job = warp; job < 3 * C::TPP; job += C::NW) {
+    const int d = job / C::TPP, t = job - d * C::TPP, mi = t / (NP / 8), ni = t - mi * (NP / 8);
+    dmma_tile<NP, LD>(Stm + (d == 2 ? 1 : 2) * MS, X + d * MS, FT + d * MS, mi, ni, lane);
+  }
+  __syncthreads();
+  // single-pass core on T (FT), results G1 -> Gs[0], G2 -> Gs[1], G3 -> Gs[2]
+  {
+    const double *L1 = vec, *s1 = vec + N, *L2 = vec + 3 * N, *s2 = vec + 4 * N, *L3 = vec + 6 * N, *s3 = vec + 7 * N;
+    const double *T1 = FT, *T2 = FT + MS, *T3 = FT + 2 * MS;
+    const int grp = warp * GPW + lane / GS, a1 = lane % GS;
+    const bool va = a1 < N;
+    const int a1c = va ? a1 : 0;
+    const double s1a = va ? s1[a1c] : 0.0, L1a = L1[a1c];
+    double g3[N];
+#pragma unroll
+    for (int a2 = 0; a2 < N; ++a2) g3[a2] = 0.0;
+    for (int k = 0; k < C::A3IT; ++k) {
+      const int a3 = grp + k * NG;
+      const bool act = a3 < N;
+      const int a3c = act ? a3 : 0;
+      const double on = (act && va) ? 1.0 : 0.0;
+      const double t2 = on * T2[a3c * LD + a1c], s3v = on * s3[a3c], base = lam + L1a + L3[a3c];
+      const double s1v = on * s1a;
+      double g2 = 0.0;
+#pragma unroll
+      for (int a2 = 0; a2 < N; ++a2) {
+        double E = s1v * T1[a3c * LD + a2];
+        E = fma(s2[a2], t2, E);
+        E = fma(s3v, T3[a2 * LD + a1c], E);
+        const double V = E * rcp_nr(base + L2[a2]);
+        g2 = fma(s2[a2], V, g2);
+        g3[a2] = fma(s3v, V, g3[a2]);
+        double v = s1v * V;
+#pragma unroll
+        for (int o = GS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (act && a1 == 0) Gs[a3 * LD + a2] = v;
+      }
+      if (act && va) Gs[MS + a3 * LD + a1] = g2;
+    }
+    if (va) {
+#pragma unroll
+      for (int a2 = 0; a2 < N; ++a2) P3[grp * NN + a2 * N + a1] = g3[a2];
+    }
+    __syncthreads();
+    for (int i = tid; i < NN; i += NT) {
+      const int a2 = i / N, a1_ = i - a2 * N;
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < NG; ++q) s += P3[q * NN + i];
+      Gs[2 * MS + a2 * LD + a1_] = s;
+    }
+  }
+  __syncthreads();
+  // back: X_d = G_d S_a^T ; U_d = S_b X_d (into G)
+  for (int job = warp; job < 3 * C::TPP; job += C::NW) {
+    const int d = job / C::TPP, t = job - d * C::TPP, mi = t / (NP / 8), ni = t - mi * (NP / 8);
+    dmma_tile<NP, LD>(Gs + d * MS, Stm + (d == 0 ? 1 : 0) * MS, X + d * MS, mi, ni, lane);
+  }
+  __syncthreads();
+  for (int job = warp; job < 3 * C::TPP; job += C::NW) {
+    const int d = job / C::TPP, t = job - d * C::TPP, mi = t / (NP / 8), ni = t - mi * (NP / 8);
+    dmma_tile<NP, LD>(Ssm + (d == 2 ? 1 : 2) * MS, X + d * MS, Gs + d * MS, mi, ni, lane);
+  }
+  __syncthreads();
+  const double *w1 = vec + 2 * N, *w2 = vec + 5 * N, *w3 = vec + 8 * N;
+  for (int i = tid; i < 3 * NN; i += NT) {
+    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
+    int j1, j2, j3;
+    if (d == 0) { j1 = c; j2 = B; j3 = A; }
+    else if (d == 1) { j2 = c; j1 = B; j3 = A; if (j1 == c) continue; }
+    else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
+    const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
+    if (!is_free(g, g1, g2, g3)) continue;
+    u[skel_index(g, g1, g2, g3)] += w1[j1] * w2[j2] * w3[j3] * Gs[d * MS + A * LD + B];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // dispatch
 // ------------------------------------------------------------------------------------------
 constexpr bool kStarSinglePass(int p) { return p <= 8; }
+
+// star kernel variant for p <= 8 (A/B experiments): 0 DMMA transforms (default), 1 DFMA transforms
+static int star_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("PMG_STAR_VARIANT");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v;
+}
 
 template <int P>
 void launch_star_p(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c, long long nb, const double* r,
                    double* u, const double* stab, const double* stabT, double lam, cudaStream_t st) {
   if constexpr (kStarSinglePass(P)) {
-    k_star_sp<P><<<(unsigned)nb, StarSpCfg<P>::NT, star_sp_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
+    if (star_variant() == 0)
+      k_star_dm<P><<<(unsigned)nb, StarDmCfg<P>::NT, star_dm_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
+    else
+      k_star_sp<P><<<(unsigned)nb, StarSpCfg<P>::NT, star_sp_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
   } else {
     k_star_t<P><<<(unsigned)nb, StarCfg<P>::NT, star_t_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
   }
@@ -621,7 +798,7 @@ cudaError_t launch_star(const LevelGeom& g, int c1, int c2, int c3, int n1c, int
 size_t hot_smem(int p, int which) {
   switch (p) {
 #define CASE(P) \
-  case P: return which == 0 ? elem_t_smem<P>() : (kStarSinglePass(P) ? star_sp_smem<P>() : star_t_smem<P>());
+  case P: return which == 0 ? elem_t_smem<P>() : (kStarSinglePass(P) ? std::max(star_sp_smem<(P <= 8 ? P : 2)>(), star_dm_smem<(P <= 8 ? P : 2)>()) : star_t_smem<P>());
     PMG_DEGREES(CASE)
 #undef CASE
     default: return 0;
@@ -636,6 +813,8 @@ cudaError_t hot_set_smem_attr(int bytes) {
     cudaError_t b = cudaFuncSetAttribute(k_star_t<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);       \
     if (b == cudaSuccess && kStarSinglePass(P))                                                        \
       b = cudaFuncSetAttribute(k_star_sp<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+    if (b == cudaSuccess && kStarSinglePass(P))                                                        \
+      b = cudaFuncSetAttribute(k_star_dm<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (a != cudaSuccess) e = a;                                                                       \
     if (b != cudaSuccess) e = b;                                                                       \
   }

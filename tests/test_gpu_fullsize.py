@@ -1,0 +1,225 @@
+"""Full-size checks at the BASELINE.json configurations, in the launch configuration bench.py
+times (the same Solver / pmg_solve path).  The oracle cannot hold these meshes, so outputs are
+checked (a) one by one at sampled points, with the oracle's dense operators built on the small
+sub-mesh that determines each sampled value (element operators depend only on the element widths;
+the star inverse of an interior vertex is the inverse of the condensed operator of its 2x2x2 block
+with a Dirichlet outer boundary, tests/test_oracle_star.py), and (b) through properties that hold at
+any size (convergence to the 1e-10 drop, symmetry, the manufactured solution)."""
+import math
+
+import numpy as np
+import pytest
+
+import pmg_inputs as pi
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _solver(case, **kw):
+    import paper_1808_03595_b200 as pmg
+    return pmg.Solver(case.k, case.widths, case.p, case.lam, **kw)
+
+
+def _grid_of(s, level, skel):
+    g = s.new_grid(level)
+    s.skel_to_grid(level, skel, g)
+    torch.cuda.synchronize()
+    return g.cpu().numpy()
+
+
+class GridView:
+    """Index helper on the global GLL grid of one level (no oracle arithmetic)."""
+
+    def __init__(self, k, p):
+        self.k, self.p = k, p
+        self.N = tuple(kd * p + 1 for kd in k)
+
+    def flat(self, i1, i2, i3):
+        return i1 + self.N[0] * (i2 + self.N[1] * i3)
+
+
+def _submesh(case, lo, n):
+    """Mesh of n[0] x n[1] x n[2] elements starting at element lo, same widths, Dirichlet outside."""
+    from oracle import mesh
+    w = [case.widths[d][lo[d]:lo[d] + n[d]] for d in range(3)]
+    return mesh.Mesh(n, w, case.p)
+
+
+def _sampled_residual(case, ug, fg, rg, samples):
+    """r at sampled skeleton points = f - sum over the elements containing the point of H_hat_e u_e."""
+    from oracle import condensed
+    p, k = case.p, case.k
+    V = GridView(k, p)
+    errs = []
+    cache = {}
+    for (i1, i2, i3) in samples:
+        want = fg[V.flat(i1, i2, i3)]
+        for e3 in {max(0, (i3 - 1) // p), min(k[2] - 1, i3 // p)}:
+            for e2 in {max(0, (i2 - 1) // p), min(k[1] - 1, i2 // p)}:
+                for e1 in {max(0, (i1 - 1) // p), min(k[0] - 1, i1 // p)}:
+                    if not (e1 * p <= i1 <= (e1 + 1) * p and e2 * p <= i2 <= (e2 + 1) * p and e3 * p <= i3 <= (e3 + 1) * p):
+                        continue
+                    sub = _submesh(case, (e1, e2, e3), (1, 1, 1))
+                    key = tuple(sub.elem_h[0].tolist())
+                    if key not in cache:
+                        cache[key] = condensed.ElementBlocks(p, sub.elem_h[0], case.lam, sub.loc_B, sub.loc_I)
+                    blk = cache[key]
+                    t1, t2, t3 = sub.local_t
+                    gidx = V.flat(e1 * p + t1, e2 * p + t2, e3 * p + t3)[sub.loc_B]
+                    ue = ug[gidx]
+                    row = [j for j, (a, b, c) in enumerate(zip(t1[sub.loc_B], t2[sub.loc_B], t3[sub.loc_B]))
+                           if (e1 * p + a, e2 * p + b, e3 * p + c) == (i1, i2, i3)][0]
+                    want -= blk.Hhat[row] @ ue
+        errs.append(abs(rg[V.flat(i1, i2, i3)] - want) / max(abs(want), np.abs(fg).max() * 1e-3))
+    return max(errs)
+
+
+def _interior_points(case, rng, nsample):
+    p, k = case.p, case.k
+    pts = []
+    while len(pts) < nsample:
+        v = [int(rng.integers(1, kd)) for kd in k]
+        kind = len(pts) % 3
+        i = [vd * p for vd in v]
+        if kind >= 1:
+            i[0] += int(rng.integers(1, p))          # edge point (x1 edge)
+        if kind == 2:
+            i[1] += int(rng.integers(1, p))          # face point (x3 face)
+        pts.append(tuple(i))
+    return pts
+
+
+@pytest.mark.parametrize("cfg,p", [(2, None), (3, 2), (3, 4), (3, 8), (3, 12), (3, 16), (4, None)])
+def test_fullsize_residual_sampled(cfg, p):
+    """(p = 24, 32: the dense element Schur complement is too large for the oracle; symmetry and the
+    full-size solve cover those degrees.)"""
+    case = pi.config(cfg, p=p)
+    s = _solver(case)
+    L = s.nlevels - 1
+    rng = np.random.default_rng(cfg * 100 + (p or 0))
+    n = s.level_info(L)[1]
+    u = torch.from_numpy(rng.standard_normal(n)).cuda()
+    f = torch.from_numpy(rng.standard_normal(n)).cuda()
+    # normalise to free-skeleton vectors through the grid (zero on non-free entries)
+    ugr, fgr = _grid_of(s, L, u), _grid_of(s, L, f)
+    uu, ff = s.new_skel(L), s.new_skel(L)
+    s.skel_from_grid(L, torch.from_numpy(ugr).cuda(), uu)
+    s.skel_from_grid(L, torch.from_numpy(fgr).cuda(), ff)
+    r = s.new_skel(L)
+    s.residual(L, uu, ff, r)
+    rgr = _grid_of(s, L, r)
+    err = _sampled_residual(case, ugr, fgr, rgr, _interior_points(case, rng, 6))
+    assert err < 1e-11, err
+    # symmetry of the full-size operator
+    a, b = s.new_skel(L), s.new_skel(L)
+    s.residual(L, uu, None, a)
+    s.residual(L, ff, None, b)
+    x, y = float((a * ff).sum()), float((uu * b).sum())
+    assert abs(x - y) <= 1e-11 * max(abs(x), 1.0)
+    s.close()
+
+
+def _sampled_vertex_smoother(case, rg, dug, rng, nsample):
+    """Correction at an interior vertex = (H_hat_v^-1 R_v r)(v) (only its own star covers it, W = 1);
+    H_hat_v^-1 = inverse of the condensed operator of the 2x2x2 block (dense LU, oracle)."""
+    from oracle import condensed
+    p, k = case.p, case.k
+    V = GridView(k, p)
+    errs = []
+    for _ in range(nsample):
+        v = [int(rng.integers(1, kd)) for kd in k]
+        sub = _submesh(case, [vd - 1 for vd in v], (2, 2, 2))
+        op = condensed.CondensedOperator(sub, case.lam)
+        fs = np.nonzero(sub.free_skel)[0]
+        Hs = op.assembled_condensed()[fs][:, fs].toarray()
+        # map the submesh's free skeleton points to the global grid
+        n1, n2 = sub.N[0], sub.N[1]
+        j3, rem = np.divmod(fs, n1 * n2)
+        j2, j1 = np.divmod(rem, n1)
+        gidx = V.flat((v[0] - 1) * p + j1, (v[1] - 1) * p + j2, (v[2] - 1) * p + j3)
+        x = np.linalg.solve(Hs, rg[gidx])
+        centre = int(np.nonzero((j1 == p) & (j2 == p) & (j3 == p))[0][0])
+        want = x[centre]
+        got = dug[V.flat(v[0] * p, v[1] * p, v[2] * p)]
+        errs.append(abs(got - want) / np.abs(x).max())
+    return max(errs)
+
+
+@pytest.mark.parametrize("cfg,p", [(2, None), (3, 4), (3, 8), (3, 16), (4, None)])
+def test_fullsize_smoother_sampled(cfg, p):
+    case = pi.config(cfg, p=p)
+    s = _solver(case)
+    L = s.nlevels - 1
+    rng = np.random.default_rng(7 + cfg + (p or 0))
+    n = s.level_info(L)[1]
+    rgr = _grid_of(s, L, torch.from_numpy(rng.standard_normal(n)).cuda())
+    r = s.new_skel(L)
+    s.skel_from_grid(L, torch.from_numpy(rgr).cuda(), r)
+    du = s.new_skel(L)
+    s.smooth(L, r, du)
+    dug = _grid_of(s, L, du)
+    err = _sampled_vertex_smoother(case, rgr, dug, rng, 3)
+    assert err < 1e-11, err
+    s.close()
+
+
+@pytest.mark.parametrize("cfg,p,max_cycles", [(2, None, 4), (3, 2, 4), (3, 4, 6), (3, 8, 4), (3, 12, 5), (3, 16, 4),
+                                              (3, 24, 5), (3, 32, 4), (1, None, 6)])
+def test_fullsize_solve_converges(cfg, p, max_cycles):
+    """The bench path at full size: pmg_solve reaches the 1e-10 drop within a handful of cycles
+    (P:21); history strictly decreasing."""
+    case = pi.config(cfg, p=p)
+    s = _solver(case)
+    L = s.nlevels - 1
+    x = [s.grid_coords(L, d) for d in range(3)]
+    f = torch.from_numpy(case.f_nodal(x)).cuda()
+    F = s.new_grid()
+    s.weak_rhs(f, F)
+    u = s.new_grid()
+    rep = s.solve(F, u, 1e-10, max_cycles=30)
+    assert rep["converged"] and rep["cycles"] <= max_cycles, rep
+    h = rep["history"]
+    assert all(b < a for a, b in zip(h, h[1:]))
+    assert torch.isfinite(u).all()
+    s.close()
+
+
+def test_fullsize_config4_manufactured():
+    """Config 4: lambda = 100, f = sin x sin y sin z on the stretched 32^3 mesh, p = 16; exact solution
+    u = f / 103; the discrete solution is spectrally accurate."""
+    case = pi.config(4)
+    s = _solver(case)
+    L = s.nlevels - 1
+    x = [s.grid_coords(L, d) for d in range(3)]
+    fn = case.f_nodal(x)
+    F = s.new_grid()
+    s.weak_rhs(torch.from_numpy(fn).cuda(), F)
+    u = s.new_grid()
+    rep = s.solve(F, u, 1e-10, max_cycles=40)
+    assert rep["converged"], rep
+    err = np.abs(u.cpu().numpy() - fn / 103.0).max()
+    assert err < 1e-9, err
+    s.close()
+
+
+def test_fullsize_config2_matches_oracle_solve():
+    """The bench workload (config 2, 2.1 M unknowns) against a full oracle solve: same cycle count,
+    solution within 1e-9 relative."""
+    from oracle import condensed, mg
+    case = pi.config(2)
+    s = _solver(case)
+    L = s.nlevels - 1
+    x = [s.grid_coords(L, d) for d in range(3)]
+    f = case.f_nodal(x)
+    F = s.new_grid()
+    s.weak_rhs(torch.from_numpy(f).cuda(), F)
+    u = s.new_grid()
+    rep = s.solve(F, u, 1e-10)
+    H = mg.Hierarchy(case.k, case.widths, case.p, case.lam)
+    m = H.levels[-1].mesh
+    u_o, rep_o = H.solve(condensed.weak_rhs(m, case.f_nodal(m.coords)), 1e-10)
+    got = u.cpu().numpy()
+    assert rep["cycles"] == rep_o["cycles"]
+    assert np.linalg.norm(got - u_o) / np.linalg.norm(u_o) < 1e-9
+    s.close()
