@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(ElemCfg<P>::NT) k_elem_apply_t(LevelGeom g, co
     if (d == 0) { t1 = s * P; t3 = A; t2 = B; }
     else if (d == 1) { t2 = s * P; t3 = A; t1 = B; }
     else { t3 = s * P; t2 = A; t1 = B; }
-    Uc[i] = __ldg(&u[skel_index(g, e1 * P + t1, e2 * P + t2, e3 * P + t3)]);
+    Uc[i] = __ldg(&u[skel_index_t<P>(g,e1 * P + t1, e2 * P + t2, e3 * P + t3)]);
   }
   __syncthreads();
   // tangential directions of face f: a (fast) = x2 for d = 0 else x1; b (slow) = x3 for d < 2 else x2
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(StarCfg<P>::NT) k_star_t(LevelGeom g, int c1, 
     int j1, j2, j3;
     if (d == 0) { j1 = c; j2 = B; j3 = A; } else if (d == 1) { j2 = c; j1 = B; j3 = A; } else { j3 = c; j1 = B; j2 = A; }
     const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
-    const double val = inside(g, g1, g2, g3) ? __ldg(&r[skel_index(g, g1, g2, g3)]) : 0.0;
+    const double val = inside(g, g1, g2, g3) ? __ldg(&r[skel_index_t<P>(g,g1, g2, g3)]) : 0.0;
     FT[i] = val * (1.0 / (double)(1 + (A == c) + (B == c)));   // inverse multiplicity
   }
   __syncthreads();
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(StarCfg<P>::NT) k_star_t(LevelGeom g, int c1, 
     else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
     const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
     if (!is_free(g, g1, g2, g3)) continue;
-    const long long idx = skel_index(g, g1, g2, g3);
+    const long long idx = skel_index_t<P>(g,g1, g2, g3);
     u[idx] += w1[j1] * w2[j2] * w3[j3] * Gs[i];
   }
 }
@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(StarSpCfg<P>::NT) k_star_sp(LevelGeom g, int c
     int j1, j2, j3;
     if (d == 0) { j1 = c; j2 = B; j3 = A; } else if (d == 1) { j2 = c; j1 = B; j3 = A; } else { j3 = c; j1 = B; j2 = A; }
     const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
-    const double val = inside(g, g1, g2, g3) ? __ldg(&r[skel_index(g, g1, g2, g3)]) : 0.0;
+    const double val = inside(g, g1, g2, g3) ? __ldg(&r[skel_index_t<P>(g,g1, g2, g3)]) : 0.0;
     FT[i] = val * (1.0 / (double)(1 + (A == c) + (B == c)));   // inverse multiplicity
   }
   __syncthreads();
@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(StarSpCfg<P>::NT) k_star_sp(LevelGeom g, int c
     else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
     const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
     if (!is_free(g, g1, g2, g3)) continue;
-    u[skel_index(g, g1, g2, g3)] += w1[j1] * w2[j2] * w3[j3] * Gs[i];
+    u[skel_index_t<P>(g,g1, g2, g3)] += w1[j1] * w2[j2] * w3[j3] * Gs[i];
   }
 }
 
@@ -646,7 +646,7 @@ __global__ void __launch_bounds__(StarDmCfg<P>::NT) k_star_dm(LevelGeom g, int c
       int j1, j2, j3;
       if (d == 0) { j1 = c; j2 = B; j3 = A; } else if (d == 1) { j2 = c; j1 = B; j3 = A; } else { j3 = c; j1 = B; j2 = A; }
       const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
-      val = inside(g, g1, g2, g3) ? __ldg(&r[skel_index(g, g1, g2, g3)]) : 0.0;
+      val = inside(g, g1, g2, g3) ? __ldg(&r[skel_index_t<P>(g, g1, g2, g3)]) : 0.0;
       val *= 1.0 / (double)(1 + (A == c) + (B == c));   // inverse multiplicity
     }
     FT[d * MS + A * LD + B] = val;
@@ -684,6 +684,9 @@ __global__ void __launch_bounds__(StarDmCfg<P>::NT) k_star_dm(LevelGeom g, int c
       const double t2 = on * T2[a3c * LD + a1c], s3v = on * s3[a3c], base = lam + L1a + L3[a3c];
       const double s1v = on * s1a;
       double g2 = 0.0;
+      double v[GS];   // s1 V for every a2 of this (a1, a3); reduced over the group's lanes below
+#pragma unroll
+      for (int a2 = 0; a2 < GS; ++a2) v[a2] = 0.0;
 #pragma unroll
       for (int a2 = 0; a2 < N; ++a2) {
         double E = s1v * T1[a3c * LD + a2];
@@ -692,12 +695,24 @@ __global__ void __launch_bounds__(StarDmCfg<P>::NT) k_star_dm(LevelGeom g, int c
         const double V = E * rcp_nr(base + L2[a2]);
         g2 = fma(s2[a2], V, g2);
         g3[a2] = fma(s3v, V, g3[a2]);
-        double v = s1v * V;
-#pragma unroll
-        for (int o = GS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (act && a1 == 0) Gs[a3 * LD + a2] = v;
+        v[a2] = s1v * V;
       }
-      if (act && va) Gs[MS + a3 * LD + a1] = g2;
+      // butterfly reduce-scatter over the GS lanes: afterwards lane a1 holds G1[a3][a2 = a1]
+      // (GS - 1 shuffles per lane instead of log2(GS) per a2)
+#pragma unroll
+      for (int off = GS / 2; off >= 1; off >>= 1) {
+        const bool upper = (a1 & off) != 0;
+#pragma unroll
+        for (int j = 0; j < off; ++j) {
+          const double send = upper ? v[j] : v[j + off];
+          const double keep = upper ? v[j + off] : v[j];
+          v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      if (act && va) {
+        Gs[a3 * LD + a1] = v[0];               // G1[a3][a2 = a1]
+        Gs[MS + a3 * LD + a1] = g2;            // G2[a3][a1]
+      }
     }
     if (va) {
 #pragma unroll
@@ -733,7 +748,7 @@ __global__ void __launch_bounds__(StarDmCfg<P>::NT) k_star_dm(LevelGeom g, int c
     else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
     const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
     if (!is_free(g, g1, g2, g3)) continue;
-    u[skel_index(g, g1, g2, g3)] += w1[j1] * w2[j2] * w3[j3] * Gs[d * MS + A * LD + B];
+    u[skel_index_t<P>(g, g1, g2, g3)] += w1[j1] * w2[j2] * w3[j3] * Gs[d * MS + A * LD + B];
   }
 }
 

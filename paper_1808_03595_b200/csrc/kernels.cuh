@@ -28,6 +28,9 @@ struct CoarseTabs {
 __global__ void k_pcg_coop_p2(LevelGeom g, CoarseTabs ct, const double* b, double* x, double* r, double* z,
                               double* pv, double* q, const double* dinv, double lam, double* part, PcgState* st,
                               double rtol, int maxit);
+__global__ void k_pcg_cluster_p2(LevelGeom g, CoarseTabs ct, const double* b, double* xout, const double* dinv,
+                                 double lam, int chunk, int halo, unsigned long long inv, PcgState* st, double rtol,
+                                 int maxit);
 
 size_t elem_apply_smem(int p, int ET);
 size_t star_smem(int p, bool s_in_smem);

@@ -29,6 +29,27 @@ __device__ __forceinline__ long long skel_index(const LevelGeom& g, int g1, int 
   return rec * g.RS + off;
 }
 
+// skel_index with the degree known at compile time (divisions by p become multiply-shifts)
+template <int P>
+__device__ __forceinline__ long long skel_index_t(const LevelGeom& g, int g1, int g2, int g3) {
+  constexpr int m = P - 1;
+  const int r1 = g1 / P, t1 = g1 - r1 * P;
+  const int r2 = g2 / P, t2 = g2 - r2 * P;
+  const int r3 = g3 / P, t3 = g3 - r3 * P;
+  const long long rec = r1 + (long long)g.V1 * (r2 + (long long)g.V2 * r3);
+  int off;
+  if (t1 == 0) {
+    if (t2 == 0) off = (t3 == 0) ? off_vert(m) : off_edge(m, 2) + t3 - 1;
+    else if (t3 == 0) off = off_edge(m, 1) + t2 - 1;
+    else off = off_face(m, 0) + (t3 - 1) * m + (t2 - 1);
+  } else if (t2 == 0) {
+    off = (t3 == 0) ? off_edge(m, 0) + t1 - 1 : off_face(m, 1) + (t3 - 1) * m + (t1 - 1);
+  } else {
+    off = off_face(m, 2) + (t2 - 1) * m + (t1 - 1);
+  }
+  return rec * (3 * m * m + 3 * m + 1) + off;
+}
+
 __device__ __forceinline__ bool inside(const LevelGeom& g, int g1, int g2, int g3) {
   return g1 >= 0 && g2 >= 0 && g3 >= 0 && g1 <= g.k1 * g.p && g2 <= g.k2 * g.p && g3 <= g.k3 * g.p;
 }
