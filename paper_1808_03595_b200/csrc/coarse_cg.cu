@@ -190,7 +190,9 @@ __device__ __forceinline__ double apply_entry(const LevelGeom& g, const CoarseTa
       double s = 0.0;
 #pragma unroll
       for (int i = 0; i < 6; ++i) s = fma(cw[side][i], fv[6 * side + i], s);
-      q = fma(-cw[side][2 * d + side], s * cw[side][6], q);
+      // c_e[2d + side] without a runtime array index (keeps cw in registers)
+      const double cd = (d == 0) ? cw[side][side] : ((d == 1) ? cw[side][2 + side] : cw[side][4 + side]);
+      q = fma(-cd, s * cw[side][6], q);
     }
   }
   return q;

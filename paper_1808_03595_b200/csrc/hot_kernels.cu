@@ -27,6 +27,25 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return fma(r, e, r);
 }
 
+// FP64 tensor-core MMA (DMMA): D(8x8) += A(8x4, row) B(4x8, col); lane l holds A[l/4][l%4],
+// B[l%4][l/4] and D[l/4][2(l%4) + {0,1}]
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// C = A * B for NP x NP row-major shared-memory matrices (leading dimension LD); one warp, tile (mi, ni)
+template <int NP, int LD>
+__device__ __forceinline__ void dmma_tile(const double* A, const double* B, double* Cm, int mi, int ni, int lane) {
+  const int r = lane >> 2, q = lane & 3;
+  double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < NP / 4; ++kk) dmma884(c0, c1, A[(8 * mi + r) * LD + 4 * kk + q], B[(4 * kk + q) * LD + 8 * ni + r]);
+  Cm[(8 * mi + r) * LD + 8 * ni + 2 * q] = c0;
+  Cm[(8 * mi + r) * LD + 8 * ni + 2 * q + 1] = c1;
+}
+
 template <int P> struct ElemCfg {
   static constexpr int M = P - 1, Q = P + 1, MM = M * M, QQ = Q * Q;
   static constexpr int NT = (P <= 4) ? 64 : (P <= 10 ? 128 : 256);
@@ -253,6 +272,222 @@ __global__ void __launch_bounds__(ElemCfg<P>::NT) k_elem_apply_t(LevelGeom g, co
     }
     y = fma(M1[t1] * M2[t2], s, y);
     Ye[o] = y - corr;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// element operator for P <= 8 with the 24 face transforms per element on DMMA (m = p - 1 padded to
+// 8, exact), a shared 1/D table (one rcp per eigen-triple instead of three), and face-interior
+// outputs evaluated from the two closed faces they depend on (row / column line sums).
+// ------------------------------------------------------------------------------------------
+template <int P> struct ElemDmCfg {
+  static constexpr int M = P - 1, Q = P + 1, MM = M * M, QQ = Q * Q, MP = 8, LD = 12, MS = MP * LD;
+  static constexpr int NT = 128, NW = 4;
+  using E = ElemCfg<P>;
+  static constexpr int TB = E::TB;
+  static constexpr int oUc = 0, oTab = 6 * QQ, oPp = oTab + 3 * TB, oPtp = oPp + 3 * MS, oA = oPtp + 3 * MS,
+                       oT = oA + 6 * MS, oG = oT + 6 * MS, oInv = oG + 6 * MS, total = oInv + MM * M;
+};
+
+template <int P>
+size_t elem_dm_smem() { return sizeof(double) * ElemDmCfg<P>::total; }
+
+template <int P>
+__global__ void __launch_bounds__(128) k_elem_dm(LevelGeom g, const double* __restrict__ u,
+                                                 const double* __restrict__ etab, double lam,
+                                                 double* __restrict__ Y, const int* __restrict__ done) {
+  using C = ElemDmCfg<P>;
+  using EC = ElemCfg<P>;
+  constexpr int M = C::M, Q = C::Q, MM = C::MM, QQ = C::QQ, NT = C::NT, TB = C::TB, LD = C::LD, MS = C::MS, MP = C::MP;
+  if (done && *done) return;
+  extern __shared__ double sm[];
+  double* Uc = sm + C::oUc;
+  double* tb = sm + C::oTab;
+  double* Pp = sm + C::oPp;
+  double* Ptp = sm + C::oPtp;
+  double* Ab = sm + C::oA;     // padded face interiors, later the back-transform intermediate
+  double* T = sm + C::oT;
+  double* G = sm + C::oG;
+  double* invD = sm + C::oInv;
+  const long long e = blockIdx.x;
+  const int e1 = (int)(e % g.k1), e2 = (int)((e / g.k1) % g.k2), e3 = (int)(e / ((long long)g.k1 * g.k2));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ET = g.ET;
+  {
+    const double* src[3] = {etab + (size_t)e1 * ET, etab + (size_t)(g.k1 + e2) * ET, etab + (size_t)(g.k1 + g.k2 + e3) * ET};
+    for (int i = tid; i < 3 * TB; i += NT) {
+      const int d = i / TB, o = i - d * TB;
+      const double* s = src[d];
+      double v;
+      if (o < EC::tP) v = s[et_lam(P) + o];
+      else if (o < EC::tPt) v = s[et_P(P) + (o - EC::tP)];
+      else if (o < EC::ta0) { int r = o - EC::tPt, ia = r / M, b = r - ia * M; v = s[et_P(P) + b * M + ia]; }
+      else if (o < EC::ta1) v = s[et_a0(P) + (o - EC::ta0)];
+      else if (o < EC::tM) v = s[et_a1(P) + (o - EC::ta1)];
+      else if (o < EC::tK) v = s[et_M(P) + (o - EC::tM)];
+      else v = s[et_K(P) + (o - EC::tK)];
+      tb[i] = v;
+    }
+    for (int i = tid; i < 3 * MP * MP; i += NT) {   // padded P[b][i] and Pt[i][b]
+      const int d = i / (MP * MP), rr = i - d * MP * MP, A = rr / MP, B = rr - A * MP;
+      const bool in = A < M && B < M;
+      Pp[d * MS + A * LD + B] = in ? src[d][et_P(P) + A * M + B] : 0.0;
+      Ptp[d * MS + A * LD + B] = in ? src[d][et_P(P) + B * M + A] : 0.0;
+    }
+  }
+  for (int i = tid; i < 6 * QQ; i += NT) {
+    const int f = i / QQ, r = i - f * QQ, A = r / Q, B = r - A * Q, d = f >> 1, s = f & 1;
+    int t1, t2, t3;
+    if (d == 0) { t1 = s * P; t3 = A; t2 = B; }
+    else if (d == 1) { t2 = s * P; t3 = A; t1 = B; }
+    else { t3 = s * P; t2 = A; t1 = B; }
+    Uc[i] = __ldg(&u[skel_index_t<P>(g, e1 * P + t1, e2 * P + t2, e3 * P + t3)]);
+  }
+  __syncthreads();
+  for (int i = tid; i < 6 * MP * MP; i += NT) {     // padded face interiors; zero G's padding
+    const int f = i / (MP * MP), rr = i - f * MP * MP, A = rr / MP, B = rr - A * MP;
+    Ab[f * MS + A * LD + B] = (A < M && B < M) ? Uc[f * QQ + (A + 1) * Q + B + 1] : 0.0;
+    G[f * MS + A * LD + B] = 0.0;
+  }
+  for (int i = tid; i < MM * M; i += NT) {          // 1/D over the interior eigen-triples
+    const int b3 = i / MM, rr = i - b3 * MM, b2 = rr / M, b1 = rr - b2 * M;
+    invD[i] = rcp_nr(lam + tb[EC::tLam + b1] + tb[TB + EC::tLam + b2] + tb[2 * TB + EC::tLam + b3]);
+  }
+  __syncthreads();
+  // tangential directions of face f: a = x2 for d = 0 else x1 ; b = x3 for d < 2 else x2
+  for (int f = warp; f < 6; f += C::NW) {            // forward A: X_f = U_f Pt_a  (X into T)
+    const int d = f >> 1, da = (d == 0) ? 1 : 0;
+    dmma_tile<MP, LD>(Ab + f * MS, Ptp + da * MS, T + f * MS, 0, 0, lane);
+  }
+  __syncthreads();
+  for (int f = warp; f < 6; f += C::NW) {            // forward B: T_f = P_b X_f  (into Ab)
+    const int d = f >> 1, db = (d == 2) ? 1 : 2;
+    dmma_tile<MP, LD>(Pp + db * MS, T + f * MS, Ab + f * MS, 0, 0, lane);
+  }
+  __syncthreads();
+  {
+    const double *a10 = tb + EC::ta0, *a11 = tb + EC::ta1;
+    const double *a20 = tb + TB + EC::ta0, *a21 = tb + TB + EC::ta1;
+    const double *a30 = tb + 2 * TB + EC::ta0, *a31 = tb + 2 * TB + EC::ta1;
+    const double *T0 = Ab, *T1 = Ab + MS, *T2 = Ab + 2 * MS, *T3 = Ab + 3 * MS, *T4 = Ab + 4 * MS, *T5 = Ab + 5 * MS;
+    for (int i = tid; i < 3 * MM; i += NT) {
+      const int pass = i / MM, r = i - pass * MM, hi = r / M, lo = r - hi * M;
+      double g0 = 0.0, g1 = 0.0;
+      if (pass == 0) {          // (b3, b2), reduce over b1 -> faces 0, 1
+        const int b3 = hi, b2 = lo;
+        const double tA = T0[b3 * LD + b2], tB = T1[b3 * LD + b2], c2 = a20[b2], c2b = a21[b2], c3 = a30[b3], c3b = a31[b3];
+#pragma unroll
+        for (int b1 = 0; b1 < M; ++b1) {
+          double Ev = a10[b1] * tA;
+          Ev = fma(a11[b1], tB, Ev);
+          Ev = fma(c2, T2[b3 * LD + b1], Ev);
+          Ev = fma(c2b, T3[b3 * LD + b1], Ev);
+          Ev = fma(c3, T4[b2 * LD + b1], Ev);
+          Ev = fma(c3b, T5[b2 * LD + b1], Ev);
+          const double V = Ev * invD[(b3 * M + b2) * M + b1];
+          g0 = fma(a10[b1], V, g0);
+          g1 = fma(a11[b1], V, g1);
+        }
+        G[0 * MS + b3 * LD + b2] = g0;
+        G[1 * MS + b3 * LD + b2] = g1;
+      } else if (pass == 1) {   // (b3, b1), reduce over b2 -> faces 2, 3
+        const int b3 = hi, b1 = lo;
+        const double tA = T2[b3 * LD + b1], tB = T3[b3 * LD + b1], c1 = a10[b1], c1b = a11[b1], c3 = a30[b3], c3b = a31[b3];
+#pragma unroll
+        for (int b2 = 0; b2 < M; ++b2) {
+          double Ev = c1 * T0[b3 * LD + b2];
+          Ev = fma(c1b, T1[b3 * LD + b2], Ev);
+          Ev = fma(a20[b2], tA, Ev);
+          Ev = fma(a21[b2], tB, Ev);
+          Ev = fma(c3, T4[b2 * LD + b1], Ev);
+          Ev = fma(c3b, T5[b2 * LD + b1], Ev);
+          const double V = Ev * invD[(b3 * M + b2) * M + b1];
+          g0 = fma(a20[b2], V, g0);
+          g1 = fma(a21[b2], V, g1);
+        }
+        G[2 * MS + b3 * LD + b1] = g0;
+        G[3 * MS + b3 * LD + b1] = g1;
+      } else {                  // (b2, b1), reduce over b3 -> faces 4, 5
+        const int b2 = hi, b1 = lo;
+        const double tA = T4[b2 * LD + b1], tB = T5[b2 * LD + b1], c1 = a10[b1], c1b = a11[b1], c2 = a20[b2], c2b = a21[b2];
+#pragma unroll
+        for (int b3 = 0; b3 < M; ++b3) {
+          double Ev = c1 * T0[b3 * LD + b2];
+          Ev = fma(c1b, T1[b3 * LD + b2], Ev);
+          Ev = fma(c2, T2[b3 * LD + b1], Ev);
+          Ev = fma(c2b, T3[b3 * LD + b1], Ev);
+          Ev = fma(a30[b3], tA, Ev);
+          Ev = fma(a31[b3], tB, Ev);
+          const double V = Ev * invD[(b3 * M + b2) * M + b1];
+          g0 = fma(a30[b3], V, g0);
+          g1 = fma(a31[b3], V, g1);
+        }
+        G[4 * MS + b2 * LD + b1] = g0;
+        G[5 * MS + b2 * LD + b1] = g1;
+      }
+    }
+  }
+  __syncthreads();
+  for (int f = warp; f < 6; f += C::NW) {            // back A: X_f = G_f P_a   (into T)
+    const int d = f >> 1, da = (d == 0) ? 1 : 0;
+    dmma_tile<MP, LD>(G + f * MS, Pp + da * MS, T + f * MS, 0, 0, lane);
+  }
+  __syncthreads();
+  for (int f = warp; f < 6; f += C::NW) {            // back B: C_f = P_b^T X_f  (into G)
+    const int d = f >> 1, db = (d == 2) ? 1 : 2;
+    dmma_tile<MP, LD>(Ptp + db * MS, T + f * MS, G + f * MS, 0, 0, lane);
+  }
+  __syncthreads();
+  const double* Mv[3] = {tb + EC::tM, tb + TB + EC::tM, tb + 2 * TB + EC::tM};
+  const double* Kv[3] = {tb + EC::tK, tb + TB + EC::tK, tb + 2 * TB + EC::tK};
+  double* Ye = Y + (size_t)e * g.YS;
+  constexpr int YS = 6 * MM + 12 * M + 8;
+  for (int o = tid; o < YS; o += NT) {
+    double y;
+    if (o < 6 * MM) {      // face interior: closed-face row / column sums and the opposite face
+      const int f = o / MM, r = o - f * MM, A = r / M, B = r - A * M, d = f >> 1, s = f & 1;
+      const int da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2;
+      const int td = s * P, ta = B + 1, tb_ = A + 1;
+      const double* Uf = Uc + f * QQ;
+      const double *Kd = Kv[d], *Ka = Kv[da], *Kb = Kv[db];
+      const double Md = Mv[d][td], Ma = Mv[da][ta], Mb = Mv[db][tb_];
+      double sa = 0.0, sb = 0.0;
+#pragma unroll
+      for (int t = 0; t <= P; ++t) {
+        sa = fma(Ka[ta * Q + t], Uf[tb_ * Q + t], sa);
+        sb = fma(Kb[tb_ * Q + t], Uf[t * Q + ta], sb);
+      }
+      const double sd = Kd[td * Q] * Uc[(2 * d) * QQ + tb_ * Q + ta] + Kd[td * Q + P] * Uc[(2 * d + 1) * QQ + tb_ * Q + ta];
+      y = lam * Md * Ma * Mb * Uf[tb_ * Q + ta];
+      y = fma(Ma * Mb, sd, y);
+      y = fma(Md * Mb, sa, y);
+      y = fma(Md * Ma, sb, y);
+      y -= G[f * MS + A * LD + B];
+    } else {               // edges and vertices: all three lines lie on the element boundary
+      int t1, t2, t3;
+      if (o < 6 * MM + 12 * M) {
+        const int r = o - 6 * MM, qe = r / M, i = r - qe * M, d = qe >> 2, sA = qe & 1, sB = (qe >> 1) & 1;
+        if (d == 0) { t1 = i + 1; t2 = sA * P; t3 = sB * P; }
+        else if (d == 1) { t2 = i + 1; t1 = sA * P; t3 = sB * P; }
+        else { t3 = i + 1; t1 = sA * P; t2 = sB * P; }
+      } else {
+        const int qv = o - 6 * MM - 12 * M;
+        t1 = (qv & 1) * P; t2 = ((qv >> 1) & 1) * P; t3 = ((qv >> 2) & 1) * P;
+      }
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int t = 0; t <= P; ++t) {
+        s1 = fma(Kv[0][t1 * Q + t], getUc<P>(Uc, t, t2, t3), s1);
+        s2 = fma(Kv[1][t2 * Q + t], getUc<P>(Uc, t1, t, t3), s2);
+        s3 = fma(Kv[2][t3 * Q + t], getUc<P>(Uc, t1, t2, t), s3);
+      }
+      const double m1 = Mv[0][t1], m2 = Mv[1][t2], m3 = Mv[2][t3];
+      y = lam * m1 * m2 * m3 * getUc<P>(Uc, t1, t2, t3);
+      y = fma(m2 * m3, s1, y);
+      y = fma(m1 * m3, s2, y);
+      y = fma(m1 * m2, s3, y);
+    }
+    Ye[o] = y;
   }
 }
 
@@ -584,23 +819,6 @@ __global__ void __launch_bounds__(StarSpCfg<P>::NT) k_star_sp(LevelGeom g, int c
 // core for load/issue slots.  Leading dimension LD = NP + 4 keeps the fragment loads at the
 // 2-wavefront minimum.  The core is the single-pass DFMA core of k_star_sp.
 // ------------------------------------------------------------------------------------------
-__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
-
-// C = A * B for NP x NP row-major shared-memory matrices (leading dimension LD); one warp, tile (mi, ni)
-template <int NP, int LD>
-__device__ __forceinline__ void dmma_tile(const double* A, const double* B, double* Cm, int mi, int ni, int lane) {
-  const int r = lane >> 2, q = lane & 3;
-  double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-  for (int kk = 0; kk < NP / 4; ++kk) dmma884(c0, c1, A[(8 * mi + r) * LD + 4 * kk + q], B[(4 * kk + q) * LD + 8 * ni + r]);
-  Cm[(8 * mi + r) * LD + 8 * ni + 2 * q] = c0;
-  Cm[(8 * mi + r) * LD + 8 * ni + 2 * q + 1] = c1;
-}
-
 template <int P> struct StarDmCfg {
   static constexpr int N = 2 * P - 1, NN = N * N, C = P - 1;
   static constexpr int NP = (N <= 8) ? 8 : 16, LD = NP + 4, MS = NP * LD, TPP = (NP / 8) * (NP / 8);
@@ -767,6 +985,28 @@ static int star_variant() {
   return v;
 }
 
+// element kernel variant for p <= 8: 0 DMMA transforms + 1/D table (default), 1 DFMA (k_elem_apply_t)
+static int elem_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("PMG_ELEM_VARIANT");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v;
+}
+
+template <int P>
+void launch_elem_p(const LevelGeom& g, const double* u, const double* etab, double lam, double* Y, const int* done,
+                   cudaStream_t st) {
+  if constexpr (P <= 8) {
+    if (elem_variant() == 0) {
+      k_elem_dm<P><<<(unsigned)g.nelem, ElemDmCfg<P>::NT, elem_dm_smem<P>(), st>>>(g, u, etab, lam, Y, done);
+      return;
+    }
+  }
+  k_elem_apply_t<P><<<(unsigned)g.nelem, ElemCfg<P>::NT, elem_t_smem<P>(), st>>>(g, u, etab, lam, Y, done);
+}
+
 template <int P>
 void launch_star_p(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c, long long nb, const double* r,
                    double* u, const double* stab, const double* stabT, double lam, cudaStream_t st) {
@@ -787,7 +1027,7 @@ cudaError_t launch_elem_apply(const LevelGeom& g, const double* u, const double*
   switch (g.p) {
 #define CASE(P)                                                                                     \
   case P:                                                                                           \
-    k_elem_apply_t<P><<<(unsigned)g.nelem, ElemCfg<P>::NT, elem_t_smem<P>(), st>>>(g, u, etab, lam, Y, done); \
+    launch_elem_p<P>(g, u, etab, lam, Y, done, st);                                                \
     break;
     PMG_DEGREES(CASE)
 #undef CASE
@@ -813,7 +1053,7 @@ cudaError_t launch_star(const LevelGeom& g, int c1, int c2, int c3, int n1c, int
 size_t hot_smem(int p, int which) {
   switch (p) {
 #define CASE(P) \
-  case P: return which == 0 ? elem_t_smem<P>() : (kStarSinglePass(P) ? std::max(star_sp_smem<(P <= 8 ? P : 2)>(), star_dm_smem<(P <= 8 ? P : 2)>()) : star_t_smem<P>());
+  case P: return which == 0 ? std::max(elem_t_smem<P>(), elem_dm_smem<(P <= 8 ? P : 2)>()) : (kStarSinglePass(P) ? std::max(star_sp_smem<(P <= 8 ? P : 2)>(), star_dm_smem<(P <= 8 ? P : 2)>()) : star_t_smem<P>());
     PMG_DEGREES(CASE)
 #undef CASE
     default: return 0;
@@ -825,6 +1065,8 @@ cudaError_t hot_set_smem_attr(int bytes) {
 #define CASE(P)                                                                                        \
   {                                                                                                    \
     cudaError_t a = cudaFuncSetAttribute(k_elem_apply_t<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+    if (a == cudaSuccess && P <= 8)                                                                    \
+      a = cudaFuncSetAttribute(k_elem_dm<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     cudaError_t b = cudaFuncSetAttribute(k_star_t<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);       \
     if (b == cudaSuccess && kStarSinglePass(P))                                                        \
       b = cudaFuncSetAttribute(k_star_sp<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \

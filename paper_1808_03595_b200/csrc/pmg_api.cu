@@ -653,7 +653,9 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
       {
         const LevelGeom& g0 = c->D[0].g;
         const char* ce = std::getenv("PMG_COARSE_CLUSTER");
-        const bool want_cluster = !(ce && ce[0] == '0');
+        // opt-in: on the 16 SMs of one cluster the per-entry index arithmetic is slower than the
+        // grid barrier it saves (measured)
+        const bool want_cluster = (ce && ce[0] == '1');
         int csz = 16;
         if (cudaFuncSetAttribute(k_pcg_cluster_p2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
           cudaGetLastError();
