@@ -198,6 +198,75 @@ __device__ __forceinline__ double apply_entry(const LevelGeom& g, const CoarseTa
   return q;
 }
 
+// Register-resident variant: when the grid has at least one thread per coarse unknown, each thread
+// keeps x, r, z, p, q, D^-1 of its entry in registers for the whole solve.  Only z is published to
+// global memory (the neighbours' stencil reads it after the barrier), so an iteration costs one
+// L2 round trip for the stencil and one per partial-sum exchange, plus the two grid barriers.
+__global__ void __launch_bounds__(256) k_pcg_coop_reg_p2(LevelGeom g, CoarseTabs ct, const double* __restrict__ b,
+                                                        double* __restrict__ xout, double* __restrict__ zpub,
+                                                        const double* __restrict__ dinv, double lam,
+                                                        double* __restrict__ part, PcgState* st, double rtol, int maxit) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[64];
+  const int nb = gridDim.x;
+  double* part_a = part;           // p.q
+  double* part_b = part + nb;      // r.r (b.b at init)
+  double* part_c = part + 2 * nb;  // r.z
+  const long long n = g.nskel;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool own = i < n;
+  const double bi = own ? b[i] : 0.0, di = own ? dinv[i] : 0.0;
+  double x = 0.0, r = bi, z = di * bi, pv = 0.0, q = 0.0;
+  if (own) zpub[i] = z;
+  double s1 = block_reduce(r * z, red);
+  if (threadIdx.x == 0) part_c[blockIdx.x] = s1;
+  double s2 = block_reduce(bi * bi, red);
+  if (threadIdx.x == 0) part_b[blockIdx.x] = s2;
+  grid.sync();
+  double rz, bb;
+  grid_totals(part_c, part_b, nb, red, rz, bb);
+  double beta = 0.0;
+  int its = 0, breakdown = 0;
+  bool done = (bb == 0.0);
+  while (!done) {
+    // p = z + beta p ; q = H_hat z + beta q ; partial p.q
+    if (own) {
+      pv = fma(beta, pv, z);
+      q = fma(beta, q, apply_entry(g, ct, GlobalAcc{zpub}, i, lam));
+    }
+    const double spq = block_reduce(pv * q, red);
+    if (threadIdx.x == 0) part_a[blockIdx.x] = spq;
+    grid.sync();
+    double pq, unused;
+    grid_totals(part_a, nullptr, nb, red, pq, unused);
+    if (!(pq > 0.0)) { breakdown = 1; break; }
+    const double alpha = rz / pq;
+    x = fma(alpha, pv, x);
+    r = fma(-alpha, q, r);
+    z = di * r;
+    if (own) zpub[i] = z;
+    const double srr = block_reduce(r * r, red);
+    if (threadIdx.x == 0) part_b[blockIdx.x] = srr;
+    const double srz = block_reduce(r * z, red);
+    if (threadIdx.x == 0) part_c[blockIdx.x] = srz;
+    grid.sync();
+    double rr, rzn;
+    grid_totals(part_b, part_c, nb, red, rr, rzn);
+    ++its;
+    if (sqrt(rr) <= rtol * sqrt(bb) || its >= maxit) break;
+    beta = rzn / rz;
+    rz = rzn;
+  }
+  if (own) xout[i] = x;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->its = its;
+    st->its_sum += its;
+    if (breakdown) st->breakdown = 1;
+    st->done = 1;
+    st->bb = bb;
+  }
+}
+
 // Two grid barriers per iteration: with p_new = z + beta p and q = H_hat p,
 //   q_new = H_hat z + beta q_old,
 // so the direction update, the operator application (on z, complete after the previous barrier)

@@ -575,11 +575,15 @@ __global__ void k_prolong(LevelGeom gf, LevelGeom gc, const double* __restrict__
 // condensation and interior recovery (O(p^4) per element via the interior fast diagonalisation)
 // cube[i3][i2][i1] in shared memory when it fits, else in a global scratch slot per block
 // ------------------------------------------------------------------------------------------
-__device__ void cube_transform(double* cube, int m, const double* S1, const double* S2, const double* S3,
+// MT > 0: compile-time m (line held in registers, loops unrolled); MT = 0: runtime m
+template <int MT>
+__device__ void cube_transform(double* cube, int m_rt, const double* S1, const double* S2, const double* S3,
                                bool transpose) {
   // transpose = true: out[b] = sum_i S[i][b] in[i]  (S^T);  false: out[i] = sum_b S[i][b] in[b]
+  const int m = MT ? MT : m_rt;
   const int tid = threadIdx.x, nt = blockDim.x, mm = m * m;
-  double tmp[32];
+  double tmp[MT ? MT : 32];
+  double lin[MT ? MT : 1];
   for (int dir = 0; dir < 3; ++dir) {
     const double* S = dir == 0 ? S1 : (dir == 1 ? S2 : S3);
     for (int line = tid; line < mm; line += nt) {
@@ -588,10 +592,22 @@ __device__ void cube_transform(double* cube, int m, const double* S1, const doub
       if (dir == 0) { base = (A * m + B) * m; stride = 1; }          // (i3, i2), along i1
       else if (dir == 1) { base = A * mm + B; stride = m; }         // (i3, i1), along i2
       else { base = A * m + B; stride = mm; }                       // (i2, i1), along i3
-      for (int o = 0; o < m; ++o) {
-        double s = 0.0;
-        for (int i = 0; i < m; ++i) s += (transpose ? S[i * m + o] : S[o * m + i]) * cube[base + i * stride];
-        tmp[o] = s;
+      if (MT) {
+#pragma unroll
+        for (int i = 0; i < (MT ? MT : 1); ++i) lin[i] = cube[base + i * stride];
+#pragma unroll
+        for (int o = 0; o < (MT ? MT : 1); ++o) {
+          double s = 0.0;
+#pragma unroll
+          for (int i = 0; i < (MT ? MT : 1); ++i) s = fma(transpose ? S[i * m + o] : S[o * m + i], lin[i], s);
+          tmp[o] = s;
+        }
+      } else {
+        for (int o = 0; o < m; ++o) {
+          double s = 0.0;
+          for (int i = 0; i < m; ++i) s += (transpose ? S[i * m + o] : S[o * m + i]) * cube[base + i * stride];
+          tmp[o] = s;
+        }
       }
       for (int o = 0; o < m; ++o) cube[base + o * stride] = tmp[o];
     }
@@ -605,11 +621,13 @@ size_t condense_smem(int p, int ET, bool cube_in_smem) {
 }
 
 // Yc[e] (6 m^2) = (H_BI H_II^-1 F_I) on the six face interiors of element e
+// PT > 0: compile-time degree; PT = 0: runtime degree
+template <int PT>
 __global__ void __launch_bounds__(256) k_condense_elem(LevelGeom g, const double* __restrict__ Fg,
                                                        const double* __restrict__ etab, double lam,
                                                        double* __restrict__ Yc, double* __restrict__ cube_g) {
   extern __shared__ double sm[];
-  const int p = g.p, m = g.m, mm = m * m, ET = g.ET;
+  const int p = PT ? PT : g.p, m = p - 1, mm = m * m, ET = g.ET;
   const bool cube_in_smem = (cube_g == nullptr);
   double* G = sm;
   double* X = G + 6 * mm;
@@ -627,7 +645,7 @@ __global__ void __launch_bounds__(256) k_condense_elem(LevelGeom g, const double
       cube[i] = Fg[(e1 * p + i1 + 1) + N1 * ((e2 * p + i2 + 1) + N2 * (long long)(e3 * p + i3 + 1))];
     }
     __syncthreads();
-    cube_transform(cube, m, tb + et_S(p), tb + ET + et_S(p), tb + 2 * ET + et_S(p), true);
+    cube_transform<PT ? PT - 1 : 0>(cube, m, tb + et_S(p), tb + ET + et_S(p), tb + 2 * ET + et_S(p), true);
     const double *L1 = tb + et_lam(p), *L2 = tb + ET + et_lam(p), *L3 = tb + 2 * ET + et_lam(p);
     for (int i = tid; i < mm * m; i += nt) {
       int b3 = i / mm, r = i - b3 * mm, b2 = r / m, b1 = r - b2 * m;
@@ -694,11 +712,12 @@ __global__ void k_condense_gather(LevelGeom g, const double* __restrict__ Fg, co
 }
 
 // u_I = S (x) S (x) S [ (S^T (x) S^T (x) S^T F_I - sum_f a_f (x) T_f) / D ],  T_f = (P_b (x) P_a) u_f
+template <int PT>
 __global__ void __launch_bounds__(256) k_recover_elem(LevelGeom g, const double* __restrict__ Fg,
                                                       const double* __restrict__ uh, const double* __restrict__ etab,
                                                       double lam, double* __restrict__ ug, double* __restrict__ cube_g) {
   extern __shared__ double sm[];
-  const int p = g.p, m = g.m, mm = m * m, ET = g.ET, q = p + 1;
+  const int p = PT ? PT : g.p, m = p - 1, mm = m * m, ET = g.ET, q = p + 1;
   const bool cube_in_smem = (cube_g == nullptr);
   double* T = sm;              // 6 mm
   double* X = T + 6 * mm;      // mm
@@ -743,7 +762,7 @@ __global__ void __launch_bounds__(256) k_recover_elem(LevelGeom g, const double*
       }
       __syncthreads();
     }
-    cube_transform(cube, m, tb + et_S(p), tb + ET + et_S(p), tb + 2 * ET + et_S(p), true);
+    cube_transform<PT ? PT - 1 : 0>(cube, m, tb + et_S(p), tb + ET + et_S(p), tb + 2 * ET + et_S(p), true);
     const double *L1 = tb + et_lam(p), *L2 = tb + ET + et_lam(p), *L3 = tb + 2 * ET + et_lam(p);
     const double *a10 = tb + et_a0(p), *a11 = tb + et_a1(p);
     const double *a20 = tb + ET + et_a0(p), *a21 = tb + ET + et_a1(p);
@@ -756,7 +775,7 @@ __global__ void __launch_bounds__(256) k_recover_elem(LevelGeom g, const double*
       cube[i] = (cube[i] - E) / (lam + L1[b1] + L2[b2] + L3[b3]);
     }
     __syncthreads();
-    cube_transform(cube, m, tb + et_S(p), tb + ET + et_S(p), tb + 2 * ET + et_S(p), false);
+    cube_transform<PT ? PT - 1 : 0>(cube, m, tb + et_S(p), tb + ET + et_S(p), tb + 2 * ET + et_S(p), false);
     for (int i = tid; i < mm * m; i += nt) {
       int i3 = i / mm, r = i - i3 * mm, i2 = r / m, i1 = r - i2 * m;
       ug[(e1 * p + i1 + 1) + N1 * ((e2 * p + i2 + 1) + N2 * (long long)(e3 * p + i3 + 1))] = cube[i];
@@ -909,6 +928,51 @@ __global__ void k_pcg_pdir(double* __restrict__ pv, const double* __restrict__ z
   const double bt = st->beta;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     pv[i] = z[i] + bt * pv[i];
+}
+
+// ------------------------------------------------------------------------------------------
+// degree dispatch of the condense / recover kernels (compile-time p for the supported degrees)
+// ------------------------------------------------------------------------------------------
+#define PMG_CR_DEGREES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) \
+  X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32)
+
+cudaError_t launch_condense_elem(int nb, int nt, size_t sm, cudaStream_t st, const LevelGeom& g, const double* Fg,
+                                 const double* etab, double lam, double* Yc, double* cube_g) {
+  switch (g.p) {
+#define CASE(P) \
+  case P: k_condense_elem<P><<<nb, nt, sm, st>>>(g, Fg, etab, lam, Yc, cube_g); break;
+    PMG_CR_DEGREES(CASE)
+#undef CASE
+    default: k_condense_elem<0><<<nb, nt, sm, st>>>(g, Fg, etab, lam, Yc, cube_g);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_recover_elem(int nb, int nt, size_t sm, cudaStream_t st, const LevelGeom& g, const double* Fg,
+                                const double* uh, const double* etab, double lam, double* ug, double* cube_g) {
+  switch (g.p) {
+#define CASE(P) \
+  case P: k_recover_elem<P><<<nb, nt, sm, st>>>(g, Fg, uh, etab, lam, ug, cube_g); break;
+    PMG_CR_DEGREES(CASE)
+#undef CASE
+    default: k_recover_elem<0><<<nb, nt, sm, st>>>(g, Fg, uh, etab, lam, ug, cube_g);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t condense_recover_set_smem_attr(int bytes) {
+  cudaError_t e = cudaSuccess;
+#define CASE(P)                                                                                              \
+  {                                                                                                          \
+    cudaError_t a = cudaFuncSetAttribute(k_condense_elem<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+    cudaError_t b = cudaFuncSetAttribute(k_recover_elem<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);  \
+    if (a != cudaSuccess) e = a;                                                                             \
+    if (b != cudaSuccess) e = b;                                                                             \
+  }
+  PMG_CR_DEGREES(CASE)
+  CASE(0)
+#undef CASE
+  return e;
 }
 
 }  // namespace pmg

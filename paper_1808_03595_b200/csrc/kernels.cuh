@@ -28,6 +28,8 @@ struct CoarseTabs {
 __global__ void k_pcg_coop_p2(LevelGeom g, CoarseTabs ct, const double* b, double* x, double* r, double* z,
                               double* pv, double* q, const double* dinv, double lam, double* part, PcgState* st,
                               double rtol, int maxit);
+__global__ void k_pcg_coop_reg_p2(LevelGeom g, CoarseTabs ct, const double* b, double* xout, double* zpub,
+                                  const double* dinv, double lam, double* part, PcgState* st, double rtol, int maxit);
 __global__ void k_pcg_cluster_p2(LevelGeom g, CoarseTabs ct, const double* b, double* xout, const double* dinv,
                                  double lam, int chunk, int halo, unsigned long long inv, PcgState* st, double rtol,
                                  int maxit);
@@ -48,10 +50,12 @@ __global__ void k_star(LevelGeom g, int c1, int c2, int c3, int n1c, int n2c, co
 __global__ void k_restrict_local(LevelGeom gf, int pc, const double* Jint, const double* rf, double* Z);
 __global__ void k_restrict_gather(LevelGeom gc, const double* Z, double* fc);
 __global__ void k_prolong(LevelGeom gf, LevelGeom gc, const double* Jint, const double* uc, double* uf);
-__global__ void k_condense_elem(LevelGeom g, const double* Fg, const double* etab, double lam, double* Yc, double* cube_g);
+cudaError_t launch_condense_elem(int nb, int nt, size_t sm, cudaStream_t st, const LevelGeom& g, const double* Fg,
+                                 const double* etab, double lam, double* Yc, double* cube_g);
+cudaError_t launch_recover_elem(int nb, int nt, size_t sm, cudaStream_t st, const LevelGeom& g, const double* Fg,
+                                const double* uh, const double* etab, double lam, double* ug, double* cube_g);
+cudaError_t condense_recover_set_smem_attr(int bytes);
 __global__ void k_condense_gather(LevelGeom g, const double* Fg, const double* Yc, double* fhat);
-__global__ void k_recover_elem(LevelGeom g, const double* Fg, const double* uh, const double* etab, double lam,
-                               double* ug, double* cube_g);
 __global__ void k_dot_partial(const double* a, const double* b, long long n, double* part, const int* done);
 __global__ void k_sum_final(const double* part, int nb, double* out);
 __global__ void k_zero(double* x, long long n);

@@ -73,6 +73,7 @@ struct pmg_ctx {
   bool ref_kernels = false;  // PMG_REFERENCE_KERNELS=1: runtime-p v1 kernels (A/B checks only)
   bool use_coop = false;     // coarse CG as one persistent cooperative kernel (p0 = 2)
   int coop_nb = 0;
+  bool coop_reg = false;     // register-resident variant (one coarse unknown per thread)
   double* ctab[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // CoarseTabs storage
   double* cV = nullptr;      // (unused)
   cudaGraphExec_t cycle_exec = nullptr;   // captured solve cycle (V-cycle + residual + norm^2)
@@ -255,6 +256,8 @@ pmg_status pcg_dev(pmg_ctx* c, const double* b, double* x) {
     CoarseTabs ct{c->ctab[0], c->ctab[1], c->ctab[2], c->ctab[3], c->ctab[4], c->ctab[5], c->ctab[6]};
     void* args[] = {&g0, &ct, (void*)&b, &x, &c->cr, &c->cz, &c->cp, &c->cq, (void*)&dinv, &lam, &part,
                     &st, &rtol, &maxit};
+    void* args_reg[] = {&g0, &ct, (void*)&b, &x, &c->cz, (void*)&dinv, &lam, &part, &st, &rtol, &maxit};
+    const void* fn = c->coop_reg ? (const void*)k_pcg_coop_reg_p2 : (const void*)k_pcg_coop_p2;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c->coop_nb);
     cfg.blockDim = dim3(kThreads);
@@ -265,7 +268,7 @@ pmg_status pcg_dev(pmg_ctx* c, const double* b, double* x) {
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CUDA_CHECK(cudaLaunchKernelExC(&cfg, (const void*)k_pcg_coop_p2, args));
+    CUDA_CHECK(cudaLaunchKernelExC(&cfg, fn, c->coop_reg ? args_reg : args));
     c->launches++;
     return PMG_OK;
   }
@@ -359,7 +362,7 @@ pmg_status condense_dev(pmg_ctx* c, const double* F, double* fhat) {
   const DevLevel& D = c->D[c->L];
   size_t sm = condense_smem(D.g.p, D.g.ET, c->cube_in_smem);
   int nb = c->cube_in_smem ? (int)std::min<long long>(D.g.nelem, 148LL * 8) : c->cube_blocks;
-  k_condense_elem<<<nb, kThreads, sm, c->st>>>(D.g, F, D.etab, c->lam, c->Y, c->cube_in_smem ? nullptr : c->cube);
+  launch_condense_elem(nb, kThreads, sm, c->st, D.g, F, D.etab, c->lam, c->Y, c->cube_in_smem ? nullptr : c->cube);
   LAUNCH_CHECK(c);
   k_condense_gather<<<grid_for(D.g.nskel), kThreads, 0, c->st>>>(D.g, F, c->Y, fhat);
   LAUNCH_CHECK(c);
@@ -372,7 +375,7 @@ pmg_status recover_dev(pmg_ctx* c, const double* uhat, const double* F, double* 
   LAUNCH_CHECK(c);
   size_t sm = recover_smem(D.g.p, D.g.ET, c->cube_in_smem);
   int nb = c->cube_in_smem ? (int)std::min<long long>(D.g.nelem, 148LL * 8) : c->cube_blocks;
-  k_recover_elem<<<nb, kThreads, sm, c->st>>>(D.g, F, uhat, D.etab, c->lam, ufull, c->cube_in_smem ? nullptr : c->cube);
+  launch_recover_elem(nb, kThreads, sm, c->st, D.g, F, uhat, D.etab, c->lam, ufull, c->cube_in_smem ? nullptr : c->cube);
   LAUNCH_CHECK(c);
   return PMG_OK;
 }
@@ -623,8 +626,8 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   cudaError_t e2 = cudaFuncSetAttribute(k_star, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
   cudaError_t e3 = cudaFuncSetAttribute(k_restrict_local, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
   cudaError_t e4 = cudaFuncSetAttribute(k_prolong, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
-  cudaError_t e5 = cudaFuncSetAttribute(k_condense_elem, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
-  cudaError_t e6 = cudaFuncSetAttribute(k_recover_elem, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  cudaError_t e5 = condense_recover_set_smem_attr(smem_optin);
+  cudaError_t e6 = cudaSuccess;
   if (e6 == cudaSuccess) e6 = hot_set_smem_attr(smem_optin);
   if (e1 || e2 || e3 || e4 || e5 || e6) { free_ctx(c); return fail(PMG_ECUDA, "cudaFuncSetAttribute failed"); }
   // persistent cooperative coarse CG when the coarse degree is 2 and the device supports it
@@ -688,6 +691,16 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
             c->cl_inv = ((1ULL << 40) + (unsigned long long)chunk - 1) / (unsigned long long)chunk;
           }
           cudaGetLastError();
+        }
+      }
+      {
+        int per_sm_reg = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_reg, k_pcg_coop_reg_p2, kThreads, 0);
+        const long long need = (c->D[0].g.nskel + kThreads - 1) / kThreads;
+        const char* re = std::getenv("PMG_COARSE_REG");
+        if (!(re && re[0] == '0') && per_sm_reg > 0 && need <= std::min<long long>((long long)per_sm_reg * nsm, 1344)) {
+          c->coop_reg = true;
+          c->coop_nb = (int)need;
         }
       }
       const char* nbenv = std::getenv("PMG_COOP_BLOCKS");   // tuning experiments only
