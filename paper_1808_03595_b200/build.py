@@ -1,4 +1,5 @@
 """Build libpmg.so in-tree for sm_100a (B200) with nvcc.  Invoked by __graft_entry__.build()."""
+import concurrent.futures
 import os
 import subprocess
 import sys
@@ -27,11 +28,16 @@ def build(verbose=False, force=False):
         return LIB
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for s in srcs:
+    def compile_one(s):
         o = os.path.join(objdir, os.path.basename(s) + ".o")
         cmd = [_nvcc()] + ARCH + FLAGS + ["-x", "cu" if s.endswith(".cu") else "c++", "-c", s, "-o", o]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return o, subprocess.run(cmd, capture_output=True, text=True)
+
+    # translation units are independent: compile them concurrently
+    with concurrent.futures.ThreadPoolExecutor(max_workers=len(srcs)) as ex:
+        results = list(ex.map(compile_one, srcs))
+    objs = []
+    for s, (o, r) in zip(srcs, results):
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("nvcc failed on " + s)

@@ -198,6 +198,69 @@ __device__ __forceinline__ double apply_entry(const LevelGeom& g, const CoarseTa
   return q;
 }
 
+// The same row of H_hat written out once: q[idx] = sum_k a[k] p[jx[k]] with the 13 line-stencil
+// entries first and the 12 face-centre entries of the (up to two) adjacent elements after them.
+// Unused slots point at idx itself with a zero coefficient (a harmless load).  The row never changes
+// during a solve, so a thread that owns idx for the whole solve builds it once and keeps it in
+// registers; each iteration is then 25 independent loads and 25 FMA.
+constexpr int kRowLen = 25;
+
+__device__ __forceinline__ void build_row(const LevelGeom& g, const CoarseTabs& ct, long long idx, double lam,
+                                          int* jx, double* a) {
+#pragma unroll
+  for (int k = 0; k < kRowLen; ++k) { jx[k] = (int)idx; a[k] = 0.0; }
+  Entry E = decode2(g, idx);
+  if (!is_free(g, E.g1, E.g2, E.g3)) return;
+  const int G[3] = {E.g1, E.g2, E.g3};
+  const int N[3] = {2 * g.k1, 2 * g.k2, 2 * g.k3};
+  const double* B[3] = {ct.b1, ct.b2, ct.b3};
+  const double* K[3] = {ct.K1, ct.K2, ct.K3};
+  double c0 = lam * __ldg(&B[0][G[0]]) * __ldg(&B[1][G[1]]) * __ldg(&B[2][G[2]]);
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2;
+    const bool full = ((G[da] & 1) == 0) || ((G[db] & 1) == 0);
+    const double w = __ldg(&B[da][G[da]]) * __ldg(&B[db][G[db]]);
+    const double* Kr = K[d] + (size_t)G[d] * 5;
+    c0 = fma(w, __ldg(&Kr[2]), c0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int o = (j < 2) ? j - 2 : j - 1;
+      const int s = G[d] + o;
+      int h[3] = {G[0], G[1], G[2]};
+      h[d] = s;
+      if (s >= 0 && s <= N[d] && (full || (s & 1) == 0)) {
+        jx[1 + 4 * d + j] = (int)sidx2(g, h[0], h[1], h[2]);
+        a[1 + 4 * d + j] = w * __ldg(&Kr[(j < 2) ? j : j + 1]);
+      }
+    }
+  }
+  a[0] = c0;
+  if (E.type < 3) {
+    const int d = E.type;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      int e[3] = {E.v1, E.v2, E.v3};
+      if (side == 1) e[d] -= 1;
+      const long long el = e[0] + (long long)g.k1 * (e[1] + (long long)g.k2 * e[2]);
+      double cw[7];
+#pragma unroll
+      for (int i = 0; i < 7; ++i) cw[i] = __ldg(&ct.ce[el * 7 + i]);
+      const double cd = (d == 0) ? cw[side] : ((d == 1) ? cw[2 + side] : cw[4 + side]);
+      const int b1 = 2 * e[0], b2 = 2 * e[1], b3 = 2 * e[2];
+      const int fb[6][3] = {{b1, b2 + 1, b3 + 1}, {b1 + 2, b2 + 1, b3 + 1}, {b1 + 1, b2, b3 + 1},
+                            {b1 + 1, b2 + 2, b3 + 1}, {b1 + 1, b2 + 1, b3}, {b1 + 1, b2 + 1, b3 + 2}};
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        if (inside(g, fb[i][0], fb[i][1], fb[i][2])) {
+          jx[13 + 6 * side + i] = (int)sidx2(g, fb[i][0], fb[i][1], fb[i][2]);
+          a[13 + 6 * side + i] = -cd * cw[6] * cw[i];
+        }
+      }
+    }
+  }
+}
+
 // Register-resident variant: when the grid has at least one thread per coarse unknown, each thread
 // keeps x, r, z, p, q, D^-1 of its entry in registers for the whole solve.  Only z is published to
 // global memory (the neighbours' stencil reads it after the barrier), so an iteration costs one
@@ -217,6 +280,9 @@ __global__ void __launch_bounds__(256) k_pcg_coop_reg_p2(LevelGeom g, CoarseTabs
   const bool own = i < n;
   const double bi = own ? b[i] : 0.0, di = own ? dinv[i] : 0.0;
   double x = 0.0, r = bi, z = di * bi, pv = 0.0, q = 0.0;
+  int jx[kRowLen];
+  double arow[kRowLen];
+  build_row(g, ct, own ? i : 0, lam, jx, arow);
   if (own) zpub[i] = z;
   double s1 = block_reduce(r * z, red);
   if (threadIdx.x == 0) part_c[blockIdx.x] = s1;
@@ -232,7 +298,13 @@ __global__ void __launch_bounds__(256) k_pcg_coop_reg_p2(LevelGeom g, CoarseTabs
     // p = z + beta p ; q = H_hat z + beta q ; partial p.q
     if (own) {
       pv = fma(beta, pv, z);
-      q = fma(beta, q, apply_entry(g, ct, GlobalAcc{zpub}, i, lam));
+      double zl[kRowLen];
+#pragma unroll
+      for (int k = 0; k < kRowLen; ++k) zl[k] = __ldcg(&zpub[jx[k]]);
+      double hz = 0.0;
+#pragma unroll
+      for (int k = 0; k < kRowLen; ++k) hz = fma(arow[k], zl[k], hz);
+      q = fma(beta, q, hz);
     }
     const double spq = block_reduce(pv * q, red);
     if (threadIdx.x == 0) part_a[blockIdx.x] = spq;
