@@ -92,9 +92,18 @@ def dist_init():
 
 
 def case_for(args, n_gpu):
+    """The workload; for n_gpu > 1 the weak-scaling variant: n_gpu z-slabs of the one-GPU problem
+    stacked along x3 (config 2: 16 x 16 x 16 n_gpu elements on (0,1)^2 x (0,n_gpu); config 5:
+    64 x 64 x 8 n_gpu, BASELINE.json)."""
     if args.config == 5:
-        return pi.config(5, n_gpu=1)      # per-replica weak-scaling slab 64x64x8
-    return pi.config(args.config, p=args.p)
+        return pi.config(5, n_gpu=n_gpu)
+    c = pi.config(args.config, p=args.p)
+    if n_gpu > 1:
+        k = (c.k[0], c.k[1], c.k[2] * n_gpu)
+        w = [c.widths[0], c.widths[1], np.tile(c.widths[2], n_gpu)]
+        c = pi.Case(c.name + "_weak%d" % n_gpu, k, w, c.p, c.lam, c.f_kind, seed=c.seed, amp=c.amp,
+                    noise=c.noise, origin=c.origin)
+    return c
 
 
 def n_stars(case):
@@ -189,10 +198,17 @@ def main():
     import paper_1808_03595_b200 as pmg
 
     case = case_for(args, ws)
-    s = pmg.Solver(case.k, case.widths, case.p, case.lam)
+    nccl_id = None
+    if ws > 1:   # z-slab decomposition: the library's own NCCL communicator (id broadcast here)
+        buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(pmg.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(buf, 0)
+        nccl_id = bytes(buf.cpu().numpy().tobytes())
+    s = pmg.Solver(case.k, case.widths, case.p, case.lam, rank=rank, nranks=ws, nccl_id=nccl_id)
     L = s.nlevels - 1
     coords = [s.grid_coords(L, d) for d in range(3)]
-    f = torch.from_numpy(case.f_nodal(coords)).cuda()
+    f = torch.from_numpy(case.f_nodal(coords, i3_offset=s.slab["z0"] * case.p)).cuda()
     F = s.new_grid()
     s.weak_rhs(f, F)
     u = s.new_grid()
@@ -242,7 +258,7 @@ def main():
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = ws * case.n_dof / (ms / 1e3)
+    value = case.n_dof / (ms / 1e3)          # all ranks' unknowns (case is the whole weak-scaled problem)
 
     # e2e: through the C ABI with host buffers (pinned), H2D of F and D2H of u inside the timed region
     e2e = None
@@ -266,15 +282,15 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         nb = F.numel() * 8
-        e2e = {"value": ws * case.n_dof / (ems / 1e3), "unit": "unknowns/s", "ms_per_step": ems,
+        e2e = {"value": case.n_dof / (ems / 1e3), "unit": "unknowns/s", "ms_per_step": ems,
                "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb}
 
     # roofline of the dominant kernel: the star smoother (finest level), FP64-pipe bound
     n = 2 * case.p - 1
     sweep_ms = sm_ms / max(sm_n, 1)
-    flops = 37.0 * n ** 3 * n_stars(case)            # Alg. 1 count x stars per sweep
+    flops = 37.0 * n ** 3 * n_stars(case) / ws       # Alg. 1 count x stars per sweep (per rank)
     achieved = flops / (sweep_ms / 1e3) / 1e12
-    bytes_alg = 24.0 * n_skel_free(case)             # read r, read+write u
+    bytes_alg = 24.0 * n_skel_free(case) / ws        # read r, read+write u, per rank
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", 6541.5)
     tr = load_traffic(case.name)
@@ -288,7 +304,7 @@ def main():
                          "frac": bytes_alg / (sweep_ms / 1e3) / 1e9 / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}}
     res_ms = rs_ms / max(rs_n, 1)
     m = case.p - 1
-    res_flops = (73.0 * m ** 3 + 24.0 * case.p * (case.p + 1) ** 2) * case.k[0] * case.k[1] * case.k[2]
+    res_flops = (73.0 * m ** 3 + 24.0 * case.p * (case.p + 1) ** 2) * case.k[0] * case.k[1] * case.k[2] / ws
     residual = {"kernel": "k_elem_apply + k_gather_resid (finest level)", "ms": res_ms,
                 "achieved_tflops": res_flops / (res_ms / 1e3) / 1e12,
                 "achieved_gbs_alg": bytes_alg / (res_ms / 1e3) / 1e9}
@@ -306,7 +322,8 @@ def main():
         "config": {"workload": case.name, "n_dof": case.n_dof, "p": case.p, "k": list(case.k), "lambda": case.lam,
                    "rtol": 1e-10, "cycles": r["cycles"], "rho": r["rho"], "coarse_iters": r["coarse_iters"],
                    "l2": "flushed between steps (512 MB write, outside the timed events)",
-                   "parallelism": "single GPU" if ws == 1 else "replicas (one independent solve per GPU; z-slab NCCL decomposition not implemented)"},
+                   "parallelism": "single GPU" if ws == 1 else
+                   "z-slab x%d (NCCL halo planes per operator, allreduce of owned norms, allgather of the coarse RHS + replicated coarse CG)" % ws},
         "roofline": roof,
         "residual_kernel": residual,
         "time_split_ms_per_step": {"smoother_all_levels": all_sm_ms / args.steps, "residual_all_levels": all_rs_ms / args.steps,

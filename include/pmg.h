@@ -28,6 +28,13 @@
  *    zero on input and are written as zero on output.
  *  - Levels: l = 0 .. L with degrees p_l = p0 2^l (l < L), p_L = p, L = ceil(log2(p/p0))
  *    (reading R10).  Level L is the finest.
+ *  - z-slabs (nranks > 1): every rank calls the same functions in the same
+ *    order.  Grid vectors are the rank's slab: grid planes z0 p .. z1 p (both shared planes
+ *    included; pmg_level_info's n_grid).  Skeleton vectors are local: the record planes zb .. z1
+ *    of pmg_slab (n_skel), ghost planes included; every call refreshes the ghost planes of its
+ *    skeleton inputs and outputs in place from the neighbour ranks, so on return every local
+ *    plane holds the undivided vector's values.  pmg_condense, pmg_recover and the layout
+ *    converters are one-GPU calls (pmg_solve condenses and recovers on slabs internally).
  */
 #ifndef PMG_H
 #define PMG_H
@@ -42,7 +49,7 @@ typedef enum {
   PMG_OK = 0,
   PMG_EINVAL = -1,      /* invalid argument (message says which) */
   PMG_ECUDA = -2,       /* a CUDA runtime call or kernel launch failed */
-  PMG_ENCCL = -3,       /* reserved for the multi-GPU path */
+  PMG_ENCCL = -3,       /* a NCCL call (or a loopback exchange) of the z-slab path failed */
   PMG_ENOCONV = -4,     /* pmg_solve: max_cycles reached before the tolerance (report filled) */
   PMG_EBREAKDOWN = -5,  /* coarse CG: p^T H p <= 0 */
   PMG_ENOMEM = -6       /* device allocation failed in pmg_setup */
@@ -55,10 +62,34 @@ typedef struct {
   double coarse_rtol; /* coarse CG relative tolerance, default 1e-8 (reading R11) */
   int coarse_maxit;   /* coarse CG iteration cap, default 10000 */
   int coarse_check;   /* coarse CG: host convergence poll every this many iterations, default 8 */
-  int rank, nranks;   /* z-slab decomposition; only nranks = 1 is implemented in this version */
-  const void* nccl_id;/* reserved (128-byte ncclUniqueId) */
+  int rank, nranks;   /* z-slab decomposition over nranks processes / GPUs:
+                         rank r owns element layers [z0_r, z1_r) (pmg_slab_plan); nranks = 1: one GPU */
+  const void* nccl_id;/* nranks > 1 with NCCL: 128-byte ncclUniqueId from pmg_nccl_unique_id on rank 0,
+                         broadcast by the caller (e.g. torch.distributed); the library creates and owns
+                         the communicator.  The caller's current CUDA device is used. */
+  void* loopback;     /* nranks > 1 in ONE process (correctness tests): a hub from pmg_loopback_create
+                         shared by the nranks contexts, each driven by its own host thread and stream;
+                         exchanges are host-synchronised device copies (no kernel waits on another
+                         rank).  Exactly one of nccl_id / loopback must be set when nranks > 1. */
   void* stream;       /* cudaStream_t; NULL = default stream */
 } pmg_options;
+
+/* z-slab plan of rank `rank` (pure host arithmetic, no GPU needed).  Element layers are split
+ * as z0 = floor(rank k3 / nranks), z1 = floor((rank+1) k3 / nranks) (k3 >= nranks required).
+ * Local skeleton vectors of a rank hold the record planes zb .. z1 (zb = max(z0 - 1, 0)): one
+ * ghost plane below (rank > 0) and the shared top plane z1, which is a ghost on every rank but
+ * the last (there it is the Dirichlet plane k3, all zero).  Owned local planes are
+ * [own_lo, own_hi): every global record plane is owned by exactly one rank.  A halo exchange
+ * sends local plane own_lo to rank-1 (it lands in that rank's plane nplanes-1) and local plane
+ * own_hi-1 to rank+1 (it lands in that rank's plane 0). */
+typedef struct {
+  int z0, z1;           /* owned element layers [z0, z1), global */
+  int zb;               /* global index of local vertex plane 0 */
+  int nplanes;          /* local vertex planes z1 - zb + 1 */
+  int own_lo, own_hi;   /* owned local record planes */
+  int lower, upper;     /* neighbour ranks, -1 if none */
+} pmg_slab;
+int pmg_slab_plan(int k3, int nranks, int rank, pmg_slab* out);   /* 0, or -1 on invalid input */
 
 typedef struct {
   int cycles;         /* V-cycles performed (n_10 of P:636 when rtol = 1e-10) */
@@ -69,6 +100,15 @@ typedef struct {
   double* history;    /* optional caller array (host) receiving ||r_n||, n = 0..cycles */
   int history_cap;    /* its capacity */
 } pmg_report;
+
+/* Multi-rank helpers.  pmg_nccl_unique_id writes a fresh 128-byte ncclUniqueId (call on rank 0
+ * only).  pmg_loopback_create returns a hub for `nranks` contexts of one process (NULL on
+ * failure); destroy it after every context that uses it. */
+pmg_status pmg_nccl_unique_id(void* out128);
+void* pmg_loopback_create(int nranks);
+void pmg_loopback_destroy(void* hub);
+/* the plan this context was set up with */
+pmg_status pmg_slab_info(const pmg_ctx* ctx, pmg_slab* out);
 
 /* Fill *opt with the defaults listed above. */
 void pmg_default_options(pmg_options* opt);

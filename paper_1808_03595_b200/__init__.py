@@ -15,6 +15,8 @@ if not os.path.exists(LIB_PATH):
     raise ImportError("libpmg.so not built: run `python paper_1808_03595_b200/build.py` "
                       "(or __graft_entry__.build()); there is no fallback implementation")
 
+import torch  # noqa: E402,F401  (load torch's NCCL before libpmg.so resolves libnccl.so.2)
+
 _lib = ctypes.CDLL(LIB_PATH)
 
 PMG_OK, PMG_EINVAL, PMG_ECUDA, PMG_ENCCL, PMG_ENOCONV, PMG_EBREAKDOWN, PMG_ENOMEM = 0, -1, -2, -3, -4, -5, -6
@@ -32,7 +34,16 @@ class Options(ctypes.Structure):
     _fields_ = [("p0", ctypes.c_int), ("weight_degree", ctypes.c_int), ("schedule", ctypes.c_int),
                 ("coarse_rtol", ctypes.c_double), ("coarse_maxit", ctypes.c_int),
                 ("coarse_check", ctypes.c_int), ("rank", ctypes.c_int), ("nranks", ctypes.c_int),
-                ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
+                ("nccl_id", ctypes.c_void_p), ("loopback", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
+
+
+class Slab(ctypes.Structure):
+    """pmg_slab: z-slab plan of one rank (include/pmg.h)."""
+    _fields_ = [("z0", ctypes.c_int), ("z1", ctypes.c_int), ("zb", ctypes.c_int), ("nplanes", ctypes.c_int),
+                ("own_lo", ctypes.c_int), ("own_hi", ctypes.c_int), ("lower", ctypes.c_int), ("upper", ctypes.c_int)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
 
 
 class Report(ctypes.Structure):
@@ -71,11 +82,19 @@ _lib.pmg_launch_count.restype = ctypes.c_longlong
 _lib.pmg_timing_enable.argtypes = [_P, ctypes.c_int]
 _lib.pmg_timing_read.argtypes = [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong)]
 _lib.pmg_timing_enable.restype = ctypes.c_int
+_lib.pmg_slab_plan.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(Slab)]
+_lib.pmg_slab_plan.restype = ctypes.c_int
+_lib.pmg_slab_info.argtypes = [_P, ctypes.POINTER(Slab)]
+_lib.pmg_nccl_unique_id.argtypes = [_P]
+_lib.pmg_loopback_create.argtypes = [ctypes.c_int]
+_lib.pmg_loopback_create.restype = _P
+_lib.pmg_loopback_destroy.argtypes = [_P]
+_lib.pmg_loopback_destroy.restype = None
 _lib.pmg_timing_read.restype = ctypes.c_int
 for _name in ("pmg_setup", "pmg_destroy", "pmg_level_info", "pmg_grid_coords", "pmg_residual", "pmg_smooth",
               "pmg_restrict", "pmg_prolong", "pmg_vcycle", "pmg_condense", "pmg_recover", "pmg_solve",
               "pmg_solve_host", "pmg_weak_rhs", "pmg_skel_from_grid", "pmg_skel_to_grid", "pmg_norm",
-              "pmg_num_levels"):
+              "pmg_num_levels", "pmg_slab_info", "pmg_nccl_unique_id"):
     getattr(_lib, _name).restype = ctypes.c_int
 
 
@@ -94,6 +113,35 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def slab_plan(k3, nranks, rank):
+    """z-slab plan of `rank` (pure host arithmetic of the library; no GPU needed)."""
+    sl = Slab()
+    if _lib.pmg_slab_plan(int(k3), int(nranks), int(rank), ctypes.byref(sl)) != 0:
+        raise PmgError(PMG_EINVAL, "invalid slab plan arguments")
+    return sl.as_dict()
+
+
+def nccl_unique_id():
+    """128-byte ncclUniqueId (bytes) for pmg_options.nccl_id; create on rank 0 and broadcast."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.pmg_nccl_unique_id(ctypes.cast(buf, _P)))
+    return buf.raw
+
+
+class Loopback:
+    """Hub shared by the contexts of one process that emulate nranks ranks (correctness tests)."""
+
+    def __init__(self, nranks):
+        self.h = _lib.pmg_loopback_create(int(nranks))
+        if not self.h:
+            raise PmgError(PMG_EINVAL, "pmg_loopback_create failed")
+
+    def close(self):
+        if self.h:
+            _lib.pmg_loopback_destroy(self.h)
+            self.h = None
+
+
 def default_options():
     o = Options()
     _lib.pmg_default_options(ctypes.byref(o))
@@ -104,11 +152,18 @@ class Solver:
     """One pmg context: the level hierarchy for (k, widths, p, lambda) on the current device."""
 
     def __init__(self, k, widths, p, lam, p0=2, schedule=0, coarse_rtol=1e-8, coarse_maxit=10000,
-                 coarse_check=8, stream=None):
+                 coarse_check=8, stream=None, rank=0, nranks=1, nccl_id=None, loopback=None):
         import numpy as np
         import torch
         o = default_options()
         o.p0, o.schedule, o.coarse_rtol, o.coarse_maxit, o.coarse_check = p0, schedule, coarse_rtol, coarse_maxit, coarse_check
+        o.rank, o.nranks = int(rank), int(nranks)
+        self._nccl_buf = None
+        if nccl_id is not None:
+            self._nccl_buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            o.nccl_id = ctypes.cast(self._nccl_buf, _P)
+        if loopback is not None:
+            o.loopback = loopback.h
         if stream is None:
             stream = torch.cuda.current_stream()
         self.stream = stream
@@ -122,6 +177,10 @@ class Solver:
         self._h = h
         self.p, self.lam = int(p), float(lam)
         self.nlevels = _lib.pmg_num_levels(h)
+        self.rank, self.nranks = int(rank), int(nranks)
+        sl = Slab()
+        _check(_lib.pmg_slab_info(h, ctypes.byref(sl)))
+        self.slab = sl.as_dict()
 
     def close(self):
         if getattr(self, "_h", None):
@@ -143,7 +202,8 @@ class Solver:
     def grid_coords(self, level, d):
         import numpy as np
         deg, _, _ = self.level_info(level)
-        x = np.zeros(self.k[d] * deg + 1)
+        nel = self.k[d] if d < 2 else self.slab["z1"] - self.slab["z0"]   # z: this rank's slab
+        x = np.zeros(nel * deg + 1)
         _check(_lib.pmg_grid_coords(self._h, level, d, x.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
         return x
 

@@ -7,7 +7,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpmg.so")
-SOURCES = ["setup_host.cpp", "kernels.cu", "hot_kernels.cu", "coarse_cg.cu", "pmg_api.cu"]
+SOURCES = ["setup_host.cpp", "comm.cpp", "kernels.cu", "hot_kernels.cu", "coarse_cg.cu", "pmg_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xptxas", "-v"]
@@ -44,7 +44,7 @@ def build(verbose=False, force=False):
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(o)
-    cmd = [_nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
+    cmd = [_nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -518,7 +518,8 @@ __global__ void __launch_bounds__(StarCfg<P>::NT) k_star_t(LevelGeom g, int c1, 
   extern __shared__ double sm[];
   const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
   const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
-  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 == 0 || v3 == g.k3)) return;
+  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 + g.zoff == 0 || v3 + g.zoff == g.K3)) return;
+  if (v3 < g.own_lo) return;   // ghost star below the slab: computed by the lower rank
   const int tid = threadIdx.x, ST = g.ST;
   const size_t row[3] = {(size_t)v1, (size_t)(g.V1 + v2), (size_t)(g.V1 + g.V2 + v3)};
   double* FT = sm + C::oFT;
@@ -685,7 +686,8 @@ __global__ void __launch_bounds__(StarSpCfg<P>::NT) k_star_sp(LevelGeom g, int c
   extern __shared__ double sm[];
   const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
   const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
-  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 == 0 || v3 == g.k3)) return;
+  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 + g.zoff == 0 || v3 + g.zoff == g.K3)) return;
+  if (v3 < g.own_lo) return;   // ghost star below the slab: computed by the lower rank
   const int tid = threadIdx.x, ST = g.ST;
   const size_t row[3] = {(size_t)v1, (size_t)(g.V1 + v2), (size_t)(g.V1 + g.V2 + v3)};
   double* FT = sm + C::oFT;
@@ -842,7 +844,8 @@ __global__ void __launch_bounds__(StarDmCfg<P>::NT) k_star_dm(LevelGeom g, int c
   extern __shared__ double sm[];
   const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
   const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
-  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 == 0 || v3 == g.k3)) return;
+  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 + g.zoff == 0 || v3 + g.zoff == g.K3)) return;
+  if (v3 < g.own_lo) return;   // ghost star below the slab: computed by the lower rank
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, ST = g.ST;
   const size_t row[3] = {(size_t)v1, (size_t)(g.V1 + v2), (size_t)(g.V1 + g.V2 + v3)};
   double* FT = sm + C::oFT;
@@ -971,26 +974,539 @@ __global__ void __launch_bounds__(StarDmCfg<P>::NT) k_star_dm(LevelGeom g, int c
 }
 
 // ------------------------------------------------------------------------------------------
+// star smoother, P <= 8, latency-oriented version of k_star_dm (same arithmetic, same citations):
+//   - every global load of the star (S rows, eigen/weight vectors, the three r planes, and the
+//     u values the star will update) is issued up front as cp.async (LDGSTS) into shared memory,
+//     so the whole gather costs one L2 round trip; the u prefetch turns the final read-modify-
+//     write into plain stores (the point sets of one colour are disjoint, so nobody
+//     else writes those u entries during the launch);
+//   - S^T is not loaded: the transposed operands read S with swapped indices;
+//   - the cross-group G3 partials are first reduced inside each warp with shuffles and then
+//     through the (idle) X buffer, so shared memory per CTA drops to ~37 KB at p = 8 and the
+//     launch bound admits 5 CTAs per SM: one colour of a 16^3 mesh (<= 729 stars) runs as a
+//     single wave on 148 SMs.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = valid ? 8 : 0;   // src-size 0: zero fill, no global access
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Compile-time point maps.  A skeleton point is addressed relative to a base record as
+//   bits 0-11: offset inside the record (face / edge / vertex slot, as skel_index_t),
+//   bits 12-14: record coordinate d is (base - 1) [star maps] or (base + 1) [element maps],
+//   bits 15-17: the point's local coordinate t_d inside that record is 0,
+// so the per-point index arithmetic of a gather / scatter is two multiply-adds instead of the
+// divisions and branches of skel_index_t.
+constexpr unsigned rec_slot(int m, int t1, int t2, int t3) {
+  if (t1 == 0) {
+    if (t2 == 0) return (t3 == 0) ? (unsigned)(3 * m * m + 3 * m) : (unsigned)(3 * m * m + 2 * m + t3 - 1);
+    if (t3 == 0) return (unsigned)(3 * m * m + m + t2 - 1);
+    return (unsigned)((t3 - 1) * m + (t2 - 1));
+  }
+  if (t2 == 0) return (t3 == 0) ? (unsigned)(3 * m * m + t1 - 1) : (unsigned)(m * m + (t3 - 1) * m + (t1 - 1));
+  return (unsigned)(2 * m * m + (t2 - 1) * m + (t1 - 1));
+}
+
+template <int P> struct StarMap { unsigned v[3 * (2 * P - 1) * (2 * P - 1)]; };
+// star plane d, position (A, B) of the (2p-1)^2 plane (A slow), relative to the star's vertex record
+template <int P> constexpr StarMap<P> make_star_map() {
+  StarMap<P> s{};
+  constexpr int N = 2 * P - 1, NN = N * N, c = P - 1, m = P - 1;
+  for (int i = 0; i < 3 * NN; ++i) {
+    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
+    int j[3] = {0, 0, 0};
+    if (d == 0) { j[0] = c; j[1] = B; j[2] = A; } else if (d == 1) { j[1] = c; j[0] = B; j[2] = A; } else { j[2] = c; j[0] = B; j[1] = A; }
+    int t[3] = {0, 0, 0};
+    unsigned code = 0;
+    for (int k = 0; k < 3; ++k) {
+      const int rel = j[k] - c;
+      if (rel < 0) { t[k] = P + rel; code |= 1u << (12 + k); } else { t[k] = rel; }
+      if (t[k] == 0) code |= 1u << (15 + k);
+    }
+    s.v[i] = code | rec_slot(m, t[0], t[1], t[2]);
+  }
+  return s;
+}
+template <int P> __device__ const StarMap<P> kStarMap = make_star_map<P>();
+
+template <int P> struct ElemMap { unsigned v[6 * (P - 1) * (P - 1) + 12 * (P - 1) + 8]; };
+// element boundary point o of the Y enumeration, relative to the element's low-corner record
+template <int P> constexpr ElemMap<P> make_elem_map() {
+  ElemMap<P> s{};
+  constexpr int M = P - 1, MM = M * M, YS = 6 * MM + 12 * M + 8;
+  for (int o = 0; o < YS; ++o) {
+    int t[3] = {0, 0, 0};
+    if (o < 6 * MM) {
+      const int f = o / MM, r = o - f * MM, A = r / M, B = r - A * M, d = f >> 1, sd = f & 1;
+      if (d == 0) { t[0] = sd * P; t[2] = A + 1; t[1] = B + 1; }
+      else if (d == 1) { t[1] = sd * P; t[2] = A + 1; t[0] = B + 1; }
+      else { t[2] = sd * P; t[1] = A + 1; t[0] = B + 1; }
+    } else if (o < 6 * MM + 12 * M) {
+      const int r = o - 6 * MM, qe = r / M, i = r - qe * M, d = qe >> 2, sA = qe & 1, sB = (qe >> 1) & 1;
+      if (d == 0) { t[0] = i + 1; t[1] = sA * P; t[2] = sB * P; }
+      else if (d == 1) { t[1] = i + 1; t[0] = sA * P; t[2] = sB * P; }
+      else { t[2] = i + 1; t[0] = sA * P; t[1] = sB * P; }
+    } else {
+      const int qv = o - 6 * MM - 12 * M;
+      t[0] = (qv & 1) * P; t[1] = ((qv >> 1) & 1) * P; t[2] = ((qv >> 2) & 1) * P;
+    }
+    unsigned code = 0;
+    for (int k = 0; k < 3; ++k)
+      if (t[k] == P) { t[k] = 0; code |= 1u << (12 + k); }
+    s.v[o] = code | rec_slot(M, t[0], t[1], t[2]);
+  }
+  return s;
+}
+template <int P> __device__ const ElemMap<P> kElemMap = make_elem_map<P>();
+
+// record-index delta of map code bits 12-14 (sign applied by the caller)
+__device__ __forceinline__ long long rec_delta(unsigned e, int V1, long long V12) {
+  return (long long)((e >> 12) & 1u) + (long long)V1 * ((e >> 13) & 1u) + V12 * ((e >> 14) & 1u);
+}
+
+// C = op(A) op(B) for NP x NP shared-memory matrices (leading dimension LD), one warp, tile (mi, ni);
+// TA / TB: read A / B transposed (A[i][k] = As[k][i], B[k][j] = Bs[j][k])
+template <int NP, int LD, bool TA, bool TB>
+__device__ __forceinline__ void dmma_tile_t(const double* A, const double* B, double* Cm, int mi, int ni, int lane) {
+  const int r = lane >> 2, q = lane & 3;
+  double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < NP / 4; ++kk) {
+    const int i = 8 * mi + r, k = 4 * kk + q, j = 8 * ni + r;
+    const double a = TA ? A[k * LD + i] : A[i * LD + k];
+    const double b = TB ? B[j * LD + k] : B[k * LD + j];
+    dmma884(c0, c1, a, b);
+  }
+  Cm[(8 * mi + r) * LD + 8 * ni + 2 * q] = c0;
+  Cm[(8 * mi + r) * LD + 8 * ni + 2 * q + 1] = c1;
+}
+
+template <int P> struct StarPfCfg {
+  static constexpr int N = 2 * P - 1, NN = N * N, C = P - 1;
+  static constexpr int NP = (N <= 8) ? 8 : 16, LD = NP + 4, MS = NP * LD, TPP = (NP / 8) * (NP / 8);
+  static constexpr int NW = 4, NT = 128, MINB = 5;
+  static constexpr int GS = NP, GPW = 32 / GS, NG = NW * GPW, A3IT = (N + NG - 1) / NG;
+  static constexpr int oFT = 0, oX = 3 * MS, oG = 6 * MS, oS = 9 * MS, oU = 12 * MS, oVec = oU + 3 * NN,
+                       total = oVec + 9 * N;
+  static_assert(NW * NN <= 3 * MS, "G3 warp partials must fit in the X buffer");
+};
+
+template <int P>
+size_t star_pf_smem() { return sizeof(double) * StarPfCfg<P>::total; }
+
+template <int P>
+__global__ void __launch_bounds__(StarPfCfg<P>::NT, StarPfCfg<P>::MINB)
+    k_star_pf(LevelGeom g, int c1, int c2, int c3, int n1c, int n2c, const double* __restrict__ r,
+              double* __restrict__ u, const double* __restrict__ stab, double lam) {
+  using C = StarPfCfg<P>;
+  constexpr int N = C::N, NN = C::NN, c = C::C, NT = C::NT, NP = C::NP, LD = C::LD, MS = C::MS;
+  constexpr int GS = C::GS, GPW = C::GPW, NG = C::NG;
+  extern __shared__ double sm[];
+  const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
+  const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
+  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 + g.zoff == 0 || v3 + g.zoff == g.K3)) return;
+  if (v3 < g.own_lo) return;   // ghost star below the slab: computed by the lower rank
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, ST = g.ST;
+  const size_t row[3] = {(size_t)v1, (size_t)(g.V1 + v2), (size_t)(g.V1 + g.V2 + v3)};
+  double* FT = sm + C::oFT;
+  double* X = sm + C::oX;
+  double* Gs = sm + C::oG;
+  double* Ssm = sm + C::oS;
+  double* Up = sm + C::oU;
+  double* vec = sm + C::oVec;
+  constexpr int RS = 3 * (P - 1) * (P - 1) + 3 * (P - 1) + 1;
+  const long long V12 = (long long)g.V1 * g.V2;
+  const long long rec0 = v1 + g.V1 * (long long)v2 + V12 * v3;
+  // interior stars (the common case) touch only inside, free points: no per-point tests
+  const bool interior = v1 > 0 && v2 > 0 && v3 > 0 && v1 < g.k1 && v2 < g.k2 && v3 + g.zoff < g.K3;
+  const StarMap<P>& map = kStarMap<P>;
+  // point of map entry e: record coordinate w_d = v_d - bit; inside the stored box iff w_d >= 0,
+  // free iff (w_d > 0 or t_d > 0) and w_d < k_d
+  auto pt_inside = [&](unsigned e) {
+    return !((v1 == 0 && (e & (1u << 12))) || (v2 == 0 && (e & (1u << 13))) || (v3 == 0 && (e & (1u << 14))));
+  };
+  auto pt_free = [&](unsigned e) {   // global test; w3 + zoff is the global record plane
+    const int w1 = v1 - (int)((e >> 12) & 1u), w2 = v2 - (int)((e >> 13) & 1u), w3 = v3 - (int)((e >> 14) & 1u);
+    const int W3 = w3 + g.zoff;
+    return w1 >= 0 && w2 >= 0 && w3 >= 0 && (w1 > 0 || !(e & (1u << 15))) && (w2 > 0 || !(e & (1u << 16))) &&
+           (W3 > 0 || !(e & (1u << 17))) && w1 < g.k1 && w2 < g.k2 && W3 < g.K3;
+  };
+  auto pt_index = [&](unsigned e) { return (rec0 - rec_delta(e, g.V1, V12)) * RS + (e & 0xFFFu); };
+  // group 0: S (padded with zeros), eigen/weight vectors, r planes (zero outside the box / padding)
+  for (int i = tid; i < 3 * NP * NP; i += NT) {
+    const int d = i / (NP * NP), rr = i - d * NP * NP, A = rr / NP, B = rr - A * NP;
+    const bool in = A < N && B < N;
+    cp_async8(&Ssm[d * MS + A * LD + B], &stab[row[d] * ST + (in ? A * N + B : 0)], in);
+    const unsigned e = in ? map.v[d * NN + A * N + B] : 0u;
+    const bool ok = in && (interior || pt_inside(e));
+    cp_async8(&FT[d * MS + A * LD + B], &r[ok ? pt_index(e) : 0], ok);
+  }
+  for (int i = tid; i < 9 * N; i += NT) { const int d = i / (3 * N); cp_async8(&vec[i], &stab[row[d] * ST + NN + i - d * 3 * N], true); }
+  cp_async_commit();
+  // group 1: the u entries this star updates (0 where the point is not free)
+  for (int i = tid; i < 3 * NN; i += NT) {
+    const unsigned e = map.v[i];
+    const bool ok = interior || pt_free(e);
+    cp_async8(&Up[i], &u[ok ? pt_index(e) : 0], ok);
+  }
+  cp_async_commit();
+  // zero G (the padding must be finite for the back transforms)
+  for (int i = tid; i < 3 * MS; i += NT) Gs[i] = 0.0;
+  cp_async_wait<1>();
+  __syncthreads();
+  // inverse multiplicity on the two lines through the vertex of each plane
+  for (int i = tid; i < 3 * 2 * N; i += NT) {
+    const int d = i / (2 * N), rr = i - d * 2 * N, line = rr / N, t = rr - line * N;
+    const int A = line ? t : c, B = line ? c : t;
+    if (line && t == c) continue;     // the vertex itself: scaled once, by the row pass
+    FT[d * MS + A * LD + B] *= 1.0 / (double)(1 + (A == c) + (B == c));
+  }
+  __syncthreads();
+  // forward: X_d = F_d S_a ; T_d = S_b^T X_d
+  for (int job = warp; job < 3 * C::TPP; job += C::NW) {
+    const int d = job / C::TPP, t = job - d * C::TPP, mi = t / (NP / 8), ni = t - mi * (NP / 8);
+    dmma_tile_t<NP, LD, false, false>(FT + d * MS, Ssm + (d == 0 ? 1 : 0) * MS, X + d * MS, mi, ni, lane);
+  }
+  __syncthreads();
+  for (int job = warp; job < 3 * C::TPP; job += C::NW) {
+    const int d = job / C::TPP, t = job - d * C::TPP, mi = t / (NP / 8), ni = t - mi * (NP / 8);
+    dmma_tile_t<NP, LD, true, false>(Ssm + (d == 2 ? 1 : 2) * MS, X + d * MS, FT + d * MS, mi, ni, lane);
+  }
+  __syncthreads();
+  // single-pass core (as k_star_dm); G3 partials reduced in-warp, then across warps through X
+  {
+    const double *L1 = vec, *s1 = vec + N, *L2 = vec + 3 * N, *s2 = vec + 4 * N, *L3 = vec + 6 * N, *s3 = vec + 7 * N;
+    const double *T1 = FT, *T2 = FT + MS, *T3 = FT + 2 * MS;
+    const int grp = warp * GPW + lane / GS, a1 = lane % GS;
+    const bool va = a1 < N;
+    const int a1c = va ? a1 : 0;
+    const double s1a = va ? s1[a1c] : 0.0, L1a = L1[a1c];
+    double g3[N];
+#pragma unroll
+    for (int a2 = 0; a2 < N; ++a2) g3[a2] = 0.0;
+    for (int k = 0; k < C::A3IT; ++k) {
+      const int a3 = grp + k * NG;
+      const bool act = a3 < N;
+      const int a3c = act ? a3 : 0;
+      const double on = (act && va) ? 1.0 : 0.0;
+      const double t2 = on * T2[a3c * LD + a1c], s3v = on * s3[a3c], base = lam + L1a + L3[a3c];
+      const double s1v = on * s1a;
+      double g2 = 0.0;
+      double v[GS];
+#pragma unroll
+      for (int a2 = 0; a2 < GS; ++a2) v[a2] = 0.0;
+#pragma unroll
+      for (int a2 = 0; a2 < N; ++a2) {
+        double E = s1v * T1[a3c * LD + a2];
+        E = fma(s2[a2], t2, E);
+        E = fma(s3v, T3[a2 * LD + a1c], E);
+        const double V = E * rcp_nr(base + L2[a2]);
+        g2 = fma(s2[a2], V, g2);
+        g3[a2] = fma(s3v, V, g3[a2]);
+        v[a2] = s1v * V;
+      }
+#pragma unroll
+      for (int off = GS / 2; off >= 1; off >>= 1) {
+        const bool upper = (a1 & off) != 0;
+#pragma unroll
+        for (int j = 0; j < off; ++j) {
+          const double send = upper ? v[j] : v[j + off];
+          const double keep = upper ? v[j + off] : v[j];
+          v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      if (act && va) {
+        Gs[a3 * LD + a1] = v[0];               // G1[a3][a2 = a1]
+        Gs[MS + a3 * LD + a1] = g2;            // G2[a3][a1]
+      }
+    }
+#pragma unroll
+    for (int off = GS; off < 32; off <<= 1) {
+#pragma unroll
+      for (int a2 = 0; a2 < N; ++a2) g3[a2] += __shfl_xor_sync(0xffffffffu, g3[a2], off);
+    }
+    if (va && lane < GS) {
+#pragma unroll
+      for (int a2 = 0; a2 < N; ++a2) X[warp * NN + a2 * N + a1] = g3[a2];
+    }
+    __syncthreads();
+    for (int i = tid; i < NN; i += NT) {
+      const int a2 = i / N, a1_ = i - a2 * N;
+      double s_ = 0.0;
+#pragma unroll
+      for (int w = 0; w < C::NW; ++w) s_ += X[w * NN + i];
+      Gs[2 * MS + a2 * LD + a1_] = s_;
+    }
+  }
+  __syncthreads();
+  // back: X_d = G_d S_a^T ; U_d = S_b X_d (into G)
+  for (int job = warp; job < 3 * C::TPP; job += C::NW) {
+    const int d = job / C::TPP, t = job - d * C::TPP, mi = t / (NP / 8), ni = t - mi * (NP / 8);
+    dmma_tile_t<NP, LD, false, true>(Gs + d * MS, Ssm + (d == 0 ? 1 : 0) * MS, X + d * MS, mi, ni, lane);
+  }
+  __syncthreads();
+  for (int job = warp; job < 3 * C::TPP; job += C::NW) {
+    const int d = job / C::TPP, t = job - d * C::TPP, mi = t / (NP / 8), ni = t - mi * (NP / 8);
+    dmma_tile_t<NP, LD, false, false>(Ssm + (d == 2 ? 1 : 2) * MS, X + d * MS, Gs + d * MS, mi, ni, lane);
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  const double *w1 = vec + 2 * N, *w2 = vec + 5 * N, *w3 = vec + 8 * N;
+  for (int i = tid; i < 3 * NN; i += NT) {
+    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
+    int j1, j2, j3;
+    if (d == 0) { j1 = c; j2 = B; j3 = A; }
+    else if (d == 1) { j2 = c; j1 = B; j3 = A; if (j1 == c) continue; }
+    else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
+    const unsigned e = map.v[i];
+    if (!interior && !pt_free(e)) continue;
+    u[pt_index(e)] = fma(w1[j1] * w2[j2] * w3[j3], Gs[d * MS + A * LD + B], Up[i]);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// element operator for P <= 8, latency-oriented version of k_elem_dm (same arithmetic and
+// citations: P:117-123, reading R1):
+//   - one cp.async pass stages the element's three table rows (contiguous in etab) and its
+//     (p+1)^3 - (p-1)^3 boundary values -- scattered straight into a zero-interior (p+1)^3 cube --
+//     so the gather is one L2 round trip with no index decoding of the table layout;
+//   - H_BB u is then three plain line sums through the cube for every output (the zero interior
+//     makes the edge / vertex / face cases identical, no branches);
+//   - only the padded P_d is built; the transposed operands of the DMMA transforms read it with
+//     swapped indices.
+// ------------------------------------------------------------------------------------------
+template <int P> struct ElemPfCfg {
+  static constexpr int M = P - 1, Q = P + 1, MM = M * M, QQ = Q * Q, QQQ = Q * QQ, MP = 8, LD = 12, MS = MP * LD;
+  static constexpr int NT = 128, NW = 4, MINB = 8;
+  static constexpr int ET = (P - 1) + 2 * (P - 1) * (P - 1) + 2 * (P - 1) + (P + 1) + (P + 1) * (P + 1);
+  static constexpr int YS = 6 * MM + 12 * M + 8;
+  static constexpr int oCube = 0, oTab = QQQ, oPp = oTab + 3 * ET, oA = oPp + 3 * MS, oT = oA + 6 * MS,
+                       oG = oT + 6 * MS, oInv = oG + 6 * MS, total = oInv + MM * M;
+};
+
+template <int P>
+size_t elem_pf_smem() { return sizeof(double) * ElemPfCfg<P>::total; }
+
+// boundary point o (0 <= o < YS) of the element in the Y enumeration -> local (t1, t2, t3)
+template <int P>
+__device__ __forceinline__ void ys_point(int o, int& t1, int& t2, int& t3) {
+  constexpr int M = P - 1, MM = M * M;
+  if (o < 6 * MM) {
+    const int f = o / MM, r = o - f * MM, A = r / M, B = r - A * M, d = f >> 1, s = f & 1;
+    if (d == 0) { t1 = s * P; t3 = A + 1; t2 = B + 1; }
+    else if (d == 1) { t2 = s * P; t3 = A + 1; t1 = B + 1; }
+    else { t3 = s * P; t2 = A + 1; t1 = B + 1; }
+  } else if (o < 6 * MM + 12 * M) {
+    const int r = o - 6 * MM, qe = r / M, i = r - qe * M, d = qe >> 2, sA = qe & 1, sB = (qe >> 1) & 1;
+    if (d == 0) { t1 = i + 1; t2 = sA * P; t3 = sB * P; }
+    else if (d == 1) { t2 = i + 1; t1 = sA * P; t3 = sB * P; }
+    else { t3 = i + 1; t1 = sA * P; t2 = sB * P; }
+  } else {
+    const int qv = o - 6 * MM - 12 * M;
+    t1 = (qv & 1) * P; t2 = ((qv >> 1) & 1) * P; t3 = ((qv >> 2) & 1) * P;
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(ElemPfCfg<P>::NT, ElemPfCfg<P>::MINB)
+    k_elem_pf(LevelGeom g, const double* __restrict__ u, const double* __restrict__ etab, double lam,
+              double* __restrict__ Y, const int* __restrict__ done) {
+  using C = ElemPfCfg<P>;
+  constexpr int M = C::M, Q = C::Q, MM = C::MM, QQ = C::QQ, QQQ = C::QQQ, NT = C::NT, ET = C::ET, LD = C::LD,
+                MS = C::MS, MP = C::MP, YS = C::YS;
+  if (done && *done) return;
+  extern __shared__ double sm[];
+  double* cube = sm + C::oCube;
+  double* tb = sm + C::oTab;
+  double* Pp = sm + C::oPp;
+  double* Ab = sm + C::oA;
+  double* T = sm + C::oT;
+  double* G = sm + C::oG;
+  double* invD = sm + C::oInv;
+  const long long e = blockIdx.x;
+  const int e1 = (int)(e % g.k1), e2 = (int)((e / g.k1) % g.k2), e3 = (int)(e / ((long long)g.k1 * g.k2));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {
+    const double* src[3] = {etab + (size_t)e1 * ET, etab + (size_t)(g.k1 + e2) * ET, etab + (size_t)(g.k1 + g.k2 + e3) * ET};
+    for (int i = tid; i < 3 * ET; i += NT) {
+      const int d = i / ET;
+      cp_async8(&tb[i], src[d] + (i - d * ET), true);
+    }
+    constexpr int RS = 3 * MM + 3 * M + 1;
+    const long long V12 = (long long)g.V1 * g.V2;
+    const long long rec0 = e1 + g.V1 * (long long)e2 + V12 * e3;
+    for (int o = tid; o < YS; o += NT) {
+      int t1, t2, t3;
+      ys_point<P>(o, t1, t2, t3);
+      const unsigned m_ = kElemMap<P>.v[o];
+      cp_async8(&cube[(t3 * Q + t2) * Q + t1], &u[(rec0 + rec_delta(m_, g.V1, V12)) * RS + (m_ & 0xFFFu)], true);
+    }
+    cp_async_commit();
+    for (int i = tid; i < M * MM; i += NT) {        // zero interior of the cube
+      const int a3 = i / MM, rr = i - a3 * MM, a2 = rr / M, a1 = rr - a2 * M;
+      cube[((a3 + 1) * Q + a2 + 1) * Q + a1 + 1] = 0.0;
+    }
+    for (int i = tid; i < 6 * MS; i += NT) G[i] = 0.0;
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+  const double* Lv[3] = {tb + et_lam(P), tb + ET + et_lam(P), tb + 2 * ET + et_lam(P)};
+  for (int i = tid; i < 3 * MP * MP; i += NT) {     // padded P_d[b][i]
+    const int d = i / (MP * MP), rr = i - d * MP * MP, A = rr / MP, B = rr - A * MP;
+    Pp[d * MS + A * LD + B] = (A < M && B < M) ? tb[d * ET + et_P(P) + A * M + B] : 0.0;
+  }
+  for (int i = tid; i < 6 * MP * MP; i += NT) {     // padded face interiors from the cube
+    const int f = i / (MP * MP), rr = i - f * MP * MP, A = rr / MP, B = rr - A * MP, d = f >> 1, sd = (f & 1) * P;
+    double v = 0.0;
+    if (A < M && B < M) {
+      const int t = (d == 0) ? ((A + 1) * Q + B + 1) * Q + sd : ((d == 1) ? ((A + 1) * Q + sd) * Q + B + 1 : (sd * Q + A + 1) * Q + B + 1);
+      v = cube[t];
+    }
+    Ab[f * MS + A * LD + B] = v;
+  }
+  for (int i = tid; i < MM * M; i += NT) {          // 1/D over the interior eigen-triples
+    const int b3 = i / MM, rr = i - b3 * MM, b2 = rr / M, b1 = rr - b2 * M;
+    invD[i] = rcp_nr(lam + Lv[0][b1] + Lv[1][b2] + Lv[2][b3]);
+  }
+  __syncthreads();
+  for (int f = warp; f < 6; f += C::NW) {            // forward A: X_f = U_f P_a^T  (into T)
+    const int d = f >> 1, da = (d == 0) ? 1 : 0;
+    dmma_tile_t<MP, LD, false, true>(Ab + f * MS, Pp + da * MS, T + f * MS, 0, 0, lane);
+  }
+  __syncthreads();
+  for (int f = warp; f < 6; f += C::NW) {            // forward B: T_f = P_b X_f  (into Ab)
+    const int d = f >> 1, db = (d == 2) ? 1 : 2;
+    dmma_tile_t<MP, LD, false, false>(Pp + db * MS, T + f * MS, Ab + f * MS, 0, 0, lane);
+  }
+  __syncthreads();
+  {
+    const double *a10 = tb + et_a0(P), *a11 = tb + et_a1(P);
+    const double *a20 = tb + ET + et_a0(P), *a21 = tb + ET + et_a1(P);
+    const double *a30 = tb + 2 * ET + et_a0(P), *a31 = tb + 2 * ET + et_a1(P);
+    const double *T0 = Ab, *T1 = Ab + MS, *T2 = Ab + 2 * MS, *T3 = Ab + 3 * MS, *T4 = Ab + 4 * MS, *T5 = Ab + 5 * MS;
+    for (int i = tid; i < 3 * MM; i += NT) {
+      const int pass = i / MM, r = i - pass * MM, hi = r / M, lo = r - hi * M;
+      double g0 = 0.0, g1 = 0.0;
+      if (pass == 0) {          // (b3, b2), reduce over b1 -> faces 0, 1
+        const int b3 = hi, b2 = lo;
+        const double tA = T0[b3 * LD + b2], tB = T1[b3 * LD + b2], c2 = a20[b2], c2b = a21[b2], c3 = a30[b3], c3b = a31[b3];
+#pragma unroll
+        for (int b1 = 0; b1 < M; ++b1) {
+          double Ev = a10[b1] * tA;
+          Ev = fma(a11[b1], tB, Ev);
+          Ev = fma(c2, T2[b3 * LD + b1], Ev);
+          Ev = fma(c2b, T3[b3 * LD + b1], Ev);
+          Ev = fma(c3, T4[b2 * LD + b1], Ev);
+          Ev = fma(c3b, T5[b2 * LD + b1], Ev);
+          const double V = Ev * invD[(b3 * M + b2) * M + b1];
+          g0 = fma(a10[b1], V, g0);
+          g1 = fma(a11[b1], V, g1);
+        }
+        G[0 * MS + b3 * LD + b2] = g0;
+        G[1 * MS + b3 * LD + b2] = g1;
+      } else if (pass == 1) {   // (b3, b1), reduce over b2 -> faces 2, 3
+        const int b3 = hi, b1 = lo;
+        const double tA = T2[b3 * LD + b1], tB = T3[b3 * LD + b1], c1 = a10[b1], c1b = a11[b1], c3 = a30[b3], c3b = a31[b3];
+#pragma unroll
+        for (int b2 = 0; b2 < M; ++b2) {
+          double Ev = c1 * T0[b3 * LD + b2];
+          Ev = fma(c1b, T1[b3 * LD + b2], Ev);
+          Ev = fma(a20[b2], tA, Ev);
+          Ev = fma(a21[b2], tB, Ev);
+          Ev = fma(c3, T4[b2 * LD + b1], Ev);
+          Ev = fma(c3b, T5[b2 * LD + b1], Ev);
+          const double V = Ev * invD[(b3 * M + b2) * M + b1];
+          g0 = fma(a20[b2], V, g0);
+          g1 = fma(a21[b2], V, g1);
+        }
+        G[2 * MS + b3 * LD + b1] = g0;
+        G[3 * MS + b3 * LD + b1] = g1;
+      } else {                  // (b2, b1), reduce over b3 -> faces 4, 5
+        const int b2 = hi, b1 = lo;
+        const double tA = T4[b2 * LD + b1], tB = T5[b2 * LD + b1], c1 = a10[b1], c1b = a11[b1], c2 = a20[b2], c2b = a21[b2];
+#pragma unroll
+        for (int b3 = 0; b3 < M; ++b3) {
+          double Ev = c1 * T0[b3 * LD + b2];
+          Ev = fma(c1b, T1[b3 * LD + b2], Ev);
+          Ev = fma(c2, T2[b3 * LD + b1], Ev);
+          Ev = fma(c2b, T3[b3 * LD + b1], Ev);
+          Ev = fma(a30[b3], tA, Ev);
+          Ev = fma(a31[b3], tB, Ev);
+          const double V = Ev * invD[(b3 * M + b2) * M + b1];
+          g0 = fma(a30[b3], V, g0);
+          g1 = fma(a31[b3], V, g1);
+        }
+        G[4 * MS + b2 * LD + b1] = g0;
+        G[5 * MS + b2 * LD + b1] = g1;
+      }
+    }
+  }
+  __syncthreads();
+  for (int f = warp; f < 6; f += C::NW) {            // back A: X_f = G_f P_a   (into T)
+    const int d = f >> 1, da = (d == 0) ? 1 : 0;
+    dmma_tile_t<MP, LD, false, false>(G + f * MS, Pp + da * MS, T + f * MS, 0, 0, lane);
+  }
+  __syncthreads();
+  for (int f = warp; f < 6; f += C::NW) {            // back B: C_f = P_b^T X_f  (into G)
+    const int d = f >> 1, db = (d == 2) ? 1 : 2;
+    dmma_tile_t<MP, LD, true, false>(Pp + db * MS, T + f * MS, G + f * MS, 0, 0, lane);
+  }
+  __syncthreads();
+  const double *M1 = tb + et_M(P), *M2 = tb + ET + et_M(P), *M3 = tb + 2 * ET + et_M(P);
+  const double *K1 = tb + et_K(P), *K2 = tb + ET + et_K(P), *K3 = tb + 2 * ET + et_K(P);
+  double* Ye = Y + (size_t)e * g.YS;
+  for (int o = tid; o < YS; o += NT) {
+    int t1, t2, t3;
+    ys_point<P>(o, t1, t2, t3);
+    const double* c1 = cube + (t3 * Q + t2) * Q;     // line along x1
+    const double* c2 = cube + t3 * QQ + t1;          // line along x2 (stride Q)
+    const double* c3 = cube + t2 * Q + t1;           // line along x3 (stride QQ)
+    double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int t = 0; t <= P; ++t) {
+      s1 = fma(K1[t1 * Q + t], c1[t], s1);
+      s2 = fma(K2[t2 * Q + t], c2[t * Q], s2);
+      s3 = fma(K3[t3 * Q + t], c3[t * QQ], s3);
+    }
+    const double m1 = M1[t1], m2 = M2[t2], m3 = M3[t3];
+    double y = lam * m1 * m2 * m3 * c1[t1];
+    y = fma(m2 * m3, s1, y);
+    y = fma(m1 * m3, s2, y);
+    y = fma(m1 * m2, s3, y);
+    if (o < 6 * MM) {
+      const int f = o / MM, r = o - f * MM, A = r / M, B = r - A * M;
+      y -= G[f * MS + A * LD + B];
+    }
+    Ye[o] = y;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // dispatch
 // ------------------------------------------------------------------------------------------
 constexpr bool kStarSinglePass(int p) { return p <= 8; }
 
-// star kernel variant for p <= 8 (A/B experiments): 0 DMMA transforms (default), 1 DFMA transforms
+// star kernel variant for p <= 8 (A/B experiments): 0 prefetching DMMA kernel k_star_pf (default),
+// 1 DFMA transforms (k_star_sp), 2 DMMA transforms without prefetch (k_star_dm)
 static int star_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("PMG_STAR_VARIANT");
-    v = (e && e[0] == '1') ? 1 : 0;
+    v = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 0;
   }
   return v;
 }
 
-// element kernel variant for p <= 8: 0 DMMA transforms + 1/D table (default), 1 DFMA (k_elem_apply_t)
+// element kernel variant for p <= 8: 0 k_elem_pf (default), 1 DFMA (k_elem_apply_t), 2 k_elem_dm
 static int elem_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("PMG_ELEM_VARIANT");
-    v = (e && e[0] == '1') ? 1 : 0;
+    v = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 0;
   }
   return v;
 }
@@ -999,7 +1515,12 @@ template <int P>
 void launch_elem_p(const LevelGeom& g, const double* u, const double* etab, double lam, double* Y, const int* done,
                    cudaStream_t st) {
   if constexpr (P <= 8) {
-    if (elem_variant() == 0) {
+    const int v = elem_variant();
+    if (v == 0) {
+      k_elem_pf<P><<<(unsigned)g.nelem, ElemPfCfg<P>::NT, elem_pf_smem<P>(), st>>>(g, u, etab, lam, Y, done);
+      return;
+    }
+    if (v == 2) {
       k_elem_dm<P><<<(unsigned)g.nelem, ElemDmCfg<P>::NT, elem_dm_smem<P>(), st>>>(g, u, etab, lam, Y, done);
       return;
     }
@@ -1011,7 +1532,10 @@ template <int P>
 void launch_star_p(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c, long long nb, const double* r,
                    double* u, const double* stab, const double* stabT, double lam, cudaStream_t st) {
   if constexpr (kStarSinglePass(P)) {
-    if (star_variant() == 0)
+    const int v = star_variant();
+    if (v == 0)
+      k_star_pf<P><<<(unsigned)nb, StarPfCfg<P>::NT, star_pf_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, lam);
+    else if (v == 2)
       k_star_dm<P><<<(unsigned)nb, StarDmCfg<P>::NT, star_dm_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
     else
       k_star_sp<P><<<(unsigned)nb, StarSpCfg<P>::NT, star_sp_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
@@ -1053,7 +1577,7 @@ cudaError_t launch_star(const LevelGeom& g, int c1, int c2, int c3, int n1c, int
 size_t hot_smem(int p, int which) {
   switch (p) {
 #define CASE(P) \
-  case P: return which == 0 ? std::max(elem_t_smem<P>(), elem_dm_smem<(P <= 8 ? P : 2)>()) : (kStarSinglePass(P) ? std::max(star_sp_smem<(P <= 8 ? P : 2)>(), star_dm_smem<(P <= 8 ? P : 2)>()) : star_t_smem<P>());
+  case P: return which == 0 ? std::max(elem_t_smem<P>(), std::max(elem_dm_smem<(P <= 8 ? P : 2)>(), elem_pf_smem<(P <= 8 ? P : 2)>())) : (kStarSinglePass(P) ? std::max(std::max(star_sp_smem<(P <= 8 ? P : 2)>(), star_dm_smem<(P <= 8 ? P : 2)>()), star_pf_smem<(P <= 8 ? P : 2)>()) : star_t_smem<P>());
     PMG_DEGREES(CASE)
 #undef CASE
     default: return 0;
@@ -1067,11 +1591,15 @@ cudaError_t hot_set_smem_attr(int bytes) {
     cudaError_t a = cudaFuncSetAttribute(k_elem_apply_t<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (a == cudaSuccess && P <= 8)                                                                    \
       a = cudaFuncSetAttribute(k_elem_dm<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+    if (a == cudaSuccess && P <= 8)                                                                    \
+      a = cudaFuncSetAttribute(k_elem_pf<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     cudaError_t b = cudaFuncSetAttribute(k_star_t<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);       \
     if (b == cudaSuccess && kStarSinglePass(P))                                                        \
       b = cudaFuncSetAttribute(k_star_sp<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (b == cudaSuccess && kStarSinglePass(P))                                                        \
       b = cudaFuncSetAttribute(k_star_dm<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+    if (b == cudaSuccess && kStarSinglePass(P))                                                        \
+      b = cudaFuncSetAttribute(k_star_pf<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (a != cudaSuccess) e = a;                                                                       \
     if (b != cudaSuccess) e = b;                                                                       \
   }

@@ -56,7 +56,7 @@ __global__ void k_weak_rhs(LevelGeom g, const double* __restrict__ b1, const dou
     int i1 = (int)(idx % N1);
     long long r = idx / N1;
     int i2 = (int)(r % N2), i3 = (int)(r / N2);
-    F[idx] = is_free(g, i1, i2, i3) ? b3[i3] * b2[i2] * b1[i1] * f[idx] : 0.0;
+    F[idx] = is_free(g, i1, i2, i3) ? b3[i3 + g.zoff * g.p] * b2[i2] * b1[i1] * f[idx] : 0.0;   // b3: global line
   }
 }
 
@@ -249,7 +249,7 @@ __global__ void k_gather_resid(LevelGeom g, const double* __restrict__ Y, const 
        idx += (long long)gridDim.x * blockDim.x) {
     Entry E = decode_entry(g, idx);
     double r = 0.0;
-    if (is_free(g, E.g1, E.g2, E.g3)) {
+    if (is_free(g, E.g1, E.g2, E.g3) && owned_plane(g, E.v3)) {
       double s = 0.0;
       auto el = [&](int a1, int a2, int a3) -> size_t {
         return ((size_t)a1 + (size_t)g.k1 * ((size_t)a2 + (size_t)g.k2 * a3)) * YS;
@@ -301,7 +301,8 @@ __global__ void __launch_bounds__(256) k_star(LevelGeom g, int c1, int c2, int c
   const int p = g.p, n = g.n, c = p - 1, nn = n * n, ST = g.ST;
   const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
   const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
-  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 == 0 || v3 == g.k3)) return;  // corner
+  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 + g.zoff == 0 || v3 + g.zoff == g.K3)) return;  // corner
+  if (v3 < g.own_lo) return;   // ghost star below the slab: computed by the lower rank
   const int tid = threadIdx.x, nt = blockDim.x;
   const double* gt[3] = {stab + (size_t)v1 * ST, stab + (size_t)(g.V1 + v2) * ST, stab + (size_t)(g.V1 + g.V2 + v3) * ST};
   double* FT = sm;
@@ -466,7 +467,7 @@ __global__ void k_restrict_gather(LevelGeom gc, const double* __restrict__ Z, do
        idx += (long long)gridDim.x * blockDim.x) {
     Entry E = decode_entry(gc, idx);
     double s = 0.0;
-    if (is_free(gc, E.g1, E.g2, E.g3)) {
+    if (is_free(gc, E.g1, E.g2, E.g3) && owned_plane(gc, E.v3)) {
       const int G[3] = {E.g1, E.g2, E.g3};
       const int K[3] = {gc.k1, gc.k2, gc.k3};
       int cand[3][2], nc[3];
@@ -696,7 +697,7 @@ __global__ void k_condense_gather(LevelGeom g, const double* __restrict__ Fg, co
        idx += (long long)gridDim.x * blockDim.x) {
     Entry E = decode_entry(g, idx);
     double r = 0.0;
-    if (is_free(g, E.g1, E.g2, E.g3)) {
+    if (is_free(g, E.g1, E.g2, E.g3) && owned_plane(g, E.v3)) {
       r = Fg[E.g1 + N1 * (E.g2 + N2 * (long long)E.g3)];
       if (E.type < 3) {
         const int d = E.type, o = E.a * m + E.b;

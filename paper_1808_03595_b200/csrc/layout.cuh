@@ -53,9 +53,13 @@ __device__ __forceinline__ long long skel_index_t(const LevelGeom& g, int g1, in
 __device__ __forceinline__ bool inside(const LevelGeom& g, int g1, int g2, int g3) {
   return g1 >= 0 && g2 >= 0 && g3 >= 0 && g1 <= g.k1 * g.p && g2 <= g.k2 * g.p && g3 <= g.k3 * g.p;
 }
+// free unknown: strictly inside the GLOBAL box (g3 is local; the slab starts at vertex plane zoff)
 __device__ __forceinline__ bool is_free(const LevelGeom& g, int g1, int g2, int g3) {
-  return g1 > 0 && g2 > 0 && g3 > 0 && g1 < g.k1 * g.p && g2 < g.k2 * g.p && g3 < g.k3 * g.p;
+  const int G3 = g3 + g.zoff * g.p;
+  return g1 > 0 && g2 > 0 && G3 > 0 && g1 < g.k1 * g.p && g2 < g.k2 * g.p && G3 < g.K3 * g.p;
 }
+// record plane v3 (local) carries element-gathered values on this rank
+__device__ __forceinline__ bool owned_plane(const LevelGeom& g, int v3) { return v3 >= g.own_lo && v3 < g.own_hi; }
 
 // Skeleton-vector entry -> record vertex, entity type (0-2 faces, 3-5 edges, 6 vertex),
 // local indices (a = slow, b = fast for faces; a for edges) and global point.

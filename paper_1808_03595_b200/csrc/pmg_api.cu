@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/pmg.h"
+#include "comm.h"
 #include "kernels.cuh"
 #include "pmg_internal.h"
 
@@ -64,9 +65,23 @@ struct pmg_ctx {
   PcgState* pcg = nullptr;
   double *cx = nullptr, *cr = nullptr, *cz = nullptr, *cp = nullptr, *cq = nullptr, *dinv = nullptr;
   double* bm[3] = {nullptr, nullptr, nullptr};
-  double* Fdev = nullptr;    // grid buffers for pmg_solve_host
+  double* Fdev = nullptr;    // grid buffers for pmg_solve_host (caller-sized: the rank's slab)
   double* Udev = nullptr;
-  long long n_grid = 0;
+  long long n_grid = 0;      // caller grid vector length (one GPU: whole grid; z-slab: planes z0 p .. z1 p)
+  // z-slab decomposition (nranks > 1)
+  Transport* tr = nullptr;   // nullptr on one GPU
+  SlabPlan slab{};           // this rank's plan
+  std::vector<SlabPlan> plans;
+  LevelGeom g0g{};           // GLOBAL coarse geometry (the coarse CG runs replicated on every rank)
+  double* f0g = nullptr;     // global coarse right-hand side / solution (nranks > 1)
+  double* u0g = nullptr;
+  double* agsend = nullptr;  // allgather staging: owned coarse planes, padded to ag_chunk
+  double* agrecv = nullptr;  // nranks x ag_chunk
+  long long ag_chunk = 0;
+  double* cxl = nullptr;     // local coarse correction (L = 0, nranks > 1)
+  double* Floc = nullptr;    // local grid buffers incl. the ghost element layer (nranks > 1)
+  double* Uloc = nullptr;
+  long long n_grid_loc = 0;
   long long launches = 0;
   int last_coarse_its = 0;
   long long coarse_its_total = 0;
@@ -133,6 +148,21 @@ namespace {
 
 int* done_ptr(pmg_ctx* c) { return reinterpret_cast<int*>(reinterpret_cast<char*>(c->pcg) + offsetof(PcgState, done)); }
 
+long long plane_len(const LevelGeom& g) { return (long long)g.V1 * g.V2 * g.RS; }
+
+// refresh the ghost record planes of a level-l skeleton vector from the neighbour ranks
+pmg_status exchange(pmg_ctx* c, int l, double* x) {
+  if (!c->tr) return PMG_OK;
+  const LevelGeom& g = c->D[l].g;
+  const long long n = plane_len(g);
+  const bool lo = c->slab.lower >= 0, hi = c->slab.upper >= 0;
+  std::string e = c->tr->halo(lo ? x + g.own_lo * n : nullptr, lo ? x : nullptr,
+                              hi ? x + (long long)(g.own_hi - 1) * n : nullptr, hi ? x + (long long)(g.V3 - 1) * n : nullptr,
+                              (size_t)n, c->st);
+  if (!e.empty()) return fail(PMG_ENCCL, "halo exchange: " + e);
+  return PMG_OK;
+}
+
 // ---------------------------------------------------------------- level operators (device)
 pmg_status residual_dev(pmg_ctx* c, int l, const double* u, const double* f, double* r, const int* done = nullptr) {
   const DevLevel& D = c->D[l];
@@ -155,7 +185,9 @@ pmg_status smooth_dev(pmg_ctx* c, int l, const double* r, double* u) {
   TimedRegion tr(c, 0, l == c->L);
   size_t sm = star_smem(g.p, c->star_s_smem);
   for (int col = 0; col < 8; ++col) {   // 8 vertex colours (parity), race-free
-    int c1 = col & 1, c2 = (col >> 1) & 1, c3 = (col >> 2) & 1;
+    // the z parity is that of the GLOBAL vertex plane, so a z-slab adds the colour corrections
+    // of every point in the same order as one GPU (bitwise identical results)
+    int c1 = col & 1, c2 = (col >> 1) & 1, c3 = ((col >> 2) & 1) ^ (g.zoff & 1);
     int n1 = (g.k1 - c1) / 2 + 1, n2 = (g.k2 - c2) / 2 + 1, n3 = (g.k3 - c3) / 2 + 1;
     long long nb = (long long)n1 * n2 * n3;
     if (c->ref_kernels)
@@ -204,8 +236,19 @@ pmg_status dot_dev(pmg_ctx* c, const double* a, const double* b, long long n, do
   return PMG_OK;
 }
 
-pmg_status norm_host(pmg_ctx* c, const double* x, long long n, double* out) {
-  pmg_status s = dot_dev(c, x, x, n, c->dres);
+// sum over the owned record planes of level l, summed over ranks (every rank gets the same value)
+pmg_status dot_owned(pmg_ctx* c, int l, const double* a, const double* b, double* out_dev) {
+  const LevelGeom& g = c->D[l].g;
+  const long long n = plane_len(g), off = g.own_lo * n, cnt = (long long)(g.own_hi - g.own_lo) * n;
+  pmg_status s = dot_dev(c, a + off, b + off, cnt, out_dev);
+  if (s || !c->tr) return s;
+  std::string e = c->tr->allreduce_sum(out_dev, 1, c->st);
+  if (!e.empty()) return fail(PMG_ENCCL, "allreduce: " + e);
+  return PMG_OK;
+}
+
+pmg_status norm_host(pmg_ctx* c, int l, const double* x, double* out) {
+  pmg_status s = dot_owned(c, l, x, x, c->dres);
   if (s) return s;
   double h = 0;
   CUDA_CHECK(cudaMemcpyAsync(&h, c->dres, sizeof(double), cudaMemcpyDeviceToHost, c->st));
@@ -220,9 +263,9 @@ pmg_status norm_host(pmg_ctx* c, const double* x, long long n, double* out) {
 pmg_status pcg_dev(pmg_ctx* c, const double* b, double* x) {
   TimedRegion tr(c, 2, true);
   const DevLevel& D = c->D[0];
-  const long long n = D.g.nskel;
+  const long long n = c->g0g.nskel;
   if (c->use_cluster) {   // one cluster launch, everything on chip
-    LevelGeom g0 = D.g;
+    LevelGeom g0 = c->g0g;
     double lam = c->lam, rtol = c->opt.coarse_rtol;
     int maxit = c->opt.coarse_maxit, chunk = c->cl_chunk, halo = c->cl_halo;
     unsigned long long inv = c->cl_inv;
@@ -247,7 +290,7 @@ pmg_status pcg_dev(pmg_ctx* c, const double* b, double* x) {
     return PMG_OK;
   }
   if (c->use_coop) {   // one launch, no host synchronisation; statistics read at the end of solve
-    LevelGeom g0 = D.g;
+    LevelGeom g0 = c->g0g;
     double lam = c->lam, rtol = c->opt.coarse_rtol;
     int maxit = c->opt.coarse_maxit;
     double* part = c->part;
@@ -272,6 +315,7 @@ pmg_status pcg_dev(pmg_ctx* c, const double* b, double* x) {
     c->launches++;
     return PMG_OK;
   }
+  (void)D;
   double* part2 = c->part + kRedBlocks;
   int* done = done_ptr(c);
   k_pcg_init<<<kRedBlocks, kThreads, 0, c->st>>>(b, c->dinv, x, c->cr, c->cz, c->cp, n, c->part, part2);
@@ -311,15 +355,54 @@ pmg_status pcg_dev(pmg_ctx* c, const double* b, double* x) {
 
 int nu_of(const pmg_ctx* c, int l) { return c->opt.schedule == 0 ? 1 : (1 << (c->L - l)); }
 
+// x_local = CG(H_hat_0, b_local).  One GPU: directly.  z-slabs: the owned coarse planes of every
+// rank are gathered into the global coarse vector, every rank runs the same (bitwise identical)
+// CG on the whole coarse system -- no collective inside the iteration -- and keeps its local
+// planes, ghosts included (SURVEY 8(e) / NEXT-2 "allgather F_0 and solve redundantly").
+pmg_status coarse_solve(pmg_ctx* c, const double* b, double* x) {
+  if (!c->tr) return pcg_dev(c, b, x);
+  const LevelGeom& g = c->D[0].g;
+  const long long n = plane_len(g);
+  const long long own = (long long)(g.own_hi - g.own_lo) * n;
+  CUDA_CHECK(cudaMemsetAsync(c->agsend, 0, c->ag_chunk * sizeof(double), c->st));
+  CUDA_CHECK(cudaMemcpyAsync(c->agsend, b + g.own_lo * n, own * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+  std::string e = c->tr->allgather(c->agsend, c->agrecv, (size_t)c->ag_chunk, c->st);
+  if (!e.empty()) return fail(PMG_ENCCL, "allgather: " + e);
+  for (size_t q = 0; q < c->plans.size(); ++q) {
+    const SlabPlan& P = c->plans[q];
+    const long long cnt = (long long)(P.own_hi - P.own_lo) * n;
+    CUDA_CHECK(cudaMemcpyAsync(c->f0g + (long long)P.z0 * n, c->agrecv + (long long)q * c->ag_chunk, cnt * sizeof(double),
+                               cudaMemcpyDeviceToDevice, c->st));
+  }
+  c->tr->exclusive_begin();
+  pmg_status s = pcg_dev(c, c->f0g, c->u0g);
+  e = c->tr->exclusive_end(c->st);
+  if (s) return s;
+  if (!e.empty()) return fail(PMG_ECUDA, "coarse CG: " + e);
+  CUDA_CHECK(cudaMemcpyAsync(x, c->u0g + (long long)c->slab.zb * n, g.nskel * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+  return PMG_OK;
+}
+
+// residual with the halo refresh of u before and of r after (no-ops on one GPU)
+pmg_status residual_x(pmg_ctx* c, int l, double* u, const double* f, double* r) {
+  pmg_status s;
+  if ((s = exchange(c, l, u))) return s;
+  if ((s = residual_dev(c, l, u, f, r))) return s;
+  return exchange(c, l, r);
+}
+
 // Alg. 3.  r_top_valid: D[L].r already holds f - H u (saves one residual).
 pmg_status vcycle_dev(pmg_ctx* c, double* u, const double* f, bool r_top_valid) {
   const int L = c->L;
   pmg_status s;
+  // z-slabs: every operator reads ghost planes that the exchanges below refresh:
+  // residual needs u's, smoother and restriction r's / f's, prolongation the coarse u's.
   if (L == 0) {  // reading R10b: u <- u + CG(f - H_0 u)
     DevLevel& D = c->D[0];
-    if (!r_top_valid && (s = residual_dev(c, 0, u, f, D.r))) return s;
-    if ((s = pcg_dev(c, D.r, c->cx))) return s;
-    k_axpy<<<grid_for(D.g.nskel), kThreads, 0, c->st>>>(u, c->cx, 1.0, D.g.nskel);
+    if (!r_top_valid && (s = residual_x(c, 0, u, f, D.r))) return s;
+    double* cx = c->tr ? c->cxl : c->cx;
+    if ((s = coarse_solve(c, D.r, cx))) return s;
+    k_axpy<<<grid_for(D.g.nskel), kThreads, 0, c->st>>>(u, cx, 1.0, D.g.nskel);
     LAUNCH_CHECK(c);
     return PMG_OK;
   }
@@ -336,22 +419,24 @@ pmg_status vcycle_dev(pmg_ctx* c, double* u, const double* f, bool r_top_valid) 
     for (int i = 0; i < nu_of(c, l); ++i) {
       const double* rin = D.r;
       if (u_zero) rin = fl;                       // f - H 0 = f exactly
-      else if (!r_valid && (s = residual_dev(c, l, ul, fl, D.r))) return s;
+      else if (!r_valid && (s = residual_x(c, l, ul, fl, D.r))) return s;
       if ((s = smooth_dev(c, l, rin, ul))) return s;
       r_valid = false;
       u_zero = false;
     }
-    if ((s = residual_dev(c, l, ul, fl, D.r))) return s;
+    if ((s = residual_x(c, l, ul, fl, D.r))) return s;
     if ((s = restrict_dev(c, l, D.r, c->D[l - 1].f))) return s;
+    if (l - 1 >= 1 && (s = exchange(c, l - 1, c->D[l - 1].f))) return s;
   }
-  if ((s = pcg_dev(c, c->D[0].f, c->D[0].u))) return s;
+  if ((s = coarse_solve(c, c->D[0].f, c->D[0].u))) return s;
   for (int l = 1; l <= L; ++l) {
     DevLevel& D = c->D[l];
     double* ul = (l == L) ? u : D.u;
     const double* fl = (l == L) ? f : D.f;
+    if (l - 1 >= 1 && (s = exchange(c, l - 1, c->D[l - 1].u))) return s;
     if ((s = prolong_dev(c, l, c->D[l - 1].u, ul))) return s;
     for (int i = 0; i < nu_of(c, l); ++i) {
-      if ((s = residual_dev(c, l, ul, fl, D.r))) return s;
+      if ((s = residual_x(c, l, ul, fl, D.r))) return s;
       if ((s = smooth_dev(c, l, D.r, ul))) return s;
     }
   }
@@ -371,7 +456,8 @@ pmg_status condense_dev(pmg_ctx* c, const double* F, double* fhat) {
 
 pmg_status recover_dev(pmg_ctx* c, const double* uhat, const double* F, double* ufull) {
   const DevLevel& D = c->D[c->L];
-  k_skel_to_grid<<<grid_for(c->n_grid), kThreads, 0, c->st>>>(D.g, uhat, ufull);
+  const long long ng = (long long)(D.g.k1 * D.g.p + 1) * (D.g.k2 * D.g.p + 1) * (D.g.k3 * D.g.p + 1);
+  k_skel_to_grid<<<grid_for(ng), kThreads, 0, c->st>>>(D.g, uhat, ufull);
   LAUNCH_CHECK(c);
   size_t sm = recover_smem(D.g.p, D.g.ET, c->cube_in_smem);
   int nb = c->cube_in_smem ? (int)std::min<long long>(D.g.nelem, 148LL * 8) : c->cube_blocks;
@@ -385,25 +471,39 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
   pmg_status s;
   c->coarse_its_total = 0;
   CUDA_CHECK(cudaMemsetAsync(c->pcg, 0, sizeof(PcgState), c->st));
-  if ((s = condense_dev(c, F, D.f))) return s;
+  const double* Floc = F;
+  if (c->tr) {
+    // the caller's slab holds grid planes z0 p .. z1 p; the local buffer adds the ghost element
+    // layer below (planes zb p .. z0 p - 1), received from the lower rank, for the condensation
+    const LevelGeom& g = D.g;
+    const long long pl = (long long)(g.k1 * g.p + 1) * (g.k2 * g.p + 1);
+    const long long ghost = (long long)(c->slab.z0 - c->slab.zb) * g.p * pl;
+    CUDA_CHECK(cudaMemcpyAsync(c->Floc + ghost, F, c->n_grid * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    const long long n = (long long)g.p * pl;   // the p planes below the rank's top plane go up
+    std::string e = c->tr->shift_up(c->Floc + c->n_grid_loc - pl - n, c->Floc, (size_t)n, c->st);
+    if (!e.empty()) return fail(PMG_ENCCL, "grid halo: " + e);
+    Floc = c->Floc;
+  }
+  if ((s = condense_dev(c, Floc, D.f))) return s;
+  if ((s = exchange(c, c->L, D.f))) return s;
   if ((s = zero_dev(c, D.u, D.g.nskel))) return s;
-  if ((s = residual_dev(c, c->L, D.u, D.f, D.r))) return s;
+  if ((s = residual_x(c, c->L, D.u, D.f, D.r))) return s;
   double r0, rn;
-  if ((s = norm_host(c, D.r, D.g.nskel, &r0))) return s;
+  if ((s = norm_host(c, c->L, D.r, &r0))) return s;
   rn = r0;
   int cycles = 0;
   if (rep && rep->history && rep->history_cap > 0) rep->history[0] = r0;
   // One cycle = V-cycle + residual + ||r||^2 into dres.  When the whole cycle is free of host
   // synchronisation (cooperative coarse CG) it is captured once into a CUDA graph and replayed:
   // ~60 kernel launches per cycle become one graph launch.
-  const bool graph_ok = c->use_coop && c->st != nullptr && !c->timing && !c->no_graph;
+  const bool graph_ok = c->use_coop && c->st != nullptr && !c->timing && !c->no_graph && (!c->tr || c->tr->graph_safe());
   if (graph_ok && !c->cycle_exec) {
     long long l0 = c->launches;
     cudaGraph_t gr = nullptr;
     CUDA_CHECK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
     pmg_status cs = vcycle_dev(c, D.u, D.f, true);
-    if (!cs) cs = residual_dev(c, c->L, D.u, D.f, D.r);
-    if (!cs) cs = dot_dev(c, D.r, D.r, D.g.nskel, c->dres);
+    if (!cs) cs = residual_x(c, c->L, D.u, D.f, D.r);
+    if (!cs) cs = dot_owned(c, c->L, D.r, D.r, c->dres);
     cudaError_t ce = cudaStreamEndCapture(c->st, &gr);
     if (cs) { if (gr) cudaGraphDestroy(gr); return cs; }
     if (ce != cudaSuccess) return fail(PMG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
@@ -422,13 +522,22 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
       rn = std::sqrt(*c->hres);
     } else {
       if ((s = vcycle_dev(c, D.u, D.f, true))) return s;
-      if ((s = residual_dev(c, c->L, D.u, D.f, D.r))) return s;
-      if ((s = norm_host(c, D.r, D.g.nskel, &rn))) return s;
+      if ((s = residual_x(c, c->L, D.u, D.f, D.r))) return s;
+      if ((s = norm_host(c, c->L, D.r, &rn))) return s;
     }
     ++cycles;
     if (rep && rep->history && cycles < rep->history_cap) rep->history[cycles] = rn;
   }
-  if ((s = recover_dev(c, D.u, F, ufull))) return s;
+  if (c->tr) {
+    if ((s = exchange(c, c->L, D.u))) return s;
+    if ((s = recover_dev(c, D.u, c->Floc, c->Uloc))) return s;
+    const LevelGeom& g = D.g;
+    const long long pl = (long long)(g.k1 * g.p + 1) * (g.k2 * g.p + 1);
+    const long long ghost = (long long)(c->slab.z0 - c->slab.zb) * g.p * pl;
+    CUDA_CHECK(cudaMemcpyAsync(ufull, c->Uloc + ghost, c->n_grid * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+  } else if ((s = recover_dev(c, D.u, F, ufull))) {
+    return s;
+  }
   if (c->use_coop) {
     PcgState hs;
     CUDA_CHECK(cudaMemcpyAsync(&hs, c->pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, c->st));
@@ -458,6 +567,9 @@ void free_ctx(pmg_ctx* c) {
   cudaFree(c->cx); cudaFree(c->cr); cudaFree(c->cz); cudaFree(c->cp); cudaFree(c->cq); cudaFree(c->dinv);
   for (int d = 0; d < 3; ++d) cudaFree(c->bm[d]);
   cudaFree(c->Fdev); cudaFree(c->Udev);
+  cudaFree(c->f0g); cudaFree(c->u0g); cudaFree(c->agsend); cudaFree(c->agrecv); cudaFree(c->cxl);
+  cudaFree(c->Floc); cudaFree(c->Uloc);
+  delete c->tr;
   for (int i = 0; i < 7; ++i) cudaFree(c->ctab[i]);
   cudaFree(c->cV);
   if (c->cycle_exec) cudaGraphExecDestroy(c->cycle_exec);
@@ -525,12 +637,20 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   if (p < o.p0) return fail(PMG_EINVAL, "p must be >= p0");
   if (o.weight_degree != 7) return fail(PMG_EINVAL, "only weight_degree = 7 is implemented (P:316)");
   if (o.schedule != 0 && o.schedule != 1) return fail(PMG_EINVAL, "schedule must be 0 or 1");
-  if (o.nranks != 1) return fail(PMG_EINVAL, "only nranks = 1 is implemented in this version");
+  if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return fail(PMG_EINVAL, "need 0 <= rank < nranks");
+  if (o.nranks > 1 && n_e[2] < o.nranks) return fail(PMG_EINVAL, "z-slabs: k3 >= nranks required");
+  if (o.nranks > 1 && o.p0 != 2) return fail(PMG_EINVAL, "z-slabs: the replicated coarse CG needs p0 = 2");
   if (!(o.coarse_rtol > 0.0) || o.coarse_maxit < 1) return fail(PMG_EINVAL, "coarse_rtol > 0 and coarse_maxit >= 1 required");
 
   pmg_ctx* c = new (std::nothrow) pmg_ctx();
   if (!c) return fail(PMG_ENOMEM, "host allocation failed");
   c->opt = o;
+  slab_plan(n_e[2], o.nranks, o.rank, &c->slab);
+  for (int q = 0; q < o.nranks; ++q) { SlabPlan P; slab_plan(n_e[2], o.nranks, q, &P); c->plans.push_back(P); }
+  {
+    std::string e = make_transport(o.rank, o.nranks, o.nccl_id, o.loopback, &c->tr);
+    if (!e.empty()) { delete c; return fail(o.loopback ? PMG_EINVAL : PMG_ENCCL, e); }
+  }
   c->st = static_cast<cudaStream_t>(o.stream);
   c->lam = lambda;
   int L = 0;
@@ -558,11 +678,35 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   size_t max_elem = 0, max_star = 0, max_tr = 0;
   size_t Ylen = 0, Zlen = 0;
   pmg_status s;
+  c->g0g = c->H[0].g;
+  const SlabPlan& sp = c->slab;
   for (int l = 0; l <= L; ++l) {
     DevLevel& D = c->D[l];
-    D.g = c->H[l].g;
-    if ((s = upload(&D.etab, c->H[l].etab)) || (s = upload(&D.stab, c->H[l].stab)) ||
-        (s = upload(&D.stabT, c->H[l].stabT))) { free_ctx(c); return s; }
+    const HostLevel& Hl = c->H[l];
+    D.g = Hl.g;
+    std::vector<double> et = Hl.etab, st = Hl.stab, stT = Hl.stabT;
+    if (c->tr) {
+      // the rank's slab: vertex planes zb .. z1, element layers zb .. z1-1 (one ghost layer
+      // below); direction-3 rows of the element / star tables sliced to match
+      LevelGeom& g = D.g;
+      const int k1 = g.k1, k2 = g.k2, V1 = g.V1, V2 = g.V2, n = g.n;
+      g.k3 = sp.z1 - sp.zb;
+      g.V3 = g.k3 + 1;
+      g.nrec = (long long)g.V1 * g.V2 * g.V3;
+      g.nskel = g.nrec * g.RS;
+      g.nelem = (long long)g.k1 * g.k2 * g.k3;
+      g.zoff = sp.zb;
+      g.K3 = Hl.g.k3;
+      g.own_lo = sp.own_lo;
+      g.own_hi = sp.own_hi;
+      et.assign(Hl.etab.begin(), Hl.etab.begin() + (size_t)(k1 + k2) * g.ET);
+      et.insert(et.end(), Hl.etab.begin() + (size_t)(k1 + k2 + sp.zb) * g.ET, Hl.etab.begin() + (size_t)(k1 + k2 + sp.z1) * g.ET);
+      st.assign(Hl.stab.begin(), Hl.stab.begin() + (size_t)(V1 + V2) * g.ST);
+      st.insert(st.end(), Hl.stab.begin() + (size_t)(V1 + V2 + sp.zb) * g.ST, Hl.stab.begin() + (size_t)(V1 + V2 + sp.z1 + 1) * g.ST);
+      stT.assign(Hl.stabT.begin(), Hl.stabT.begin() + (size_t)(V1 + V2) * n * n);
+      stT.insert(stT.end(), Hl.stabT.begin() + (size_t)(V1 + V2 + sp.zb) * n * n, Hl.stabT.begin() + (size_t)(V1 + V2 + sp.z1 + 1) * n * n);
+    }
+    if ((s = upload(&D.etab, et)) || (s = upload(&D.stab, st)) || (s = upload(&D.stabT, stT))) { free_ctx(c); return s; }
     max_elem = std::max(max_elem, hot_smem(D.g.p, 0));
     max_star = std::max(max_star, hot_smem(D.g.p, 1));
     if (l >= 1 && (s = upload(&D.Jint, c->H[l].Jint))) { free_ctx(c); return s; }
@@ -603,7 +747,23 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
     c->cube_blocks = 296;
     if (dalloc(&c->cube, (size_t)c->cube_blocks * gt.m * gt.m * gt.m)) { free_ctx(c); return fail(PMG_ENOMEM, "cudaMalloc failed (cube)"); }
   }
-  long long n0 = c->D[0].g.nskel;
+  long long n0 = c->g0g.nskel;
+  if (c->tr) {
+    const long long pl = plane_len(c->D[0].g);
+    int maxown = 0;
+    for (const SlabPlan& P : c->plans) maxown = std::max(maxown, P.own_hi - P.own_lo);
+    c->ag_chunk = (long long)maxown * pl;
+    const LevelGeom& gt_ = c->D[L].g;
+    c->n_grid_loc = (long long)(gt_.k1 * p + 1) * (gt_.k2 * p + 1) * (gt_.k3 * p + 1);
+    if (dalloc(&c->f0g, n0) || dalloc(&c->u0g, n0) || dalloc(&c->agsend, c->ag_chunk) ||
+        dalloc(&c->agrecv, c->ag_chunk * o.nranks) || dalloc(&c->cxl, c->D[0].g.nskel) ||
+        dalloc(&c->Floc, c->n_grid_loc) || dalloc(&c->Uloc, c->n_grid_loc)) {
+      free_ctx(c);
+      return fail(PMG_ENOMEM, "cudaMalloc failed (z-slab buffers)");
+    }
+    cudaMemset(c->f0g, 0, n0 * sizeof(double));
+    cudaMemset(c->Floc, 0, c->n_grid_loc * sizeof(double));
+  }
   if (dalloc(&c->cx, n0) || dalloc(&c->cr, n0) || dalloc(&c->cz, n0) || dalloc(&c->cp, n0) || dalloc(&c->cq, n0)) {
     free_ctx(c);
     return fail(PMG_ENOMEM, "cudaMalloc failed (coarse CG vectors)");
@@ -618,7 +778,7 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
       for (int t = 0; t <= p; ++t) b[e * p + t] += 0.5 * widths[d][e] * ww[t];
     if ((s = upload(&c->bm[d], b))) { free_ctx(c); return s; }
   }
-  c->n_grid = (long long)(n_e[0] * p + 1) * (n_e[1] * p + 1) * (n_e[2] * p + 1);
+  c->n_grid = (long long)(n_e[0] * p + 1) * (n_e[1] * p + 1) * ((sp.z1 - sp.z0) * p + 1);
   if (dalloc(&c->Fdev, c->n_grid) || dalloc(&c->Udev, c->n_grid)) { free_ctx(c); return fail(PMG_ENOMEM, "cudaMalloc failed (grid buffers)"); }
   // the attribute is per function, not per context: always allow the device maximum so that
   // several contexts with different degrees can coexist
@@ -638,7 +798,7 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_coop_p2, kThreads, 0);
     const char* env = std::getenv("PMG_COARSE_MULTIKERNEL");
     if (coop && per_sm > 0 && c->D[0].g.p == 2 && !(env && env[0] == '1')) {
-      long long want = (c->D[0].g.nskel + kThreads - 1) / kThreads;
+      long long want = (c->g0g.nskel + kThreads - 1) / kThreads;
       long long cap = std::min<long long>((long long)per_sm * nsm, 1344);
       c->coop_nb = (int)std::max<long long>(1, std::min(want, cap));
       c->use_coop = true;
@@ -654,7 +814,7 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
       }
       // cluster variant: all CG vectors of a coarse system that fits in 16 SMs' shared memory
       {
-        const LevelGeom& g0 = c->D[0].g;
+        const LevelGeom& g0 = c->g0g;
         const char* ce = std::getenv("PMG_COARSE_CLUSTER");
         // opt-in: on the 16 SMs of one cluster the per-entry index arithmetic is slower than the
         // grid barrier it saves (measured)
@@ -696,7 +856,7 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
       {
         int per_sm_reg = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_reg, k_pcg_coop_reg_p2, kThreads, 0);
-        const long long need = (c->D[0].g.nskel + kThreads - 1) / kThreads;
+        const long long need = (c->g0g.nskel + kThreads - 1) / kThreads;
         const char* re = std::getenv("PMG_COARSE_REG");
         if (!(re && re[0] == '0') && per_sm_reg > 0 && need <= std::min<long long>((long long)per_sm_reg * nsm, 1344)) {
           c->coop_reg = true;
@@ -706,6 +866,10 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
       const char* nbenv = std::getenv("PMG_COOP_BLOCKS");   // tuning experiments only
       if (nbenv && std::atoi(nbenv) > 0) c->coop_nb = (int)std::min<long long>(std::atoi(nbenv), cap);
     }
+  }
+  if (c->tr && !c->use_coop) {
+    free_ctx(c);
+    return fail(PMG_EINVAL, "z-slabs need the cooperative coarse CG (p0 = 2, cooperative launch support)");
   }
   cudaError_t es = cudaDeviceSynchronize();
   if (es != cudaSuccess) { free_ctx(c); return fail(PMG_ECUDA, std::string("setup: ") + cudaGetErrorString(es)); }
@@ -727,8 +891,8 @@ pmg_status pmg_level_info(const pmg_ctx* c, int level, int* degree, long long* n
   if (s) return s;
   const LevelGeom& g = c->D[level].g;
   if (degree) *degree = g.p;
-  if (n_skel) *n_skel = g.nskel;
-  if (n_grid) *n_grid = (long long)(g.k1 * g.p + 1) * (g.k2 * g.p + 1) * (g.k3 * g.p + 1);
+  if (n_skel) *n_skel = g.nskel;   // local (ghost planes included) on z-slabs
+  if (n_grid) *n_grid = (long long)(g.k1 * g.p + 1) * (g.k2 * g.p + 1) * ((c->slab.z1 - c->slab.z0) * g.p + 1);
   return PMG_OK;
 }
 
@@ -737,7 +901,12 @@ pmg_status pmg_grid_coords(const pmg_ctx* c, int level, int d, double* coords_ho
   if (s) return s;
   if (d < 0 || d > 2 || !coords_host) return fail(PMG_EINVAL, "bad direction or NULL output");
   const auto& x = c->H[level].coords[d];
-  std::memcpy(coords_host, x.data(), x.size() * sizeof(double));
+  if (d == 2) {   // the rank's slab: nodes z0 p .. z1 p (the whole line on one GPU)
+    const int p = c->H[level].p;
+    std::memcpy(coords_host, x.data() + (size_t)c->slab.z0 * p, (size_t)((c->slab.z1 - c->slab.z0) * p + 1) * sizeof(double));
+  } else {
+    std::memcpy(coords_host, x.data(), x.size() * sizeof(double));
+  }
   return PMG_OK;
 }
 
@@ -746,7 +915,7 @@ pmg_status pmg_residual(pmg_ctx* c, int level, const double* u_hat, const double
   if (s) return s;
   if (!u_hat || !r_hat) return fail(PMG_EINVAL, "NULL vector");
   if (u_hat == r_hat) return fail(PMG_EINVAL, "u_hat and r_hat must not alias");
-  return residual_dev(c, level, u_hat, f_hat, r_hat);
+  return residual_x(c, level, const_cast<double*>(u_hat), f_hat, r_hat);   // z-slabs: ghosts refreshed
 }
 
 pmg_status pmg_smooth(pmg_ctx* c, int level, const double* r_hat, double* u_hat) {
@@ -754,7 +923,9 @@ pmg_status pmg_smooth(pmg_ctx* c, int level, const double* r_hat, double* u_hat)
   if (s) return s;
   if (!u_hat || !r_hat) return fail(PMG_EINVAL, "NULL vector");
   if (u_hat == r_hat) return fail(PMG_EINVAL, "u_hat and r_hat must not alias");
-  return smooth_dev(c, level, r_hat, u_hat);
+  if ((s = exchange(c, level, const_cast<double*>(r_hat)))) return s;
+  if ((s = smooth_dev(c, level, r_hat, u_hat))) return s;
+  return exchange(c, level, u_hat);
 }
 
 pmg_status pmg_restrict(pmg_ctx* c, int level, const double* r_fine, double* f_coarse) {
@@ -762,7 +933,9 @@ pmg_status pmg_restrict(pmg_ctx* c, int level, const double* r_fine, double* f_c
   if (s) return s;
   if (level < 1) return fail(PMG_EINVAL, "restrict needs a fine level >= 1");
   if (!r_fine || !f_coarse) return fail(PMG_EINVAL, "NULL vector");
-  return restrict_dev(c, level, r_fine, f_coarse);
+  if ((s = exchange(c, level, const_cast<double*>(r_fine)))) return s;
+  if ((s = restrict_dev(c, level, r_fine, f_coarse))) return s;
+  return exchange(c, level - 1, f_coarse);
 }
 
 pmg_status pmg_prolong(pmg_ctx* c, int level, const double* u_coarse, double* u_fine) {
@@ -770,23 +943,30 @@ pmg_status pmg_prolong(pmg_ctx* c, int level, const double* u_coarse, double* u_
   if (s) return s;
   if (level < 1) return fail(PMG_EINVAL, "prolong needs a fine level >= 1");
   if (!u_coarse || !u_fine) return fail(PMG_EINVAL, "NULL vector");
-  return prolong_dev(c, level, u_coarse, u_fine);
+  if ((s = exchange(c, level - 1, const_cast<double*>(u_coarse)))) return s;
+  if ((s = prolong_dev(c, level, u_coarse, u_fine))) return s;
+  return exchange(c, level, u_fine);
 }
 
 pmg_status pmg_vcycle(pmg_ctx* c, double* u_hat, const double* f_hat) {
   if (!c) return fail(PMG_EINVAL, "ctx is NULL");
   if (!u_hat || !f_hat) return fail(PMG_EINVAL, "NULL vector");
-  return vcycle_dev(c, u_hat, f_hat, false);
+  pmg_status s;
+  if ((s = exchange(c, c->L, const_cast<double*>(f_hat)))) return s;
+  if ((s = vcycle_dev(c, u_hat, f_hat, false))) return s;
+  return exchange(c, c->L, u_hat);
 }
 
 pmg_status pmg_condense(pmg_ctx* c, const double* F_full, double* f_hat) {
   if (!c) return fail(PMG_EINVAL, "ctx is NULL");
+  if (c->tr) return fail(PMG_EINVAL, "pmg_condense: one GPU only (pmg_solve condenses on z-slabs)");
   if (!F_full || !f_hat) return fail(PMG_EINVAL, "NULL vector");
   return condense_dev(c, F_full, f_hat);
 }
 
 pmg_status pmg_recover(pmg_ctx* c, const double* u_hat, const double* F_full, double* u_full) {
   if (!c) return fail(PMG_EINVAL, "ctx is NULL");
+  if (c->tr) return fail(PMG_EINVAL, "pmg_recover: one GPU only (pmg_solve recovers on z-slabs)");
   if (!u_hat || !F_full || !u_full) return fail(PMG_EINVAL, "NULL vector");
   return recover_dev(c, u_hat, F_full, u_full);
 }
@@ -812,7 +992,10 @@ pmg_status pmg_solve_host(pmg_ctx* c, const double* F_host, double* u_host, doub
 pmg_status pmg_weak_rhs(pmg_ctx* c, const double* f_nodal, double* F_full) {
   if (!c) return fail(PMG_EINVAL, "ctx is NULL");
   if (!f_nodal || !F_full) return fail(PMG_EINVAL, "NULL vector");
-  k_weak_rhs<<<grid_for(c->n_grid), kThreads, 0, c->st>>>(c->D[c->L].g, c->bm[0], c->bm[1], c->bm[2], f_nodal, F_full);
+  LevelGeom g = c->D[c->L].g;   // the caller's slab: element layers z0 .. z1-1
+  g.k3 = c->slab.z1 - c->slab.z0;
+  g.zoff = c->slab.z0;
+  k_weak_rhs<<<grid_for(c->n_grid), kThreads, 0, c->st>>>(g, c->bm[0], c->bm[1], c->bm[2], f_nodal, F_full);
   LAUNCH_CHECK(c);
   return PMG_OK;
 }
@@ -821,6 +1004,7 @@ pmg_status pmg_skel_from_grid(pmg_ctx* c, int level, const double* grid, double*
   pmg_status s = check_level(c, level);
   if (s) return s;
   if (!grid || !skel) return fail(PMG_EINVAL, "NULL vector");
+  if (c->tr) return fail(PMG_EINVAL, "layout converters: one GPU only");
   k_skel_from_grid<<<grid_for(c->D[level].g.nskel), kThreads, 0, c->st>>>(c->D[level].g, grid, skel);
   LAUNCH_CHECK(c);
   return PMG_OK;
@@ -830,6 +1014,7 @@ pmg_status pmg_skel_to_grid(pmg_ctx* c, int level, const double* skel, double* g
   pmg_status s = check_level(c, level);
   if (s) return s;
   if (!grid || !skel) return fail(PMG_EINVAL, "NULL vector");
+  if (c->tr) return fail(PMG_EINVAL, "layout converters: one GPU only");
   const LevelGeom& g = c->D[level].g;
   long long ng = (long long)(g.k1 * g.p + 1) * (g.k2 * g.p + 1) * (g.k3 * g.p + 1);
   k_skel_to_grid<<<grid_for(ng), kThreads, 0, c->st>>>(g, skel, grid);
@@ -841,10 +1026,35 @@ pmg_status pmg_norm(pmg_ctx* c, int level, const double* x_hat, double* out_host
   pmg_status s = check_level(c, level);
   if (s) return s;
   if (!x_hat || !out_host) return fail(PMG_EINVAL, "NULL pointer");
-  return norm_host(c, x_hat, c->D[level].g.nskel, out_host);
+  return norm_host(c, level, x_hat, out_host);
 }
 
 long long pmg_launch_count(const pmg_ctx* c) { return c ? c->launches : -1; }
+
+int pmg_slab_plan(int k3, int nranks, int rank, pmg_slab* out) {
+  SlabPlan P;
+  if (!out || slab_plan(k3, nranks, rank, &P) != 0) return -1;
+  out->z0 = P.z0; out->z1 = P.z1; out->zb = P.zb; out->nplanes = P.nplanes;
+  out->own_lo = P.own_lo; out->own_hi = P.own_hi; out->lower = P.lower; out->upper = P.upper;
+  return 0;
+}
+
+pmg_status pmg_slab_info(const pmg_ctx* c, pmg_slab* out) {
+  if (!c || !out) return fail(PMG_EINVAL, "NULL argument");
+  const SlabPlan& P = c->slab;
+  out->z0 = P.z0; out->z1 = P.z1; out->zb = P.zb; out->nplanes = P.nplanes;
+  out->own_lo = P.own_lo; out->own_hi = P.own_hi; out->lower = P.lower; out->upper = P.upper;
+  return PMG_OK;
+}
+
+pmg_status pmg_nccl_unique_id(void* out128) {
+  if (!out128) return fail(PMG_EINVAL, "NULL output");
+  std::string e = nccl_unique_id(out128);
+  return e.empty() ? PMG_OK : fail(PMG_ENCCL, e);
+}
+
+void* pmg_loopback_create(int nranks) { return loopback_create(nranks); }
+void pmg_loopback_destroy(void* hub) { loopback_destroy(hub); }
 
 pmg_status pmg_timing_enable(pmg_ctx* c, int enable) {
   if (!c) return fail(PMG_EINVAL, "ctx is NULL");

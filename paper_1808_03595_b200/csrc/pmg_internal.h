@@ -24,6 +24,13 @@ struct LevelGeom {
   long long nrec;       // V1 V2 V3
   long long nskel;      // nrec * RS
   long long nelem;      // k1 k2 k3
+  // z-slab decomposition: this geometry holds vertex planes
+  // zoff .. zoff + k3 of a global mesh with K3 element layers.  Dirichlet tests (is_free) use the
+  // global plane zoff + v3; array bounds (inside) stay local.  Element-gathered skeleton values
+  // (residual, condensed RHS, restriction) are computed on the owned record planes
+  // [own_lo, own_hi); the other (ghost) planes are filled by the halo exchange.
+  // One GPU: zoff = 0, K3 = k3, own_lo = 0, own_hi = V3.
+  int zoff, K3, own_lo, own_hi;
 };
 
 // Element table, per direction d and 1-D element e_d (width h), m = p - 1, q = p + 1:

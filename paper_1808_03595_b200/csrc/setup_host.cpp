@@ -160,6 +160,7 @@ std::string build_level(HostLevel& L, int p, const int k[3], const double* const
   g.nrec = (long long)g.V1 * g.V2 * g.V3;
   g.nskel = g.nrec * g.RS;
   g.nelem = (long long)k[0] * k[1] * k[2];
+  g.zoff = 0; g.K3 = k[2]; g.own_lo = 0; g.own_hi = g.V3;
 
   std::vector<double> xi, wq;
   gll(p, xi, wq);

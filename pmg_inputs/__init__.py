@@ -65,10 +65,13 @@ class Case:
         """Unknowns n_e p^3 (the paper's convention)."""
         return self.k[0] * self.k[1] * self.k[2] * self.p ** 3
 
-    def f_nodal(self, coords):
-        """Nodal f on the global grid (flat, x1 fastest) given the three 1-D coordinate arrays."""
+    def f_nodal(self, coords, i3_offset=0):
+        """Nodal f on the global grid (flat, x1 fastest) given the three 1-D coordinate arrays.
+        A z-slab passes its own x3 nodes and the global index of its first plane (i3_offset):
+        the values are those of the undivided grid on those planes."""
         N1, N2, N3 = self.N
-        g = np.arange(N1 * N2 * N3, dtype=np.uint64)
+        n3 = len(coords[2])
+        g = np.arange(N1 * N2 * n3, dtype=np.uint64) + np.uint64(N1 * N2 * int(i3_offset))
         if self.f_kind == "uniform":
             return uniform_pm1(self.seed, g)
         if self.f_kind == "normal":

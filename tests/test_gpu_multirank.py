@@ -1,0 +1,188 @@
+"""z-slab decomposition on ONE GPU through the library's loopback transport (DESIGN.md
+"Multi-GPU"): nranks contexts in one process, one host thread and one stream each; every
+exchange is a host-synchronised device copy, so no kernel ever waits for another rank.
+
+The decomposition changes no arithmetic of any point (each value is computed from the same
+inputs in the same order), so the operators and the V-cycle must reproduce the one-GPU result on
+every owned plane BITWISE; the solve (whose stopping test sums owned partial norms across ranks)
+must match to 1e-12 with the same cycle count."""
+import threading
+
+import numpy as np
+import pytest
+
+import pmg_inputs as pi
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "k325_p4_lam1.7_stretched": dict(k=(3, 2, 5), p=4, lam=1.7, stretch=1.4),
+    "k334_p8_lam0": dict(k=(3, 3, 4), p=8, lam=0.0, stretch=None),
+    "k236_p2_lam0.3": dict(k=(2, 3, 6), p=2, lam=0.3, stretch=None),     # L = 0: CG only
+    "k227_p5_lam0": dict(k=(2, 2, 7), p=5, lam=0.0, stretch=1.2),
+}
+
+
+def run_ranks(nr, case, fn, **kw):
+    """fn(solver, rank) on nr loopback ranks (threads); returns the per-rank results."""
+    import paper_1808_03595_b200 as pmg
+    hub = pmg.Loopback(nr)
+    out, errs = [None] * nr, []
+    solvers = [None] * nr
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                s = pmg.Solver(case.k, case.widths, case.p, case.lam, rank=r, nranks=nr, loopback=hub,
+                               stream=st, **kw)
+                solvers[r] = s
+                out[r] = fn(s, r)
+                st.synchronize()
+        except Exception as e:  # surfaced below
+            errs.append((r, e))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(nr)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for s in solvers:
+        if s is not None:
+            s.close()
+    hub.close()
+    assert not errs, errs
+    return out
+
+
+def one_gpu(case, **kw):
+    import paper_1808_03595_b200 as pmg
+    return pmg.Solver(case.k, case.widths, case.p, case.lam, **kw)
+
+
+def global_F(case, s1):
+    x = [s1.grid_coords(s1.nlevels - 1, d) for d in range(3)]
+    f = torch.from_numpy(case.f_nodal(x)).cuda()
+    F = s1.new_grid()
+    s1.weak_rhs(f, F)
+    torch.cuda.synchronize()
+    return f.cpu().numpy(), F.cpu().numpy()
+
+
+def planes(s1, level):
+    """(plane length, global skeleton vector length) of a level of the one-GPU solver."""
+    _, n, _ = s1.level_info(level)
+    return n // (s1.k[2] + 1), n
+
+
+@pytest.mark.parametrize("nr", [2, 3])
+@pytest.mark.parametrize("name", list(CASES))
+def test_solve_matches_one_gpu(name, nr):
+    cfg = CASES[name]
+    case = pi.small_case(cfg["k"], cfg["p"], cfg["lam"], stretch=cfg["stretch"])
+    s1 = one_gpu(case)
+    f_np, F_np = global_F(case, s1)
+    u1 = s1.new_grid()
+    rep1 = s1.solve(torch.from_numpy(F_np).cuda(), u1, 1e-10)
+    u1 = u1.cpu().numpy()
+    N1, N2 = case.k[0] * case.p + 1, case.k[1] * case.p + 1
+    pl = N1 * N2
+    s1.close()
+
+    def fn(s, r):
+        sl = s.slab
+        lo, hi = sl["z0"] * case.p * pl, (sl["z1"] * case.p + 1) * pl
+        f_loc = torch.from_numpy(f_np[lo:hi].copy()).cuda()
+        F_loc = s.new_grid()
+        s.weak_rhs(f_loc, F_loc)          # the slab's weak RHS (global 1-D masses)
+        u = s.new_grid()
+        rep = s.solve(F_loc, u, 1e-10)
+        torch.cuda.current_stream().synchronize()
+        return sl, F_loc.cpu().numpy(), u.cpu().numpy(), rep
+
+    res = run_ranks(nr, case, fn)
+    for sl, F_loc, u, rep in res:
+        lo, hi = sl["z0"] * case.p * pl, (sl["z1"] * case.p + 1) * pl
+        assert np.array_equal(F_loc, F_np[lo:hi])
+        assert rep["cycles"] == rep1["cycles"], (rep["cycles"], rep1["cycles"])
+        err = np.abs(u - u1[lo:hi]).max() / np.abs(u1).max()
+        assert err <= 1e-12, err
+
+
+@pytest.mark.parametrize("nr", [2, 3])
+@pytest.mark.parametrize("name", ["k325_p4_lam1.7_stretched", "k334_p8_lam0", "k236_p2_lam0.3"])
+def test_operators_and_vcycle_bitwise(name, nr):
+    cfg = CASES[name]
+    case = pi.small_case(cfg["k"], cfg["p"], cfg["lam"], stretch=cfg["stretch"])
+    s1 = one_gpu(case, coarse_rtol=1e-13)
+    L = s1.nlevels - 1
+    rng = np.random.default_rng(2)
+    vecs = {}
+    for l in range(L + 1):
+        pl, n = planes(s1, l)
+        for key in ("u", "f"):
+            g = s1.new_grid(l)
+            g.copy_(torch.from_numpy(rng.standard_normal(g.numel())))
+            sk = s1.new_skel(l)
+            s1.skel_from_grid(l, g, sk)        # zero on non-free entries
+            vecs[(key, l)] = sk
+    ref = {}
+    for l in range(L + 1):
+        r = s1.new_skel(l)
+        s1.residual(l, vecs[("u", l)], vecs[("f", l)], r)
+        ref[("res", l)] = r.cpu().numpy()
+        u = vecs[("u", l)].clone()
+        s1.smooth(l, vecs[("f", l)], u)
+        ref[("smooth", l)] = u.cpu().numpy()
+        if l >= 1:
+            fc = s1.new_skel(l - 1)
+            s1.restrict(l, vecs[("f", l)], fc)
+            ref[("restrict", l)] = fc.cpu().numpy()
+            uf = vecs[("u", l)].clone()
+            s1.prolong(l, vecs[("u", l - 1)], uf)
+            ref[("prolong", l)] = uf.cpu().numpy()
+    uv = vecs[("u", L)].clone()
+    s1.vcycle(uv, vecs[("f", L)])
+    ref["vcycle"] = uv.cpu().numpy()
+    host = {k: v.cpu().numpy() for k, v in vecs.items()}
+    plen = {l: planes(s1, l)[0] for l in range(L + 1)}
+    s1.close()
+
+    def fn(s, r):
+        sl = s.slab
+        out = {}
+
+        def loc(key, l):
+            a = host[(key, l)].reshape(-1, plen[l])[sl["zb"]:sl["z1"] + 1]
+            return torch.from_numpy(a.reshape(-1).copy()).cuda()
+        for l in range(L + 1):
+            rr = s.new_skel(l)
+            s.residual(l, loc("u", l), loc("f", l), rr)
+            out[("res", l)] = rr
+            u = loc("u", l)
+            s.smooth(l, loc("f", l), u)
+            out[("smooth", l)] = u
+            if l >= 1:
+                fc = s.new_skel(l - 1)
+                s.restrict(l, loc("f", l), fc)
+                out[("restrict", l)] = fc
+                uf = loc("u", l)
+                s.prolong(l, loc("u", l - 1), uf)
+                out[("prolong", l)] = uf
+        uv = loc("u", L)
+        s.vcycle(uv, loc("f", L))
+        out["vcycle"] = uv
+        torch.cuda.current_stream().synchronize()
+        return sl, {k: v.cpu().numpy() for k, v in out.items()}
+
+    res = run_ranks(nr, case, fn, coarse_rtol=1e-13)
+    for sl, out in res:
+        for key, val in out.items():
+            l = L if key == "vcycle" else (key[1] - 1 if key[0] == "restrict" else key[1])
+            P = plen[l]
+            want = ref[key].reshape(-1, P)[sl["zb"]:sl["z1"] + 1]
+            got = val.reshape(-1, P)
+            # every local plane, ghosts included, is refreshed after each call
+            assert np.array_equal(got, want), (key, sl, np.abs(got - want).max())
