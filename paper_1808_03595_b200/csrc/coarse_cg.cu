@@ -339,6 +339,146 @@ __global__ void __launch_bounds__(256) k_pcg_coop_reg_p2(LevelGeom g, CoarseTabs
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Pipelined (single-reduction) Jacobi-PCG, Ghysels & Vanroose's recurrence: the same Krylov
+// iterates as k_pcg_coop_reg_p2 in exact arithmetic (reading R11: "CG" on the coarse level,
+// P:440), but every iteration needs ONE grid barrier instead of two: the dot products
+// (r,u), (w,u), (r,r) of iteration i and the publication of m_i = D^-1 w_i share it, and the
+// operator application n_i = H m_i runs after it, overlapping nothing but needing nothing else.
+//   r0 = b, u0 = D^-1 r0, w0 = H u0;  per iteration:
+//     gamma = (r,u), delta = (w,u), rho = (r,r)          [barrier]   stop if sqrt(rho) <= rtol |b|
+//     m = D^-1 w (published before the barrier), n = H m
+//     beta = gamma / gamma_old, alpha = gamma / (delta - beta gamma / alpha_old)   (first: 0, gamma/delta)
+//     z = n + beta z, q = m + beta q, s = w + beta s, p = u + beta p
+//     x += alpha p, r -= alpha s, u -= alpha q, w -= alpha z
+// Stops at the first iterate with ||r|| <= rtol ||b||, as the oracle's pcg().  m is double-
+// buffered (iteration parity) because neighbours may still read m_i while m_(i+1) is written;
+// so are the per-block partial sums.  Used when the requested coarse tolerance is >= 1e-11 (the
+// recurrence's attainable accuracy is a few orders above the standard one's); tighter requests
+// (the 1e-13 parity runs) take the two-barrier kernel.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void block_reduce3(double a, double b, double c, double* red, int nb_part_slot,
+                                              double* pa, double* pb, double* pc) {
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
+    c += __shfl_down_sync(0xffffffffu, c, o);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+  __syncthreads();
+  if (lane == 0) { red[w] = a; red[32 + w] = b; red[64 + w] = c; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sa = 0.0, sb = 0.0, sc = 0.0;
+    for (int i = 0; i < nw; ++i) { sa += red[i]; sb += red[32 + i]; sc += red[64 + i]; }
+    pa[nb_part_slot] = sa;
+    pb[nb_part_slot] = sb;
+    pc[nb_part_slot] = sc;
+  }
+}
+
+__device__ __forceinline__ void grid_totals3(const double* pa, const double* pb, const double* pc, int nb, double* red,
+                                             double& ta, double& tb, double& tc) {
+  double a = 0.0, b = 0.0, c = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    a += __ldcg(&pa[i]);
+    b += __ldcg(&pb[i]);
+    c += __ldcg(&pc[i]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+  __syncthreads();
+  if (lane == 0) { red[w] = a; red[32 + w] = b; red[64 + w] = c; }
+  __syncthreads();
+  double sa = 0.0, sb = 0.0, sc = 0.0;
+  for (int i = 0; i < nw; ++i) { sa += red[i]; sb += red[32 + i]; sc += red[64 + i]; }
+  ta = sa; tb = sb; tc = sc;
+}
+
+__global__ void __launch_bounds__(256) k_pcg_gv_p2(LevelGeom g, CoarseTabs ct, const double* __restrict__ b,
+                                                  double* __restrict__ xout, double* __restrict__ mbuf,
+                                                  const double* __restrict__ dinv, double lam,
+                                                  double* __restrict__ part, PcgState* st, double rtol, int maxit) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[96];
+  const int nb = gridDim.x;
+  const long long n = g.nskel;
+  double* mb[2] = {mbuf, mbuf + n};                 // m_i in mb[i & 1]; u0 is published in mb[1]
+  double* pt[2][3] = {{part, part + nb, part + 2 * nb}, {part + 3 * nb, part + 4 * nb, part + 5 * nb}};
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool own = i < n;
+  const double bi = own ? b[i] : 0.0, di = own ? dinv[i] : 0.0;
+  int jx[kRowLen];
+  double arow[kRowLen];
+  build_row(g, ct, own ? i : 0, lam, jx, arow);
+  auto apply = [&](const double* v) {
+    double zl[kRowLen];
+#pragma unroll
+    for (int k = 0; k < kRowLen; ++k) zl[k] = __ldcg(&v[jx[k]]);
+    double h = 0.0;
+#pragma unroll
+    for (int k = 0; k < kRowLen; ++k) h = fma(arow[k], zl[k], h);
+    return h;
+  };
+  double x = 0.0, r = bi, u = di * bi;
+  if (own) mb[1][i] = u;
+  grid.sync();
+  double w = own ? apply(mb[1]) : 0.0;
+  double m = di * w;
+  if (own) mb[0][i] = m;
+  block_reduce3(r * u, w * u, r * r, red, blockIdx.x, pt[0][0], pt[0][1], pt[0][2]);
+  grid.sync();
+  double z = 0.0, q = 0.0, s = 0.0, pv = 0.0;
+  double gamma_old = 1.0, alpha_old = 1.0, bb = -1.0;
+  int its = 0, breakdown = 0;
+  for (int it = 0;; ++it) {
+    // n_i = H m_i is issued first: its L2 loads overlap the partial-sum loads of grid_totals3
+    const double nv = own ? apply(mb[it & 1]) : 0.0;
+    double gamma, delta, rho;
+    grid_totals3(pt[it & 1][0], pt[it & 1][1], pt[it & 1][2], nb, red, gamma, delta, rho);
+    if (it == 0) bb = rho;                            // ||b||^2 (r0 = b)
+    if (bb == 0.0 || sqrt(rho) <= rtol * sqrt(bb) || its >= maxit) break;
+    double alpha, beta;
+    if (it == 0) {
+      beta = 0.0;
+      alpha = gamma / delta;
+      if (!(delta > 0.0)) { breakdown = 1; break; }
+    } else {
+      beta = gamma / gamma_old;
+      const double den = delta - beta * gamma / alpha_old;
+      if (!(den > 0.0)) { breakdown = 1; break; }
+      alpha = gamma / den;
+    }
+    z = fma(beta, z, nv);
+    q = fma(beta, q, m);
+    s = fma(beta, s, w);
+    pv = fma(beta, pv, u);
+    x = fma(alpha, pv, x);
+    r = fma(-alpha, s, r);
+    u = fma(-alpha, q, u);
+    w = fma(-alpha, z, w);
+    m = di * w;
+    if (own) mb[(it + 1) & 1][i] = m;
+    ++its;
+    gamma_old = gamma;
+    alpha_old = alpha;
+    block_reduce3(r * u, w * u, r * r, red, blockIdx.x, pt[(it + 1) & 1][0], pt[(it + 1) & 1][1], pt[(it + 1) & 1][2]);
+    grid.sync();
+  }
+  if (own) xout[i] = x;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->its = its;
+    st->its_sum += its;
+    if (breakdown) st->breakdown = 1;
+    st->done = 1;
+    st->bb = bb;
+  }
+}
+
 // Two grid barriers per iteration: with p_new = z + beta p and q = H_hat p,
 //   q_new = H_hat z + beta q_old,
 // so the direction update, the operator application (on z, complete after the previous barrier)

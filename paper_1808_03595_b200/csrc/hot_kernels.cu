@@ -1091,7 +1091,7 @@ template <int P> struct StarPfCfg {
   static constexpr int NW = 4, NT = 128, MINB = 5;
   static constexpr int GS = NP, GPW = 32 / GS, NG = NW * GPW, A3IT = (N + NG - 1) / NG;
   static constexpr int oFT = 0, oX = 3 * MS, oG = 6 * MS, oS = 9 * MS, oU = 12 * MS, oVec = oU + 3 * NN,
-                       total = oVec + 9 * N;
+                       oBase = oVec + 9 * N, total = oBase + 8;
   static_assert(NW * NN <= 3 * MS, "G3 warp partials must fit in the X buffer");
 };
 
@@ -1124,38 +1124,54 @@ __global__ void __launch_bounds__(StarPfCfg<P>::NT, StarPfCfg<P>::MINB)
   // interior stars (the common case) touch only inside, free points: no per-point tests
   const bool interior = v1 > 0 && v2 > 0 && v3 > 0 && v1 < g.k1 && v2 < g.k2 && v3 + g.zoff < g.K3;
   const StarMap<P>& map = kStarMap<P>;
-  // point of map entry e: record coordinate w_d = v_d - bit; inside the stored box iff w_d >= 0,
-  // free iff (w_d > 0 or t_d > 0) and w_d < k_d
-  auto pt_inside = [&](unsigned e) {
-    return !((v1 == 0 && (e & (1u << 12))) || (v2 == 0 && (e & (1u << 13))) || (v3 == 0 && (e & (1u << 14))));
-  };
-  auto pt_free = [&](unsigned e) {   // global test; w3 + zoff is the global record plane
+  // point of map entry e: record coordinate w_d = v_d - bit; free iff (w_d > 0 or t_d > 0) and
+  // w_d < k_d (global in z); stored (readable) iff w_d >= 0
+  auto pt_free = [&](unsigned e) {
     const int w1 = v1 - (int)((e >> 12) & 1u), w2 = v2 - (int)((e >> 13) & 1u), w3 = v3 - (int)((e >> 14) & 1u);
     const int W3 = w3 + g.zoff;
     return w1 >= 0 && w2 >= 0 && w3 >= 0 && (w1 > 0 || !(e & (1u << 15))) && (w2 > 0 || !(e & (1u << 16))) &&
            (W3 > 0 || !(e & (1u << 17))) && w1 < g.k1 && w2 < g.k2 && W3 < g.K3;
   };
-  auto pt_index = [&](unsigned e) { return (rec0 - rec_delta(e, g.V1, V12)) * RS + (e & 0xFFFu); };
-  // group 0: S (padded with zeros), eigen/weight vectors, r planes (zero outside the box / padding)
-  for (int i = tid; i < 3 * NP * NP; i += NT) {
-    const int d = i / (NP * NP), rr = i - d * NP * NP, A = rr / NP, B = rr - A * NP;
-    const bool in = A < N && B < N;
-    cp_async8(&Ssm[d * MS + A * LD + B], &stab[row[d] * ST + (in ? A * N + B : 0)], in);
-    const unsigned e = in ? map.v[d * NN + A * N + B] : 0u;
-    const bool ok = in && (interior || pt_inside(e));
-    cp_async8(&FT[d * MS + A * LD + B], &r[ok ? pt_index(e) : 0], ok);
+  // record base index of each of the 8 record-offset codes (-1: record outside the stored box)
+  long long* s_base = reinterpret_cast<long long*>(sm + C::oBase);
+  if (tid < 8) {
+    const int b1 = tid & 1, b2 = (tid >> 1) & 1, b3 = (tid >> 2) & 1;
+    const bool ok = !((v1 == 0 && b1) || (v2 == 0 && b2) || (v3 == 0 && b3));
+    s_base[tid] = ok ? (rec0 - (b1 + g.V1 * (long long)b2 + V12 * b3)) * RS : -1LL;
   }
-  for (int i = tid; i < 9 * N; i += NT) { const int d = i / (3 * N); cp_async8(&vec[i], &stab[row[d] * ST + NN + i - d * 3 * N], true); }
+  const size_t srow[3] = {row[0] * ST, row[1] * ST, row[2] * ST};
+  __syncthreads();
+  // group 0: S rows, eigen/weight vectors, the r planes
+  for (int i = tid; i < 3 * NN; i += NT) {
+    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
+    cp_async8(&Ssm[d * MS + A * LD + B], &stab[srow[d] + rr], true);
+    const unsigned e = map.v[i];
+    const long long base = s_base[(e >> 12) & 7u];
+    const bool ok = base >= 0;
+    cp_async8(&FT[d * MS + A * LD + B], &r[ok ? base + (e & 0xFFFu) : 0], ok);
+  }
+  for (int i = tid; i < 9 * N; i += NT) { const int d = i / (3 * N); cp_async8(&vec[i], &stab[srow[d] + NN + i - d * 3 * N], true); }
   cp_async_commit();
   // group 1: the u entries this star updates (0 where the point is not free)
   for (int i = tid; i < 3 * NN; i += NT) {
     const unsigned e = map.v[i];
-    const bool ok = interior || pt_free(e);
-    cp_async8(&Up[i], &u[ok ? pt_index(e) : 0], ok);
+    const long long base = s_base[(e >> 12) & 7u];
+    const bool ok = base >= 0 && (interior || pt_free(e));
+    cp_async8(&Up[i], &u[ok ? base + (e & 0xFFFu) : 0], ok);
   }
   cp_async_commit();
-  // zero G (the padding must be finite for the back transforms)
-  for (int i = tid; i < 3 * MS; i += NT) Gs[i] = 0.0;
+  // zero the padding rows / columns of F, S and G (the transforms read them; must be finite)
+  constexpr int PADN = NP * NP - NN, PC = NP - N;   // columns N.. of rows < N, then rows N..
+  for (int i = tid; i < 3 * PADN; i += NT) {
+    const int d = i / PADN, k = i - d * PADN;
+    int A, B;
+    if (k < N * PC) { A = k / PC; B = N + (k - A * PC); }
+    else { const int k2 = k - N * PC; A = N + k2 / NP; B = k2 - (A - N) * NP; }
+    const int o = d * MS + A * LD + B;
+    FT[o] = 0.0;
+    Ssm[o] = 0.0;
+    Gs[o] = 0.0;
+  }
   cp_async_wait<1>();
   __syncthreads();
   // inverse multiplicity on the two lines through the vertex of each plane
@@ -1264,7 +1280,7 @@ __global__ void __launch_bounds__(StarPfCfg<P>::NT, StarPfCfg<P>::MINB)
     else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
     const unsigned e = map.v[i];
     if (!interior && !pt_free(e)) continue;
-    u[pt_index(e)] = fma(w1[j1] * w2[j2] * w3[j3], Gs[d * MS + A * LD + B], Up[i]);
+    u[s_base[(e >> 12) & 7u] + (e & 0xFFFu)] = fma(w1[j1] * w2[j2] * w3[j3], Gs[d * MS + A * LD + B], Up[i]);
   }
 }
 
@@ -1486,6 +1502,71 @@ __global__ void __launch_bounds__(ElemPfCfg<P>::NT, ElemPfCfg<P>::MINB)
 }
 
 // ------------------------------------------------------------------------------------------
+// residual gather, degree-templated: one block per vertex record (3-D grid, no index division),
+// one thread per record slot.  Same sums in the same order as k_gather_resid (kernels.cu):
+// r = F - sum over the elements sharing the point of their outputs Y.
+// ------------------------------------------------------------------------------------------
+template <int P>
+__global__ void __launch_bounds__(256) k_gather_resid_t(LevelGeom g, const double* __restrict__ Y,
+                                                        const double* __restrict__ F, double* __restrict__ out,
+                                                        const int* __restrict__ done) {
+  if (done && *done) return;
+  constexpr int m = P - 1, mm = m * m, RS = 3 * mm + 3 * m + 1, YS = 6 * mm + 12 * m + 8;
+  const int v1 = blockIdx.x, v2 = blockIdx.y, v3 = blockIdx.z;
+  const long long rec = v1 + (long long)g.V1 * (v2 + (long long)g.V2 * v3);
+  const bool own = owned_plane(g, v3);
+  auto el = [&](int a1, int a2, int a3) -> size_t {
+    return ((size_t)a1 + (size_t)g.k1 * ((size_t)a2 + (size_t)g.k2 * a3)) * YS;
+  };
+  for (int o = threadIdx.x; o < RS; o += blockDim.x) {
+    int t1 = 0, t2 = 0, t3 = 0, type, a = 0, b = 0;
+    if (o < 3 * mm) {
+      type = o / mm;
+      const int rr = o - type * mm;
+      a = rr / m; b = rr - a * m;
+      if (type == 0) { t3 = a + 1; t2 = b + 1; } else if (type == 1) { t3 = a + 1; t1 = b + 1; } else { t2 = a + 1; t1 = b + 1; }
+    } else if (o < 3 * mm + 3 * m) {
+      const int rr = o - 3 * mm, d = rr / m;
+      type = 3 + d;
+      a = rr - d * m;
+      if (d == 0) t1 = a + 1; else if (d == 1) t2 = a + 1; else t3 = a + 1;
+    } else {
+      type = 6;
+    }
+    double r = 0.0;
+    if (own && is_free(g, v1 * P + t1, v2 * P + t2, v3 * P + t3)) {
+      double s_ = 0.0;
+      if (type < 3) {
+        const int d = type, oo = a * m + b;
+        int w1 = v1, w2 = v2, w3 = v3;
+        if (d == 0) w1 -= 1; else if (d == 1) w2 -= 1; else w3 -= 1;
+        s_ = Y[el(w1, w2, w3) + (2 * d + 1) * mm + oo] + Y[el(v1, v2, v3) + (2 * d) * mm + oo];
+      } else if (type < 6) {
+        const int d = type - 3;
+        for (int bB = 0; bB < 2; ++bB)
+          for (int bA = 0; bA < 2; ++bA) {
+            int a1 = v1, a2 = v2, a3 = v3;
+            if (d == 0) { a2 += bA - 1; a3 += bB - 1; }
+            else if (d == 1) { a1 += bA - 1; a3 += bB - 1; }
+            else { a1 += bA - 1; a2 += bB - 1; }
+            const int qe = 4 * d + (1 - bA) + 2 * (1 - bB);
+            s_ += Y[el(a1, a2, a3) + 6 * mm + qe * m + a];
+          }
+      } else {
+        for (int c3 = 0; c3 < 2; ++c3)
+          for (int c2 = 0; c2 < 2; ++c2)
+            for (int c1 = 0; c1 < 2; ++c1) {
+              const int qv = (1 - c1) + 2 * (1 - c2) + 4 * (1 - c3);
+              s_ += Y[el(v1 - 1 + c1, v2 - 1 + c2, v3 - 1 + c3) + 6 * mm + 12 * m + qv];
+            }
+      }
+      r = F ? F[rec * RS + o] - s_ : s_;
+    }
+    out[rec * RS + o] = r;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // dispatch
 // ------------------------------------------------------------------------------------------
 constexpr bool kStarSinglePass(int p) { return p <= 8; }
@@ -1553,6 +1634,24 @@ cudaError_t launch_elem_apply(const LevelGeom& g, const double* u, const double*
   case P:                                                                                           \
     launch_elem_p<P>(g, u, etab, lam, Y, done, st);                                                \
     break;
+    PMG_DEGREES(CASE)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_resid(const LevelGeom& g, const double* Y, const double* F, double* out, const int* done,
+                                cudaStream_t st) {
+  const dim3 grid((unsigned)g.V1, (unsigned)g.V2, (unsigned)g.V3);
+  switch (g.p) {
+#define CASE(P)                                                                                     \
+  case P: {                                                                                         \
+    constexpr int RS = 3 * (P - 1) * (P - 1) + 3 * (P - 1) + 1;                                     \
+    const int nt = RS < 64 ? 64 : (RS < 128 ? 128 : 256);                                           \
+    k_gather_resid_t<P><<<grid, nt, 0, st>>>(g, Y, F, out, done);                                   \
+    break;                                                                                          \
+  }
     PMG_DEGREES(CASE)
 #undef CASE
     default: return cudaErrorInvalidValue;

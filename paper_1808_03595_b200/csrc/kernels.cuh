@@ -16,6 +16,8 @@ cudaError_t launch_elem_apply(const LevelGeom& g, const double* u, const double*
                               const int* done, cudaStream_t st);
 cudaError_t launch_star(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c, long long nb, const double* r,
                         double* u, const double* stab, const double* stabT, double lam, cudaStream_t st);
+cudaError_t launch_gather_resid(const LevelGeom& g, const double* Y, const double* F, double* out, const int* done,
+                                cudaStream_t st);
 size_t hot_smem(int p, int which);   // which: 0 element, 1 star
 cudaError_t hot_set_smem_attr(int bytes);
 
@@ -30,6 +32,8 @@ __global__ void k_pcg_coop_p2(LevelGeom g, CoarseTabs ct, const double* b, doubl
                               double rtol, int maxit);
 __global__ void k_pcg_coop_reg_p2(LevelGeom g, CoarseTabs ct, const double* b, double* xout, double* zpub,
                                   const double* dinv, double lam, double* part, PcgState* st, double rtol, int maxit);
+__global__ void k_pcg_gv_p2(LevelGeom g, CoarseTabs ct, const double* b, double* xout, double* mbuf,
+                            const double* dinv, double lam, double* part, PcgState* st, double rtol, int maxit);
 __global__ void k_pcg_cluster_p2(LevelGeom g, CoarseTabs ct, const double* b, double* xout, const double* dinv,
                                  double lam, int chunk, int halo, unsigned long long inv, PcgState* st, double rtol,
                                  int maxit);

@@ -89,6 +89,8 @@ struct pmg_ctx {
   bool use_coop = false;     // coarse CG as one persistent cooperative kernel (p0 = 2)
   int coop_nb = 0;
   bool coop_reg = false;     // register-resident variant (one coarse unknown per thread)
+  bool coop_gv = false;      // register-resident pipelined variant (one grid barrier per iteration)
+  double* cgm = nullptr;     // its double-buffered m vector (2 n0)
   double* ctab[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // CoarseTabs storage
   double* cV = nullptr;      // (unused)
   cudaGraphExec_t cycle_exec = nullptr;   // captured solve cycle (V-cycle + residual + norm^2)
@@ -174,7 +176,10 @@ pmg_status residual_dev(pmg_ctx* c, int l, const double* u, const double* f, dou
     launch_elem_apply(D.g, u, D.etab, c->lam, c->Y, done, c->st);
   }
   LAUNCH_CHECK(c);
-  k_gather_resid<<<grid_for(D.g.nskel), kThreads, 0, c->st>>>(D.g, c->Y, f, r, done);
+  if (c->ref_kernels)
+    k_gather_resid<<<grid_for(D.g.nskel), kThreads, 0, c->st>>>(D.g, c->Y, f, r, done);
+  else
+    launch_gather_resid(D.g, c->Y, f, r, done, c->st);
   LAUNCH_CHECK(c);
   return PMG_OK;
 }
@@ -300,7 +305,11 @@ pmg_status pcg_dev(pmg_ctx* c, const double* b, double* x) {
     void* args[] = {&g0, &ct, (void*)&b, &x, &c->cr, &c->cz, &c->cp, &c->cq, (void*)&dinv, &lam, &part,
                     &st, &rtol, &maxit};
     void* args_reg[] = {&g0, &ct, (void*)&b, &x, &c->cz, (void*)&dinv, &lam, &part, &st, &rtol, &maxit};
-    const void* fn = c->coop_reg ? (const void*)k_pcg_coop_reg_p2 : (const void*)k_pcg_coop_p2;
+    void* args_gv[] = {&g0, &ct, (void*)&b, &x, &c->cgm, (void*)&dinv, &lam, &part, &st, &rtol, &maxit};
+    // the pipelined recurrence for the performance tolerance; the two-barrier kernel for the very
+    // tight parity tolerances (attainable accuracy, see coarse_cg.cu)
+    const bool gv = c->coop_gv && rtol >= 1e-11;
+    const void* fn = gv ? (const void*)k_pcg_gv_p2 : (c->coop_reg ? (const void*)k_pcg_coop_reg_p2 : (const void*)k_pcg_coop_p2);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c->coop_nb);
     cfg.blockDim = dim3(kThreads);
@@ -311,7 +320,7 @@ pmg_status pcg_dev(pmg_ctx* c, const double* b, double* x) {
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CUDA_CHECK(cudaLaunchKernelExC(&cfg, fn, c->coop_reg ? args_reg : args));
+    CUDA_CHECK(cudaLaunchKernelExC(&cfg, fn, gv ? args_gv : (c->coop_reg ? args_reg : args)));
     c->launches++;
     return PMG_OK;
   }
@@ -564,6 +573,7 @@ void free_ctx(pmg_ctx* c) {
     cudaFree(D.etab); cudaFree(D.stab); cudaFree(D.Jint); cudaFree(D.u); cudaFree(D.f); cudaFree(D.r);
   }
   cudaFree(c->Y); cudaFree(c->Z); cudaFree(c->cube); cudaFree(c->part); cudaFree(c->dres); cudaFree(c->pcg);
+  cudaFree(c->cgm);
   cudaFree(c->cx); cudaFree(c->cr); cudaFree(c->cz); cudaFree(c->cp); cudaFree(c->cq); cudaFree(c->dinv);
   for (int d = 0; d < 3; ++d) cudaFree(c->bm[d]);
   cudaFree(c->Fdev); cudaFree(c->Udev);
@@ -738,7 +748,7 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
     free_ctx(c);
     return fail(PMG_EINVAL, "shared-memory plan exceeds the device limit for this p");
   }
-  if (dalloc(&c->Y, Ylen) || dalloc(&c->Z, Zlen) || dalloc(&c->part, 4096) || dalloc(&c->dres, 8) ||
+  if (dalloc(&c->Y, Ylen) || dalloc(&c->Z, Zlen) || dalloc(&c->part, 16384) || dalloc(&c->dres, 8) ||
       dalloc(&c->pcg, 1)) {
     free_ctx(c);
     return fail(PMG_ENOMEM, "cudaMalloc failed (workspaces)");
@@ -861,6 +871,12 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
         if (!(re && re[0] == '0') && per_sm_reg > 0 && need <= std::min<long long>((long long)per_sm_reg * nsm, 1344)) {
           c->coop_reg = true;
           c->coop_nb = (int)need;
+          int per_sm_gv = 0;
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_gv, k_pcg_gv_p2, kThreads, 0);
+          const char* ge = std::getenv("PMG_COARSE_GV");
+          if (!(ge && ge[0] == '0') && per_sm_gv > 0 && need <= (long long)per_sm_gv * nsm &&
+              dalloc(&c->cgm, 2 * c->g0g.nskel) == cudaSuccess)
+            c->coop_gv = true;
         }
       }
       const char* nbenv = std::getenv("PMG_COOP_BLOCKS");   // tuning experiments only

@@ -244,3 +244,41 @@ def test_coarse_cg_paths_agree(name, monkeypatch):
         s.close()
     assert rel(outs[0], outs[1]) < 1e-11
     assert rel(outs[0], P.orc.vcycle(np.zeros_like(f), f)) < OP_TOL
+
+
+@pytest.mark.parametrize("name", ["k323_p4_lam1.7_stretched", "k333_p8_lam0", "k332_p2_lam0"])
+def test_pipelined_coarse_cg_matches_standard(name, monkeypatch):
+    """The single-barrier (pipelined) coarse CG used at the performance tolerance reproduces the
+    standard two-barrier Jacobi-PCG: same coarse iteration count over a solve (+-1 per coarse
+    solve), and V-cycle outputs that agree to the coarse tolerance's accuracy; against the oracle's
+    standard PCG V-cycle at the same tolerance likewise."""
+    import paper_1808_03595_b200 as pmg
+    from oracle import mg
+    P = pair(name)
+    case = P.case
+    L = P.gpu.nlevels - 1
+    f = P.rand_skel(L)
+    outs, its = [], []
+    for env in ("1", "0"):
+        monkeypatch.setenv("PMG_COARSE_GV", env)
+        s = pmg.Solver(case.k, case.widths, case.p, case.lam, coarse_rtol=1e-10)
+        u = s.new_skel(L)
+        fs = torch.from_numpy(np.ascontiguousarray(f)).cuda()
+        fh = s.new_skel(L)
+        s.skel_from_grid(L, fs, fh)
+        s.vcycle(u, fh)
+        g = s.new_grid(L)
+        s.skel_to_grid(L, u, g)
+        F = torch.from_numpy(np.ascontiguousarray(P.rng.standard_normal(g.numel()))).cuda()
+        Fw = s.new_grid(L)
+        s.weak_rhs(F, Fw)
+        ug = s.new_grid(L)
+        rep = s.solve(Fw, ug, 1e-10)
+        torch.cuda.synchronize()
+        outs.append(g.cpu().numpy())
+        its.append((rep["coarse_iters"], rep["cycles"]))
+        s.close()
+    assert rel(outs[0], outs[1]) < 1e-7
+    assert its[0][1] == its[1][1] and abs(its[0][0] - its[1][0]) <= its[0][1] + 1, its
+    orc = mg.Hierarchy(case.k, case.widths, case.p, case.lam, coarse_rtol=1e-10)
+    assert rel(outs[0], orc.vcycle(np.zeros_like(f), f)) < 1e-7
