@@ -141,3 +141,41 @@ class Hierarchy:
         rep = dict(cycles=cycles, r0=r0, r_final=rn, rho=rho, history=hist,
                    converged=bool(rn <= rtol * r0), u_hat=u, f_hat=fhat)
         return u_full, rep
+
+    def solve_ipcg(self, F, rtol=1e-10, max_iters=50):
+        """Alg. 5, Krylov-accelerated multigrid, verbatim: inexact preconditioned CG
+        (Golub & Ye) with one V-cycle from zero as the preconditioner.  kMG with schedule 0, kvMG
+        with schedule 1.  Stopping test as Alg. 4 (reading R12): ||r|| <= rtol ||r_0||.
+        Returns (u_full, report dict) like solve()."""
+        top = self.levels[-1]
+        op = top.op
+        fhat = op.condense(F)
+        u = np.zeros(top.mesh.ntot)
+        r = op.residual(u, fhat)                       # initial residual
+        s = r.copy()                                   # ensures beta = 0 on the first iteration
+        p = np.zeros_like(r)
+        delta = 1.0
+        r0 = math.sqrt(float(r @ r))
+        hist = [r0]
+        its = 0
+        rn = r0
+        while rn > rtol * r0 and its < max_iters:
+            z = self.vcycle(np.zeros_like(r), r)        # preconditioner
+            gamma = float(z @ r)
+            gamma0 = float(z @ s)
+            beta = (gamma - gamma0) / delta
+            delta = gamma
+            p = beta * p + z                            # update search vector
+            q = op.apply(p)                             # effect of p
+            alpha = gamma / float(q @ p)                # step width
+            s = r.copy()                                # save old residual
+            u = u + alpha * p
+            r = r - alpha * q
+            rn = math.sqrt(float(r @ r))
+            hist.append(rn)
+            its += 1
+        rho = (rn / r0) ** (1.0 / its) if its and r0 > 0 else 0.0
+        u_full = op.recover(u, F)
+        rep = dict(cycles=its, r0=r0, r_final=rn, rho=rho, history=hist,
+                   converged=bool(rn <= rtol * r0), u_hat=u, f_hat=fhat)
+        return u_full, rep

@@ -1085,14 +1085,16 @@ __device__ __forceinline__ void dmma_tile_t(const double* A, const double* B, do
   Cm[(8 * mi + r) * LD + 8 * ni + 2 * q + 1] = c1;
 }
 
+// p <= 8: n_S padded to 8 / 16, 4 warps, 5 CTAs per SM; 9 <= p <= 16: n_S padded to 32, 8 warps
+// (lanes own a1, each warp one a3 group), one CTA per SM, G3 warp partials in their own buffer
 template <int P> struct StarPfCfg {
   static constexpr int N = 2 * P - 1, NN = N * N, C = P - 1;
-  static constexpr int NP = (N <= 8) ? 8 : 16, LD = NP + 4, MS = NP * LD, TPP = (NP / 8) * (NP / 8);
-  static constexpr int NW = 4, NT = 128, MINB = 5;
+  static constexpr int NP = (N <= 8) ? 8 : (N <= 16 ? 16 : 32), LD = NP + 4, MS = NP * LD, TPP = (NP / 8) * (NP / 8);
+  static constexpr int NW = (P <= 8) ? 4 : 8, NT = 32 * NW, MINB = (P <= 8) ? 5 : 1;
   static constexpr int GS = NP, GPW = 32 / GS, NG = NW * GPW, A3IT = (N + NG - 1) / NG;
+  static constexpr bool P3SEP = NW * NN > 3 * MS;
   static constexpr int oFT = 0, oX = 3 * MS, oG = 6 * MS, oS = 9 * MS, oU = 12 * MS, oVec = oU + 3 * NN,
-                       oBase = oVec + 9 * N, total = oBase + 8;
-  static_assert(NW * NN <= 3 * MS, "G3 warp partials must fit in the X buffer");
+                       oBase = oVec + 9 * N, oP3 = P3SEP ? oBase + 8 : oX, total = P3SEP ? oP3 + NW * NN : oBase + 8;
 };
 
 template <int P>
@@ -1245,16 +1247,17 @@ __global__ void __launch_bounds__(StarPfCfg<P>::NT, StarPfCfg<P>::MINB)
 #pragma unroll
       for (int a2 = 0; a2 < N; ++a2) g3[a2] += __shfl_xor_sync(0xffffffffu, g3[a2], off);
     }
+    double* P3 = sm + C::oP3;
     if (va && lane < GS) {
 #pragma unroll
-      for (int a2 = 0; a2 < N; ++a2) X[warp * NN + a2 * N + a1] = g3[a2];
+      for (int a2 = 0; a2 < N; ++a2) P3[warp * NN + a2 * N + a1] = g3[a2];
     }
     __syncthreads();
     for (int i = tid; i < NN; i += NT) {
       const int a2 = i / N, a1_ = i - a2 * N;
       double s_ = 0.0;
 #pragma unroll
-      for (int w = 0; w < C::NW; ++w) s_ += X[w * NN + i];
+      for (int w = 0; w < C::NW; ++w) s_ += P3[w * NN + i];
       Gs[2 * MS + a2 * LD + a1_] = s_;
     }
   }
@@ -1569,7 +1572,8 @@ __global__ void __launch_bounds__(256) k_gather_resid_t(LevelGeom g, const doubl
 // ------------------------------------------------------------------------------------------
 // dispatch
 // ------------------------------------------------------------------------------------------
-constexpr bool kStarSinglePass(int p) { return p <= 8; }
+constexpr bool kStarSinglePass(int p) { return p <= 8; }   // k_star_sp / k_star_dm variants
+constexpr bool kStarPf(int p) { return p <= 16; }          // k_star_pf (default up to p = 16)
 
 // star kernel variant for p <= 8 (A/B experiments): 0 prefetching DMMA kernel k_star_pf (default),
 // 1 DFMA transforms (k_star_sp), 2 DMMA transforms without prefetch (k_star_dm)
@@ -1612,7 +1616,9 @@ void launch_elem_p(const LevelGeom& g, const double* u, const double* etab, doub
 template <int P>
 void launch_star_p(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c, long long nb, const double* r,
                    double* u, const double* stab, const double* stabT, double lam, cudaStream_t st) {
-  if constexpr (kStarSinglePass(P)) {
+  if constexpr (kStarPf(P) && !kStarSinglePass(P)) {
+    k_star_pf<P><<<(unsigned)nb, StarPfCfg<P>::NT, star_pf_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, lam);
+  } else if constexpr (kStarSinglePass(P)) {
     const int v = star_variant();
     if (v == 0)
       k_star_pf<P><<<(unsigned)nb, StarPfCfg<P>::NT, star_pf_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, lam);
@@ -1676,7 +1682,7 @@ cudaError_t launch_star(const LevelGeom& g, int c1, int c2, int c3, int n1c, int
 size_t hot_smem(int p, int which) {
   switch (p) {
 #define CASE(P) \
-  case P: return which == 0 ? std::max(elem_t_smem<P>(), std::max(elem_dm_smem<(P <= 8 ? P : 2)>(), elem_pf_smem<(P <= 8 ? P : 2)>())) : (kStarSinglePass(P) ? std::max(std::max(star_sp_smem<(P <= 8 ? P : 2)>(), star_dm_smem<(P <= 8 ? P : 2)>()), star_pf_smem<(P <= 8 ? P : 2)>()) : star_t_smem<P>());
+  case P: return which == 0 ? std::max(elem_t_smem<P>(), std::max(elem_dm_smem<(P <= 8 ? P : 2)>(), elem_pf_smem<(P <= 8 ? P : 2)>())) : (kStarSinglePass(P) ? std::max(std::max(star_sp_smem<(P <= 8 ? P : 2)>(), star_dm_smem<(P <= 8 ? P : 2)>()), star_pf_smem<(P <= 8 ? P : 2)>()) : (kStarPf(P) ? star_pf_smem<(P <= 16 ? P : 2)>() : star_t_smem<P>()));
     PMG_DEGREES(CASE)
 #undef CASE
     default: return 0;
@@ -1697,8 +1703,8 @@ cudaError_t hot_set_smem_attr(int bytes) {
       b = cudaFuncSetAttribute(k_star_sp<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (b == cudaSuccess && kStarSinglePass(P))                                                        \
       b = cudaFuncSetAttribute(k_star_dm<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
-    if (b == cudaSuccess && kStarSinglePass(P))                                                        \
-      b = cudaFuncSetAttribute(k_star_pf<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+    if (b == cudaSuccess && kStarPf(P))                                                                \
+      b = cudaFuncSetAttribute(k_star_pf<(P <= 16 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (a != cudaSuccess) e = a;                                                                       \
     if (b != cudaSuccess) e = b;                                                                       \
   }

@@ -118,3 +118,32 @@ def test_spectral_convergence_manufactured():
         errs.append(np.abs(u - 0.75 * s).max())
     assert all(b < 0.2 * a for a, b in zip(errs, errs[1:])), errs
     assert errs[-1] < 1e-5
+
+
+def _iters_krylov(alpha, p, schedule):
+    k = (8, 8, 8)
+    w = [pi.geometric_widths(8, 2 * math.pi, alpha)] * 3
+    H = mg.Hierarchy(k, w, p, 0.0, schedule=schedule)
+    m = H.levels[-1].mesh
+    f = np.random.default_rng(0).uniform(-1, 1, m.ntot)
+    _, rep = H.solve_ipcg(condensed.weak_rhs(m, f), 1e-10, max_iters=60)
+    return rep
+
+
+@pytest.mark.parametrize("solver,alpha,p", [("kMG", 1, 4), ("kMG", 1.5, 4), ("kMG", 2, 4), ("kvMG", 1, 4),
+                                            ("kvMG", 1.5, 4)])
+def test_krylov_iteration_counts_match_paper_table(solver, alpha, p):
+    """Alg. 5 (ipCG with a V-cycle preconditioner) against the kMG / kvMG rows of
+    Table tab:stretched_poly_iterations, +-1 as for MG."""
+    gold = json.load(open(GOLD))
+    want = gold[solver][str(alpha if alpha != 1 else 1)][gold["p"].index(p)]
+    rep = _iters_krylov(alpha, p, 0 if solver == "kMG" else 1)
+    assert rep["converged"]
+    assert abs(rep["cycles"] - want) <= 1, (rep["cycles"], want)
+
+
+def test_krylov_accelerates_on_stretched_mesh():
+    """Krylov acceleration lowers the stretched-mesh iteration counts of MG."""
+    H_mg = _iters(2, 4)
+    H_k = _iters_krylov(2, 4, 0)
+    assert H_k["cycles"] < H_mg["cycles"]
