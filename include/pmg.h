@@ -59,6 +59,9 @@ typedef struct {
   int p0;             /* coarse degree, default 2 */
   int weight_degree;  /* degree of the weight polynomial, default 7; only 7 supported */
   int schedule;       /* 0: nu_pre = nu_post = 1 ("MG"); 1: 2^(L-l) */
+  int solver;         /* pmg_solve: 0 = multigrid fixpoint iteration (Alg. 4, "MG");
+                         1 = Krylov-accelerated multigrid, inexact preconditioned CG with one V-cycle
+                         from zero as preconditioner (Alg. 5; "kMG", with schedule 1 "kvMG") */
   double coarse_rtol; /* coarse CG relative tolerance, default 1e-8 (reading R11) */
   int coarse_maxit;   /* coarse CG iteration cap, default 10000 */
   int coarse_check;   /* coarse CG: host convergence poll every this many iterations, default 8 */
@@ -92,7 +95,7 @@ typedef struct {
 int pmg_slab_plan(int k3, int nranks, int rank, pmg_slab* out);   /* 0, or -1 on invalid input */
 
 typedef struct {
-  int cycles;         /* V-cycles performed (n_10 of P:636 when rtol = 1e-10) */
+  int cycles;         /* V-cycles performed (n_10 of P:636 when rtol = 1e-10); ipCG iterations for solver 1 */
   int converged;      /* 1 if ||r_n|| <= rtol ||r_0|| */
   double r0, r_final; /* ||r_hat||_2 over free skeleton unknowns, before / after */
   double rho;         /* (r_final / r0)^(1/cycles) */

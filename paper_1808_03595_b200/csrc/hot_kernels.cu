@@ -74,6 +74,8 @@ template <int P>
 __global__ void __launch_bounds__(ElemCfg<P>::NT) k_elem_apply_t(LevelGeom g, const double* __restrict__ u,
                                                                  const double* __restrict__ etab, double lam,
                                                                  double* __restrict__ Y, const int* __restrict__ done) {
+  pdl_wait();
+  pdl_trigger();
   using C = ElemCfg<P>;
   constexpr int M = C::M, Q = C::Q, MM = C::MM, QQ = C::QQ, NT = C::NT, TB = C::TB;
   if (done && *done) return;
@@ -513,6 +515,8 @@ __global__ void __launch_bounds__(StarCfg<P>::NT) k_star_t(LevelGeom g, int c1, 
                                                           const double* __restrict__ r, double* __restrict__ u,
                                                           const double* __restrict__ stab, const double* __restrict__ stabT,
                                                           double lam) {
+  pdl_wait();
+  pdl_trigger();
   using C = StarCfg<P>;
   constexpr int N = C::N, NN = C::NN, c = C::C, NT = C::NT, XPL = C::XPL;
   extern __shared__ double sm[];
@@ -1143,16 +1147,21 @@ __global__ void __launch_bounds__(StarPfCfg<P>::NT, StarPfCfg<P>::MINB)
   }
   const size_t srow[3] = {row[0] * ST, row[1] * ST, row[2] * ST};
   __syncthreads();
-  // group 0: S rows, eigen/weight vectors, the r planes
+  // group 0: S rows, eigen/weight vectors (setup tables: before the dependency wait), the r planes
   for (int i = tid; i < 3 * NN; i += NT) {
     const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
     cp_async8(&Ssm[d * MS + A * LD + B], &stab[srow[d] + rr], true);
+  }
+  for (int i = tid; i < 9 * N; i += NT) { const int d = i / (3 * N); cp_async8(&vec[i], &stab[srow[d] + NN + i - d * 3 * N], true); }
+  pdl_wait();
+  pdl_trigger();
+  for (int i = tid; i < 3 * NN; i += NT) {
+    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
     const unsigned e = map.v[i];
     const long long base = s_base[(e >> 12) & 7u];
     const bool ok = base >= 0;
     cp_async8(&FT[d * MS + A * LD + B], &r[ok ? base + (e & 0xFFFu) : 0], ok);
   }
-  for (int i = tid; i < 9 * N; i += NT) { const int d = i / (3 * N); cp_async8(&vec[i], &stab[srow[d] + NN + i - d * 3 * N], true); }
   cp_async_commit();
   // group 1: the u entries this star updates (0 where the point is not free)
   for (int i = tid; i < 3 * NN; i += NT) {
@@ -1335,9 +1344,8 @@ __global__ void __launch_bounds__(ElemPfCfg<P>::NT, ElemPfCfg<P>::MINB)
     k_elem_pf(LevelGeom g, const double* __restrict__ u, const double* __restrict__ etab, double lam,
               double* __restrict__ Y, const int* __restrict__ done) {
   using C = ElemPfCfg<P>;
-  constexpr int M = C::M, Q = C::Q, MM = C::MM, QQ = C::QQ, QQQ = C::QQQ, NT = C::NT, ET = C::ET, LD = C::LD,
+  constexpr int M = C::M, Q = C::Q, MM = C::MM, QQ = C::QQ, NT = C::NT, ET = C::ET, LD = C::LD,
                 MS = C::MS, MP = C::MP, YS = C::YS;
-  if (done && *done) return;
   extern __shared__ double sm[];
   double* cube = sm + C::oCube;
   double* tb = sm + C::oTab;
@@ -1355,6 +1363,9 @@ __global__ void __launch_bounds__(ElemPfCfg<P>::NT, ElemPfCfg<P>::MINB)
       const int d = i / ET;
       cp_async8(&tb[i], src[d] + (i - d * ET), true);
     }
+    pdl_wait();
+  pdl_trigger();
+    if (done && *done) return;   // (uniform per block; the issued cp.async only target this block's smem)
     constexpr int RS = 3 * MM + 3 * M + 1;
     const long long V12 = (long long)g.V1 * g.V2;
     const long long rec0 = e1 + g.V1 * (long long)e2 + V12 * e3;
@@ -1513,6 +1524,8 @@ template <int P>
 __global__ void __launch_bounds__(256) k_gather_resid_t(LevelGeom g, const double* __restrict__ Y,
                                                         const double* __restrict__ F, double* __restrict__ out,
                                                         const int* __restrict__ done) {
+  pdl_wait();
+  pdl_trigger();
   if (done && *done) return;
   constexpr int m = P - 1, mm = m * m, RS = 3 * mm + 3 * m + 1, YS = 6 * mm + 12 * m + 8;
   const int v1 = blockIdx.x, v2 = blockIdx.y, v3 = blockIdx.z;
@@ -1602,7 +1615,7 @@ void launch_elem_p(const LevelGeom& g, const double* u, const double* etab, doub
   if constexpr (P <= 8) {
     const int v = elem_variant();
     if (v == 0) {
-      k_elem_pf<P><<<(unsigned)g.nelem, ElemPfCfg<P>::NT, elem_pf_smem<P>(), st>>>(g, u, etab, lam, Y, done);
+      launch_pdl(k_elem_pf<P>, dim3((unsigned)g.nelem), dim3(ElemPfCfg<P>::NT), elem_pf_smem<P>(), st, g, u, etab, lam, Y, done);
       return;
     }
     if (v == 2) {
@@ -1610,24 +1623,24 @@ void launch_elem_p(const LevelGeom& g, const double* u, const double* etab, doub
       return;
     }
   }
-  k_elem_apply_t<P><<<(unsigned)g.nelem, ElemCfg<P>::NT, elem_t_smem<P>(), st>>>(g, u, etab, lam, Y, done);
+  launch_pdl(k_elem_apply_t<P>, dim3((unsigned)g.nelem), dim3(ElemCfg<P>::NT), elem_t_smem<P>(), st, g, u, etab, lam, Y, done);
 }
 
 template <int P>
 void launch_star_p(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c, long long nb, const double* r,
                    double* u, const double* stab, const double* stabT, double lam, cudaStream_t st) {
   if constexpr (kStarPf(P) && !kStarSinglePass(P)) {
-    k_star_pf<P><<<(unsigned)nb, StarPfCfg<P>::NT, star_pf_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, lam);
+    launch_pdl(k_star_pf<P>, dim3((unsigned)nb), dim3(StarPfCfg<P>::NT), star_pf_smem<P>(), st, g, c1, c2, c3, n1c, n2c, r, u, stab, lam);
   } else if constexpr (kStarSinglePass(P)) {
     const int v = star_variant();
     if (v == 0)
-      k_star_pf<P><<<(unsigned)nb, StarPfCfg<P>::NT, star_pf_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, lam);
+      launch_pdl(k_star_pf<P>, dim3((unsigned)nb), dim3(StarPfCfg<P>::NT), star_pf_smem<P>(), st, g, c1, c2, c3, n1c, n2c, r, u, stab, lam);
     else if (v == 2)
       k_star_dm<P><<<(unsigned)nb, StarDmCfg<P>::NT, star_dm_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
     else
       k_star_sp<P><<<(unsigned)nb, StarSpCfg<P>::NT, star_sp_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
   } else {
-    k_star_t<P><<<(unsigned)nb, StarCfg<P>::NT, star_t_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
+    launch_pdl(k_star_t<P>, dim3((unsigned)nb), dim3(StarCfg<P>::NT), star_t_smem<P>(), st, g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
   }
 }
 #define PMG_DEGREES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) \
@@ -1655,7 +1668,7 @@ cudaError_t launch_gather_resid(const LevelGeom& g, const double* Y, const doubl
   case P: {                                                                                         \
     constexpr int RS = 3 * (P - 1) * (P - 1) + 3 * (P - 1) + 1;                                     \
     const int nt = RS < 64 ? 64 : (RS < 128 ? 128 : 256);                                           \
-    k_gather_resid_t<P><<<grid, nt, 0, st>>>(g, Y, F, out, done);                                   \
+    launch_pdl(k_gather_resid_t<P>, grid, dim3(nt), 0, st, g, Y, F, out, done);                     \
     break;                                                                                          \
   }
     PMG_DEGREES(CASE)

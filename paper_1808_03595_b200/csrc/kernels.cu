@@ -12,10 +12,21 @@
 //   converters, weak RHS, BLAS-1, coarse-CG pieces.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "layout.cuh"
 
 namespace pmg {
+
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("PMG_NO_PDL");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
 
 // ------------------------------------------------------------------------------------------
 // layout converters and weak right-hand side
@@ -424,6 +435,8 @@ size_t transfer_smem(int pf, int pc) {
 // Z[v] = [3 closed coarse faces qc x qc][3 closed coarse edges qc][vertex]
 __global__ void k_restrict_local(LevelGeom gf, int pc, const double* __restrict__ Jint,
                                  const double* __restrict__ rf, double* __restrict__ Z) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double sm[];
   const int mf = gf.m, qc = pc + 1, ZS = 3 * qc * qc + 3 * qc + 1;
   double* J = sm;             // mf x qc
@@ -462,6 +475,8 @@ __global__ void k_restrict_local(LevelGeom gf, int pc, const double* __restrict_
 }
 
 __global__ void k_restrict_gather(LevelGeom gc, const double* __restrict__ Z, double* __restrict__ fc) {
+  pdl_wait();
+  pdl_trigger();
   const int pc = gc.p, qc = pc + 1, ZS = 3 * qc * qc + 3 * qc + 1;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < gc.nskel;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -512,6 +527,8 @@ __global__ void k_restrict_gather(LevelGeom gc, const double* __restrict__ Z, do
 
 __global__ void k_prolong(LevelGeom gf, LevelGeom gc, const double* __restrict__ Jint,
                           const double* __restrict__ uc, double* __restrict__ uf) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double sm[];
   const int mf = gf.m, pc = gc.p, qc = pc + 1, pf = gf.p;
   double* C = sm;                      // 3 qc^2 closed faces, 3 qc closed edges, 1 vertex
@@ -809,6 +826,8 @@ __device__ __forceinline__ double block_sum(double v) {
 
 __global__ void k_dot_partial(const double* __restrict__ a, const double* __restrict__ b, long long n,
                               double* __restrict__ part, const int* __restrict__ done) {
+  pdl_wait();
+  pdl_trigger();
   if (done && *done) return;
   double s = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -818,6 +837,8 @@ __global__ void k_dot_partial(const double* __restrict__ a, const double* __rest
 }
 
 __global__ void k_sum_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   double s = 0.0;
   for (int i = threadIdx.x; i < nb; i += blockDim.x) s += part[i];
   s = block_sum(s);
@@ -825,7 +846,45 @@ __global__ void k_sum_final(const double* __restrict__ part, int nb, double* __r
 }
 
 __global__ void k_zero(double* __restrict__ x, long long n) {
+  pdl_wait();
+  pdl_trigger();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) x[i] = 0.0;
+}
+
+// ---- Alg. 5 (ipCG) vector steps; scalars live on the device: ks = [gamma, gamma0,
+// delta, beta, q.p, alpha, breakdown]
+__global__ void k_ipcg_beta(double* ks) {
+  pdl_wait();
+  pdl_trigger();        // beta = (gamma - gamma0) / delta ; delta = gamma
+  ks[3] = (ks[0] - ks[1]) / ks[2];
+  ks[2] = ks[0];
+}
+__global__ void k_ipcg_dir(double* __restrict__ p, const double* __restrict__ z, const double* __restrict__ ks,
+                           long long n) {
+  pdl_wait();
+  pdl_trigger();        // p = beta p + z
+  const double beta = ks[3];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
+}
+__global__ void k_ipcg_alpha(double* ks) {
+  pdl_wait();
+  pdl_trigger();       // alpha = gamma / (q.p)
+  if (!(ks[4] > 0.0)) ks[6] = 1.0;
+  ks[5] = ks[0] / ks[4];
+}
+__global__ void k_ipcg_update(double* __restrict__ u, double* __restrict__ r, double* __restrict__ s,
+                              const double* __restrict__ p, const double* __restrict__ q, const double* __restrict__ ks,
+                              long long n) {
+  pdl_wait();
+  pdl_trigger();     // s = r ; u += alpha p ; r -= alpha q
+  const double alpha = ks[5];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double ri = r[i];
+    s[i] = ri;
+    u[i] = fma(alpha, p[i], u[i]);
+    r[i] = fma(-alpha, q[i], ri);
+  }
 }
 
 __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, double a, long long n) {

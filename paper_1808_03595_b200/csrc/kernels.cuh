@@ -6,6 +6,33 @@
 
 namespace pmg {
 
+// Programmatic dependent launch (sm_90+): a kernel launched with launch_pdl may be scheduled while
+// its predecessor in the stream drains; it must execute pdl_wait() before touching anything the
+// predecessor writes (griddepcontrol.wait returns once the predecessor has completed and its
+// memory is visible; a no-op when the kernel was launched normally).  Prologues that only read
+// setup tables run before the wait and overlap the predecessor's tail.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// let the next kernel in the stream start launching once every block of this grid has executed this
+// (its blocks then run their table prologue on free SM slots and wait in pdl_wait)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+bool pdl_enabled();   // PMG_NO_PDL=1 disables (A/B experiments)
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 struct PcgState {
   double rz, bb, pq, alpha, beta, rr;
   int done, its, breakdown, its_sum;   // its_sum / breakdown accumulate over coarse solves (reset per pmg_solve)
@@ -64,6 +91,11 @@ __global__ void k_dot_partial(const double* a, const double* b, long long n, dou
 __global__ void k_sum_final(const double* part, int nb, double* out);
 __global__ void k_zero(double* x, long long n);
 __global__ void k_axpy(double* y, const double* x, double a, long long n);
+__global__ void k_ipcg_beta(double* ks);
+__global__ void k_ipcg_dir(double* p, const double* z, const double* ks, long long n);
+__global__ void k_ipcg_alpha(double* ks);
+__global__ void k_ipcg_update(double* u, double* r, double* s, const double* p, const double* q, const double* ks,
+                              long long n);
 __global__ void k_pcg_init(const double* b, const double* dinv, double* x, double* r, double* z, double* pv,
                            long long n, double* part_rz, double* part_bb);
 __global__ void k_pcg_init_final(const double* part_rz, const double* part_bb, int nb, PcgState* st);

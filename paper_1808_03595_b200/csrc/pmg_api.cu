@@ -79,6 +79,9 @@ struct pmg_ctx {
   double* agrecv = nullptr;  // nranks x ag_chunk
   long long ag_chunk = 0;
   double* cxl = nullptr;     // local coarse correction (L = 0, nranks > 1)
+  double *kz = nullptr, *ks_ = nullptr, *kp = nullptr, *kq = nullptr, *kr = nullptr;   // ipCG vectors (Alg. 5)
+  double* kscal = nullptr;   // ipCG device scalars [gamma, gamma0, delta, beta, q.p, alpha, breakdown]
+  cudaGraphExec_t ipcg_exec = nullptr;
   double* Floc = nullptr;    // local grid buffers incl. the ghost element layer (nranks > 1)
   double* Uloc = nullptr;
   long long n_grid_loc = 0;
@@ -212,9 +215,10 @@ int transfer_threads(int pf) { return pf <= 8 ? 64 : (pf <= 16 ? 128 : 256); }
 pmg_status restrict_dev(pmg_ctx* c, int l, const double* rf, double* fc) {
   const DevLevel& F = c->D[l];
   const DevLevel& C = c->D[l - 1];
-  k_restrict_local<<<(unsigned)F.g.nrec, transfer_threads(F.g.p), transfer_smem(F.g.p, C.g.p), c->st>>>(F.g, C.g.p, F.Jint, rf, c->Z);
+  launch_pdl(k_restrict_local, dim3((unsigned)F.g.nrec), dim3(transfer_threads(F.g.p)), transfer_smem(F.g.p, C.g.p), c->st,
+             F.g, C.g.p, (const double*)F.Jint, rf, c->Z);
   LAUNCH_CHECK(c);
-  k_restrict_gather<<<grid_for(C.g.nskel), kThreads, 0, c->st>>>(C.g, c->Z, fc);
+  launch_pdl(k_restrict_gather, dim3(grid_for(C.g.nskel)), dim3(kThreads), 0, c->st, C.g, (const double*)c->Z, fc);
   LAUNCH_CHECK(c);
   return PMG_OK;
 }
@@ -222,21 +226,22 @@ pmg_status restrict_dev(pmg_ctx* c, int l, const double* rf, double* fc) {
 pmg_status prolong_dev(pmg_ctx* c, int l, const double* uc, double* uf) {
   const DevLevel& F = c->D[l];
   const DevLevel& C = c->D[l - 1];
-  k_prolong<<<(unsigned)F.g.nrec, transfer_threads(F.g.p), transfer_smem(F.g.p, C.g.p), c->st>>>(F.g, C.g, F.Jint, uc, uf);
+  launch_pdl(k_prolong, dim3((unsigned)F.g.nrec), dim3(transfer_threads(F.g.p)), transfer_smem(F.g.p, C.g.p), c->st,
+             F.g, C.g, (const double*)F.Jint, uc, uf);
   LAUNCH_CHECK(c);
   return PMG_OK;
 }
 
 pmg_status zero_dev(pmg_ctx* c, double* x, long long n) {
-  k_zero<<<grid_for(n), kThreads, 0, c->st>>>(x, n);
+  launch_pdl(k_zero, dim3(grid_for(n)), dim3(kThreads), 0, c->st, x, n);
   LAUNCH_CHECK(c);
   return PMG_OK;
 }
 
 pmg_status dot_dev(pmg_ctx* c, const double* a, const double* b, long long n, double* out_dev) {
-  k_dot_partial<<<kRedBlocks, kThreads, 0, c->st>>>(a, b, n, c->part, nullptr);
+  launch_pdl(k_dot_partial, dim3(kRedBlocks), dim3(kThreads), 0, c->st, a, b, n, c->part, (const int*)nullptr);
   LAUNCH_CHECK(c);
-  k_sum_final<<<1, 1024, 0, c->st>>>(c->part, kRedBlocks, out_dev);
+  launch_pdl(k_sum_final, dim3(1), dim3(1024), 0, c->st, (const double*)c->part, (int)kRedBlocks, out_dev);
   LAUNCH_CHECK(c);
   return PMG_OK;
 }
@@ -475,6 +480,31 @@ pmg_status recover_dev(pmg_ctx* c, const double* uhat, const double* F, double* 
   return PMG_OK;
 }
 
+// One iteration of Alg. 5 (ipCG with a V-cycle preconditioner) on the device; ends with
+// ||r||^2 in dres.  Vectors: r = kr, s = ks_, p = kp, q = kq, z = kz; scalars in kscal.
+pmg_status ipcg_iter(pmg_ctx* c) {
+  DevLevel& D = c->D[c->L];
+  const long long n = D.g.nskel;
+  pmg_status s;
+  // z = MultigridCycle(0, r): the top-level residual of u = 0 is r itself (no operator call)
+  CUDA_CHECK(cudaMemcpyAsync(D.r, c->kr, n * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+  if ((s = zero_dev(c, c->kz, n))) return s;
+  if ((s = vcycle_dev(c, c->kz, c->kr, true))) return s;
+  if ((s = dot_owned(c, c->L, c->kz, c->kr, c->kscal + 0))) return s;   // gamma  = z^T r
+  if ((s = dot_owned(c, c->L, c->kz, c->ks_, c->kscal + 1))) return s;  // gamma0 = z^T s
+  k_ipcg_beta<<<1, 1, 0, c->st>>>(c->kscal);                              // beta = (gamma - gamma0) / delta
+  LAUNCH_CHECK(c);
+  k_ipcg_dir<<<grid_for(n), kThreads, 0, c->st>>>(c->kp, c->kz, c->kscal, n);   // p = beta p + z
+  LAUNCH_CHECK(c);
+  if ((s = residual_x(c, c->L, c->kp, nullptr, c->kq))) return s;         // q = H p
+  if ((s = dot_owned(c, c->L, c->kq, c->kp, c->kscal + 4))) return s;   // q^T p
+  k_ipcg_alpha<<<1, 1, 0, c->st>>>(c->kscal);                             // alpha = gamma / q^T p
+  LAUNCH_CHECK(c);
+  k_ipcg_update<<<grid_for(n), kThreads, 0, c->st>>>(D.u, c->kr, c->ks_, c->kp, c->kq, c->kscal, n);
+  LAUNCH_CHECK(c);
+  return dot_owned(c, c->L, c->kr, c->kr, c->dres);
+}
+
 pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, int max_cycles, pmg_report* rep) {
   DevLevel& D = c->D[c->L];
   pmg_status s;
@@ -502,6 +532,16 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
   rn = r0;
   int cycles = 0;
   if (rep && rep->history && rep->history_cap > 0) rep->history[0] = r0;
+  const bool krylov = c->opt.solver == 1;
+  if (krylov) {   // Alg. 5 initialisation: r = F - H u (above), s = r, p = 0, delta = 1
+    const long long n = D.g.nskel;
+    CUDA_CHECK(cudaMemcpyAsync(c->kr, D.r, n * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    CUDA_CHECK(cudaMemcpyAsync(c->ks_, D.r, n * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    CUDA_CHECK(cudaMemsetAsync(c->kp, 0, n * sizeof(double), c->st));
+    const double init[8] = {0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    CUDA_CHECK(cudaMemcpyAsync(c->kscal, init, sizeof(init), cudaMemcpyHostToDevice, c->st));
+    CUDA_CHECK(cudaStreamSynchronize(c->st));   // `init` is a host stack array
+  }
   // One cycle = V-cycle + residual + ||r||^2 into dres.  When the whole cycle is free of host
   // synchronisation (cooperative coarse CG) it is captured once into a CUDA graph and replayed:
   // ~60 kernel launches per cycle become one graph launch.
@@ -510,9 +550,14 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
     long long l0 = c->launches;
     cudaGraph_t gr = nullptr;
     CUDA_CHECK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
-    pmg_status cs = vcycle_dev(c, D.u, D.f, true);
-    if (!cs) cs = residual_x(c, c->L, D.u, D.f, D.r);
-    if (!cs) cs = dot_owned(c, c->L, D.r, D.r, c->dres);
+    pmg_status cs;
+    if (krylov) {
+      cs = ipcg_iter(c);
+    } else {
+      cs = vcycle_dev(c, D.u, D.f, true);
+      if (!cs) cs = residual_x(c, c->L, D.u, D.f, D.r);
+      if (!cs) cs = dot_owned(c, c->L, D.r, D.r, c->dres);
+    }
     cudaError_t ce = cudaStreamEndCapture(c->st, &gr);
     if (cs) { if (gr) cudaGraphDestroy(gr); return cs; }
     if (ce != cudaSuccess) return fail(PMG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
@@ -529,6 +574,12 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
       CUDA_CHECK(cudaMemcpyAsync(c->hres, c->dres, sizeof(double), cudaMemcpyDeviceToHost, c->st));
       CUDA_CHECK(cudaStreamSynchronize(c->st));
       rn = std::sqrt(*c->hres);
+    } else if (krylov) {
+      if ((s = ipcg_iter(c))) return s;
+      double h = 0;
+      CUDA_CHECK(cudaMemcpyAsync(&h, c->dres, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      CUDA_CHECK(cudaStreamSynchronize(c->st));
+      rn = std::sqrt(h);
     } else {
       if ((s = vcycle_dev(c, D.u, D.f, true))) return s;
       if ((s = residual_x(c, c->L, D.u, D.f, D.r))) return s;
@@ -553,6 +604,12 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
     CUDA_CHECK(cudaStreamSynchronize(c->st));
     c->coarse_its_total = hs.its_sum;
     if (hs.breakdown) return fail(PMG_EBREAKDOWN, "coarse CG breakdown: p^T H p <= 0");
+  }
+  if (krylov) {
+    double ks[8];
+    CUDA_CHECK(cudaMemcpyAsync(ks, c->kscal, sizeof(ks), cudaMemcpyDeviceToHost, c->st));
+    CUDA_CHECK(cudaStreamSynchronize(c->st));
+    if (ks[6] != 0.0) return fail(PMG_EBREAKDOWN, "ipCG breakdown: p^T H p <= 0");
   }
   bool conv = rn <= rtol * r0;
   if (rep) {
@@ -579,6 +636,8 @@ void free_ctx(pmg_ctx* c) {
   cudaFree(c->Fdev); cudaFree(c->Udev);
   cudaFree(c->f0g); cudaFree(c->u0g); cudaFree(c->agsend); cudaFree(c->agrecv); cudaFree(c->cxl);
   cudaFree(c->Floc); cudaFree(c->Uloc);
+  cudaFree(c->kz); cudaFree(c->ks_); cudaFree(c->kp); cudaFree(c->kq); cudaFree(c->kr); cudaFree(c->kscal);
+  if (c->ipcg_exec) cudaGraphExecDestroy(c->ipcg_exec);
   delete c->tr;
   for (int i = 0; i < 7; ++i) cudaFree(c->ctab[i]);
   cudaFree(c->cV);
@@ -616,6 +675,7 @@ void pmg_default_options(pmg_options* o) {
   o->p0 = 2;
   o->weight_degree = 7;
   o->schedule = 0;
+  o->solver = 0;
   o->coarse_rtol = 1e-8;
   o->coarse_maxit = 10000;
   o->coarse_check = 8;
@@ -647,6 +707,7 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   if (p < o.p0) return fail(PMG_EINVAL, "p must be >= p0");
   if (o.weight_degree != 7) return fail(PMG_EINVAL, "only weight_degree = 7 is implemented (P:316)");
   if (o.schedule != 0 && o.schedule != 1) return fail(PMG_EINVAL, "schedule must be 0 or 1");
+  if (o.solver != 0 && o.solver != 1) return fail(PMG_EINVAL, "solver must be 0 (MG) or 1 (ipCG)");
   if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return fail(PMG_EINVAL, "need 0 <= rank < nranks");
   if (o.nranks > 1 && n_e[2] < o.nranks) return fail(PMG_EINVAL, "z-slabs: k3 >= nranks required");
   if (o.nranks > 1 && o.p0 != 2) return fail(PMG_EINVAL, "z-slabs: the replicated coarse CG needs p0 = 2");
@@ -752,6 +813,14 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
       dalloc(&c->pcg, 1)) {
     free_ctx(c);
     return fail(PMG_ENOMEM, "cudaMalloc failed (workspaces)");
+  }
+  if (o.solver == 1) {
+    const long long nt = c->D[L].g.nskel;
+    if (dalloc(&c->kz, nt) || dalloc(&c->ks_, nt) || dalloc(&c->kp, nt) || dalloc(&c->kq, nt) || dalloc(&c->kr, nt) ||
+        dalloc(&c->kscal, 8)) {
+      free_ctx(c);
+      return fail(PMG_ENOMEM, "cudaMalloc failed (ipCG vectors)");
+    }
   }
   if (!c->cube_in_smem) {
     c->cube_blocks = 296;

@@ -186,3 +186,30 @@ def test_operators_and_vcycle_bitwise(name, nr):
             got = val.reshape(-1, P)
             # every local plane, ghosts included, is refreshed after each call
             assert np.array_equal(got, want), (key, sl, np.abs(got - want).max())
+
+
+@pytest.mark.parametrize("nr", [2, 3])
+def test_krylov_solve_matches_one_gpu(nr):
+    cfg = CASES["k325_p4_lam1.7_stretched"]
+    case = pi.small_case(cfg["k"], cfg["p"], cfg["lam"], stretch=cfg["stretch"])
+    s1 = one_gpu(case, solver=1)
+    f_np, F_np = global_F(case, s1)
+    u1 = s1.new_grid()
+    rep1 = s1.solve(torch.from_numpy(F_np).cuda(), u1, 1e-10)
+    u1 = u1.cpu().numpy()
+    pl = (case.k[0] * case.p + 1) * (case.k[1] * case.p + 1)
+    s1.close()
+
+    def fn(s, r):
+        sl = s.slab
+        lo, hi = sl["z0"] * case.p * pl, (sl["z1"] * case.p + 1) * pl
+        F_loc = torch.from_numpy(F_np[lo:hi].copy()).cuda()
+        u = s.new_grid()
+        rep = s.solve(F_loc, u, 1e-10)
+        torch.cuda.current_stream().synchronize()
+        return sl, u.cpu().numpy(), rep
+
+    for sl, u, rep in run_ranks(nr, case, fn, solver=1):
+        lo, hi = sl["z0"] * case.p * pl, (sl["z1"] * case.p + 1) * pl
+        assert rep["cycles"] == rep1["cycles"]
+        assert np.abs(u - u1[lo:hi]).max() <= 1e-12 * np.abs(u1).max()

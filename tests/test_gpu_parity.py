@@ -282,3 +282,49 @@ def test_pipelined_coarse_cg_matches_standard(name, monkeypatch):
     assert its[0][1] == its[1][1] and abs(its[0][0] - its[1][0]) <= its[0][1] + 1, its
     orc = mg.Hierarchy(case.k, case.widths, case.p, case.lam, coarse_rtol=1e-10)
     assert rel(outs[0], orc.vcycle(np.zeros_like(f), f)) < 1e-7
+
+
+@pytest.mark.parametrize("schedule", [0, 1])
+@pytest.mark.parametrize("name", ["k323_p4_lam1.7_stretched", "k232_p5_lam0", "k333_p8_lam0", "k332_p2_lam0"])
+def test_krylov_solve_parity(name, schedule):
+    """Alg. 5 (ipCG + V-cycle preconditioner; kMG / kvMG) on the GPU against the oracle's verbatim
+    Alg. 5: same iteration count and residual history, solution within the solve tolerance."""
+    import paper_1808_03595_b200 as pmg
+    from oracle import condensed, mg
+    cfg = CASES[name]
+    case = pi.small_case(cfg["k"], cfg["p"], cfg["lam"], stretch=cfg["stretch"])
+    orc = mg.Hierarchy(case.k, case.widths, case.p, case.lam, coarse_rtol=1e-13, schedule=schedule)
+    m = orc.levels[-1].mesh
+    F = condensed.weak_rhs(m, pi.uniform_pm1(6, np.arange(m.ntot)))
+    u_o, rep_o = orc.solve_ipcg(F, 1e-10)
+    s = pmg.Solver(case.k, case.widths, case.p, case.lam, coarse_rtol=1e-13, schedule=schedule, solver=1)
+    ug = s.new_grid()
+    rep = s.solve(torch.from_numpy(F).cuda(), ug, 1e-10)
+    torch.cuda.synchronize()
+    assert rep["converged"] and rep["cycles"] == rep_o["cycles"], (rep["cycles"], rep_o["cycles"])
+    h, ho = np.array(rep["history"]), np.array(rep_o["history"])
+    assert np.all(np.abs(h - ho) <= 1e-8 * ho[0]), (h, ho)
+    assert rel(ug.cpu().numpy(), u_o) < SOLVE_TOL
+    s.close()
+
+
+@pytest.mark.parametrize("solver,alpha", [("kMG", 1), ("kMG", 1.5), ("kMG", 2), ("MG", 1.5)])
+def test_gpu_iteration_counts_match_paper_table(solver, alpha):
+    """Table tab:stretched_poly_iterations on the GPU path at p = 4: 8^3 elements on
+    (0, 2 pi)^3 with expansion factor alpha (reading R13), lambda = 0, random RHS, 1e-10 drop."""
+    import json
+    import math
+    import os
+    import paper_1808_03595_b200 as pmg
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "stretched_poly_iterations.json")))
+    want = gold[solver][str(alpha)][gold["p"].index(4)]
+    k = (8, 8, 8)
+    w = [pi.geometric_widths(8, 2 * math.pi, alpha)] * 3
+    s = pmg.Solver(k, w, 4, 0.0, solver=1 if solver != "MG" else 0)
+    f = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, s.level_info(s.nlevels - 1)[2])).cuda()
+    F = s.new_grid()
+    s.weak_rhs(f, F)
+    u = s.new_grid()
+    rep = s.solve(F, u, 1e-10, max_cycles=60)
+    assert rep["converged"] and abs(rep["cycles"] - want) <= 1, (rep["cycles"], want)
+    s.close()
