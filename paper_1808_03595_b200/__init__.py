@@ -9,7 +9,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpmg.so")
+LIB_PATH = os.environ.get("PMG_LIB") or os.path.join(HERE, "libpmg.so")   # PMG_LIB: experiment builds only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError("libpmg.so not built: run `python paper_1808_03595_b200/build.py` "

@@ -20,17 +20,20 @@ def _nvcc():
     return "nvcc"
 
 
-def build(verbose=False, force=False):
+def build(verbose=False, force=False, lib=None, extra=()):
+    """lib / extra: experiment builds (another output name, extra -D flags); the product build
+    is build() with the defaults."""
+    LIB = lib or globals()["LIB"]
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     deps.append(os.path.join(HERE, "..", "include", "pmg.h"))
     if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps):
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" + ("_" + os.path.basename(LIB).replace(".so", "") if lib else ""))
     os.makedirs(objdir, exist_ok=True)
     def compile_one(s):
         o = os.path.join(objdir, os.path.basename(s) + ".o")
-        cmd = [_nvcc()] + ARCH + FLAGS + ["-x", "cu" if s.endswith(".cu") else "c++", "-c", s, "-o", o]
+        cmd = [_nvcc()] + ARCH + FLAGS + list(extra) + ["-x", "cu" if s.endswith(".cu") else "c++", "-c", s, "-o", o]
         return o, subprocess.run(cmd, capture_output=True, text=True)
 
     # translation units are independent: compile them concurrently

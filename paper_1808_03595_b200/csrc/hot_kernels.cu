@@ -1067,6 +1067,27 @@ template <int P> constexpr ElemMap<P> make_elem_map() {
 }
 template <int P> __device__ const ElemMap<P> kElemMap = make_elem_map<P>();
 
+template <int P> struct FaceMap { unsigned v[6 * (P + 1) * (P + 1)]; };
+// closed face f = 2d + s, position (A slow, B fast) as in the element kernels' face arrays,
+// relative to the element's low-corner record (same encoding as ElemMap)
+template <int P> constexpr FaceMap<P> make_face_map() {
+  FaceMap<P> s{};
+  constexpr int Q = P + 1, QQ = Q * Q;
+  for (int i = 0; i < 6 * QQ; ++i) {
+    const int f = i / QQ, r = i - f * QQ, A = r / Q, B = r - A * Q, d = f >> 1, sd = f & 1;
+    int t[3] = {0, 0, 0};
+    if (d == 0) { t[0] = sd * P; t[2] = A; t[1] = B; }
+    else if (d == 1) { t[1] = sd * P; t[2] = A; t[0] = B; }
+    else { t[2] = sd * P; t[1] = A; t[0] = B; }
+    unsigned code = 0;
+    for (int k = 0; k < 3; ++k)
+      if (t[k] == P) { t[k] = 0; code |= 1u << (12 + k); }
+    s.v[i] = code | rec_slot(P - 1, t[0], t[1], t[2]);
+  }
+  return s;
+}
+template <int P> __device__ const FaceMap<P> kFaceMap = make_face_map<P>();
+
 // record-index delta of map code bits 12-14 (sign applied by the caller)
 __device__ __forceinline__ long long rec_delta(unsigned e, int V1, long long V12) {
   return (long long)((e >> 12) & 1u) + (long long)V1 * ((e >> 13) & 1u) + V12 * ((e >> 14) & 1u);
@@ -1094,7 +1115,10 @@ __device__ __forceinline__ void dmma_tile_t(const double* A, const double* B, do
 template <int P> struct StarPfCfg {
   static constexpr int N = 2 * P - 1, NN = N * N, C = P - 1;
   static constexpr int NP = (N <= 8) ? 8 : (N <= 16 ? 16 : 32), LD = NP + 4, MS = NP * LD, TPP = (NP / 8) * (NP / 8);
-  static constexpr int NW = (P <= 8) ? 4 : 8, NT = 32 * NW, MINB = (P <= 8) ? 5 : 1;
+#ifndef PMG_STAR_MINB
+#define PMG_STAR_MINB 5
+#endif
+  static constexpr int NW = (P <= 8) ? 4 : 8, NT = 32 * NW, MINB = (P <= 8) ? PMG_STAR_MINB : 1;
   static constexpr int GS = NP, GPW = 32 / GS, NG = NW * GPW, A3IT = (N + NG - 1) / NG;
   static constexpr bool P3SEP = NW * NN > 3 * MS;
   static constexpr int oFT = 0, oX = 3 * MS, oG = 6 * MS, oS = 9 * MS, oU = 12 * MS, oVec = oU + 3 * NN,
@@ -1516,6 +1540,205 @@ __global__ void __launch_bounds__(ElemPfCfg<P>::NT, ElemPfCfg<P>::MINB)
 }
 
 // ------------------------------------------------------------------------------------------
+// element operator for 9 <= P <= 16 (same arithmetic and citations as k_elem_pf / k_elem_dm;
+// P:117-123, reading R1): 8 warps, m = p - 1 padded to 16 for the DMMA face transforms, closed
+// face arrays (the (p+1)^3 cube would not leave room for two CTAs per SM), a shared 1/D table, the
+// forward-transform intermediate aliased with G (G is zeroed after the forward pass).
+// ------------------------------------------------------------------------------------------
+template <int P> struct Elem16Cfg {
+  static constexpr int M = P - 1, Q = P + 1, MM = M * M, QQ = Q * Q, MP = 16, LD = 20, MS = MP * LD;
+  static constexpr int NT = 256, NW = 8;
+  static constexpr int ET = (P - 1) + 2 * (P - 1) * (P - 1) + 2 * (P - 1) + (P + 1) + (P + 1) * (P + 1);
+  static constexpr int YS = 6 * MM + 12 * M + 8;
+  static constexpr int oUc = 0, oTab = 6 * QQ, oPp = oTab + 3 * ET, oA = oPp + 3 * MS, oTG = oA + 6 * MS,
+                       oInv = oTG + 6 * MS, total = oInv + MM * M;
+};
+
+template <int P>
+size_t elem16_smem() { return sizeof(double) * Elem16Cfg<P>::total; }
+
+template <int P>
+__global__ void __launch_bounds__(256, 2) k_elem_pf16(LevelGeom g, const double* __restrict__ u,
+                                                    const double* __restrict__ etab, double lam,
+                                                    double* __restrict__ Y, const int* __restrict__ done) {
+  using C = Elem16Cfg<P>;
+  constexpr int M = C::M, Q = C::Q, MM = C::MM, QQ = C::QQ, NT = C::NT, ET = C::ET, LD = C::LD, MS = C::MS,
+                MP = C::MP, YS = C::YS;
+  extern __shared__ double sm[];
+  double* Uc = sm + C::oUc;
+  double* tb = sm + C::oTab;
+  double* Pp = sm + C::oPp;
+  double* Ab = sm + C::oA;
+  double* T = sm + C::oTG;     // forward intermediate, then G
+  double* G = sm + C::oTG;
+  double* invD = sm + C::oInv;
+  const long long e = blockIdx.x;
+  const int e1 = (int)(e % g.k1), e2 = (int)((e / g.k1) % g.k2), e3 = (int)(e / ((long long)g.k1 * g.k2));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {
+    const double* src[3] = {etab + (size_t)e1 * ET, etab + (size_t)(g.k1 + e2) * ET, etab + (size_t)(g.k1 + g.k2 + e3) * ET};
+    for (int i = tid; i < 3 * ET; i += NT) {
+      const int d = i / ET;
+      cp_async8(&tb[i], src[d] + (i - d * ET), true);
+    }
+    pdl_wait();
+    pdl_trigger();
+    if (done && *done) return;
+    constexpr int RS = 3 * MM + 3 * M + 1;
+    const long long V12 = (long long)g.V1 * g.V2;
+    const long long rec0 = e1 + g.V1 * (long long)e2 + V12 * e3;
+    for (int i = tid; i < 6 * QQ; i += NT) {
+      const unsigned m_ = kFaceMap<P>.v[i];
+      cp_async8(&Uc[i], &u[(rec0 + rec_delta(m_, g.V1, V12)) * RS + (m_ & 0xFFFu)], true);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+  for (int i = tid; i < 3 * MP * MP; i += NT) {     // padded P_d[b][i]
+    const int d = i / (MP * MP), rr = i - d * MP * MP, A = rr / MP, B = rr - A * MP;
+    Pp[d * MS + A * LD + B] = (A < M && B < M) ? tb[d * ET + et_P(P) + A * M + B] : 0.0;
+  }
+  for (int i = tid; i < 6 * MP * MP; i += NT) {     // padded face interiors
+    const int f = i / (MP * MP), rr = i - f * MP * MP, A = rr / MP, B = rr - A * MP;
+    Ab[f * MS + A * LD + B] = (A < M && B < M) ? Uc[f * QQ + (A + 1) * Q + B + 1] : 0.0;
+  }
+  for (int i = tid; i < MM * M; i += NT) {          // 1/D over the interior eigen-triples
+    const int b3 = i / MM, rr = i - b3 * MM, b2 = rr / M, b1 = rr - b2 * M;
+    invD[i] = rcp_nr(lam + tb[et_lam(P) + b1] + tb[ET + et_lam(P) + b2] + tb[2 * ET + et_lam(P) + b3]);
+  }
+  __syncthreads();
+  constexpr int TPP = (MP / 8) * (MP / 8);
+  for (int job = warp; job < 6 * TPP; job += C::NW) {     // forward A: X_f = U_f P_a^T  (into T)
+    const int f = job / TPP, t = job - f * TPP, mi = t / (MP / 8), ni = t - mi * (MP / 8), d = f >> 1, da = (d == 0) ? 1 : 0;
+    dmma_tile_t<MP, LD, false, true>(Ab + f * MS, Pp + da * MS, T + f * MS, mi, ni, lane);
+  }
+  __syncthreads();
+  for (int job = warp; job < 6 * TPP; job += C::NW) {     // forward B: T_f = P_b X_f  (into Ab)
+    const int f = job / TPP, t = job - f * TPP, mi = t / (MP / 8), ni = t - mi * (MP / 8), d = f >> 1, db = (d == 2) ? 1 : 2;
+    dmma_tile_t<MP, LD, false, false>(Pp + db * MS, T + f * MS, Ab + f * MS, mi, ni, lane);
+  }
+  __syncthreads();
+  for (int i = tid; i < 6 * MS; i += NT) G[i] = 0.0;     // T is dead: G takes its place
+  __syncthreads();
+  {
+    const double *a10 = tb + et_a0(P), *a11 = tb + et_a1(P);
+    const double *a20 = tb + ET + et_a0(P), *a21 = tb + ET + et_a1(P);
+    const double *a30 = tb + 2 * ET + et_a0(P), *a31 = tb + 2 * ET + et_a1(P);
+    const double *T0 = Ab, *T1 = Ab + MS, *T2 = Ab + 2 * MS, *T3 = Ab + 3 * MS, *T4 = Ab + 4 * MS, *T5 = Ab + 5 * MS;
+    for (int i = tid; i < 3 * MM; i += NT) {
+      const int pass = i / MM, r = i - pass * MM, hi = r / M, lo = r - hi * M;
+      double g0 = 0.0, g1 = 0.0;
+      if (pass == 0) {
+        const int b3 = hi, b2 = lo;
+        const double tA = T0[b3 * LD + b2], tB = T1[b3 * LD + b2], c2 = a20[b2], c2b = a21[b2], c3 = a30[b3], c3b = a31[b3];
+#pragma unroll 5
+        for (int b1 = 0; b1 < M; ++b1) {
+          double Ev = a10[b1] * tA;
+          Ev = fma(a11[b1], tB, Ev);
+          Ev = fma(c2, T2[b3 * LD + b1], Ev);
+          Ev = fma(c2b, T3[b3 * LD + b1], Ev);
+          Ev = fma(c3, T4[b2 * LD + b1], Ev);
+          Ev = fma(c3b, T5[b2 * LD + b1], Ev);
+          const double V = Ev * invD[(b3 * M + b2) * M + b1];
+          g0 = fma(a10[b1], V, g0);
+          g1 = fma(a11[b1], V, g1);
+        }
+        G[0 * MS + b3 * LD + b2] = g0;
+        G[1 * MS + b3 * LD + b2] = g1;
+      } else if (pass == 1) {
+        const int b3 = hi, b1 = lo;
+        const double tA = T2[b3 * LD + b1], tB = T3[b3 * LD + b1], c1 = a10[b1], c1b = a11[b1], c3 = a30[b3], c3b = a31[b3];
+#pragma unroll 5
+        for (int b2 = 0; b2 < M; ++b2) {
+          double Ev = c1 * T0[b3 * LD + b2];
+          Ev = fma(c1b, T1[b3 * LD + b2], Ev);
+          Ev = fma(a20[b2], tA, Ev);
+          Ev = fma(a21[b2], tB, Ev);
+          Ev = fma(c3, T4[b2 * LD + b1], Ev);
+          Ev = fma(c3b, T5[b2 * LD + b1], Ev);
+          const double V = Ev * invD[(b3 * M + b2) * M + b1];
+          g0 = fma(a20[b2], V, g0);
+          g1 = fma(a21[b2], V, g1);
+        }
+        G[2 * MS + b3 * LD + b1] = g0;
+        G[3 * MS + b3 * LD + b1] = g1;
+      } else {
+        const int b2 = hi, b1 = lo;
+        const double tA = T4[b2 * LD + b1], tB = T5[b2 * LD + b1], c1 = a10[b1], c1b = a11[b1], c2 = a20[b2], c2b = a21[b2];
+#pragma unroll 5
+        for (int b3 = 0; b3 < M; ++b3) {
+          double Ev = c1 * T0[b3 * LD + b2];
+          Ev = fma(c1b, T1[b3 * LD + b2], Ev);
+          Ev = fma(c2, T2[b3 * LD + b1], Ev);
+          Ev = fma(c2b, T3[b3 * LD + b1], Ev);
+          Ev = fma(a30[b3], tA, Ev);
+          Ev = fma(a31[b3], tB, Ev);
+          const double V = Ev * invD[(b3 * M + b2) * M + b1];
+          g0 = fma(a30[b3], V, g0);
+          g1 = fma(a31[b3], V, g1);
+        }
+        G[4 * MS + b2 * LD + b1] = g0;
+        G[5 * MS + b2 * LD + b1] = g1;
+      }
+    }
+  }
+  __syncthreads();
+  for (int job = warp; job < 6 * TPP; job += C::NW) {     // back A: X_f = G_f P_a   (into Ab)
+    const int f = job / TPP, t = job - f * TPP, mi = t / (MP / 8), ni = t - mi * (MP / 8), d = f >> 1, da = (d == 0) ? 1 : 0;
+    dmma_tile_t<MP, LD, false, false>(G + f * MS, Pp + da * MS, Ab + f * MS, mi, ni, lane);
+  }
+  __syncthreads();
+  for (int job = warp; job < 6 * TPP; job += C::NW) {     // back B: C_f = P_b^T X_f  (into G)
+    const int f = job / TPP, t = job - f * TPP, mi = t / (MP / 8), ni = t - mi * (MP / 8), d = f >> 1, db = (d == 2) ? 1 : 2;
+    dmma_tile_t<MP, LD, true, false>(Pp + db * MS, Ab + f * MS, G + f * MS, mi, ni, lane);
+  }
+  __syncthreads();
+  const double* Mv[3] = {tb + et_M(P), tb + ET + et_M(P), tb + 2 * ET + et_M(P)};
+  const double* Kv[3] = {tb + et_K(P), tb + ET + et_K(P), tb + 2 * ET + et_K(P)};
+  double* Ye = Y + (size_t)e * g.YS;
+  for (int o = tid; o < YS; o += NT) {
+    double y;
+    if (o < 6 * MM) {      // face interior: closed-face row / column sums and the opposite face
+      const int f = o / MM, r = o - f * MM, A = r / M, B = r - A * M, d = f >> 1, s_ = f & 1;
+      const int da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2;
+      const int td = s_ * P, ta = B + 1, tb_ = A + 1;
+      const double* Uf = Uc + f * QQ;
+      const double *Kd = Kv[d], *Ka = Kv[da], *Kb = Kv[db];
+      const double Md = Mv[d][td], Ma = Mv[da][ta], Mb = Mv[db][tb_];
+      double sa = 0.0, sb = 0.0;
+#pragma unroll
+      for (int t = 0; t <= P; ++t) {
+        sa = fma(Ka[ta * Q + t], Uf[tb_ * Q + t], sa);
+        sb = fma(Kb[tb_ * Q + t], Uf[t * Q + ta], sb);
+      }
+      const double sd = Kd[td * Q] * Uc[(2 * d) * QQ + tb_ * Q + ta] + Kd[td * Q + P] * Uc[(2 * d + 1) * QQ + tb_ * Q + ta];
+      y = lam * Md * Ma * Mb * Uf[tb_ * Q + ta];
+      y = fma(Ma * Mb, sd, y);
+      y = fma(Md * Mb, sa, y);
+      y = fma(Md * Ma, sb, y);
+      y -= G[f * MS + A * LD + B];
+    } else {               // edges and vertices: all three lines lie on the element boundary
+      int t1, t2, t3;
+      ys_point<P>(o, t1, t2, t3);
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int t = 0; t <= P; ++t) {
+        s1 = fma(Kv[0][t1 * Q + t], getUc<P>(Uc, t, t2, t3), s1);
+        s2 = fma(Kv[1][t2 * Q + t], getUc<P>(Uc, t1, t, t3), s2);
+        s3 = fma(Kv[2][t3 * Q + t], getUc<P>(Uc, t1, t2, t), s3);
+      }
+      const double m1 = Mv[0][t1], m2 = Mv[1][t2], m3 = Mv[2][t3];
+      y = lam * m1 * m2 * m3 * getUc<P>(Uc, t1, t2, t3);
+      y = fma(m2 * m3, s1, y);
+      y = fma(m1 * m3, s2, y);
+      y = fma(m1 * m2, s3, y);
+    }
+    Ye[o] = y;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // residual gather, degree-templated: one block per vertex record (3-D grid, no index division),
 // one thread per record slot.  Same sums in the same order as k_gather_resid (kernels.cu):
 // r = F - sum over the elements sharing the point of their outputs Y.
@@ -1623,6 +1846,12 @@ void launch_elem_p(const LevelGeom& g, const double* u, const double* etab, doub
       return;
     }
   }
+  if constexpr (P > 8 && P <= 16) {
+    if (elem_variant() == 0) {
+      launch_pdl(k_elem_pf16<P>, dim3((unsigned)g.nelem), dim3(Elem16Cfg<P>::NT), elem16_smem<P>(), st, g, u, etab, lam, Y, done);
+      return;
+    }
+  }
   launch_pdl(k_elem_apply_t<P>, dim3((unsigned)g.nelem), dim3(ElemCfg<P>::NT), elem_t_smem<P>(), st, g, u, etab, lam, Y, done);
 }
 
@@ -1695,7 +1924,7 @@ cudaError_t launch_star(const LevelGeom& g, int c1, int c2, int c3, int n1c, int
 size_t hot_smem(int p, int which) {
   switch (p) {
 #define CASE(P) \
-  case P: return which == 0 ? std::max(elem_t_smem<P>(), std::max(elem_dm_smem<(P <= 8 ? P : 2)>(), elem_pf_smem<(P <= 8 ? P : 2)>())) : (kStarSinglePass(P) ? std::max(std::max(star_sp_smem<(P <= 8 ? P : 2)>(), star_dm_smem<(P <= 8 ? P : 2)>()), star_pf_smem<(P <= 8 ? P : 2)>()) : (kStarPf(P) ? star_pf_smem<(P <= 16 ? P : 2)>() : star_t_smem<P>()));
+  case P: return which == 0 ? std::max(std::max(elem_t_smem<P>(), elem16_smem<(P > 8 && P <= 16 ? P : 9)>()), std::max(elem_dm_smem<(P <= 8 ? P : 2)>(), elem_pf_smem<(P <= 8 ? P : 2)>())) : (kStarSinglePass(P) ? std::max(std::max(star_sp_smem<(P <= 8 ? P : 2)>(), star_dm_smem<(P <= 8 ? P : 2)>()), star_pf_smem<(P <= 8 ? P : 2)>()) : (kStarPf(P) ? star_pf_smem<(P <= 16 ? P : 2)>() : star_t_smem<P>()));
     PMG_DEGREES(CASE)
 #undef CASE
     default: return 0;
@@ -1711,6 +1940,8 @@ cudaError_t hot_set_smem_attr(int bytes) {
       a = cudaFuncSetAttribute(k_elem_dm<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (a == cudaSuccess && P <= 8)                                                                    \
       a = cudaFuncSetAttribute(k_elem_pf<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+    if (a == cudaSuccess && P > 8 && P <= 16)                                                          \
+      a = cudaFuncSetAttribute(k_elem_pf16<(P > 8 && P <= 16 ? P : 9)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     cudaError_t b = cudaFuncSetAttribute(k_star_t<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);       \
     if (b == cudaSuccess && kStarSinglePass(P))                                                        \
       b = cudaFuncSetAttribute(k_star_sp<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
