@@ -479,6 +479,112 @@ __global__ void __launch_bounds__(256) k_pcg_gv_p2(LevelGeom g, CoarseTabs ct, c
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Pipelined Jacobi-PCG for coarse systems too large for one thread per unknown (more unknowns
+// than resident threads: 16^3+ elements at p0 = 2): the same recurrence as k_pcg_gv_p2, grid-
+// stride over the unknowns, the CG vectors in global memory (L2-resident at these sizes), and
+// the rows of H_hat written out once at setup in column-major ELL form (k_build_coarse_ell: 25
+// index / coefficient pairs per unknown, build_row above), so an operator application is 25
+// coalesced loads of the row plus 25 gathers -- no index arithmetic in the iteration.
+// ------------------------------------------------------------------------------------------
+__global__ void k_build_coarse_ell(LevelGeom g, CoarseTabs ct, double lam, int* __restrict__ ellc,
+                                   double* __restrict__ ella) {
+  const long long n = g.nskel;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    int jx[kRowLen];
+    double a[kRowLen];
+    build_row(g, ct, i, lam, jx, a);
+#pragma unroll
+    for (int k = 0; k < kRowLen; ++k) {
+      ellc[k * n + i] = jx[k];
+      ella[k * n + i] = a[k];
+    }
+  }
+}
+
+// vec: 8 n doubles [x | r | u | w | z | q | s | p]; mbuf: 2 n (m_i in slot i & 1)
+__global__ void __launch_bounds__(256) k_pcg_gv_ell_p2(long long n, const double* __restrict__ b,
+                                                      double* __restrict__ xout, double* __restrict__ vec,
+                                                      double* __restrict__ mbuf, const double* __restrict__ dinv,
+                                                      const int* __restrict__ ellc, const double* __restrict__ ella,
+                                                      double* __restrict__ part, PcgState* st, double rtol, int maxit) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[96];
+  const int nb = gridDim.x;
+  const long long T = (long long)gridDim.x * blockDim.x, t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  double *X = vec, *R = vec + n, *U = vec + 2 * n, *W = vec + 3 * n, *Z = vec + 4 * n, *Q = vec + 5 * n,
+         *S = vec + 6 * n, *Pv = vec + 7 * n;
+  double* mb[2] = {mbuf, mbuf + n};
+  double* pt[2][3] = {{part, part + nb, part + 2 * nb}, {part + 3 * nb, part + 4 * nb, part + 5 * nb}};
+  auto apply = [&](const double* v, long long j) {
+    double h = 0.0;
+#pragma unroll
+    for (int k = 0; k < kRowLen; ++k) h = fma(__ldg(&ella[k * n + j]), __ldcg(&v[__ldg(&ellc[k * n + j])]), h);
+    return h;
+  };
+  // r0 = b, u0 = D^-1 b (published in mb[1] for w0 = H u0)
+  for (long long j = t0; j < n; j += T) {
+    const double bj = b[j], uj = dinv[j] * bj;
+    X[j] = 0.0; R[j] = bj; U[j] = uj; Z[j] = 0.0; Q[j] = 0.0; S[j] = 0.0; Pv[j] = 0.0;
+    mb[1][j] = uj;
+  }
+  grid.sync();
+  double sa = 0.0, sb = 0.0, sc = 0.0;
+  for (long long j = t0; j < n; j += T) {
+    const double w = apply(mb[1], j), m = dinv[j] * w, rj = R[j], uj = U[j];
+    W[j] = w;
+    mb[0][j] = m;
+    sa = fma(rj, uj, sa); sb = fma(w, uj, sb); sc = fma(rj, rj, sc);
+  }
+  block_reduce3(sa, sb, sc, red, blockIdx.x, pt[0][0], pt[0][1], pt[0][2]);
+  grid.sync();
+  double gamma_old = 1.0, alpha_old = 1.0, bb = -1.0;
+  int its = 0, breakdown = 0;
+  for (int it = 0;; ++it) {
+    double gamma, delta, rho;
+    grid_totals3(pt[it & 1][0], pt[it & 1][1], pt[it & 1][2], nb, red, gamma, delta, rho);
+    if (it == 0) bb = rho;
+    if (bb == 0.0 || sqrt(rho) <= rtol * sqrt(bb) || its >= maxit) break;
+    double alpha, beta;
+    if (it == 0) {
+      beta = 0.0;
+      if (!(delta > 0.0)) { breakdown = 1; break; }
+      alpha = gamma / delta;
+    } else {
+      beta = gamma / gamma_old;
+      const double den = delta - beta * gamma / alpha_old;
+      if (!(den > 0.0)) { breakdown = 1; break; }
+      alpha = gamma / den;
+    }
+    const double* mcur = mb[it & 1];
+    double* mnext = mb[(it + 1) & 1];
+    sa = 0.0; sb = 0.0; sc = 0.0;
+    for (long long j = t0; j < n; j += T) {
+      const double nv = apply(mcur, j), m = __ldcg(&mcur[j]);
+      const double z = fma(beta, Z[j], nv), q = fma(beta, Q[j], m);
+      const double w0 = W[j], s = fma(beta, S[j], w0), pv = fma(beta, Pv[j], U[j]);
+      const double x = fma(alpha, pv, X[j]), r = fma(-alpha, s, R[j]);
+      const double u = fma(-alpha, q, U[j]), w = fma(-alpha, z, w0);
+      Z[j] = z; Q[j] = q; S[j] = s; Pv[j] = pv; X[j] = x; R[j] = r; U[j] = u; W[j] = w;
+      mnext[j] = dinv[j] * w;
+      sa = fma(r, u, sa); sb = fma(w, u, sb); sc = fma(r, r, sc);
+    }
+    ++its;
+    gamma_old = gamma;
+    alpha_old = alpha;
+    block_reduce3(sa, sb, sc, red, blockIdx.x, pt[(it + 1) & 1][0], pt[(it + 1) & 1][1], pt[(it + 1) & 1][2]);
+    grid.sync();
+  }
+  for (long long j = t0; j < n; j += T) xout[j] = X[j];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->its = its;
+    st->its_sum += its;
+    if (breakdown) st->breakdown = 1;
+    st->done = 1;
+    st->bb = bb;
+  }
+}
+
 // Two grid barriers per iteration: with p_new = z + beta p and q = H_hat p,
 //   q_new = H_hat z + beta q_old,
 // so the direction update, the operator application (on z, complete after the previous barrier)

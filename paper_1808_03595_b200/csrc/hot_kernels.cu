@@ -1540,6 +1540,191 @@ __global__ void __launch_bounds__(ElemPfCfg<P>::NT, ElemPfCfg<P>::MINB)
 }
 
 // ------------------------------------------------------------------------------------------
+// star smoother, P <= 4: one WARP per star, four stars per CTA (same arithmetic and citations as
+// k_star_pf: Alg. 1 + Alg. 2).  At n_S <= 7 a 128-thread star leaves most lanes idle
+// in every phase; here each warp runs its star alone with __syncwarp only (no CTA barrier), the
+// G3 partials of the warp's four a3 groups are reduced with two xor shuffles, and 20 stars share
+// an SM.
+// ------------------------------------------------------------------------------------------
+template <int P> struct StarWCfg {
+  static constexpr int N = 2 * P - 1, NN = N * N, C = P - 1, NP = 8, LD = 12, MS = NP * LD;
+  static constexpr int SPB = 4, NT = 32 * SPB;                // stars (warps) per block
+  static constexpr int GS = 8, GPW = 4, A3IT = (N + GPW - 1) / GPW;
+  static constexpr int oFT = 0, oX = 3 * MS, oG = 6 * MS, oS = 9 * MS, oU = 12 * MS, oVec = oU + 3 * NN,
+                       oBase = oVec + 9 * N, per_star = oBase + 8, total = SPB * per_star;
+};
+
+template <int P>
+size_t star_w_smem() { return sizeof(double) * StarWCfg<P>::total; }
+
+template <int P>
+__global__ void __launch_bounds__(128) k_star_w(LevelGeom g, int c1, int c2, int c3, int n1c, int n2c, long long nstars,
+                                               const double* __restrict__ r, double* __restrict__ u,
+                                               const double* __restrict__ stab, double lam) {
+  using C = StarWCfg<P>;
+  constexpr int N = C::N, NN = C::NN, c = C::C, NP = C::NP, LD = C::LD, MS = C::MS, GS = C::GS;
+  extern __shared__ double smem_all[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* sm = smem_all + warp * C::per_star;
+  const long long b = (long long)blockIdx.x * C::SPB + warp;
+  if (b >= nstars) return;
+  const int i1 = (int)(b % n1c), rest = (int)(b / n1c), i2 = rest % n2c, i3 = rest / n2c;
+  const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
+  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 + g.zoff == 0 || v3 + g.zoff == g.K3)) return;
+  if (v3 < g.own_lo) return;
+  const int ST = g.ST;
+  double* FT = sm + C::oFT;
+  double* X = sm + C::oX;
+  double* Gs = sm + C::oG;
+  double* Ssm = sm + C::oS;
+  double* Up = sm + C::oU;
+  double* vec = sm + C::oVec;
+  constexpr int RS = 3 * (P - 1) * (P - 1) + 3 * (P - 1) + 1;
+  const long long V12 = (long long)g.V1 * g.V2;
+  const long long rec0 = v1 + g.V1 * (long long)v2 + V12 * v3;
+  const bool interior = v1 > 0 && v2 > 0 && v3 > 0 && v1 < g.k1 && v2 < g.k2 && v3 + g.zoff < g.K3;
+  const StarMap<P>& map = kStarMap<P>;
+  auto pt_free = [&](unsigned e) {
+    const int w1 = v1 - (int)((e >> 12) & 1u), w2 = v2 - (int)((e >> 13) & 1u), w3 = v3 - (int)((e >> 14) & 1u);
+    const int W3 = w3 + g.zoff;
+    return w1 >= 0 && w2 >= 0 && w3 >= 0 && (w1 > 0 || !(e & (1u << 15))) && (w2 > 0 || !(e & (1u << 16))) &&
+           (W3 > 0 || !(e & (1u << 17))) && w1 < g.k1 && w2 < g.k2 && W3 < g.K3;
+  };
+  long long* s_base = reinterpret_cast<long long*>(sm + C::oBase);
+  if (lane < 8) {
+    const int b1 = lane & 1, b2 = (lane >> 1) & 1, b3 = (lane >> 2) & 1;
+    const bool ok = !((v1 == 0 && b1) || (v2 == 0 && b2) || (v3 == 0 && b3));
+    s_base[lane] = ok ? (rec0 - (b1 + g.V1 * (long long)b2 + V12 * b3)) * RS : -1LL;
+  }
+  const size_t srow[3] = {(size_t)v1 * ST, (size_t)(g.V1 + v2) * ST, (size_t)(g.V1 + g.V2 + v3) * ST};
+  for (int i = lane; i < 3 * NN; i += 32) {
+    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
+    cp_async8(&Ssm[d * MS + A * LD + B], &stab[srow[d] + rr], true);
+  }
+  for (int i = lane; i < 9 * N; i += 32) { const int d = i / (3 * N); cp_async8(&vec[i], &stab[srow[d] + NN + i - d * 3 * N], true); }
+  pdl_wait();
+  pdl_trigger();
+  __syncwarp();
+  for (int i = lane; i < 3 * NN; i += 32) {
+    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
+    const unsigned e = map.v[i];
+    const long long base = s_base[(e >> 12) & 7u];
+    const bool ok = base >= 0;
+    cp_async8(&FT[d * MS + A * LD + B], &r[ok ? base + (e & 0xFFFu) : 0], ok);
+  }
+  cp_async_commit();
+  for (int i = lane; i < 3 * NN; i += 32) {
+    const unsigned e = map.v[i];
+    const long long base = s_base[(e >> 12) & 7u];
+    const bool ok = base >= 0 && (interior || pt_free(e));
+    cp_async8(&Up[i], &u[ok ? base + (e & 0xFFFu) : 0], ok);
+  }
+  cp_async_commit();
+  constexpr int PADN = NP * NP - NN, PC = NP - N;
+  for (int i = lane; i < 3 * PADN; i += 32) {
+    const int d = i / PADN, k = i - d * PADN;
+    int A, B;
+    if (k < N * PC) { A = k / PC; B = N + (k - A * PC); }
+    else { const int k2 = k - N * PC; A = N + k2 / NP; B = k2 - (A - N) * NP; }
+    const int o = d * MS + A * LD + B;
+    FT[o] = 0.0;
+    Ssm[o] = 0.0;
+    Gs[o] = 0.0;
+  }
+  cp_async_wait<1>();
+  __syncwarp();
+  for (int i = lane; i < 3 * 2 * N; i += 32) {   // inverse multiplicity
+    const int d = i / (2 * N), rr = i - d * 2 * N, line = rr / N, t = rr - line * N;
+    const int A = line ? t : c, B = line ? c : t;
+    if (line && t == c) continue;
+    FT[d * MS + A * LD + B] *= 1.0 / (double)(1 + (A == c) + (B == c));
+  }
+  __syncwarp();
+#pragma unroll
+  for (int d = 0; d < 3; ++d) dmma_tile_t<NP, LD, false, false>(FT + d * MS, Ssm + (d == 0 ? 1 : 0) * MS, X + d * MS, 0, 0, lane);
+  __syncwarp();
+#pragma unroll
+  for (int d = 0; d < 3; ++d) dmma_tile_t<NP, LD, true, false>(Ssm + (d == 2 ? 1 : 2) * MS, X + d * MS, FT + d * MS, 0, 0, lane);
+  __syncwarp();
+  {
+    const double *L1 = vec, *s1 = vec + N, *L2 = vec + 3 * N, *s2 = vec + 4 * N, *L3 = vec + 6 * N, *s3 = vec + 7 * N;
+    const double *T1 = FT, *T2 = FT + MS, *T3 = FT + 2 * MS;
+    const int grp = lane / GS, a1 = lane % GS;
+    const bool va = a1 < N;
+    const int a1c = va ? a1 : 0;
+    const double s1a = va ? s1[a1c] : 0.0, L1a = L1[a1c];
+    double g3[N];
+#pragma unroll
+    for (int a2 = 0; a2 < N; ++a2) g3[a2] = 0.0;
+#pragma unroll
+    for (int k = 0; k < C::A3IT; ++k) {
+      const int a3 = grp + k * C::GPW;
+      const bool act = a3 < N;
+      const int a3c = act ? a3 : 0;
+      const double on = (act && va) ? 1.0 : 0.0;
+      const double t2 = on * T2[a3c * LD + a1c], s3v = on * s3[a3c], base = lam + L1a + L3[a3c];
+      const double s1v = on * s1a;
+      double g2 = 0.0;
+      double v[GS];
+#pragma unroll
+      for (int a2 = 0; a2 < GS; ++a2) v[a2] = 0.0;
+#pragma unroll
+      for (int a2 = 0; a2 < N; ++a2) {
+        double E = s1v * T1[a3c * LD + a2];
+        E = fma(s2[a2], t2, E);
+        E = fma(s3v, T3[a2 * LD + a1c], E);
+        const double V = E * rcp_nr(base + L2[a2]);
+        g2 = fma(s2[a2], V, g2);
+        g3[a2] = fma(s3v, V, g3[a2]);
+        v[a2] = s1v * V;
+      }
+#pragma unroll
+      for (int off = GS / 2; off >= 1; off >>= 1) {
+        const bool upper = (a1 & off) != 0;
+#pragma unroll
+        for (int j = 0; j < off; ++j) {
+          const double send = upper ? v[j] : v[j + off];
+          const double keep = upper ? v[j + off] : v[j];
+          v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      if (act && va) {
+        Gs[a3 * LD + a1] = v[0];
+        Gs[MS + a3 * LD + a1] = g2;
+      }
+    }
+#pragma unroll
+    for (int off = GS; off < 32; off <<= 1) {
+#pragma unroll
+      for (int a2 = 0; a2 < N; ++a2) g3[a2] += __shfl_xor_sync(0xffffffffu, g3[a2], off);
+    }
+    if (va && lane < GS) {
+#pragma unroll
+      for (int a2 = 0; a2 < N; ++a2) Gs[2 * MS + a2 * LD + a1] = g3[a2];
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int d = 0; d < 3; ++d) dmma_tile_t<NP, LD, false, true>(Gs + d * MS, Ssm + (d == 0 ? 1 : 0) * MS, X + d * MS, 0, 0, lane);
+  __syncwarp();
+#pragma unroll
+  for (int d = 0; d < 3; ++d) dmma_tile_t<NP, LD, false, false>(Ssm + (d == 2 ? 1 : 2) * MS, X + d * MS, Gs + d * MS, 0, 0, lane);
+  cp_async_wait<0>();
+  __syncwarp();
+  const double *w1 = vec + 2 * N, *w2 = vec + 5 * N, *w3 = vec + 8 * N;
+  for (int i = lane; i < 3 * NN; i += 32) {
+    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
+    int j1, j2, j3;
+    if (d == 0) { j1 = c; j2 = B; j3 = A; }
+    else if (d == 1) { j2 = c; j1 = B; j3 = A; if (j1 == c) continue; }
+    else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
+    const unsigned e = map.v[i];
+    if (!interior && !pt_free(e)) continue;
+    u[s_base[(e >> 12) & 7u] + (e & 0xFFFu)] = fma(w1[j1] * w2[j2] * w3[j3], Gs[d * MS + A * LD + B], Up[i]);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // element operator for 9 <= P <= 16 (same arithmetic and citations as k_elem_pf / k_elem_dm;
 // P:117-123, reading R1): 8 warps, m = p - 1 padded to 16 for the DMMA face transforms, closed
 // face arrays (the (p+1)^3 cube would not leave room for two CTAs per SM), a shared 1/D table, the
@@ -1809,15 +1994,16 @@ __global__ void __launch_bounds__(256) k_gather_resid_t(LevelGeom g, const doubl
 // dispatch
 // ------------------------------------------------------------------------------------------
 constexpr bool kStarSinglePass(int p) { return p <= 8; }   // k_star_sp / k_star_dm variants
-constexpr bool kStarPf(int p) { return p <= 16; }          // k_star_pf (default up to p = 16)
+constexpr bool kStarPf(int p) { return p <= 16; }          // k_star_pf (default for 5 <= p <= 16)
 
-// star kernel variant for p <= 8 (A/B experiments): 0 prefetching DMMA kernel k_star_pf (default),
-// 1 DFMA transforms (k_star_sp), 2 DMMA transforms without prefetch (k_star_dm)
+// star kernel variant for p <= 8 (A/B experiments): 0 default (k_star_w for p <= 4, k_star_pf
+// above), 1 DFMA transforms (k_star_sp), 2 DMMA transforms without prefetch (k_star_dm),
+// 3 k_star_pf at every p <= 8
 static int star_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("PMG_STAR_VARIANT");
-    v = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 0;
+    v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
   }
   return v;
 }
@@ -1862,7 +2048,16 @@ void launch_star_p(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c,
     launch_pdl(k_star_pf<P>, dim3((unsigned)nb), dim3(StarPfCfg<P>::NT), star_pf_smem<P>(), st, g, c1, c2, c3, n1c, n2c, r, u, stab, lam);
   } else if constexpr (kStarSinglePass(P)) {
     const int v = star_variant();
-    if (v == 0)
+    if constexpr (P <= 4) {
+      // warp per star pays off once a colour has many waves of 128-thread stars (large meshes);
+      // for a few hundred stars the shorter per-star chain of k_star_pf wins (measured, config 2)
+      if (v == 0 && nb >= 4LL * 148 * StarPfCfg<P>::MINB) {
+        launch_pdl(k_star_w<P>, dim3((unsigned)((nb + StarWCfg<P>::SPB - 1) / StarWCfg<P>::SPB)), dim3(StarWCfg<P>::NT),
+                   star_w_smem<P>(), st, g, c1, c2, c3, n1c, n2c, nb, r, u, stab, lam);
+        return;
+      }
+    }
+    if (v == 0 || v == 3)
       launch_pdl(k_star_pf<P>, dim3((unsigned)nb), dim3(StarPfCfg<P>::NT), star_pf_smem<P>(), st, g, c1, c2, c3, n1c, n2c, r, u, stab, lam);
     else if (v == 2)
       k_star_dm<P><<<(unsigned)nb, StarDmCfg<P>::NT, star_dm_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
@@ -1924,7 +2119,7 @@ cudaError_t launch_star(const LevelGeom& g, int c1, int c2, int c3, int n1c, int
 size_t hot_smem(int p, int which) {
   switch (p) {
 #define CASE(P) \
-  case P: return which == 0 ? std::max(std::max(elem_t_smem<P>(), elem16_smem<(P > 8 && P <= 16 ? P : 9)>()), std::max(elem_dm_smem<(P <= 8 ? P : 2)>(), elem_pf_smem<(P <= 8 ? P : 2)>())) : (kStarSinglePass(P) ? std::max(std::max(star_sp_smem<(P <= 8 ? P : 2)>(), star_dm_smem<(P <= 8 ? P : 2)>()), star_pf_smem<(P <= 8 ? P : 2)>()) : (kStarPf(P) ? star_pf_smem<(P <= 16 ? P : 2)>() : star_t_smem<P>()));
+  case P: return which == 0 ? std::max(std::max(elem_t_smem<P>(), elem16_smem<(P > 8 && P <= 16 ? P : 9)>()), std::max(elem_dm_smem<(P <= 8 ? P : 2)>(), elem_pf_smem<(P <= 8 ? P : 2)>())) : (kStarSinglePass(P) ? std::max(std::max(std::max(star_sp_smem<(P <= 8 ? P : 2)>(), star_dm_smem<(P <= 8 ? P : 2)>()), star_pf_smem<(P <= 8 ? P : 2)>()), star_w_smem<(P <= 4 ? P : 2)>()) : (kStarPf(P) ? star_pf_smem<(P <= 16 ? P : 2)>() : star_t_smem<P>()));
     PMG_DEGREES(CASE)
 #undef CASE
     default: return 0;
@@ -1947,6 +2142,8 @@ cudaError_t hot_set_smem_attr(int bytes) {
       b = cudaFuncSetAttribute(k_star_sp<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (b == cudaSuccess && kStarSinglePass(P))                                                        \
       b = cudaFuncSetAttribute(k_star_dm<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+    if (b == cudaSuccess && P <= 4)                                                                    \
+      b = cudaFuncSetAttribute(k_star_w<(P <= 4 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (b == cudaSuccess && kStarPf(P))                                                                \
       b = cudaFuncSetAttribute(k_star_pf<(P <= 16 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (a != cudaSuccess) e = a;                                                                       \

@@ -61,6 +61,9 @@ __global__ void k_pcg_coop_reg_p2(LevelGeom g, CoarseTabs ct, const double* b, d
                                   const double* dinv, double lam, double* part, PcgState* st, double rtol, int maxit);
 __global__ void k_pcg_gv_p2(LevelGeom g, CoarseTabs ct, const double* b, double* xout, double* mbuf,
                             const double* dinv, double lam, double* part, PcgState* st, double rtol, int maxit);
+__global__ void k_build_coarse_ell(LevelGeom g, CoarseTabs ct, double lam, int* ellc, double* ella);
+__global__ void k_pcg_gv_ell_p2(long long n, const double* b, double* xout, double* vec, double* mbuf, const double* dinv,
+                                const int* ellc, const double* ella, double* part, PcgState* st, double rtol, int maxit);
 __global__ void k_pcg_cluster_p2(LevelGeom g, CoarseTabs ct, const double* b, double* xout, const double* dinv,
                                  double lam, int chunk, int halo, unsigned long long inv, PcgState* st, double rtol,
                                  int maxit);

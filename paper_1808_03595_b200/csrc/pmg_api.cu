@@ -94,6 +94,11 @@ struct pmg_ctx {
   bool coop_reg = false;     // register-resident variant (one coarse unknown per thread)
   bool coop_gv = false;      // register-resident pipelined variant (one grid barrier per iteration)
   double* cgm = nullptr;     // its double-buffered m vector (2 n0)
+  bool coop_ell = false;     // large coarse systems: pipelined grid-stride CG over ELL rows
+  int ell_nb = 0;
+  int* ellc = nullptr;       // 25 n0 column indices (column-major ELL)
+  double* ella = nullptr;    // 25 n0 coefficients
+  double* ellv = nullptr;    // 8 n0 CG vectors
   double* ctab[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // CoarseTabs storage
   double* cV = nullptr;      // (unused)
   cudaGraphExec_t cycle_exec = nullptr;   // captured solve cycle (V-cycle + residual + norm^2)
@@ -311,6 +316,22 @@ pmg_status pcg_dev(pmg_ctx* c, const double* b, double* x) {
                     &st, &rtol, &maxit};
     void* args_reg[] = {&g0, &ct, (void*)&b, &x, &c->cz, (void*)&dinv, &lam, &part, &st, &rtol, &maxit};
     void* args_gv[] = {&g0, &ct, (void*)&b, &x, &c->cgm, (void*)&dinv, &lam, &part, &st, &rtol, &maxit};
+    if (c->coop_ell && rtol >= 1e-11) {   // large coarse system: grid-stride pipelined CG on ELL rows
+      long long n0 = g0.nskel;
+      void* args_ell[] = {&n0, (void*)&b, &x, &c->ellv, &c->cgm, (void*)&dinv, &c->ellc, &c->ella, &part, &st, &rtol, &maxit};
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(c->ell_nb);
+      cfg.blockDim = dim3(kThreads);
+      cfg.stream = c->st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CUDA_CHECK(cudaLaunchKernelExC(&cfg, (const void*)k_pcg_gv_ell_p2, args_ell));
+      c->launches++;
+      return PMG_OK;
+    }
     // the pipelined recurrence for the performance tolerance; the two-barrier kernel for the very
     // tight parity tolerances (attainable accuracy, see coarse_cg.cu)
     const bool gv = c->coop_gv && rtol >= 1e-11;
@@ -630,7 +651,7 @@ void free_ctx(pmg_ctx* c) {
     cudaFree(D.etab); cudaFree(D.stab); cudaFree(D.Jint); cudaFree(D.u); cudaFree(D.f); cudaFree(D.r);
   }
   cudaFree(c->Y); cudaFree(c->Z); cudaFree(c->cube); cudaFree(c->part); cudaFree(c->dres); cudaFree(c->pcg);
-  cudaFree(c->cgm);
+  cudaFree(c->cgm); cudaFree(c->ellc); cudaFree(c->ella); cudaFree(c->ellv);
   cudaFree(c->cx); cudaFree(c->cr); cudaFree(c->cz); cudaFree(c->cp); cudaFree(c->cq); cudaFree(c->dinv);
   for (int d = 0; d < 3; ++d) cudaFree(c->bm[d]);
   cudaFree(c->Fdev); cudaFree(c->Udev);
@@ -946,6 +967,25 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
           if (!(ge && ge[0] == '0') && per_sm_gv > 0 && need <= (long long)per_sm_gv * nsm &&
               dalloc(&c->cgm, 2 * c->g0g.nskel) == cudaSuccess)
             c->coop_gv = true;
+        }
+        // more coarse unknowns than the register-resident kernels can hold: ELL rows + grid-stride
+        int per_sm_ell = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_ell, k_pcg_gv_ell_p2, kThreads, 0);
+        const char* le = std::getenv("PMG_COARSE_ELL");
+        if (!c->coop_gv && !(le && le[0] == '0') && per_sm_ell > 0) {
+          const long long n0e = c->g0g.nskel;
+          if (dalloc(&c->ellc, 25 * n0e) == cudaSuccess && dalloc(&c->ella, 25 * n0e) == cudaSuccess &&
+              dalloc(&c->ellv, 8 * n0e) == cudaSuccess && (c->cgm || dalloc(&c->cgm, 2 * n0e) == cudaSuccess)) {
+            CoarseTabs ct{c->ctab[0], c->ctab[1], c->ctab[2], c->ctab[3], c->ctab[4], c->ctab[5], c->ctab[6]};
+            k_build_coarse_ell<<<grid_for(n0e), kThreads>>>(c->g0g, ct, lambda, c->ellc, c->ella);
+            if (cudaGetLastError() == cudaSuccess) {
+              c->coop_ell = true;
+              c->ell_nb = (int)std::min<long long>((long long)per_sm_ell * nsm, std::max<long long>(1, (n0e + kThreads - 1) / kThreads));
+              c->ell_nb = std::min(c->ell_nb, 2048);
+            }
+          } else {
+            cudaGetLastError();
+          }
         }
       }
       const char* nbenv = std::getenv("PMG_COOP_BLOCKS");   // tuning experiments only

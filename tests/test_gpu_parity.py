@@ -246,12 +246,14 @@ def test_coarse_cg_paths_agree(name, monkeypatch):
     assert rel(outs[0], P.orc.vcycle(np.zeros_like(f), f)) < OP_TOL
 
 
+@pytest.mark.parametrize("kind", ["registers", "ell"])
 @pytest.mark.parametrize("name", ["k323_p4_lam1.7_stretched", "k333_p8_lam0", "k332_p2_lam0"])
-def test_pipelined_coarse_cg_matches_standard(name, monkeypatch):
-    """The single-barrier (pipelined) coarse CG used at the performance tolerance reproduces the
-    standard two-barrier Jacobi-PCG: same coarse iteration count over a solve (+-1 per coarse
-    solve), and V-cycle outputs that agree to the coarse tolerance's accuracy; against the oracle's
-    standard PCG V-cycle at the same tolerance likewise."""
+def test_pipelined_coarse_cg_matches_standard(name, kind, monkeypatch):
+    """The single-barrier (pipelined) coarse CG used at the performance tolerance -- register-
+    resident (one thread per unknown) or grid-stride over ELL rows (large coarse systems) --
+    reproduces the standard two-barrier Jacobi-PCG: same coarse iteration count over a solve (+-1
+    per coarse solve), and V-cycle outputs that agree to the coarse tolerance's accuracy; against
+    the oracle's standard PCG V-cycle at the same tolerance likewise."""
     import paper_1808_03595_b200 as pmg
     from oracle import mg
     P = pair(name)
@@ -259,8 +261,10 @@ def test_pipelined_coarse_cg_matches_standard(name, monkeypatch):
     L = P.gpu.nlevels - 1
     f = P.rand_skel(L)
     outs, its = [], []
-    for env in ("1", "0"):
-        monkeypatch.setenv("PMG_COARSE_GV", env)
+    envs = [("1", "0"), ("0", "0")] if kind == "registers" else [("0", "1"), ("0", "0")]
+    for gv, ell in envs:
+        monkeypatch.setenv("PMG_COARSE_GV", gv)
+        monkeypatch.setenv("PMG_COARSE_ELL", ell)
         s = pmg.Solver(case.k, case.widths, case.p, case.lam, coarse_rtol=1e-10)
         u = s.new_skel(L)
         fs = torch.from_numpy(np.ascontiguousarray(f)).cuda()
@@ -327,4 +331,24 @@ def test_gpu_iteration_counts_match_paper_table(solver, alpha):
     u = s.new_grid()
     rep = s.solve(F, u, 1e-10, max_cycles=60)
     assert rep["converged"] and abs(rep["cycles"] - want) <= 1, (rep["cycles"], want)
+    s.close()
+
+
+@pytest.mark.parametrize("k,p", [((1, 1, 1), 4), ((1, 2, 3), 3), ((1, 1, 4), 2), ((2, 1, 1), 6)])
+def test_degenerate_meshes(k, p):
+    """Edge cases: one element per direction (k = 1: every element face is Dirichlet, the condensed
+    system is empty or one-dimensional per line) -- the solve must still equal the oracle's."""
+    import paper_1808_03595_b200 as pmg
+    from oracle import condensed, mg
+    case = pi.small_case(k, p, 0.9, stretch=None)
+    orc = mg.Hierarchy(case.k, case.widths, p, case.lam, coarse_rtol=1e-13)
+    m = orc.levels[-1].mesh
+    F = condensed.weak_rhs(m, pi.uniform_pm1(9, np.arange(m.ntot)))
+    u_o, rep_o = orc.solve(F, 1e-10)
+    s = pmg.Solver(case.k, case.widths, p, case.lam, coarse_rtol=1e-13)
+    ug = s.new_grid()
+    rep = s.solve(torch.from_numpy(F).cuda(), ug, 1e-10)
+    torch.cuda.synchronize()
+    assert rep["cycles"] == rep_o["cycles"], (rep["cycles"], rep_o["cycles"])
+    assert rel(ug.cpu().numpy(), u_o) < SOLVE_TOL
     s.close()
