@@ -668,140 +668,4 @@ __global__ void __launch_bounds__(256) k_pcg_coop_p2(LevelGeom g, CoarseTabs ct,
   }
 }
 
-// ------------------------------------------------------------------------------------------
-// The same iteration on ONE thread-block cluster (up to 16 CTAs, distributed shared memory) for
-// coarse systems that fit on chip: every CG vector lives in shared memory, the grid barrier becomes
-// a cluster barrier (~0.2 us instead of 1.2 us), and the vector traffic never leaves the SMs.
-// CTA k owns the contiguous index range [k chunk, (k+1) chunk).  The 13-point stencil of an entry
-// reaches at most one record plane away, so each CTA keeps z on its range extended by a halo of
-// H = 7 (1 + V1 + V1 V2) + 7 entries on both sides, refreshed from the neighbours' shared memory
-// (DSMEM) once per iteration; the operator application is then purely local.  Partial sums are
-// exchanged through DSMEM and added in rank order by every CTA (deterministic, identical).
-// ------------------------------------------------------------------------------------------
-struct SmemAcc {     // z on the CTA's extended range: global index i -> zx[i - lo]
-  const double* zx;
-  long long lo;
-  __device__ __forceinline__ double operator()(long long i) const { return i < 0 ? 0.0 : zx[i - lo]; }
-};
-
-__global__ void __launch_bounds__(512, 1) k_pcg_cluster_p2(LevelGeom g, CoarseTabs ct, const double* __restrict__ b,
-                                                           double* __restrict__ xout, const double* __restrict__ dinv,
-                                                           double lam, int chunk, int halo, unsigned long long inv,
-                                                           PcgState* st, double rtol, int maxit) {
-  cg::cluster_group cl = cg::this_cluster();
-  const int rank = (int)cl.block_rank(), csz = (int)cl.num_blocks();
-  extern __shared__ double sm[];
-  double* x = sm;
-  double* r = x + chunk;
-  double* pv = r + chunk;
-  double* q = pv + chunk;
-  double* zx = q + chunk;                  // chunk + 2 halo
-  __shared__ double part[5];               // this CTA's partials: p.q, r.r, r.z, b.b, scratch
-  __shared__ double red[64];
-  const long long n = g.nskel, base = (long long)rank * chunk;
-  const int nloc = (int)max(0LL, min((long long)chunk, n - base));
-  const int tid = threadIdx.x, nt = blockDim.x;
-  double* z = zx + halo;                   // local part of z
-  const SmemAcc acc{zx, base - halo};
-  auto owner_of = [&](long long j) -> int { return (int)(((unsigned long long)j * inv) >> 40); };
-  auto totals = [&](int k0, int k1, double& t0, double& t1) {   // sum of part[k] over ranks, rank order
-    double a = 0.0, c = 0.0;
-    for (int q_ = 0; q_ < csz; ++q_) {
-      const double* rp = cl.map_shared_rank(part, q_);
-      a += rp[k0];
-      c += rp[k1];
-    }
-    t0 = a;
-    t1 = c;
-  };
-  auto reduce2 = [&](double a, double c, int k0, int k1) {       // block sums -> part[k0], part[k1]
-    for (int o = 16; o > 0; o >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, o);
-      c += __shfl_xor_sync(0xffffffffu, c, o);
-    }
-    const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
-    __syncthreads();
-    if (lane == 0) { red[w] = a; red[32 + w] = c; }
-    __syncthreads();
-    if (tid == 0) {
-      double sa = 0.0, sc = 0.0;
-      for (int i = 0; i < nw; ++i) { sa += red[i]; sc += red[32 + i]; }
-      part[k0] = sa;
-      part[k1] = sc;
-    }
-  };
-  auto refresh_halo = [&]() {   // zx outside the local range from the owners' shared memory
-    for (int t = tid; t < 2 * halo; t += nt) {
-      const long long j = (t < halo) ? base - halo + t : base + nloc + (t - halo);
-      double v = 0.0;
-      if (j >= 0 && j < n) {
-        const int o = owner_of(j);
-        const double* rz = cl.map_shared_rank(zx, o);
-        v = rz[halo + (j - (long long)o * chunk)];
-      }
-      zx[(t < halo) ? t : halo + nloc + (t - halo)] = v;
-    }
-  };
-  double s1 = 0.0, s2 = 0.0;
-  for (int i = tid; i < nloc; i += nt) {
-    const double bi = b[base + i], zi = dinv[base + i] * bi;
-    x[i] = 0.0; r[i] = bi; z[i] = zi; pv[i] = 0.0; q[i] = 0.0;
-    s1 = fma(bi, zi, s1); s2 = fma(bi, bi, s2);
-  }
-  reduce2(s1, s2, 2, 3);
-  cl.sync();
-  double rz, bb;
-  totals(2, 3, rz, bb);
-  refresh_halo();
-  __syncthreads();
-  double beta = 0.0;
-  int its = 0, breakdown = 0;
-  bool done = (bb == 0.0);
-  while (!done) {
-    double spq = 0.0;
-    for (int i = tid; i < nloc; i += nt) {       // p = z + beta p ; q = H z + beta q
-      const double pi_ = fma(beta, pv[i], z[i]);
-      const double qi = fma(beta, q[i], apply_entry(g, ct, acc, base + i, lam));
-      pv[i] = pi_;
-      q[i] = qi;
-      spq = fma(pi_, qi, spq);
-    }
-    reduce2(spq, 0.0, 0, 4);
-    cl.sync();
-    double pq, unused;
-    totals(0, 4, pq, unused);
-    if (!(pq > 0.0)) { breakdown = 1; break; }
-    const double alpha = rz / pq;
-    double srr = 0.0, srz = 0.0;
-    for (int i = tid; i < nloc; i += nt) {
-      x[i] = fma(alpha, pv[i], x[i]);
-      const double ri = fma(-alpha, q[i], r[i]);
-      r[i] = ri;
-      const double zi = dinv[base + i] * ri;
-      z[i] = zi;
-      srr = fma(ri, ri, srr);
-      srz = fma(ri, zi, srz);
-    }
-    reduce2(srr, srz, 1, 2);
-    cl.sync();
-    double rr, rzn;
-    totals(1, 2, rr, rzn);
-    ++its;
-    if (sqrt(rr) <= rtol * sqrt(bb) || its >= maxit) break;
-    beta = rzn / rz;
-    rz = rzn;
-    refresh_halo();
-    __syncthreads();
-  }
-  for (int i = tid; i < nloc; i += nt) xout[base + i] = x[i];
-  cl.sync();   // no CTA leaves while others may still read its shared memory
-  if (rank == 0 && tid == 0) {
-    st->its = its;
-    st->its_sum += its;
-    if (breakdown) st->breakdown = 1;
-    st->done = 1;
-    st->bb = bb;
-  }
-}
-
 }  // namespace pmg

@@ -1999,23 +1999,15 @@ constexpr bool kStarPf(int p) { return p <= 16; }          // k_star_pf (default
 // star kernel variant for p <= 8 (A/B experiments): 0 default (k_star_w for p <= 4, k_star_pf
 // above), 1 DFMA transforms (k_star_sp), 2 DMMA transforms without prefetch (k_star_dm),
 // 3 k_star_pf at every p <= 8
-static int star_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("PMG_STAR_VARIANT");
-    v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
-  }
-  return v;
+static int star_variant() {   // read at every launch (launches are captured into graphs once)
+  const char* e = std::getenv("PMG_STAR_VARIANT");
+  return (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
 }
 
 // element kernel variant for p <= 8: 0 k_elem_pf (default), 1 DFMA (k_elem_apply_t), 2 k_elem_dm
 static int elem_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("PMG_ELEM_VARIANT");
-    v = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 0;
-  }
-  return v;
+  const char* e = std::getenv("PMG_ELEM_VARIANT");
+  return (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 0;
 }
 
 template <int P>

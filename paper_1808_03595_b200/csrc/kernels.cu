@@ -433,12 +433,15 @@ size_t transfer_smem(int pf, int pc) {
 }
 
 // Z[v] = [3 closed coarse faces qc x qc][3 closed coarse edges qc][vertex]
-__global__ void k_restrict_local(LevelGeom gf, int pc, const double* __restrict__ Jint,
-                                 const double* __restrict__ rf, double* __restrict__ Z) {
+// PF_ / PC_ > 0: degrees known at compile time (unrolled loops, constant divisions); 0: runtime
+template <int PF_, int PC_>
+__global__ void k_restrict_local_t(LevelGeom gf, int pc_rt, const double* __restrict__ Jint,
+                                   const double* __restrict__ rf, double* __restrict__ Z) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ double sm[];
-  const int mf = gf.m, qc = pc + 1, ZS = 3 * qc * qc + 3 * qc + 1;
+  const int pc = PC_ > 0 ? PC_ : pc_rt;
+  const int mf = PF_ > 0 ? PF_ - 1 : gf.m, qc = pc + 1, ZS = 3 * qc * qc + 3 * qc + 1;
   double* J = sm;             // mf x qc
   double* X = J + mf * qc;    // mf x qc
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -474,10 +477,11 @@ __global__ void k_restrict_local(LevelGeom gf, int pc, const double* __restrict_
   if (tid == 0) Zr[ZS - 1] = R[off_vert(mf)];
 }
 
-__global__ void k_restrict_gather(LevelGeom gc, const double* __restrict__ Z, double* __restrict__ fc) {
+template <int PC_>
+__global__ void k_restrict_gather_t(LevelGeom gc, const double* __restrict__ Z, double* __restrict__ fc) {
   pdl_wait();
   pdl_trigger();
-  const int pc = gc.p, qc = pc + 1, ZS = 3 * qc * qc + 3 * qc + 1;
+  const int pc = PC_ > 0 ? PC_ : gc.p, qc = pc + 1, ZS = 3 * qc * qc + 3 * qc + 1;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < gc.nskel;
        idx += (long long)gridDim.x * blockDim.x) {
     Entry E = decode_entry(gc, idx);
@@ -525,12 +529,13 @@ __global__ void k_restrict_gather(LevelGeom gc, const double* __restrict__ Z, do
   }
 }
 
-__global__ void k_prolong(LevelGeom gf, LevelGeom gc, const double* __restrict__ Jint,
-                          const double* __restrict__ uc, double* __restrict__ uf) {
+template <int PF_, int PC_>
+__global__ void k_prolong_t(LevelGeom gf, LevelGeom gc, const double* __restrict__ Jint,
+                            const double* __restrict__ uc, double* __restrict__ uf) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ double sm[];
-  const int mf = gf.m, pc = gc.p, qc = pc + 1, pf = gf.p;
+  const int pf = PF_ > 0 ? PF_ : gf.p, mf = pf - 1, pc = PC_ > 0 ? PC_ : gc.p, qc = pc + 1;
   double* C = sm;                      // 3 qc^2 closed faces, 3 qc closed edges, 1 vertex
   double* J = C + 3 * qc * qc + 3 * qc + 1;  // mf x qc
   double* X = J + mf * qc;             // qc x mf
@@ -1032,6 +1037,61 @@ cudaError_t condense_recover_set_smem_attr(int bytes) {
   PMG_CR_DEGREES(CASE)
   CASE(0)
 #undef CASE
+  return e;
+}
+
+}  // namespace pmg
+
+namespace pmg {
+
+// restriction / prolongation launchers: compile-time degree pairs of the hierarchies the solver
+// builds (p_l = 2 p_(l-1), and the top levels of p = 12, 24), the runtime kernels otherwise
+#define PMG_TRANSFER_PAIRS(X) X(4, 2) X(8, 4) X(16, 8) X(32, 16) X(12, 8) X(24, 16) X(3, 2) X(6, 4)
+
+cudaError_t launch_restrict(const LevelGeom& gf, const LevelGeom& gc, const double* Jint, const double* rf, double* Z,
+                            double* fc, int nt_local, size_t smem, int gather_blocks, cudaStream_t st) {
+  const int pf = gf.p, pc = gc.p;
+  cudaError_t e = cudaSuccess;
+  bool done = false;
+#define CASE(A, B)                                                                                           \
+  if (!done && pf == A && pc == B) {                                                                         \
+    e = launch_pdl(k_restrict_local_t<A, B>, dim3((unsigned)gf.nrec), dim3(nt_local), smem, st, gf, pc, Jint, rf, Z); \
+    done = true;                                                                                             \
+  }
+  PMG_TRANSFER_PAIRS(CASE)
+#undef CASE
+  if (!done)
+    e = launch_pdl(k_restrict_local_t<0, 0>, dim3((unsigned)gf.nrec), dim3(nt_local), smem, st, gf, pc, Jint, rf, Z);
+  if (e != cudaSuccess) return e;
+  switch (pc) {
+    case 2: return launch_pdl(k_restrict_gather_t<2>, dim3(gather_blocks), dim3(256), 0, st, gc, (const double*)Z, fc);
+    case 4: return launch_pdl(k_restrict_gather_t<4>, dim3(gather_blocks), dim3(256), 0, st, gc, (const double*)Z, fc);
+    case 8: return launch_pdl(k_restrict_gather_t<8>, dim3(gather_blocks), dim3(256), 0, st, gc, (const double*)Z, fc);
+    case 16: return launch_pdl(k_restrict_gather_t<16>, dim3(gather_blocks), dim3(256), 0, st, gc, (const double*)Z, fc);
+    default: return launch_pdl(k_restrict_gather_t<0>, dim3(gather_blocks), dim3(256), 0, st, gc, (const double*)Z, fc);
+  }
+}
+
+cudaError_t launch_prolong(const LevelGeom& gf, const LevelGeom& gc, const double* Jint, const double* uc, double* uf,
+                           int nt, size_t smem, cudaStream_t st) {
+  const int pf = gf.p, pc = gc.p;
+#define CASE(A, B)                                                                                           \
+  if (pf == A && pc == B)                                                                                    \
+    return launch_pdl(k_prolong_t<A, B>, dim3((unsigned)gf.nrec), dim3(nt), smem, st, gf, gc, Jint, uc, uf);
+  PMG_TRANSFER_PAIRS(CASE)
+#undef CASE
+  return launch_pdl(k_prolong_t<0, 0>, dim3((unsigned)gf.nrec), dim3(nt), smem, st, gf, gc, Jint, uc, uf);
+}
+
+cudaError_t transfer_set_smem_attr(int bytes) {
+  cudaError_t e = cudaSuccess;
+#define CASE(A, B)                                                                                           \
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_restrict_local_t<A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_prolong_t<A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  PMG_TRANSFER_PAIRS(CASE)
+#undef CASE
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_restrict_local_t<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_prolong_t<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   return e;
 }
 

@@ -64,10 +64,6 @@ __global__ void k_pcg_gv_p2(LevelGeom g, CoarseTabs ct, const double* b, double*
 __global__ void k_build_coarse_ell(LevelGeom g, CoarseTabs ct, double lam, int* ellc, double* ella);
 __global__ void k_pcg_gv_ell_p2(long long n, const double* b, double* xout, double* vec, double* mbuf, const double* dinv,
                                 const int* ellc, const double* ella, double* part, PcgState* st, double rtol, int maxit);
-__global__ void k_pcg_cluster_p2(LevelGeom g, CoarseTabs ct, const double* b, double* xout, const double* dinv,
-                                 double lam, int chunk, int halo, unsigned long long inv, PcgState* st, double rtol,
-                                 int maxit);
-
 size_t elem_apply_smem(int p, int ET);
 size_t star_smem(int p, bool s_in_smem);
 size_t transfer_smem(int pf, int pc);
@@ -81,9 +77,11 @@ __global__ void k_elem_apply(LevelGeom g, const double* u, const double* etab, d
 __global__ void k_gather_resid(LevelGeom g, const double* Y, const double* F, double* out, const int* done);
 __global__ void k_star(LevelGeom g, int c1, int c2, int c3, int n1c, int n2c, const double* r, double* u,
                        const double* stab, double lam, int s_in_smem);
-__global__ void k_restrict_local(LevelGeom gf, int pc, const double* Jint, const double* rf, double* Z);
-__global__ void k_restrict_gather(LevelGeom gc, const double* Z, double* fc);
-__global__ void k_prolong(LevelGeom gf, LevelGeom gc, const double* Jint, const double* uc, double* uf);
+cudaError_t launch_restrict(const LevelGeom& gf, const LevelGeom& gc, const double* Jint, const double* rf, double* Z,
+                            double* fc, int nt_local, size_t smem, int gather_blocks, cudaStream_t st);
+cudaError_t launch_prolong(const LevelGeom& gf, const LevelGeom& gc, const double* Jint, const double* uc, double* uf,
+                           int nt, size_t smem, cudaStream_t st);
+cudaError_t transfer_set_smem_attr(int bytes);
 cudaError_t launch_condense_elem(int nb, int nt, size_t sm, cudaStream_t st, const LevelGeom& g, const double* Fg,
                                  const double* etab, double lam, double* Yc, double* cube_g);
 cudaError_t launch_recover_elem(int nb, int nt, size_t sm, cudaStream_t st, const LevelGeom& g, const double* Fg,

@@ -105,10 +105,6 @@ struct pmg_ctx {
   long long launches_per_cycle = 0;
   double* hres = nullptr;    // pinned host scalar
   bool no_graph = false;     // PMG_NO_GRAPH=1
-  bool use_cluster = false;  // coarse CG on one thread-block cluster (DSMEM) when it fits
-  int cl_size = 0, cl_chunk = 0, cl_halo = 0, cl_threads = 512;
-  unsigned long long cl_inv = 0;
-  size_t cl_smem = 0;
   // event timing (pmg_timing_enable)
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -220,19 +216,17 @@ int transfer_threads(int pf) { return pf <= 8 ? 64 : (pf <= 16 ? 128 : 256); }
 pmg_status restrict_dev(pmg_ctx* c, int l, const double* rf, double* fc) {
   const DevLevel& F = c->D[l];
   const DevLevel& C = c->D[l - 1];
-  launch_pdl(k_restrict_local, dim3((unsigned)F.g.nrec), dim3(transfer_threads(F.g.p)), transfer_smem(F.g.p, C.g.p), c->st,
-             F.g, C.g.p, (const double*)F.Jint, rf, c->Z);
+  launch_restrict(F.g, C.g, F.Jint, rf, c->Z, fc, transfer_threads(F.g.p), transfer_smem(F.g.p, C.g.p),
+                  grid_for(C.g.nskel), c->st);
   LAUNCH_CHECK(c);
-  launch_pdl(k_restrict_gather, dim3(grid_for(C.g.nskel)), dim3(kThreads), 0, c->st, C.g, (const double*)c->Z, fc);
-  LAUNCH_CHECK(c);
+  c->launches++;   // local + gather
   return PMG_OK;
 }
 
 pmg_status prolong_dev(pmg_ctx* c, int l, const double* uc, double* uf) {
   const DevLevel& F = c->D[l];
   const DevLevel& C = c->D[l - 1];
-  launch_pdl(k_prolong, dim3((unsigned)F.g.nrec), dim3(transfer_threads(F.g.p)), transfer_smem(F.g.p, C.g.p), c->st,
-             F.g, C.g, (const double*)F.Jint, uc, uf);
+  launch_prolong(F.g, C.g, F.Jint, uc, uf, transfer_threads(F.g.p), transfer_smem(F.g.p, C.g.p), c->st);
   LAUNCH_CHECK(c);
   return PMG_OK;
 }
@@ -279,31 +273,6 @@ pmg_status pcg_dev(pmg_ctx* c, const double* b, double* x) {
   TimedRegion tr(c, 2, true);
   const DevLevel& D = c->D[0];
   const long long n = c->g0g.nskel;
-  if (c->use_cluster) {   // one cluster launch, everything on chip
-    LevelGeom g0 = c->g0g;
-    double lam = c->lam, rtol = c->opt.coarse_rtol;
-    int maxit = c->opt.coarse_maxit, chunk = c->cl_chunk, halo = c->cl_halo;
-    unsigned long long inv = c->cl_inv;
-    PcgState* st = c->pcg;
-    const double* dinv = c->dinv;
-    CoarseTabs ct{c->ctab[0], c->ctab[1], c->ctab[2], c->ctab[3], c->ctab[4], c->ctab[5], c->ctab[6]};
-    void* args[] = {&g0, &ct, (void*)&b, &x, (void*)&dinv, &lam, &chunk, &halo, &inv, &st, &rtol, &maxit};
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(c->cl_size);
-    cfg.blockDim = dim3(c->cl_threads);
-    cfg.dynamicSmemBytes = c->cl_smem;
-    cfg.stream = c->st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = c->cl_size;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    CUDA_CHECK(cudaLaunchKernelExC(&cfg, (const void*)k_pcg_cluster_p2, args));
-    c->launches++;
-    return PMG_OK;
-  }
   if (c->use_coop) {   // one launch, no host synchronisation; statistics read at the end of solve
     LevelGeom g0 = c->g0g;
     double lam = c->lam, rtol = c->opt.coarse_rtol;
@@ -884,8 +853,8 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   // several contexts with different degrees can coexist
   cudaError_t e1 = cudaFuncSetAttribute(k_elem_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
   cudaError_t e2 = cudaFuncSetAttribute(k_star, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
-  cudaError_t e3 = cudaFuncSetAttribute(k_restrict_local, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
-  cudaError_t e4 = cudaFuncSetAttribute(k_prolong, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  cudaError_t e3 = transfer_set_smem_attr(smem_optin);
+  cudaError_t e4 = cudaSuccess;
   cudaError_t e5 = condense_recover_set_smem_attr(smem_optin);
   cudaError_t e6 = cudaSuccess;
   if (e6 == cudaSuccess) e6 = hot_set_smem_attr(smem_optin);
@@ -911,47 +880,6 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
       if (cudaMallocHost(reinterpret_cast<void**>(&c->hres), sizeof(double)) != cudaSuccess) {
         free_ctx(c);
         return fail(PMG_ENOMEM, "cudaMallocHost failed");
-      }
-      // cluster variant: all CG vectors of a coarse system that fits in 16 SMs' shared memory
-      {
-        const LevelGeom& g0 = c->g0g;
-        const char* ce = std::getenv("PMG_COARSE_CLUSTER");
-        // opt-in: on the 16 SMs of one cluster the per-entry index arithmetic is slower than the
-        // grid barrier it saves (measured)
-        const bool want_cluster = (ce && ce[0] == '1');
-        int csz = 16;
-        if (cudaFuncSetAttribute(k_pcg_cluster_p2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
-          cudaGetLastError();
-          csz = 8;
-        }
-        const long long n0 = g0.nskel;
-        const int chunk = (int)((n0 + csz - 1) / csz);
-        const long long halo = 7LL * (1 + g0.V1 + (long long)g0.V1 * g0.V2) + 7;
-        const size_t smem = sizeof(double) * (size_t)(5LL * chunk + 2 * halo);
-        if (want_cluster && smem <= (size_t)smem_optin - 2048 && halo < (1LL << 30)) {
-          cudaFuncSetAttribute(k_pcg_cluster_p2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin - 2048);
-          cudaLaunchConfig_t cfg = {};
-          cfg.gridDim = dim3(csz);
-          cfg.blockDim = dim3(c->cl_threads);
-          cfg.dynamicSmemBytes = smem;
-          cudaLaunchAttribute attr[1];
-          attr[0].id = cudaLaunchAttributeClusterDimension;
-          attr[0].val.clusterDim.x = csz;
-          attr[0].val.clusterDim.y = 1;
-          attr[0].val.clusterDim.z = 1;
-          cfg.attrs = attr;
-          cfg.numAttrs = 1;
-          int nclusters = 0;
-          if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)k_pcg_cluster_p2, &cfg) == cudaSuccess && nclusters > 0) {
-            c->use_cluster = true;
-            c->cl_size = csz;
-            c->cl_chunk = chunk;
-            c->cl_halo = (int)halo;
-            c->cl_smem = smem;
-            c->cl_inv = ((1ULL << 40) + (unsigned long long)chunk - 1) / (unsigned long long)chunk;
-          }
-          cudaGetLastError();
-        }
       }
       {
         int per_sm_reg = 0;

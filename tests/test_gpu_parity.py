@@ -352,3 +352,43 @@ def test_degenerate_meshes(k, p):
     assert rep["cycles"] == rep_o["cycles"], (rep["cycles"], rep_o["cycles"])
     assert rel(ug.cpu().numpy(), u_o) < SOLVE_TOL
     s.close()
+
+
+@pytest.mark.parametrize("name", ["k323_p4_lam1.7_stretched", "k333_p8_lam0", "k222_p6_lam2"])
+def test_kernel_variants_agree(name, monkeypatch):
+    """The alternative kernels kept for A/B measurements compute the same operators as the
+    defaults: star smoother variants (DFMA transforms, DMMA without prefetch, 128-thread prefetching
+    kernel at p <= 4), element-operator variants (DFMA, DMMA without the boundary cube), and the
+    runtime-degree reference kernels."""
+    import paper_1808_03595_b200 as pmg
+    P = pair(name)
+    case = P.case
+    rng = np.random.default_rng(4)
+    outs = {}
+    for label, env in [("default", {}), ("star1", {"PMG_STAR_VARIANT": "1"}), ("star2", {"PMG_STAR_VARIANT": "2"}),
+                       ("star3", {"PMG_STAR_VARIANT": "3"}), ("elem1", {"PMG_ELEM_VARIANT": "1"}),
+                       ("elem2", {"PMG_ELEM_VARIANT": "2"}), ("ref", {"PMG_REFERENCE_KERNELS": "1"})]:
+        for k in ("PMG_STAR_VARIANT", "PMG_ELEM_VARIANT", "PMG_REFERENCE_KERNELS"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        s = pmg.Solver(case.k, case.widths, case.p, case.lam, coarse_rtol=1e-13)
+        res = []
+        for l in range(s.nlevels):
+            g = torch.from_numpy(np.random.default_rng(l).standard_normal(s.level_info(l)[2])).cuda()
+            x = s.new_skel(l)
+            s.skel_from_grid(l, g, x)
+            r = s.new_skel(l)
+            s.residual(l, x, None, r)
+            u = s.new_skel(l)
+            s.smooth(l, x, u)
+            torch.cuda.synchronize()
+            res.append((r.cpu().numpy(), u.cpu().numpy()))
+        outs[label] = res
+        s.close()
+    base = outs["default"]
+    for label, res in outs.items():
+        for (r, u), (r0, u0) in zip(res, base):
+            assert rel(r, r0) < 1e-12, (label, rel(r, r0))
+            assert rel(u, u0) < 1e-12, (label, rel(u, u0))
+    del rng
