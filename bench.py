@@ -328,6 +328,11 @@ def main():
         "residual_kernel": residual,
         "time_split_ms_per_step": {"smoother_all_levels": all_sm_ms / args.steps, "residual_all_levels": all_rs_ms / args.steps,
                                    "coarse_cg": cg_ms / args.steps},
+        # the coarse CG is the largest single kernel at config 2 but is latency bound (no roofline
+        # applies): one grid barrier (1.2 us measured, profiles/r01_gridsync.txt) per iteration
+        "coarse_cg": {"share_of_step": (cg_ms / args.steps) / ms, "iterations_per_solve": r["coarse_iters"],
+                      "us_per_iteration": 1e3 * (cg_ms / args.steps) / max(1, r["coarse_iters"]),
+                      "bound": "latency: one grid barrier + two overlapped L2 round trips per iteration"},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

@@ -235,7 +235,10 @@ struct LoopTransport : Transport {
 
 std::string make_transport(int rank, int nranks, const void* nccl_id, void* loopback, Transport** out) {
   *out = nullptr;
-  if (nranks == 1) return "";
+  // one rank without a transport: plain one-GPU path.  One rank WITH an nccl_id builds a
+  // communicator of size 1 -- the whole z-slab machinery (allgathered coarse RHS, allreduced
+  // norms, NCCL calls inside the captured graph) runs with no neighbours (tests on one GPU).
+  if (nranks == 1 && !nccl_id && !loopback) return "";
   if ((nccl_id != nullptr) == (loopback != nullptr)) return "nranks > 1 needs exactly one of nccl_id / loopback";
   if (loopback) {
     LoopHub* hub = static_cast<LoopHub*>(loopback);

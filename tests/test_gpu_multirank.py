@@ -213,3 +213,29 @@ def test_krylov_solve_matches_one_gpu(nr):
         lo, hi = sl["z0"] * case.p * pl, (sl["z1"] * case.p + 1) * pl
         assert rep["cycles"] == rep1["cycles"]
         assert np.abs(u - u1[lo:hi]).max() <= 1e-12 * np.abs(u1).max()
+
+
+@pytest.mark.parametrize("solver", [0, 1])
+@pytest.mark.parametrize("name", ["k325_p4_lam1.7_stretched", "k334_p8_lam0", "k236_p2_lam0.3"])
+def test_nccl_transport_single_rank(name, solver):
+    """The NCCL transport on one GPU (a communicator of size 1): the library loads NCCL, builds the
+    communicator from a unique id, and runs the whole z-slab solve path -- slab tables, the
+    allgathered coarse right-hand side, allreduced norms, NCCL calls captured into the solve's CUDA
+    graph -- with no neighbours.  It must reproduce the plain one-GPU solve bitwise."""
+    import paper_1808_03595_b200 as pmg
+    cfg = CASES[name]
+    case = pi.small_case(cfg["k"], cfg["p"], cfg["lam"], stretch=cfg["stretch"])
+    s1 = one_gpu(case, solver=solver)
+    f_np, F_np = global_F(case, s1)
+    u1 = s1.new_grid()
+    rep1 = s1.solve(torch.from_numpy(F_np).cuda(), u1, 1e-10)
+    s1.close()
+    s = pmg.Solver(case.k, case.widths, case.p, case.lam, rank=0, nranks=1, nccl_id=pmg.nccl_unique_id(),
+                   solver=solver)
+    u = s.new_grid()
+    rep = s.solve(torch.from_numpy(F_np).cuda(), u, 1e-10)
+    rep2 = s.solve(torch.from_numpy(F_np).cuda(), u, 1e-10)      # graph replay
+    torch.cuda.synchronize()
+    assert rep["cycles"] == rep1["cycles"] == rep2["cycles"]
+    assert torch.equal(u, u1)
+    s.close()
