@@ -1540,6 +1540,156 @@ __global__ void __launch_bounds__(ElemPfCfg<P>::NT, ElemPfCfg<P>::MINB)
 }
 
 // ------------------------------------------------------------------------------------------
+// star smoother, 17 <= P <= 32 (same arithmetic and citations as k_star_t: Alg. 1 + Alg. 2,
+// P:294-331): the twelve n_S x n_S transforms on DMMA with n_S padded to 64 (LD 68), S read from
+// the L2-resident star tables (guarded: zero outside n_S) instead of being staged, the 3-pass core
+// of k_star_t (a single-pass core's cross-warp partials do not fit next to two padded plane
+// triples in 227 KB).  A DFMA transform needs two shared-memory loads per FMA; a DMMA does 256 FMA
+// per two fragment loads.
+// ------------------------------------------------------------------------------------------
+template <int P> struct StarTmCfg {
+  static constexpr int N = 2 * P - 1, NN = N * N, C = P - 1, NP = 64, LD = 68, MS = NP * LD;
+  static constexpr int NT = 256, NW = 8, TPP = (NP / 8) * (NP / 8);
+  static constexpr int oFT = 0, oG = 3 * MS, oVec = 6 * MS, total = oVec + 9 * N;
+};
+
+template <int P>
+size_t star_tm_smem() { return sizeof(double) * StarTmCfg<P>::total; }
+
+// C(8x8 tile mi, ni) = A B with element accessors a(i, k), b(k, j); one warp
+template <int KT, class FA, class FB>
+__device__ __forceinline__ void dmma_tile_fn(const FA& a, const FB& b, double* Cm, int ldc, int mi, int ni, int lane) {
+  const int r = lane >> 2, q = lane & 3;
+  double c0 = 0.0, c1 = 0.0;
+#pragma unroll 4
+  for (int kk = 0; kk < KT / 4; ++kk) dmma884(c0, c1, a(8 * mi + r, 4 * kk + q), b(4 * kk + q, 8 * ni + r));
+  Cm[(8 * mi + r) * ldc + 8 * ni + 2 * q] = c0;
+  Cm[(8 * mi + r) * ldc + 8 * ni + 2 * q + 1] = c1;
+}
+
+template <int P>
+__global__ void __launch_bounds__(256, 1) k_star_tm(LevelGeom g, int c1, int c2, int c3, int n1c, int n2c,
+                                                   const double* __restrict__ r, double* __restrict__ u,
+                                                   const double* __restrict__ stab, double lam) {
+  using C = StarTmCfg<P>;
+  constexpr int N = C::N, NN = C::NN, c = C::C, NT = C::NT, NP = C::NP, LD = C::LD, MS = C::MS, TPP = C::TPP;
+  extern __shared__ double sm[];
+  const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
+  const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
+  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 + g.zoff == 0 || v3 + g.zoff == g.K3)) return;
+  if (v3 < g.own_lo) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, ST = g.ST;
+  const double* S[3] = {stab + (size_t)v1 * ST, stab + (size_t)(g.V1 + v2) * ST, stab + (size_t)(g.V1 + g.V2 + v3) * ST};
+  double* FT = sm + C::oFT;
+  double* Gs = sm + C::oG;
+  double* vec = sm + C::oVec;
+  for (int i = tid; i < 9 * N; i += NT) { const int d = i / (3 * N); vec[i] = __ldg(&S[d][NN + i - d * 3 * N]); }
+  for (int i = tid; i < 3 * MS; i += NT) FT[i] = 0.0;           // padding must be finite (zero)
+  pdl_wait();
+  pdl_trigger();
+  __syncthreads();
+  const int o1 = (v1 - 1) * P + 1, o2 = (v2 - 1) * P + 1, o3 = (v3 - 1) * P + 1;
+  for (int i = tid; i < 3 * NN; i += NT) {
+    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
+    int j1, j2, j3;
+    if (d == 0) { j1 = c; j2 = B; j3 = A; } else if (d == 1) { j2 = c; j1 = B; j3 = A; } else { j3 = c; j1 = B; j2 = A; }
+    const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
+    const double val = inside(g, g1, g2, g3) ? __ldg(&r[skel_index_t<P>(g, g1, g2, g3)]) : 0.0;
+    FT[d * MS + A * LD + B] = val * (1.0 / (double)(1 + (A == c) + (B == c)));   // inverse multiplicity
+  }
+  __syncthreads();
+  auto sget = [](const double* Sd, int row, int col) { return (row < N && col < N) ? __ldg(&Sd[row * N + col]) : 0.0; };
+  // forward A: X_d = F_d S_a  (X into G's space)
+  for (int job = warp; job < 3 * TPP; job += C::NW) {
+    const int d = job / TPP, t = job - d * TPP, mi = t >> 3, ni = t & 7;
+    const double* Fd = FT + d * MS;
+    const double* Sa = S[d == 0 ? 1 : 0];
+    dmma_tile_fn<NP>([&](int i, int k) { return Fd[i * LD + k]; }, [&](int k, int j) { return sget(Sa, k, j); },
+                     Gs + d * MS, LD, mi, ni, lane);
+  }
+  __syncthreads();
+  // forward B: T_d = S_b^T X_d  (into FT)
+  for (int job = warp; job < 3 * TPP; job += C::NW) {
+    const int d = job / TPP, t = job - d * TPP, mi = t >> 3, ni = t & 7;
+    const double* Xd = Gs + d * MS;
+    const double* Sb = S[d == 2 ? 1 : 2];
+    dmma_tile_fn<NP>([&](int i, int k) { return sget(Sb, k, i); }, [&](int k, int j) { return Xd[k * LD + j]; },
+                     FT + d * MS, LD, mi, ni, lane);
+  }
+  __syncthreads();
+  // fused core (expand / D^-1 / contract), three passes each reducing along one axis (k_star_t)
+  {
+    const double *L1 = vec, *s1 = vec + N, *L2 = vec + 3 * N, *s2 = vec + 4 * N, *L3 = vec + 6 * N, *s3 = vec + 7 * N;
+    const double *T1 = FT, *T2 = FT + MS, *T3 = FT + 2 * MS;
+    for (int i = tid; i < 3 * NN; i += NT) {
+      const int pass = i / NN, rr = i - pass * NN, hi = rr / N, lo = rr - hi * N;
+      double acc = 0.0;
+      if (pass == 0) {          // G1[a3][a2] = sum_a1 s1[a1] E
+        const int a3 = hi, a2 = lo;
+        const double t1 = T1[a3 * LD + a2], x2 = s2[a2], x3 = s3[a3], base = lam + L2[a2] + L3[a3];
+#pragma unroll 8
+        for (int a1 = 0; a1 < N; ++a1) {
+          double E = s1[a1] * t1;
+          E = fma(x2, T2[a3 * LD + a1], E);
+          E = fma(x3, T3[a2 * LD + a1], E);
+          acc = fma(s1[a1], E * rcp_nr(base + L1[a1]), acc);
+        }
+      } else if (pass == 1) {   // G2[a3][a1] = sum_a2 s2[a2] E
+        const int a3 = hi, a1 = lo;
+        const double t2 = T2[a3 * LD + a1], x1 = s1[a1], x3 = s3[a3], base = lam + L1[a1] + L3[a3];
+#pragma unroll 8
+        for (int a2 = 0; a2 < N; ++a2) {
+          double E = x1 * T1[a3 * LD + a2];
+          E = fma(s2[a2], t2, E);
+          E = fma(x3, T3[a2 * LD + a1], E);
+          acc = fma(s2[a2], E * rcp_nr(base + L2[a2]), acc);
+        }
+      } else {                  // G3[a2][a1] = sum_a3 s3[a3] E
+        const int a2 = hi, a1 = lo;
+        const double t3 = T3[a2 * LD + a1], x1 = s1[a1], x2 = s2[a2], base = lam + L1[a1] + L2[a2];
+#pragma unroll 8
+        for (int a3 = 0; a3 < N; ++a3) {
+          double E = x1 * T1[a3 * LD + a2];
+          E = fma(x2, T2[a3 * LD + a1], E);
+          E = fma(s3[a3], t3, E);
+          acc = fma(s3[a3], E * rcp_nr(base + L3[a3]), acc);
+        }
+      }
+      Gs[pass * MS + hi * LD + lo] = acc;
+    }
+  }
+  __syncthreads();
+  // back A: X_d = G_d S_a^T  (into FT) ; back B: U_d = S_b X_d  (into G)
+  for (int job = warp; job < 3 * TPP; job += C::NW) {
+    const int d = job / TPP, t = job - d * TPP, mi = t >> 3, ni = t & 7;
+    const double* Gd = Gs + d * MS;
+    const double* Sa = S[d == 0 ? 1 : 0];
+    dmma_tile_fn<NP>([&](int i, int k) { return Gd[i * LD + k]; }, [&](int k, int j) { return sget(Sa, j, k); },
+                     FT + d * MS, LD, mi, ni, lane);
+  }
+  __syncthreads();
+  for (int job = warp; job < 3 * TPP; job += C::NW) {
+    const int d = job / TPP, t = job - d * TPP, mi = t >> 3, ni = t & 7;
+    const double* Xd = FT + d * MS;
+    const double* Sb = S[d == 2 ? 1 : 2];
+    dmma_tile_fn<NP>([&](int i, int k) { return sget(Sb, i, k); }, [&](int k, int j) { return Xd[k * LD + j]; },
+                     Gs + d * MS, LD, mi, ni, lane);
+  }
+  __syncthreads();
+  const double *w1 = vec + 2 * N, *w2 = vec + 5 * N, *w3 = vec + 8 * N;
+  for (int i = tid; i < 3 * NN; i += NT) {
+    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
+    int j1, j2, j3;
+    if (d == 0) { j1 = c; j2 = B; j3 = A; }
+    else if (d == 1) { j2 = c; j1 = B; j3 = A; if (j1 == c) continue; }
+    else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
+    const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
+    if (!is_free(g, g1, g2, g3)) continue;
+    u[skel_index_t<P>(g, g1, g2, g3)] += w1[j1] * w2[j2] * w3[j3] * Gs[d * MS + A * LD + B];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // star smoother, P <= 4: one WARP per star, four stars per CTA (same arithmetic and citations as
 // k_star_pf: Alg. 1 + Alg. 2).  At n_S <= 7 a 128-thread star leaves most lanes idle
 // in every phase; here each warp runs its star alone with __syncwarp only (no CTA barrier), the
@@ -2056,6 +2206,12 @@ void launch_star_p(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c,
     else
       k_star_sp<P><<<(unsigned)nb, StarSpCfg<P>::NT, star_sp_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
   } else {
+    if constexpr (P > 16) {
+      if (star_variant() != 1) {   // 1: the DFMA-transform kernel (A/B)
+        launch_pdl(k_star_tm<P>, dim3((unsigned)nb), dim3(StarTmCfg<P>::NT), star_tm_smem<P>(), st, g, c1, c2, c3, n1c, n2c, r, u, stab, lam);
+        return;
+      }
+    }
     launch_pdl(k_star_t<P>, dim3((unsigned)nb), dim3(StarCfg<P>::NT), star_t_smem<P>(), st, g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
   }
 }
@@ -2111,7 +2267,7 @@ cudaError_t launch_star(const LevelGeom& g, int c1, int c2, int c3, int n1c, int
 size_t hot_smem(int p, int which) {
   switch (p) {
 #define CASE(P) \
-  case P: return which == 0 ? std::max(std::max(elem_t_smem<P>(), elem16_smem<(P > 8 && P <= 16 ? P : 9)>()), std::max(elem_dm_smem<(P <= 8 ? P : 2)>(), elem_pf_smem<(P <= 8 ? P : 2)>())) : (kStarSinglePass(P) ? std::max(std::max(std::max(star_sp_smem<(P <= 8 ? P : 2)>(), star_dm_smem<(P <= 8 ? P : 2)>()), star_pf_smem<(P <= 8 ? P : 2)>()), star_w_smem<(P <= 4 ? P : 2)>()) : (kStarPf(P) ? star_pf_smem<(P <= 16 ? P : 2)>() : star_t_smem<P>()));
+  case P: return which == 0 ? std::max(std::max(elem_t_smem<P>(), elem16_smem<(P > 8 && P <= 16 ? P : 9)>()), std::max(elem_dm_smem<(P <= 8 ? P : 2)>(), elem_pf_smem<(P <= 8 ? P : 2)>())) : (kStarSinglePass(P) ? std::max(std::max(std::max(star_sp_smem<(P <= 8 ? P : 2)>(), star_dm_smem<(P <= 8 ? P : 2)>()), star_pf_smem<(P <= 8 ? P : 2)>()), star_w_smem<(P <= 4 ? P : 2)>()) : (kStarPf(P) ? star_pf_smem<(P <= 16 ? P : 2)>() : std::max(star_t_smem<P>(), star_tm_smem<(P > 16 ? P : 17)>())));
     PMG_DEGREES(CASE)
 #undef CASE
     default: return 0;
@@ -2134,6 +2290,8 @@ cudaError_t hot_set_smem_attr(int bytes) {
       b = cudaFuncSetAttribute(k_star_sp<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (b == cudaSuccess && kStarSinglePass(P))                                                        \
       b = cudaFuncSetAttribute(k_star_dm<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+    if (b == cudaSuccess && P > 16)                                                                    \
+      b = cudaFuncSetAttribute(k_star_tm<(P > 16 ? P : 17)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (b == cudaSuccess && P <= 4)                                                                    \
       b = cudaFuncSetAttribute(k_star_w<(P <= 4 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (b == cudaSuccess && kStarPf(P))                                                                \

@@ -146,7 +146,7 @@ def _sampled_vertex_smoother(case, rg, dug, rng, nsample):
     return max(errs)
 
 
-@pytest.mark.parametrize("cfg,p", [(2, None), (3, 4), (3, 8), (3, 12), (3, 16), (4, None)])
+@pytest.mark.parametrize("cfg,p", [(2, None), (3, 4), (3, 8), (3, 12), (3, 16), (3, 24), (4, None)])
 def test_fullsize_smoother_sampled(cfg, p):
     case = pi.config(cfg, p=p)
     s = _solver(case)

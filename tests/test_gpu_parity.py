@@ -392,3 +392,56 @@ def test_kernel_variants_agree(name, monkeypatch):
             assert rel(r, r0) < 1e-12, (label, rel(r, r0))
             assert rel(u, u0) < 1e-12, (label, rel(u, u0))
     del rng
+
+
+def test_solve_host_and_report_paths():
+    """pmg_solve_host (host buffers, pageable and pinned) equals the device solve bitwise; repeated
+    solves are bitwise deterministic (graph replay); max_cycles too small returns PMG_ENOCONV with
+    the report filled and u written."""
+    import paper_1808_03595_b200 as pmg
+    from oracle import condensed
+    P = pair("k323_p4_lam1.7_stretched")
+    s = P.gpu
+    L = s.nlevels - 1
+    m = P.mesh(L)
+    F = condensed.weak_rhs(m, pi.uniform_pm1(12, np.arange(m.ntot)))
+    Fd = torch.from_numpy(F).cuda()
+    u1, u2 = s.new_grid(), s.new_grid()
+    r1 = s.solve(Fd, u1, 1e-10)
+    r2 = s.solve(Fd, u2, 1e-10)
+    torch.cuda.synchronize()
+    assert torch.equal(u1, u2) and r1["history"] == r2["history"]
+    uh = np.zeros_like(F)
+    rh = s.solve_host(np.ascontiguousarray(F), uh, 1e-10)
+    assert rh["cycles"] == r1["cycles"] and np.array_equal(uh, u1.cpu().numpy())
+    Fp = torch.from_numpy(F).pin_memory()
+    up = torch.zeros_like(Fp).pin_memory()
+    s.solve_host(Fp, up, 1e-10)
+    assert np.array_equal(up.numpy(), uh)
+    u3 = s.new_grid()
+    r3 = s.solve(Fd, u3, 1e-10, max_cycles=1)
+    torch.cuda.synchronize()
+    assert r3["status"] == pmg.PMG_ENOCONV and not r3["converged"] and r3["cycles"] == 1
+    assert r3["r_final"] < r3["r0"] and float(u3.abs().max()) > 0
+
+
+@pytest.mark.parametrize("k,p", [((2, 3, 2), 17), ((2, 2, 2), 24), ((2, 2, 3), 32)])
+def test_high_degree_star_kernels_agree(k, p, monkeypatch):
+    """p > 16: the DMMA-transform star kernel (k_star_tm, default) and the DFMA-transform kernel
+    (k_star_t) compute the same smoother; oracle parity at p = 24 is in test_gpu_fullsize."""
+    import paper_1808_03595_b200 as pmg
+    case = pi.small_case(k, p, 0.4, stretch=1.3)
+    outs = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("PMG_STAR_VARIANT", v)
+        s = pmg.Solver(case.k, case.widths, p, case.lam)
+        L = s.nlevels - 1
+        g = torch.from_numpy(np.random.default_rng(p).standard_normal(s.level_info(L)[2])).cuda()
+        r = s.new_skel(L)
+        s.skel_from_grid(L, g, r)
+        u = s.new_skel(L)
+        s.smooth(L, r, u)
+        torch.cuda.synchronize()
+        outs.append(u.cpu().numpy())
+        s.close()
+    assert rel(outs[0], outs[1]) < 1e-12
