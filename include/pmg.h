@@ -6,7 +6,8 @@
  *
  * Problem (Eq. helmholtz_equation):  lambda u - Laplace(u) = f on a box of
  * k1 x k2 x k3 cuboidal spectral elements of degree p (widths per direction), with
- * homogeneous Dirichlet conditions on the box boundary.  All arithmetic is FP64.
+ * homogeneous Dirichlet conditions on the box boundary -- or homogeneous Neumann on
+ * the faces selected by pmg_options.neumann.  All arithmetic is FP64.
  *
  * Conventions shared by every call
  *  - Every call returns pmg_status; PMG_OK = 0.  No C++ exception crosses the ABI.  On an
@@ -24,8 +25,8 @@
  *    the interiors of the three faces and three edges leaving the vertex in +x_d direction,
  *    then the vertex itself: [f1: (p-1)^2][f2: (p-1)^2][f3: (p-1)^2][e1: p-1][e2][e3][vertex].
  *    Length = (k1+1)(k2+1)(k3+1) * (3(p-1)^2 + 3(p-1) + 1) doubles (pmg_level_info).
- *    Entries that are not free unknowns (on the Dirichlet boundary or outside the box) are
- *    zero on input and are written as zero on output.
+ *    Entries that are not free unknowns (on a Dirichlet face or outside the box) are zero on
+ *    input and are written as zero on output.
  *  - Levels: l = 0 .. L with degrees p_l = p0 2^l (l < L), p_L = p, L = ceil(log2(p/p0))
  *    (reading R10).  Level L is the finest.
  *  - z-slabs (nranks > 1): every rank calls the same functions in the same
@@ -59,6 +60,9 @@ typedef struct {
   int p0;             /* coarse degree, default 2 */
   int weight_degree;  /* degree of the weight polynomial, default 7; only 7 supported */
   int schedule;       /* 0: nu_pre = nu_post = 1 ("MG"); 1: 2^(L-l) */
+  int neumann;        /* homogeneous Neumann faces (bitmask: bit 2d / 2d+1 = low / high face of
+                         direction d); every other face is homogeneous
+                         Dirichlet.  Default 0 (all Dirichlet).  All six Neumann needs lambda > 0. */
   int solver;         /* pmg_solve: 0 = multigrid fixpoint iteration (Alg. 4, "MG");
                          1 = Krylov-accelerated multigrid, inexact preconditioned CG with one V-cycle
                          from zero as preconditioner (Alg. 5; "kMG", with schedule 1 "kvMG") */

@@ -12,7 +12,10 @@ from .gll import gll
 
 
 class Mesh:
-    def __init__(self, k, widths, p, origin=(0.0, 0.0, 0.0)):
+    def __init__(self, k, widths, p, origin=(0.0, 0.0, 0.0), neumann=0):
+        """neumann: bit 2d / 2d+1 set = homogeneous Neumann on the low / high face of direction d
+        (SURVEY 8(f) NEXT-3); every other face is homogeneous Dirichlet."""
+        self.neumann = int(neumann)
         self.k = tuple(int(v) for v in k)
         self.p = int(p)
         if self.p < 1:
@@ -39,13 +42,20 @@ class Mesh:
         i3, i2, i1 = np.meshgrid(np.arange(self.N[2]), np.arange(self.N[1]), np.arange(self.N[0]),
                                  indexing="ij")
         self.idx = (i1, i2, i3)
-        interior = ((i1 > 0) & (i1 < self.N[0] - 1) & (i2 > 0) & (i2 < self.N[1] - 1)
-                    & (i3 > 0) & (i3 < self.N[2] - 1))
+        interior = self.free1d(0, i1) & self.free1d(1, i2) & self.free1d(2, i3)
         skel = (i1 % self.p == 0) | (i2 % self.p == 0) | (i3 % self.p == 0)
-        self.free = interior.ravel()              # not on the Dirichlet boundary
+        self.free = interior.ravel()              # not on a Dirichlet face
         self.skel = skel.ravel()                  # element-boundary points
         self.free_skel = self.free & self.skel    # condensed unknowns
         self._build_elements()
+
+    def free1d(self, d, g):
+        """Global 1-D indices g along d that are unknowns: inside [0, N_d - 1] and not on a
+        Dirichlet end (a Neumann end point is an unknown)."""
+        g = np.asarray(g)
+        lo = bool(self.neumann >> (2 * d) & 1)
+        hi = bool(self.neumann >> (2 * d + 1) & 1)
+        return (g >= 0) & (g <= self.N[d] - 1) & ((g > 0) | lo) & ((g < self.N[d] - 1) | hi)
 
     def flat(self, i1, i2, i3):
         return np.asarray(i1) + self.N[0] * (np.asarray(i2) + self.N[1] * np.asarray(i3))

@@ -29,8 +29,8 @@ def level_degrees(p, p0=2):
 
 
 class Level:
-    def __init__(self, k, widths, p, lam, pw):
-        self.mesh = Mesh(k, widths, p)
+    def __init__(self, k, widths, p, lam, pw, neumann=0):
+        self.mesh = Mesh(k, widths, p, neumann=neumann)
         self.op = CondensedOperator(self.mesh, lam)
         self.smoother = StarSmoother(self.op, pw)
         d = self.op.diag()
@@ -68,10 +68,11 @@ def pcg(level, b, rtol, maxit):
 
 class Hierarchy:
     def __init__(self, k, widths, p, lam, p0=2, pw=7, schedule=0, coarse_rtol=1e-8,
-                 coarse_maxit=10000):
+                 coarse_maxit=10000, neumann=0):
+        """neumann: face bitmask of homogeneous Neumann faces (Mesh; NEXT-3)."""
         self.degrees = level_degrees(p, p0)
         self.L = len(self.degrees) - 1
-        self.levels = [Level(k, widths, q, lam, pw) for q in self.degrees]
+        self.levels = [Level(k, widths, q, lam, pw, neumann) for q in self.degrees]
         self.transfers = [None] + [Transfer(self.levels[l - 1].mesh, self.levels[l].mesh)
                                    for l in range(1, self.L + 1)]
         self.schedule = schedule

@@ -6,7 +6,8 @@ P:151-163: the subdomain of vertex i is the 2x2x2 element block around it; after
 P:309-333 Alg. 2: loop over all vertex stars, extract, invert, weight and add.
 P:312-316: W_i is the restriction of w(x)w(x)w with w the degree-7 weight polynomial.
 P:348-375 Sec. 3.3: boundary vertices keep the same star shape; points outside the domain or
-  on the Dirichlet boundary are decoupled (identity padding) and receive no correction.
+  on a Dirichlet face are decoupled (identity padding) and receive no correction; points on a
+  Neumann face are unknowns of the star (NEXT-3).
 
 The oracle inverts every star by a DENSE LU factorisation of its explicitly assembled condensed
 operator (the north-star oracle; "matrix inversion").  ``star_matrix_block`` builds
@@ -41,8 +42,7 @@ def star_points(mesh, v):
     j1, j2, j3 = j1.ravel(), j2.ravel(), j3.ravel()
     on_plane = (j1 == c) | (j2 == c) | (j3 == c)
     G1, G2, G3 = g[0][j1], g[1][j2], g[2][j3]
-    valid = ((G1 > 0) & (G1 < mesh.N[0] - 1) & (G2 > 0) & (G2 < mesh.N[1] - 1)
-             & (G3 > 0) & (G3 < mesh.N[2] - 1))
+    valid = mesh.free1d(0, G1) & mesh.free1d(1, G2) & mesh.free1d(2, G3)
     keep = on_plane & valid
     return mesh.flat(G1[keep], G2[keep], G3[keep]), (j1[keep], j2[keep], j3[keep])
 
@@ -130,7 +130,7 @@ def star_1d(mesh, v, d):
                     K[j, i] += Ke[t, s]
             M[j, j] += Me[t, t]
     g = star_index_range(mesh, v, d)
-    valid = (g > 0) & (g < mesh.N[d] - 1)
+    valid = mesh.free1d(d, g)
     return M, K, valid
 
 

@@ -149,9 +149,11 @@ __device__ __forceinline__ double apply_entry(const LevelGeom& g, const CoarseTa
     for (int side = 0; side < 2; ++side) {
       int e[3] = {E.v1, E.v2, E.v3};
       if (side == 1) e[d] -= 1;
+      const bool ein = e[d] >= 0 && e[d] < (d == 0 ? g.k1 : (d == 1 ? g.k2 : g.k3));   // Neumann face: one element
+      if (!ein) e[d] = 0;
       const long long el = e[0] + (long long)g.k1 * (e[1] + (long long)g.k2 * e[2]);
 #pragma unroll
-      for (int i = 0; i < 7; ++i) cw[side][i] = __ldg(&ct.ce[el * 7 + i]);
+      for (int i = 0; i < 7; ++i) cw[side][i] = ein ? __ldg(&ct.ce[el * 7 + i]) : 0.0;
       const int b1 = 2 * e[0], b2 = 2 * e[1], b3 = 2 * e[2];
       fx[6 * side + 0] = sidx_or_neg(g, b1, b2 + 1, b3 + 1);
       fx[6 * side + 1] = sidx_or_neg(g, b1 + 2, b2 + 1, b3 + 1);
@@ -242,6 +244,7 @@ __device__ __forceinline__ void build_row(const LevelGeom& g, const CoarseTabs& 
     for (int side = 0; side < 2; ++side) {
       int e[3] = {E.v1, E.v2, E.v3};
       if (side == 1) e[d] -= 1;
+      if (e[d] < 0 || e[d] >= (d == 0 ? g.k1 : (d == 1 ? g.k2 : g.k3))) continue;   // Neumann face: one element
       const long long el = e[0] + (long long)g.k1 * (e[1] + (long long)g.k2 * e[2]);
       double cw[7];
 #pragma unroll

@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(StarCfg<P>::NT) k_star_t(LevelGeom g, int c1, 
   extern __shared__ double sm[];
   const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
   const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
-  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 + g.zoff == 0 || v3 + g.zoff == g.K3)) return;
+  if (star_empty(g, v1, v2, v3)) return;
   if (v3 < g.own_lo) return;   // ghost star below the slab: computed by the lower rank
   const int tid = threadIdx.x, ST = g.ST;
   const size_t row[3] = {(size_t)v1, (size_t)(g.V1 + v2), (size_t)(g.V1 + g.V2 + v3)};
@@ -690,7 +690,7 @@ __global__ void __launch_bounds__(StarSpCfg<P>::NT) k_star_sp(LevelGeom g, int c
   extern __shared__ double sm[];
   const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
   const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
-  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 + g.zoff == 0 || v3 + g.zoff == g.K3)) return;
+  if (star_empty(g, v1, v2, v3)) return;
   if (v3 < g.own_lo) return;   // ghost star below the slab: computed by the lower rank
   const int tid = threadIdx.x, ST = g.ST;
   const size_t row[3] = {(size_t)v1, (size_t)(g.V1 + v2), (size_t)(g.V1 + g.V2 + v3)};
@@ -848,7 +848,7 @@ __global__ void __launch_bounds__(StarDmCfg<P>::NT) k_star_dm(LevelGeom g, int c
   extern __shared__ double sm[];
   const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
   const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
-  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 + g.zoff == 0 || v3 + g.zoff == g.K3)) return;
+  if (star_empty(g, v1, v2, v3)) return;
   if (v3 < g.own_lo) return;   // ghost star below the slab: computed by the lower rank
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, ST = g.ST;
   const size_t row[3] = {(size_t)v1, (size_t)(g.V1 + v2), (size_t)(g.V1 + g.V2 + v3)};
@@ -1138,7 +1138,7 @@ __global__ void __launch_bounds__(StarPfCfg<P>::NT, StarPfCfg<P>::MINB)
   extern __shared__ double sm[];
   const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
   const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
-  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 + g.zoff == 0 || v3 + g.zoff == g.K3)) return;
+  if (star_empty(g, v1, v2, v3)) return;
   if (v3 < g.own_lo) return;   // ghost star below the slab: computed by the lower rank
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, ST = g.ST;
   const size_t row[3] = {(size_t)v1, (size_t)(g.V1 + v2), (size_t)(g.V1 + g.V2 + v3)};
@@ -1156,11 +1156,15 @@ __global__ void __launch_bounds__(StarPfCfg<P>::NT, StarPfCfg<P>::MINB)
   const StarMap<P>& map = kStarMap<P>;
   // point of map entry e: record coordinate w_d = v_d - bit; free iff (w_d > 0 or t_d > 0) and
   // w_d < k_d (global in z); stored (readable) iff w_d >= 0
-  auto pt_free = [&](unsigned e) {
+  auto pt_free = [&](unsigned e) {   // global test (w3 + zoff is the global record plane), Neumann faces free
     const int w1 = v1 - (int)((e >> 12) & 1u), w2 = v2 - (int)((e >> 13) & 1u), w3 = v3 - (int)((e >> 14) & 1u);
     const int W3 = w3 + g.zoff;
-    return w1 >= 0 && w2 >= 0 && w3 >= 0 && (w1 > 0 || !(e & (1u << 15))) && (w2 > 0 || !(e & (1u << 16))) &&
-           (W3 > 0 || !(e & (1u << 17))) && w1 < g.k1 && w2 < g.k2 && W3 < g.K3;
+    // the point is G_d = w_d p + t_d (0 <= t_d < p), t_d == 0 iff bit 15 + d
+    const bool z1 = e & (1u << 15), z2 = e & (1u << 16), z3 = e & (1u << 17);
+    return w1 >= 0 && w2 >= 0 && w3 >= 0 &&
+           (w1 > 0 || !z1 || (g.neu & 1)) && (w1 < g.k1 || (z1 && w1 == g.k1 && (g.neu & 2))) &&
+           (w2 > 0 || !z2 || (g.neu & 4)) && (w2 < g.k2 || (z2 && w2 == g.k2 && (g.neu & 8))) &&
+           (W3 > 0 || !z3 || (g.neu & 16)) && (W3 < g.K3 || (z3 && W3 == g.K3 && (g.neu & 32)));
   };
   // record base index of each of the 8 record-offset codes (-1: record outside the stored box)
   long long* s_base = reinterpret_cast<long long*>(sm + C::oBase);
@@ -1576,7 +1580,7 @@ __global__ void __launch_bounds__(256, 1) k_star_tm(LevelGeom g, int c1, int c2,
   extern __shared__ double sm[];
   const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
   const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
-  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 + g.zoff == 0 || v3 + g.zoff == g.K3)) return;
+  if (star_empty(g, v1, v2, v3)) return;
   if (v3 < g.own_lo) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, ST = g.ST;
   const double* S[3] = {stab + (size_t)v1 * ST, stab + (size_t)(g.V1 + v2) * ST, stab + (size_t)(g.V1 + g.V2 + v3) * ST};
@@ -1720,7 +1724,7 @@ __global__ void __launch_bounds__(128) k_star_w(LevelGeom g, int c1, int c2, int
   if (b >= nstars) return;
   const int i1 = (int)(b % n1c), rest = (int)(b / n1c), i2 = rest % n2c, i3 = rest / n2c;
   const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
-  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 + g.zoff == 0 || v3 + g.zoff == g.K3)) return;
+  if (star_empty(g, v1, v2, v3)) return;
   if (v3 < g.own_lo) return;
   const int ST = g.ST;
   double* FT = sm + C::oFT;
@@ -1734,11 +1738,15 @@ __global__ void __launch_bounds__(128) k_star_w(LevelGeom g, int c1, int c2, int
   const long long rec0 = v1 + g.V1 * (long long)v2 + V12 * v3;
   const bool interior = v1 > 0 && v2 > 0 && v3 > 0 && v1 < g.k1 && v2 < g.k2 && v3 + g.zoff < g.K3;
   const StarMap<P>& map = kStarMap<P>;
-  auto pt_free = [&](unsigned e) {
+  auto pt_free = [&](unsigned e) {   // global test (w3 + zoff is the global record plane), Neumann faces free
     const int w1 = v1 - (int)((e >> 12) & 1u), w2 = v2 - (int)((e >> 13) & 1u), w3 = v3 - (int)((e >> 14) & 1u);
     const int W3 = w3 + g.zoff;
-    return w1 >= 0 && w2 >= 0 && w3 >= 0 && (w1 > 0 || !(e & (1u << 15))) && (w2 > 0 || !(e & (1u << 16))) &&
-           (W3 > 0 || !(e & (1u << 17))) && w1 < g.k1 && w2 < g.k2 && W3 < g.K3;
+    // the point is G_d = w_d p + t_d (0 <= t_d < p), t_d == 0 iff bit 15 + d
+    const bool z1 = e & (1u << 15), z2 = e & (1u << 16), z3 = e & (1u << 17);
+    return w1 >= 0 && w2 >= 0 && w3 >= 0 &&
+           (w1 > 0 || !z1 || (g.neu & 1)) && (w1 < g.k1 || (z1 && w1 == g.k1 && (g.neu & 2))) &&
+           (w2 > 0 || !z2 || (g.neu & 4)) && (w2 < g.k2 || (z2 && w2 == g.k2 && (g.neu & 8))) &&
+           (W3 > 0 || !z3 || (g.neu & 16)) && (W3 < g.K3 || (z3 && W3 == g.K3 && (g.neu & 32)));
   };
   long long* s_base = reinterpret_cast<long long*>(sm + C::oBase);
   if (lane < 8) {
@@ -2092,6 +2100,9 @@ __global__ void __launch_bounds__(256) k_gather_resid_t(LevelGeom g, const doubl
   auto el = [&](int a1, int a2, int a3) -> size_t {
     return ((size_t)a1 + (size_t)g.k1 * ((size_t)a2 + (size_t)g.k2 * a3)) * YS;
   };
+  auto yat = [&](int a1, int a2, int a3, int off) -> double {   // 0 outside the box (Neumann faces)
+    return (a1 >= 0 && a2 >= 0 && a3 >= 0 && a1 < g.k1 && a2 < g.k2 && a3 < g.k3) ? Y[el(a1, a2, a3) + off] : 0.0;
+  };
   for (int o = threadIdx.x; o < RS; o += blockDim.x) {
     int t1 = 0, t2 = 0, t3 = 0, type, a = 0, b = 0;
     if (o < 3 * mm) {
@@ -2114,7 +2125,7 @@ __global__ void __launch_bounds__(256) k_gather_resid_t(LevelGeom g, const doubl
         const int d = type, oo = a * m + b;
         int w1 = v1, w2 = v2, w3 = v3;
         if (d == 0) w1 -= 1; else if (d == 1) w2 -= 1; else w3 -= 1;
-        s_ = Y[el(w1, w2, w3) + (2 * d + 1) * mm + oo] + Y[el(v1, v2, v3) + (2 * d) * mm + oo];
+        s_ = yat(w1, w2, w3, (2 * d + 1) * mm + oo) + yat(v1, v2, v3, (2 * d) * mm + oo);
       } else if (type < 6) {
         const int d = type - 3;
         for (int bB = 0; bB < 2; ++bB)
@@ -2124,14 +2135,14 @@ __global__ void __launch_bounds__(256) k_gather_resid_t(LevelGeom g, const doubl
             else if (d == 1) { a1 += bA - 1; a3 += bB - 1; }
             else { a1 += bA - 1; a2 += bB - 1; }
             const int qe = 4 * d + (1 - bA) + 2 * (1 - bB);
-            s_ += Y[el(a1, a2, a3) + 6 * mm + qe * m + a];
+            s_ += yat(a1, a2, a3, 6 * mm + qe * m + a);
           }
       } else {
         for (int c3 = 0; c3 < 2; ++c3)
           for (int c2 = 0; c2 < 2; ++c2)
             for (int c1 = 0; c1 < 2; ++c1) {
               const int qv = (1 - c1) + 2 * (1 - c2) + 4 * (1 - c3);
-              s_ += Y[el(v1 - 1 + c1, v2 - 1 + c2, v3 - 1 + c3) + 6 * mm + 12 * m + qv];
+              s_ += yat(v1 - 1 + c1, v2 - 1 + c2, v3 - 1 + c3, 6 * mm + 12 * m + qv);
             }
       }
       r = F ? F[rec * RS + o] - s_ : s_;

@@ -265,11 +265,15 @@ __global__ void k_gather_resid(LevelGeom g, const double* __restrict__ Y, const 
       auto el = [&](int a1, int a2, int a3) -> size_t {
         return ((size_t)a1 + (size_t)g.k1 * ((size_t)a2 + (size_t)g.k2 * a3)) * YS;
       };
+      // element output, 0 for an element outside the box (a Neumann-face point has one side only)
+      auto yat = [&](int a1, int a2, int a3, int off) -> double {
+        return (a1 >= 0 && a2 >= 0 && a3 >= 0 && a1 < g.k1 && a2 < g.k2 && a3 < g.k3) ? Y[el(a1, a2, a3) + off] : 0.0;
+      };
       if (E.type < 3) {
         const int d = E.type, o = E.a * m + E.b;
         int w1 = E.v1, w2 = E.v2, w3 = E.v3;
         if (d == 0) w1 -= 1; else if (d == 1) w2 -= 1; else w3 -= 1;
-        s = Y[el(w1, w2, w3) + (2 * d + 1) * mm + o] + Y[el(E.v1, E.v2, E.v3) + (2 * d) * mm + o];
+        s = yat(w1, w2, w3, (2 * d + 1) * mm + o) + yat(E.v1, E.v2, E.v3, (2 * d) * mm + o);
       } else if (E.type < 6) {
         const int d = E.type - 3;
         for (int bB = 0; bB < 2; ++bB)
@@ -279,14 +283,14 @@ __global__ void k_gather_resid(LevelGeom g, const double* __restrict__ Y, const 
             else if (d == 1) { a1 += bA - 1; a3 += bB - 1; }
             else { a1 += bA - 1; a2 += bB - 1; }
             int qe = 4 * d + (1 - bA) + 2 * (1 - bB);
-            s += Y[el(a1, a2, a3) + 6 * mm + qe * m + E.a];
+            s += yat(a1, a2, a3, 6 * mm + qe * m + E.a);
           }
       } else {
         for (int c3 = 0; c3 < 2; ++c3)
           for (int c2 = 0; c2 < 2; ++c2)
             for (int c1 = 0; c1 < 2; ++c1) {
               int qv = (1 - c1) + 2 * (1 - c2) + 4 * (1 - c3);
-              s += Y[el(E.v1 - 1 + c1, E.v2 - 1 + c2, E.v3 - 1 + c3) + 6 * mm + 12 * m + qv];
+              s += yat(E.v1 - 1 + c1, E.v2 - 1 + c2, E.v3 - 1 + c3, 6 * mm + 12 * m + qv);
             }
       }
       r = F ? F[idx] - s : s;
@@ -312,7 +316,7 @@ __global__ void __launch_bounds__(256) k_star(LevelGeom g, int c1, int c2, int c
   const int p = g.p, n = g.n, c = p - 1, nn = n * n, ST = g.ST;
   const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
   const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
-  if ((v1 == 0 || v1 == g.k1) && (v2 == 0 || v2 == g.k2) && (v3 + g.zoff == 0 || v3 + g.zoff == g.K3)) return;  // corner
+  if (star_empty(g, v1, v2, v3)) return;  // corner
   if (v3 < g.own_lo) return;   // ghost star below the slab: computed by the lower rank
   const int tid = threadIdx.x, nt = blockDim.x;
   const double* gt[3] = {stab + (size_t)v1 * ST, stab + (size_t)(g.V1 + v2) * ST, stab + (size_t)(g.V1 + g.V2 + v3) * ST};
@@ -725,9 +729,11 @@ __global__ void k_condense_gather(LevelGeom g, const double* __restrict__ Fg, co
         const int d = E.type, o = E.a * m + E.b;
         int w1 = E.v1, w2 = E.v2, w3 = E.v3;
         if (d == 0) w1 -= 1; else if (d == 1) w2 -= 1; else w3 -= 1;
-        size_t elo = (size_t)w1 + (size_t)g.k1 * ((size_t)w2 + (size_t)g.k2 * w3);
-        size_t ehi = (size_t)E.v1 + (size_t)g.k1 * ((size_t)E.v2 + (size_t)g.k2 * E.v3);
-        r -= Yc[elo * 6 * mm + (2 * d + 1) * mm + o] + Yc[ehi * 6 * mm + (2 * d) * mm + o];
+        const bool lo_in = w1 >= 0 && w2 >= 0 && w3 >= 0;                               // Neumann face: one side
+        const bool hi_in = E.v1 < g.k1 && E.v2 < g.k2 && E.v3 < g.k3;
+        size_t elo = lo_in ? (size_t)w1 + (size_t)g.k1 * ((size_t)w2 + (size_t)g.k2 * w3) : 0;
+        size_t ehi = hi_in ? (size_t)E.v1 + (size_t)g.k1 * ((size_t)E.v2 + (size_t)g.k2 * E.v3) : 0;
+        r -= (lo_in ? Yc[elo * 6 * mm + (2 * d + 1) * mm + o] : 0.0) + (hi_in ? Yc[ehi * 6 * mm + (2 * d) * mm + o] : 0.0);
       }
     }
     fhat[idx] = r;

@@ -54,9 +54,19 @@ __device__ __forceinline__ bool inside(const LevelGeom& g, int g1, int g2, int g
   return g1 >= 0 && g2 >= 0 && g3 >= 0 && g1 <= g.k1 * g.p && g2 <= g.k2 * g.p && g3 <= g.k3 * g.p;
 }
 // free unknown: strictly inside the GLOBAL box (g3 is local; the slab starts at vertex plane zoff)
+// Neumann faces (g.neu) keep their points as unknowns
 __device__ __forceinline__ bool is_free(const LevelGeom& g, int g1, int g2, int g3) {
   const int G3 = g3 + g.zoff * g.p;
-  return g1 > 0 && g2 > 0 && G3 > 0 && g1 < g.k1 * g.p && g2 < g.k2 * g.p && G3 < g.K3 * g.p;
+  return free_1d(g1, g.k1 * g.p, g.neu & 1, (g.neu >> 1) & 1) && free_1d(g2, g.k2 * g.p, (g.neu >> 2) & 1, (g.neu >> 3) & 1) &&
+         free_1d(G3, g.K3 * g.p, (g.neu >> 4) & 1, (g.neu >> 5) & 1);
+}
+// a box-corner star has no unknown iff the three faces meeting at the corner are Dirichlet
+__device__ __forceinline__ bool star_empty(const LevelGeom& g, int v1, int v2, int v3) {
+  const int V3 = v3 + g.zoff;
+  const bool c1 = v1 == 0 || v1 == g.k1, c2 = v2 == 0 || v2 == g.k2, c3 = V3 == 0 || V3 == g.K3;
+  if (!(c1 && c2 && c3)) return false;
+  const int f1 = v1 == 0 ? 0 : 1, f2 = v2 == 0 ? 2 : 3, f3 = V3 == 0 ? 4 : 5;
+  return !((g.neu >> f1) & 1) && !((g.neu >> f2) & 1) && !((g.neu >> f3) & 1);
 }
 // record plane v3 (local) carries element-gathered values on this rank
 __device__ __forceinline__ bool owned_plane(const LevelGeom& g, int v3) { return v3 >= g.own_lo && v3 < g.own_hi; }

@@ -666,6 +666,7 @@ void pmg_default_options(pmg_options* o) {
   o->weight_degree = 7;
   o->schedule = 0;
   o->solver = 0;
+  o->neumann = 0;
   o->coarse_rtol = 1e-8;
   o->coarse_maxit = 10000;
   o->coarse_check = 8;
@@ -698,6 +699,8 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   if (o.weight_degree != 7) return fail(PMG_EINVAL, "only weight_degree = 7 is implemented (P:316)");
   if (o.schedule != 0 && o.schedule != 1) return fail(PMG_EINVAL, "schedule must be 0 or 1");
   if (o.solver != 0 && o.solver != 1) return fail(PMG_EINVAL, "solver must be 0 (MG) or 1 (ipCG)");
+  if (o.neumann < 0 || o.neumann > 63) return fail(PMG_EINVAL, "neumann is a 6-bit face mask");
+  if (o.neumann == 63 && lambda == 0.0) return fail(PMG_EINVAL, "all-Neumann Poisson (lambda = 0) is singular");
   if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return fail(PMG_EINVAL, "need 0 <= rank < nranks");
   if (o.nranks > 1 && n_e[2] < o.nranks) return fail(PMG_EINVAL, "z-slabs: k3 >= nranks required");
   if (o.nranks > 1 && o.p0 != 2) return fail(PMG_EINVAL, "z-slabs: the replicated coarse CG needs p0 = 2");
@@ -723,7 +726,7 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   c->H.resize(L + 1);
   c->D.resize(L + 1);
   for (int l = 0; l <= L; ++l) {
-    std::string err = build_level(c->H[l], deg[l], n_e, widths, lambda, o.weight_degree);
+    std::string err = build_level(c->H[l], deg[l], n_e, widths, lambda, o.weight_degree, o.neumann);
     if (!err.empty()) { free_ctx(c); return fail(PMG_EINVAL, err); }
     if (l >= 1) build_interp(c->H[l], deg[l - 1]);
   }

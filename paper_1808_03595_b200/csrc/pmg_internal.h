@@ -31,7 +31,15 @@ struct LevelGeom {
   // [own_lo, own_hi); the other (ghost) planes are filled by the halo exchange.
   // One GPU: zoff = 0, K3 = k3, own_lo = 0, own_hi = V3.
   int zoff, K3, own_lo, own_hi;
+  // homogeneous Neumann faces (NEXT-3): bit 2d / 2d+1 = low / high face of direction d;
+  // every other face is homogeneous Dirichlet
+  int neu;
 };
+
+// is global 1-D index G (0 <= G <= n_el p) an unknown along a direction with the given end flags?
+PMG_HD inline bool free_1d(int G, int n_el_p, bool neu_lo, bool neu_hi) {
+  return G >= 0 && G <= n_el_p && (G > 0 || neu_lo) && (G < n_el_p || neu_hi);
+}
 
 // Element table, per direction d and 1-D element e_d (width h), m = p - 1, q = p + 1:
 //   [0, m)            Lambda_d  (interior generalised eigenvalues, S^T K_II S = Lambda)
@@ -69,7 +77,7 @@ struct HostLevel {
 
 // Host setup; returns an empty string on success, else an error message.
 std::string build_level(HostLevel& L, int p, const int k[3], const double* const widths[3],
-                        double lambda, int weight_degree);
+                        double lambda, int weight_degree, int neumann = 0);
 std::string build_interp(HostLevel& fine, int p_coarse);
 // diag(H_hat) for the given level in skeleton record layout (free entries only, others 0).
 std::string coarse_diag(const HostLevel& L, double lambda, std::vector<double>& diag);

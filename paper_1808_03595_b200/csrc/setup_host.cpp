@@ -143,7 +143,7 @@ static double weight7(double t) {
 }
 
 std::string build_level(HostLevel& L, int p, const int k[3], const double* const widths[3],
-                        double lambda, int weight_degree) {
+                        double lambda, int weight_degree, int neumann) {
   (void)lambda;
   if (weight_degree != 7) return "only weight_degree = 7 is implemented (P:316)";
   if (p < 2 || p > 32) return "degree p must be in [2, 32]";
@@ -161,6 +161,7 @@ std::string build_level(HostLevel& L, int p, const int k[3], const double* const
   g.nskel = g.nrec * g.RS;
   g.nelem = (long long)k[0] * k[1] * k[2];
   g.zoff = 0; g.K3 = k[2]; g.own_lo = 0; g.own_hi = g.V3;
+  g.neu = neumann;
 
   std::vector<double> xi, wq;
   gll(p, xi, wq);
@@ -231,8 +232,8 @@ std::string build_level(HostLevel& L, int p, const int k[3], const double* const
       }
       std::vector<int> cpl;
       for (int j = 0; j < n; ++j) {
-        long long gg = (long long)(v - 1) * p + 1 + j;
-        if (gg > 0 && gg < (long long)k[d] * p) cpl.push_back(j);
+        long long gg = (long long)(v - 1) * p + 1 + j;   // unknowns of the star line (Dirichlet ends padded)
+        if (free_1d((int)gg, k[d] * p, (neumann >> (2 * d)) & 1, (neumann >> (2 * d + 1)) & 1)) cpl.push_back(j);
       }
       int nc = (int)cpl.size();
       std::vector<double> S(n * n, 0.0), lamv(n, 1.0);
@@ -396,7 +397,9 @@ std::string coarse_diag(const HostLevel& L, double lambda, std::vector<double>& 
                 v -= Ma * Ma * Mb * Mb * sum;
               }
               int g1 = e1 * p + t1, g2 = e2 * p + t2, g3 = e3 * p + t3;
-              bool fr = g1 > 0 && g1 < g.k1 * p && g2 > 0 && g2 < g.k2 * p && g3 > 0 && g3 < g.k3 * p;
+              bool fr = free_1d(g1, g.k1 * p, g.neu & 1, (g.neu >> 1) & 1) &&
+                        free_1d(g2, g.k2 * p, (g.neu >> 2) & 1, (g.neu >> 3) & 1) &&
+                        free_1d(g3, g.k3 * p, (g.neu >> 4) & 1, (g.neu >> 5) & 1);
               if (fr) diag[host_skel_index(g, g1, g2, g3)] += v;
             }
       }

@@ -239,3 +239,34 @@ def test_nccl_transport_single_rank(name, solver):
     assert rep["cycles"] == rep1["cycles"] == rep2["cycles"]
     assert torch.equal(u, u1)
     s.close()
+
+
+@pytest.mark.parametrize("nr", [2, 3])
+def test_neumann_z_faces_multirank(nr):
+    """Neumann faces across the slab boundary logic: the bottom / top z faces belong to the first /
+    last rank (global plane test), x faces to every rank."""
+    cfg = CASES["k325_p4_lam1.7_stretched"]
+    case = pi.small_case(cfg["k"], cfg["p"], cfg["lam"], stretch=cfg["stretch"])
+    s1 = one_gpu(case, neumann=0b110011)
+    f_np, F_np = global_F(case, s1)
+    u1 = s1.new_grid()
+    rep1 = s1.solve(torch.from_numpy(F_np).cuda(), u1, 1e-10)
+    u1 = u1.cpu().numpy()
+    pl = (case.k[0] * case.p + 1) * (case.k[1] * case.p + 1)
+    s1.close()
+
+    def fn(s, r):
+        sl = s.slab
+        lo, hi = sl["z0"] * case.p * pl, (sl["z1"] * case.p + 1) * pl
+        F_loc = s.new_grid()
+        s.weak_rhs(torch.from_numpy(f_np[lo:hi].copy()).cuda(), F_loc)
+        u = s.new_grid()
+        rep = s.solve(F_loc, u, 1e-10)
+        torch.cuda.current_stream().synchronize()
+        return sl, F_loc.cpu().numpy(), u.cpu().numpy(), rep
+
+    for sl, F_loc, u, rep in run_ranks(nr, case, fn, neumann=0b110011):
+        lo, hi = sl["z0"] * case.p * pl, (sl["z1"] * case.p + 1) * pl
+        assert np.array_equal(F_loc, F_np[lo:hi])
+        assert rep["cycles"] == rep1["cycles"]
+        assert np.abs(u - u1[lo:hi]).max() <= 1e-12 * np.abs(u1).max()

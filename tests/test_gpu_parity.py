@@ -31,13 +31,15 @@ def rel(a, b):
 class Pair:
     """Oracle hierarchy + GPU solver for the same problem."""
 
-    def __init__(self, k, p, lam, stretch, coarse_rtol=1e-13, schedule=0):
+    def __init__(self, k, p, lam, stretch, coarse_rtol=1e-13, schedule=0, neumann=0):
         from oracle import mg
         import paper_1808_03595_b200 as pmg
         case = pi.small_case(k, p, lam, stretch=stretch)
         self.case = case
-        self.orc = mg.Hierarchy(case.k, case.widths, p, lam, coarse_rtol=coarse_rtol, schedule=schedule)
-        self.gpu = pmg.Solver(case.k, case.widths, p, lam, coarse_rtol=coarse_rtol, schedule=schedule)
+        self.orc = mg.Hierarchy(case.k, case.widths, p, lam, coarse_rtol=coarse_rtol, schedule=schedule,
+                                neumann=neumann)
+        self.gpu = pmg.Solver(case.k, case.widths, p, lam, coarse_rtol=coarse_rtol, schedule=schedule,
+                              neumann=neumann)
         assert self.gpu.nlevels == len(self.orc.levels)
         self.rng = np.random.default_rng(11)
 
@@ -445,3 +447,96 @@ def test_high_degree_star_kernels_agree(k, p, monkeypatch):
         outs.append(u.cpu().numpy())
         s.close()
     assert rel(outs[0], outs[1]) < 1e-12
+
+
+
+NEUMANN_CASES = {
+    "k323_p4_neu_x": dict(k=(3, 2, 3), p=4, lam=1.7, stretch=1.6, neumann=0b000011),
+    "k232_p5_neu_mixed": dict(k=(2, 3, 2), p=5, lam=0.0, stretch=None, neumann=0b100110),
+    "k333_p8_neu_all": dict(k=(3, 3, 3), p=8, lam=0.9, stretch=None, neumann=0b111111),
+    "k332_p2_neu_z": dict(k=(3, 3, 2), p=2, lam=0.0, stretch=None, neumann=0b110000),
+}
+_NPAIRS = {}
+
+
+def npair(name):
+    if name not in _NPAIRS:
+        _NPAIRS[name] = Pair(**NEUMANN_CASES[name])
+    return _NPAIRS[name]
+
+
+@pytest.mark.parametrize("name", list(NEUMANN_CASES))
+def test_neumann_operators_parity(name):
+    """Homogeneous Neumann faces (NEXT-3): residual, smoother, restriction,
+    prolongation and V-cycle against the oracle on the same inputs, per-operator tolerance."""
+    P = npair(name)
+    L = P.gpu.nlevels - 1
+    for l in range(L + 1):
+        orc = P.orc.levels[l]
+        u = P.rand_skel(l)
+        f = P.rand_skel(l)
+        r = P.gpu.new_skel(l)
+        P.gpu.residual(l, P.to_skel(l, u), P.to_skel(l, f), r)
+        assert rel(P.to_grid(l, r), orc.op.residual(u, f)) < OP_TOL
+        du = P.gpu.new_skel(l)
+        P.gpu.smooth(l, P.to_skel(l, f), du)
+        assert rel(P.to_grid(l, du), orc.smoother.apply(f)) < OP_TOL
+        if l >= 1:
+            T = P.orc.transfers[l]
+            fc = P.gpu.new_skel(l - 1)
+            P.gpu.restrict(l, P.to_skel(l, f), fc)
+            assert rel(P.to_grid(l - 1, fc), T.restrict(f)) < OP_TOL
+            uc = P.rand_skel(l - 1)
+            uf = P.gpu.new_skel(l)
+            P.gpu.prolong(l, P.to_skel(l - 1, uc), uf)
+            assert rel(P.to_grid(l, uf), T.prolong(uc)) < OP_TOL
+    f = P.rand_skel(L)
+    u = P.gpu.new_skel(L)
+    P.gpu.vcycle(u, P.to_skel(L, f))
+    assert rel(P.to_grid(L, u), P.orc.vcycle(np.zeros_like(f), f)) < OP_TOL
+
+
+@pytest.mark.parametrize("name", list(NEUMANN_CASES))
+def test_neumann_solve_parity(name):
+    from oracle import condensed
+    P = npair(name)
+    L = P.gpu.nlevels - 1
+    m = P.mesh(L)
+    F = condensed.weak_rhs(m, pi.uniform_pm1(5, np.arange(m.ntot)))
+    u_orc, rep_o = P.orc.solve(F, 1e-10)
+    ug = P.gpu.new_grid()
+    rep = P.gpu.solve(torch.from_numpy(F).cuda(), ug, 1e-10)
+    torch.cuda.synchronize()
+    assert rep["converged"] and rep["cycles"] == rep_o["cycles"], (rep["cycles"], rep_o["cycles"])
+    assert rel(ug.cpu().numpy(), u_orc) < SOLVE_TOL
+
+
+@pytest.mark.parametrize("neu,kind", [(0b111111, "cos"), (0b111100, "sin")])
+def test_neumann_manufactured_on_gpu(neu, kind):
+    """lambda = 1 on (0, pi)^3, 4^3 elements, p = 8: u = cos x cos y cos z (all faces Neumann) or
+    sin x cos y cos z (Dirichlet x faces); f = 4 u; the GPU solve reproduces u to spectral accuracy."""
+    import math
+    import paper_1808_03595_b200 as pmg
+    k = (4, 4, 4)
+    s = pmg.Solver(k, pi.uniform_widths(k, (math.pi,) * 3), 8, 1.0, neumann=neu)
+    L = s.nlevels - 1
+    x = [s.grid_coords(L, d) for d in range(3)]
+    X3, X2, X1 = np.meshgrid(x[2], x[1], x[0], indexing="ij")
+    ue = ((np.cos(X1) if kind == "cos" else np.sin(X1)) * np.cos(X2) * np.cos(X3)).ravel()
+    F = s.new_grid()
+    s.weak_rhs(torch.from_numpy(4.0 * ue).cuda(), F)
+    u = s.new_grid()
+    rep = s.solve(F, u, 1e-12)
+    torch.cuda.synchronize()
+    assert rep["converged"]
+    assert np.abs(u.cpu().numpy() - ue).max() < 1e-6
+    s.close()
+
+
+def test_neumann_invalid_options():
+    import paper_1808_03595_b200 as pmg
+    case = pi.small_case((2, 2, 2), 4, 0.0)
+    with pytest.raises(pmg.PmgError):
+        pmg.Solver(case.k, case.widths, 4, 0.0, neumann=63)      # singular all-Neumann Poisson
+    with pytest.raises(pmg.PmgError):
+        pmg.Solver(case.k, case.widths, 4, 1.0, neumann=64)
