@@ -96,8 +96,10 @@ struct pmg_ctx {
   double* cgm = nullptr;     // its double-buffered m vector (2 n0)
   bool coop_ell = false;     // large coarse systems: pipelined grid-stride CG over ELL rows
   int ell_nb = 0;
-  int* ellc = nullptr;       // 25 n0 column indices (column-major ELL)
-  double* ella = nullptr;    // 25 n0 coefficients
+  int* ellc = nullptr;       // 25 n0 column indices (column-major ELL), inside the ella block
+  double* ella = nullptr;    // 25 n0 coefficients, then the indices (one block: one L2 window)
+  cudaAccessPolicyWindow ell_win{};   // L2 persistence of the ELL rows (when the device allows it)
+  bool ell_persist = false;
   double* ellv = nullptr;    // 8 n0 CG vectors
   double* ctab[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // CoarseTabs storage
   double* cV = nullptr;      // (unused)
@@ -292,11 +294,13 @@ pmg_status pcg_dev(pmg_ctx* c, const double* b, double* x) {
       cfg.gridDim = dim3(c->ell_nb);
       cfg.blockDim = dim3(kThreads);
       cfg.stream = c->st;
-      cudaLaunchAttribute attr[1];
+      cudaLaunchAttribute attr[2];
       attr[0].id = cudaLaunchAttributeCooperative;
       attr[0].val.cooperative = 1;
+      attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+      attr[1].val.accessPolicyWindow = c->ell_win;
       cfg.attrs = attr;
-      cfg.numAttrs = 1;
+      cfg.numAttrs = c->ell_persist ? 2 : 1;
       CUDA_CHECK(cudaLaunchKernelExC(&cfg, (const void*)k_pcg_gv_ell_p2, args_ell));
       c->launches++;
       return PMG_OK;
@@ -620,7 +624,7 @@ void free_ctx(pmg_ctx* c) {
     cudaFree(D.etab); cudaFree(D.stab); cudaFree(D.Jint); cudaFree(D.u); cudaFree(D.f); cudaFree(D.r);
   }
   cudaFree(c->Y); cudaFree(c->Z); cudaFree(c->cube); cudaFree(c->part); cudaFree(c->dres); cudaFree(c->pcg);
-  cudaFree(c->cgm); cudaFree(c->ellc); cudaFree(c->ella); cudaFree(c->ellv);
+  cudaFree(c->cgm); cudaFree(c->ella); cudaFree(c->ellv);
   cudaFree(c->cx); cudaFree(c->cr); cudaFree(c->cz); cudaFree(c->cp); cudaFree(c->cq); cudaFree(c->dinv);
   for (int d = 0; d < 3; ++d) cudaFree(c->bm[d]);
   cudaFree(c->Fdev); cudaFree(c->Udev);
@@ -905,8 +909,29 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
         const char* le = std::getenv("PMG_COARSE_ELL");
         if (!c->coop_gv && !(le && le[0] == '0') && per_sm_ell > 0) {
           const long long n0e = c->g0g.nskel;
-          if (dalloc(&c->ellc, 25 * n0e) == cudaSuccess && dalloc(&c->ella, 25 * n0e) == cudaSuccess &&
+          if (dalloc(&c->ella, 25 * n0e + (25 * n0e + 1) / 2) == cudaSuccess &&
               dalloc(&c->ellv, 8 * n0e) == cudaSuccess && (c->cgm || dalloc(&c->cgm, 2 * n0e) == cudaSuccess)) {
+            c->ellc = reinterpret_cast<int*>(c->ella + 25 * n0e);
+            // the rows are re-read every iteration: ask L2 to keep them (set-aside persisting lines)
+            int maxp = 0, maxwin = 0;
+            cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+            cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+            const char* np_ = std::getenv("PMG_NO_L2PERSIST");
+            const size_t rows = sizeof(double) * (size_t)(25 * n0e + (25 * n0e + 1) / 2);
+            if (maxp > 0 && maxwin > 0 && !(np_ && np_[0] == '1')) {
+              size_t cur = 0;
+              cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+              const size_t want = std::min<size_t>((size_t)maxp, rows);
+              if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+              cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+              c->ell_win.base_ptr = c->ella;
+              c->ell_win.num_bytes = std::min<size_t>(rows, (size_t)maxwin);
+              c->ell_win.hitRatio = (float)std::min(1.0, (double)cur / (double)c->ell_win.num_bytes);
+              c->ell_win.hitProp = cudaAccessPropertyPersisting;
+              c->ell_win.missProp = cudaAccessPropertyStreaming;
+              c->ell_persist = cur > 0;
+            }
+            cudaGetLastError();
             CoarseTabs ct{c->ctab[0], c->ctab[1], c->ctab[2], c->ctab[3], c->ctab[4], c->ctab[5], c->ctab[6]};
             k_build_coarse_ell<<<grid_for(n0e), kThreads>>>(c->g0g, ct, lambda, c->ellc, c->ella);
             if (cudaGetLastError() == cudaSuccess) {

