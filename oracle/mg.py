@@ -68,14 +68,23 @@ def pcg(level, b, rtol, maxit):
 
 class Hierarchy:
     def __init__(self, k, widths, p, lam, p0=2, pw=7, schedule=0, coarse_rtol=1e-8,
-                 coarse_maxit=10000, neumann=0):
-        """neumann: face bitmask of homogeneous Neumann faces (Mesh; NEXT-3)."""
+                 coarse_maxit=10000, neumann=0, coarse_solver="auto"):
+        """neumann: face bitmask of homogeneous Neumann faces (Mesh; NEXT-3).
+        coarse_solver: "jacobi" (Jacobi-PCG, reading R11), "hmg" (CG preconditioned by the
+        h-multigrid V-cycle of oracle/hmg.py, reading R16) or "auto" (hmg iff more than 16^3
+        elements and every k_d coarsenable -- the rule the GPU library uses)."""
         self.degrees = level_degrees(p, p0)
         self.L = len(self.degrees) - 1
         self.levels = [Level(k, widths, q, lam, pw, neumann) for q in self.degrees]
         self.transfers = [None] + [Transfer(self.levels[l - 1].mesh, self.levels[l].mesh)
                                    for l in range(1, self.L + 1)]
         self.schedule = schedule
+        from . import hmg as _hmg
+        if coarse_solver == "auto":
+            ne = int(np.prod(k))
+            coarse_solver = "hmg" if (p0 == 2 and ne > 4096 and _hmg.coarsenable(k)) else "jacobi"
+        self.coarse_solver = coarse_solver
+        self.hmg = _hmg.HMultigrid(k, widths, lam, neumann) if coarse_solver == "hmg" else None
         self.coarse_rtol = coarse_rtol
         self.coarse_maxit = coarse_maxit
         self.coarse_its = []
@@ -89,6 +98,11 @@ class Hierarchy:
         return u + lv.smoother.apply(lv.op.residual(u, f))
 
     def coarse_solve(self, f0):
+        if self.hmg is not None:
+            from .hmg import pcg_hmg
+            x, its = pcg_hmg(self.levels[0], self.hmg, f0, self.coarse_rtol, self.coarse_maxit)
+            self.coarse_its.append(its)
+            return x
         x, its = pcg(self.levels[0], f0, self.coarse_rtol, self.coarse_maxit)
         self.coarse_its.append(its)
         return x
