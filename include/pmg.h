@@ -69,6 +69,11 @@ typedef struct {
   double coarse_rtol; /* coarse CG relative tolerance, default 1e-8 (reading R11) */
   int coarse_maxit;   /* coarse CG iteration cap, default 10000 */
   int coarse_check;   /* coarse CG: host convergence poll every this many iterations, default 8 */
+  int coarse_solver;  /* preconditioner of the coarse CG: 1 = Jacobi (reading R11), 2 = h-multigrid
+                         V-cycle over element-merged p0 = 2 levels (NEXT-2, reading R16),
+                         0 = automatic: h-multigrid iff more than 12288 elements, some k_d even with
+                         k_d / 2 >= 2, and lambda L_min^2 < 100 (L_min the shortest box edge: a
+                         mass-dominated coarse system converges fast under Jacobi) (default) */
   int rank, nranks;   /* z-slab decomposition over nranks processes / GPUs:
                          rank r owns element layers [z0_r, z1_r) (pmg_slab_plan); nranks = 1: one GPU */
   const void* nccl_id;/* nranks > 1 with NCCL: 128-byte ncclUniqueId from pmg_nccl_unique_id on rank 0,

@@ -5,8 +5,10 @@ used in the paper; "alpha = 1 can be attained by reverting to an appropriate low
 solver".  Reading R16: the coarse level keeps its conjugate-gradient iteration
 and gains a symmetric h-multigrid V-cycle as preconditioner:
 
-  - h-levels: the p = 2 condensed system on k, k/2, k/4, ... elements per direction (pairs of
-    elements merged, widths summed) while every k_d is even and k_d / 2 >= 2;
+  - h-levels: the p = 2 condensed system on element-merged meshes: a direction is halved (pairs
+    of elements merged, widths summed) while its k_d is even with k_d / 2 >= 2 (directions that
+    cannot be halved keep their elements: semi-coarsening); levels continue while any direction
+    halves;
   - transfer: P = fine free skeleton <- coarse free skeleton, the coarse element's quadratic
     (tensor GLL Lagrange basis on {-1, 0, 1}) evaluated at the fine nodes, with the coarse
     element's interior (centre) value given by its harmonic extension
@@ -14,7 +16,8 @@ and gains a symmetric h-multigrid V-cycle as preconditioner:
     restriction R = P^T;
   - smoother: nu damped Jacobi sweeps x <- x + omega D^-1 (f - A x), omega = 0.6, before and after
     the coarse correction (symmetric V-cycle);
-  - coarsest h-level: COARSEST_SWEEPS damped Jacobi sweeps from zero (a fixed symmetric operator).
+  - coarsest h-level (at most DENSE_MAX free unknowns): solved exactly (dense); larger coarsest
+    levels: COARSEST_SWEEPS damped Jacobi sweeps from zero (a fixed symmetric operator).
 
 Plain NumPy/SciPy, every step written out; test infrastructure only.
 """
@@ -28,10 +31,29 @@ from .mesh import Mesh
 OMEGA = 0.6
 NU = 2
 COARSEST_SWEEPS = 40
+DENSE_MAX = 1500
+
+
+def halvable(kd):
+    return kd % 2 == 0 and kd // 2 >= 2
 
 
 def coarsenable(k):
-    return all(kd % 2 == 0 and kd // 2 >= 2 for kd in k)
+    return any(halvable(kd) for kd in k)
+
+
+def coarsen(k, widths):
+    """(k_c, widths_c): every halvable direction merged pairwise, the others unchanged."""
+    kc, wc = [], []
+    for kd, w in zip(k, widths):
+        w = np.asarray(w)
+        if halvable(kd):
+            kc.append(kd // 2)
+            wc.append(w[0::2] + w[1::2])
+        else:
+            kc.append(kd)
+            wc.append(w.copy())
+    return tuple(kc), wc
 
 
 def merged_widths(widths):
@@ -56,7 +78,8 @@ def h_prolongation(mesh_c, mesh_f, lam):
     N1, N2 = mesh_f.N[0], mesh_f.N[1]
     for gf in fs:
         G = (gf % N1, (gf // N1) % N2, gf // (N1 * N2))
-        ec = [min(G[d] // 4, mesh_c.k[d] - 1) for d in range(3)]
+        ratio = [mesh_f.k[d] // mesh_c.k[d] for d in range(3)]          # 2 (merged) or 1 (kept)
+        ec = [min(G[d] // (2 * ratio[d]), mesh_c.k[d] - 1) for d in range(3)]
         w = np.ones(27)
         for d in range(3):
             xa = mesh_c.coords[d][ec[d] * p]
@@ -94,7 +117,8 @@ class HMultigrid:
         self.levels = [HLevel(k, widths, lam, neumann)]
         while coarsenable(self.levels[-1].mesh.k):
             m = self.levels[-1].mesh
-            self.levels.append(HLevel(tuple(kd // 2 for kd in m.k), merged_widths(m.widths), lam, neumann))
+            kc, wc = coarsen(m.k, m.widths)
+            self.levels.append(HLevel(kc, wc, lam, neumann))
         self.P = [h_prolongation(self.levels[l + 1].mesh, self.levels[l].mesh, lam)
                   for l in range(len(self.levels) - 1)]
         self.R = [P.T.tocsr() for P in self.P]
@@ -109,6 +133,11 @@ class HMultigrid:
         lv = self.levels[l]
         x = np.zeros(lv.mesh.ntot)
         if l == len(self.levels) - 1:
+            fs = np.nonzero(lv.mesh.free_skel)[0]
+            if len(fs) <= DENSE_MAX:
+                A = lv.op.assembled_condensed()[fs][:, fs].toarray()
+                x[fs] = np.linalg.solve(A, np.asarray(f)[fs])
+                return x
             return self.smooth(l, x, f, COARSEST_SWEEPS)
         x = self.smooth(l, x, f, NU)
         r = (f - lv.op.apply(x)) * lv.mesh.free_skel

@@ -71,8 +71,8 @@ class Hierarchy:
                  coarse_maxit=10000, neumann=0, coarse_solver="auto"):
         """neumann: face bitmask of homogeneous Neumann faces (Mesh; NEXT-3).
         coarse_solver: "jacobi" (Jacobi-PCG, reading R11), "hmg" (CG preconditioned by the
-        h-multigrid V-cycle of oracle/hmg.py, reading R16) or "auto" (hmg iff more than 16^3
-        elements and every k_d coarsenable -- the rule the GPU library uses)."""
+        h-multigrid V-cycle of oracle/hmg.py, reading R16) or "auto" (hmg iff more than 12288
+        elements, some k_d halvable and lambda L_min^2 < 100 -- the rule the GPU library uses)."""
         self.degrees = level_degrees(p, p0)
         self.L = len(self.degrees) - 1
         self.levels = [Level(k, widths, q, lam, pw, neumann) for q in self.degrees]
@@ -82,7 +82,9 @@ class Hierarchy:
         from . import hmg as _hmg
         if coarse_solver == "auto":
             ne = int(np.prod(k))
-            coarse_solver = "hmg" if (p0 == 2 and ne > 4096 and _hmg.coarsenable(k)) else "jacobi"
+            lmin = min(float(np.sum(w)) for w in widths)
+            coarse_solver = ("hmg" if (p0 == 2 and ne > 12288 and _hmg.coarsenable(k) and lam * lmin * lmin < 100.0)
+                             else "jacobi")
         self.coarse_solver = coarse_solver
         self.hmg = _hmg.HMultigrid(k, widths, lam, neumann) if coarse_solver == "hmg" else None
         self.coarse_rtol = coarse_rtol

@@ -34,7 +34,8 @@ class Options(ctypes.Structure):
     _fields_ = [("p0", ctypes.c_int), ("weight_degree", ctypes.c_int), ("schedule", ctypes.c_int),
                 ("neumann", ctypes.c_int), ("solver", ctypes.c_int),
                 ("coarse_rtol", ctypes.c_double), ("coarse_maxit", ctypes.c_int),
-                ("coarse_check", ctypes.c_int), ("rank", ctypes.c_int), ("nranks", ctypes.c_int),
+                ("coarse_check", ctypes.c_int), ("coarse_solver", ctypes.c_int),
+                ("rank", ctypes.c_int), ("nranks", ctypes.c_int),
                 ("nccl_id", ctypes.c_void_p), ("loopback", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
 
 
@@ -154,7 +155,7 @@ class Solver:
 
     def __init__(self, k, widths, p, lam, p0=2, schedule=0, coarse_rtol=1e-8, coarse_maxit=10000,
                  coarse_check=8, stream=None, rank=0, nranks=1, nccl_id=None, loopback=None, solver=0,
-                 neumann=0):
+                 neumann=0, coarse_solver=0):
         """solver 0: MG fixpoint iteration (Alg. 4); 1: Krylov-accelerated MG (ipCG, Alg. 5).
         neumann: face bitmask of homogeneous Neumann faces (bit 2d / 2d+1: low / high face of d)."""
         import numpy as np
@@ -164,6 +165,7 @@ class Solver:
         o.rank, o.nranks = int(rank), int(nranks)
         o.solver = int(solver)
         o.neumann = int(neumann)
+        o.coarse_solver = int(coarse_solver)
         self._nccl_buf = None
         if nccl_id is not None:
             self._nccl_buf = ctypes.create_string_buffer(bytes(nccl_id), 128)

@@ -588,6 +588,191 @@ __global__ void __launch_bounds__(256) k_pcg_gv_ell_p2(long long n, const double
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// CG on the coarse system with the h-multigrid V-cycle as preconditioner (reading R16,
+// oracle/hmg.py): one cooperative launch; every step of the V-cycle is a grid-stride loop over the
+// level's unknowns followed by a grid barrier; the coarsest level (a few hundred unknowns) is
+// smoothed by block 0 alone with block barriers.  Damped Jacobi (omega = 0.6), two sweeps before and
+// after the coarse correction, 40 sweeps on the coarsest level -- the oracle's constants.
+// ------------------------------------------------------------------------------------------
+namespace {
+constexpr double kHmgOmega = 0.6;
+constexpr int kHmgNu = 2, kHmgCoarsest = 40;
+
+__device__ __forceinline__ double ell_row(const double* __restrict__ val, const int* __restrict__ col, long long n,
+                                          long long i, const double* __restrict__ v) {
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < kRowLen; ++k) s = fma(__ldg(&val[k * n + i]), __ldcg(&v[__ldg(&col[k * n + i])]), s);
+  return s;
+}
+
+// one CSR row reduced by a whole warp: lane j takes entries j, j + 32, ... in order, then a fixed
+// xor tree (deterministic); every lane returns the row value.  The transfer rows are up to ~125
+// long (restriction), too long for one thread's dependent load chain.
+__device__ __forceinline__ double csr_row_warp(const int* __restrict__ ptr, const int* __restrict__ col,
+                                               const double* __restrict__ val, long long i,
+                                               const double* __restrict__ v, int lane) {
+  double s = 0.0;
+  const int k1 = __ldg(&ptr[i + 1]);
+  for (int k = __ldg(&ptr[i]) + lane; k < k1; k += 32) s = fma(__ldg(&val[k]), __ldcg(&v[__ldg(&col[k])]), s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
+// z = V-cycle(f_0) into h.x[0]; h.f[0] holds the right-hand side
+__device__ void hmg_vcycle(const HmgDev& h, cg::grid_group& grid, long long t0, long long T) {
+  const int L = h.nlev - 1;
+  for (int l = 0; l < L; ++l) {
+    const long long n = h.n[l];
+    double *x = h.x[l], *r = h.r[l];
+    const double *f = h.f[l], *di = h.dinv[l];
+    for (long long i = t0; i < n; i += T) x[i] = kHmgOmega * di[i] * f[i];          // first sweep from zero
+    grid.sync();
+    for (int s = 1; s < kHmgNu; ++s) {
+      for (long long i = t0; i < n; i += T) r[i] = f[i] - ell_row(h.Aval[l], h.Acol[l], n, i, x);
+      grid.sync();
+      for (long long i = t0; i < n; i += T) x[i] = fma(kHmgOmega * di[i], r[i], x[i]);
+      grid.sync();
+    }
+    for (long long i = t0; i < n; i += T) r[i] = f[i] - ell_row(h.Aval[l], h.Acol[l], n, i, x);
+    grid.sync();
+    const long long nc = h.n[l + 1];
+    for (long long i = t0 >> 5; i < nc; i += T >> 5) {
+      const double v = csr_row_warp(h.Rptr[l], h.Rcol[l], h.Rval[l], i, r, (int)(t0 & 31));
+      if ((t0 & 31) == 0) h.f[l + 1][i] = v;
+    }
+    grid.sync();
+  }
+  if (h.ncf > 0) {                       // coarsest level: x = A^-1 f (dense inverse, warp per row)
+    const int lane = (int)(t0 & 31);
+    for (long long i = t0 >> 5; i < h.ncf; i += T >> 5) {
+      const double* row = h.cinv + i * (long long)h.ncf;
+      double s = 0.0;
+      for (int j = lane; j < h.ncf; j += 32) s = fma(__ldg(&row[j]), __ldcg(&h.f[L][__ldg(&h.cidx[j])]), s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) h.x[L][__ldg(&h.cidx[i])] = s;
+    }
+  } else if (blockIdx.x == 0) {          // large coarsest level: block 0, Jacobi sweeps, block barriers
+    const long long n = h.n[L];
+    double *x = h.x[L], *r = h.r[L];
+    const double *f = h.f[L], *di = h.dinv[L];
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) x[i] = kHmgOmega * di[i] * f[i];
+    __syncthreads();
+    for (int s = 1; s < kHmgCoarsest; ++s) {
+      for (long long i = threadIdx.x; i < n; i += blockDim.x) r[i] = f[i] - ell_row(h.Aval[L], h.Acol[L], n, i, x);
+      __syncthreads();
+      for (long long i = threadIdx.x; i < n; i += blockDim.x) x[i] = fma(kHmgOmega * di[i], r[i], x[i]);
+      __syncthreads();
+    }
+  }
+  grid.sync();
+  for (int l = L - 1; l >= 0; --l) {
+    const long long n = h.n[l];
+    double *x = h.x[l], *r = h.r[l];
+    const double *f = h.f[l], *di = h.dinv[l];
+    for (long long i = t0 >> 5; i < n; i += T >> 5) {
+      const double v = csr_row_warp(h.Pptr[l], h.Pcol[l], h.Pval[l], i, h.x[l + 1], (int)(t0 & 31));
+      if ((t0 & 31) == 0) x[i] += v;
+    }
+    grid.sync();
+    for (int s = 0; s < kHmgNu; ++s) {
+      for (long long i = t0; i < n; i += T) r[i] = f[i] - ell_row(h.Aval[l], h.Acol[l], n, i, x);
+      grid.sync();
+      for (long long i = t0; i < n; i += T) x[i] = fma(kHmgOmega * di[i], r[i], x[i]);
+      grid.sync();
+    }
+  }
+}
+}  // namespace
+
+// Standard PCG (as mg.pcg / hmg.pcg_hmg): x = 0, r = b, z = M^-1 r, p = z; q = A p, alpha = r.z / p.q,
+// x += alpha p, r -= alpha q, stop at ||r|| <= rtol ||b||, z = M^-1 r, beta = r.z_new / r.z, p = z + beta p.
+// r lives in h.f[0] (the V-cycle's right-hand side), z in h.x[0].
+__global__ void __launch_bounds__(256) k_pcg_hmg_p2(HmgDev h, const double* __restrict__ b, double* __restrict__ xout,
+                                                   double* __restrict__ pv, double* __restrict__ q,
+                                                   double* __restrict__ part, PcgState* st, double rtol, int maxit) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[96];
+  const int nb = gridDim.x;
+  const long long n = h.n[0];
+  const long long T = (long long)gridDim.x * blockDim.x, t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  double* R = h.f[0];
+  double* Z = h.x[0];
+  double *pa = part, *pb = part + nb, *pc = part + 2 * nb;
+  double sb = 0.0;
+  for (long long i = t0; i < n; i += T) {
+    const double bi = b[i];
+    xout[i] = 0.0;
+    R[i] = bi;
+    sb = fma(bi, bi, sb);
+  }
+  block_reduce3(sb, 0.0, 0.0, red, blockIdx.x, pa, pb, pc);
+  grid.sync();
+  double bb, d1, d2;
+  grid_totals3(pa, pb, pc, nb, red, bb, d1, d2);
+  int its = 0, breakdown = 0;
+  if (bb > 0.0) {
+    hmg_vcycle(h, grid, t0, T);
+    double srz = 0.0;
+    for (long long i = t0; i < n; i += T) {
+      pv[i] = Z[i];
+      srz = fma(R[i], Z[i], srz);
+    }
+    block_reduce3(srz, 0.0, 0.0, red, blockIdx.x, pa, pb, pc);
+    grid.sync();
+    double rz;
+    grid_totals3(pa, pb, pc, nb, red, rz, d1, d2);
+    for (;;) {
+      double spq = 0.0;
+      for (long long i = t0; i < n; i += T) {
+        const double qi = ell_row(h.Aval[0], h.Acol[0], n, i, pv);
+        q[i] = qi;
+        spq = fma(pv[i], qi, spq);
+      }
+      block_reduce3(spq, 0.0, 0.0, red, blockIdx.x, pa, pb, pc);
+      grid.sync();
+      double pq;
+      grid_totals3(pa, pb, pc, nb, red, pq, d1, d2);
+      if (!(pq > 0.0)) { breakdown = 1; break; }
+      const double alpha = rz / pq;
+      double srr = 0.0;
+      for (long long i = t0; i < n; i += T) {
+        xout[i] = fma(alpha, pv[i], xout[i]);
+        const double ri = fma(-alpha, q[i], R[i]);
+        R[i] = ri;
+        srr = fma(ri, ri, srr);
+      }
+      block_reduce3(srr, 0.0, 0.0, red, blockIdx.x, pa, pb, pc);
+      grid.sync();
+      double rr;
+      grid_totals3(pa, pb, pc, nb, red, rr, d1, d2);
+      ++its;
+      if (sqrt(rr) <= rtol * sqrt(bb) || its >= maxit) break;
+      hmg_vcycle(h, grid, t0, T);
+      double srz2 = 0.0;
+      for (long long i = t0; i < n; i += T) srz2 = fma(R[i], Z[i], srz2);
+      block_reduce3(srz2, 0.0, 0.0, red, blockIdx.x, pa, pb, pc);
+      grid.sync();
+      double rzn;
+      grid_totals3(pa, pb, pc, nb, red, rzn, d1, d2);
+      const double beta = rzn / rz;
+      rz = rzn;
+      for (long long i = t0; i < n; i += T) pv[i] = fma(beta, pv[i], Z[i]);
+      grid.sync();
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->its = its;
+    st->its_sum += its;
+    if (breakdown) st->breakdown = 1;
+    st->done = 1;
+    st->bb = bb;
+  }
+}
+
 // Two grid barriers per iteration: with p_new = z + beta p and q = H_hat p,
 //   q_new = H_hat z + beta q_old,
 // so the direction update, the operator application (on z, complete after the previous barrier)

@@ -61,6 +61,31 @@ __global__ void k_pcg_coop_reg_p2(LevelGeom g, CoarseTabs ct, const double* b, d
                                   const double* dinv, double lam, double* part, PcgState* st, double rtol, int maxit);
 __global__ void k_pcg_gv_p2(LevelGeom g, CoarseTabs ct, const double* b, double* xout, double* mbuf,
                             const double* dinv, double lam, double* part, PcgState* st, double rtol, int maxit);
+// h-multigrid preconditioned coarse CG (reading R16): level 0 is the p0 = 2 coarse system, level
+// l + 1 has half the elements per direction; ELL rows per level, CSR transfers P_l (l <- l+1) and
+// R_l = P_l^T; per-level work vectors x, f, r.
+constexpr int kMaxHLevels = 8;
+struct HmgDev {
+  int nlev;
+  long long n[kMaxHLevels];
+  const double* Aval[kMaxHLevels];
+  const int* Acol[kMaxHLevels];
+  const double* dinv[kMaxHLevels];
+  double* x[kMaxHLevels];
+  double* f[kMaxHLevels];
+  double* r[kMaxHLevels];
+  const int* Pptr[kMaxHLevels];
+  const int* Pcol[kMaxHLevels];
+  const double* Pval[kMaxHLevels];
+  const int* Rptr[kMaxHLevels];
+  const int* Rcol[kMaxHLevels];
+  const double* Rval[kMaxHLevels];
+  int ncf;                 // coarsest level solved exactly: its free unknowns (0: Jacobi sweeps instead)
+  const int* cidx;         // their skeleton indices
+  const double* cinv;      // dense inverse (ncf x ncf, row-major) of the coarsest condensed operator
+};
+__global__ void k_pcg_hmg_p2(HmgDev h, const double* b, double* xout, double* pv, double* q, double* part, PcgState* st,
+                             double rtol, int maxit);
 __global__ void k_build_coarse_ell(LevelGeom g, CoarseTabs ct, double lam, int* ellc, double* ella);
 __global__ void k_pcg_gv_ell_p2(long long n, const double* b, double* xout, double* vec, double* mbuf, const double* dinv,
                                 const int* ellc, const double* ella, double* part, PcgState* st, double rtol, int maxit);

@@ -100,6 +100,13 @@ struct pmg_ctx {
   double* ella = nullptr;    // 25 n0 coefficients, then the indices (one block: one L2 window)
   cudaAccessPolicyWindow ell_win{};   // L2 persistence of the ELL rows (when the device allows it)
   bool ell_persist = false;
+  // h-multigrid preconditioned coarse CG (reading R16)
+  bool use_hmg = false;
+  int hmg_nb = 0;
+  HmgDev hmg{};
+  std::vector<HostLevel> hhost;      // h-levels 1.. (level 0 is H[0])
+  std::vector<void*> hmg_allocs;     // device buffers owned by the h-hierarchy
+  double *hpv = nullptr, *hq = nullptr;
   double* ellv = nullptr;    // 8 n0 CG vectors
   double* ctab[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // CoarseTabs storage
   double* cV = nullptr;      // (unused)
@@ -157,6 +164,12 @@ namespace {
 int* done_ptr(pmg_ctx* c) { return reinterpret_cast<int*>(reinterpret_cast<char*>(c->pcg) + offsetof(PcgState, done)); }
 
 long long plane_len(const LevelGeom& g) { return (long long)g.V1 * g.V2 * g.RS; }
+
+int nsm_dev(int dev) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
 
 // refresh the ghost record planes of a level-l skeleton vector from the neighbour ranks
 pmg_status exchange(pmg_ctx* c, int l, double* x) {
@@ -287,6 +300,21 @@ pmg_status pcg_dev(pmg_ctx* c, const double* b, double* x) {
                     &st, &rtol, &maxit};
     void* args_reg[] = {&g0, &ct, (void*)&b, &x, &c->cz, (void*)&dinv, &lam, &part, &st, &rtol, &maxit};
     void* args_gv[] = {&g0, &ct, (void*)&b, &x, &c->cgm, (void*)&dinv, &lam, &part, &st, &rtol, &maxit};
+    if (c->use_hmg) {   // CG preconditioned by the h-multigrid V-cycle (reading R16)
+      void* args_h[] = {&c->hmg, (void*)&b, &x, &c->hpv, &c->hq, &part, &st, &rtol, &maxit};
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(c->hmg_nb);
+      cfg.blockDim = dim3(kThreads);
+      cfg.stream = c->st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CUDA_CHECK(cudaLaunchKernelExC(&cfg, (const void*)k_pcg_hmg_p2, args_h));
+      c->launches++;
+      return PMG_OK;
+    }
     if (c->coop_ell && rtol >= 1e-11) {   // large coarse system: grid-stride pipelined CG on ELL rows
       long long n0 = g0.nskel;
       void* args_ell[] = {&n0, (void*)&b, &x, &c->ellv, &c->cgm, (void*)&dinv, &c->ellc, &c->ella, &part, &st, &rtol, &maxit};
@@ -625,6 +653,8 @@ void free_ctx(pmg_ctx* c) {
   }
   cudaFree(c->Y); cudaFree(c->Z); cudaFree(c->cube); cudaFree(c->part); cudaFree(c->dres); cudaFree(c->pcg);
   cudaFree(c->cgm); cudaFree(c->ella); cudaFree(c->ellv);
+  for (void* a : c->hmg_allocs) cudaFree(a);
+  cudaFree(c->hpv); cudaFree(c->hq);
   cudaFree(c->cx); cudaFree(c->cr); cudaFree(c->cz); cudaFree(c->cp); cudaFree(c->cq); cudaFree(c->dinv);
   for (int d = 0; d < 3; ++d) cudaFree(c->bm[d]);
   cudaFree(c->Fdev); cudaFree(c->Udev);
@@ -674,6 +704,7 @@ void pmg_default_options(pmg_options* o) {
   o->coarse_rtol = 1e-8;
   o->coarse_maxit = 10000;
   o->coarse_check = 8;
+  o->coarse_solver = 0;
   o->rank = 0;
   o->nranks = 1;
   o->nccl_id = nullptr;
@@ -703,6 +734,7 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   if (o.weight_degree != 7) return fail(PMG_EINVAL, "only weight_degree = 7 is implemented (P:316)");
   if (o.schedule != 0 && o.schedule != 1) return fail(PMG_EINVAL, "schedule must be 0 or 1");
   if (o.solver != 0 && o.solver != 1) return fail(PMG_EINVAL, "solver must be 0 (MG) or 1 (ipCG)");
+  if (o.coarse_solver < 0 || o.coarse_solver > 2) return fail(PMG_EINVAL, "coarse_solver must be 0 (auto), 1 (Jacobi) or 2 (h-multigrid)");
   if (o.neumann < 0 || o.neumann > 63) return fail(PMG_EINVAL, "neumann is a 6-bit face mask");
   if (o.neumann == 63 && lambda == 0.0) return fail(PMG_EINVAL, "all-Neumann Poisson (lambda = 0) is singular");
   if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return fail(PMG_EINVAL, "need 0 <= rank < nranks");
@@ -946,6 +978,179 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
       }
       const char* nbenv = std::getenv("PMG_COOP_BLOCKS");   // tuning experiments only
       if (nbenv && std::atoi(nbenv) > 0) c->coop_nb = (int)std::min<long long>(std::atoi(nbenv), cap);
+    }
+  }
+  // h-multigrid coarse preconditioner (reading R16): element-merged p0 = 2 levels
+  {
+    const LevelGeom& g0 = c->g0g;
+    const int k0[3] = {g0.k1, g0.k2, g0.k3};
+    auto halvable = [](int kd) { return kd % 2 == 0 && kd / 2 >= 2; };
+    auto coarsenable = [&](const int* k) { return halvable(k[0]) || halvable(k[1]) || halvable(k[2]); };
+    const long long ne0 = (long long)k0[0] * k0[1] * k0[2];
+    // automatic choice: a large coarse system whose Jacobi-PCG iteration count grows with the mesh,
+    // i.e. not mass dominated: lambda L_min^2 < 100 (L_min the shortest box edge; config 4's
+    // lambda = 100 on (0, 2 pi) converges in ~45 Jacobi-PCG iterations and stays on Jacobi)
+    double Lmin = 1e300;
+    for (int d = 0; d < 3; ++d) {
+      double Ld = 0.0;
+      for (int e = 0; e < n_e[d]; ++e) Ld += widths[d][e];
+      Lmin = std::min(Lmin, Ld);
+    }
+    const bool want = c->use_coop && c->D[0].g.p == 2 &&
+                      (o.coarse_solver == 2 ||
+                       (o.coarse_solver == 0 && ne0 > 12288 && coarsenable(k0) && lambda * Lmin * Lmin < 100.0));
+    if (o.coarse_solver == 2 && !(c->use_coop && coarsenable(k0))) {
+      free_ctx(c);
+      return fail(PMG_EINVAL, "coarse_solver = 2 needs p0 = 2 and some k_d even with k_d / 2 >= 2");
+    }
+    if (want) {
+      // widths of every h-level (pairwise sums), host tables, ELL rows, 1/diag, transfers
+      std::vector<std::vector<double>> wl[3];
+      for (int d = 0; d < 3; ++d) wl[d].push_back(std::vector<double>(widths[d], widths[d] + n_e[d]));
+      int kl[3] = {k0[0], k0[1], k0[2]};
+      std::vector<const HostLevel*> hl{&c->H[0]};
+      c->hhost.reserve(kMaxHLevels);
+      while (coarsenable(kl) && (int)hl.size() < kMaxHLevels) {
+        int kn[3];
+        const double* wp[3];
+        for (int d = 0; d < 3; ++d) {   // semi-coarsening: only halvable directions merge
+          const bool hv = halvable(kl[d]);
+          kn[d] = hv ? kl[d] / 2 : kl[d];
+          std::vector<double> w2(kn[d]);
+          for (int e = 0; e < kn[d]; ++e) w2[e] = hv ? wl[d].back()[2 * e] + wl[d].back()[2 * e + 1] : wl[d].back()[e];
+          wl[d].push_back(w2);
+        }
+        for (int d = 0; d < 3; ++d) wp[d] = wl[d].back().data();
+        c->hhost.emplace_back();
+        std::string err = build_level(c->hhost.back(), 2, kn, wp, lambda, o.weight_degree, o.neumann);
+        if (!err.empty()) { free_ctx(c); return fail(PMG_EINVAL, "h-level: " + err); }
+        hl.push_back(&c->hhost.back());
+        for (int d = 0; d < 3; ++d) kl[d] = kn[d];
+      }
+      HmgDev& h = c->hmg;
+      h.nlev = (int)hl.size();
+      bool ok = true;
+      auto dal = [&](double** ptr, size_t cnt) {
+        if (!ok || dalloc(ptr, cnt) != cudaSuccess) { ok = false; return; }
+        c->hmg_allocs.push_back(*ptr);
+        cudaMemset(*ptr, 0, cnt * sizeof(double));
+      };
+      auto up_d = [&](const std::vector<double>& v) -> const double* {
+        double* p_ = nullptr;
+        dal(&p_, std::max<size_t>(1, v.size()));
+        if (ok) cudaMemcpy(p_, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice);
+        return p_;
+      };
+      auto up_i = [&](const std::vector<int>& v) -> const int* {
+        double* p_ = nullptr;
+        dal(&p_, std::max<size_t>(1, (v.size() + 1) / 2));
+        if (ok) cudaMemcpy(p_, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice);
+        return reinterpret_cast<const int*>(p_);
+      };
+      for (int l = 0; l < h.nlev && ok; ++l) {
+        const HostLevel& HL = *hl[l];
+        const long long n = HL.g.nskel;
+        h.n[l] = n;
+        std::vector<double> tabs[7];
+        coarse_tables(HL, lambda, tabs);
+        const double* ct_d[7];
+        for (int i = 0; i < 7; ++i) ct_d[i] = up_d(tabs[i]);
+        double *val = nullptr, *colblk = nullptr;
+        dal(&val, 25 * n);
+        dal(&colblk, (25 * n + 1) / 2);
+        if (!ok) break;
+        CoarseTabs ct{ct_d[0], ct_d[1], ct_d[2], ct_d[3], ct_d[4], ct_d[5], ct_d[6]};
+        k_build_coarse_ell<<<grid_for(n), kThreads>>>(HL.g, ct, lambda, reinterpret_cast<int*>(colblk), val);
+        h.Aval[l] = val;
+        h.Acol[l] = reinterpret_cast<const int*>(colblk);
+        std::vector<double> dg, di;
+        coarse_diag(HL, lambda, dg);
+        di.resize(dg.size());
+        for (size_t i = 0; i < dg.size(); ++i) di[i] = dg[i] != 0.0 ? 1.0 / dg[i] : 0.0;
+        h.dinv[l] = up_d(di);
+        dal(&h.x[l], n);
+        dal(&h.f[l], n);
+        dal(&h.r[l], n);
+        if (l + 1 < h.nlev) {
+          std::vector<int> Pp, Pc, Rp, Rc;
+          std::vector<double> Pv, Rv;
+          std::string err = build_h_transfer(HL, *hl[l + 1], lambda, o.neumann, Pp, Pc, Pv, Rp, Rc, Rv);
+          if (!err.empty()) { free_ctx(c); return fail(PMG_EINVAL, err); }
+          h.Pptr[l] = up_i(Pp); h.Pcol[l] = up_i(Pc); h.Pval[l] = up_d(Pv);
+          h.Rptr[l] = up_i(Rp); h.Rcol[l] = up_i(Rc); h.Rval[l] = up_d(Rv);
+        }
+      }
+      if (ok) {
+        const long long n0h = h.n[0];
+        if (dalloc(&c->hpv, n0h) != cudaSuccess || dalloc(&c->hq, n0h) != cudaSuccess) ok = false;
+      }
+      // coarsest level: dense inverse over its free unknowns (<= 1500, as the oracle), assembled
+      // from the ELL rows; Cholesky-based inversion on the host
+      h.ncf = 0;
+      if (ok) {
+        const int Lc = h.nlev - 1;
+        const long long n = h.n[Lc];
+        std::vector<double> val(25 * n), dinvL(n);
+        std::vector<int> col(25 * n);
+        cudaDeviceSynchronize();
+        cudaMemcpy(val.data(), h.Aval[Lc], val.size() * sizeof(double), cudaMemcpyDeviceToHost);
+        cudaMemcpy(col.data(), h.Acol[Lc], col.size() * sizeof(int), cudaMemcpyDeviceToHost);
+        cudaMemcpy(dinvL.data(), h.dinv[Lc], n * sizeof(double), cudaMemcpyDeviceToHost);
+        std::vector<int> fidx, pos(n, -1);
+        for (long long i = 0; i < n; ++i) if (dinvL[i] != 0.0) { pos[i] = (int)fidx.size(); fidx.push_back((int)i); }
+        const int nf = (int)fidx.size();
+        if (nf > 0 && nf <= 1500) {
+          std::vector<double> A((size_t)nf * nf, 0.0);
+          for (int a = 0; a < nf; ++a)
+            for (int kx = 0; kx < 25; ++kx) {
+              const long long e = (long long)kx * n + fidx[a];
+              if (val[e] != 0.0 && pos[col[e]] >= 0) A[(size_t)a * nf + pos[col[e]]] += val[e];
+            }
+          // Cholesky A = L L^T, then A^-1 column by column
+          bool spd = true;
+          for (int j = 0; j < nf && spd; ++j) {
+            double d = A[(size_t)j * nf + j];
+            for (int k = 0; k < j; ++k) d -= A[(size_t)j * nf + k] * A[(size_t)j * nf + k];
+            if (!(d > 0.0)) { spd = false; break; }
+            d = std::sqrt(d);
+            A[(size_t)j * nf + j] = d;
+            for (int i = j + 1; i < nf; ++i) {
+              double v = A[(size_t)i * nf + j];
+              for (int k = 0; k < j; ++k) v -= A[(size_t)i * nf + k] * A[(size_t)j * nf + k];
+              A[(size_t)i * nf + j] = v / d;
+            }
+          }
+          if (spd) {
+            std::vector<double> inv((size_t)nf * nf), y(nf);
+            for (int cidx_ = 0; cidx_ < nf; ++cidx_) {
+              for (int i = 0; i < nf; ++i) {             // L y = e_c
+                double v = (i == cidx_) ? 1.0 : 0.0;
+                for (int k = 0; k < i; ++k) v -= A[(size_t)i * nf + k] * y[k];
+                y[i] = v / A[(size_t)i * nf + i];
+              }
+              for (int i = nf - 1; i >= 0; --i) {        // L^T x = y
+                double v = y[i];
+                for (int k = i + 1; k < nf; ++k) v -= A[(size_t)k * nf + i] * y[k];
+                y[i] = v / A[(size_t)i * nf + i];
+              }
+              for (int i = 0; i < nf; ++i) inv[(size_t)i * nf + cidx_] = y[i];
+            }
+            h.cinv = up_d(inv);
+            h.cidx = up_i(fidx);
+            if (ok) h.ncf = nf;
+          }
+        }
+      }
+      int per_sm_h = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_h, k_pcg_hmg_p2, kThreads, 0);
+      if (!ok || per_sm_h <= 0 || cudaGetLastError() != cudaSuccess) {
+        free_ctx(c);
+        return fail(PMG_ENOMEM, "h-multigrid coarse solver: allocation / setup failed");
+      }
+      c->hmg_nb = (int)std::min<long long>((long long)per_sm_h * nsm_dev(dev),
+                                           std::max<long long>(1, (h.n[0] + kThreads - 1) / kThreads));
+      c->hmg_nb = std::min(c->hmg_nb, 2048);
+      c->use_hmg = true;
     }
   }
   if (c->tr && !c->use_coop) {

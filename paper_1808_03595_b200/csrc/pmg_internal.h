@@ -85,5 +85,10 @@ std::string coarse_diag(const HostLevel& L, double lambda, std::vector<double>& 
 std::string coarse_tables(const HostLevel& L, double lambda, std::vector<double> tabs[7]);
 // 1-D GLL nodes and weights (p >= 1)
 void gll(int p, std::vector<double>& x, std::vector<double>& w);
+// h-multigrid transfer between two p = 2 levels (k_fine = 2 k_coarse): CSR P (fine <- coarse) and
+// R = P^T over skeleton entries (reading R16)
+std::string build_h_transfer(const HostLevel& fine, const HostLevel& coarse, double lambda, int neumann,
+                             std::vector<int>& Pptr, std::vector<int>& Pcol, std::vector<double>& Pval,
+                             std::vector<int>& Rptr, std::vector<int>& Rcol, std::vector<double>& Rval);
 
 }  // namespace pmg

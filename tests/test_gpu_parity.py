@@ -542,3 +542,66 @@ def test_neumann_invalid_options():
         pmg.Solver(case.k, case.widths, 4, 0.0, neumann=63)      # singular all-Neumann Poisson
     with pytest.raises(pmg.PmgError):
         pmg.Solver(case.k, case.widths, 4, 1.0, neumann=64)
+
+
+HMG_CASES = {
+    "k444_p4_lam0.6": dict(k=(4, 4, 4), p=4, lam=0.6, stretch=1.3, neumann=0),
+    "k844_p2_lam0": dict(k=(8, 4, 4), p=2, lam=0.0, stretch=None, neumann=0),          # L = 0: CG only
+    "k448_p8_neu": dict(k=(4, 4, 8), p=8, lam=0.9, stretch=None, neumann=0b110011),
+}
+
+
+@pytest.mark.parametrize("name", list(HMG_CASES))
+def test_hmg_coarse_solver_parity(name):
+    """The h-multigrid preconditioned coarse CG (NEXT-2, reading R16) forced on small meshes: the
+    V-cycle and the solve against the oracle running the same preconditioner (oracle/hmg.py)."""
+    import paper_1808_03595_b200 as pmg
+    from oracle import condensed, mg
+    cfg = HMG_CASES[name]
+    case = pi.small_case(cfg["k"], cfg["p"], cfg["lam"], stretch=cfg["stretch"])
+    orc = mg.Hierarchy(case.k, case.widths, case.p, case.lam, coarse_rtol=1e-13, neumann=cfg["neumann"],
+                       coarse_solver="hmg")
+    s = pmg.Solver(case.k, case.widths, case.p, case.lam, coarse_rtol=1e-13, neumann=cfg["neumann"],
+                   coarse_solver=2)
+    L = s.nlevels - 1
+    m = orc.levels[-1].mesh
+    f = np.random.default_rng(3).standard_normal(m.ntot) * m.free_skel
+    fs = s.new_skel(L)
+    s.skel_from_grid(L, torch.from_numpy(f).cuda(), fs)
+    u = s.new_skel(L)
+    s.vcycle(u, fs)
+    g = s.new_grid(L)
+    s.skel_to_grid(L, u, g)
+    torch.cuda.synchronize()
+    assert rel(g.cpu().numpy(), orc.vcycle(np.zeros_like(f), f)) < OP_TOL
+    F = condensed.weak_rhs(m, pi.uniform_pm1(8, np.arange(m.ntot)))
+    u_o, rep_o = orc.solve(F, 1e-10)
+    ug = s.new_grid()
+    rep = s.solve(torch.from_numpy(F).cuda(), ug, 1e-10)
+    torch.cuda.synchronize()
+    assert rep["cycles"] == rep_o["cycles"] and rel(ug.cpu().numpy(), u_o) < SOLVE_TOL
+    s.close()
+
+
+def test_hmg_auto_on_large_mesh_matches_jacobi():
+    """32^3 elements at p = 4 (coarse 32^3 at p0 = 2, 226 k unknowns): the automatic choice takes the
+    h-multigrid coarse CG; the solve agrees with the Jacobi-PCG one and needs far fewer coarse
+    iterations."""
+    import paper_1808_03595_b200 as pmg
+    k = (32, 32, 32)
+    w = pi.uniform_widths(k, (1.0,) * 3)
+    outs = []
+    for cs in (0, 1):
+        s = pmg.Solver(k, w, 4, 0.0, coarse_solver=cs)
+        f = torch.from_numpy(np.random.default_rng(1).uniform(-1, 1, s.level_info(s.nlevels - 1)[2])).cuda()
+        F = s.new_grid()
+        s.weak_rhs(f, F)
+        u = s.new_grid()
+        rep = s.solve(F, u, 1e-10)
+        torch.cuda.synchronize()
+        outs.append((u.cpu().numpy(), rep))
+        s.close()
+    (u0, r0), (u1, r1) = outs
+    assert r0["converged"] and r1["converged"] and r0["cycles"] == r1["cycles"]
+    assert np.linalg.norm(u0 - u1) <= 1e-8 * np.linalg.norm(u1)
+    assert r0["coarse_iters"] * 5 < r1["coarse_iters"], (r0["coarse_iters"], r1["coarse_iters"])

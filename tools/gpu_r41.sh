@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "hmg" > gpurun_out/pytest_hmg.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_hmg.log; tail -2 gpurun_out/pytest_hmg.log
+timeout 600 python bench.py --config 4 --steps 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_cfg4_r41.json 2>&1; python -c "
+import json; d=json.loads(open('gpurun_out/bench_cfg4_r41.json').read().strip().splitlines()[-1]); print(4, d['value'], d['ms_per_step'], d['config']['coarse_iters'], d['time_split_ms_per_step'])"
