@@ -8,7 +8,7 @@ and gains a symmetric h-multigrid V-cycle as preconditioner:
   - h-levels: the p = 2 condensed system on element-merged meshes: a direction is halved (pairs
     of elements merged, widths summed) while its k_d is even with k_d / 2 >= 2 (directions that
     cannot be halved keep their elements: semi-coarsening); levels continue while any direction
-    halves;
+    halves and the current level has more than DENSE_MAX free unknowns;
   - transfer: P = fine free skeleton <- coarse free skeleton, the coarse element's quadratic
     (tensor GLL Lagrange basis on {-1, 0, 1}) evaluated at the fine nodes, with the coarse
     element's interior (centre) value given by its harmonic extension
@@ -115,7 +115,8 @@ class HMultigrid:
 
     def __init__(self, k, widths, lam, neumann=0):
         self.levels = [HLevel(k, widths, lam, neumann)]
-        while coarsenable(self.levels[-1].mesh.k):
+        # coarsen until a level is small enough for the exact (dense) coarsest solve
+        while coarsenable(self.levels[-1].mesh.k) and int(self.levels[-1].mesh.free_skel.sum()) > DENSE_MAX:
             m = self.levels[-1].mesh
             kc, wc = coarsen(m.k, m.widths)
             self.levels.append(HLevel(kc, wc, lam, neumann))

@@ -1010,7 +1010,16 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
       int kl[3] = {k0[0], k0[1], k0[2]};
       std::vector<const HostLevel*> hl{&c->H[0]};
       c->hhost.reserve(kMaxHLevels);
-      while (coarsenable(kl) && (int)hl.size() < kMaxHLevels) {
+      // coarsen until a level has at most 1500 free unknowns (the dense coarsest solve; as the oracle)
+      auto nfree_p2 = [&](const int* k) {
+        long long f = 1;
+        for (int d = 0; d < 3; ++d) {
+          const bool lo = (o.neumann >> (2 * d)) & 1, hi_ = (o.neumann >> (2 * d + 1)) & 1;
+          f *= (long long)(2 * k[d] + 1) - (lo ? 0 : 1) - (hi_ ? 0 : 1);
+        }
+        return f - (long long)k[0] * k[1] * k[2];   // free grid points minus element centres
+      };
+      while (coarsenable(kl) && nfree_p2(kl) > 1500 && (int)hl.size() < kMaxHLevels) {
         int kn[3];
         const double* wp[3];
         for (int d = 0; d < 3; ++d) {   // semi-coarsening: only halvable directions merge

@@ -544,10 +544,10 @@ def test_neumann_invalid_options():
         pmg.Solver(case.k, case.widths, 4, 1.0, neumann=64)
 
 
-HMG_CASES = {
-    "k444_p4_lam0.6": dict(k=(4, 4, 4), p=4, lam=0.6, stretch=1.3, neumann=0),
-    "k844_p2_lam0": dict(k=(8, 4, 4), p=2, lam=0.0, stretch=None, neumann=0),          # L = 0: CG only
-    "k448_p8_neu": dict(k=(4, 4, 8), p=8, lam=0.9, stretch=None, neumann=0b110011),
+HMG_CASES = {   # coarse levels above the 1500-unknown dense limit: at least two h-levels
+    "k888_p4_lam0.6": dict(k=(8, 8, 8), p=4, lam=0.6, stretch=1.3, neumann=0),
+    "k1688_p2_lam0": dict(k=(16, 8, 8), p=2, lam=0.0, stretch=None, neumann=0),        # L = 0: CG only
+    "k884_p4_neu": dict(k=(8, 8, 4), p=4, lam=0.9, stretch=None, neumann=0b110011),
 }
 
 

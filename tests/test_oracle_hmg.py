@@ -62,7 +62,8 @@ def test_hmg_pcg_solves_and_is_mesh_independent():
             assert np.abs(x[fs] - xd).max() <= 1e-8 * np.abs(xd).max()
         if n <= 8:
             its_j.append(mg.pcg(mg.Level(k, w, 2, 0.0, 7), b, 1e-10, 10000)[1])
-    assert max(its_h) <= 16 and max(its_h) - min(its_h) <= 3, its_h
+    # at 4^3 the level itself is small enough for the exact coarsest solve (one iteration)
+    assert its_h[0] <= 2 and max(its_h[1:]) <= 16 and abs(its_h[2] - its_h[1]) <= 3, its_h
     assert its_j[1] > 1.5 * its_j[0]                 # Jacobi-PCG grows with the element count
 
 
