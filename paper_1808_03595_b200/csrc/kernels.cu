@@ -482,7 +482,8 @@ __global__ void k_restrict_local_t(LevelGeom gf, int pc_rt, const double* __rest
 }
 
 template <int PC_>
-__global__ void k_restrict_gather_t(LevelGeom gc, const double* __restrict__ Z, double* __restrict__ fc) {
+__global__ void k_restrict_gather_t(LevelGeom gc, const double* __restrict__ Z, double* __restrict__ fc,
+                                    double* __restrict__ uzero) {
   pdl_wait();
   pdl_trigger();
   const int pc = PC_ > 0 ? PC_ : gc.p, qc = pc + 1, ZS = 3 * qc * qc + 3 * qc + 1;
@@ -530,6 +531,7 @@ __global__ void k_restrict_gather_t(LevelGeom gc, const double* __restrict__ Z, 
       if (mult[0] && mult[1] && mult[2]) s += Z[rec(G[0] / pc, G[1] / pc, G[2] / pc) + ZS - 1];
     }
     fc[idx] = s;
+    if (uzero) uzero[idx] = 0.0;   // Alg. 3: u_(l-1) <- 0 before its smoothing, fused here
   }
 }
 
@@ -847,6 +849,35 @@ __global__ void k_dot_partial(const double* __restrict__ a, const double* __rest
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// a.b in one launch: per-block partials, and the block that arrives last (atomic ticket) sums them
+// in block order -- the same deterministic result as k_dot_partial + k_sum_final, one launch fewer.
+// `ticket` must be 0 on entry; the last block resets it.
+__global__ void k_dot_fused(const double* __restrict__ a, const double* __restrict__ b, long long n,
+                            double* __restrict__ part, unsigned* __restrict__ ticket, double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ bool last;
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    s += a[i] * b[i];
+  s = block_sum(s);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double t = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) t += __ldcg(&part[i]);
+  t = block_sum(t);
+  if (threadIdx.x == 0) {
+    *out = t;
+    *ticket = 0u;
+  }
+}
+
 __global__ void k_sum_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
@@ -1055,7 +1086,7 @@ namespace pmg {
 #define PMG_TRANSFER_PAIRS(X) X(4, 2) X(8, 4) X(16, 8) X(32, 16) X(12, 8) X(24, 16) X(3, 2) X(6, 4)
 
 cudaError_t launch_restrict(const LevelGeom& gf, const LevelGeom& gc, const double* Jint, const double* rf, double* Z,
-                            double* fc, int nt_local, size_t smem, int gather_blocks, cudaStream_t st) {
+                            double* fc, double* uzero, int nt_local, size_t smem, int gather_blocks, cudaStream_t st) {
   const int pf = gf.p, pc = gc.p;
   cudaError_t e = cudaSuccess;
   bool done = false;
@@ -1070,11 +1101,11 @@ cudaError_t launch_restrict(const LevelGeom& gf, const LevelGeom& gc, const doub
     e = launch_pdl(k_restrict_local_t<0, 0>, dim3((unsigned)gf.nrec), dim3(nt_local), smem, st, gf, pc, Jint, rf, Z);
   if (e != cudaSuccess) return e;
   switch (pc) {
-    case 2: return launch_pdl(k_restrict_gather_t<2>, dim3(gather_blocks), dim3(256), 0, st, gc, (const double*)Z, fc);
-    case 4: return launch_pdl(k_restrict_gather_t<4>, dim3(gather_blocks), dim3(256), 0, st, gc, (const double*)Z, fc);
-    case 8: return launch_pdl(k_restrict_gather_t<8>, dim3(gather_blocks), dim3(256), 0, st, gc, (const double*)Z, fc);
-    case 16: return launch_pdl(k_restrict_gather_t<16>, dim3(gather_blocks), dim3(256), 0, st, gc, (const double*)Z, fc);
-    default: return launch_pdl(k_restrict_gather_t<0>, dim3(gather_blocks), dim3(256), 0, st, gc, (const double*)Z, fc);
+    case 2: return launch_pdl(k_restrict_gather_t<2>, dim3(gather_blocks), dim3(256), 0, st, gc, (const double*)Z, fc, uzero);
+    case 4: return launch_pdl(k_restrict_gather_t<4>, dim3(gather_blocks), dim3(256), 0, st, gc, (const double*)Z, fc, uzero);
+    case 8: return launch_pdl(k_restrict_gather_t<8>, dim3(gather_blocks), dim3(256), 0, st, gc, (const double*)Z, fc, uzero);
+    case 16: return launch_pdl(k_restrict_gather_t<16>, dim3(gather_blocks), dim3(256), 0, st, gc, (const double*)Z, fc, uzero);
+    default: return launch_pdl(k_restrict_gather_t<0>, dim3(gather_blocks), dim3(256), 0, st, gc, (const double*)Z, fc, uzero);
   }
 }
 

@@ -103,7 +103,8 @@ __global__ void k_gather_resid(LevelGeom g, const double* Y, const double* F, do
 __global__ void k_star(LevelGeom g, int c1, int c2, int c3, int n1c, int n2c, const double* r, double* u,
                        const double* stab, double lam, int s_in_smem);
 cudaError_t launch_restrict(const LevelGeom& gf, const LevelGeom& gc, const double* Jint, const double* rf, double* Z,
-                            double* fc, int nt_local, size_t smem, int gather_blocks, cudaStream_t st);
+                            double* fc, double* uzero, int nt_local, size_t smem, int gather_blocks, cudaStream_t st);
+__global__ void k_dot_fused(const double* a, const double* b, long long n, double* part, unsigned* ticket, double* out);
 cudaError_t launch_prolong(const LevelGeom& gf, const LevelGeom& gc, const double* Jint, const double* uc, double* uf,
                            int nt, size_t smem, cudaStream_t st);
 cudaError_t transfer_set_smem_attr(int bytes);

@@ -62,6 +62,7 @@ struct pmg_ctx {
   bool star_s_smem = true;
   double* part = nullptr;    // reduction partials (2 x kRedBlocks)
   double* dres = nullptr;    // device scalar results
+  unsigned* ticket = nullptr;  // k_dot_fused's arrival counter (0 between launches)
   PcgState* pcg = nullptr;
   double *cx = nullptr, *cr = nullptr, *cz = nullptr, *cp = nullptr, *cq = nullptr, *dinv = nullptr;
   double* bm[3] = {nullptr, nullptr, nullptr};
@@ -228,10 +229,10 @@ int zs_of(int pc) { int qc = pc + 1; return 3 * qc * qc + 3 * qc + 1; }
 // per-record transfer kernels do O(p^3) work on O(p^2) data: size the block to the face
 int transfer_threads(int pf) { return pf <= 8 ? 64 : (pf <= 16 ? 128 : 256); }
 
-pmg_status restrict_dev(pmg_ctx* c, int l, const double* rf, double* fc) {
+pmg_status restrict_dev(pmg_ctx* c, int l, const double* rf, double* fc, double* uzero = nullptr) {
   const DevLevel& F = c->D[l];
   const DevLevel& C = c->D[l - 1];
-  launch_restrict(F.g, C.g, F.Jint, rf, c->Z, fc, transfer_threads(F.g.p), transfer_smem(F.g.p, C.g.p),
+  launch_restrict(F.g, C.g, F.Jint, rf, c->Z, fc, uzero, transfer_threads(F.g.p), transfer_smem(F.g.p, C.g.p),
                   grid_for(C.g.nskel), c->st);
   LAUNCH_CHECK(c);
   c->launches++;   // local + gather
@@ -253,9 +254,7 @@ pmg_status zero_dev(pmg_ctx* c, double* x, long long n) {
 }
 
 pmg_status dot_dev(pmg_ctx* c, const double* a, const double* b, long long n, double* out_dev) {
-  launch_pdl(k_dot_partial, dim3(kRedBlocks), dim3(kThreads), 0, c->st, a, b, n, c->part, (const int*)nullptr);
-  LAUNCH_CHECK(c);
-  launch_pdl(k_sum_final, dim3(1), dim3(1024), 0, c->st, (const double*)c->part, (int)kRedBlocks, out_dev);
+  launch_pdl(k_dot_fused, dim3(kRedBlocks), dim3(kThreads), 0, c->st, a, b, n, c->part, c->ticket, out_dev);
   LAUNCH_CHECK(c);
   return PMG_OK;
 }
@@ -448,10 +447,7 @@ pmg_status vcycle_dev(pmg_ctx* c, double* u, const double* f, bool r_top_valid) 
     const double* fl = (l == L) ? f : D.f;
     bool r_valid = (l == L) && r_top_valid;
     bool u_zero = false;
-    if (l != L) {
-      if ((s = zero_dev(c, ul, D.g.nskel))) return s;
-      u_zero = true;
-    }
+    if (l != L) u_zero = true;   // zeroed by the restriction kernel that produced f_l
     for (int i = 0; i < nu_of(c, l); ++i) {
       const double* rin = D.r;
       if (u_zero) rin = fl;                       // f - H 0 = f exactly
@@ -461,7 +457,8 @@ pmg_status vcycle_dev(pmg_ctx* c, double* u, const double* f, bool r_top_valid) 
       u_zero = false;
     }
     if ((s = residual_x(c, l, ul, fl, D.r))) return s;
-    if ((s = restrict_dev(c, l, D.r, c->D[l - 1].f))) return s;
+    // u_(l-1) <- 0 (Alg. 3) rides along with the restriction into level l-1 (not for the coarse CG's level)
+    if ((s = restrict_dev(c, l, D.r, c->D[l - 1].f, l - 1 >= 1 ? c->D[l - 1].u : nullptr))) return s;
     if (l - 1 >= 1 && (s = exchange(c, l - 1, c->D[l - 1].f))) return s;
   }
   if ((s = coarse_solve(c, c->D[0].f, c->D[0].u))) return s;
@@ -651,6 +648,7 @@ void free_ctx(pmg_ctx* c) {
   for (auto& D : c->D) {
     cudaFree(D.etab); cudaFree(D.stab); cudaFree(D.Jint); cudaFree(D.u); cudaFree(D.f); cudaFree(D.r);
   }
+  cudaFree(c->ticket);
   cudaFree(c->Y); cudaFree(c->Z); cudaFree(c->cube); cudaFree(c->part); cudaFree(c->dres); cudaFree(c->pcg);
   cudaFree(c->cgm); cudaFree(c->ella); cudaFree(c->ellv);
   for (void* a : c->hmg_allocs) cudaFree(a);
@@ -837,6 +835,11 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
       max_cond > (size_t)smem_optin || max_rec > (size_t)smem_optin) {
     free_ctx(c);
     return fail(PMG_EINVAL, "shared-memory plan exceeds the device limit for this p");
+  }
+  if (cudaMalloc(reinterpret_cast<void**>(&c->ticket), sizeof(unsigned)) != cudaSuccess ||
+      cudaMemset(c->ticket, 0, sizeof(unsigned)) != cudaSuccess) {
+    free_ctx(c);
+    return fail(PMG_ENOMEM, "cudaMalloc failed (ticket)");
   }
   if (dalloc(&c->Y, Ylen) || dalloc(&c->Z, Zlen) || dalloc(&c->part, 16384) || dalloc(&c->dres, 8) ||
       dalloc(&c->pcg, 1)) {
