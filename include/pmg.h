@@ -66,7 +66,7 @@ typedef struct {
   int solver;         /* pmg_solve: 0 = multigrid fixpoint iteration (Alg. 4, "MG");
                          1 = Krylov-accelerated multigrid, inexact preconditioned CG with one V-cycle
                          from zero as preconditioner (Alg. 5; "kMG", with schedule 1 "kvMG") */
-  double coarse_rtol; /* coarse CG relative tolerance, default 1e-8 (reading R11) */
+  double coarse_rtol; /* coarse CG relative tolerance, default 1e-4 (reading R11) */
   int coarse_maxit;   /* coarse CG iteration cap, default 10000 */
   int coarse_check;   /* coarse CG: host convergence poll every this many iterations, default 8 */
   int coarse_solver;  /* preconditioner of the coarse CG: 1 = Jacobi (reading R11), 2 = h-multigrid

@@ -67,7 +67,7 @@ def pcg(level, b, rtol, maxit):
 
 
 class Hierarchy:
-    def __init__(self, k, widths, p, lam, p0=2, pw=7, schedule=0, coarse_rtol=1e-8,
+    def __init__(self, k, widths, p, lam, p0=2, pw=7, schedule=0, coarse_rtol=1e-4,
                  coarse_maxit=10000, neumann=0, coarse_solver="auto"):
         """neumann: face bitmask of homogeneous Neumann faces (Mesh; NEXT-3).
         coarse_solver: "jacobi" (Jacobi-PCG, reading R11), "hmg" (CG preconditioned by the

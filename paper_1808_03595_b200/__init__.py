@@ -153,7 +153,7 @@ def default_options():
 class Solver:
     """One pmg context: the level hierarchy for (k, widths, p, lambda) on the current device."""
 
-    def __init__(self, k, widths, p, lam, p0=2, schedule=0, coarse_rtol=1e-8, coarse_maxit=10000,
+    def __init__(self, k, widths, p, lam, p0=2, schedule=0, coarse_rtol=1e-4, coarse_maxit=10000,
                  coarse_check=8, stream=None, rank=0, nranks=1, nccl_id=None, loopback=None, solver=0,
                  neumann=0, coarse_solver=0):
         """solver 0: MG fixpoint iteration (Alg. 4); 1: Krylov-accelerated MG (ipCG, Alg. 5).

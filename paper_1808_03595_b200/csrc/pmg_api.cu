@@ -699,7 +699,7 @@ void pmg_default_options(pmg_options* o) {
   o->schedule = 0;
   o->solver = 0;
   o->neumann = 0;
-  o->coarse_rtol = 1e-8;
+  o->coarse_rtol = 1e-4;
   o->coarse_maxit = 10000;
   o->coarse_check = 8;
   o->coarse_solver = 0;
