@@ -18,6 +18,7 @@ import numpy as np
 from .mesh import Mesh
 from .condensed import CondensedOperator
 from .smoother import StarSmoother
+from .ecsmoother import ECSmoother
 from .transfer import Transfer
 
 
@@ -29,10 +30,13 @@ def level_degrees(p, p0=2):
 
 
 class Level:
-    def __init__(self, k, widths, p, lam, pw, neumann=0):
+    def __init__(self, k, widths, p, lam, pw, neumann=0, smoother="star"):
+        """smoother: "star" (vertex stars, Alg. 2) or "element" (element-centred blocks, NEXT-4)."""
         self.mesh = Mesh(k, widths, p, neumann=neumann)
         self.op = CondensedOperator(self.mesh, lam)
-        self.smoother = StarSmoother(self.op, pw)
+        if smoother not in ("star", "element"):
+            raise ValueError("smoother must be 'star' or 'element'")
+        self.smoother = StarSmoother(self.op, pw) if smoother == "star" else ECSmoother(self.op, pw)
         d = self.op.diag()
         self.dinv = np.where(self.mesh.free_skel, 1.0 / np.where(d != 0, d, 1.0), 0.0)
 
@@ -68,14 +72,15 @@ def pcg(level, b, rtol, maxit):
 
 class Hierarchy:
     def __init__(self, k, widths, p, lam, p0=2, pw=7, schedule=0, coarse_rtol=1e-4,
-                 coarse_maxit=10000, neumann=0, coarse_solver="auto"):
+                 coarse_maxit=10000, neumann=0, coarse_solver="auto", smoother="star"):
         """neumann: face bitmask of homogeneous Neumann faces (Mesh; NEXT-3).
         coarse_solver: "jacobi" (Jacobi-PCG, reading R11), "hmg" (CG preconditioned by the
         h-multigrid V-cycle of oracle/hmg.py, reading R16) or "auto" (hmg iff more than 12288
         elements, some k_d halvable and lambda L_min^2 < 100 -- the rule the GPU library uses)."""
         self.degrees = level_degrees(p, p0)
         self.L = len(self.degrees) - 1
-        self.levels = [Level(k, widths, q, lam, pw, neumann) for q in self.degrees]
+        self.levels = [Level(k, widths, q, lam, pw, neumann, smoother if l > 0 else "star")
+                       for l, q in enumerate(self.degrees)]
         self.transfers = [None] + [Transfer(self.levels[l - 1].mesh, self.levels[l].mesh)
                                    for l in range(1, self.L + 1)]
         self.schedule = schedule
