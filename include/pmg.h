@@ -66,6 +66,10 @@ typedef struct {
   int solver;         /* pmg_solve: 0 = multigrid fixpoint iteration (Alg. 4, "MG");
                          1 = Krylov-accelerated multigrid, inexact preconditioned CG with one V-cycle
                          from zero as preconditioner (Alg. 5; "kMG", with schedule 1 "kvMG") */
+  int smoother;       /* 0 = vertex-star additive Schwarz (Alg. 2) (default); 1 = element-centred
+                         3 x 3 x 3 block smoother (six face planes per block,
+                         n_S = 3p - 1, weights of reading R17), 27 colours; one GPU only (nranks = 1) and
+                         p <= 16 (else PMG_EINVAL) */
   double coarse_rtol; /* coarse CG relative tolerance, default 1e-4 (reading R11) */
   int coarse_maxit;   /* coarse CG iteration cap, default 10000 */
   int coarse_check;   /* coarse CG: host convergence poll every this many iterations, default 8 */

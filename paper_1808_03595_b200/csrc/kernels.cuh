@@ -108,6 +108,12 @@ __global__ void k_dot_fused(const double* a, const double* b, long long n, doubl
 cudaError_t launch_prolong(const LevelGeom& gf, const LevelGeom& gc, const double* Jint, const double* uc, double* uf,
                            int nt, size_t smem, cudaStream_t st);
 cudaError_t transfer_set_smem_attr(int bytes);
+
+// element-centred block smoother (ec_smoother.cu)
+size_t ec_smem(int p);
+cudaError_t ec_set_smem_attr(int bytes);
+void launch_ec(const LevelGeom& g, int c1, int c2, int c3, const double* r, double* u, const double* ectab,
+               double lam, cudaStream_t st);
 cudaError_t launch_condense_elem(int nb, int nt, size_t sm, cudaStream_t st, const LevelGeom& g, const double* Fg,
                                  const double* etab, double lam, double* Yc, double* cube_g);
 cudaError_t launch_recover_elem(int nb, int nt, size_t sm, cudaStream_t st, const LevelGeom& g, const double* Fg,

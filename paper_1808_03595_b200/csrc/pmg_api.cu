@@ -39,6 +39,7 @@ struct DevLevel {
   double* etab = nullptr;
   double* stab = nullptr;
   double* stabT = nullptr;
+  double* ectab = nullptr;   // element-centred smoother tables (opt.smoother == 1)
   double* Jint = nullptr;
   double* u = nullptr;
   double* f = nullptr;
@@ -208,6 +209,13 @@ pmg_status smooth_dev(pmg_ctx* c, int l, const double* r, double* u) {
   const DevLevel& D = c->D[l];
   const LevelGeom& g = D.g;
   TimedRegion tr(c, 0, l == c->L);
+  if (c->opt.smoother == 1) {   // element-centred blocks (NEXT-4): 27 colours, element index mod 3
+    for (int col = 0; col < 27; ++col) {
+      launch_ec(g, col % 3, (col / 3) % 3, col / 9, r, u, D.ectab, c->lam, c->st);
+      LAUNCH_CHECK(c);
+    }
+    return PMG_OK;
+  }
   size_t sm = star_smem(g.p, c->star_s_smem);
   for (int col = 0; col < 8; ++col) {   // 8 vertex colours (parity), race-free
     // the z parity is that of the GLOBAL vertex plane, so a z-slab adds the colour corrections
@@ -646,7 +654,8 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
 void free_ctx(pmg_ctx* c) {
   if (!c) return;
   for (auto& D : c->D) {
-    cudaFree(D.etab); cudaFree(D.stab); cudaFree(D.Jint); cudaFree(D.u); cudaFree(D.f); cudaFree(D.r);
+    cudaFree(D.etab); cudaFree(D.stab); cudaFree(D.stabT); cudaFree(D.ectab); cudaFree(D.Jint);
+    cudaFree(D.u); cudaFree(D.f); cudaFree(D.r);
   }
   cudaFree(c->ticket);
   cudaFree(c->Y); cudaFree(c->Z); cudaFree(c->cube); cudaFree(c->part); cudaFree(c->dres); cudaFree(c->pcg);
@@ -703,6 +712,7 @@ void pmg_default_options(pmg_options* o) {
   o->coarse_maxit = 10000;
   o->coarse_check = 8;
   o->coarse_solver = 0;
+  o->smoother = 0;
   o->rank = 0;
   o->nranks = 1;
   o->nccl_id = nullptr;
@@ -739,6 +749,9 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   if (o.nranks > 1 && n_e[2] < o.nranks) return fail(PMG_EINVAL, "z-slabs: k3 >= nranks required");
   if (o.nranks > 1 && o.p0 != 2) return fail(PMG_EINVAL, "z-slabs: the replicated coarse CG needs p0 = 2");
   if (!(o.coarse_rtol > 0.0) || o.coarse_maxit < 1) return fail(PMG_EINVAL, "coarse_rtol > 0 and coarse_maxit >= 1 required");
+  if (o.smoother != 0 && o.smoother != 1) return fail(PMG_EINVAL, "smoother must be 0 (vertex stars) or 1 (element-centred blocks)");
+  if (o.smoother == 1 && o.nranks > 1) return fail(PMG_EINVAL, "the element-centred smoother runs on one GPU (nranks = 1)");
+  if (o.smoother == 1 && p > 16) return fail(PMG_EINVAL, "the element-centred smoother supports p <= 16");
 
   pmg_ctx* c = new (std::nothrow) pmg_ctx();
   if (!c) return fail(PMG_ENOMEM, "host allocation failed");
@@ -763,6 +776,10 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
     std::string err = build_level(c->H[l], deg[l], n_e, widths, lambda, o.weight_degree, o.neumann);
     if (!err.empty()) { free_ctx(c); return fail(PMG_EINVAL, err); }
     if (l >= 1) build_interp(c->H[l], deg[l - 1]);
+    if (l >= 1 && o.smoother == 1) {
+      err = build_ec_tables(c->H[l], n_e, widths, o.neumann);
+      if (!err.empty()) { free_ctx(c); return fail(PMG_EINVAL, err); }
+    }
   }
   std::vector<double> diag;
   coarse_diag(c->H[0], lambda, diag);
@@ -808,6 +825,7 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
     max_elem = std::max(max_elem, hot_smem(D.g.p, 0));
     max_star = std::max(max_star, hot_smem(D.g.p, 1));
     if (l >= 1 && (s = upload(&D.Jint, c->H[l].Jint))) { free_ctx(c); return s; }
+    if (l >= 1 && o.smoother == 1 && (s = upload(&D.ectab, c->H[l].ectab))) { free_ctx(c); return s; }
     if (dalloc(&D.u, D.g.nskel) || dalloc(&D.f, D.g.nskel) || dalloc(&D.r, D.g.nskel)) { free_ctx(c); return fail(PMG_ENOMEM, "cudaMalloc failed (level vectors)"); }
     cudaMemset(D.u, 0, D.g.nskel * sizeof(double));
     cudaMemset(D.f, 0, D.g.nskel * sizeof(double));
@@ -897,6 +915,10 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   cudaError_t e2 = cudaFuncSetAttribute(k_star, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
   cudaError_t e3 = transfer_set_smem_attr(smem_optin);
   cudaError_t e4 = cudaSuccess;
+  if (o.smoother == 1) {
+    if (ec_smem(p) > (size_t)smem_optin) { free_ctx(c); return fail(PMG_EINVAL, "element-centred smoother: shared memory exceeds the device limit"); }
+    e4 = ec_set_smem_attr(smem_optin);
+  }
   cudaError_t e5 = condense_recover_set_smem_attr(smem_optin);
   cudaError_t e6 = cudaSuccess;
   if (e6 == cudaSuccess) e6 = hot_set_smem_attr(smem_optin);

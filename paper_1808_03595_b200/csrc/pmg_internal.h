@@ -65,12 +65,23 @@ PMG_HD inline int et_K(int p) { int m = p - 1; return 3 * m + 2 * m * m + p + 1;
 //   [.., +n)   w[j]  weight polynomial at star point j (1 at the vertex)
 PMG_HD inline int star_table_stride(int p) { int n = 2 * p - 1; return n * n + 3 * n; }
 
+// Element-centred block table, per direction d and element line
+// e_d, n3 = 3p - 1 (three elements, outer block ends dropped), planes at c_lo = p - 1, c_hi = 2p - 1:
+//   [0, n3^2)   S[j][a]   (padded generalised eigenvectors of the assembled 1-D block, S^T M S = I)
+//   [.., +n3)   Lambda[a] (padded with 1 at decoupled points)
+//   [.., +n3)   S[c_lo][a]
+//   [.., +n3)   S[c_hi][a]
+//   [.., +n3)   omega[j]  (1-D weight, reading R17)
+PMG_HD inline int ec_n(int p) { return 3 * p - 1; }
+PMG_HD inline int ec_table_stride(int p) { int n = 3 * p - 1; return n * n + 4 * n; }
+
 struct HostLevel {
   int p;
   LevelGeom g;
   std::vector<double> etab;      // (k1 + k2 + k3) * ET
   std::vector<double> stab;      // (V1 + V2 + V3) * ST
   std::vector<double> stabT;     // (V1 + V2 + V3) * n^2: S^T of each star table row
+  std::vector<double> ectab;     // (k1 + k2 + k3) * ec_table_stride(p) (element-centred smoother only)
   std::vector<double> Jint;      // (p - 1) x (p_c + 1): rows 1..p-1 of J (coarse -> this level)
   std::vector<double> coords[3];
 };
@@ -79,6 +90,8 @@ struct HostLevel {
 std::string build_level(HostLevel& L, int p, const int k[3], const double* const widths[3],
                         double lambda, int weight_degree, int neumann = 0);
 std::string build_interp(HostLevel& fine, int p_coarse);
+// element-centred block tables (fills L.ectab; L built by build_level with the same k, widths)
+std::string build_ec_tables(HostLevel& L, const int k[3], const double* const widths[3], int neumann);
 // diag(H_hat) for the given level in skeleton record layout (free entries only, others 0).
 std::string coarse_diag(const HostLevel& L, double lambda, std::vector<double>& diag);
 // p = 2 coarse CG operator tables (coarse_cg.cu)

@@ -269,6 +269,80 @@ std::string build_level(HostLevel& L, int p, const int k[3], const double* const
   return "";
 }
 
+// Element-centred block tables (oracle/ecsmoother.py): per direction
+// and element line e the 1-D mass / stiffness of the elements e-1, e, e+1 (those in the mesh)
+// assembled on the n3 = 3p - 1 block points (outer ends dropped), identity-padded at the
+// points outside the domain or on a Dirichlet end, and their generalised eigenpairs; the rows of
+// S at the centre element's faces; the 1-D weight of reading R17:
+//   omega_e = 1/2 [(1 + [e = 0]) w_{X_e} + (1 + [e = k-1]) w_{X_{e+1}}],
+// w_V(x) = w(reference distance from V) on the two elements adjoining V.
+std::string build_ec_tables(HostLevel& L, const int k[3], const double* const widths[3], int neumann) {
+  const int p = L.p, n = ec_n(p), q = p + 1, ES = ec_table_stride(p);
+  const int clo = p - 1, chi = 2 * p - 1;
+  if (p > 16) return "element-centred smoother: level degree p must be <= 16";
+  std::vector<double> xi, wq;
+  gll(p, xi, wq);
+  std::vector<double> Kh = ref_stiffness(p, xi, wq);
+  L.ectab.assign((size_t)(k[0] + k[1] + k[2]) * ES, 0.0);
+  size_t base = 0;
+  for (int d = 0; d < 3; ++d)
+    for (int e = 0; e < k[d]; ++e, ++base) {
+      double* T = &L.ectab[base * ES];
+      std::vector<double> M(n, 0.0), K(n * n, 0.0);
+      for (int side = 0; side < 3; ++side) {
+        const int el = e - 1 + side;
+        if (el < 0 || el >= k[d]) continue;
+        const double h = widths[d][el];
+        for (int t = 0; t <= p; ++t) {
+          const int j = side * p - 1 + t;
+          if (j < 0 || j >= n) continue;
+          M[j] += 0.5 * h * wq[t];
+          for (int s = 0; s <= p; ++s) {
+            const int i = side * p - 1 + s;
+            if (i >= 0 && i < n) K[j * n + i] += (2.0 / h) * Kh[t * q + s];
+          }
+        }
+      }
+      std::vector<int> cpl;
+      for (int j = 0; j < n; ++j) {
+        const long long gg = (long long)(e - 1) * p + 1 + j;
+        if (free_1d((int)gg, k[d] * p, (neumann >> (2 * d)) & 1, (neumann >> (2 * d + 1)) & 1)) cpl.push_back(j);
+      }
+      const int nc = (int)cpl.size();
+      std::vector<double> S(n * n, 0.0), lamv(n, 1.0);
+      for (int j = 0; j < n; ++j) S[j * n + j] = 1.0;
+      if (nc > 0) {
+        std::vector<double> Kc(nc * nc), Mc(nc), Sc, lc;
+        for (int a = 0; a < nc; ++a) {
+          Mc[a] = M[cpl[a]];
+          for (int b = 0; b < nc; ++b) Kc[a * nc + b] = K[cpl[a] * n + cpl[b]];
+        }
+        gen_eig_diagM(nc, Kc, Mc, Sc, lc);
+        for (int a = 0; a < nc; ++a) S[cpl[a] * n + cpl[a]] = 0.0;
+        for (int a = 0; a < nc; ++a)
+          for (int b = 0; b < nc; ++b) S[cpl[a] * n + cpl[b]] = Sc[a * nc + b];
+        for (int b = 0; b < nc; ++b) lamv[cpl[b]] = lc[b];
+      }
+      for (int i = 0; i < n * n; ++i) T[i] = S[i];
+      for (int a = 0; a < n; ++a) {
+        T[n * n + a] = lamv[a];
+        T[n * n + n + a] = S[clo * n + a];
+        T[n * n + 2 * n + a] = S[chi * n + a];
+      }
+      const double mlo = (e == 0) ? 2.0 : 1.0, mhi = (e == k[d] - 1) ? 2.0 : 1.0;
+      for (int j = 0; j < n; ++j) {
+        const int side = (j + 1) / p, t = (j + 1) - side * p;   // element e - 1 + side, local node t
+        const double u = 0.5 * (xi[t] + 1.0);                    // reference position in that element
+        double wlo = 0.0, whi = 0.0;                             // w_{X_e}, w_{X_{e+1}}
+        if (side == 0) wlo = weight7(1.0 - u);
+        else if (side == 1) { wlo = weight7(u); whi = weight7(1.0 - u); }
+        else whi = weight7(u);
+        T[n * n + 3 * n + j] = 0.5 * (mlo * wlo + mhi * whi);
+      }
+    }
+  return "";
+}
+
 std::string build_interp(HostLevel& fine, int pc) {
   int pf = fine.p;
   std::vector<double> xc, wc, xf, wf;

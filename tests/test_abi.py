@@ -61,3 +61,20 @@ def test_setup_rejects_bad_arguments_before_touching_the_gpu():
         st = lib.pmg_setup(ctypes.byref(h), ne, wp, p, lam, None)
         assert st == pmg.PMG_EINVAL and not h.value, (k, p, lam, st)
         assert lib.pmg_last_error()
+
+
+def test_smoother_option_validated_before_touching_the_gpu():
+    """smoother: 0 vertex stars (default), 1 element-centred blocks (NEXT-4): p <= 16, one rank."""
+    import numpy as np
+    import paper_1808_03595_b200 as pmg
+    lib = pmg._lib
+    assert pmg.default_options().smoother == 0
+    ws = [np.ones(2)] * 3
+    ne = (ctypes.c_int * 3)(2, 2, 2)
+    wp = (ctypes.POINTER(ctypes.c_double) * 3)(*[x.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) for x in ws])
+    for p, sm, nranks in [(4, 2, 1), (4, -1, 1), (20, 1, 1), (4, 1, 2)]:
+        o = pmg.default_options()
+        o.smoother, o.nranks = sm, nranks
+        h = ctypes.c_void_p()
+        assert lib.pmg_setup(ctypes.byref(h), ne, wp, p, 0.0, ctypes.byref(o)) == pmg.PMG_EINVAL
+        assert not h.value and b"smoother" in lib.pmg_last_error()
