@@ -17,9 +17,10 @@
 // indices mod 3 per direction): the points of one colour are disjoint and the read-modify-write
 // of u_hat is race-free (the star's 8-colouring argument, A.3, with stride 3).
 //
-// One CTA of 256 threads per block; planes and workspace in shared memory (12 n3^2 doubles,
-// 212 KB at p = 16, the supported maximum); the 1-D eigenvector matrices are read from the
-// L2-resident table.  Runtime degree: this is the NEXT-4 smoother, correctness first.
+// One CTA of 512 threads per block; planes and workspace in shared memory (12 n3^2 doubles,
+// 212 KB at p = 16, the supported maximum); the three 1-D eigenvector matrices are staged in
+// shared memory too when they fit (p <= 14), else read from the L2-resident table.  Degree-templated
+// (2 <= p <= 16): every loop fully unrolled with compile-time strides.
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
@@ -28,24 +29,45 @@
 namespace pmg {
 namespace {
 
-constexpr int kEcThreads = 256;
+constexpr int kEcThreads = 1024;
 
 // plane d: slow / fast in-plane directions (same orientation as the star planes)
 __device__ __forceinline__ int ec_slow(int d) { return d == 2 ? 1 : 2; }
 __device__ __forceinline__ int ec_fast(int d) { return d == 0 ? 1 : 0; }
 
+// 1 / x: MUFU approximation + two Newton steps (the star kernels' reciprocal)
+__device__ __forceinline__ double ec_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// sum_k x[k * SX] y[k * SY], k < N, four independent partial sums (k ascending within each)
+template <int N, int SX, int SY>
+__device__ __forceinline__ double ec_dot(const double* x, const double* y) {
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < N; ++k) s[k & 3] = fma(x[k * SX], y[k * SY], s[k & 3]);
+  return (s[0] + s[1]) + (s[2] + s[3]);
+}
+
+template <int P>
 __global__ void __launch_bounds__(kEcThreads) k_ec_block(LevelGeom g, int c1, int c2, int c3, int n1, int n2,
                                                        const double* __restrict__ r, double* __restrict__ u,
-                                                       const double* __restrict__ ectab, double lam) {
+                                                       const double* __restrict__ ectab, double lam, int stage_s) {
   extern __shared__ double sm[];
-  const int p = g.p, n = ec_n(p), nn = n * n, ES = ec_table_stride(p);
-  const int clo = p - 1, chi = 2 * p - 1;
+  constexpr int p = P, n = 3 * P - 1, nn = n * n, ES = n * n + 4 * n;
+  constexpr int clo = p - 1, chi = 2 * p - 1;
   const int b = blockIdx.x, i1 = b % n1, rest = b / n1, i2 = rest % n2, i3 = rest / n2;
   const int e[3] = {c1 + 3 * i1, c2 + 3 * i2, c3 + 3 * i3};
   const int tid = threadIdx.x;
   double* F = sm;                  // 6 planes (d, s): index (2d + s) * nn + A * n + B
   double* G = sm + 6 * nn;         // 6 planes workspace
   double* vec = sm + 12 * nn;      // per direction: Lambda, s_lo, s_hi, omega (4n each)
+  double* Ssm = vec + 12 * n;      // S_d staged (stage_s), 3 nn
   const double* S[3];
   for (int d = 0; d < 3; ++d) {
     const int row = (d == 0 ? 0 : (d == 1 ? g.k1 : g.k1 + g.k2)) + e[d];
@@ -55,6 +77,17 @@ __global__ void __launch_bounds__(kEcThreads) k_ec_block(LevelGeom g, int c1, in
     const int d = i / (4 * n), o = i - d * 4 * n;
     vec[i] = __ldg(&S[d][nn + o]);
   }
+  // S_d staged in shared memory when the three fit next to the planes (p <= 14): the transforms
+  // then address it as Ssm + d nn (shared loads); otherwise straight from the L2-resident table
+  constexpr bool STAGE = (15 * nn + 12 * n) * 8 <= 227 * 1024;
+  (void)stage_s;
+  if (STAGE) {
+    for (int i = tid; i < 3 * nn; i += kEcThreads) {
+      const int d = i / nn;
+      Ssm[i] = __ldg(&S[d][i - d * nn]);
+    }
+  }
+  auto Smat = [&](int d) -> const double* { return STAGE ? Ssm + d * nn : S[d]; };
   pdl_wait();
   pdl_trigger();
   // 1. gather
@@ -69,7 +102,7 @@ __global__ void __launch_bounds__(kEcThreads) k_ec_block(LevelGeom g, int c1, in
     double v = 0.0;
     if (is_free(g, g1, g2, g3)) {
       const int np = 1 + (A == clo || A == chi) + (B == clo || B == chi);
-      v = __ldg(&r[skel_index(g, g1, g2, g3)]) / (double)np;
+      v = __ldg(&r[skel_index_t<P>(g, g1, g2, g3)]) / (double)np;
     }
     F[i] = v;
   }
@@ -77,42 +110,73 @@ __global__ void __launch_bounds__(kEcThreads) k_ec_block(LevelGeom g, int c1, in
   // 2. forward transforms: X = F S_fast (into G), T = S_slow^T X (into F)
   for (int i = tid; i < 6 * nn; i += kEcThreads) {
     const int pl = i / nn, rr = i - pl * nn, A = rr / n, bb = rr - A * n;
-    const double* Sf = S[ec_fast(pl >> 1)];
-    const double* Fr = F + pl * nn + A * n;
-    double s = 0.0;
-    for (int B = 0; B < n; ++B) s = fma(Fr[B], __ldg(&Sf[B * n + bb]), s);
-    G[i] = s;
+    G[i] = ec_dot<n, 1, n>(F + pl * nn + A * n, Smat(ec_fast(pl >> 1)) + bb);
   }
   __syncthreads();
   for (int i = tid; i < 6 * nn; i += kEcThreads) {
     const int pl = i / nn, rr = i - pl * nn, a = rr / n, bb = rr - a * n;
-    const double* Ss = S[ec_slow(pl >> 1)];
-    const double* X = G + pl * nn + bb;
-    double s = 0.0;
-    for (int A = 0; A < n; ++A) s = fma(__ldg(&Ss[A * n + a]), X[A * n], s);
-    F[i] = s;
+    F[i] = ec_dot<n, n, n>(Smat(ec_slow(pl >> 1)) + a, G + pl * nn + bb);
   }
   __syncthreads();
-  // 3. core, one pass per normal direction d: thread owns (a_slow, a_fast), loops over a_d
-  const double* Lv[3] = {vec, vec + 4 * n, vec + 8 * n};
+  // 3. core, one pass per normal direction d: the thread owns the (a_slow, a_fast) pair of plane d
+  //    and loops over a_d.  T_{q,s} is indexed [a_slow(q)][a_fast(q)]:
+  //    q = 0: [a3][a2], q = 1: [a3][a1], q = 2: [a2][a1].
+  const double *L1 = vec, *L2 = vec + 4 * n, *L3 = vec + 8 * n;   // Lambda, then s_lo at +n, s_hi at +2n
+  const double *T0 = F, *T1 = F + nn, *T2 = F + 2 * nn, *T3 = F + 3 * nn, *T4 = F + 4 * nn, *T5 = F + 5 * nn;
   for (int i = tid; i < 3 * nn; i += kEcThreads) {
     const int d = i / nn, rr = i - d * nn, as = rr / n, af = rr - as * n;
-    int a[3];
-    a[ec_slow(d)] = as;
-    a[ec_fast(d)] = af;
     double glo = 0.0, ghi = 0.0;
-    for (int ad = 0; ad < n; ++ad) {
-      a[d] = ad;
-      double E = 0.0;
+    if (d == 0) {                  // (a3, a2) fixed, a1 runs
+      const int a3 = as, a2 = af;
+      const double t0 = T0[a3 * n + a2], t1 = T1[a3 * n + a2];
+      const double base = lam + L2[a2] + L3[a3];
+      const double c2l = L2[n + a2], c2h = L2[2 * n + a2], c3l = L3[n + a3], c3h = L3[2 * n + a3];
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const int idx = a[ec_slow(q)] * n + a[ec_fast(q)];
-        E = fma(Lv[q][n + a[q]], F[(2 * q) * nn + idx], E);
-        E = fma(Lv[q][2 * n + a[q]], F[(2 * q + 1) * nn + idx], E);
+      for (int a1 = 0; a1 < n; ++a1) {
+        double E = L1[n + a1] * t0;
+        E = fma(L1[2 * n + a1], t1, E);
+        E = fma(c2l, T2[a3 * n + a1], E);
+        E = fma(c2h, T3[a3 * n + a1], E);
+        E = fma(c3l, T4[a2 * n + a1], E);
+        E = fma(c3h, T5[a2 * n + a1], E);
+        const double V = E * ec_rcp(base + L1[a1]);
+        glo = fma(L1[n + a1], V, glo);
+        ghi = fma(L1[2 * n + a1], V, ghi);
       }
-      const double V = E / (lam + Lv[0][a[0]] + Lv[1][a[1]] + Lv[2][a[2]]);
-      glo = fma(Lv[d][n + ad], V, glo);
-      ghi = fma(Lv[d][2 * n + ad], V, ghi);
+    } else if (d == 1) {           // (a3, a1) fixed, a2 runs
+      const int a3 = as, a1 = af;
+      const double t2 = T2[a3 * n + a1], t3 = T3[a3 * n + a1];
+      const double base = lam + L1[a1] + L3[a3];
+      const double c1l = L1[n + a1], c1h = L1[2 * n + a1], c3l = L3[n + a3], c3h = L3[2 * n + a3];
+#pragma unroll
+      for (int a2 = 0; a2 < n; ++a2) {
+        double E = c1l * T0[a3 * n + a2];
+        E = fma(c1h, T1[a3 * n + a2], E);
+        E = fma(L2[n + a2], t2, E);
+        E = fma(L2[2 * n + a2], t3, E);
+        E = fma(c3l, T4[a2 * n + a1], E);
+        E = fma(c3h, T5[a2 * n + a1], E);
+        const double V = E * ec_rcp(base + L2[a2]);
+        glo = fma(L2[n + a2], V, glo);
+        ghi = fma(L2[2 * n + a2], V, ghi);
+      }
+    } else {                       // (a2, a1) fixed, a3 runs
+      const int a2 = as, a1 = af;
+      const double t4 = T4[a2 * n + a1], t5 = T5[a2 * n + a1];
+      const double base = lam + L1[a1] + L2[a2];
+      const double c1l = L1[n + a1], c1h = L1[2 * n + a1], c2l = L2[n + a2], c2h = L2[2 * n + a2];
+#pragma unroll
+      for (int a3 = 0; a3 < n; ++a3) {
+        double E = c1l * T0[a3 * n + a2];
+        E = fma(c1h, T1[a3 * n + a2], E);
+        E = fma(c2l, T2[a3 * n + a1], E);
+        E = fma(c2h, T3[a3 * n + a1], E);
+        E = fma(L3[n + a3], t4, E);
+        E = fma(L3[2 * n + a3], t5, E);
+        const double V = E * ec_rcp(base + L3[a3]);
+        glo = fma(L3[n + a3], V, glo);
+        ghi = fma(L3[2 * n + a3], V, ghi);
+      }
     }
     G[(2 * d) * nn + rr] = glo;
     G[(2 * d + 1) * nn + rr] = ghi;
@@ -121,20 +185,12 @@ __global__ void __launch_bounds__(kEcThreads) k_ec_block(LevelGeom g, int c1, in
   // 4. back transforms: X = G S_fast^T (into F), U = S_slow X (into G)
   for (int i = tid; i < 6 * nn; i += kEcThreads) {
     const int pl = i / nn, rr = i - pl * nn, a = rr / n, B = rr - a * n;
-    const double* Sf = S[ec_fast(pl >> 1)];
-    const double* Gr = G + pl * nn + a * n;
-    double s = 0.0;
-    for (int bb = 0; bb < n; ++bb) s = fma(Gr[bb], __ldg(&Sf[B * n + bb]), s);
-    F[i] = s;
+    F[i] = ec_dot<n, 1, 1>(G + pl * nn + a * n, Smat(ec_fast(pl >> 1)) + B * n);
   }
   __syncthreads();
   for (int i = tid; i < 6 * nn; i += kEcThreads) {
     const int pl = i / nn, rr = i - pl * nn, A = rr / n, B = rr - A * n;
-    const double* Ss = S[ec_slow(pl >> 1)];
-    const double* X = F + pl * nn + B;
-    double s = 0.0;
-    for (int a = 0; a < n; ++a) s = fma(__ldg(&Ss[A * n + a]), X[a * n], s);
-    G[i] = s;
+    G[i] = ec_dot<n, 1, n>(Smat(ec_slow(pl >> 1)) + A * n, F + pl * nn + B);
   }
   __syncthreads();
   // 5. weighted scatter-add: a point on several planes is written by the lowest (d, s) plane
@@ -149,21 +205,30 @@ __global__ void __launch_bounds__(kEcThreads) k_ec_block(LevelGeom g, int c1, in
     if (dup) continue;
     const int g1 = o[0] + j[0], g2 = o[1] + j[1], g3 = o[2] + j[2];
     if (!is_free(g, g1, g2, g3)) continue;
-    const double w = Lv[0][3 * n + j[0]] * Lv[1][3 * n + j[1]] * Lv[2][3 * n + j[2]];
-    const long long idx = skel_index(g, g1, g2, g3);
+    const double w = vec[3 * n + j[0]] * vec[7 * n + j[1]] * vec[11 * n + j[2]];
+    const long long idx = skel_index_t<P>(g, g1, g2, g3);
     u[idx] = fma(w, G[i], u[idx]);
   }
 }
 
 }  // namespace
 
-size_t ec_smem(int p) {
+size_t ec_smem(int p) {   // planes + workspace + vectors (the minimum; S staged when it fits)
   const int n = ec_n(p);
   return sizeof(double) * (size_t)(12 * n * n + 12 * n);
 }
 
+
+#define PMG_EC_DEGREES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
+
 cudaError_t ec_set_smem_attr(int bytes) {
-  return cudaFuncSetAttribute(k_ec_block, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaError_t e = cudaSuccess, a;
+#define PMG_EC_ATTR(P) \
+  a = cudaFuncSetAttribute(k_ec_block<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+  if (a != cudaSuccess) e = a;
+  PMG_EC_DEGREES(PMG_EC_ATTR)
+#undef PMG_EC_ATTR
+  return e;
 }
 
 // one colour (c1, c2, c3) in {0,1,2}^3 of the element-centred sweep
@@ -172,7 +237,19 @@ void launch_ec(const LevelGeom& g, int c1, int c2, int c3, const double* r, doub
   const int n1 = (g.k1 - c1 + 2) / 3, n2 = (g.k2 - c2 + 2) / 3, n3 = (g.k3 - c3 + 2) / 3;
   const long long nb = (long long)n1 * n2 * n3;
   if (nb <= 0) return;
-  launch_pdl(k_ec_block, dim3((unsigned)nb), dim3(kEcThreads), ec_smem(g.p), st, g, c1, c2, c3, n1, n2, r, u, ectab, lam);
+  const int n = ec_n(g.p);
+  const size_t staged = ec_smem(g.p) + sizeof(double) * (size_t)(3 * n * n);
+  const int stage = (15 * n * n + 12 * n) * 8 <= 227 * 1024 ? 1 : 0;   // as the kernel's STAGE (p <= 14)
+  const size_t smem = stage ? staged : ec_smem(g.p);
+  switch (g.p) {
+#define PMG_EC_CASE(P) \
+  case P: \
+    launch_pdl(k_ec_block<P>, dim3((unsigned)nb), dim3(kEcThreads), smem, st, g, c1, c2, c3, n1, n2, r, u, ectab, lam, stage); \
+    break;
+    PMG_EC_DEGREES(PMG_EC_CASE)
+#undef PMG_EC_CASE
+    default: break;
+  }
 }
 
 }  // namespace pmg

@@ -776,7 +776,7 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
     std::string err = build_level(c->H[l], deg[l], n_e, widths, lambda, o.weight_degree, o.neumann);
     if (!err.empty()) { free_ctx(c); return fail(PMG_EINVAL, err); }
     if (l >= 1) build_interp(c->H[l], deg[l - 1]);
-    if (l >= 1 && o.smoother == 1) {
+    if (o.smoother == 1) {   // every level (pmg_smooth may be called on any level)
       err = build_ec_tables(c->H[l], n_e, widths, o.neumann);
       if (!err.empty()) { free_ctx(c); return fail(PMG_EINVAL, err); }
     }
@@ -825,7 +825,7 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
     max_elem = std::max(max_elem, hot_smem(D.g.p, 0));
     max_star = std::max(max_star, hot_smem(D.g.p, 1));
     if (l >= 1 && (s = upload(&D.Jint, c->H[l].Jint))) { free_ctx(c); return s; }
-    if (l >= 1 && o.smoother == 1 && (s = upload(&D.ectab, c->H[l].ectab))) { free_ctx(c); return s; }
+    if (o.smoother == 1 && (s = upload(&D.ectab, c->H[l].ectab))) { free_ctx(c); return s; }
     if (dalloc(&D.u, D.g.nskel) || dalloc(&D.f, D.g.nskel) || dalloc(&D.r, D.g.nskel)) { free_ctx(c); return fail(PMG_ENOMEM, "cudaMalloc failed (level vectors)"); }
     cudaMemset(D.u, 0, D.g.nskel * sizeof(double));
     cudaMemset(D.f, 0, D.g.nskel * sizeof(double));
