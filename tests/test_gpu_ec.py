@@ -141,3 +141,23 @@ def test_ec_invalid_options():
     hub = pmg.Loopback(2)
     with pytest.raises(pmg.PmgError):
         pmg.Solver((2, 2, 4), w[:2] + [np.ones(4)], 4, 0.0, smoother=1, rank=0, nranks=2, loopback=hub)
+
+
+@pytest.mark.parametrize("p", [4, 8, 13])
+def test_ec_kernel_variants_agree(p, monkeypatch):
+    """The DMMA kernel (p <= 13, default) and the DFMA kernel (PMG_EC_VARIANT=dfma; the only one
+    for p = 14 .. 16) apply the same smoother."""
+    import paper_1808_03595_b200 as pmg
+    case = pi.small_case((4, 3, 3), p, 0.6, stretch=1.3)
+    s = pmg.Solver(case.k, case.widths, p, 0.6, smoother=1)
+    l = s.nlevels - 1
+    r = torch.from_numpy(np.random.default_rng(p).standard_normal(s.level_info(l)[1])).cuda()
+    outs = []
+    for var in ("mma", "dfma"):
+        monkeypatch.setenv("PMG_EC_VARIANT", var)
+        u = s.new_skel(l)
+        s.smooth(l, r, u)
+        torch.cuda.synchronize()
+        outs.append(u.cpu().numpy())
+    s.close()
+    assert rel(outs[0], outs[1]) < 1e-13
