@@ -118,10 +118,10 @@ def n_skel_free(case):
     return full - k[0] * k[1] * k[2] * m ** 3
 
 
-def oracle_solve_timer(case, reps, warm=0):
+def oracle_solve_timer(case, reps, warm=0, smoother="star"):
     """Time full oracle solves (setup excluded) on the host cores; returns (seconds per solve, cycles)."""
     from oracle import condensed, mg
-    H = mg.Hierarchy(case.k, case.widths, case.p, case.lam)
+    H = mg.Hierarchy(case.k, case.widths, case.p, case.lam, smoother=smoother)
     m = H.levels[-1].mesh
     F = condensed.weak_rhs(m, case.f_nodal(m.coords))
     for _ in range(warm):
@@ -183,6 +183,8 @@ def main():
     ap.add_argument("--p", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--smoother", default="star", choices=["star", "element"],
+                    help="vertex stars (Alg. 2, the headline) or element-centred blocks (NEXT-4)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -205,7 +207,8 @@ def main():
             buf.copy_(torch.frombuffer(bytearray(pmg.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(buf, 0)
         nccl_id = bytes(buf.cpu().numpy().tobytes())
-    s = pmg.Solver(case.k, case.widths, case.p, case.lam, rank=rank, nranks=ws, nccl_id=nccl_id)
+    ec = args.smoother == "element"
+    s = pmg.Solver(case.k, case.widths, case.p, case.lam, rank=rank, nranks=ws, nccl_id=nccl_id, smoother=1 if ec else 0)
     L = s.nlevels - 1
     coords = [s.grid_coords(L, d) for d in range(3)]
     f = torch.from_numpy(case.f_nodal(coords, i3_offset=s.slab["z0"] * case.p)).cuda()
@@ -286,18 +289,23 @@ def main():
                "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb}
 
     # roofline of the dominant kernel: the star smoother (finest level), FP64-pipe bound
-    n = 2 * case.p - 1
     sweep_ms = sm_ms / max(sm_n, 1)
-    flops = 37.0 * n ** 3 * n_stars(case) / ws       # Alg. 1 count x stars per sweep (per rank)
+    if ec:   # element-centred blocks: 73 n_S^3 per block, n_S = 3p - 1, one block per element
+        n = 3 * case.p - 1
+        flops = 73.0 * n ** 3 * case.k[0] * case.k[1] * case.k[2] / ws
+    else:
+        n = 2 * case.p - 1
+        flops = 37.0 * n ** 3 * n_stars(case) / ws       # Alg. 1 count x stars per sweep (per rank)
     achieved = flops / (sweep_ms / 1e3) / 1e12
     bytes_alg = 24.0 * n_skel_free(case) / ws        # read r, read+write u, per rank
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", 6541.5)
     tr = load_traffic(case.name)
     traffic = tr.get("k_star_bytes_per_sweep")
-    roof = {"kernel": "k_star (8 colour launches = 1 smoother sweep, finest level)", "bound": "alu",
+    roof = {"kernel": ("k_ec_block_mma (27 colour launches = 1 element-centred sweep, finest level)" if ec else
+                       "k_star (8 colour launches = 1 smoother sweep, finest level)"), "bound": "alu",
             "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
-            "traffic": traffic, "algorithmic_flops_per_sweep": flops, "sweep_ms": sweep_ms,
+            "traffic": None if ec else traffic, "algorithmic_flops_per_sweep": flops, "sweep_ms": sweep_ms,
             "peak_source": "derived: 64 FP64 FMA/clk/SM x 148 SMs x 1.965 GHz (no FP64 entry in MEASURED_PEAKS.json); "
                            "measured DFMA microbenchmark 34.1 TFLOP/s (profiles/r01_step0_fp64_peaks.jsonl)",
             "hbm_view": {"achieved_gbs": bytes_alg / (sweep_ms / 1e3) / 1e9, "peak_gbs": hbm,
@@ -310,7 +318,7 @@ def main():
                 "achieved_gbs_alg": bytes_alg / (res_ms / 1e3) / 1e9}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        ts, cyc = oracle_solve_timer(case, 3)
+        ts, cyc = oracle_solve_timer(case, 3, smoother=args.smoother)
         tcpu = statistics.mean(ts)
         cpu = {"value": case.n_dof / tcpu, "unit": "unknowns/s", "cores": cores(), "kind": "oracle",
                "sample": "3 full oracle solves of %s (setup excluded), %.2f s each, %d cycles" % (case.name, tcpu, cyc)}
@@ -319,7 +327,7 @@ def main():
         "metric": METRIC, "value": value, "unit": "unknowns/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": case.name, "n_dof": case.n_dof, "p": case.p, "k": list(case.k), "lambda": case.lam,
+        "config": {"workload": case.name + ("_element_centred" if ec else ""), "smoother": args.smoother, "n_dof": case.n_dof, "p": case.p, "k": list(case.k), "lambda": case.lam,
                    "rtol": 1e-10, "cycles": r["cycles"], "rho": r["rho"], "coarse_iters": r["coarse_iters"],
                    "l2": "flushed between steps (512 MB write, outside the timed events)",
                    "parallelism": "single GPU" if ws == 1 else
