@@ -621,6 +621,17 @@ __device__ __forceinline__ double csr_row_warp(const int* __restrict__ ptr, cons
   return s;
 }
 
+// one CSR row by one thread (the prolongation rows: at most 26 entries, one coarse element's
+// skeleton; a warp per row would leave most lanes idle and serialise the rows)
+__device__ __forceinline__ double csr_row_thread(const int* __restrict__ ptr, const int* __restrict__ col,
+                                                 const double* __restrict__ val, long long i,
+                                                 const double* __restrict__ v) {
+  double s = 0.0;
+  const int k1 = __ldg(&ptr[i + 1]);
+  for (int k = __ldg(&ptr[i]); k < k1; ++k) s = fma(__ldg(&val[k]), __ldcg(&v[__ldg(&col[k])]), s);
+  return s;
+}
+
 // z = V-cycle(f_0) into h.x[0]; h.f[0] holds the right-hand side
 __device__ void hmg_vcycle(const HmgDev& h, cg::grid_group& grid, long long t0, long long T) {
   const int L = h.nlev - 1;
@@ -673,10 +684,7 @@ __device__ void hmg_vcycle(const HmgDev& h, cg::grid_group& grid, long long t0, 
     const long long n = h.n[l];
     double *x = h.x[l], *r = h.r[l];
     const double *f = h.f[l], *di = h.dinv[l];
-    for (long long i = t0 >> 5; i < n; i += T >> 5) {
-      const double v = csr_row_warp(h.Pptr[l], h.Pcol[l], h.Pval[l], i, h.x[l + 1], (int)(t0 & 31));
-      if ((t0 & 31) == 0) x[i] += v;
-    }
+    for (long long i = t0; i < n; i += T) x[i] += csr_row_thread(h.Pptr[l], h.Pcol[l], h.Pval[l], i, h.x[l + 1]);
     grid.sync();
     for (int s = 0; s < kHmgNu; ++s) {
       for (long long i = t0; i < n; i += T) r[i] = f[i] - ell_row(h.Aval[l], h.Acol[l], n, i, x);
