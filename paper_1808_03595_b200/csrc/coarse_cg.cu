@@ -639,14 +639,22 @@ __device__ void hmg_vcycle(const HmgDev& h, cg::grid_group& grid, long long t0, 
     const long long n = h.n[l];
     double *x = h.x[l], *r = h.r[l];
     const double *f = h.f[l], *di = h.dinv[l];
-    for (long long i = t0; i < n; i += T) x[i] = kHmgOmega * di[i] * f[i];          // first sweep from zero
-    grid.sync();
-    for (int s = 1; s < kHmgNu; ++s) {
-      for (long long i = t0; i < n; i += T) r[i] = f[i] - ell_row(h.Aval[l], h.Acol[l], n, i, x);
-      grid.sync();
-      for (long long i = t0; i < n; i += T) x[i] = fma(kHmgOmega * di[i], r[i], x[i]);
-      grid.sync();
+    // the two pre-sweeps from zero in one pass: x1 = omega D^-1 f is local, so
+    // x2_i = x1_i + omega d_i (f_i - sum_j A_ij x1_j) gathers omega d_j f_j directly
+    static_assert(kHmgNu == 2, "the fused sweeps below are written for nu = 2");
+    for (long long i = t0; i < n; i += T) {
+      const double* val = h.Aval[l];
+      const int* col = h.Acol[l];
+      double ax = 0.0;
+#pragma unroll
+      for (int k = 0; k < kRowLen; ++k) {
+        const int j = __ldg(&col[k * n + i]);
+        ax = fma(__ldg(&val[k * n + i]), kHmgOmega * __ldg(&di[j]) * __ldcg(&f[j]), ax);
+      }
+      const double x1 = kHmgOmega * di[i] * f[i];
+      x[i] = fma(kHmgOmega * di[i], f[i] - ax, x1);
     }
+    grid.sync();
     for (long long i = t0; i < n; i += T) r[i] = f[i] - ell_row(h.Aval[l], h.Acol[l], n, i, x);
     grid.sync();
     const long long nc = h.n[l + 1];
@@ -686,12 +694,11 @@ __device__ void hmg_vcycle(const HmgDev& h, cg::grid_group& grid, long long t0, 
     const double *f = h.f[l], *di = h.dinv[l];
     for (long long i = t0; i < n; i += T) x[i] += csr_row_thread(h.Pptr[l], h.Pcol[l], h.Pval[l], i, h.x[l + 1]);
     grid.sync();
-    for (int s = 0; s < kHmgNu; ++s) {
-      for (long long i = t0; i < n; i += T) r[i] = f[i] - ell_row(h.Aval[l], h.Acol[l], n, i, x);
-      grid.sync();
-      for (long long i = t0; i < n; i += T) x[i] = fma(kHmgOmega * di[i], r[i], x[i]);
-      grid.sync();
-    }
+    // two post-sweeps, each one pass, ping-pong x -> r -> x (r is free here)
+    for (long long i = t0; i < n; i += T) r[i] = fma(kHmgOmega * di[i], f[i] - ell_row(h.Aval[l], h.Acol[l], n, i, x), x[i]);
+    grid.sync();
+    for (long long i = t0; i < n; i += T) x[i] = fma(kHmgOmega * di[i], f[i] - ell_row(h.Aval[l], h.Acol[l], n, i, r), r[i]);
+    grid.sync();
   }
 }
 }  // namespace
