@@ -161,3 +161,23 @@ def test_ec_kernel_variants_agree(p, monkeypatch):
         outs.append(u.cpu().numpy())
     s.close()
     assert rel(outs[0], outs[1]) < 1e-13
+
+
+@pytest.mark.parametrize("k,p", [((1, 1, 1), 4), ((1, 2, 3), 3), ((2, 1, 1), 6)])
+def test_ec_degenerate_meshes(k, p):
+    """One element in some direction: blocks hang over the boundary on both sides (identity padding
+    at both block ends) -- smoother and solve still equal the oracle's."""
+    from oracle import condensed, mg
+    import paper_1808_03595_b200 as pmg
+    case = pi.small_case(k, p, 0.9, stretch=None)
+    orc = mg.Hierarchy(case.k, case.widths, p, case.lam, coarse_rtol=1e-13, smoother="element")
+    m = orc.levels[-1].mesh
+    F = condensed.weak_rhs(m, pi.uniform_pm1(9, np.arange(m.ntot)))
+    u_o, rep_o = orc.solve(F, 1e-10)
+    s = pmg.Solver(case.k, case.widths, p, case.lam, coarse_rtol=1e-13, smoother=1)
+    ug = s.new_grid()
+    rep = s.solve(torch.from_numpy(F).cuda(), ug, 1e-10)
+    torch.cuda.synchronize()
+    assert rep["cycles"] == rep_o["cycles"], (rep["cycles"], rep_o["cycles"])
+    assert rel(ug.cpu().numpy(), u_o) < SOLVE_TOL
+    s.close()

@@ -605,3 +605,22 @@ def test_hmg_auto_on_large_mesh_matches_jacobi():
     assert r0["converged"] and r1["converged"] and r0["cycles"] == r1["cycles"]
     assert np.linalg.norm(u0 - u1) <= 1e-8 * np.linalg.norm(u1)
     assert r0["coarse_iters"] * 5 < r1["coarse_iters"], (r0["coarse_iters"], r1["coarse_iters"])
+
+
+@pytest.mark.parametrize("solver", [0, 1])
+def test_zero_rhs_returns_zero(solver):
+    """Degenerate input: F = 0 gives r0 = 0, no cycle, u = 0 (as the oracle's Alg. 4 loop)."""
+    import paper_1808_03595_b200 as pmg
+    from oracle import mg
+    case = pi.small_case((3, 2, 2), 4, 0.5, stretch=1.2)
+    s = pmg.Solver(case.k, case.widths, 4, 0.5, solver=solver)
+    F = s.new_grid()
+    u = s.new_grid()
+    u.fill_(7.0)
+    rep = s.solve(F, u, 1e-10)
+    torch.cuda.synchronize()
+    orc = mg.Hierarchy(case.k, case.widths, 4, 0.5)
+    u_o, rep_o = orc.solve(np.zeros(F.numel()), 1e-10)
+    assert rep["converged"] and rep["cycles"] == rep_o["cycles"] == 0 and rep["r0"] == 0.0
+    assert float(u.abs().max()) == 0.0 and np.abs(u_o).max() == 0.0
+    s.close()
