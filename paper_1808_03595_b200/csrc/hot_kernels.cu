@@ -1122,7 +1122,10 @@ template <int P> struct StarPfCfg {
   static constexpr int GS = NP, GPW = 32 / GS, NG = NW * GPW, A3IT = (N + NG - 1) / NG;
   static constexpr bool P3SEP = NW * NN > 3 * MS;
   static constexpr int oFT = 0, oX = 3 * MS, oG = 6 * MS, oS = 9 * MS, oU = 12 * MS, oVec = oU + 3 * NN,
-                       oBase = oVec + 9 * N, oP3 = P3SEP ? oBase + 8 : oX, total = P3SEP ? oP3 + NW * NN : oBase + 8;
+                       oBase = oVec + 9 * N, oP3 = P3SEP ? oBase + 8 : oX, endP3 = P3SEP ? oP3 + NW * NN : oBase + 8;
+  // the compile-time point map, copied to shared memory in the prologue (before the dependency
+  // wait): every later map read is a shared load instead of a dependent global round trip
+  static constexpr int oMap = endP3, total = oMap + (3 * NN + 1) / 2;
 };
 
 template <int P>
@@ -1153,7 +1156,8 @@ __global__ void __launch_bounds__(StarPfCfg<P>::NT, StarPfCfg<P>::MINB)
   const long long rec0 = v1 + g.V1 * (long long)v2 + V12 * v3;
   // interior stars (the common case) touch only inside, free points: no per-point tests
   const bool interior = v1 > 0 && v2 > 0 && v3 > 0 && v1 < g.k1 && v2 < g.k2 && v3 + g.zoff < g.K3;
-  const StarMap<P>& map = kStarMap<P>;
+  unsigned* map_s = reinterpret_cast<unsigned*>(sm + C::oMap);
+  for (int i = tid; i < 3 * NN; i += NT) map_s[i] = __ldg(&kStarMap<P>.v[i]);
   // point of map entry e: record coordinate w_d = v_d - bit; free iff (w_d > 0 or t_d > 0) and
   // w_d < k_d (global in z); stored (readable) iff w_d >= 0
   auto pt_free = [&](unsigned e) {   // global test (w3 + zoff is the global record plane), Neumann faces free
@@ -1185,7 +1189,7 @@ __global__ void __launch_bounds__(StarPfCfg<P>::NT, StarPfCfg<P>::MINB)
   pdl_trigger();
   for (int i = tid; i < 3 * NN; i += NT) {
     const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
-    const unsigned e = map.v[i];
+    const unsigned e = map_s[i];
     const long long base = s_base[(e >> 12) & 7u];
     const bool ok = base >= 0;
     cp_async8(&FT[d * MS + A * LD + B], &r[ok ? base + (e & 0xFFFu) : 0], ok);
@@ -1193,7 +1197,7 @@ __global__ void __launch_bounds__(StarPfCfg<P>::NT, StarPfCfg<P>::MINB)
   cp_async_commit();
   // group 1: the u entries this star updates (0 where the point is not free)
   for (int i = tid; i < 3 * NN; i += NT) {
-    const unsigned e = map.v[i];
+    const unsigned e = map_s[i];
     const long long base = s_base[(e >> 12) & 7u];
     const bool ok = base >= 0 && (interior || pt_free(e));
     cp_async8(&Up[i], &u[ok ? base + (e & 0xFFFu) : 0], ok);
@@ -1318,7 +1322,7 @@ __global__ void __launch_bounds__(StarPfCfg<P>::NT, StarPfCfg<P>::MINB)
     if (d == 0) { j1 = c; j2 = B; j3 = A; }
     else if (d == 1) { j2 = c; j1 = B; j3 = A; if (j1 == c) continue; }
     else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
-    const unsigned e = map.v[i];
+    const unsigned e = map_s[i];
     if (!interior && !pt_free(e)) continue;
     u[s_base[(e >> 12) & 7u] + (e & 0xFFFu)] = fma(w1[j1] * w2[j2] * w3[j3], Gs[d * MS + A * LD + B], Up[i]);
   }
@@ -1343,7 +1347,7 @@ template <int P> struct ElemPfCfg {
   static constexpr int ET = (P - 1) + 2 * (P - 1) * (P - 1) + 2 * (P - 1) + (P + 1) + (P + 1) * (P + 1);
   static constexpr int YS = 6 * MM + 12 * M + 8;
   static constexpr int oCube = 0, oTab = QQQ, oPp = oTab + 3 * ET, oA = oPp + 3 * MS, oT = oA + 6 * MS,
-                       oG = oT + 6 * MS, oInv = oG + 6 * MS, total = oInv + MM * M;
+                       oG = oT + 6 * MS, oInv = oG + 6 * MS, oMap = oInv + MM * M, total = oMap + (YS + 1) / 2;
 };
 
 template <int P>
@@ -1393,6 +1397,9 @@ __global__ void __launch_bounds__(ElemPfCfg<P>::NT, ElemPfCfg<P>::MINB)
       const int d = i / ET;
       cp_async8(&tb[i], src[d] + (i - d * ET), true);
     }
+    unsigned* map_s = reinterpret_cast<unsigned*>(sm + C::oMap);   // the point map, before the wait
+    for (int o = tid; o < YS; o += NT) map_s[o] = __ldg(&kElemMap<P>.v[o]);
+    __syncthreads();
     pdl_wait();
   pdl_trigger();
     if (done && *done) return;   // (uniform per block; the issued cp.async only target this block's smem)
@@ -1402,7 +1409,7 @@ __global__ void __launch_bounds__(ElemPfCfg<P>::NT, ElemPfCfg<P>::MINB)
     for (int o = tid; o < YS; o += NT) {
       int t1, t2, t3;
       ys_point<P>(o, t1, t2, t3);
-      const unsigned m_ = kElemMap<P>.v[o];
+      const unsigned m_ = map_s[o];
       cp_async8(&cube[(t3 * Q + t2) * Q + t1], &u[(rec0 + rec_delta(m_, g.V1, V12)) * RS + (m_ & 0xFFFu)], true);
     }
     cp_async_commit();
