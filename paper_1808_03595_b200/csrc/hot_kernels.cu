@@ -1714,7 +1714,7 @@ template <int P> struct StarWCfg {
   static constexpr int SPB = 4, NT = 32 * SPB;                // stars (warps) per block
   static constexpr int GS = 8, GPW = 4, A3IT = (N + GPW - 1) / GPW;
   static constexpr int oFT = 0, oX = 3 * MS, oG = 6 * MS, oS = 9 * MS, oU = 12 * MS, oVec = oU + 3 * NN,
-                       oBase = oVec + 9 * N, per_star = oBase + 8, total = SPB * per_star;
+                       oBase = oVec + 9 * N, per_star = oBase + 8, oMap = SPB * per_star, total = oMap + (3 * NN + 1) / 2;
 };
 
 template <int P>
@@ -1729,6 +1729,10 @@ __global__ void __launch_bounds__(128) k_star_w(LevelGeom g, int c1, int c2, int
   extern __shared__ double smem_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* sm = smem_all + warp * C::per_star;
+  // the point map in shared memory, shared by the block's four stars (before any early exit)
+  unsigned* map_s = reinterpret_cast<unsigned*>(smem_all + C::oMap);
+  for (int i = threadIdx.x; i < 3 * NN; i += C::NT) map_s[i] = __ldg(&kStarMap<P>.v[i]);
+  __syncthreads();
   const long long b = (long long)blockIdx.x * C::SPB + warp;
   if (b >= nstars) return;
   const int i1 = (int)(b % n1c), rest = (int)(b / n1c), i2 = rest % n2c, i3 = rest / n2c;
@@ -1746,7 +1750,6 @@ __global__ void __launch_bounds__(128) k_star_w(LevelGeom g, int c1, int c2, int
   const long long V12 = (long long)g.V1 * g.V2;
   const long long rec0 = v1 + g.V1 * (long long)v2 + V12 * v3;
   const bool interior = v1 > 0 && v2 > 0 && v3 > 0 && v1 < g.k1 && v2 < g.k2 && v3 + g.zoff < g.K3;
-  const StarMap<P>& map = kStarMap<P>;
   auto pt_free = [&](unsigned e) {   // global test (w3 + zoff is the global record plane), Neumann faces free
     const int w1 = v1 - (int)((e >> 12) & 1u), w2 = v2 - (int)((e >> 13) & 1u), w3 = v3 - (int)((e >> 14) & 1u);
     const int W3 = w3 + g.zoff;
@@ -1774,14 +1777,14 @@ __global__ void __launch_bounds__(128) k_star_w(LevelGeom g, int c1, int c2, int
   __syncwarp();
   for (int i = lane; i < 3 * NN; i += 32) {
     const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
-    const unsigned e = map.v[i];
+    const unsigned e = map_s[i];
     const long long base = s_base[(e >> 12) & 7u];
     const bool ok = base >= 0;
     cp_async8(&FT[d * MS + A * LD + B], &r[ok ? base + (e & 0xFFFu) : 0], ok);
   }
   cp_async_commit();
   for (int i = lane; i < 3 * NN; i += 32) {
-    const unsigned e = map.v[i];
+    const unsigned e = map_s[i];
     const long long base = s_base[(e >> 12) & 7u];
     const bool ok = base >= 0 && (interior || pt_free(e));
     cp_async8(&Up[i], &u[ok ? base + (e & 0xFFFu) : 0], ok);
@@ -1885,7 +1888,7 @@ __global__ void __launch_bounds__(128) k_star_w(LevelGeom g, int c1, int c2, int
     if (d == 0) { j1 = c; j2 = B; j3 = A; }
     else if (d == 1) { j2 = c; j1 = B; j3 = A; if (j1 == c) continue; }
     else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
-    const unsigned e = map.v[i];
+    const unsigned e = map_s[i];
     if (!interior && !pt_free(e)) continue;
     u[s_base[(e >> 12) & 7u] + (e & 0xFFFu)] = fma(w1[j1] * w2[j2] * w3[j3], Gs[d * MS + A * LD + B], Up[i]);
   }
@@ -1903,7 +1906,7 @@ template <int P> struct Elem16Cfg {
   static constexpr int ET = (P - 1) + 2 * (P - 1) * (P - 1) + 2 * (P - 1) + (P + 1) + (P + 1) * (P + 1);
   static constexpr int YS = 6 * MM + 12 * M + 8;
   static constexpr int oUc = 0, oTab = 6 * QQ, oPp = oTab + 3 * ET, oA = oPp + 3 * MS, oTG = oA + 6 * MS,
-                       oInv = oTG + 6 * MS, total = oInv + MM * M;
+                       oInv = oTG + 6 * MS, oMap = oInv + MM * M, total = oMap + (6 * QQ + 1) / 2;
 };
 
 template <int P>
@@ -1933,6 +1936,9 @@ __global__ void __launch_bounds__(256, 2) k_elem_pf16(LevelGeom g, const double*
       const int d = i / ET;
       cp_async8(&tb[i], src[d] + (i - d * ET), true);
     }
+    unsigned* map_s = reinterpret_cast<unsigned*>(sm + C::oMap);   // the face map, before the wait
+    for (int i = tid; i < 6 * QQ; i += NT) map_s[i] = __ldg(&kFaceMap<P>.v[i]);
+    __syncthreads();
     pdl_wait();
     pdl_trigger();
     if (done && *done) return;
@@ -1940,7 +1946,7 @@ __global__ void __launch_bounds__(256, 2) k_elem_pf16(LevelGeom g, const double*
     const long long V12 = (long long)g.V1 * g.V2;
     const long long rec0 = e1 + g.V1 * (long long)e2 + V12 * e3;
     for (int i = tid; i < 6 * QQ; i += NT) {
-      const unsigned m_ = kFaceMap<P>.v[i];
+      const unsigned m_ = map_s[i];
       cp_async8(&Uc[i], &u[(rec0 + rec_delta(m_, g.V1, V12)) * RS + (m_ & 0xFFFu)], true);
     }
     cp_async_commit();
