@@ -1533,11 +1533,26 @@ __global__ void __launch_bounds__(ElemPfCfg<P>::NT, ElemPfCfg<P>::MINB)
     const double* c2 = cube + t3 * QQ + t1;          // line along x2 (stride Q)
     const double* c3 = cube + t2 * Q + t1;           // line along x3 (stride QQ)
     double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    // a line through a face point along the face normal crosses the zero interior: only its two
+    // end values are nonzero (the skipped terms are exact zeros, the sums are unchanged)
+    const int nd = o < 6 * MM ? (o / MM) >> 1 : 3;
+    if (nd == 0) {
+      s1 = fma(K1[t1 * Q + P], c1[P], K1[t1 * Q] * c1[0]);
+    } else {
 #pragma unroll
-    for (int t = 0; t <= P; ++t) {
-      s1 = fma(K1[t1 * Q + t], c1[t], s1);
-      s2 = fma(K2[t2 * Q + t], c2[t * Q], s2);
-      s3 = fma(K3[t3 * Q + t], c3[t * QQ], s3);
+      for (int t = 0; t <= P; ++t) s1 = fma(K1[t1 * Q + t], c1[t], s1);
+    }
+    if (nd == 1) {
+      s2 = fma(K2[t2 * Q + P], c2[P * Q], K2[t2 * Q] * c2[0]);
+    } else {
+#pragma unroll
+      for (int t = 0; t <= P; ++t) s2 = fma(K2[t2 * Q + t], c2[t * Q], s2);
+    }
+    if (nd == 2) {
+      s3 = fma(K3[t3 * Q + P], c3[P * QQ], K3[t3 * Q] * c3[0]);
+    } else {
+#pragma unroll
+      for (int t = 0; t <= P; ++t) s3 = fma(K3[t3 * Q + t], c3[t * QQ], s3);
     }
     const double m1 = M1[t1], m2 = M2[t2], m3 = M3[t3];
     double y = lam * m1 * m2 * m3 * c1[t1];
