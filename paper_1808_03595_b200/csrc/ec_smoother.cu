@@ -59,7 +59,7 @@ __device__ __forceinline__ double ec_dot(const double* x, const double* y) {
 template <int P>
 __global__ void __launch_bounds__(kEcThreads) k_ec_block(LevelGeom g, int c1, int c2, int c3, int n1, int n2,
                                                        const double* __restrict__ r, double* __restrict__ u,
-                                                       const double* __restrict__ ectab, double lam, int stage_s) {
+                                                       const double* __restrict__ ectab, double lam) {
   extern __shared__ double sm[];
   constexpr int p = P, n = 3 * P - 1, nn = n * n, ES = n * n + 4 * n;
   constexpr int clo = p - 1, chi = 2 * p - 1;
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kEcThreads) k_ec_block(LevelGeom g, int c1, in
   double* F = sm;                  // 6 planes (d, s): index (2d + s) * nn + A * n + B
   double* G = sm + 6 * nn;         // 6 planes workspace
   double* vec = sm + 12 * nn;      // per direction: Lambda, s_lo, s_hi, omega (4n each)
-  double* Ssm = vec + 12 * n;      // S_d staged (stage_s), 3 nn
+  double* Ssm = vec + 12 * n;      // S_d staged (STAGE), 3 nn
   const double* S[3];
   for (int d = 0; d < 3; ++d) {
     const int row = (d == 0 ? 0 : (d == 1 ? g.k1 : g.k1 + g.k2)) + e[d];
@@ -82,7 +82,6 @@ __global__ void __launch_bounds__(kEcThreads) k_ec_block(LevelGeom g, int c1, in
   // S_d staged in shared memory when the three fit next to the planes (p <= 14): the transforms
   // then address it as Ssm + d nn (shared loads); otherwise straight from the L2-resident table
   constexpr bool STAGE = (15 * nn + 12 * n) * 8 <= 227 * 1024;
-  (void)stage_s;
   if (STAGE) {
     for (int i = tid; i < 3 * nn; i += kEcThreads) {
       const int d = i / nn;
@@ -448,13 +447,12 @@ void launch_ec(const LevelGeom& g, int c1, int c2, int c3, const double* r, doub
     }
   }
   const int n = ec_n(g.p);
-  const size_t staged = ec_smem(g.p) + sizeof(double) * (size_t)(3 * n * n);
-  const int stage = (15 * n * n + 12 * n) * 8 <= 227 * 1024 ? 1 : 0;   // as the kernel's STAGE (p <= 14)
-  const size_t smem = stage ? staged : ec_smem(g.p);
+  const bool stage = (15 * n * n + 12 * n) * 8 <= 227 * 1024;   // as the kernel's STAGE (p <= 14)
+  const size_t smem = ec_smem(g.p) + (stage ? sizeof(double) * (size_t)(3 * n * n) : 0);
   switch (g.p) {
 #define PMG_EC_CASE(P) \
   case P: \
-    launch_pdl(k_ec_block<P>, dim3((unsigned)nb), dim3(kEcThreads), smem, st, g, c1, c2, c3, n1, n2, r, u, ectab, lam, stage); \
+    launch_pdl(k_ec_block<P>, dim3((unsigned)nb), dim3(kEcThreads), smem, st, g, c1, c2, c3, n1, n2, r, u, ectab, lam); \
     break;
     PMG_EC_DEGREES(PMG_EC_CASE)
 #undef PMG_EC_CASE

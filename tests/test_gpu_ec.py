@@ -181,3 +181,27 @@ def test_ec_degenerate_meshes(k, p):
     assert rep["cycles"] == rep_o["cycles"], (rep["cycles"], rep_o["cycles"])
     assert rel(ug.cpu().numpy(), u_o) < SOLVE_TOL
     s.close()
+
+
+@pytest.mark.parametrize("p", [14, 16])
+def test_ec_high_degree_dfma_parity(p):
+    """p = 14 .. 16 run the DFMA kernel (the DMMA planes do not fit shared memory): one smoother
+    application per level against the oracle's dense-LU blocks on a 2 x 2 x 1 mesh (z faces
+    Neumann so that the single element layer has unknowns)."""
+    from oracle import mg
+    import paper_1808_03595_b200 as pmg
+    case = pi.small_case((2, 2, 1), p, 0.8, stretch=1.2)
+    orc = mg.Hierarchy(case.k, case.widths, p, 0.8, neumann=0b110000, smoother="element")
+    s = pmg.Solver(case.k, case.widths, p, 0.8, neumann=0b110000, smoother=1)
+    rng = np.random.default_rng(p)
+    for l in range(1, s.nlevels):
+        m = orc.levels[l].mesh
+        r = rng.standard_normal(m.ntot) * m.free_skel
+        rs, us = s.new_skel(l), s.new_skel(l)
+        s.skel_from_grid(l, torch.from_numpy(r).cuda(), rs)
+        s.smooth(l, rs, us)
+        ug = s.new_grid(l)
+        s.skel_to_grid(l, us, ug)
+        torch.cuda.synchronize()
+        assert rel(ug.cpu().numpy(), orc.levels[l].smoother.apply(r)) < OP_TOL, (p, l)
+    s.close()
