@@ -1,0 +1,13 @@
+import sys, os
+sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
+import torch
+import paper_1808_03595_b200 as pmg, pmg_inputs as pi
+case = pi.config(3, p=4)      # 64^3 elements: the coarse CG takes the h-multigrid preconditioner
+s = pmg.Solver(case.k, case.widths, case.p, case.lam)
+L = s.nlevels - 1
+x = [s.grid_coords(L, d) for d in range(3)]
+F = s.new_grid(); s.weak_rhs(torch.from_numpy(case.f_nodal(x)).cuda(), F)
+u = s.new_grid()
+s.solve(F, u, 1e-10)
+torch.cuda.synchronize()
+print("ok")
