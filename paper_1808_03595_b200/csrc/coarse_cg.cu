@@ -632,8 +632,11 @@ __device__ __forceinline__ double csr_row_thread(const int* __restrict__ ptr, co
   return s;
 }
 
-// z = V-cycle(f_0) into h.x[0]; h.f[0] holds the right-hand side
-__device__ void hmg_vcycle(const HmgDev& h, cg::grid_group& grid, long long t0, long long T) {
+// z = V-cycle(f_0) into h.x[0]; h.f[0] holds the right-hand side.  With rz_part set, the block's
+// partial of f_0 . z (the CG's r.z) is formed in the last level-0 sweep and published before the
+// V-cycle's final barrier, which then doubles as the CG's reduction barrier.
+__device__ void hmg_vcycle(const HmgDev& h, cg::grid_group& grid, long long t0, long long T,
+                           double* red = nullptr, double* rz_part = nullptr) {
   const int L = h.nlev - 1;
   for (int l = 0; l < L; ++l) {
     const long long n = h.n[l];
@@ -697,7 +700,20 @@ __device__ void hmg_vcycle(const HmgDev& h, cg::grid_group& grid, long long t0, 
     // two post-sweeps, each one pass, ping-pong x -> r -> x (r is free here)
     for (long long i = t0; i < n; i += T) r[i] = fma(kHmgOmega * di[i], f[i] - ell_row(h.Aval[l], h.Acol[l], n, i, x), x[i]);
     grid.sync();
-    for (long long i = t0; i < n; i += T) x[i] = fma(kHmgOmega * di[i], f[i] - ell_row(h.Aval[l], h.Acol[l], n, i, r), r[i]);
+    double srz = 0.0;
+    for (long long i = t0; i < n; i += T) {
+      const double xi = fma(kHmgOmega * di[i], f[i] - ell_row(h.Aval[l], h.Acol[l], n, i, r), r[i]);
+      x[i] = xi;
+      srz = fma(f[i], xi, srz);
+    }
+    if (l == 0 && rz_part) block_reduce3(srz, srz, srz, red, blockIdx.x, rz_part, rz_part, rz_part);
+    grid.sync();
+  }
+  if (L == 0 && rz_part) {   // a single h-level (the dense solve alone): r.z after it
+    const long long n = h.n[0];
+    double srz = 0.0;
+    for (long long i = t0; i < n; i += T) srz = fma(h.f[0][i], __ldcg(&h.x[0][i]), srz);
+    block_reduce3(srz, srz, srz, red, blockIdx.x, rz_part, rz_part, rz_part);
     grid.sync();
   }
 }
@@ -730,27 +746,28 @@ __global__ void __launch_bounds__(256) k_pcg_hmg_p2(HmgDev h, const double* __re
   grid_totals3(pa, pb, pc, nb, red, bb, d1, d2);
   int its = 0, breakdown = 0;
   if (bb > 0.0) {
-    hmg_vcycle(h, grid, t0, T);
-    double srz = 0.0;
-    for (long long i = t0; i < n; i += T) {
-      pv[i] = Z[i];
-      srz = fma(R[i], Z[i], srz);
-    }
-    block_reduce3(srz, 0.0, 0.0, red, blockIdx.x, pa, pb, pc);
-    grid.sync();
-    double rz;
-    grid_totals3(pa, pb, pc, nb, red, rz, d1, d2);
-    for (;;) {
+    // partial sums: p.q in pa, r.r in pb, r.z in pc -- consecutive reductions use different
+    // buffers, so a block that runs ahead never overwrites a partial another block still reads.
+    // Two grid barriers per iteration besides the V-cycle's: with p_new = z + beta p,
+    // q_new = H z + beta q_old, so the direction, the operator application (z is complete after
+    // the V-cycle) and p.q share one phase; r.z is reduced inside the V-cycle's last sweep
+    hmg_vcycle(h, grid, t0, T, red, pc);
+    double rz, pq;
+    grid_totals3(pc, pc, pc, nb, red, rz, d1, d2);
+    {
       double spq = 0.0;
       for (long long i = t0; i < n; i += T) {
-        const double qi = ell_row(h.Aval[0], h.Acol[0], n, i, pv);
+        const double zi = Z[i];
+        const double qi = ell_row(h.Aval[0], h.Acol[0], n, i, Z);
+        pv[i] = zi;
         q[i] = qi;
-        spq = fma(pv[i], qi, spq);
+        spq = fma(zi, qi, spq);
       }
-      block_reduce3(spq, 0.0, 0.0, red, blockIdx.x, pa, pb, pc);
+      block_reduce3(spq, spq, spq, red, blockIdx.x, pa, pa, pa);
       grid.sync();
-      double pq;
-      grid_totals3(pa, pb, pc, nb, red, pq, d1, d2);
+      grid_totals3(pa, pa, pa, nb, red, pq, d1, d2);
+    }
+    for (;;) {
       if (!(pq > 0.0)) { breakdown = 1; break; }
       const double alpha = rz / pq;
       double srr = 0.0;
@@ -760,23 +777,28 @@ __global__ void __launch_bounds__(256) k_pcg_hmg_p2(HmgDev h, const double* __re
         R[i] = ri;
         srr = fma(ri, ri, srr);
       }
-      block_reduce3(srr, 0.0, 0.0, red, blockIdx.x, pa, pb, pc);
+      block_reduce3(srr, srr, srr, red, blockIdx.x, pb, pb, pb);
       grid.sync();
       double rr;
-      grid_totals3(pa, pb, pc, nb, red, rr, d1, d2);
+      grid_totals3(pb, pb, pb, nb, red, rr, d1, d2);
       ++its;
       if (sqrt(rr) <= rtol * sqrt(bb) || its >= maxit) break;
-      hmg_vcycle(h, grid, t0, T);
-      double srz2 = 0.0;
-      for (long long i = t0; i < n; i += T) srz2 = fma(R[i], Z[i], srz2);
-      block_reduce3(srz2, 0.0, 0.0, red, blockIdx.x, pa, pb, pc);
-      grid.sync();
+      hmg_vcycle(h, grid, t0, T, red, pc);
       double rzn;
-      grid_totals3(pa, pb, pc, nb, red, rzn, d1, d2);
+      grid_totals3(pc, pc, pc, nb, red, rzn, d1, d2);
       const double beta = rzn / rz;
       rz = rzn;
-      for (long long i = t0; i < n; i += T) pv[i] = fma(beta, pv[i], Z[i]);
+      double spq = 0.0;
+      for (long long i = t0; i < n; i += T) {
+        const double pvi = fma(beta, pv[i], Z[i]);
+        const double qi = fma(beta, q[i], ell_row(h.Aval[0], h.Acol[0], n, i, Z));
+        pv[i] = pvi;
+        q[i] = qi;
+        spq = fma(pvi, qi, spq);
+      }
+      block_reduce3(spq, spq, spq, red, blockIdx.x, pa, pa, pa);
       grid.sync();
+      grid_totals3(pa, pa, pa, nb, red, pq, d1, d2);
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
