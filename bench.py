@@ -1,16 +1,24 @@
 """Benchmark: unknowns/s of a 1e-10 residual-drop pMG solve (FP64) on B200, BASELINE.json metric.
 
 One "step" = one full pmg_solve (Alg. 4: condense, V-cycles until ||r|| <= 1e-10 ||r_0||,
-recover) of the workload, inputs resident in HBM.  Default workload: BASELINE configs[1]
-(Poisson, 16^3 elements, p = 8, f ~ U[-1,1] seed 1, 2,097,152 unknowns).  L2 (126 MB) is
-flushed between timed steps by writing a 512 MB buffer (outside the per-step events).
+recover) of the workload, inputs resident in HBM.  Default workload: BASELINE configs[4], the
+north star's scaling configuration -- Poisson, 64 x 64 x (8 N) elements, p = 16, f ~ U[-1,1] seed 4,
+134 M unknowns per GPU (weak scaling, "cfg5_poisson_64x64x8N_p16"); --strong splits the whole
+64^3-element problem (1.07e9 unknowns) over the N GPUs instead.  N > 1 runs the z-slab
+decomposition (one process per GPU under torchrun, NCCL halo planes per operator, allreduced
+norms, allgathered coarse right-hand side with a replicated coarse CG).
+L2 (126 MB) is flushed between timed steps by writing a 512 MB buffer (outside the per-step
+events); the vectors themselves (1.1 GB grid, 0.2 GB skeleton per vector) exceed L2 anyway.
 
-  python bench.py [--gpus N --steps K --warmup W] [--config 2] [--p P] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--config 5|4|3|2|1] [--p P] [--strong]
+                  [--impl reference]
 
---impl reference times the CPU oracle (oracle/, test infrastructure) on the same config: the
-deliberately slow, plain program the GPU path is checked against.  Under torchrun (N > 1) only
-rank 0 runs it.  N > 1 in this version runs one independent replica of the workload per GPU
-(the z-slab decomposition with NCCL halos is not implemented yet), scaling "weak".
+--impl reference times the CPU oracle (oracle/, test infrastructure) on the same workload: the
+deliberately slow, plain program the GPU path is checked against.  For configs 4 and 5 (and any
+workload over 2^22 unknowns) each step is one oracle solve of an 8 x 8 x 8-element sub-box with
+the same degree, lambda and width sequence, reported per unknown ("oracle, extrapolated": the
+sub-box's coarse solve is cheaper than the full problem's, which favours the oracle).  Under
+torchrun (N > 1) only rank 0 runs it.
 """
 import argparse
 import json
@@ -93,9 +101,13 @@ def dist_init():
 
 def case_for(args, n_gpu):
     """The workload; for n_gpu > 1 the weak-scaling variant: n_gpu z-slabs of the one-GPU problem
-    stacked along x3 (config 2: 16 x 16 x 16 n_gpu elements on (0,1)^2 x (0,n_gpu); config 5:
-    64 x 64 x 8 n_gpu, BASELINE.json)."""
+    stacked along x3 (config 5: 64 x 64 x 8 n_gpu elements, BASELINE.json; other configs: k3 n_gpu),
+    or with --strong (config 5 only) the whole 64^3-element problem split into n_gpu slabs."""
     if args.config == 5:
+        if args.strong:
+            k = (64, 64, 64)
+            return pi.Case("cfg5_poisson_64x64x64_p16", k, pi.uniform_widths(k, (1.0, 1.0, 1.0)), 16, 0.0,
+                           "uniform", seed=4)
         return pi.config(5, n_gpu=n_gpu)
     c = pi.config(args.config, p=args.p)
     if n_gpu > 1:
@@ -104,6 +116,30 @@ def case_for(args, n_gpu):
         c = pi.Case(c.name + "_weak%d" % n_gpu, k, w, c.p, c.lam, c.f_kind, seed=c.seed, amp=c.amp,
                     noise=c.noise, origin=c.origin)
     return c
+
+
+SUBBOX = 8          # oracle baseline of large workloads: an 8 x 8 x 8-element sub-box
+FULL_ORACLE_MAX = 1 << 22
+
+
+def oracle_case(case):
+    """The problem the oracle times for `case`: the case itself when small, else the sub-box of its
+    first SUBBOX elements per direction (same p, lambda, widths, right-hand side recipe)."""
+    if case.n_dof <= FULL_ORACLE_MAX:
+        return case, "full"
+    k = tuple(min(SUBBOX, kd) for kd in case.k)
+    w = [np.asarray(case.widths[d][:k[d]]) for d in range(3)]
+    sub = pi.Case(case.name + "_subbox%dx%dx%d" % k, k, w, case.p, case.lam, case.f_kind, seed=case.seed,
+                  amp=case.amp, noise=case.noise, origin=case.origin)
+    return sub, "sub"
+
+
+def workload_config(case, ws, strong):
+    """The config dict both arms print (identical keys and values)."""
+    return {"workload": case.name, "n_dof": case.n_dof, "p": case.p, "k": list(case.k), "lambda": case.lam,
+            "rtol": 1e-10, "n_ranks": ws, "decomposition": ("z-slabs" if ws > 1 else "none"),
+            "scaling_mode": "strong" if strong else "weak",
+            "l2": "flushed between steps (512 MB write, outside the timed events); grid vectors exceed L2"}
 
 
 def n_stars(case):
@@ -135,6 +171,19 @@ def oracle_solve_timer(case, reps, warm=0, smoother="star"):
     return ts, cyc
 
 
+def oracle_baseline(case, reps, warm=0, smoother="star"):
+    """cpu_baseline / reference-arm measurement: (unknowns/s, seconds per timed solve, cycles, kind, sample)."""
+    oc, mode = oracle_case(case)
+    ts, cyc = oracle_solve_timer(oc, reps, warm=warm, smoother=smoother)
+    t = statistics.mean(ts)
+    if mode == "full":
+        return oc.n_dof / t, t, cyc, "oracle", "%d full oracle solves (dense Schur / dense-LU stars; setup excluded) of %s, %.2f s each, %d cycles" % (reps, oc.name, t, cyc)
+    return (oc.n_dof / t, t, cyc, "oracle, extrapolated",
+            "%d oracle solves (setup excluded) of the %dx%dx%d-element sub-box of %s (same p, lambda, widths, "
+            "f recipe; %d unknowns, %.2f s each, %d cycles), reported per unknown; the full problem's larger "
+            "coarse solve is not included" % (reps, oc.k[0], oc.k[1], oc.k[2], case.name, oc.n_dof, t, cyc))
+
+
 def cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -146,19 +195,15 @@ def run_reference(args, ws, rank):
     if rank != 0:
         return 0
     case = case_for(args, ws)
-    ts, cyc = oracle_solve_timer(case, args.steps, warm=args.warmup)
-    t = statistics.mean(ts)
-    val = case.n_dof / t
+    val, t, cyc, kind, sample = oracle_baseline(case, args.steps, warm=args.warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "unknowns/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": case.name, "n_dof": case.n_dof, "p": case.p, "k": list(case.k), "lambda": case.lam,
-                   "rtol": 1e-10, "cycles": cyc},
-        "cpu_baseline": {"value": val, "unit": "unknowns/s", "cores": cores(), "kind": "oracle",
-                         "sample": "%d full oracle solves (dense Schur / dense-LU stars; setup excluded) of %s"
-                                   % (args.steps, case.name)},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": case.n_dof / val * 1e3, "higher_is_better": True,
+        "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(case, ws, args.strong),
+        "cpu_baseline": {"value": val, "unit": "unknowns/s", "cores": cores(), "kind": kind, "sample": sample},
         "e2e": {"value": val, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "solve": {"cycles": cyc, "seconds_per_timed_solve": t},
     }
     print(json.dumps(line))
     return 0
@@ -179,7 +224,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--strong", action="store_true", help="config 5: the whole 64^3 problem over N GPUs")
     ap.add_argument("--p", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -318,20 +364,24 @@ def main():
                 "achieved_gbs_alg": bytes_alg / (res_ms / 1e3) / 1e9}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        ts, cyc = oracle_solve_timer(case, 3, smoother=args.smoother)
-        tcpu = statistics.mean(ts)
-        cpu = {"value": case.n_dof / tcpu, "unit": "unknowns/s", "cores": cores(), "kind": "oracle",
-               "sample": "3 full oracle solves of %s (setup excluded), %.2f s each, %d cycles" % (case.name, tcpu, cyc)}
+        val, t, cyc, kind, sample = oracle_baseline(case, 3, smoother=args.smoother)
+        cpu = {"value": val, "unit": "unknowns/s", "cores": cores(), "kind": kind, "sample": sample}
     r = reps[-1]
+    cfg = workload_config(case, ws, args.strong)
+    if ec:
+        cfg["workload"] += "_element_centred"
     line = {
         "metric": METRIC, "value": value, "unit": "unknowns/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if args.strong else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": case.name + ("_element_centred" if ec else ""), "smoother": args.smoother, "n_dof": case.n_dof, "p": case.p, "k": list(case.k), "lambda": case.lam,
-                   "rtol": 1e-10, "cycles": r["cycles"], "rho": r["rho"], "coarse_iters": r["coarse_iters"],
-                   "l2": "flushed between steps (512 MB write, outside the timed events)",
-                   "parallelism": "single GPU" if ws == 1 else
-                   "z-slab x%d (NCCL halo planes per operator, allreduce of owned norms, allgather of the coarse RHS + replicated coarse CG)" % ws},
+        "config": cfg,
+        "parallelism": ("single GPU" if ws == 1 else
+                        "z-slab x%d (NCCL halo planes per operator, allreduce of owned norms, allgather of the "
+                        "coarse RHS + replicated coarse CG)" % ws),
+        "solve": {"smoother": args.smoother, "cycles": r["cycles"], "rho": r["rho"], "coarse_iters": r["coarse_iters"],
+                  "phase_ms": {"condense": r["t_condense"], "cycles": r["t_cycles"], "coarse_cg": r["t_coarse"],
+                               "recover": r["t_recover"]}},
         "roofline": roof,
         "residual_kernel": residual,
         "time_split_ms_per_step": {"smoother_all_levels": all_sm_ms / args.steps, "residual_all_levels": all_rs_ms / args.steps,

@@ -115,6 +115,11 @@ typedef struct {
   int coarse_iters;   /* total coarse CG iterations over the whole solve */
   double* history;    /* optional caller array (host) receiving ||r_n||, n = 0..cycles */
   int history_cap;    /* its capacity */
+  /* phase times of the solve in milliseconds (CUDA events on the context stream):
+   * condensation (Alg. 4 line 2, incl. the z-slab grid halo), the cycle loop (V-cycles + stopping
+   * residuals + the per-cycle host read of ||r||), the coarse solves inside it (summed over cycles),
+   * and the interior recovery */
+  double t_condense, t_cycles, t_coarse, t_recover;
 } pmg_report;
 
 /* Multi-rank helpers.  pmg_nccl_unique_id writes a fresh 128-byte ncclUniqueId (call on rank 0
@@ -132,7 +137,7 @@ void pmg_default_options(pmg_options* opt);
 /* Build the level hierarchy (host: GLL, 1-D mass/stiffness, element and star generalised
  * eigenpairs with identity padding at the boundary, weights, interpolation matrices, coarse
  * diagonal; device: tables and workspaces).  n_e[3] = (k1, k2, k3) >= 1; widths[d] is a HOST
- * array of k_d positive finite element widths; p in [1, 32] (p >= p0 for pmg_vcycle /
+ * array of k_d positive finite element widths; p in [2, 32] (p >= p0 for pmg_vcycle /
  * pmg_solve); lambda >= 0; opt may be NULL.  Errors: PMG_EINVAL, PMG_ENOMEM, PMG_ECUDA. */
 pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths[3], int p,
                      double lambda, const pmg_options* opt);

@@ -51,7 +51,9 @@ class Slab(ctypes.Structure):
 class Report(ctypes.Structure):
     _fields_ = [("cycles", ctypes.c_int), ("converged", ctypes.c_int), ("r0", ctypes.c_double),
                 ("r_final", ctypes.c_double), ("rho", ctypes.c_double), ("coarse_iters", ctypes.c_int),
-                ("history", ctypes.POINTER(ctypes.c_double)), ("history_cap", ctypes.c_int)]
+                ("history", ctypes.POINTER(ctypes.c_double)), ("history_cap", ctypes.c_int),
+                ("t_condense", ctypes.c_double), ("t_cycles", ctypes.c_double), ("t_coarse", ctypes.c_double),
+                ("t_recover", ctypes.c_double)]
 
 
 _P = ctypes.c_void_p
@@ -265,7 +267,8 @@ class Solver:
     def _report(self, rep, hist, status):
         return dict(cycles=rep.cycles, converged=bool(rep.converged), r0=rep.r0, r_final=rep.r_final,
                     rho=rep.rho, coarse_iters=rep.coarse_iters,
-                    history=list(hist[:rep.cycles + 1]), status=status)
+                    history=list(hist[:rep.cycles + 1]), status=status,
+                    t_condense=rep.t_condense, t_cycles=rep.t_cycles, t_coarse=rep.t_coarse, t_recover=rep.t_recover)
 
     def solve(self, F, u, rtol=1e-10, max_cycles=50):
         hist = (ctypes.c_double * (max_cycles + 1))()

@@ -1,0 +1,419 @@
+// Condensed element operator for 9 <= p <= 16 (P:117-123 with the O(p^3) evaluation of reading R1,
+// SURVEY App. A.1): Y_e = H_hat_e u_e = H_BB u_e - C u_e on the element's boundary points, one CTA of
+// 4 warps per element, three CTAs per SM.  Same arithmetic as k_elem_pf16 (hot_kernels.cu),
+// re-planned from its ncu profile (round 2 start: shared-memory bound, L1/TEX 90 %, 44 % of the
+// samples in the gather / table set-up):
+//   - the element's tables come from a padded per-(direction, 1-D element) table that is the shared
+//     memory image itself (P_d as MP x 20, Lambda, a0, a1, M, K~ = M^-1 K row-scaled): one 16-byte
+//     cp.async stream, no set-up loops;
+//   - the six closed faces are gathered once into (MP+1) x 20 arrays; the DMMA transforms read the
+//     face interiors from them with a (1, 1) offset (the padded index is the t = p boundary line,
+//     multiplied by a zero table entry or -- for H_BB -- the wanted boundary term);
+//   - H_BB's tangential line sums of the face interiors are one DMMA GEMM pair per face accumulated
+//     into one tile set, Z = U K~_a^T + K~_b U (the M factors of the two terms folded into K~), so
+//     only the t = 0 terms and the normal terms remain scalar;
+//   - the Schur correction runs in one pass over the interior eigen-triples (lanes b1, 2 groups per
+//     warp, b3 per group, b2 in registers): E, V = E / D (rcp + one cubic Newton step), the x2-face
+//     contractions in registers, the x3-face contractions in register arrays reduced over the 8
+//     groups in a fixed-order tree, the x1-face contractions by a 16-lane butterfly reduce-scatter.
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+#include "layout.cuh"
+
+namespace pmg {
+namespace {
+
+__device__ __forceinline__ double rcp3e(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
+__device__ __forceinline__ void dmma_e(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void cpa8e(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cpa16e(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+
+}  // namespace
+
+// padded element table row (host: pmg_api.cu), per direction d and 1-D element e_d:
+//   [oP]  P[b][i] = S[i][b] M_II[i]  (MP x LDT, zero padded)
+//   [oL]  Lambda[b] (MP, padded with 1)      [oA0] a0[b], [oA1] a1[b] (MP, zero padded)
+//   [oM]  M[t], t = 0..p (LDT, zero padded)  [oK]  K~[t][t'] = K[t][t'] / M[t] ((P+1) x LDT, zero padded)
+template <int P> struct Elem16 {
+  static constexpr int M = P - 1, Q = P + 1, MM = M * M;
+  static constexpr int MP = (P + 7) / 8 * 8;               // transform size; index MP-1 >= m reaches t = p
+  static constexpr int LDT = (MP + 1 + 3) / 8 * 8 + 4;      // >= MP + 1 and = 4 (mod 8): conflict-free DMMA fragments
+  static constexpr int UR = MP + 1;                          // closed-face rows (>= Q)
+  static constexpr int FS = UR * LDT;                        // closed-face stride
+  static constexpr int MS = MP * LDT;                        // transform matrix stride
+  static constexpr int oP = 0, oL = MS, oA0 = oL + MP, oA1 = oA0 + MP, oM = oA1 + MP, oK = oM + LDT,
+                       ETP = oK + Q * LDT + ((Q * LDT) & 1);
+  static constexpr int NT = 128;
+  static constexpr int YS = 6 * MM + 12 * M + 8;
+  // shared memory (doubles): three table rows, six closed faces, X (6 MS), T / G / C (6 MS)
+  static constexpr int oTab = 0, oU = 3 * ETP, oX = oU + 6 * FS, oT = oX + 6 * MS, total = oT + 6 * MS;
+};
+
+template <int P>
+size_t elem16_smem2() { return sizeof(double) * Elem16<P>::total; }
+
+int elem16_etp(int p) {
+  switch (p) {
+#define CASE(PP) case PP: return Elem16<PP>::ETP;
+    CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+#undef CASE
+    default: return 0;
+  }
+}
+
+// host: padded element-table row from the element-table row (layout of pmg_internal.h)
+void elem16_table_row(int p, const double* et, double* out) {
+  const int m = p - 1, q = p + 1;
+  int MP = (p + 7) / 8 * 8, LDT = (MP + 1 + 3) / 8 * 8 + 4;
+  const int oL = MP * LDT, oA0 = oL + MP, oA1 = oA0 + MP, oM = oA1 + MP, oK = oM + LDT;
+  for (int b = 0; b < m; ++b)
+    for (int i = 0; i < m; ++i) out[b * LDT + i] = et[et_P(p) + b * m + i];
+  for (int b = 0; b < MP; ++b) {
+    out[oL + b] = b < m ? et[et_lam(p) + b] : 1.0;
+    out[oA0 + b] = b < m ? et[et_a0(p) + b] : 0.0;
+    out[oA1 + b] = b < m ? et[et_a1(p) + b] : 0.0;
+  }
+  for (int t = 0; t < q; ++t) out[oM + t] = et[et_M(p) + t];
+  for (int t = 0; t < q; ++t)
+    for (int s = 0; s < q; ++s) out[oK + t * LDT + s] = et[et_K(p) + t * q + s] / et[et_M(p) + t];
+}
+
+template <int P>
+__global__ void __launch_bounds__(128, 3)
+    k_elem16(LevelGeom g, const double* __restrict__ u, const double* __restrict__ etabP, double lam,
+             double* __restrict__ Y, const int* __restrict__ done) {
+  using K = Elem16<P>;
+  constexpr int M = K::M, Q = K::Q, MM = K::MM, MP = K::MP, LDT = K::LDT, UR = K::UR, FS = K::FS, MS = K::MS,
+                ETP = K::ETP, NT = K::NT, YS = K::YS;
+  constexpr int RS = 3 * MM + 3 * M + 1;
+  extern __shared__ double sm[];
+  double* tb = sm + K::oTab;
+  double* Uc = sm + K::oU;
+  double* X = sm + K::oX;
+  double* T = sm + K::oT;
+  const long long e = blockIdx.x;
+  const int e1 = (int)(e % g.k1), e2 = (int)((e / g.k1) % g.k2), e3 = (int)(e / ((long long)g.k1 * g.k2));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // ---- tables (before the dependency wait)
+  {
+    for (int i = tid; i < 3 * (ETP / 2); i += NT) {
+      const int d = i / (ETP / 2), ch = i - d * (ETP / 2);
+      const size_t row = d == 0 ? (size_t)e1 : (d == 1 ? (size_t)(g.k1 + e2) : (size_t)(g.k1 + g.k2 + e3));
+      cpa16e(tb + d * ETP + 2 * ch, etabP + row * ETP + 2 * ch);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+  // closed-face rows / columns beyond t = p (p < MP) are read by the padded transforms: zero them
+  if constexpr (UR > Q || LDT > Q) {
+    for (int i = tid; i < 6 * FS; i += NT) {
+      const int r_ = (i % FS) / LDT, c_ = i % LDT;
+      if (r_ >= Q || c_ >= Q) Uc[i] = 0.0;
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (done && *done) return;
+  // ---- gather the six closed faces: face f = 2 d + s (normal d at t_d = s p), rows tb (slow
+  // tangential direction db), columns ta (fast tangential direction da); the face interior is a
+  // contiguous (p-1)^2 run of one record, the rim comes from edge and vertex slots
+  {
+    const long long V12 = (long long)g.V1 * g.V2;
+    const long long rec0 = e1 + g.V1 * (long long)e2 + V12 * e3;
+    auto recb = [&](int o1, int o2, int o3) { return (rec0 + o1 + g.V1 * (long long)o2 + V12 * o3) * RS; };
+    for (int idx = tid; idx < 6 * MM; idx += NT) {
+      const int f = idx / MM, l = idx - f * MM, A = l / M, B = l - A * M, d = f >> 1, s = f & 1;
+      const long long b = recb(d == 0 ? s : 0, d == 1 ? s : 0, d == 2 ? s : 0) + d * MM;
+      cpa8e(&Uc[f * FS + (A + 1) * LDT + B + 1], u + b + A * M + B);
+    }
+    // rim: 4 p points per face, (tb, ta) walked around the boundary
+    for (int idx = tid; idx < 6 * 4 * P; idx += NT) {
+      const int f = idx / (4 * P), rr = idx - f * 4 * P, side = rr / P, i = rr - side * P, d = f >> 1, s = f & 1;
+      int ta, tbb;
+      if (side == 0) { tbb = 0; ta = i; } else if (side == 1) { ta = P; tbb = i; }
+      else if (side == 2) { tbb = P; ta = P - i; } else { ta = 0; tbb = P - i; }
+      // element-local (t1, t2, t3): d normal, a = fast, b = slow tangential direction
+      int x1, x2, x3;
+      if (d == 0) { x1 = s * P; x2 = ta; x3 = tbb; }
+      else if (d == 1) { x2 = s * P; x1 = ta; x3 = tbb; }
+      else { x3 = s * P; x1 = ta; x2 = tbb; }
+      const int o1 = x1 == P, o2 = x2 == P, o3 = x3 == P;   // t = p: next record, local 0
+      if (o1) x1 = 0;
+      if (o2) x2 = 0;
+      if (o3) x3 = 0;
+      int slot;
+      if (x1 == 0) {
+        if (x2 == 0) slot = (x3 == 0) ? 3 * MM + 3 * M : 3 * MM + 2 * M + x3 - 1;
+        else if (x3 == 0) slot = 3 * MM + M + x2 - 1;
+        else slot = (x3 - 1) * M + (x2 - 1);
+      } else if (x2 == 0) {
+        slot = (x3 == 0) ? 3 * MM + x1 - 1 : MM + (x3 - 1) * M + (x1 - 1);
+      } else {
+        slot = 2 * MM + (x2 - 1) * M + (x1 - 1);
+      }
+      cpa8e(&Uc[f * FS + tbb * LDT + ta], u + recb(o1, o2, o3) + slot);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  const int r8 = lane >> 2, q4 = lane & 3;
+  // ---- forward transforms: X_f = U_f P_a^T, then T_f = P_b X_f (2 x 2 tile blocks: one job per
+  // face and GEMM, 12 DMMA jobs per stage over 4 warps)
+  constexpr int T8 = MP / 8;
+  auto gemm = [&](auto TA, auto TB, const double* A, int lda, const double* B, int ldb, double* Cm, int ldc) {
+    // C (MP x MP) = op(A) op(B); one warp
+    for (int mi = 0; mi < T8; ++mi)
+      for (int ni = 0; ni < T8; ni += 2) {
+        double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        const bool two = ni + 1 < T8;
+#pragma unroll
+        for (int kk = 0; kk < MP / 4; ++kk) {
+          const int k = 4 * kk + q4, ii = 8 * mi + r8;
+          const double a = decltype(TA)::value ? A[k * lda + ii] : A[ii * lda + k];
+          const int j0 = 8 * ni + r8, j1 = j0 + 8;
+          const double b0 = decltype(TB)::value ? B[j0 * ldb + k] : B[k * ldb + j0];
+          dmma_e(c[0][0], c[0][1], a, b0);
+          if (two) {
+            const double b1 = decltype(TB)::value ? B[j1 * ldb + k] : B[k * ldb + j1];
+            dmma_e(c[1][0], c[1][1], a, b1);
+          }
+        }
+        *reinterpret_cast<double2*>(Cm + (8 * mi + r8) * ldc + 8 * ni + 2 * q4) = make_double2(c[0][0], c[0][1]);
+        if (two) *reinterpret_cast<double2*>(Cm + (8 * mi + r8) * ldc + 8 * ni + 8 + 2 * q4) = make_double2(c[1][0], c[1][1]);
+      }
+  };
+  using TT = std::true_type;
+  using FF = std::false_type;
+  for (int f = warp; f < 6; f += 4) {   // X_f = U_f,int P_a^T
+    const int d = f >> 1, da = (d == 0) ? 1 : 0;
+    gemm(FF{}, TT{}, Uc + f * FS + LDT + 1, LDT, tb + da * ETP + K::oP, LDT, X + f * MS, LDT);
+  }
+  __syncthreads();
+  for (int f = warp; f < 6; f += 4) {   // T_f = P_b X_f
+    const int d = f >> 1, db = (d == 2) ? 1 : 2;
+    gemm(FF{}, FF{}, tb + db * ETP + K::oP, LDT, X + f * MS, LDT, T + f * MS, LDT);
+  }
+  __syncthreads();
+  // ---- core over the interior eigen-triples (b1 lanes, b3 per 16-lane group, b2 in registers)
+  {
+    const double *a10 = tb + K::oA0, *a11 = tb + K::oA1;
+    const double *a20 = tb + ETP + K::oA0, *a21 = tb + ETP + K::oA1;
+    const double *a30 = tb + 2 * ETP + K::oA0, *a31 = tb + 2 * ETP + K::oA1;
+    const double *L1 = tb + K::oL, *L2 = tb + ETP + K::oL, *L3 = tb + 2 * ETP + K::oL;
+    const int b1 = lane & 15, grp = warp * 2 + (lane >> 4);
+    const bool vb1 = b1 < M;
+    const int b1c = vb1 ? b1 : 0;
+    const double c10 = vb1 ? a10[b1c] : 0.0, c11 = vb1 ? a11[b1c] : 0.0, L1v = L1[b1c];
+    double g4[M], g5[M];
+#pragma unroll
+    for (int b2 = 0; b2 < M; ++b2) g4[b2] = g5[b2] = 0.0;
+#pragma unroll 1
+    for (int it = 0; it < 2; ++it) {
+      const int b3 = grp + 8 * it;
+      const bool vb3 = b3 < M;
+      const int b3c = vb3 ? b3 : grp;   // invalid: a row this group owns (no cross-group race)
+      const double on = (vb1 && vb3) ? 1.0 : 0.0;
+      const double t2 = on * T[2 * MS + b3c * LDT + b1c], t3 = on * T[3 * MS + b3c * LDT + b1c];
+      const double c30 = on * a30[b3c], c31 = on * a31[b3c], c10v = on * c10, c11v = on * c11;
+      const double base = lam + L1v + L3[b3c];
+      double g2 = 0.0, g3 = 0.0;
+#pragma unroll
+      for (int ch = 0; ch < MP / 8; ++ch) {
+        double w[16];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int b2 = 8 * ch + j;
+          if (b2 < M) {
+            double E = c10v * T[0 * MS + b3c * LDT + b2];
+            E = fma(c11v, T[1 * MS + b3c * LDT + b2], E);
+            E = fma(a20[b2], t2, E);
+            E = fma(a21[b2], t3, E);
+            E = fma(c30, T[4 * MS + b2 * LDT + b1c], E);
+            E = fma(c31, T[5 * MS + b2 * LDT + b1c], E);
+            const double V = E * rcp3e(base + L2[b2]);
+            g2 = fma(a20[b2], V, g2);
+            g3 = fma(a21[b2], V, g3);
+            g4[b2] = fma(c30, V, g4[b2]);
+            g5[b2] = fma(c31, V, g5[b2]);
+            w[j] = c10 * V;
+            w[8 + j] = c11 * V;
+          } else {
+            w[j] = 0.0;
+            w[8 + j] = 0.0;
+          }
+        }
+        // reduce-scatter over the 16 lanes of the group: lane b1 ends with value b1 (j = b1 & 7 of
+        // face 0 for b1 < 8, of face 1 for b1 >= 8)
+#pragma unroll
+        for (int off = 8, half = 8; off >= 1; off >>= 1, half >>= 1) {
+          const bool upper = (lane & off) != 0;
+#pragma unroll
+          for (int j = 0; j < half; ++j) {
+            const double send = upper ? w[j] : w[j + half];
+            const double keep = upper ? w[j + half] : w[j];
+            w[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+          }
+        }
+        const int b2 = 8 * ch + (b1 & 7);
+        if (vb3 && b2 < M) T[(b1 >> 3) * MS + b3 * LDT + b2] = w[0];   // G0 / G1 over T0 / T1 row b3
+      }
+      if (vb3 && vb1) {
+        T[2 * MS + b3 * LDT + b1] = g2;
+        T[3 * MS + b3 * LDT + b1] = g3;
+      }
+    }
+    // G4 / G5: the two groups of a warp, then the four warps (w0 + w2) + (w1 + w3) through X
+#pragma unroll
+    for (int b2 = 0; b2 < M; ++b2) {
+      g4[b2] += __shfl_xor_sync(0xffffffffu, g4[b2], 16);
+      g5[b2] += __shfl_xor_sync(0xffffffffu, g5[b2], 16);
+    }
+    __syncthreads();   // every group is done reading T4 / T5
+    const bool wr = vb1 && lane < 16;
+    double* P0 = X;             // partial of warps 1 (+3)
+    if (wr && (warp == 0 || warp == 2)) {
+      double* dst = T + 4 * MS;
+      if (warp == 0) {
+#pragma unroll
+        for (int b2 = 0; b2 < M; ++b2) { dst[b2 * LDT + b1] = g4[b2]; dst[MS + b2 * LDT + b1] = g5[b2]; }
+      }
+    } else if (wr && warp == 1) {
+#pragma unroll
+      for (int b2 = 0; b2 < M; ++b2) { P0[b2 * LDT + b1] = g4[b2]; P0[MS + b2 * LDT + b1] = g5[b2]; }
+    }
+    __syncthreads();
+    if (wr && warp == 2) {
+      double* dst = T + 4 * MS;
+#pragma unroll
+      for (int b2 = 0; b2 < M; ++b2) { dst[b2 * LDT + b1] += g4[b2]; dst[MS + b2 * LDT + b1] += g5[b2]; }
+    } else if (wr && warp == 3) {
+#pragma unroll
+      for (int b2 = 0; b2 < M; ++b2) { P0[b2 * LDT + b1] += g4[b2]; P0[MS + b2 * LDT + b1] += g5[b2]; }
+    }
+    __syncthreads();
+    for (int i = tid; i < 2 * M * 16; i += NT) {
+      const int h = i / (M * 16), rr = i - h * M * 16, b2 = rr >> 4, b1_ = rr & 15;
+      if (b1_ < M) T[(4 + h) * MS + b2 * LDT + b1_] += P0[h * MS + b2 * LDT + b1_];
+    }
+    __syncthreads();
+  }
+  // ---- back transforms: X_f = G_f P_a, then C_f = P_b^T X_f (into T)
+  for (int f = warp; f < 6; f += 4) {
+    const int d = f >> 1, da = (d == 0) ? 1 : 0;
+    gemm(FF{}, FF{}, T + f * MS, LDT, tb + da * ETP + K::oP, LDT, X + f * MS, LDT);
+  }
+  __syncthreads();
+  for (int f = warp; f < 6; f += 4) {
+    const int d = f >> 1, db = (d == 2) ? 1 : 2;
+    gemm(TT{}, FF{}, tb + db * ETP + K::oP, LDT, X + f * MS, LDT, T + f * MS, LDT);
+  }
+  __syncthreads();
+  // ---- H_BB tangential line sums of the face interiors: Z_f = U_f K~_a^T + K~_b U_f (t = 1 .. MP;
+  // beyond t = p the table is zero), one accumulation (into X)
+  for (int f = warp; f < 6; f += 4) {
+    const int d = f >> 1, da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2;
+    const double* U = Uc + f * FS + LDT + 1;                 // U[tb-1][t-1]
+    const double* Ka = tb + da * ETP + K::oK + LDT + 1;      // Ka[ta-1][t-1] = K~_a[ta][t]
+    const double* Kb = tb + db * ETP + K::oK + LDT + 1;
+    for (int mi = 0; mi < T8; ++mi)
+      for (int ni = 0; ni < T8; ++ni) {
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < MP / 4; ++kk) {
+          const int k = 4 * kk + q4, ii = 8 * mi + r8, jj = 8 * ni + r8;
+          dmma_e(c0, c1, U[ii * LDT + k], Ka[jj * LDT + k]);     // sum_t U[tb][t] K~a[ta][t]
+          dmma_e(c0, c1, Kb[ii * LDT + k], U[k * LDT + jj]);     // sum_t K~b[tb][t] U[t][ta]
+        }
+        *reinterpret_cast<double2*>(X + f * MS + (8 * mi + r8) * LDT + 8 * ni + 2 * q4) = make_double2(c0, c1);
+      }
+  }
+  __syncthreads();
+  // ---- outputs: face interiors, then edges and vertices (all three lines lie on the boundary)
+  auto Mv = [&](int d) { return tb + d * ETP + K::oM; };
+  auto Kt = [&](int d) { return tb + d * ETP + K::oK; };
+  double* Ye = Y + (size_t)e * g.YS;
+  for (int o = tid; o < 6 * MM; o += NT) {
+    const int f = o / MM, r = o - f * MM, A = r / M, B = r - A * M, d = f >> 1, s_ = f & 1;
+    const int da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2;
+    const int td = s_ * P, ta = B + 1, tbb = A + 1;
+    const double* Uf = Uc + f * FS;
+    const double* Kd = Kt(d);
+    const double uv = Uf[tbb * LDT + ta];
+    double z = X[f * MS + A * LDT + B];
+    z = fma(Kt(da)[ta * LDT], Uf[tbb * LDT], z);                     // t = 0 term along a
+    z = fma(Kt(db)[tbb * LDT], Uf[ta], z);                           // t = 0 term along b
+    z = fma(Kd[td * LDT], Uc[(2 * d) * FS + tbb * LDT + ta], z);     // normal line: the two faces
+    z = fma(Kd[td * LDT + P], Uc[(2 * d + 1) * FS + tbb * LDT + ta], z);
+    z = fma(lam, uv, z);
+    Ye[o] = Mv(d)[td] * Mv(da)[ta] * Mv(db)[tbb] * z - T[f * MS + A * LDT + B];
+  }
+  auto getU = [&](int t1, int t2, int t3) -> double {   // boundary point of the element cube
+    if (t1 == 0 || t1 == P) return Uc[(t1 == P ? 1 : 0) * FS + t3 * LDT + t2];
+    if (t2 == 0 || t2 == P) return Uc[(2 + (t2 == P ? 1 : 0)) * FS + t3 * LDT + t1];
+    return Uc[(4 + (t3 == P ? 1 : 0)) * FS + t2 * LDT + t1];
+  };
+  for (int o = 6 * MM + tid; o < YS; o += NT) {
+    int t1, t2, t3;
+    if (o < 6 * MM + 12 * M) {
+      const int r = o - 6 * MM, qe = r / M, i = r - qe * M, d = qe >> 2, sA = qe & 1, sB = (qe >> 1) & 1;
+      if (d == 0) { t1 = i + 1; t2 = sA * P; t3 = sB * P; }
+      else if (d == 1) { t2 = i + 1; t1 = sA * P; t3 = sB * P; }
+      else { t3 = i + 1; t1 = sA * P; t2 = sB * P; }
+    } else {
+      const int qv = o - 6 * MM - 12 * M;
+      t1 = (qv & 1) * P; t2 = ((qv >> 1) & 1) * P; t3 = ((qv >> 2) & 1) * P;
+    }
+    double z = lam * getU(t1, t2, t3);
+#pragma unroll
+    for (int t = 0; t <= P; ++t) {
+      z = fma(Kt(0)[t1 * LDT + t], getU(t, t2, t3), z);
+      z = fma(Kt(1)[t2 * LDT + t], getU(t1, t, t3), z);
+      z = fma(Kt(2)[t3 * LDT + t], getU(t1, t2, t), z);
+    }
+    Ye[o] = Mv(0)[t1] * Mv(1)[t2] * Mv(2)[t3] * z;
+  }
+}
+
+cudaError_t launch_elem16(const LevelGeom& g, const double* u, const double* etabP, double lam, double* Y, const int* done,
+                          cudaStream_t st) {
+  switch (g.p) {
+#define CASE(PP)                                                                                                      \
+  case PP:                                                                                                            \
+    return launch_pdl(k_elem16<PP>, dim3((unsigned)g.nelem), dim3(Elem16<PP>::NT), elem16_smem2<PP>(), st, g, u, etabP, \
+                      lam, Y, done);
+    CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t elem16_set_smem_attr() {
+  cudaError_t e = cudaSuccess;
+#define CASE(PP)                                                                                   \
+  {                                                                                                \
+    cudaError_t a = cudaFuncSetAttribute(k_elem16<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                         (int)elem16_smem2<PP>());                                 \
+    if (a != cudaSuccess) e = a;                                                                   \
+  }
+  CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+#undef CASE
+  return e;
+}
+
+}  // namespace pmg

@@ -2195,6 +2195,13 @@ static int star_variant() {   // read at every launch (launches are captured int
   return (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
 }
 
+// stars per colour from which k_star_w (warp per star, p <= 4) replaces k_star_pf; PMG_STAR_W_MIN
+// overrides the default (tests force the kernel onto small parity meshes with 0)
+static long long star_w_min(long long dflt) {
+  const char* e = std::getenv("PMG_STAR_W_MIN");
+  return (e && e[0]) ? std::atoll(e) : dflt;
+}
+
 // element kernel variant for p <= 8: 0 k_elem_pf (default), 1 DFMA (k_elem_apply_t), 2 k_elem_dm
 static int elem_variant() {
   const char* e = std::getenv("PMG_ELEM_VARIANT");
@@ -2234,7 +2241,7 @@ void launch_star_p(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c,
     if constexpr (P <= 4) {
       // warp per star pays off once a colour has many waves of 128-thread stars (large meshes);
       // for a few hundred stars the shorter per-star chain of k_star_pf wins (measured, config 2)
-      if (v == 0 && nb >= 4LL * 148 * StarPfCfg<P>::MINB) {
+      if (v == 0 && nb >= star_w_min(4LL * 148 * StarPfCfg<P>::MINB)) {
         launch_pdl(k_star_w<P>, dim3((unsigned)((nb + StarWCfg<P>::SPB - 1) / StarWCfg<P>::SPB)), dim3(StarWCfg<P>::NT),
                    star_w_smem<P>(), st, g, c1, c2, c3, n1c, n2c, nb, r, u, stab, lam);
         return;

@@ -46,6 +46,19 @@ cudaError_t launch_star(const LevelGeom& g, int c1, int c2, int c3, int n1c, int
 cudaError_t launch_gather_resid(const LevelGeom& g, const double* Y, const double* F, double* out, const int* done,
                                 cudaStream_t st);
 size_t hot_smem(int p, int which);   // which: 0 element, 1 star
+// star smoother for 9 <= p <= 16 (star16.cu): padded star table stabP, rows of star16_stp(p) doubles
+// per vertex line: S as NP x NP (zero padded), Lambda (padded with 1), s = S[c][:], w (padded 0)
+cudaError_t launch_star16(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c, long long nb, const double* r,
+                          double* u, const double* stabP, double lam, cudaStream_t st);
+int star16_np(int p);
+cudaError_t star16_set_smem_attr();
+// condensed element operator for 9 <= p <= 16 (elem16.cu): padded element table etabP, rows of
+// elem16_etp(p) doubles per direction and 1-D element, built by elem16_table_row from an etab row
+cudaError_t launch_elem16(const LevelGeom& g, const double* u, const double* etabP, double lam, double* Y, const int* done,
+                          cudaStream_t st);
+int elem16_etp(int p);
+void elem16_table_row(int p, const double* et_row, double* out_row);
+cudaError_t elem16_set_smem_attr();
 cudaError_t hot_set_smem_attr(int bytes);
 
 // p = 2 coarse operator tables (coarse_cg.cu): assembled 1-D lumped masses b_d[2k_d+1], assembled

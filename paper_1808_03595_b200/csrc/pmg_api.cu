@@ -39,6 +39,8 @@ struct DevLevel {
   double* etab = nullptr;
   double* stab = nullptr;
   double* stabT = nullptr;
+  double* stabP = nullptr;   // padded star table of k_star16 (9 <= p <= 16)
+  double* etabP = nullptr;   // padded element table of k_elem16 (9 <= p <= 16)
   double* ectab = nullptr;   // element-centred smoother tables (opt.smoother == 1)
   double* Jint = nullptr;
   double* u = nullptr;
@@ -102,6 +104,8 @@ struct pmg_ctx {
   double* ella = nullptr;    // 25 n0 coefficients, then the indices (one block: one L2 window)
   cudaAccessPolicyWindow ell_win{};   // L2 persistence of the ELL rows (when the device allows it)
   bool ell_persist = false;
+  bool l2_limit_set = false;          // this context raised cudaLimitPersistingL2CacheSize
+  size_t l2_limit_prev = 0;           // ... from this value (restored on destroy)
   // h-multigrid preconditioned coarse CG (reading R16)
   bool use_hmg = false;
   int hmg_nb = 0;
@@ -116,6 +120,15 @@ struct pmg_ctx {
   long long launches_per_cycle = 0;
   double* hres = nullptr;    // pinned host scalar
   bool no_graph = false;     // PMG_NO_GRAPH=1
+  bool no_star16 = false;    // PMG_NO_STAR16=1: previous star kernel at 9 <= p <= 16 (A/B)
+  bool no_elem16 = false;    // PMG_NO_ELEM16=1: previous element kernel at 9 <= p <= 16 (A/B)
+  // pmg_report phase times: solve-phase events and the coarse-solve bracket (recorded as external
+  // event nodes inside the captured cycle graph), created at setup
+  cudaEvent_t ev_ph[4] = {nullptr, nullptr, nullptr, nullptr};   // start, condensed, cycles done, recovered
+  cudaEvent_t ev_cg[2] = {nullptr, nullptr};                     // around the coarse solve of a V-cycle
+  bool cg_mark = false;      // record ev_cg inside vcycle_dev (pmg_solve only)
+  bool capturing = false;    // inside the cycle-graph capture: event records become external event nodes
+  double t_coarse_acc = 0.0;
   // event timing (pmg_timing_enable)
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -193,6 +206,8 @@ pmg_status residual_dev(pmg_ctx* c, int l, const double* u, const double* f, dou
   if (c->ref_kernels) {
     size_t sm = elem_apply_smem(D.g.p, D.g.ET);
     k_elem_apply<<<(unsigned)D.g.nelem, kThreads, sm, c->st>>>(D.g, u, D.etab, c->lam, c->Y, done);
+  } else if (D.etabP && !c->no_elem16) {
+    launch_elem16(D.g, u, D.etabP, c->lam, c->Y, done, c->st);
   } else {
     launch_elem_apply(D.g, u, D.etab, c->lam, c->Y, done, c->st);
   }
@@ -225,6 +240,8 @@ pmg_status smooth_dev(pmg_ctx* c, int l, const double* r, double* u) {
     long long nb = (long long)n1 * n2 * n3;
     if (c->ref_kernels)
       k_star<<<(unsigned)nb, kThreads, sm, c->st>>>(g, c1, c2, c3, n1, n2, r, u, D.stab, c->lam, c->star_s_smem ? 1 : 0);
+    else if (D.stabP && !c->no_star16)
+      launch_star16(g, c1, c2, c3, n1, n2, nb, r, u, D.stabP, c->lam, c->st);
     else
       launch_star(g, c1, c2, c3, n1, n2, nb, r, u, D.stab, D.stabT, c->lam, c->st);
     LAUNCH_CHECK(c);
@@ -434,6 +451,14 @@ pmg_status residual_x(pmg_ctx* c, int l, double* u, const double* f, double* r) 
   return exchange(c, l, r);
 }
 
+// pmg_report t_coarse: event i (0 before, 1 after) around the coarse solve of a V-cycle inside pmg_solve
+pmg_status mark_coarse(pmg_ctx* c, int i) {
+  if (!c->cg_mark) return PMG_OK;
+  if (c->capturing) CUDA_CHECK(cudaEventRecordWithFlags(c->ev_cg[i], c->st, cudaEventRecordExternal));
+  else CUDA_CHECK(cudaEventRecord(c->ev_cg[i], c->st));
+  return PMG_OK;
+}
+
 // Alg. 3.  r_top_valid: D[L].r already holds f - H u (saves one residual).
 pmg_status vcycle_dev(pmg_ctx* c, double* u, const double* f, bool r_top_valid) {
   const int L = c->L;
@@ -444,7 +469,9 @@ pmg_status vcycle_dev(pmg_ctx* c, double* u, const double* f, bool r_top_valid) 
     DevLevel& D = c->D[0];
     if (!r_top_valid && (s = residual_x(c, 0, u, f, D.r))) return s;
     double* cx = c->tr ? c->cxl : c->cx;
+    if ((s = mark_coarse(c, 0))) return s;
     if ((s = coarse_solve(c, D.r, cx))) return s;
+    if ((s = mark_coarse(c, 1))) return s;
     k_axpy<<<grid_for(D.g.nskel), kThreads, 0, c->st>>>(u, cx, 1.0, D.g.nskel);
     LAUNCH_CHECK(c);
     return PMG_OK;
@@ -469,7 +496,9 @@ pmg_status vcycle_dev(pmg_ctx* c, double* u, const double* f, bool r_top_valid) 
     if ((s = restrict_dev(c, l, D.r, c->D[l - 1].f, l - 1 >= 1 ? c->D[l - 1].u : nullptr))) return s;
     if (l - 1 >= 1 && (s = exchange(c, l - 1, c->D[l - 1].f))) return s;
   }
+  if ((s = mark_coarse(c, 0))) return s;
   if ((s = coarse_solve(c, c->D[0].f, c->D[0].u))) return s;
+  if ((s = mark_coarse(c, 1))) return s;
   for (int l = 1; l <= L; ++l) {
     DevLevel& D = c->D[l];
     double* ul = (l == L) ? u : D.u;
@@ -536,6 +565,8 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
   DevLevel& D = c->D[c->L];
   pmg_status s;
   c->coarse_its_total = 0;
+  c->t_coarse_acc = 0.0;
+  CUDA_CHECK(cudaEventRecord(c->ev_ph[0], c->st));
   CUDA_CHECK(cudaMemsetAsync(c->pcg, 0, sizeof(PcgState), c->st));
   const double* Floc = F;
   if (c->tr) {
@@ -552,6 +583,7 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
   }
   if ((s = condense_dev(c, Floc, D.f))) return s;
   if ((s = exchange(c, c->L, D.f))) return s;
+  CUDA_CHECK(cudaEventRecord(c->ev_ph[1], c->st));
   if ((s = zero_dev(c, D.u, D.g.nskel))) return s;
   if ((s = residual_x(c, c->L, D.u, D.f, D.r))) return s;
   double r0, rn;
@@ -573,11 +605,13 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
   // synchronisation (cooperative coarse CG) it is captured once into a CUDA graph and replayed:
   // ~60 kernel launches per cycle become one graph launch.
   const bool graph_ok = c->use_coop && c->st != nullptr && !c->timing && !c->no_graph && (!c->tr || c->tr->graph_safe());
+  c->cg_mark = true;   // bracket the coarse solve of every V-cycle (pmg_report t_coarse)
   if (graph_ok && !c->cycle_exec) {
     long long l0 = c->launches;
     cudaGraph_t gr = nullptr;
     CUDA_CHECK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
     pmg_status cs;
+    c->capturing = true;
     if (krylov) {
       cs = ipcg_iter(c);
     } else {
@@ -585,6 +619,7 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
       if (!cs) cs = residual_x(c, c->L, D.u, D.f, D.r);
       if (!cs) cs = dot_owned(c, c->L, D.r, D.r, c->dres);
     }
+    c->capturing = false;
     cudaError_t ce = cudaStreamEndCapture(c->st, &gr);
     if (cs) { if (gr) cudaGraphDestroy(gr); return cs; }
     if (ce != cudaSuccess) return fail(PMG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
@@ -614,7 +649,12 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
     }
     ++cycles;
     if (rep && rep->history && cycles < rep->history_cap) rep->history[cycles] = rn;
+    float cms = 0.f;   // the cycle's stream work has completed (its residual norm was read)
+    if (cudaEventElapsedTime(&cms, c->ev_cg[0], c->ev_cg[1]) == cudaSuccess) c->t_coarse_acc += cms;
+    else cudaGetLastError();   // not recorded (no coarse solve): not an error of the solve
   }
+  c->cg_mark = false;
+  CUDA_CHECK(cudaEventRecord(c->ev_ph[2], c->st));
   if (c->tr) {
     if ((s = exchange(c, c->L, D.u))) return s;
     if ((s = recover_dev(c, D.u, c->Floc, c->Uloc))) return s;
@@ -638,8 +678,16 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
     CUDA_CHECK(cudaStreamSynchronize(c->st));
     if (ks[6] != 0.0) return fail(PMG_EBREAKDOWN, "ipCG breakdown: p^T H p <= 0");
   }
+  CUDA_CHECK(cudaEventRecord(c->ev_ph[3], c->st));
   bool conv = rn <= rtol * r0;
   if (rep) {
+    float t[3] = {0.f, 0.f, 0.f};
+    CUDA_CHECK(cudaEventSynchronize(c->ev_ph[3]));
+    for (int i = 0; i < 3; ++i) CUDA_CHECK(cudaEventElapsedTime(&t[i], c->ev_ph[i], c->ev_ph[i + 1]));
+    rep->t_condense = t[0];
+    rep->t_cycles = t[1];
+    rep->t_recover = t[2];
+    rep->t_coarse = c->t_coarse_acc;
     rep->cycles = cycles;
     rep->converged = conv ? 1 : 0;
     rep->r0 = r0;
@@ -654,7 +702,7 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
 void free_ctx(pmg_ctx* c) {
   if (!c) return;
   for (auto& D : c->D) {
-    cudaFree(D.etab); cudaFree(D.stab); cudaFree(D.stabT); cudaFree(D.ectab); cudaFree(D.Jint);
+    cudaFree(D.etab); cudaFree(D.stab); cudaFree(D.stabT); cudaFree(D.stabP); cudaFree(D.etabP); cudaFree(D.ectab); cudaFree(D.Jint);
     cudaFree(D.u); cudaFree(D.f); cudaFree(D.r);
   }
   cudaFree(c->ticket);
@@ -676,6 +724,8 @@ void free_ctx(pmg_ctx* c) {
   if (c->hres) cudaFreeHost(c->hres);
   ev_reset(c);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->ev_ph) if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->ev_cg) if (e) cudaEventDestroy(e);
   delete c;
 }
 
@@ -822,6 +872,28 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
       stT.insert(stT.end(), Hl.stabT.begin() + (size_t)(V1 + V2 + sp.zb) * n * n, Hl.stabT.begin() + (size_t)(V1 + V2 + sp.z1 + 1) * n * n);
     }
     if ((s = upload(&D.etab, et)) || (s = upload(&D.stab, st)) || (s = upload(&D.stabT, stT))) { free_ctx(c); return s; }
+    if (D.g.p >= 9 && D.g.p <= 16) {   // k_star16's padded table: NP x NP S, then Lambda (pad 1), s, w (pad 0)
+      const int n = D.g.n, NP = star16_np(D.g.p), STP = NP * NP + 3 * NP;
+      const size_t rows = st.size() / D.g.ST;
+      std::vector<double> sp(rows * STP, 0.0);
+      for (size_t q = 0; q < rows; ++q) {
+        const double* src = st.data() + q * D.g.ST;
+        double* dst = sp.data() + q * STP;
+        for (int j = 0; j < n; ++j)
+          for (int a = 0; a < n; ++a) dst[j * NP + a] = src[j * n + a];
+        for (int a = 0; a < NP; ++a) {
+          dst[NP * NP + a] = a < n ? src[n * n + a] : 1.0;
+          dst[NP * NP + NP + a] = a < n ? src[n * n + n + a] : 0.0;
+          dst[NP * NP + 2 * NP + a] = a < n ? src[n * n + 2 * n + a] : 0.0;
+        }
+      }
+      if ((s = upload(&D.stabP, sp))) { free_ctx(c); return s; }
+      const int ETP = elem16_etp(D.g.p);   // k_elem16's padded element table
+      const size_t erows = et.size() / D.g.ET;
+      std::vector<double> ep(erows * ETP, 0.0);
+      for (size_t q = 0; q < erows; ++q) elem16_table_row(D.g.p, et.data() + q * D.g.ET, ep.data() + q * ETP);
+      if ((s = upload(&D.etabP, ep))) { free_ctx(c); return s; }
+    }
     max_elem = std::max(max_elem, hot_smem(D.g.p, 0));
     max_star = std::max(max_star, hot_smem(D.g.p, 1));
     if (l >= 1 && (s = upload(&D.Jint, c->H[l].Jint))) { free_ctx(c); return s; }
@@ -921,7 +993,15 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   }
   cudaError_t e5 = condense_recover_set_smem_attr(smem_optin);
   cudaError_t e6 = cudaSuccess;
+  {
+    const char* e = std::getenv("PMG_NO_STAR16");
+    c->no_star16 = e && e[0] == '1';
+    e = std::getenv("PMG_NO_ELEM16");
+    c->no_elem16 = e && e[0] == '1';
+  }
   if (e6 == cudaSuccess) e6 = hot_set_smem_attr(smem_optin);
+  if (e6 == cudaSuccess) e6 = star16_set_smem_attr();
+  if (e6 == cudaSuccess) e6 = elem16_set_smem_attr();
   if (e1 || e2 || e3 || e4 || e5 || e6) { free_ctx(c); return fail(PMG_ECUDA, "cudaFuncSetAttribute failed"); }
   // persistent cooperative coarse CG when the coarse degree is 2 and the device supports it
   {
@@ -979,6 +1059,8 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
               size_t cur = 0;
               cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
               const size_t want = std::min<size_t>((size_t)maxp, rows);
+              c->l2_limit_prev = cur;   // restored by pmg_destroy
+              c->l2_limit_set = true;
               if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
               cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
               c->ell_win.base_ptr = c->ella;
@@ -1191,6 +1273,10 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
     free_ctx(c);
     return fail(PMG_EINVAL, "z-slabs need the cooperative coarse CG (p0 = 2, cooperative launch support)");
   }
+  for (auto& e : c->ev_ph)
+    if (cudaEventCreate(&e) != cudaSuccess) { free_ctx(c); return fail(PMG_ECUDA, "setup: cudaEventCreate"); }
+  for (auto& e : c->ev_cg)
+    if (cudaEventCreate(&e) != cudaSuccess) { free_ctx(c); return fail(PMG_ECUDA, "setup: cudaEventCreate"); }
   cudaError_t es = cudaDeviceSynchronize();
   if (es != cudaSuccess) { free_ctx(c); return fail(PMG_ECUDA, std::string("setup: ") + cudaGetErrorString(es)); }
   *out = c;
@@ -1200,6 +1286,11 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
 pmg_status pmg_destroy(pmg_ctx* c) {
   if (!c) return fail(PMG_EINVAL, "ctx is NULL");
   cudaStreamSynchronize(c->st);
+  if (c->l2_limit_set) {   // release the set-aside persisting L2 lines of the coarse ELL rows
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, c->l2_limit_prev);
+    cudaGetLastError();
+  }
   free_ctx(c);
   return PMG_OK;
 }

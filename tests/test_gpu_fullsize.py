@@ -90,10 +90,11 @@ def _interior_points(case, rng, nsample):
     return pts
 
 
-@pytest.mark.parametrize("cfg,p", [(2, None), (3, 2), (3, 4), (3, 8), (3, 12), (3, 16), (4, None)])
+@pytest.mark.parametrize("cfg,p", [(2, None), (3, 2), (3, 4), (3, 8), (3, 12), (3, 16), (3, 24), (4, None)])
 def test_fullsize_residual_sampled(cfg, p):
-    """(p = 24, 32: the dense element Schur complement is too large for the oracle; symmetry and the
-    full-size solve cover those degrees.)"""
+    """Bench-size residual at sampled vertex / edge / face points against the oracle's dense element
+    Schur complements (p = 32 is compared element-wise on the small k222_p32 parity mesh instead: the
+    same kernel, k_elem_apply_t<32>)."""
     case = pi.config(cfg, p=p)
     s = _solver(case)
     L = s.nlevels - 1
@@ -120,34 +121,57 @@ def test_fullsize_residual_sampled(cfg, p):
     s.close()
 
 
-def _sampled_vertex_smoother(case, rg, dug, rng, nsample):
-    """Correction at an interior vertex = (H_hat_v^-1 R_v r)(v) (only its own star covers it, W = 1);
-    H_hat_v^-1 = inverse of the condensed operator of the 2x2x2 block (dense LU, oracle)."""
-    from oracle import condensed
+def _sampled_smoother(case, rg, dug, rng, nsample):
+    """Smoother correction at sampled interior skeleton points (vertex, edge-interior and
+    face-interior points, in turn): sum over the stars whose planes contain the point of
+    W_v(x) (H_hat_v^-1 R_v r)(x) (Eq. smoother_definition).  Each star inverse is the
+    dense solve of the oracle's assembled condensed star operator on the 2x2x2-element sub-mesh
+    around v (the block sees nothing else; Dirichlet outside is the block's own boundary),
+    and W_v is the oracle's weight at the point.  A vertex is covered by its own star only (W = 1),
+    an edge point by 2 stars, a face point by 4 (the weighted multi-star sum)."""
+    from oracle import condensed, smoother
     p, k = case.p, case.k
     V = GridView(k, p)
     errs = []
-    for _ in range(nsample):
-        v = [int(rng.integers(1, kd)) for kd in k]
-        sub = _submesh(case, [vd - 1 for vd in v], (2, 2, 2))
-        op = condensed.CondensedOperator(sub, case.lam)
-        fs = np.nonzero(sub.free_skel)[0]
-        Hs = op.assembled_condensed()[fs][:, fs].toarray()
-        # map the submesh's free skeleton points to the global grid
-        n1, n2 = sub.N[0], sub.N[1]
-        j3, rem = np.divmod(fs, n1 * n2)
-        j2, j1 = np.divmod(rem, n1)
-        gidx = V.flat((v[0] - 1) * p + j1, (v[1] - 1) * p + j2, (v[2] - 1) * p + j3)
-        x = np.linalg.solve(Hs, rg[gidx])
-        centre = int(np.nonzero((j1 == p) & (j2 == p) & (j3 == p))[0][0])
-        want = x[centre]
-        got = dug[V.flat(v[0] * p, v[1] * p, v[2] * p)]
-        errs.append(abs(got - want) / np.abs(x).max())
+    blocks = {}
+    for i in range(nsample):
+        kind = i % 3
+        x = [int(rng.integers(2, kd - 1)) * p for kd in k]          # an interior vertex, one element from the box
+        if kind >= 1:
+            x[0] += int(rng.integers(1, p))                          # edge along x1
+        if kind == 2:
+            x[1] += int(rng.integers(1, p))                          # face normal to x3
+        stars = [(v1, v2, v3) for v1 in {x[0] // p, -(-x[0] // p)} for v2 in {x[1] // p, -(-x[1] // p)}
+                 for v3 in {x[2] // p, -(-x[2] // p)}
+                 if sum(int(x[d] == vd * p) for d, vd in enumerate((v1, v2, v3))) >= 1]
+        assert len(stars) == (1, 2, 4)[kind], stars
+        want, scale = 0.0, 0.0
+        for v in stars:
+            sub = _submesh(case, [vd - 1 for vd in v], (2, 2, 2))
+            key = (tuple(np.round(np.concatenate(sub.widths), 15)), case.lam)
+            if key not in blocks:
+                op = condensed.CondensedOperator(sub, case.lam)
+                pts, loc = smoother.star_points(sub, (1, 1, 1))
+                H = smoother.star_matrix_block(op, (1, 1, 1), pts)
+                blocks[key] = (pts, loc, np.linalg.inv(H), smoother.star_weights(sub, (1, 1, 1), loc))
+            pts, loc, Hinv, W = blocks[key]
+            n1, n2 = sub.N[0], sub.N[1]
+            j3, rem = np.divmod(pts, n1 * n2)
+            j2, j1 = np.divmod(rem, n1)
+            gidx = V.flat((v[0] - 1) * p + j1, (v[1] - 1) * p + j2, (v[2] - 1) * p + j3)
+            xs = Hinv @ rg[gidx]
+            at = int(np.nonzero(gidx == V.flat(*x))[0][0])
+            want += W[at] * xs[at]
+            scale = max(scale, np.abs(xs).max())
+        errs.append(abs(dug[V.flat(*x)] - want) / scale)
     return max(errs)
 
 
-@pytest.mark.parametrize("cfg,p", [(2, None), (3, 4), (3, 8), (3, 12), (3, 16), (3, 24), (4, None)])
+@pytest.mark.parametrize("cfg,p", [(2, None), (3, 2), (3, 4), (3, 8), (3, 12), (3, 16), (3, 24), (4, None)])
 def test_fullsize_smoother_sampled(cfg, p):
+    """The bench-size smoother (every production star kernel: k_star_w at p <= 4 on these meshes,
+    k_star_pf, k_star_tm) at sampled vertex, edge and face points against the oracle's dense star
+    solves and weights."""
     case = pi.config(cfg, p=p)
     s = _solver(case)
     L = s.nlevels - 1
@@ -159,8 +183,38 @@ def test_fullsize_smoother_sampled(cfg, p):
     du = s.new_skel(L)
     s.smooth(L, r, du)
     dug = _grid_of(s, L, du)
-    err = _sampled_vertex_smoother(case, rgr, dug, rng, 3)
+    err = _sampled_smoother(case, rgr, dug, rng, 6)
     assert err < 1e-11, err
+    s.close()
+
+
+@pytest.mark.parametrize("p,stretch,lam", [(2, None, 0.0), (3, 1.02, 0.4), (4, 1.05, 0.7)])
+def test_large_mesh_operators_full_vector(p, stretch, lam):
+    """29 x 28 x 28 elements (>= 2960 stars per colour: the warp-per-star kernel k_star_w that the
+    p = 2 / 4 levels of configs 3-5 run) -- residual and smoother on every level of the hierarchy
+    against the oracle element-wise (full vectors)."""
+    from oracle import mg
+    k = (29, 28, 28)
+    case = pi.small_case(k, p, lam, stretch=stretch)
+    s = _solver(case, coarse_rtol=1e-13)
+    for l in range(s.nlevels):
+        deg = s.level_info(l)[0]
+        lv = mg.Level(case.k, case.widths, deg, lam, 7)
+        m = lv.mesh
+        rng = np.random.default_rng(40 + l)
+        u = rng.standard_normal(m.ntot) * m.free_skel
+        f = rng.standard_normal(m.ntot) * m.free_skel
+        us, fs, r, du = s.new_skel(l), s.new_skel(l), s.new_skel(l), s.new_skel(l)
+        s.skel_from_grid(l, torch.from_numpy(u).cuda(), us)
+        s.skel_from_grid(l, torch.from_numpy(f).cuda(), fs)
+        s.residual(l, us, fs, r)
+        s.smooth(l, fs, du)
+        rg, dg = _grid_of(s, l, r), _grid_of(s, l, du)
+        want_r, want_s = lv.op.residual(u, f), lv.smoother.apply(f)
+        for got, want in ((rg, want_r), (dg, want_s)):
+            e2 = np.linalg.norm(got - want) / np.linalg.norm(want)
+            ei = np.abs(got - want).max() / np.abs(want).max()
+            assert e2 < 1e-11 and ei < 1e-10, (l, e2, ei)
     s.close()
 
 

@@ -13,6 +13,10 @@ pytestmark = pytest.mark.gpu
 OP_TOL = 1e-11
 SOLVE_TOL = 1e-9
 
+# Every degree class of the production kernels has a case: p <= 4 (k_star_pf / k_star_w, k_elem_pf),
+# 5..8 (k_star_pf, k_elem_pf), 9..16 (k_star_pf<P> with n_S padded to 32, k_elem_pf16), 17..32
+# (k_star_tm, k_elem_apply_t); each hierarchy also runs the lower levels' kernels.  p = 32 needs
+# ~60 GB of host memory for the oracle's dense p = 32 element Schur complement.
 CASES = {
     "k323_p4_lam1.7_stretched": dict(k=(3, 2, 3), p=4, lam=1.7, stretch=1.6),
     "k232_p5_lam0": dict(k=(2, 3, 2), p=5, lam=0.0, stretch=None),
@@ -20,12 +24,30 @@ CASES = {
     "k422_p3_lam0.5": dict(k=(4, 2, 2), p=3, lam=0.5, stretch=1.3),
     "k332_p2_lam0": dict(k=(3, 3, 2), p=2, lam=0.0, stretch=None),
     "k222_p6_lam2": dict(k=(2, 2, 2), p=6, lam=2.0, stretch=1.2),
+    "k222_p12_lam0.3_stretched": dict(k=(2, 2, 2), p=12, lam=0.3, stretch=1.3),
+    "k322_p16_lam0": dict(k=(3, 2, 2), p=16, lam=0.0, stretch=None),
+    "k223_p13_lam4_stretched": dict(k=(2, 2, 3), p=13, lam=4.0, stretch=1.4),
+    "k222_p24_lam1": dict(k=(2, 2, 2), p=24, lam=1.0, stretch=None),
+    "k222_p32_lam0": dict(k=(2, 2, 2), p=32, lam=0.0, stretch=None),
 }
+BIG_HOST = {"k222_p32_lam0": 120}     # GB of available host memory the oracle needs
 
 
 def rel(a, b):
     nb = np.linalg.norm(b)
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def rel_inf(a, b):
+    nb = np.abs(b).max() if np.size(b) else 0.0
+    return np.abs(a - b).max() / (nb if nb > 0 else 1.0) if np.size(b) else 0.0
+
+
+def close(a, b, tol):
+    """Relative 2-norm error below tol and, alongside (SURVEY 8(c) parity protocol), relative max-norm
+    error below 10 tol (a single entry can carry more of the rounding than the 2-norm average)."""
+    e2, ei = rel(a, b), rel_inf(a, b)
+    return e2 < tol and ei < 10 * tol
 
 
 class Pair:
@@ -68,6 +90,11 @@ _PAIRS = {}
 
 def pair(name):
     if name not in _PAIRS:
+        need = BIG_HOST.get(name)
+        if need:
+            import psutil
+            if psutil.virtual_memory().available < need * 2 ** 30:
+                pytest.skip("oracle needs ~%d GB of host memory for this degree" % need)
         _PAIRS[name] = Pair(**CASES[name])
     return _PAIRS[name]
 
@@ -106,10 +133,10 @@ def test_residual_parity(name):
         u, f = P.rand_skel(l), P.rand_skel(l)
         r = P.gpu.new_skel(l)
         P.gpu.residual(l, P.to_skel(l, u), P.to_skel(l, f), r)
-        assert rel(P.to_grid(l, r), op.residual(u, f)) < OP_TOL, l
+        assert close(P.to_grid(l, r), op.residual(u, f), OP_TOL), l
         q = P.gpu.new_skel(l)
         P.gpu.residual(l, P.to_skel(l, u), None, q)              # operator apply
-        assert rel(P.to_grid(l, q), op.apply(u)) < OP_TOL, l
+        assert close(P.to_grid(l, q), op.apply(u), OP_TOL), l
 
 
 @pytest.mark.parametrize("name", list(CASES))
@@ -133,7 +160,7 @@ def test_smooth_parity(name):
         u = P.to_skel(l, u0)
         P.gpu.smooth(l, P.to_skel(l, r), u)
         want = u0 + sm.apply(r)
-        assert rel(P.to_grid(l, u) - u0, want - u0) < OP_TOL, l
+        assert close(P.to_grid(l, u) - u0, want - u0, OP_TOL), l
 
 
 @pytest.mark.parametrize("name", [n for n in CASES if CASES[n]["p"] > 2])
@@ -144,11 +171,11 @@ def test_transfer_parity(name):
         rf = P.rand_skel(l)
         fc = P.gpu.new_skel(l - 1)
         P.gpu.restrict(l, P.to_skel(l, rf), fc)
-        assert rel(P.to_grid(l - 1, fc), T.restrict(rf)) < OP_TOL, l
+        assert close(P.to_grid(l - 1, fc), T.restrict(rf), OP_TOL), l
         uc, uf0 = P.rand_skel(l - 1), P.rand_skel(l)
         uf = P.to_skel(l, uf0)
         P.gpu.prolong(l, P.to_skel(l - 1, uc), uf)
-        assert rel(P.to_grid(l, uf), uf0 + T.prolong(uc)) < OP_TOL, l
+        assert close(P.to_grid(l, uf) - uf0, T.prolong(uc), OP_TOL), l
 
 
 @pytest.mark.parametrize("name", list(CASES))
@@ -161,12 +188,12 @@ def test_condense_recover_parity(name):
     Fd = torch.from_numpy(F).cuda()
     fh = P.gpu.new_skel(L)
     P.gpu.condense(Fd, fh)
-    assert rel(P.to_grid(L, fh), op.condense(F)) < OP_TOL
+    assert close(P.to_grid(L, fh), op.condense(F), OP_TOL)
     uh = P.rand_skel(L)
     ug = P.gpu.new_grid()
     P.gpu.recover(P.to_skel(L, uh), Fd, ug)
     torch.cuda.synchronize()
-    assert rel(ug.cpu().numpy(), op.recover(uh, F)) < OP_TOL
+    assert close(ug.cpu().numpy(), op.recover(uh, F), OP_TOL)
 
 
 @pytest.mark.parametrize("name", list(CASES))
@@ -177,7 +204,7 @@ def test_vcycle_parity(name):
     u = P.to_skel(L, u0)
     P.gpu.vcycle(u, P.to_skel(L, f))
     want = P.orc.vcycle(u0, f)
-    assert rel(P.to_grid(L, u), want) < OP_TOL
+    assert close(P.to_grid(L, u), want, OP_TOL)
 
 
 @pytest.mark.parametrize("name", list(CASES))
@@ -193,8 +220,11 @@ def test_solve_parity(name):
     rep = P.gpu.solve(torch.from_numpy(F).cuda(), ug, 1e-10)
     torch.cuda.synchronize()
     assert rep["converged"] and rep["cycles"] == rep_o["cycles"]
-    assert rel(ug.cpu().numpy(), u_orc) < SOLVE_TOL
+    assert close(ug.cpu().numpy(), u_orc, SOLVE_TOL)
     assert abs(rep["r0"] - rep_o["r0"]) <= 1e-12 * rep_o["r0"]
+    # phase times of the report: all measured, the coarse solves inside the cycle loop
+    assert rep["t_condense"] > 0 and rep["t_cycles"] > 0 and rep["t_recover"] > 0
+    assert 0 < rep["t_coarse"] <= rep["t_cycles"]
 
 
 def test_smoother_deterministic():
@@ -245,7 +275,7 @@ def test_coarse_cg_paths_agree(name, monkeypatch):
         outs.append(g.cpu().numpy())
         s.close()
     assert rel(outs[0], outs[1]) < 1e-11
-    assert rel(outs[0], P.orc.vcycle(np.zeros_like(f), f)) < OP_TOL
+    assert close(outs[0], P.orc.vcycle(np.zeros_like(f), f), OP_TOL)
 
 
 @pytest.mark.parametrize("kind", ["registers", "ell"])
@@ -312,30 +342,61 @@ def test_krylov_solve_parity(name, schedule):
     assert rep["converged"] and rep["cycles"] == rep_o["cycles"], (rep["cycles"], rep_o["cycles"])
     h, ho = np.array(rep["history"]), np.array(rep_o["history"])
     assert np.all(np.abs(h - ho) <= 1e-8 * ho[0]), (h, ho)
-    assert rel(ug.cpu().numpy(), u_o) < SOLVE_TOL
+    assert close(ug.cpu().numpy(), u_o, SOLVE_TOL)
     s.close()
 
 
-@pytest.mark.parametrize("solver,alpha", [("kMG", 1), ("kMG", 1.5), ("kMG", 2), ("MG", 1.5)])
-def test_gpu_iteration_counts_match_paper_table(solver, alpha):
-    """Table tab:stretched_poly_iterations on the GPU path at p = 4: 8^3 elements on
-    (0, 2 pi)^3 with expansion factor alpha (reading R13), lambda = 0, random RHS, 1e-10 drop."""
-    import json
-    import math
-    import os
+TABLE_SOLVERS = {"MG": dict(solver=0, schedule=0), "kMG": dict(solver=1, schedule=0), "kvMG": dict(solver=1, schedule=1)}
+
+
+def _gpu_iters(k, widths, p, solver):
     import paper_1808_03595_b200 as pmg
-    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "stretched_poly_iterations.json")))
-    want = gold[solver][str(alpha)][gold["p"].index(4)]
-    k = (8, 8, 8)
-    w = [pi.geometric_widths(8, 2 * math.pi, alpha)] * 3
-    s = pmg.Solver(k, w, 4, 0.0, solver=1 if solver != "MG" else 0)
+    s = pmg.Solver(k, widths, p, 0.0, **TABLE_SOLVERS[solver])
     f = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, s.level_info(s.nlevels - 1)[2])).cuda()
     F = s.new_grid()
     s.weak_rhs(f, F)
     u = s.new_grid()
-    rep = s.solve(F, u, 1e-10, max_cycles=60)
-    assert rep["converged"] and abs(rep["cycles"] - want) <= 1, (rep["cycles"], want)
+    rep = s.solve(F, u, 1e-10, max_cycles=200)
+    torch.cuda.synchronize()
     s.close()
+    return rep
+
+
+@pytest.mark.parametrize("p", [4, 8, 16, 32])
+@pytest.mark.parametrize("alpha", [1, 1.5, 2])
+def test_gpu_iteration_counts_match_paper_table(alpha, p):
+    """All 36 cells of Table tab:stretched_poly_iterations -- MG, kMG and kvMG (Alg. 4 / 5,
+    nu = 1 or 2^(L-l)) at p = 4, 8, 16, 32 and expansion factor alpha = 1, 1.5, 2 (reading R13) -- on
+    the GPU path: 8^3 elements on (0, 2 pi)^3, lambda = 0, random RHS, 1e-10 drop; within +-1 of the
+    printed count (the paper's random RHS and coarse tolerance are unstated)."""
+    import json
+    import math
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "stretched_poly_iterations.json")))
+    w = [pi.geometric_widths(8, 2 * math.pi, alpha)] * 3
+    for solver in ("MG", "kMG", "kvMG"):
+        want = gold[solver][str(alpha)][gold["p"].index(p)]
+        rep = _gpu_iters((8, 8, 8), w, p, solver)
+        assert rep["converged"] and abs(rep["cycles"] - want) <= 1, (solver, rep["cycles"], want)
+
+
+def test_gpu_anisotropic_meshes_paper_claims():
+    """Sec. 5.3: 8^3 elements of degree 16 on (0, 2 pi AR) x (0, pi ceil(AR/2)) x (0, 2 pi).
+    The figure's data are not in the source, so the text's claims are checked: MG needs about three
+    iterations at AR = 1 and "increases from three to sixty" at AR = 48; Krylov acceleration "helps,
+    but does not completely remove the effect"; more smoothing per level (kvMG) "keeps the number of
+    iterations mostly stable until AR = 8"."""
+    import math
+
+    def iters(AR, solver):
+        L = (2 * math.pi * AR, math.pi * math.ceil(AR / 2), 2 * math.pi)
+        return _gpu_iters((8, 8, 8), pi.uniform_widths((8, 8, 8), L), 16, solver)["cycles"]
+    mg1, mg48 = iters(1, "MG"), iters(48, "MG")
+    k1, k48 = iters(1, "kMG"), iters(48, "kMG")
+    kv1, kv8 = iters(1, "kvMG"), iters(8, "kvMG")
+    assert 2 <= mg1 <= 4 and 40 <= mg48 <= 80, (mg1, mg48)
+    assert k48 < mg48 / 2 and k48 > 2 * k1, (k1, k48, mg48)
+    assert kv8 <= kv1 + 2, (kv1, kv8)
 
 
 @pytest.mark.parametrize("k,p", [((1, 1, 1), 4), ((1, 2, 3), 3), ((1, 1, 4), 2), ((2, 1, 1), 6)])
@@ -354,7 +415,7 @@ def test_degenerate_meshes(k, p):
     rep = s.solve(torch.from_numpy(F).cuda(), ug, 1e-10)
     torch.cuda.synchronize()
     assert rep["cycles"] == rep_o["cycles"], (rep["cycles"], rep_o["cycles"])
-    assert rel(ug.cpu().numpy(), u_o) < SOLVE_TOL
+    assert close(ug.cpu().numpy(), u_o, SOLVE_TOL)
     s.close()
 
 
@@ -479,23 +540,23 @@ def test_neumann_operators_parity(name):
         f = P.rand_skel(l)
         r = P.gpu.new_skel(l)
         P.gpu.residual(l, P.to_skel(l, u), P.to_skel(l, f), r)
-        assert rel(P.to_grid(l, r), orc.op.residual(u, f)) < OP_TOL
+        assert close(P.to_grid(l, r), orc.op.residual(u, f), OP_TOL)
         du = P.gpu.new_skel(l)
         P.gpu.smooth(l, P.to_skel(l, f), du)
-        assert rel(P.to_grid(l, du), orc.smoother.apply(f)) < OP_TOL
+        assert close(P.to_grid(l, du), orc.smoother.apply(f), OP_TOL)
         if l >= 1:
             T = P.orc.transfers[l]
             fc = P.gpu.new_skel(l - 1)
             P.gpu.restrict(l, P.to_skel(l, f), fc)
-            assert rel(P.to_grid(l - 1, fc), T.restrict(f)) < OP_TOL
+            assert close(P.to_grid(l - 1, fc), T.restrict(f), OP_TOL)
             uc = P.rand_skel(l - 1)
             uf = P.gpu.new_skel(l)
             P.gpu.prolong(l, P.to_skel(l - 1, uc), uf)
-            assert rel(P.to_grid(l, uf), T.prolong(uc)) < OP_TOL
+            assert close(P.to_grid(l, uf), T.prolong(uc), OP_TOL)
     f = P.rand_skel(L)
     u = P.gpu.new_skel(L)
     P.gpu.vcycle(u, P.to_skel(L, f))
-    assert rel(P.to_grid(L, u), P.orc.vcycle(np.zeros_like(f), f)) < OP_TOL
+    assert close(P.to_grid(L, u), P.orc.vcycle(np.zeros_like(f), f), OP_TOL)
 
 
 @pytest.mark.parametrize("name", list(NEUMANN_CASES))
@@ -510,7 +571,7 @@ def test_neumann_solve_parity(name):
     rep = P.gpu.solve(torch.from_numpy(F).cuda(), ug, 1e-10)
     torch.cuda.synchronize()
     assert rep["converged"] and rep["cycles"] == rep_o["cycles"], (rep["cycles"], rep_o["cycles"])
-    assert rel(ug.cpu().numpy(), u_orc) < SOLVE_TOL
+    assert close(ug.cpu().numpy(), u_orc, SOLVE_TOL)
 
 
 @pytest.mark.parametrize("neu,kind", [(0b111111, "cos"), (0b111100, "sin")])
@@ -573,13 +634,13 @@ def test_hmg_coarse_solver_parity(name):
     g = s.new_grid(L)
     s.skel_to_grid(L, u, g)
     torch.cuda.synchronize()
-    assert rel(g.cpu().numpy(), orc.vcycle(np.zeros_like(f), f)) < OP_TOL
+    assert close(g.cpu().numpy(), orc.vcycle(np.zeros_like(f), f), OP_TOL)
     F = condensed.weak_rhs(m, pi.uniform_pm1(8, np.arange(m.ntot)))
     u_o, rep_o = orc.solve(F, 1e-10)
     ug = s.new_grid()
     rep = s.solve(torch.from_numpy(F).cuda(), ug, 1e-10)
     torch.cuda.synchronize()
-    assert rep["cycles"] == rep_o["cycles"] and rel(ug.cpu().numpy(), u_o) < SOLVE_TOL
+    assert rep["cycles"] == rep_o["cycles"] and close(ug.cpu().numpy(), u_o, SOLVE_TOL)
     s.close()
 
 
@@ -623,4 +684,28 @@ def test_zero_rhs_returns_zero(solver):
     u_o, rep_o = orc.solve(np.zeros(F.numel()), 1e-10)
     assert rep["converged"] and rep["cycles"] == rep_o["cycles"] == 0 and rep["r0"] == 0.0
     assert float(u.abs().max()) == 0.0 and np.abs(u_o).max() == 0.0
+    s.close()
+
+
+@pytest.mark.parametrize("name", ["k323_p4_lam1.7_stretched", "k422_p3_lam0.5", "k332_p2_lam0"])
+def test_warp_star_kernel_forced_parity(name, monkeypatch):
+    """The warp-per-star smoother kernel (k_star_w, p <= 4) that the large meshes of configs 3-5 run on
+    their p = 2 / 4 levels, forced onto the ragged parity meshes (every star boundary case: padded
+    lines, Dirichlet corners, stretched widths) and compared with the oracle on every level."""
+    import paper_1808_03595_b200 as pmg
+    monkeypatch.setenv("PMG_STAR_W_MIN", "0")
+    P = pair(name)
+    case = P.case
+    s = pmg.Solver(case.k, case.widths, case.p, case.lam, coarse_rtol=1e-13)
+    for l in range(s.nlevels):
+        sm = P.orc.levels[l].smoother
+        r = P.rand_skel(l)
+        rs = s.new_skel(l)
+        s.skel_from_grid(l, torch.from_numpy(r).cuda(), rs)
+        du = s.new_skel(l)
+        s.smooth(l, rs, du)
+        g = s.new_grid(l)
+        s.skel_to_grid(l, du, g)
+        torch.cuda.synchronize()
+        assert close(g.cpu().numpy(), sm.apply(r), OP_TOL), l
     s.close()

@@ -147,3 +147,38 @@ def test_krylov_accelerates_on_stretched_mesh():
     H_mg = _iters(2, 4)
     H_k = _iters_krylov(2, 4, 0)
     assert H_k["cycles"] < H_mg["cycles"]
+
+
+@pytest.mark.parametrize("schedule,ratio,limit", [(0, 1 / 8, 8 / 7), (1, 1 / 4, 4 / 3)])
+def test_smoothing_schedule_effort_per_level(schedule, ratio, limit, monkeypatch):
+    """P:557-558 (Sec. 4.4): with constant smoothing the effort of a coarser level is 1/8 of the next
+    finer one (geometric series <= 8/7); with nu_pre,l = nu_post,l = 2^(L-l) it is 2 (1/2)^3 = 1/4
+    (series <= 4/3), the finest level smoothing once before and once after.  Counted from
+    the smoothing steps one oracle V-cycle actually performs (p = 16: L = 3, degrees 2, 4, 8, 16;
+    the smoother costs O(p_l^3) per element).  A wrong exponent in the schedule (2^l,
+    2^(L-l+1)) changes either the finest count or the ratio."""
+    k = (2, 2, 2)
+    H = mg.Hierarchy(k, pi.uniform_widths(k, (1.0, 1.0, 1.0)), 16, 0.0, schedule=schedule)
+    calls = [0] * (H.L + 1)
+    orig = H.smooth_step
+
+    def counting(l, u, f):
+        calls[l] += 1
+        return orig(l, u, f)
+    monkeypatch.setattr(H, "smooth_step", counting)
+    f = np.random.default_rng(0).standard_normal(H.levels[-1].mesh.ntot) * H.levels[-1].mesh.free_skel
+    H.vcycle(np.zeros_like(f), f)
+    assert calls[H.L] == 2 and calls[0] == 0
+    effort = [calls[l] * H.degrees[l] ** 3 for l in range(H.L + 1)]
+    for l in range(2, H.L + 1):
+        assert effort[l - 1] == ratio * effort[l], (calls, effort)
+    assert sum(effort) / effort[H.L] < limit
+
+
+@pytest.mark.parametrize("solver", ["kMG", "kvMG"])
+def test_krylov_counts_p16_match_paper_table(solver):
+    """Table tab:stretched_poly_iterations, alpha = 1, p = 16: kMG 3, kvMG 2 (+-1)."""
+    gold = json.load(open(GOLD))
+    want = gold[solver]["1"][gold["p"].index(16)]
+    rep = _iters_krylov(1, 16, 0 if solver == "kMG" else 1)
+    assert rep["converged"] and abs(rep["cycles"] - want) <= 1, (rep["cycles"], want)
