@@ -173,41 +173,38 @@ __global__ void __launch_bounds__(128, 3)
   asm volatile("cp.async.wait_group 0;\n" ::);
   __syncthreads();
   const int r8 = lane >> 2, q4 = lane & 3;
-  // ---- forward transforms: X_f = U_f P_a^T, then T_f = P_b X_f (2 x 2 tile blocks: one job per
-  // face and GEMM, 12 DMMA jobs per stage over 4 warps)
-  constexpr int T8 = MP / 8;
-  auto gemm = [&](auto TA, auto TB, const double* A, int lda, const double* B, int ldb, double* Cm, int ldc) {
-    // C (MP x MP) = op(A) op(B); one warp
-    for (int mi = 0; mi < T8; ++mi)
-      for (int ni = 0; ni < T8; ni += 2) {
-        double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-        const bool two = ni + 1 < T8;
+  // ---- forward transforms: X_f = U_f P_a^T, then T_f = P_b X_f.  Jobs = (face, 8-row tile panel):
+  // 6 T8 jobs per stage over the 4 warps, each panel 1 x T8 tiles (one A fragment per k step serves
+  // every tile of the panel)
+  constexpr int T8 = MP / 8, NJ = 6 * T8;
+  auto panel = [&](auto TA, auto TB, const double* A, int lda, const double* B, int ldb, double* Cm, int ldc, int mi) {
+    double c[T8][2];
 #pragma unroll
-        for (int kk = 0; kk < MP / 4; ++kk) {
-          const int k = 4 * kk + q4, ii = 8 * mi + r8;
-          const double a = decltype(TA)::value ? A[k * lda + ii] : A[ii * lda + k];
-          const int j0 = 8 * ni + r8, j1 = j0 + 8;
-          const double b0 = decltype(TB)::value ? B[j0 * ldb + k] : B[k * ldb + j0];
-          dmma_e(c[0][0], c[0][1], a, b0);
-          if (two) {
-            const double b1 = decltype(TB)::value ? B[j1 * ldb + k] : B[k * ldb + j1];
-            dmma_e(c[1][0], c[1][1], a, b1);
-          }
-        }
-        *reinterpret_cast<double2*>(Cm + (8 * mi + r8) * ldc + 8 * ni + 2 * q4) = make_double2(c[0][0], c[0][1]);
-        if (two) *reinterpret_cast<double2*>(Cm + (8 * mi + r8) * ldc + 8 * ni + 8 + 2 * q4) = make_double2(c[1][0], c[1][1]);
+    for (int j = 0; j < T8; ++j) c[j][0] = c[j][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < MP / 4; ++kk) {
+      const int k = 4 * kk + q4, ii = 8 * mi + r8;
+      const double a = decltype(TA)::value ? A[k * lda + ii] : A[ii * lda + k];
+#pragma unroll
+      for (int j = 0; j < T8; ++j) {
+        const int jj = 8 * j + r8;
+        dmma_e(c[j][0], c[j][1], a, decltype(TB)::value ? B[jj * ldb + k] : B[k * ldb + jj]);
       }
+    }
+#pragma unroll
+    for (int j = 0; j < T8; ++j)
+      *reinterpret_cast<double2*>(Cm + (8 * mi + r8) * ldc + 8 * j + 2 * q4) = make_double2(c[j][0], c[j][1]);
   };
   using TT = std::true_type;
   using FF = std::false_type;
-  for (int f = warp; f < 6; f += 4) {   // X_f = U_f,int P_a^T
-    const int d = f >> 1, da = (d == 0) ? 1 : 0;
-    gemm(FF{}, TT{}, Uc + f * FS + LDT + 1, LDT, tb + da * ETP + K::oP, LDT, X + f * MS, LDT);
+  for (int job = warp; job < NJ; job += 4) {   // X_f = U_f,int P_a^T
+    const int f = job / T8, mi = job - f * T8, d = f >> 1, da = (d == 0) ? 1 : 0;
+    panel(FF{}, TT{}, Uc + f * FS + LDT + 1, LDT, tb + da * ETP + K::oP, LDT, X + f * MS, LDT, mi);
   }
   __syncthreads();
-  for (int f = warp; f < 6; f += 4) {   // T_f = P_b X_f
-    const int d = f >> 1, db = (d == 2) ? 1 : 2;
-    gemm(FF{}, FF{}, tb + db * ETP + K::oP, LDT, X + f * MS, LDT, T + f * MS, LDT);
+  for (int job = warp; job < NJ; job += 4) {   // T_f = P_b X_f
+    const int f = job / T8, mi = job - f * T8, d = f >> 1, db = (d == 2) ? 1 : 2;
+    panel(FF{}, FF{}, tb + db * ETP + K::oP, LDT, X + f * MS, LDT, T + f * MS, LDT, mi);
   }
   __syncthreads();
   // ---- core over the interior eigen-triples (b1 lanes, b3 per 16-lane group, b2 in registers)
@@ -314,59 +311,85 @@ __global__ void __launch_bounds__(128, 3)
     __syncthreads();
   }
   // ---- back transforms: X_f = G_f P_a, then C_f = P_b^T X_f (into T)
-  for (int f = warp; f < 6; f += 4) {
-    const int d = f >> 1, da = (d == 0) ? 1 : 0;
-    gemm(FF{}, FF{}, T + f * MS, LDT, tb + da * ETP + K::oP, LDT, X + f * MS, LDT);
+  for (int job = warp; job < NJ; job += 4) {
+    const int f = job / T8, mi = job - f * T8, d = f >> 1, da = (d == 0) ? 1 : 0;
+    panel(FF{}, FF{}, T + f * MS, LDT, tb + da * ETP + K::oP, LDT, X + f * MS, LDT, mi);
   }
   __syncthreads();
-  for (int f = warp; f < 6; f += 4) {
-    const int d = f >> 1, db = (d == 2) ? 1 : 2;
-    gemm(TT{}, FF{}, tb + db * ETP + K::oP, LDT, X + f * MS, LDT, T + f * MS, LDT);
+  for (int job = warp; job < NJ; job += 4) {
+    const int f = job / T8, mi = job - f * T8, d = f >> 1, db = (d == 2) ? 1 : 2;
+    panel(TT{}, FF{}, tb + db * ETP + K::oP, LDT, X + f * MS, LDT, T + f * MS, LDT, mi);
   }
   __syncthreads();
   // ---- H_BB tangential line sums of the face interiors: Z_f = U_f K~_a^T + K~_b U_f (t = 1 .. MP;
-  // beyond t = p the table is zero), one accumulation (into X)
-  for (int f = warp; f < 6; f += 4) {
-    const int d = f >> 1, da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2;
+  // beyond t = p the table is zero), both products accumulated in one tile panel (into X)
+  for (int job = warp; job < NJ; job += 4) {
+    const int f = job / T8, mi = job - f * T8, d = f >> 1, da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2;
     const double* U = Uc + f * FS + LDT + 1;                 // U[tb-1][t-1]
     const double* Ka = tb + da * ETP + K::oK + LDT + 1;      // Ka[ta-1][t-1] = K~_a[ta][t]
     const double* Kb = tb + db * ETP + K::oK + LDT + 1;
-    for (int mi = 0; mi < T8; ++mi)
-      for (int ni = 0; ni < T8; ++ni) {
-        double c0 = 0.0, c1 = 0.0;
+    double c[T8][2];
 #pragma unroll
-        for (int kk = 0; kk < MP / 4; ++kk) {
-          const int k = 4 * kk + q4, ii = 8 * mi + r8, jj = 8 * ni + r8;
-          dmma_e(c0, c1, U[ii * LDT + k], Ka[jj * LDT + k]);     // sum_t U[tb][t] K~a[ta][t]
-          dmma_e(c0, c1, Kb[ii * LDT + k], U[k * LDT + jj]);     // sum_t K~b[tb][t] U[t][ta]
-        }
-        *reinterpret_cast<double2*>(X + f * MS + (8 * mi + r8) * LDT + 8 * ni + 2 * q4) = make_double2(c0, c1);
+    for (int j = 0; j < T8; ++j) c[j][0] = c[j][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < MP / 4; ++kk) {
+      const int k = 4 * kk + q4, ii = 8 * mi + r8;
+      const double ua = U[ii * LDT + k], kb = Kb[ii * LDT + k];
+#pragma unroll
+      for (int j = 0; j < T8; ++j) {
+        const int jj = 8 * j + r8;
+        dmma_e(c[j][0], c[j][1], ua, Ka[jj * LDT + k]);     // sum_t U[tb][t] K~a[ta][t]
+        dmma_e(c[j][0], c[j][1], kb, U[k * LDT + jj]);      // sum_t K~b[tb][t] U[t][ta]
       }
+    }
+#pragma unroll
+    for (int j = 0; j < T8; ++j)
+      *reinterpret_cast<double2*>(X + f * MS + (8 * mi + r8) * LDT + 8 * j + 2 * q4) = make_double2(c[j][0], c[j][1]);
   }
   __syncthreads();
-  // ---- outputs: face interiors, then edges and vertices (all three lines lie on the boundary)
+  // ---- outputs: face interiors (thread = block position (A, B), all six faces), then edges and
+  // vertices (all three lines lie on the element boundary)
   auto Mv = [&](int d) { return tb + d * ETP + K::oM; };
   auto Kt = [&](int d) { return tb + d * ETP + K::oK; };
   double* Ye = Y + (size_t)e * g.YS;
-  for (int o = tid; o < 6 * MM; o += NT) {
-    const int f = o / MM, r = o - f * MM, A = r / M, B = r - A * M, d = f >> 1, s_ = f & 1;
-    const int da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2;
-    const int td = s_ * P, ta = B + 1, tbb = A + 1;
-    const double* Uf = Uc + f * FS;
-    const double* Kd = Kt(d);
-    const double uv = Uf[tbb * LDT + ta];
-    double z = X[f * MS + A * LDT + B];
-    z = fma(Kt(da)[ta * LDT], Uf[tbb * LDT], z);                     // t = 0 term along a
-    z = fma(Kt(db)[tbb * LDT], Uf[ta], z);                           // t = 0 term along b
-    z = fma(Kd[td * LDT], Uc[(2 * d) * FS + tbb * LDT + ta], z);     // normal line: the two faces
-    z = fma(Kd[td * LDT + P], Uc[(2 * d + 1) * FS + tbb * LDT + ta], z);
-    z = fma(lam, uv, z);
-    Ye[o] = Mv(d)[td] * Mv(da)[ta] * Mv(db)[tbb] * z - T[f * MS + A * LDT + B];
+#pragma unroll
+  for (int k = 0; k < (MM + NT - 1) / NT; ++k) {
+    const int l = tid + k * NT;
+    if (l < MM) {
+      const int A = l / M, B = l - A * M, ta = B + 1, tbb = A + 1;
+#pragma unroll
+      for (int f = 0; f < 6; ++f) {
+        const int d = f >> 1, s_ = f & 1, da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2, td = s_ * P;
+        const double* Uf = Uc + f * FS;
+        const double* Kd = Kt(d);
+        double z = X[f * MS + A * LDT + B];
+        z = fma(Kt(da)[ta * LDT], Uf[tbb * LDT], z);                     // t = 0 term along a
+        z = fma(Kt(db)[tbb * LDT], Uf[ta], z);                           // t = 0 term along b
+        z = fma(Kd[td * LDT], Uc[(2 * d) * FS + tbb * LDT + ta], z);     // normal line: the two faces
+        z = fma(Kd[td * LDT + P], Uc[(2 * d + 1) * FS + tbb * LDT + ta], z);
+        z = fma(lam, Uf[tbb * LDT + ta], z);
+        Ye[f * MM + l] = Mv(d)[td] * Mv(da)[ta] * Mv(db)[tbb] * z - T[f * MS + A * LDT + B];
+      }
+    }
   }
-  auto getU = [&](int t1, int t2, int t3) -> double {   // boundary point of the element cube
-    if (t1 == 0 || t1 == P) return Uc[(t1 == P ? 1 : 0) * FS + t3 * LDT + t2];
-    if (t2 == 0 || t2 == P) return Uc[(2 + (t2 == P ? 1 : 0)) * FS + t3 * LDT + t1];
-    return Uc[(4 + (t3 == P ? 1 : 0)) * FS + t2 * LDT + t1];
+  // a boundary line along d through (t1, t2, t3) lies in a face whose normal n != d has t_n in {0, p}:
+  // in that face's closed array it is a row (d the fast direction) or a column
+  auto line = [&](int d, int t1, int t2, int t3) -> double {
+    int n;
+    if (d != 0 && (t1 == 0 || t1 == P)) n = 0;
+    else if (d != 1 && (t2 == 0 || t2 == P)) n = 1;
+    else n = 2;
+    const int tn = n == 0 ? t1 : (n == 1 ? t2 : t3);
+    const int fa = (n == 0) ? 1 : 0;                        // fast direction of the face
+    const int ta = fa == 0 ? t1 : t2, tbb = n == 2 ? t2 : t3;
+    const double* Uf = Uc + (2 * n + (tn == P ? 1 : 0)) * FS;
+    const double* ptr = (d == fa) ? Uf + tbb * LDT : Uf + ta;
+    const int st = (d == fa) ? 1 : LDT;
+    const double* Kr = Kt(d) + (d == 0 ? t1 : (d == 1 ? t2 : t3)) * LDT;
+    double z = 0.0;
+#pragma unroll
+    for (int t = 0; t <= P; ++t) z = fma(Kr[t], ptr[t * st], z);
+    return z;
   };
   for (int o = 6 * MM + tid; o < YS; o += NT) {
     int t1, t2, t3;
@@ -379,13 +402,14 @@ __global__ void __launch_bounds__(128, 3)
       const int qv = o - 6 * MM - 12 * M;
       t1 = (qv & 1) * P; t2 = ((qv >> 1) & 1) * P; t3 = ((qv >> 2) & 1) * P;
     }
-    double z = lam * getU(t1, t2, t3);
-#pragma unroll
-    for (int t = 0; t <= P; ++t) {
-      z = fma(Kt(0)[t1 * LDT + t], getU(t, t2, t3), z);
-      z = fma(Kt(1)[t2 * LDT + t], getU(t1, t, t3), z);
-      z = fma(Kt(2)[t3 * LDT + t], getU(t1, t2, t), z);
-    }
+    // the point's own value: in the face normal x1 if t1 is on the boundary, else x2, else x3
+    const int n = (t1 == 0 || t1 == P) ? 0 : ((t2 == 0 || t2 == P) ? 1 : 2);
+    const int tn = n == 0 ? t1 : (n == 1 ? t2 : t3);
+    const int ta = n == 0 ? t2 : t1, tbb = n == 2 ? t2 : t3;
+    double z = lam * Uc[(2 * n + (tn == P ? 1 : 0)) * FS + tbb * LDT + ta];
+    z += line(0, t1, t2, t3);
+    z += line(1, t1, t2, t3);
+    z += line(2, t1, t2, t3);
     Ye[o] = Mv(0)[t1] * Mv(1)[t2] * Mv(2)[t3] * z;
   }
 }

@@ -138,7 +138,6 @@ __global__ void __launch_bounds__(128, 3)
   long long* lb = reinterpret_cast<long long*>(sm + K::oLb);
   const long long V12 = (long long)g.V1 * g.V2;
   const long long rec0 = v1 + g.V1 * (long long)v2 + V12 * v3;
-  const bool interior = v1 > 0 && v2 > 0 && v3 > 0 && v1 < g.k1 && v2 < g.k2 && v3 + g.zoff < g.K3;
   // ---- setup tables (before the dependency wait): S_d padded NP x NP, then Lambda, s, w
   {
     auto row = [&](int d) -> size_t {   // star-table row of the vertex line along direction d
@@ -180,11 +179,19 @@ __global__ void __launch_bounds__(128, 3)
   pdl_wait();
   pdl_trigger();
   // ---- gather the three star planes of r (zero outside the stored box)
-  for (int idx = tid; idx < 12 * MM; idx += NT) {
-    const int f = idx / MM, l = idx - f * MM, Al = l / M, Bl = l - Al * M;
-    const int d = f >> 2, qa = (f >> 1) & 1, qb = f & 1;
-    const long long b = fb[f];
-    cpa8(&R[d * MS + (Al + qa * P) * LD + Bl + qb * P], r + (b < 0 ? 0 : b + Al * M + Bl), b >= 0);
+  // face blocks: thread t owns block positions l = t, t + NT (decoded once), for all 12 blocks
+#pragma unroll
+  for (int k = 0; k < (MM + NT - 1) / NT; ++k) {
+    const int l = tid + k * NT;
+    if (l < MM) {
+      const int Al = l / M, Bl = l - Al * M, lo = Al * LD + Bl;
+#pragma unroll
+      for (int f = 0; f < 12; ++f) {
+        const int d = f >> 2, qa = (f >> 1) & 1, qb = f & 1;
+        const long long b = fb[f];
+        cpa8(&R[d * MS + qa * P * LD + qb * P + lo], r + (b < 0 ? 0 : b + l), b >= 0);
+      }
+    }
   }
   // the two vertex lines of each plane: plane 0 rows A = c (x2 line) / cols B = c (x3 line), plane 1
   // A = c (x1 line) / B = c (x3 line), plane 2 A = c (x1 line) / B = c (x2 line)
@@ -344,38 +351,35 @@ __global__ void __launch_bounds__(128, 3)
   }
   // ---- weighted scatter-add of the unique star points (u += W U; one colour's stars are disjoint)
   const double *w1 = vec + 2 * NP, *w2 = vec + 5 * NP, *w3 = vec + 8 * NP;
-  auto freept = [&](int j1, int j2, int j3) {   // star point -> free unknown of the (global) mesh?
-    return is_free(g, (v1 - 1) * P + 1 + j1, (v2 - 1) * P + 1 + j2, (v3 - 1) * P + 1 + j3);
-  };
-  // faces: two passes (loads first, then stores) in register batches of EPT points per thread
-  constexpr int FE = 12 * MM, EPT = (FE + NT - 1) / NT;
-  double uo[EPT];
+  // Points that are not unknowns (Dirichlet faces, stored entries outside the box) get U = 0
+  // exactly: their rows of S_d are identity rows, their r entries are zero, and the vertex row s_d
+  // vanishes on them, so u there is rewritten unchanged and no free-point test is needed.  Faces:
+  // loads of the thread's u entries first (two block positions x 12 blocks), then the stores.
+  constexpr int KR = (MM + NT - 1) / NT;
+  double uo[KR][12];
 #pragma unroll
-  for (int k = 0; k < EPT; ++k) {
-    const int idx = tid + k * NT;
-    uo[k] = 0.0;
-    if (idx < FE) {
-      const int f = idx / MM, l = idx - f * MM, Al = l / M, Bl = l - Al * M;
+  for (int k = 0; k < KR; ++k) {
+    const int l = tid + k * NT;
+#pragma unroll
+    for (int f = 0; f < 12; ++f) {
       const long long b = fb[f];
-      if (b >= 0) uo[k] = u[b + Al * M + Bl];
+      uo[k][f] = (l < MM && b >= 0) ? u[b + l] : 0.0;
     }
   }
 #pragma unroll
-  for (int k = 0; k < EPT; ++k) {
-    const int idx = tid + k * NT;
-    if (idx < FE) {
-      const int f = idx / MM, l = idx - f * MM, Al = l / M, Bl = l - Al * M;
-      const int d = f >> 2, qa = (f >> 1) & 1, qb = f & 1;
-      const int A = Al + qa * P, B = Bl + qb * P;
-      const long long b = fb[f];
-      if (b < 0) continue;
-      int j1, j2, j3;
-      double W;
-      if (d == 0) { j1 = C; j2 = B; j3 = A; W = w2[B] * w3[A]; }
-      else if (d == 1) { j2 = C; j1 = B; j3 = A; W = w1[B] * w3[A]; }
-      else { j3 = C; j1 = B; j2 = A; W = w1[B] * w2[A]; }
-      if (!interior && !freept(j1, j2, j3)) continue;
-      u[b + Al * M + Bl] = fma(W, R[d * MS + A * LD + B], uo[k]);
+  for (int k = 0; k < KR; ++k) {
+    const int l = tid + k * NT;
+    if (l < MM) {
+      const int Al = l / M, Bl = l - Al * M;
+#pragma unroll
+      for (int f = 0; f < 12; ++f) {
+        const int d = f >> 2, qa = (f >> 1) & 1, qb = f & 1;
+        const int A = Al + qa * P, B = Bl + qb * P;
+        const long long b = fb[f];
+        if (b < 0) continue;
+        const double W = d == 0 ? w2[B] * w3[A] : (d == 1 ? w1[B] * w3[A] : w1[B] * w2[A]);
+        u[b + l] = fma(W, R[d * MS + A * LD + B], uo[k][f]);
+      }
     }
   }
   // the three vertex lines (x2 line and x3 line from plane 0 -- the vertex with the x2 line --, x1 line
@@ -388,12 +392,12 @@ __global__ void __launch_bounds__(128, 3)
       if (j < C) src = lb[2 * e] < 0 ? -1LL : lb[2 * e] + j;
       else if (j == C) src = base[0] < 0 ? -1LL : base[0] + 3 * MM + 3 * M;
       else src = lb[2 * e + 1] < 0 ? -1LL : lb[2 * e + 1] + (j - P);
-      int j1 = C, j2 = C, j3 = C, o;
+      int o;
       double W;
-      if (e3 == 0) { j2 = j; o = C * LD + j; W = w2[j]; }                 // plane 0, A = c, B = j
-      else if (e3 == 1) { j3 = j; o = j * LD + C; W = w3[j]; }            // plane 0, A = j, B = c
-      else { j1 = j; o = MS + C * LD + j; W = w1[j]; }                    // plane 1, A = c, B = j
-      if (src >= 0 && (interior || freept(j1, j2, j3))) {
+      if (e3 == 0) { o = C * LD + j; W = w2[j]; }                 // plane 0, A = c, B = j
+      else if (e3 == 1) { o = j * LD + C; W = w3[j]; }            // plane 0, A = j, B = c
+      else { o = MS + C * LD + j; W = w1[j]; }                    // plane 1, A = c, B = j
+      if (src >= 0) {
         const double uold = u[src];
         u[src] = fma(W, R[o], uold);
       }
