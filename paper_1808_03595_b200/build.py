@@ -7,7 +7,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpmg.so")
-SOURCES = ["setup_host.cpp", "comm.cpp", "kernels.cu", "hot_kernels.cu", "star16.cu", "elem16.cu", "coarse_cg.cu", "ec_smoother.cu", "pmg_api.cu"]
+SOURCES = ["setup_host.cpp", "comm.cpp", "kernels.cu", "hot_kernels.cu", "star16.cu", "elem16.cu", "cr16.cu", "coarse_cg.cu", "ec_smoother.cu", "pmg_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xptxas", "-v"]

@@ -50,6 +50,7 @@ __device__ __forceinline__ void cpa16e(double* dst, const double* src) {
 //   [oP]  P[b][i] = S[i][b] M_II[i]  (MP x LDT, zero padded)
 //   [oL]  Lambda[b] (MP, padded with 1)      [oA0] a0[b], [oA1] a1[b] (MP, zero padded)
 //   [oM]  M[t], t = 0..p (LDT, zero padded)  [oK]  K~[t][t'] = K[t][t'] / M[t] ((P+1) x LDT, zero padded)
+//   [oS]  S[i][b] (MP x LDT, zero padded): interior eigenvectors, S^T K_II S = Lambda, S^T M_II S = I
 template <int P> struct Elem16 {
   static constexpr int M = P - 1, Q = P + 1, MM = M * M;
   static constexpr int MP = (P + 7) / 8 * 8;               // transform size; index MP-1 >= m reaches t = p
@@ -59,6 +60,9 @@ template <int P> struct Elem16 {
   static constexpr int MS = MP * LDT;                        // transform matrix stride
   static constexpr int oP = 0, oL = MS, oA0 = oL + MP, oA1 = oA0 + MP, oM = oA1 + MP, oK = oM + LDT,
                        ETP = oK + Q * LDT + ((Q * LDT) & 1);
+  // the table row continues with S[i][b] (MP x LDT) for condensation / recovery (cr16.cu); the
+  // element operator copies only the first ETP doubles of a row
+  static constexpr int oS = ETP, ETS = ETP + MS;
   static constexpr int NT = 128;
   static constexpr int YS = 6 * MM + 12 * M + 8;
   // shared memory (doubles): three table rows, six closed faces, X (6 MS), T / G / C (6 MS)
@@ -68,9 +72,9 @@ template <int P> struct Elem16 {
 template <int P>
 size_t elem16_smem2() { return sizeof(double) * Elem16<P>::total; }
 
-int elem16_etp(int p) {
+int elem16_etp(int p) {   // row stride of the padded element table
   switch (p) {
-#define CASE(PP) case PP: return Elem16<PP>::ETP;
+#define CASE(PP) case PP: return Elem16<PP>::ETS;
     CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
 #undef CASE
     default: return 0;
@@ -92,6 +96,9 @@ void elem16_table_row(int p, const double* et, double* out) {
   for (int t = 0; t < q; ++t) out[oM + t] = et[et_M(p) + t];
   for (int t = 0; t < q; ++t)
     for (int s = 0; s < q; ++s) out[oK + t * LDT + s] = et[et_K(p) + t * q + s] / et[et_M(p) + t];
+  const int oS = oK + q * LDT + ((q * LDT) & 1);
+  for (int i = 0; i < m; ++i)
+    for (int b = 0; b < m; ++b) out[oS + i * LDT + b] = et[et_S(p) + i * m + b];
 }
 
 template <int P>
@@ -107,23 +114,24 @@ __global__ void __launch_bounds__(128, 3)
   double* Uc = sm + K::oU;
   double* X = sm + K::oX;
   double* T = sm + K::oT;
-  const long long e = blockIdx.x;
-  const int e1 = (int)(e % g.k1), e2 = (int)((e / g.k1) % g.k2), e3 = (int)(e / ((long long)g.k1 * g.k2));
+  const int e1 = blockIdx.x, e2 = blockIdx.y, e3 = blockIdx.z;   // 3-D grid over the elements
+  const long long e = e1 + (long long)g.k1 * (e2 + (long long)g.k2 * e3);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // ---- tables (before the dependency wait)
   {
     for (int i = tid; i < 3 * (ETP / 2); i += NT) {
       const int d = i / (ETP / 2), ch = i - d * (ETP / 2);
       const size_t row = d == 0 ? (size_t)e1 : (d == 1 ? (size_t)(g.k1 + e2) : (size_t)(g.k1 + g.k2 + e3));
-      cpa16e(tb + d * ETP + 2 * ch, etabP + row * ETP + 2 * ch);
+      cpa16e(tb + d * ETP + 2 * ch, etabP + row * K::ETS + 2 * ch);
     }
     asm volatile("cp.async.commit_group;\n" ::);
   }
   // closed-face rows / columns beyond t = p (p < MP) are read by the padded transforms: zero them
-  if constexpr (UR > Q || LDT > Q) {
-    for (int i = tid; i < 6 * FS; i += NT) {
-      const int r_ = (i % FS) / LDT, c_ = i % LDT;
-      if (r_ >= Q || c_ >= Q) Uc[i] = 0.0;
+  if constexpr (UR > Q) {   // p < MP: rows and columns Q .. MP of the closed faces are read
+    for (int i = tid; i < 6 * UR * (UR - Q); i += NT) {
+      const int f = i / (UR * (UR - Q)), rr = i - f * UR * (UR - Q), a = rr / (UR - Q), b = Q + rr - a * (UR - Q);
+      Uc[f * FS + a * LDT + b] = 0.0;   // columns Q .. MP of every row
+      Uc[f * FS + b * LDT + a] = 0.0;   // rows Q .. MP
     }
   }
   pdl_wait();
@@ -136,10 +144,17 @@ __global__ void __launch_bounds__(128, 3)
     const long long V12 = (long long)g.V1 * g.V2;
     const long long rec0 = e1 + g.V1 * (long long)e2 + V12 * e3;
     auto recb = [&](int o1, int o2, int o3) { return (rec0 + o1 + g.V1 * (long long)o2 + V12 * o3) * RS; };
-    for (int idx = tid; idx < 6 * MM; idx += NT) {
-      const int f = idx / MM, l = idx - f * MM, A = l / M, B = l - A * M, d = f >> 1, s = f & 1;
-      const long long b = recb(d == 0 ? s : 0, d == 1 ? s : 0, d == 2 ? s : 0) + d * MM;
-      cpa8e(&Uc[f * FS + (A + 1) * LDT + B + 1], u + b + A * M + B);
+#pragma unroll
+    for (int k = 0; k < (MM + NT - 1) / NT; ++k) {   // face interiors: thread = block position l
+      const int l = tid + k * NT;
+      if (l < MM) {
+        const int A = l / M, B = l - A * M, lo = (A + 1) * LDT + B + 1;
+#pragma unroll
+        for (int f = 0; f < 6; ++f) {
+          const int d = f >> 1, s = f & 1;
+          cpa8e(&Uc[f * FS + lo], u + recb(d == 0 ? s : 0, d == 1 ? s : 0, d == 2 ? s : 0) + d * MM + l);
+        }
+      }
     }
     // rim: 4 p points per face, (tb, ta) walked around the boundary
     for (int idx = tid; idx < 6 * 4 * P; idx += NT) {
@@ -419,8 +434,8 @@ cudaError_t launch_elem16(const LevelGeom& g, const double* u, const double* eta
   switch (g.p) {
 #define CASE(PP)                                                                                                      \
   case PP:                                                                                                            \
-    return launch_pdl(k_elem16<PP>, dim3((unsigned)g.nelem), dim3(Elem16<PP>::NT), elem16_smem2<PP>(), st, g, u, etabP, \
-                      lam, Y, done);
+    return launch_pdl(k_elem16<PP>, dim3((unsigned)g.k1, (unsigned)g.k2, (unsigned)g.k3), dim3(Elem16<PP>::NT),            \
+                      elem16_smem2<PP>(), st, g, u, etabP, lam, Y, done);
     CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
 #undef CASE
     default: return cudaErrorInvalidValue;

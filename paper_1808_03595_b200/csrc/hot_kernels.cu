@@ -278,707 +278,7 @@ __global__ void __launch_bounds__(ElemCfg<P>::NT) k_elem_apply_t(LevelGeom g, co
 }
 
 // ------------------------------------------------------------------------------------------
-// element operator for P <= 8 with the 24 face transforms per element on DMMA (m = p - 1 padded to
-// 8, exact), a shared 1/D table (one rcp per eigen-triple instead of three), and face-interior
-// outputs evaluated from the two closed faces they depend on (row / column line sums).
-// ------------------------------------------------------------------------------------------
-template <int P> struct ElemDmCfg {
-  static constexpr int M = P - 1, Q = P + 1, MM = M * M, QQ = Q * Q, MP = 8, LD = 12, MS = MP * LD;
-  static constexpr int NT = 128, NW = 4;
-  using E = ElemCfg<P>;
-  static constexpr int TB = E::TB;
-  static constexpr int oUc = 0, oTab = 6 * QQ, oPp = oTab + 3 * TB, oPtp = oPp + 3 * MS, oA = oPtp + 3 * MS,
-                       oT = oA + 6 * MS, oG = oT + 6 * MS, oInv = oG + 6 * MS, total = oInv + MM * M;
-};
-
-template <int P>
-size_t elem_dm_smem() { return sizeof(double) * ElemDmCfg<P>::total; }
-
-template <int P>
-__global__ void __launch_bounds__(128) k_elem_dm(LevelGeom g, const double* __restrict__ u,
-                                                 const double* __restrict__ etab, double lam,
-                                                 double* __restrict__ Y, const int* __restrict__ done) {
-  using C = ElemDmCfg<P>;
-  using EC = ElemCfg<P>;
-  constexpr int M = C::M, Q = C::Q, MM = C::MM, QQ = C::QQ, NT = C::NT, TB = C::TB, LD = C::LD, MS = C::MS, MP = C::MP;
-  if (done && *done) return;
-  extern __shared__ double sm[];
-  double* Uc = sm + C::oUc;
-  double* tb = sm + C::oTab;
-  double* Pp = sm + C::oPp;
-  double* Ptp = sm + C::oPtp;
-  double* Ab = sm + C::oA;     // padded face interiors, later the back-transform intermediate
-  double* T = sm + C::oT;
-  double* G = sm + C::oG;
-  double* invD = sm + C::oInv;
-  const long long e = blockIdx.x;
-  const int e1 = (int)(e % g.k1), e2 = (int)((e / g.k1) % g.k2), e3 = (int)(e / ((long long)g.k1 * g.k2));
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int ET = g.ET;
-  {
-    const double* src[3] = {etab + (size_t)e1 * ET, etab + (size_t)(g.k1 + e2) * ET, etab + (size_t)(g.k1 + g.k2 + e3) * ET};
-    for (int i = tid; i < 3 * TB; i += NT) {
-      const int d = i / TB, o = i - d * TB;
-      const double* s = src[d];
-      double v;
-      if (o < EC::tP) v = s[et_lam(P) + o];
-      else if (o < EC::tPt) v = s[et_P(P) + (o - EC::tP)];
-      else if (o < EC::ta0) { int r = o - EC::tPt, ia = r / M, b = r - ia * M; v = s[et_P(P) + b * M + ia]; }
-      else if (o < EC::ta1) v = s[et_a0(P) + (o - EC::ta0)];
-      else if (o < EC::tM) v = s[et_a1(P) + (o - EC::ta1)];
-      else if (o < EC::tK) v = s[et_M(P) + (o - EC::tM)];
-      else v = s[et_K(P) + (o - EC::tK)];
-      tb[i] = v;
-    }
-    for (int i = tid; i < 3 * MP * MP; i += NT) {   // padded P[b][i] and Pt[i][b]
-      const int d = i / (MP * MP), rr = i - d * MP * MP, A = rr / MP, B = rr - A * MP;
-      const bool in = A < M && B < M;
-      Pp[d * MS + A * LD + B] = in ? src[d][et_P(P) + A * M + B] : 0.0;
-      Ptp[d * MS + A * LD + B] = in ? src[d][et_P(P) + B * M + A] : 0.0;
-    }
-  }
-  for (int i = tid; i < 6 * QQ; i += NT) {
-    const int f = i / QQ, r = i - f * QQ, A = r / Q, B = r - A * Q, d = f >> 1, s = f & 1;
-    int t1, t2, t3;
-    if (d == 0) { t1 = s * P; t3 = A; t2 = B; }
-    else if (d == 1) { t2 = s * P; t3 = A; t1 = B; }
-    else { t3 = s * P; t2 = A; t1 = B; }
-    Uc[i] = __ldg(&u[skel_index_t<P>(g, e1 * P + t1, e2 * P + t2, e3 * P + t3)]);
-  }
-  __syncthreads();
-  for (int i = tid; i < 6 * MP * MP; i += NT) {     // padded face interiors; zero G's padding
-    const int f = i / (MP * MP), rr = i - f * MP * MP, A = rr / MP, B = rr - A * MP;
-    Ab[f * MS + A * LD + B] = (A < M && B < M) ? Uc[f * QQ + (A + 1) * Q + B + 1] : 0.0;
-    G[f * MS + A * LD + B] = 0.0;
-  }
-  for (int i = tid; i < MM * M; i += NT) {          // 1/D over the interior eigen-triples
-    const int b3 = i / MM, rr = i - b3 * MM, b2 = rr / M, b1 = rr - b2 * M;
-    invD[i] = rcp_nr(lam + tb[EC::tLam + b1] + tb[TB + EC::tLam + b2] + tb[2 * TB + EC::tLam + b3]);
-  }
-  __syncthreads();
-  // tangential directions of face f: a = x2 for d = 0 else x1 ; b = x3 for d < 2 else x2
-  for (int f = warp; f < 6; f += C::NW) {            // forward A: X_f = U_f Pt_a  (X into T)
-    const int d = f >> 1, da = (d == 0) ? 1 : 0;
-    dmma_tile<MP, LD>(Ab + f * MS, Ptp + da * MS, T + f * MS, 0, 0, lane);
-  }
-  __syncthreads();
-  for (int f = warp; f < 6; f += C::NW) {            // forward B: T_f = P_b X_f  (into Ab)
-    const int d = f >> 1, db = (d == 2) ? 1 : 2;
-    dmma_tile<MP, LD>(Pp + db * MS, T + f * MS, Ab + f * MS, 0, 0, lane);
-  }
-  __syncthreads();
-  {
-    const double *a10 = tb + EC::ta0, *a11 = tb + EC::ta1;
-    const double *a20 = tb + TB + EC::ta0, *a21 = tb + TB + EC::ta1;
-    const double *a30 = tb + 2 * TB + EC::ta0, *a31 = tb + 2 * TB + EC::ta1;
-    const double *T0 = Ab, *T1 = Ab + MS, *T2 = Ab + 2 * MS, *T3 = Ab + 3 * MS, *T4 = Ab + 4 * MS, *T5 = Ab + 5 * MS;
-    for (int i = tid; i < 3 * MM; i += NT) {
-      const int pass = i / MM, r = i - pass * MM, hi = r / M, lo = r - hi * M;
-      double g0 = 0.0, g1 = 0.0;
-      if (pass == 0) {          // (b3, b2), reduce over b1 -> faces 0, 1
-        const int b3 = hi, b2 = lo;
-        const double tA = T0[b3 * LD + b2], tB = T1[b3 * LD + b2], c2 = a20[b2], c2b = a21[b2], c3 = a30[b3], c3b = a31[b3];
-#pragma unroll
-        for (int b1 = 0; b1 < M; ++b1) {
-          double Ev = a10[b1] * tA;
-          Ev = fma(a11[b1], tB, Ev);
-          Ev = fma(c2, T2[b3 * LD + b1], Ev);
-          Ev = fma(c2b, T3[b3 * LD + b1], Ev);
-          Ev = fma(c3, T4[b2 * LD + b1], Ev);
-          Ev = fma(c3b, T5[b2 * LD + b1], Ev);
-          const double V = Ev * invD[(b3 * M + b2) * M + b1];
-          g0 = fma(a10[b1], V, g0);
-          g1 = fma(a11[b1], V, g1);
-        }
-        G[0 * MS + b3 * LD + b2] = g0;
-        G[1 * MS + b3 * LD + b2] = g1;
-      } else if (pass == 1) {   // (b3, b1), reduce over b2 -> faces 2, 3
-        const int b3 = hi, b1 = lo;
-        const double tA = T2[b3 * LD + b1], tB = T3[b3 * LD + b1], c1 = a10[b1], c1b = a11[b1], c3 = a30[b3], c3b = a31[b3];
-#pragma unroll
-        for (int b2 = 0; b2 < M; ++b2) {
-          double Ev = c1 * T0[b3 * LD + b2];
-          Ev = fma(c1b, T1[b3 * LD + b2], Ev);
-          Ev = fma(a20[b2], tA, Ev);
-          Ev = fma(a21[b2], tB, Ev);
-          Ev = fma(c3, T4[b2 * LD + b1], Ev);
-          Ev = fma(c3b, T5[b2 * LD + b1], Ev);
-          const double V = Ev * invD[(b3 * M + b2) * M + b1];
-          g0 = fma(a20[b2], V, g0);
-          g1 = fma(a21[b2], V, g1);
-        }
-        G[2 * MS + b3 * LD + b1] = g0;
-        G[3 * MS + b3 * LD + b1] = g1;
-      } else {                  // (b2, b1), reduce over b3 -> faces 4, 5
-        const int b2 = hi, b1 = lo;
-        const double tA = T4[b2 * LD + b1], tB = T5[b2 * LD + b1], c1 = a10[b1], c1b = a11[b1], c2 = a20[b2], c2b = a21[b2];
-#pragma unroll
-        for (int b3 = 0; b3 < M; ++b3) {
-          double Ev = c1 * T0[b3 * LD + b2];
-          Ev = fma(c1b, T1[b3 * LD + b2], Ev);
-          Ev = fma(c2, T2[b3 * LD + b1], Ev);
-          Ev = fma(c2b, T3[b3 * LD + b1], Ev);
-          Ev = fma(a30[b3], tA, Ev);
-          Ev = fma(a31[b3], tB, Ev);
-          const double V = Ev * invD[(b3 * M + b2) * M + b1];
-          g0 = fma(a30[b3], V, g0);
-          g1 = fma(a31[b3], V, g1);
-        }
-        G[4 * MS + b2 * LD + b1] = g0;
-        G[5 * MS + b2 * LD + b1] = g1;
-      }
-    }
-  }
-  __syncthreads();
-  for (int f = warp; f < 6; f += C::NW) {            // back A: X_f = G_f P_a   (into T)
-    const int d = f >> 1, da = (d == 0) ? 1 : 0;
-    dmma_tile<MP, LD>(G + f * MS, Pp + da * MS, T + f * MS, 0, 0, lane);
-  }
-  __syncthreads();
-  for (int f = warp; f < 6; f += C::NW) {            // back B: C_f = P_b^T X_f  (into G)
-    const int d = f >> 1, db = (d == 2) ? 1 : 2;
-    dmma_tile<MP, LD>(Ptp + db * MS, T + f * MS, G + f * MS, 0, 0, lane);
-  }
-  __syncthreads();
-  const double* Mv[3] = {tb + EC::tM, tb + TB + EC::tM, tb + 2 * TB + EC::tM};
-  const double* Kv[3] = {tb + EC::tK, tb + TB + EC::tK, tb + 2 * TB + EC::tK};
-  double* Ye = Y + (size_t)e * g.YS;
-  constexpr int YS = 6 * MM + 12 * M + 8;
-  for (int o = tid; o < YS; o += NT) {
-    double y;
-    if (o < 6 * MM) {      // face interior: closed-face row / column sums and the opposite face
-      const int f = o / MM, r = o - f * MM, A = r / M, B = r - A * M, d = f >> 1, s = f & 1;
-      const int da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2;
-      const int td = s * P, ta = B + 1, tb_ = A + 1;
-      const double* Uf = Uc + f * QQ;
-      const double *Kd = Kv[d], *Ka = Kv[da], *Kb = Kv[db];
-      const double Md = Mv[d][td], Ma = Mv[da][ta], Mb = Mv[db][tb_];
-      double sa = 0.0, sb = 0.0;
-#pragma unroll
-      for (int t = 0; t <= P; ++t) {
-        sa = fma(Ka[ta * Q + t], Uf[tb_ * Q + t], sa);
-        sb = fma(Kb[tb_ * Q + t], Uf[t * Q + ta], sb);
-      }
-      const double sd = Kd[td * Q] * Uc[(2 * d) * QQ + tb_ * Q + ta] + Kd[td * Q + P] * Uc[(2 * d + 1) * QQ + tb_ * Q + ta];
-      y = lam * Md * Ma * Mb * Uf[tb_ * Q + ta];
-      y = fma(Ma * Mb, sd, y);
-      y = fma(Md * Mb, sa, y);
-      y = fma(Md * Ma, sb, y);
-      y -= G[f * MS + A * LD + B];
-    } else {               // edges and vertices: all three lines lie on the element boundary
-      int t1, t2, t3;
-      if (o < 6 * MM + 12 * M) {
-        const int r = o - 6 * MM, qe = r / M, i = r - qe * M, d = qe >> 2, sA = qe & 1, sB = (qe >> 1) & 1;
-        if (d == 0) { t1 = i + 1; t2 = sA * P; t3 = sB * P; }
-        else if (d == 1) { t2 = i + 1; t1 = sA * P; t3 = sB * P; }
-        else { t3 = i + 1; t1 = sA * P; t2 = sB * P; }
-      } else {
-        const int qv = o - 6 * MM - 12 * M;
-        t1 = (qv & 1) * P; t2 = ((qv >> 1) & 1) * P; t3 = ((qv >> 2) & 1) * P;
-      }
-      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-      for (int t = 0; t <= P; ++t) {
-        s1 = fma(Kv[0][t1 * Q + t], getUc<P>(Uc, t, t2, t3), s1);
-        s2 = fma(Kv[1][t2 * Q + t], getUc<P>(Uc, t1, t, t3), s2);
-        s3 = fma(Kv[2][t3 * Q + t], getUc<P>(Uc, t1, t2, t), s3);
-      }
-      const double m1 = Mv[0][t1], m2 = Mv[1][t2], m3 = Mv[2][t3];
-      y = lam * m1 * m2 * m3 * getUc<P>(Uc, t1, t2, t3);
-      y = fma(m2 * m3, s1, y);
-      y = fma(m1 * m3, s2, y);
-      y = fma(m1 * m2, s3, y);
-    }
-    Ye[o] = y;
-  }
-}
-
-// ------------------------------------------------------------------------------------------
-// star smoother, one colour, degree P (n = 2P - 1, vertex index c = P - 1)
-// ------------------------------------------------------------------------------------------
-template <int P> struct StarCfg {
-  static constexpr int N = 2 * P - 1, NN = N * N, C = P - 1;
-  static constexpr int NT = (P <= 4) ? 64 : (P <= 8 ? 128 : 256);
-  static constexpr bool S_SMEM = (P <= 16);         // S and S^T staged in shared memory
-  static constexpr int XPL = 3;                      // planes per transform step
-  // X aliases G in the forward transform and FT in the back transform; U is written into G
-  static constexpr int oFT = 0, oG = 3 * NN, oVec = 6 * NN, oS = oVec + 9 * N;
-  static constexpr int total = oS + (S_SMEM ? 6 * NN : 0);
-};
-
-template <int P>
-size_t star_t_smem() { return sizeof(double) * StarCfg<P>::total; }
-
-// star table (global) per direction and vertex line: [S n^2][Lambda n][s n][w n]; S^T is built on the fly
-template <int P>
-__global__ void __launch_bounds__(StarCfg<P>::NT) k_star_t(LevelGeom g, int c1, int c2, int c3, int n1c, int n2c,
-                                                          const double* __restrict__ r, double* __restrict__ u,
-                                                          const double* __restrict__ stab, const double* __restrict__ stabT,
-                                                          double lam) {
-  pdl_wait();
-  pdl_trigger();
-  using C = StarCfg<P>;
-  constexpr int N = C::N, NN = C::NN, c = C::C, NT = C::NT, XPL = C::XPL;
-  extern __shared__ double sm[];
-  const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
-  const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
-  if (star_empty(g, v1, v2, v3)) return;
-  if (v3 < g.own_lo) return;   // ghost star below the slab: computed by the lower rank
-  const int tid = threadIdx.x, ST = g.ST;
-  const size_t row[3] = {(size_t)v1, (size_t)(g.V1 + v2), (size_t)(g.V1 + g.V2 + v3)};
-  double* FT = sm + C::oFT;
-  double* Gs = sm + C::oG;
-  double* X = Gs;
-  double* vec = sm + C::oVec;
-  const double* S[3];
-  const double* St[3];
-  if (C::S_SMEM) {
-    double* Ssm = sm + C::oS;
-    for (int i = tid; i < 6 * NN; i += NT) {
-      const int k = i / NN, o = i - k * NN;     // k = 0..2: S of direction k; 3..5: S^T
-      Ssm[i] = (k < 3) ? __ldg(&stab[row[k] * ST + o]) : __ldg(&stabT[row[k - 3] * NN + o]);
-    }
-    for (int d = 0; d < 3; ++d) { S[d] = Ssm + d * NN; St[d] = Ssm + (3 + d) * NN; }
-  } else {
-    for (int d = 0; d < 3; ++d) { S[d] = stab + row[d] * ST; St[d] = stabT + row[d] * NN; }
-  }
-  for (int i = tid; i < 9 * N; i += NT) { const int d = i / (3 * N); vec[i] = __ldg(&stab[row[d] * ST + NN + i - d * 3 * N]); }
-  const int o1 = (v1 - 1) * P + 1, o2 = (v2 - 1) * P + 1, o3 = (v3 - 1) * P + 1;
-  for (int i = tid; i < 3 * NN; i += NT) {
-    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
-    int j1, j2, j3;
-    if (d == 0) { j1 = c; j2 = B; j3 = A; } else if (d == 1) { j2 = c; j1 = B; j3 = A; } else { j3 = c; j1 = B; j2 = A; }
-    const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
-    const double val = inside(g, g1, g2, g3) ? __ldg(&r[skel_index_t<P>(g,g1, g2, g3)]) : 0.0;
-    FT[i] = val * (1.0 / (double)(1 + (A == c) + (B == c)));   // inverse multiplicity
-  }
-  __syncthreads();
-  // forward: X_d[jb][aa] = sum_ja F_d[jb][ja] S_a[ja][aa];  T_d[ab][aa] = sum_jb S_b[jb][ab] X_d[jb][aa]
-  for (int d0 = 0; d0 < 3; d0 += XPL) {
-    for (int i = tid; i < XPL * NN; i += NT) {
-      const int dd = i / NN, rr = i - dd * NN, jb = rr / N, aa = rr - jb * N, d = d0 + dd;
-      const double* Sa = S[d == 0 ? 1 : 0];
-      const double* F = FT + d * NN + jb * N;
-      double s = 0.0;
-#pragma unroll
-      for (int ja = 0; ja < N; ++ja) s = fma(F[ja], Sa[ja * N + aa], s);
-      X[i] = s;
-    }
-    __syncthreads();
-    for (int i = tid; i < XPL * NN; i += NT) {
-      const int dd = i / NN, rr = i - dd * NN, ab = rr / N, aa = rr - ab * N, d = d0 + dd;
-      const double* Sb = S[d == 2 ? 1 : 2];
-      const double* Xd = X + dd * NN;
-      double s = 0.0;
-#pragma unroll
-      for (int jb = 0; jb < N; ++jb) s = fma(Sb[jb * N + ab], Xd[jb * N + aa], s);
-      FT[d * NN + rr] = s;
-    }
-    __syncthreads();
-  }
-  // fused core (expand / D^-1 / contract), three passes each reducing along one axis
-  {
-    const double *L1 = vec, *s1 = vec + N, *L2 = vec + 3 * N, *s2 = vec + 4 * N, *L3 = vec + 6 * N, *s3 = vec + 7 * N;
-    const double *T1 = FT, *T2 = FT + NN, *T3 = FT + 2 * NN;
-    for (int i = tid; i < 3 * NN; i += NT) {
-      const int pass = i / NN, rr = i - pass * NN, hi = rr / N, lo = rr - hi * N;
-      double acc = 0.0;
-      if (pass == 0) {          // G1[a3][a2] = sum_a1 s1[a1] E
-        const int a3 = hi, a2 = lo;
-        const double t1 = T1[rr], x2 = s2[a2], x3 = s3[a3], base = lam + L2[a2] + L3[a3];
-#pragma unroll
-        for (int a1 = 0; a1 < N; ++a1) {
-          double E = s1[a1] * t1;
-          E = fma(x2, T2[a3 * N + a1], E);
-          E = fma(x3, T3[a2 * N + a1], E);
-          acc = fma(s1[a1], E * rcp_nr(base + L1[a1]), acc);
-        }
-      } else if (pass == 1) {   // G2[a3][a1] = sum_a2 s2[a2] E
-        const int a3 = hi, a1 = lo;
-        const double t2 = T2[rr], x1 = s1[a1], x3 = s3[a3], base = lam + L1[a1] + L3[a3];
-#pragma unroll
-        for (int a2 = 0; a2 < N; ++a2) {
-          double E = x1 * T1[a3 * N + a2];
-          E = fma(s2[a2], t2, E);
-          E = fma(x3, T3[a2 * N + a1], E);
-          acc = fma(s2[a2], E * rcp_nr(base + L2[a2]), acc);
-        }
-      } else {                  // G3[a2][a1] = sum_a3 s3[a3] E
-        const int a2 = hi, a1 = lo;
-        const double t3 = T3[rr], x1 = s1[a1], x2 = s2[a2], base = lam + L1[a1] + L2[a2];
-#pragma unroll
-        for (int a3 = 0; a3 < N; ++a3) {
-          double E = x1 * T1[a3 * N + a2];
-          E = fma(x2, T2[a3 * N + a1], E);
-          E = fma(s3[a3], t3, E);
-          acc = fma(s3[a3], E * rcp_nr(base + L3[a3]), acc);
-        }
-      }
-      Gs[i] = acc;
-    }
-  }
-  __syncthreads();
-  // back: X_d[ab][ja] = sum_aa G_d[ab][aa] S_a^T[aa][ja]  (X in FT's space);
-  //       U_d[jb][ja] = sum_ab S_b[jb][ab] X_d[ab][ja]      (U in G's space)
-  X = FT;
-  for (int d0 = 0; d0 < 3; d0 += XPL) {
-    for (int i = tid; i < XPL * NN; i += NT) {
-      const int dd = i / NN, rr = i - dd * NN, ab = rr / N, ja = rr - ab * N, d = d0 + dd;
-      const double* Sta = St[d == 0 ? 1 : 0];
-      const double* Gd = Gs + d * NN + ab * N;
-      double s = 0.0;
-#pragma unroll
-      for (int aa = 0; aa < N; ++aa) s = fma(Gd[aa], Sta[aa * N + ja], s);
-      X[i] = s;
-    }
-    __syncthreads();
-    for (int i = tid; i < XPL * NN; i += NT) {
-      const int dd = i / NN, rr = i - dd * NN, jb = rr / N, ja = rr - jb * N, d = d0 + dd;
-      const double* Sb = S[d == 2 ? 1 : 2];
-      const double* Xd = X + dd * NN;
-      double s = 0.0;
-#pragma unroll
-      for (int ab = 0; ab < N; ++ab) s = fma(Sb[jb * N + ab], Xd[ab * N + ja], s);
-      Gs[d * NN + rr] = s;
-    }
-    __syncthreads();
-  }
-  const double *w1 = vec + 2 * N, *w2 = vec + 5 * N, *w3 = vec + 8 * N;
-  for (int i = tid; i < 3 * NN; i += NT) {
-    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
-    int j1, j2, j3;
-    if (d == 0) { j1 = c; j2 = B; j3 = A; }
-    else if (d == 1) { j2 = c; j1 = B; j3 = A; if (j1 == c) continue; }
-    else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
-    const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
-    if (!is_free(g, g1, g2, g3)) continue;
-    const long long idx = skel_index_t<P>(g,g1, g2, g3);
-    u[idx] += w1[j1] * w2[j2] * w3[j3] * Gs[i];
-  }
-}
-
-// ------------------------------------------------------------------------------------------
-// star smoother with a single-pass core (P <= 8): every (a1, a2, a3) triple of the eigenspace is
-// visited once.  Lanes of a GS-lane group own a1, groups own a3 values, a2 runs in registers:
-//   G2[a3][a1] = sum_a2 s2 V   accumulates in a register,
-//   G1[a3][a2] = sum_a1 s1 V   is a shuffle reduction inside the group,
-//   G3[a2][a1] = sum_a3 s3 V   is a per-group register partial, summed over groups in a fixed
-//                              order through shared memory (deterministic).
-// Per triple: 3 FMA for E, 1 add + rcp (MUFU + 4 FMA), 1 mul, 3 accumulations, ~log2(GS)/GS
-// shuffles -- versus three recomputations of E and 1/D in the 3-pass core.
-// ------------------------------------------------------------------------------------------
-template <int P> struct StarSpCfg {
-  static constexpr int N = 2 * P - 1, NN = N * N, C = P - 1;
-  static constexpr int GS = (N <= 4) ? 4 : (N <= 8 ? 8 : (N <= 16 ? 16 : 32));
-  static constexpr int NW = (P <= 4) ? 2 : 4;
-  static constexpr int NT = 32 * NW, GPW = 32 / GS, NG = NW * GPW;
-  static constexpr int A3IT = (N + NG - 1) / NG;      // warp-uniform a3 trip count
-  static constexpr int oFT = 0, oG = 3 * NN, oP3 = 6 * NN, oS = oP3 + NG * NN, oVec = oS + 6 * NN;
-  static constexpr int total = oVec + 9 * N;
-};
-
-template <int P>
-size_t star_sp_smem() { return sizeof(double) * StarSpCfg<P>::total; }
-
-template <int P>
-__global__ void __launch_bounds__(StarSpCfg<P>::NT) k_star_sp(LevelGeom g, int c1, int c2, int c3, int n1c, int n2c,
-                                                             const double* __restrict__ r, double* __restrict__ u,
-                                                             const double* __restrict__ stab,
-                                                             const double* __restrict__ stabT, double lam) {
-  using C = StarSpCfg<P>;
-  constexpr int N = C::N, NN = C::NN, c = C::C, NT = C::NT, GS = C::GS, GPW = C::GPW, NG = C::NG;
-  extern __shared__ double sm[];
-  const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
-  const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
-  if (star_empty(g, v1, v2, v3)) return;
-  if (v3 < g.own_lo) return;   // ghost star below the slab: computed by the lower rank
-  const int tid = threadIdx.x, ST = g.ST;
-  const size_t row[3] = {(size_t)v1, (size_t)(g.V1 + v2), (size_t)(g.V1 + g.V2 + v3)};
-  double* FT = sm + C::oFT;
-  double* Gs = sm + C::oG;
-  double* P3 = sm + C::oP3;
-  double* Ssm = sm + C::oS;
-  double* vec = sm + C::oVec;
-  for (int i = tid; i < 6 * NN; i += NT) {
-    const int k = i / NN, o = i - k * NN;
-    Ssm[i] = (k < 3) ? __ldg(&stab[row[k] * ST + o]) : __ldg(&stabT[row[k - 3] * NN + o]);
-  }
-  for (int i = tid; i < 9 * N; i += NT) { const int d = i / (3 * N); vec[i] = __ldg(&stab[row[d] * ST + NN + i - d * 3 * N]); }
-  const double* S[3] = {Ssm, Ssm + NN, Ssm + 2 * NN};
-  const double* St[3] = {Ssm + 3 * NN, Ssm + 4 * NN, Ssm + 5 * NN};
-  const int o1 = (v1 - 1) * P + 1, o2 = (v2 - 1) * P + 1, o3 = (v3 - 1) * P + 1;
-  for (int i = tid; i < 3 * NN; i += NT) {
-    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
-    int j1, j2, j3;
-    if (d == 0) { j1 = c; j2 = B; j3 = A; } else if (d == 1) { j2 = c; j1 = B; j3 = A; } else { j3 = c; j1 = B; j2 = A; }
-    const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
-    const double val = inside(g, g1, g2, g3) ? __ldg(&r[skel_index_t<P>(g,g1, g2, g3)]) : 0.0;
-    FT[i] = val * (1.0 / (double)(1 + (A == c) + (B == c)));   // inverse multiplicity
-  }
-  __syncthreads();
-  double* X = Gs;
-  for (int i = tid; i < 3 * NN; i += NT) {      // X_d = F_d S_a
-    const int d = i / NN, rr = i - d * NN, jb = rr / N, aa = rr - jb * N;
-    const double* Sa = S[d == 0 ? 1 : 0];
-    const double* F = FT + d * NN + jb * N;
-    double s = 0.0;
-#pragma unroll
-    for (int ja = 0; ja < N; ++ja) s = fma(F[ja], Sa[ja * N + aa], s);
-    X[i] = s;
-  }
-  __syncthreads();
-  for (int i = tid; i < 3 * NN; i += NT) {      // T_d = S_b^T X_d
-    const int d = i / NN, rr = i - d * NN, ab = rr / N, aa = rr - ab * N;
-    const double* Sb = S[d == 2 ? 1 : 2];
-    const double* Xd = X + d * NN;
-    double s = 0.0;
-#pragma unroll
-    for (int jb = 0; jb < N; ++jb) s = fma(Sb[jb * N + ab], Xd[jb * N + aa], s);
-    FT[i] = s;
-  }
-  __syncthreads();
-  {
-    const double *L1 = vec, *s1 = vec + N, *L2 = vec + 3 * N, *s2 = vec + 4 * N, *L3 = vec + 6 * N, *s3 = vec + 7 * N;
-    const double *T1 = FT, *T2 = FT + NN, *T3 = FT + 2 * NN;
-    const int lane = tid & 31, w = tid >> 5, grp = w * GPW + lane / GS, a1 = lane % GS;
-    const bool va = a1 < N;
-    const int a1c = va ? a1 : 0;
-    const double s1a = va ? s1[a1c] : 0.0, L1a = L1[a1c];
-    double g3[N];
-#pragma unroll
-    for (int a2 = 0; a2 < N; ++a2) g3[a2] = 0.0;
-    for (int k = 0; k < C::A3IT; ++k) {
-      const int a3 = grp + k * NG;
-      const bool act = a3 < N;
-      const int a3c = act ? a3 : 0;
-      const double on = (act && va) ? 1.0 : 0.0;
-      const double t2 = on * T2[a3c * N + a1c], s3v = on * s3[a3c], base = lam + L1a + L3[a3c];
-      const double s1v = on * s1a;
-      double g2 = 0.0;
-#pragma unroll
-      for (int a2 = 0; a2 < N; ++a2) {
-        double E = s1v * T1[a3c * N + a2];
-        E = fma(s2[a2], t2, E);
-        E = fma(s3v, T3[a2 * N + a1c], E);
-        const double V = E * rcp_nr(base + L2[a2]);
-        g2 = fma(s2[a2], V, g2);
-        g3[a2] = fma(s3v, V, g3[a2]);
-        double v = s1v * V;
-#pragma unroll
-        for (int o = GS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (act && a1 == 0) Gs[a3 * N + a2] = v;              // G1[a3][a2]
-      }
-      if (act && va) Gs[NN + a3 * N + a1] = g2;               // G2[a3][a1]
-    }
-    if (va) {
-#pragma unroll
-      for (int a2 = 0; a2 < N; ++a2) P3[grp * NN + a2 * N + a1] = g3[a2];
-    }
-    __syncthreads();
-    for (int i = tid; i < NN; i += NT) {                       // G3[a2][a1] = sum over groups
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < NG; ++q) s += P3[q * NN + i];
-      Gs[2 * NN + i] = s;
-    }
-  }
-  __syncthreads();
-  X = FT;
-  for (int i = tid; i < 3 * NN; i += NT) {      // X_d = G_d S_a^T
-    const int d = i / NN, rr = i - d * NN, ab = rr / N, ja = rr - ab * N;
-    const double* Sta = St[d == 0 ? 1 : 0];
-    const double* Gd = Gs + d * NN + ab * N;
-    double s = 0.0;
-#pragma unroll
-    for (int aa = 0; aa < N; ++aa) s = fma(Gd[aa], Sta[aa * N + ja], s);
-    X[i] = s;
-  }
-  __syncthreads();
-  for (int i = tid; i < 3 * NN; i += NT) {      // U_d = S_b X_d
-    const int d = i / NN, rr = i - d * NN, jb = rr / N, ja = rr - jb * N;
-    const double* Sb = S[d == 2 ? 1 : 2];
-    const double* Xd = X + d * NN;
-    double s = 0.0;
-#pragma unroll
-    for (int ab = 0; ab < N; ++ab) s = fma(Sb[jb * N + ab], Xd[ab * N + ja], s);
-    Gs[i] = s;
-  }
-  __syncthreads();
-  const double *w1 = vec + 2 * N, *w2 = vec + 5 * N, *w3 = vec + 8 * N;
-  for (int i = tid; i < 3 * NN; i += NT) {
-    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
-    int j1, j2, j3;
-    if (d == 0) { j1 = c; j2 = B; j3 = A; }
-    else if (d == 1) { j2 = c; j1 = B; j3 = A; if (j1 == c) continue; }
-    else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
-    const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
-    if (!is_free(g, g1, g2, g3)) continue;
-    u[skel_index_t<P>(g,g1, g2, g3)] += w1[j1] * w2[j2] * w3[j3] * Gs[i];
-  }
-}
-
-// ------------------------------------------------------------------------------------------
-// star smoother, P <= 8: the twelve n x n transforms per star (3 planes x 2 forward, 2 back) run
-// on the FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64; tcgen05 has no f64 kind).  n_S is padded to
-// NP = 8 or 16 with zero rows/columns (exact).  One DMMA = 256 FMA per warp from two shared-memory
-// operand loads per lane, instead of 32 FMA per two loads -- the transforms stop competing with the
-// core for load/issue slots.  Leading dimension LD = NP + 4 keeps the fragment loads at the
-// 2-wavefront minimum.  The core is the single-pass DFMA core of k_star_sp.
-// ------------------------------------------------------------------------------------------
-template <int P> struct StarDmCfg {
-  static constexpr int N = 2 * P - 1, NN = N * N, C = P - 1;
-  static constexpr int NP = (N <= 8) ? 8 : 16, LD = NP + 4, MS = NP * LD, TPP = (NP / 8) * (NP / 8);
-  static constexpr int NW = 4, NT = 128;
-  static constexpr int GS = NP, GPW = 32 / GS, NG = NW * GPW, A3IT = (N + NG - 1) / NG;
-  static constexpr int oFT = 0, oX = 3 * MS, oG = 6 * MS, oS = 9 * MS, oSt = 12 * MS, oP3 = 15 * MS,
-                       oVec = oP3 + NG * NN, total = oVec + 9 * N;
-};
-
-template <int P>
-size_t star_dm_smem() { return sizeof(double) * StarDmCfg<P>::total; }
-
-template <int P>
-__global__ void __launch_bounds__(StarDmCfg<P>::NT) k_star_dm(LevelGeom g, int c1, int c2, int c3, int n1c, int n2c,
-                                                             const double* __restrict__ r, double* __restrict__ u,
-                                                             const double* __restrict__ stab,
-                                                             const double* __restrict__ stabT, double lam) {
-  using C = StarDmCfg<P>;
-  constexpr int N = C::N, NN = C::NN, c = C::C, NT = C::NT, NP = C::NP, LD = C::LD, MS = C::MS;
-  constexpr int GS = C::GS, GPW = C::GPW, NG = C::NG;
-  extern __shared__ double sm[];
-  const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
-  const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
-  if (star_empty(g, v1, v2, v3)) return;
-  if (v3 < g.own_lo) return;   // ghost star below the slab: computed by the lower rank
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, ST = g.ST;
-  const size_t row[3] = {(size_t)v1, (size_t)(g.V1 + v2), (size_t)(g.V1 + g.V2 + v3)};
-  double* FT = sm + C::oFT;
-  double* X = sm + C::oX;
-  double* Gs = sm + C::oG;
-  double* Ssm = sm + C::oS;
-  double* Stm = sm + C::oSt;
-  double* P3 = sm + C::oP3;
-  double* vec = sm + C::oVec;
-  const int o1 = (v1 - 1) * P + 1, o2 = (v2 - 1) * P + 1, o3 = (v3 - 1) * P + 1;
-  // padded operands: S, S^T, the three faces (/ multiplicity), zeroed G
-  for (int i = tid; i < 3 * NP * NP; i += NT) {
-    const int d = i / (NP * NP), rr = i - d * NP * NP, A = rr / NP, B = rr - A * NP;
-    const bool in = A < N && B < N;
-    Ssm[d * MS + A * LD + B] = in ? __ldg(&stab[row[d] * ST + A * N + B]) : 0.0;
-    Stm[d * MS + A * LD + B] = in ? __ldg(&stabT[row[d] * NN + A * N + B]) : 0.0;
-    double val = 0.0;
-    if (in) {
-      int j1, j2, j3;
-      if (d == 0) { j1 = c; j2 = B; j3 = A; } else if (d == 1) { j2 = c; j1 = B; j3 = A; } else { j3 = c; j1 = B; j2 = A; }
-      const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
-      val = inside(g, g1, g2, g3) ? __ldg(&r[skel_index_t<P>(g, g1, g2, g3)]) : 0.0;
-      val *= 1.0 / (double)(1 + (A == c) + (B == c));   // inverse multiplicity
-    }
-    FT[d * MS + A * LD + B] = val;
-    Gs[d * MS + A * LD + B] = 0.0;
-  }
-  for (int i = tid; i < 9 * N; i += NT) { const int d = i / (3 * N); vec[i] = __ldg(&stab[row[d] * ST + NN + i - d * 3 * N]); }
-  __syncthreads();
-  // forward: X_d = F_d S_a ; T_d = S_b^T X_d  (tile jobs: 3 planes x TPP tiles over the warps)
-  for (int job = warp; job < 3 * C::TPP; job += C::NW) {
-    const int d = job / C::TPP, t = job - d * C::TPP, mi = t / (NP / 8), ni = t - mi * (NP / 8);
-    dmma_tile<NP, LD>(FT + d * MS, Ssm + (d == 0 ? 1 : 0) * MS, X + d * MS, mi, ni, lane);
-  }
-  __syncthreads();
-  for (int job = warp; job < 3 * C::TPP; job += C::NW) {
-    const int d = job / C::TPP, t = job - d * C::TPP, mi = t / (NP / 8), ni = t - mi * (NP / 8);
-    dmma_tile<NP, LD>(Stm + (d == 2 ? 1 : 2) * MS, X + d * MS, FT + d * MS, mi, ni, lane);
-  }
-  __syncthreads();
-  // single-pass core on T (FT), results G1 -> Gs[0], G2 -> Gs[1], G3 -> Gs[2]
-  {
-    const double *L1 = vec, *s1 = vec + N, *L2 = vec + 3 * N, *s2 = vec + 4 * N, *L3 = vec + 6 * N, *s3 = vec + 7 * N;
-    const double *T1 = FT, *T2 = FT + MS, *T3 = FT + 2 * MS;
-    const int grp = warp * GPW + lane / GS, a1 = lane % GS;
-    const bool va = a1 < N;
-    const int a1c = va ? a1 : 0;
-    const double s1a = va ? s1[a1c] : 0.0, L1a = L1[a1c];
-    double g3[N];
-#pragma unroll
-    for (int a2 = 0; a2 < N; ++a2) g3[a2] = 0.0;
-    for (int k = 0; k < C::A3IT; ++k) {
-      const int a3 = grp + k * NG;
-      const bool act = a3 < N;
-      const int a3c = act ? a3 : 0;
-      const double on = (act && va) ? 1.0 : 0.0;
-      const double t2 = on * T2[a3c * LD + a1c], s3v = on * s3[a3c], base = lam + L1a + L3[a3c];
-      const double s1v = on * s1a;
-      double g2 = 0.0;
-      double v[GS];   // s1 V for every a2 of this (a1, a3); reduced over the group's lanes below
-#pragma unroll
-      for (int a2 = 0; a2 < GS; ++a2) v[a2] = 0.0;
-#pragma unroll
-      for (int a2 = 0; a2 < N; ++a2) {
-        double E = s1v * T1[a3c * LD + a2];
-        E = fma(s2[a2], t2, E);
-        E = fma(s3v, T3[a2 * LD + a1c], E);
-        const double V = E * rcp_nr(base + L2[a2]);
-        g2 = fma(s2[a2], V, g2);
-        g3[a2] = fma(s3v, V, g3[a2]);
-        v[a2] = s1v * V;
-      }
-      // butterfly reduce-scatter over the GS lanes: afterwards lane a1 holds G1[a3][a2 = a1]
-      // (GS - 1 shuffles per lane instead of log2(GS) per a2)
-#pragma unroll
-      for (int off = GS / 2; off >= 1; off >>= 1) {
-        const bool upper = (a1 & off) != 0;
-#pragma unroll
-        for (int j = 0; j < off; ++j) {
-          const double send = upper ? v[j] : v[j + off];
-          const double keep = upper ? v[j + off] : v[j];
-          v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-        }
-      }
-      if (act && va) {
-        Gs[a3 * LD + a1] = v[0];               // G1[a3][a2 = a1]
-        Gs[MS + a3 * LD + a1] = g2;            // G2[a3][a1]
-      }
-    }
-    if (va) {
-#pragma unroll
-      for (int a2 = 0; a2 < N; ++a2) P3[grp * NN + a2 * N + a1] = g3[a2];
-    }
-    __syncthreads();
-    for (int i = tid; i < NN; i += NT) {
-      const int a2 = i / N, a1_ = i - a2 * N;
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < NG; ++q) s += P3[q * NN + i];
-      Gs[2 * MS + a2 * LD + a1_] = s;
-    }
-  }
-  __syncthreads();
-  // back: X_d = G_d S_a^T ; U_d = S_b X_d (into G)
-  for (int job = warp; job < 3 * C::TPP; job += C::NW) {
-    const int d = job / C::TPP, t = job - d * C::TPP, mi = t / (NP / 8), ni = t - mi * (NP / 8);
-    dmma_tile<NP, LD>(Gs + d * MS, Stm + (d == 0 ? 1 : 0) * MS, X + d * MS, mi, ni, lane);
-  }
-  __syncthreads();
-  for (int job = warp; job < 3 * C::TPP; job += C::NW) {
-    const int d = job / C::TPP, t = job - d * C::TPP, mi = t / (NP / 8), ni = t - mi * (NP / 8);
-    dmma_tile<NP, LD>(Ssm + (d == 2 ? 1 : 2) * MS, X + d * MS, Gs + d * MS, mi, ni, lane);
-  }
-  __syncthreads();
-  const double *w1 = vec + 2 * N, *w2 = vec + 5 * N, *w3 = vec + 8 * N;
-  for (int i = tid; i < 3 * NN; i += NT) {
-    const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
-    int j1, j2, j3;
-    if (d == 0) { j1 = c; j2 = B; j3 = A; }
-    else if (d == 1) { j2 = c; j1 = B; j3 = A; if (j1 == c) continue; }
-    else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
-    const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
-    if (!is_free(g, g1, g2, g3)) continue;
-    u[skel_index_t<P>(g, g1, g2, g3)] += w1[j1] * w2[j2] * w3[j3] * Gs[d * MS + A * LD + B];
-  }
-}
-
-// ------------------------------------------------------------------------------------------
-// star smoother, P <= 8, latency-oriented version of k_star_dm (same arithmetic, same citations):
+// star smoother, P <= 8 (Alg. 1 + Alg. 2; the p = 9..16 kernel is star16.cu):
 //   - every global load of the star (S rows, eigen/weight vectors, the three r planes, and the
 //     u values the star will update) is issued up front as cp.async (LDGSTS) into shared memory,
 //     so the whole gather costs one L2 round trip; the u prefetch turns the final read-modify-
@@ -1910,208 +1210,6 @@ __global__ void __launch_bounds__(128) k_star_w(LevelGeom g, int c1, int c2, int
 }
 
 // ------------------------------------------------------------------------------------------
-// element operator for 9 <= P <= 16 (same arithmetic and citations as k_elem_pf / k_elem_dm;
-// P:117-123, reading R1): 8 warps, m = p - 1 padded to 16 for the DMMA face transforms, closed
-// face arrays (the (p+1)^3 cube would not leave room for two CTAs per SM), a shared 1/D table, the
-// forward-transform intermediate aliased with G (G is zeroed after the forward pass).
-// ------------------------------------------------------------------------------------------
-template <int P> struct Elem16Cfg {
-  static constexpr int M = P - 1, Q = P + 1, MM = M * M, QQ = Q * Q, MP = 16, LD = 20, MS = MP * LD;
-  static constexpr int NT = 256, NW = 8;
-  static constexpr int ET = (P - 1) + 2 * (P - 1) * (P - 1) + 2 * (P - 1) + (P + 1) + (P + 1) * (P + 1);
-  static constexpr int YS = 6 * MM + 12 * M + 8;
-  static constexpr int oUc = 0, oTab = 6 * QQ, oPp = oTab + 3 * ET, oA = oPp + 3 * MS, oTG = oA + 6 * MS,
-                       oInv = oTG + 6 * MS, oMap = oInv + MM * M, total = oMap + (6 * QQ + 1) / 2;
-};
-
-template <int P>
-size_t elem16_smem() { return sizeof(double) * Elem16Cfg<P>::total; }
-
-template <int P>
-__global__ void __launch_bounds__(256, 2) k_elem_pf16(LevelGeom g, const double* __restrict__ u,
-                                                    const double* __restrict__ etab, double lam,
-                                                    double* __restrict__ Y, const int* __restrict__ done) {
-  using C = Elem16Cfg<P>;
-  constexpr int M = C::M, Q = C::Q, MM = C::MM, QQ = C::QQ, NT = C::NT, ET = C::ET, LD = C::LD, MS = C::MS,
-                MP = C::MP, YS = C::YS;
-  extern __shared__ double sm[];
-  double* Uc = sm + C::oUc;
-  double* tb = sm + C::oTab;
-  double* Pp = sm + C::oPp;
-  double* Ab = sm + C::oA;
-  double* T = sm + C::oTG;     // forward intermediate, then G
-  double* G = sm + C::oTG;
-  double* invD = sm + C::oInv;
-  const long long e = blockIdx.x;
-  const int e1 = (int)(e % g.k1), e2 = (int)((e / g.k1) % g.k2), e3 = (int)(e / ((long long)g.k1 * g.k2));
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  {
-    const double* src[3] = {etab + (size_t)e1 * ET, etab + (size_t)(g.k1 + e2) * ET, etab + (size_t)(g.k1 + g.k2 + e3) * ET};
-    for (int i = tid; i < 3 * ET; i += NT) {
-      const int d = i / ET;
-      cp_async8(&tb[i], src[d] + (i - d * ET), true);
-    }
-    unsigned* map_s = reinterpret_cast<unsigned*>(sm + C::oMap);   // the face map, before the wait
-    for (int i = tid; i < 6 * QQ; i += NT) map_s[i] = __ldg(&kFaceMap<P>.v[i]);
-    __syncthreads();
-    pdl_wait();
-    pdl_trigger();
-    if (done && *done) return;
-    constexpr int RS = 3 * MM + 3 * M + 1;
-    const long long V12 = (long long)g.V1 * g.V2;
-    const long long rec0 = e1 + g.V1 * (long long)e2 + V12 * e3;
-    for (int i = tid; i < 6 * QQ; i += NT) {
-      const unsigned m_ = map_s[i];
-      cp_async8(&Uc[i], &u[(rec0 + rec_delta(m_, g.V1, V12)) * RS + (m_ & 0xFFFu)], true);
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-  }
-  for (int i = tid; i < 3 * MP * MP; i += NT) {     // padded P_d[b][i]
-    const int d = i / (MP * MP), rr = i - d * MP * MP, A = rr / MP, B = rr - A * MP;
-    Pp[d * MS + A * LD + B] = (A < M && B < M) ? tb[d * ET + et_P(P) + A * M + B] : 0.0;
-  }
-  for (int i = tid; i < 6 * MP * MP; i += NT) {     // padded face interiors
-    const int f = i / (MP * MP), rr = i - f * MP * MP, A = rr / MP, B = rr - A * MP;
-    Ab[f * MS + A * LD + B] = (A < M && B < M) ? Uc[f * QQ + (A + 1) * Q + B + 1] : 0.0;
-  }
-  for (int i = tid; i < MM * M; i += NT) {          // 1/D over the interior eigen-triples
-    const int b3 = i / MM, rr = i - b3 * MM, b2 = rr / M, b1 = rr - b2 * M;
-    invD[i] = rcp_nr(lam + tb[et_lam(P) + b1] + tb[ET + et_lam(P) + b2] + tb[2 * ET + et_lam(P) + b3]);
-  }
-  __syncthreads();
-  constexpr int TPP = (MP / 8) * (MP / 8);
-  for (int job = warp; job < 6 * TPP; job += C::NW) {     // forward A: X_f = U_f P_a^T  (into T)
-    const int f = job / TPP, t = job - f * TPP, mi = t / (MP / 8), ni = t - mi * (MP / 8), d = f >> 1, da = (d == 0) ? 1 : 0;
-    dmma_tile_t<MP, LD, false, true>(Ab + f * MS, Pp + da * MS, T + f * MS, mi, ni, lane);
-  }
-  __syncthreads();
-  for (int job = warp; job < 6 * TPP; job += C::NW) {     // forward B: T_f = P_b X_f  (into Ab)
-    const int f = job / TPP, t = job - f * TPP, mi = t / (MP / 8), ni = t - mi * (MP / 8), d = f >> 1, db = (d == 2) ? 1 : 2;
-    dmma_tile_t<MP, LD, false, false>(Pp + db * MS, T + f * MS, Ab + f * MS, mi, ni, lane);
-  }
-  __syncthreads();
-  for (int i = tid; i < 6 * MS; i += NT) G[i] = 0.0;     // T is dead: G takes its place
-  __syncthreads();
-  {
-    const double *a10 = tb + et_a0(P), *a11 = tb + et_a1(P);
-    const double *a20 = tb + ET + et_a0(P), *a21 = tb + ET + et_a1(P);
-    const double *a30 = tb + 2 * ET + et_a0(P), *a31 = tb + 2 * ET + et_a1(P);
-    const double *T0 = Ab, *T1 = Ab + MS, *T2 = Ab + 2 * MS, *T3 = Ab + 3 * MS, *T4 = Ab + 4 * MS, *T5 = Ab + 5 * MS;
-    for (int i = tid; i < 3 * MM; i += NT) {
-      const int pass = i / MM, r = i - pass * MM, hi = r / M, lo = r - hi * M;
-      double g0 = 0.0, g1 = 0.0;
-      if (pass == 0) {
-        const int b3 = hi, b2 = lo;
-        const double tA = T0[b3 * LD + b2], tB = T1[b3 * LD + b2], c2 = a20[b2], c2b = a21[b2], c3 = a30[b3], c3b = a31[b3];
-#pragma unroll 5
-        for (int b1 = 0; b1 < M; ++b1) {
-          double Ev = a10[b1] * tA;
-          Ev = fma(a11[b1], tB, Ev);
-          Ev = fma(c2, T2[b3 * LD + b1], Ev);
-          Ev = fma(c2b, T3[b3 * LD + b1], Ev);
-          Ev = fma(c3, T4[b2 * LD + b1], Ev);
-          Ev = fma(c3b, T5[b2 * LD + b1], Ev);
-          const double V = Ev * invD[(b3 * M + b2) * M + b1];
-          g0 = fma(a10[b1], V, g0);
-          g1 = fma(a11[b1], V, g1);
-        }
-        G[0 * MS + b3 * LD + b2] = g0;
-        G[1 * MS + b3 * LD + b2] = g1;
-      } else if (pass == 1) {
-        const int b3 = hi, b1 = lo;
-        const double tA = T2[b3 * LD + b1], tB = T3[b3 * LD + b1], c1 = a10[b1], c1b = a11[b1], c3 = a30[b3], c3b = a31[b3];
-#pragma unroll 5
-        for (int b2 = 0; b2 < M; ++b2) {
-          double Ev = c1 * T0[b3 * LD + b2];
-          Ev = fma(c1b, T1[b3 * LD + b2], Ev);
-          Ev = fma(a20[b2], tA, Ev);
-          Ev = fma(a21[b2], tB, Ev);
-          Ev = fma(c3, T4[b2 * LD + b1], Ev);
-          Ev = fma(c3b, T5[b2 * LD + b1], Ev);
-          const double V = Ev * invD[(b3 * M + b2) * M + b1];
-          g0 = fma(a20[b2], V, g0);
-          g1 = fma(a21[b2], V, g1);
-        }
-        G[2 * MS + b3 * LD + b1] = g0;
-        G[3 * MS + b3 * LD + b1] = g1;
-      } else {
-        const int b2 = hi, b1 = lo;
-        const double tA = T4[b2 * LD + b1], tB = T5[b2 * LD + b1], c1 = a10[b1], c1b = a11[b1], c2 = a20[b2], c2b = a21[b2];
-#pragma unroll 5
-        for (int b3 = 0; b3 < M; ++b3) {
-          double Ev = c1 * T0[b3 * LD + b2];
-          Ev = fma(c1b, T1[b3 * LD + b2], Ev);
-          Ev = fma(c2, T2[b3 * LD + b1], Ev);
-          Ev = fma(c2b, T3[b3 * LD + b1], Ev);
-          Ev = fma(a30[b3], tA, Ev);
-          Ev = fma(a31[b3], tB, Ev);
-          const double V = Ev * invD[(b3 * M + b2) * M + b1];
-          g0 = fma(a30[b3], V, g0);
-          g1 = fma(a31[b3], V, g1);
-        }
-        G[4 * MS + b2 * LD + b1] = g0;
-        G[5 * MS + b2 * LD + b1] = g1;
-      }
-    }
-  }
-  __syncthreads();
-  for (int job = warp; job < 6 * TPP; job += C::NW) {     // back A: X_f = G_f P_a   (into Ab)
-    const int f = job / TPP, t = job - f * TPP, mi = t / (MP / 8), ni = t - mi * (MP / 8), d = f >> 1, da = (d == 0) ? 1 : 0;
-    dmma_tile_t<MP, LD, false, false>(G + f * MS, Pp + da * MS, Ab + f * MS, mi, ni, lane);
-  }
-  __syncthreads();
-  for (int job = warp; job < 6 * TPP; job += C::NW) {     // back B: C_f = P_b^T X_f  (into G)
-    const int f = job / TPP, t = job - f * TPP, mi = t / (MP / 8), ni = t - mi * (MP / 8), d = f >> 1, db = (d == 2) ? 1 : 2;
-    dmma_tile_t<MP, LD, true, false>(Pp + db * MS, Ab + f * MS, G + f * MS, mi, ni, lane);
-  }
-  __syncthreads();
-  const double* Mv[3] = {tb + et_M(P), tb + ET + et_M(P), tb + 2 * ET + et_M(P)};
-  const double* Kv[3] = {tb + et_K(P), tb + ET + et_K(P), tb + 2 * ET + et_K(P)};
-  double* Ye = Y + (size_t)e * g.YS;
-  for (int o = tid; o < YS; o += NT) {
-    double y;
-    if (o < 6 * MM) {      // face interior: closed-face row / column sums and the opposite face
-      const int f = o / MM, r = o - f * MM, A = r / M, B = r - A * M, d = f >> 1, s_ = f & 1;
-      const int da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2;
-      const int td = s_ * P, ta = B + 1, tb_ = A + 1;
-      const double* Uf = Uc + f * QQ;
-      const double *Kd = Kv[d], *Ka = Kv[da], *Kb = Kv[db];
-      const double Md = Mv[d][td], Ma = Mv[da][ta], Mb = Mv[db][tb_];
-      double sa = 0.0, sb = 0.0;
-#pragma unroll
-      for (int t = 0; t <= P; ++t) {
-        sa = fma(Ka[ta * Q + t], Uf[tb_ * Q + t], sa);
-        sb = fma(Kb[tb_ * Q + t], Uf[t * Q + ta], sb);
-      }
-      const double sd = Kd[td * Q] * Uc[(2 * d) * QQ + tb_ * Q + ta] + Kd[td * Q + P] * Uc[(2 * d + 1) * QQ + tb_ * Q + ta];
-      y = lam * Md * Ma * Mb * Uf[tb_ * Q + ta];
-      y = fma(Ma * Mb, sd, y);
-      y = fma(Md * Mb, sa, y);
-      y = fma(Md * Ma, sb, y);
-      y -= G[f * MS + A * LD + B];
-    } else {               // edges and vertices: all three lines lie on the element boundary
-      int t1, t2, t3;
-      ys_point<P>(o, t1, t2, t3);
-      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-      for (int t = 0; t <= P; ++t) {
-        s1 = fma(Kv[0][t1 * Q + t], getUc<P>(Uc, t, t2, t3), s1);
-        s2 = fma(Kv[1][t2 * Q + t], getUc<P>(Uc, t1, t, t3), s2);
-        s3 = fma(Kv[2][t3 * Q + t], getUc<P>(Uc, t1, t2, t), s3);
-      }
-      const double m1 = Mv[0][t1], m2 = Mv[1][t2], m3 = Mv[2][t3];
-      y = lam * m1 * m2 * m3 * getUc<P>(Uc, t1, t2, t3);
-      y = fma(m2 * m3, s1, y);
-      y = fma(m1 * m3, s2, y);
-      y = fma(m1 * m2, s3, y);
-    }
-    Ye[o] = y;
-  }
-}
-
-// ------------------------------------------------------------------------------------------
 // residual gather, degree-templated: one block per vertex record (3-D grid, no index division),
 // one thread per record slot.  Same sums in the same order as k_gather_resid (kernels.cu):
 // r = F - sum over the elements sharing the point of their outputs Y.
@@ -2182,19 +1280,11 @@ __global__ void __launch_bounds__(256) k_gather_resid_t(LevelGeom g, const doubl
 }
 
 // ------------------------------------------------------------------------------------------
-// dispatch
+// dispatch: one production kernel per degree range
+//   element operator: k_elem_pf (p <= 8), k_elem16 (9..16, elem16.cu), k_elem_apply_t (17..32)
+//   star smoother:    k_star_w (p <= 4 and >= star_w_min stars per colour), k_star_pf (p <= 8),
+//                     k_star16 (9..16, star16.cu), k_star_tm (17..32)
 // ------------------------------------------------------------------------------------------
-constexpr bool kStarSinglePass(int p) { return p <= 8; }   // k_star_sp / k_star_dm variants
-constexpr bool kStarPf(int p) { return p <= 16; }          // k_star_pf (default for 5 <= p <= 16)
-
-// star kernel variant for p <= 8 (A/B experiments): 0 default (k_star_w for p <= 4, k_star_pf
-// above), 1 DFMA transforms (k_star_sp), 2 DMMA transforms without prefetch (k_star_dm),
-// 3 k_star_pf at every p <= 8
-static int star_variant() {   // read at every launch (launches are captured into graphs once)
-  const char* e = std::getenv("PMG_STAR_VARIANT");
-  return (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
-}
-
 // stars per colour from which k_star_w (warp per star, p <= 4) replaces k_star_pf; PMG_STAR_W_MIN
 // overrides the default (tests force the kernel onto small parity meshes with 0)
 static long long star_w_min(long long dflt) {
@@ -2202,82 +1292,52 @@ static long long star_w_min(long long dflt) {
   return (e && e[0]) ? std::atoll(e) : dflt;
 }
 
-// element kernel variant for p <= 8: 0 k_elem_pf (default), 1 DFMA (k_elem_apply_t), 2 k_elem_dm
-static int elem_variant() {
-  const char* e = std::getenv("PMG_ELEM_VARIANT");
-  return (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 0;
+template <int P>
+cudaError_t launch_elem_p(const LevelGeom& g, const double* u, const double* etab, const double* etabP, double lam,
+                          double* Y, const int* done, cudaStream_t st) {
+  if constexpr (P <= 8)
+    return launch_pdl(k_elem_pf<P>, dim3((unsigned)g.nelem), dim3(ElemPfCfg<P>::NT), elem_pf_smem<P>(), st, g, u, etab, lam,
+                      Y, done);
+  else if constexpr (P <= 16)
+    return launch_elem16(g, u, etabP, lam, Y, done, st);
+  else
+    return launch_pdl(k_elem_apply_t<P>, dim3((unsigned)g.nelem), dim3(ElemCfg<P>::NT), elem_t_smem<P>(), st, g, u, etab,
+                      lam, Y, done);
 }
 
 template <int P>
-void launch_elem_p(const LevelGeom& g, const double* u, const double* etab, double lam, double* Y, const int* done,
-                   cudaStream_t st) {
+cudaError_t launch_star_p(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c, long long nb, const double* r,
+                          double* u, const double* stab, const double* stabP, double lam, cudaStream_t st) {
   if constexpr (P <= 8) {
-    const int v = elem_variant();
-    if (v == 0) {
-      launch_pdl(k_elem_pf<P>, dim3((unsigned)g.nelem), dim3(ElemPfCfg<P>::NT), elem_pf_smem<P>(), st, g, u, etab, lam, Y, done);
-      return;
-    }
-    if (v == 2) {
-      k_elem_dm<P><<<(unsigned)g.nelem, ElemDmCfg<P>::NT, elem_dm_smem<P>(), st>>>(g, u, etab, lam, Y, done);
-      return;
-    }
-  }
-  if constexpr (P > 8 && P <= 16) {
-    if (elem_variant() == 0) {
-      launch_pdl(k_elem_pf16<P>, dim3((unsigned)g.nelem), dim3(Elem16Cfg<P>::NT), elem16_smem<P>(), st, g, u, etab, lam, Y, done);
-      return;
-    }
-  }
-  launch_pdl(k_elem_apply_t<P>, dim3((unsigned)g.nelem), dim3(ElemCfg<P>::NT), elem_t_smem<P>(), st, g, u, etab, lam, Y, done);
-}
-
-template <int P>
-void launch_star_p(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c, long long nb, const double* r,
-                   double* u, const double* stab, const double* stabT, double lam, cudaStream_t st) {
-  if constexpr (kStarPf(P) && !kStarSinglePass(P)) {
-    launch_pdl(k_star_pf<P>, dim3((unsigned)nb), dim3(StarPfCfg<P>::NT), star_pf_smem<P>(), st, g, c1, c2, c3, n1c, n2c, r, u, stab, lam);
-  } else if constexpr (kStarSinglePass(P)) {
-    const int v = star_variant();
     if constexpr (P <= 4) {
       // warp per star pays off once a colour has many waves of 128-thread stars (large meshes);
       // for a few hundred stars the shorter per-star chain of k_star_pf wins (measured, config 2)
-      if (v == 0 && nb >= star_w_min(4LL * 148 * StarPfCfg<P>::MINB)) {
-        launch_pdl(k_star_w<P>, dim3((unsigned)((nb + StarWCfg<P>::SPB - 1) / StarWCfg<P>::SPB)), dim3(StarWCfg<P>::NT),
-                   star_w_smem<P>(), st, g, c1, c2, c3, n1c, n2c, nb, r, u, stab, lam);
-        return;
-      }
+      if (nb >= star_w_min(4LL * 148 * StarPfCfg<P>::MINB))
+        return launch_pdl(k_star_w<P>, dim3((unsigned)((nb + StarWCfg<P>::SPB - 1) / StarWCfg<P>::SPB)),
+                          dim3(StarWCfg<P>::NT), star_w_smem<P>(), st, g, c1, c2, c3, n1c, n2c, nb, r, u, stab, lam);
     }
-    if (v == 0 || v == 3)
-      launch_pdl(k_star_pf<P>, dim3((unsigned)nb), dim3(StarPfCfg<P>::NT), star_pf_smem<P>(), st, g, c1, c2, c3, n1c, n2c, r, u, stab, lam);
-    else if (v == 2)
-      k_star_dm<P><<<(unsigned)nb, StarDmCfg<P>::NT, star_dm_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
-    else
-      k_star_sp<P><<<(unsigned)nb, StarSpCfg<P>::NT, star_sp_smem<P>(), st>>>(g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
+    return launch_pdl(k_star_pf<P>, dim3((unsigned)nb), dim3(StarPfCfg<P>::NT), star_pf_smem<P>(), st, g, c1, c2, c3, n1c,
+                      n2c, r, u, stab, lam);
+  } else if constexpr (P <= 16) {
+    return launch_star16(g, c1, c2, c3, n1c, n2c, nb, r, u, stabP, lam, st);
   } else {
-    if constexpr (P > 16) {
-      if (star_variant() != 1) {   // 1: the DFMA-transform kernel (A/B)
-        launch_pdl(k_star_tm<P>, dim3((unsigned)nb), dim3(StarTmCfg<P>::NT), star_tm_smem<P>(), st, g, c1, c2, c3, n1c, n2c, r, u, stab, lam);
-        return;
-      }
-    }
-    launch_pdl(k_star_t<P>, dim3((unsigned)nb), dim3(StarCfg<P>::NT), star_t_smem<P>(), st, g, c1, c2, c3, n1c, n2c, r, u, stab, stabT, lam);
+    return launch_pdl(k_star_tm<P>, dim3((unsigned)nb), dim3(StarTmCfg<P>::NT), star_tm_smem<P>(), st, g, c1, c2, c3, n1c,
+                      n2c, r, u, stab, lam);
   }
 }
+
 #define PMG_DEGREES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) \
   X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32)
 
-cudaError_t launch_elem_apply(const LevelGeom& g, const double* u, const double* etab, double lam, double* Y,
-                              const int* done, cudaStream_t st) {
+cudaError_t launch_elem_apply(const LevelGeom& g, const double* u, const double* etab, const double* etabP, double lam,
+                              double* Y, const int* done, cudaStream_t st) {
   switch (g.p) {
-#define CASE(P)                                                                                     \
-  case P:                                                                                           \
-    launch_elem_p<P>(g, u, etab, lam, Y, done, st);                                                \
-    break;
+#define CASE(P) \
+  case P: return launch_elem_p<P>(g, u, etab, etabP, lam, Y, done, st);
     PMG_DEGREES(CASE)
 #undef CASE
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_gather_resid(const LevelGeom& g, const double* Y, const double* F, double* out, const int* done,
@@ -2288,34 +1348,34 @@ cudaError_t launch_gather_resid(const LevelGeom& g, const double* Y, const doubl
   case P: {                                                                                         \
     constexpr int RS = 3 * (P - 1) * (P - 1) + 3 * (P - 1) + 1;                                     \
     const int nt = RS < 64 ? 64 : (RS < 128 ? 128 : 256);                                           \
-    launch_pdl(k_gather_resid_t<P>, grid, dim3(nt), 0, st, g, Y, F, out, done);                     \
-    break;                                                                                          \
+    return launch_pdl(k_gather_resid_t<P>, grid, dim3(nt), 0, st, g, Y, F, out, done);              \
   }
     PMG_DEGREES(CASE)
 #undef CASE
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_star(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c, long long nb, const double* r,
-                        double* u, const double* stab, const double* stabT, double lam, cudaStream_t st) {
+                        double* u, const double* stab, const double* stabP, double lam, cudaStream_t st) {
   switch (g.p) {
-#define CASE(P)                                                                                     \
-  case P:                                                                                           \
-    launch_star_p<P>(g, c1, c2, c3, n1c, n2c, nb, r, u, stab, stabT, lam, st);                    \
-    break;
+#define CASE(P) \
+  case P: return launch_star_p<P>(g, c1, c2, c3, n1c, n2c, nb, r, u, stab, stabP, lam, st);
     PMG_DEGREES(CASE)
 #undef CASE
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
+// dynamic shared memory of the production kernels (which 0: element operator, 1: star smoother;
+// the p = 9..16 kernels have fixed footprints set in star16.cu / elem16.cu)
 size_t hot_smem(int p, int which) {
   switch (p) {
-#define CASE(P) \
-  case P: return which == 0 ? std::max(std::max(elem_t_smem<P>(), elem16_smem<(P > 8 && P <= 16 ? P : 9)>()), std::max(elem_dm_smem<(P <= 8 ? P : 2)>(), elem_pf_smem<(P <= 8 ? P : 2)>())) : (kStarSinglePass(P) ? std::max(std::max(std::max(star_sp_smem<(P <= 8 ? P : 2)>(), star_dm_smem<(P <= 8 ? P : 2)>()), star_pf_smem<(P <= 8 ? P : 2)>()), star_w_smem<(P <= 4 ? P : 2)>()) : (kStarPf(P) ? star_pf_smem<(P <= 16 ? P : 2)>() : std::max(star_t_smem<P>(), star_tm_smem<(P > 16 ? P : 17)>())));
+#define CASE(P)                                                                                              \
+  case P:                                                                                                    \
+    if (which == 0) return P <= 8 ? elem_pf_smem<(P <= 8 ? P : 2)>() : (P > 16 ? elem_t_smem<P>() : 0);      \
+    return P <= 4 ? std::max(star_pf_smem<(P <= 4 ? P : 2)>(), star_w_smem<(P <= 4 ? P : 2)>())            \
+                  : (P <= 8 ? star_pf_smem<(P <= 8 ? P : 2)>() : (P > 16 ? star_tm_smem<(P > 16 ? P : 17)>() : 0));
     PMG_DEGREES(CASE)
 #undef CASE
     default: return 0;
@@ -2324,31 +1384,22 @@ size_t hot_smem(int p, int which) {
 
 cudaError_t hot_set_smem_attr(int bytes) {
   cudaError_t e = cudaSuccess;
-#define CASE(P)                                                                                        \
-  {                                                                                                    \
-    cudaError_t a = cudaFuncSetAttribute(k_elem_apply_t<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
-    if (a == cudaSuccess && P <= 8)                                                                    \
-      a = cudaFuncSetAttribute(k_elem_dm<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
-    if (a == cudaSuccess && P <= 8)                                                                    \
-      a = cudaFuncSetAttribute(k_elem_pf<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
-    if (a == cudaSuccess && P > 8 && P <= 16)                                                          \
-      a = cudaFuncSetAttribute(k_elem_pf16<(P > 8 && P <= 16 ? P : 9)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
-    cudaError_t b = cudaFuncSetAttribute(k_star_t<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);       \
-    if (b == cudaSuccess && kStarSinglePass(P))                                                        \
-      b = cudaFuncSetAttribute(k_star_sp<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
-    if (b == cudaSuccess && kStarSinglePass(P))                                                        \
-      b = cudaFuncSetAttribute(k_star_dm<(P <= 8 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
-    if (b == cudaSuccess && P > 16)                                                                    \
-      b = cudaFuncSetAttribute(k_star_tm<(P > 16 ? P : 17)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
-    if (b == cudaSuccess && P <= 4)                                                                    \
-      b = cudaFuncSetAttribute(k_star_w<(P <= 4 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
-    if (b == cudaSuccess && kStarPf(P))                                                                \
-      b = cudaFuncSetAttribute(k_star_pf<(P <= 16 ? P : 2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
-    if (a != cudaSuccess) e = a;                                                                       \
-    if (b != cudaSuccess) e = b;                                                                       \
+#define SET(K)                                                                        \
+  {                                                                                   \
+    cudaError_t a = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+    if (a != cudaSuccess) e = a;                                                      \
   }
-  PMG_DEGREES(CASE)
-#undef CASE
+#define CASE8(P) SET(k_elem_pf<P>) SET(k_star_pf<P>)
+#define CASE4(P) SET(k_star_w<P>)
+#define CASE32(P) SET(k_elem_apply_t<P>) SET(k_star_tm<P>)
+  CASE8(2) CASE8(3) CASE8(4) CASE8(5) CASE8(6) CASE8(7) CASE8(8)
+  CASE4(2) CASE4(3) CASE4(4)
+  CASE32(17) CASE32(18) CASE32(19) CASE32(20) CASE32(21) CASE32(22) CASE32(23) CASE32(24) CASE32(25) CASE32(26)
+  CASE32(27) CASE32(28) CASE32(29) CASE32(30) CASE32(31) CASE32(32)
+#undef CASE8
+#undef CASE4
+#undef CASE32
+#undef SET
   return e;
 }
 

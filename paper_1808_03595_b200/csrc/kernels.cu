@@ -1,9 +1,7 @@
-// FP64 CUDA kernels of the p-multigrid hot path for sm_100a (B200).
-// Runtime degree p (2 <= p <= 32).  Citations: P:n = PAPER.md line n.
+// FP64 CUDA kernels of the p-multigrid path for sm_100a (B200) besides the degree-specialised
+// element operator and star smoother (hot_kernels.cu, star16.cu, elem16.cu).  Citations: P:n =
+// PAPER.md line n.
 //
-//   k_elem_apply      condensed element operator  y_e = H_hat_e u_B  in O(p^3)   (R1)
-//   k_gather_resid    r = F - sum_e Q_e y_e  (or  q = sum_e Q_e y_e)
-//   k_star            vertex-star smoother, one colour of Alg. 2 with Alg. 1
 //   k_restrict_local  per fine record: J^T of its faces/edges (closed, coarse)
 //   k_restrict_gather coarse record entries gather the closed contributions
 //   k_prolong         u_f += J_hat u_c per fine record
@@ -68,363 +66,6 @@ __global__ void k_weak_rhs(LevelGeom g, const double* __restrict__ b1, const dou
     long long r = idx / N1;
     int i2 = (int)(r % N2), i3 = (int)(r / N2);
     F[idx] = is_free(g, i1, i2, i3) ? b3[i3 + g.zoff * g.p] * b2[i2] * b1[i1] * f[idx] : 0.0;   // b3: global line
-  }
-}
-
-// ------------------------------------------------------------------------------------------
-// element operator H_hat_e u_B
-// H_hat_e u = H_BB u - C u,  C u = H_BI H_II^-1 H_IB u touches face interiors only:
-//   T_f = (P_b (x) P_a) U_f,  P = S^T M_II;  E = sum_f a_f (x)_d T_f;  V = E / (lam + L1+L2+L3);
-//   C_f = (P_b^T (x) P_a^T) [sum_{beta_d} a_f V]
-// ------------------------------------------------------------------------------------------
-__device__ __forceinline__ double getU(const double* Uc, int q, int p, int t1, int t2, int t3) {
-  const int qq = q * q;
-  if (t1 == 0 || t1 == p) return Uc[((t1 == p) ? 1 : 0) * qq + t3 * q + t2];
-  if (t2 == 0 || t2 == p) return Uc[(2 + ((t2 == p) ? 1 : 0)) * qq + t3 * q + t1];
-  return Uc[(4 + ((t3 == p) ? 1 : 0)) * qq + t2 * q + t1];
-}
-
-size_t elem_apply_smem(int p, int ET) {
-  int m = p - 1, q = p + 1;
-  return sizeof(double) * (size_t)(6 * q * q + 13 * m * m + 3 * ET);
-}
-
-__global__ void __launch_bounds__(256) k_elem_apply(LevelGeom g, const double* __restrict__ u,
-                                                    const double* __restrict__ etab, double lam,
-                                                    double* __restrict__ Y, const int* __restrict__ done) {
-  if (done && *done) return;
-  extern __shared__ double sm[];
-  const int p = g.p, m = g.m, q = p + 1, qq = q * q, mm = m * m, ET = g.ET;
-  double* Uc = sm;
-  double* T = Uc + 6 * qq;
-  double* G = T + 6 * mm;
-  double* X = G + 6 * mm;
-  double* tb = X + mm;
-  const long long e = blockIdx.x;
-  const int e1 = (int)(e % g.k1), e2 = (int)((e / g.k1) % g.k2), e3 = (int)(e / ((long long)g.k1 * g.k2));
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const double* src0 = etab + (size_t)e1 * ET;
-  const double* src1 = etab + (size_t)(g.k1 + e2) * ET;
-  const double* src2 = etab + (size_t)(g.k1 + g.k2 + e3) * ET;
-  for (int i = tid; i < ET; i += nt) { tb[i] = src0[i]; tb[ET + i] = src1[i]; tb[2 * ET + i] = src2[i]; }
-  for (int i = tid; i < 6 * qq; i += nt) {
-    int f = i / qq, r = i - f * qq, A = r / q, B = r - A * q, d = f >> 1, s = f & 1;
-    int t1, t2, t3;
-    if (d == 0) { t1 = s * p; t3 = A; t2 = B; }
-    else if (d == 1) { t2 = s * p; t3 = A; t1 = B; }
-    else { t3 = s * p; t2 = A; t1 = B; }
-    Uc[i] = u[skel_index(g, e1 * p + t1, e2 * p + t2, e3 * p + t3)];
-  }
-  __syncthreads();
-  // forward face transforms T_f[bb][ba] = sum P_b[bb][ib] P_a[ba][ia] U_f[ib][ia]
-  for (int f = 0; f < 6; ++f) {
-    const int d = f >> 1, da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2;
-    const double* Pa = tb + da * ET + et_P(p);
-    const double* Pb = tb + db * ET + et_P(p);
-    const double* U = Uc + f * qq;
-    for (int i = tid; i < mm; i += nt) {
-      int ib = i / m, ba = i - ib * m;
-      double s = 0.0;
-      for (int ia = 0; ia < m; ++ia) s += U[(ib + 1) * q + ia + 1] * Pa[ba * m + ia];
-      X[i] = s;
-    }
-    __syncthreads();
-    double* Tf = T + f * mm;
-    for (int i = tid; i < mm; i += nt) {
-      int bb = i / m, ba = i - bb * m;
-      double s = 0.0;
-      for (int ib = 0; ib < m; ++ib) s += Pb[bb * m + ib] * X[ib * m + ba];
-      Tf[i] = s;
-    }
-    __syncthreads();
-  }
-  const double *L1 = tb + et_lam(p), *L2 = tb + ET + et_lam(p), *L3 = tb + 2 * ET + et_lam(p);
-  const double *a10 = tb + et_a0(p), *a11 = tb + et_a1(p);
-  const double *a20 = tb + ET + et_a0(p), *a21 = tb + ET + et_a1(p);
-  const double *a30 = tb + 2 * ET + et_a0(p), *a31 = tb + 2 * ET + et_a1(p);
-  const double *T0 = T, *T1 = T + mm, *T2 = T + 2 * mm, *T3 = T + 3 * mm, *T4 = T + 4 * mm, *T5 = T + 5 * mm;
-  // faces 0,1 (normal x1): G[b3][b2] = sum_b1 a1s[b1] V
-  for (int i = tid; i < mm; i += nt) {
-    int b3 = i / m, b2 = i - b3 * m;
-    double tA = T0[i], tB = T1[i], c2 = a20[b2], c2b = a21[b2], c3 = a30[b3], c3b = a31[b3];
-    double base = lam + L2[b2] + L3[b3], g0 = 0.0, g1 = 0.0;
-    for (int b1 = 0; b1 < m; ++b1) {
-      double E = a10[b1] * tA + a11[b1] * tB + c2 * T2[b3 * m + b1] + c2b * T3[b3 * m + b1] +
-                 c3 * T4[b2 * m + b1] + c3b * T5[b2 * m + b1];
-      double V = E / (base + L1[b1]);
-      g0 += a10[b1] * V;
-      g1 += a11[b1] * V;
-    }
-    G[i] = g0;
-    G[mm + i] = g1;
-  }
-  // faces 2,3 (normal x2): G[b3][b1] = sum_b2 a2s[b2] V
-  for (int i = tid; i < mm; i += nt) {
-    int b3 = i / m, b1 = i - b3 * m;
-    double tA = T2[i], tB = T3[i], c1 = a10[b1], c1b = a11[b1], c3 = a30[b3], c3b = a31[b3];
-    double base = lam + L1[b1] + L3[b3], g0 = 0.0, g1 = 0.0;
-    for (int b2 = 0; b2 < m; ++b2) {
-      double E = c1 * T0[b3 * m + b2] + c1b * T1[b3 * m + b2] + a20[b2] * tA + a21[b2] * tB +
-                 c3 * T4[b2 * m + b1] + c3b * T5[b2 * m + b1];
-      double V = E / (base + L2[b2]);
-      g0 += a20[b2] * V;
-      g1 += a21[b2] * V;
-    }
-    G[2 * mm + i] = g0;
-    G[3 * mm + i] = g1;
-  }
-  // faces 4,5 (normal x3): G[b2][b1] = sum_b3 a3s[b3] V
-  for (int i = tid; i < mm; i += nt) {
-    int b2 = i / m, b1 = i - b2 * m;
-    double tA = T4[i], tB = T5[i], c1 = a10[b1], c1b = a11[b1], c2 = a20[b2], c2b = a21[b2];
-    double base = lam + L1[b1] + L2[b2], g0 = 0.0, g1 = 0.0;
-    for (int b3 = 0; b3 < m; ++b3) {
-      double E = c1 * T0[b3 * m + b2] + c1b * T1[b3 * m + b2] + c2 * T2[b3 * m + b1] + c2b * T3[b3 * m + b1] +
-                 a30[b3] * tA + a31[b3] * tB;
-      double V = E / (base + L3[b3]);
-      g0 += a30[b3] * V;
-      g1 += a31[b3] * V;
-    }
-    G[4 * mm + i] = g0;
-    G[5 * mm + i] = g1;
-  }
-  __syncthreads();
-  // back transforms C_f[ib][ia] = sum P_b[bb][ib] P_a[ba][ia] G_f[bb][ba]  -> stored in T_f
-  for (int f = 0; f < 6; ++f) {
-    const int d = f >> 1, da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2;
-    const double* Pa = tb + da * ET + et_P(p);
-    const double* Pb = tb + db * ET + et_P(p);
-    const double* Gf = G + f * mm;
-    for (int i = tid; i < mm; i += nt) {
-      int bb = i / m, ia = i - bb * m;
-      double s = 0.0;
-      for (int ba = 0; ba < m; ++ba) s += Gf[bb * m + ba] * Pa[ba * m + ia];
-      X[i] = s;
-    }
-    __syncthreads();
-    double* Cf = T + f * mm;
-    for (int i = tid; i < mm; i += nt) {
-      int ib = i / m, ia = i - ib * m;
-      double s = 0.0;
-      for (int bb = 0; bb < m; ++bb) s += Pb[bb * m + ib] * X[bb * m + ia];
-      Cf[i] = s;
-    }
-    __syncthreads();
-  }
-  // H_BB u on every boundary point, minus C on face interiors
-  const double *M1 = tb + et_M(p), *M2 = tb + ET + et_M(p), *M3 = tb + 2 * ET + et_M(p);
-  const double *K1 = tb + et_K(p), *K2 = tb + ET + et_K(p), *K3 = tb + 2 * ET + et_K(p);
-  double* Ye = Y + (size_t)e * g.YS;
-  for (int o = tid; o < g.YS; o += nt) {
-    int t1, t2, t3;
-    double corr = 0.0;
-    if (o < 6 * mm) {
-      int f = o / mm, r = o - f * mm, A = r / m, B = r - A * m, d = f >> 1, s = f & 1;
-      if (d == 0) { t1 = s * p; t3 = A + 1; t2 = B + 1; }
-      else if (d == 1) { t2 = s * p; t3 = A + 1; t1 = B + 1; }
-      else { t3 = s * p; t2 = A + 1; t1 = B + 1; }
-      corr = T[o];
-    } else if (o < 6 * mm + 12 * m) {
-      int r = o - 6 * mm, qe = r / m, i = r - qe * m, d = qe >> 2, sA = qe & 1, sB = (qe >> 1) & 1;
-      if (d == 0) { t1 = i + 1; t2 = sA * p; t3 = sB * p; }
-      else if (d == 1) { t2 = i + 1; t1 = sA * p; t3 = sB * p; }
-      else { t3 = i + 1; t1 = sA * p; t2 = sB * p; }
-    } else {
-      int qv = o - 6 * mm - 12 * m;
-      t1 = (qv & 1) * p; t2 = ((qv >> 1) & 1) * p; t3 = ((qv >> 2) & 1) * p;
-    }
-    const bool bd1 = (t1 == 0 || t1 == p), bd2 = (t2 == 0 || t2 == p), bd3 = (t3 == 0 || t3 == p);
-    double y = lam * M1[t1] * M2[t2] * M3[t3] * getU(Uc, q, p, t1, t2, t3);
-    double s = 0.0;
-    if (bd2 || bd3) { for (int t = 0; t <= p; ++t) s += K1[t1 * q + t] * getU(Uc, q, p, t, t2, t3); }
-    else s = K1[t1 * q] * getU(Uc, q, p, 0, t2, t3) + K1[t1 * q + p] * getU(Uc, q, p, p, t2, t3);
-    y += M2[t2] * M3[t3] * s;
-    s = 0.0;
-    if (bd1 || bd3) { for (int t = 0; t <= p; ++t) s += K2[t2 * q + t] * getU(Uc, q, p, t1, t, t3); }
-    else s = K2[t2 * q] * getU(Uc, q, p, t1, 0, t3) + K2[t2 * q + p] * getU(Uc, q, p, t1, p, t3);
-    y += M1[t1] * M3[t3] * s;
-    s = 0.0;
-    if (bd1 || bd2) { for (int t = 0; t <= p; ++t) s += K3[t3 * q + t] * getU(Uc, q, p, t1, t2, t); }
-    else s = K3[t3 * q] * getU(Uc, q, p, t1, t2, 0) + K3[t3 * q + p] * getU(Uc, q, p, t1, t2, p);
-    y += M1[t1] * M2[t2] * s;
-    Ye[o] = y - corr;
-  }
-}
-
-// out = F - sum_e Y_e (residual, F != NULL) or sum_e Y_e (apply, F == NULL), free entries only
-__global__ void k_gather_resid(LevelGeom g, const double* __restrict__ Y, const double* __restrict__ F,
-                               double* __restrict__ out, const int* __restrict__ done) {
-  if (done && *done) return;
-  const int m = g.m, mm = m * m, YS = g.YS;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.nskel;
-       idx += (long long)gridDim.x * blockDim.x) {
-    Entry E = decode_entry(g, idx);
-    double r = 0.0;
-    if (is_free(g, E.g1, E.g2, E.g3) && owned_plane(g, E.v3)) {
-      double s = 0.0;
-      auto el = [&](int a1, int a2, int a3) -> size_t {
-        return ((size_t)a1 + (size_t)g.k1 * ((size_t)a2 + (size_t)g.k2 * a3)) * YS;
-      };
-      // element output, 0 for an element outside the box (a Neumann-face point has one side only)
-      auto yat = [&](int a1, int a2, int a3, int off) -> double {
-        return (a1 >= 0 && a2 >= 0 && a3 >= 0 && a1 < g.k1 && a2 < g.k2 && a3 < g.k3) ? Y[el(a1, a2, a3) + off] : 0.0;
-      };
-      if (E.type < 3) {
-        const int d = E.type, o = E.a * m + E.b;
-        int w1 = E.v1, w2 = E.v2, w3 = E.v3;
-        if (d == 0) w1 -= 1; else if (d == 1) w2 -= 1; else w3 -= 1;
-        s = yat(w1, w2, w3, (2 * d + 1) * mm + o) + yat(E.v1, E.v2, E.v3, (2 * d) * mm + o);
-      } else if (E.type < 6) {
-        const int d = E.type - 3;
-        for (int bB = 0; bB < 2; ++bB)
-          for (int bA = 0; bA < 2; ++bA) {
-            int a1 = E.v1, a2 = E.v2, a3 = E.v3;
-            if (d == 0) { a2 += bA - 1; a3 += bB - 1; }
-            else if (d == 1) { a1 += bA - 1; a3 += bB - 1; }
-            else { a1 += bA - 1; a2 += bB - 1; }
-            int qe = 4 * d + (1 - bA) + 2 * (1 - bB);
-            s += yat(a1, a2, a3, 6 * mm + qe * m + E.a);
-          }
-      } else {
-        for (int c3 = 0; c3 < 2; ++c3)
-          for (int c2 = 0; c2 < 2; ++c2)
-            for (int c1 = 0; c1 < 2; ++c1) {
-              int qv = (1 - c1) + 2 * (1 - c2) + 4 * (1 - c3);
-              s += yat(E.v1 - 1 + c1, E.v2 - 1 + c2, E.v3 - 1 + c3, 6 * mm + 12 * m + qv);
-            }
-      }
-      r = F ? F[idx] - s : s;
-    }
-    out[idx] = r;
-  }
-}
-
-// ------------------------------------------------------------------------------------------
-// star smoother, one colour: per star
-//   gather 3 planes / multiplicity -> T_d = S_b^T F_d S_a -> fused expand / divide / contract
-//   -> U_d = S_b G_d S_a^T -> weight -> add into u (race-free within a colour)
-// ------------------------------------------------------------------------------------------
-size_t star_smem(int p, bool s_in_smem) {
-  int n = 2 * p - 1;
-  return sizeof(double) * (size_t)(7 * n * n + 9 * n + (s_in_smem ? 3 * n * n : 0));
-}
-
-__global__ void __launch_bounds__(256) k_star(LevelGeom g, int c1, int c2, int c3, int n1c, int n2c,
-                                              const double* __restrict__ r, double* __restrict__ u,
-                                              const double* __restrict__ stab, double lam, int s_in_smem) {
-  extern __shared__ double sm[];
-  const int p = g.p, n = g.n, c = p - 1, nn = n * n, ST = g.ST;
-  const int b = blockIdx.x, i1 = b % n1c, rest = b / n1c, i2 = rest % n2c, i3 = rest / n2c;
-  const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
-  if (star_empty(g, v1, v2, v3)) return;  // corner
-  if (v3 < g.own_lo) return;   // ghost star below the slab: computed by the lower rank
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const double* gt[3] = {stab + (size_t)v1 * ST, stab + (size_t)(g.V1 + v2) * ST, stab + (size_t)(g.V1 + g.V2 + v3) * ST};
-  double* FT = sm;
-  double* Gs = FT + 3 * nn;
-  double* X = Gs + 3 * nn;
-  double* vec = X + nn;  // per direction: Lambda[n], s[n], w[n]
-  double* Ssm = vec + 9 * n;
-  for (int i = tid; i < 9 * n; i += nt) { int d = i / (3 * n); vec[i] = gt[d][nn + i - d * 3 * n]; }
-  const double* S[3];
-  if (s_in_smem) {
-    for (int i = tid; i < 3 * nn; i += nt) { int d = i / nn; Ssm[i] = gt[d][i - d * nn]; }
-    S[0] = Ssm; S[1] = Ssm + nn; S[2] = Ssm + 2 * nn;
-  } else {
-    S[0] = gt[0]; S[1] = gt[1]; S[2] = gt[2];
-  }
-  const int o1 = (v1 - 1) * p + 1, o2 = (v2 - 1) * p + 1, o3 = (v3 - 1) * p + 1;
-  for (int i = tid; i < 3 * nn; i += nt) {
-    int d = i / nn, rr = i - d * nn, A = rr / n, B = rr - A * n, j1, j2, j3;
-    if (d == 0) { j1 = c; j2 = B; j3 = A; } else if (d == 1) { j2 = c; j1 = B; j3 = A; } else { j3 = c; j1 = B; j2 = A; }
-    int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
-    double val = inside(g, g1, g2, g3) ? r[skel_index(g, g1, g2, g3)] : 0.0;
-    FT[i] = val / (double)(1 + (A == c) + (B == c));   // inverse multiplicity
-  }
-  __syncthreads();
-  // forward: T_d[ab][aa] = sum_{jb,ja} S_b[jb][ab] F_d[jb][ja] S_a[ja][aa]
-  for (int d = 0; d < 3; ++d) {
-    const double* Sa = S[d == 0 ? 1 : 0];
-    const double* Sb = S[d == 2 ? 1 : 2];
-    double* F = FT + d * nn;
-    for (int i = tid; i < nn; i += nt) {
-      int jb = i / n, aa = i - jb * n;
-      double s = 0.0;
-      for (int ja = 0; ja < n; ++ja) s += F[jb * n + ja] * Sa[ja * n + aa];
-      X[i] = s;
-    }
-    __syncthreads();
-    for (int i = tid; i < nn; i += nt) {
-      int ab = i / n, aa = i - ab * n;
-      double s = 0.0;
-      for (int jb = 0; jb < n; ++jb) s += Sb[jb * n + ab] * X[jb * n + aa];
-      F[i] = s;
-    }
-    __syncthreads();
-  }
-  const double *L1 = vec, *s1 = vec + n, *w1 = vec + 2 * n;
-  const double *L2 = vec + 3 * n, *s2 = vec + 4 * n, *w2 = vec + 5 * n;
-  const double *L3 = vec + 6 * n, *s3 = vec + 7 * n, *w3 = vec + 8 * n;
-  const double *T1 = FT, *T2 = FT + nn, *T3 = FT + 2 * nn;
-  // fused core (Alg. 1 expand / D^-1 / contract): three passes, each reducing along one axis
-  for (int i = tid; i < nn; i += nt) {  // G1[a3][a2] = sum_a1 s1[a1] E
-    int a3 = i / n, a2 = i - a3 * n;
-    double t1 = T1[i], c2 = s2[a2], c3 = s3[a3], base = lam + L2[a2] + L3[a3], acc = 0.0;
-    for (int a1 = 0; a1 < n; ++a1) {
-      double E = (s1[a1] * t1 + c2 * T2[a3 * n + a1] + c3 * T3[a2 * n + a1]) / (base + L1[a1]);
-      acc += s1[a1] * E;
-    }
-    Gs[i] = acc;
-  }
-  for (int i = tid; i < nn; i += nt) {  // G2[a3][a1] = sum_a2 s2[a2] E
-    int a3 = i / n, a1 = i - a3 * n;
-    double t2 = T2[i], c1 = s1[a1], c3 = s3[a3], base = lam + L1[a1] + L3[a3], acc = 0.0;
-    for (int a2 = 0; a2 < n; ++a2) {
-      double E = (c1 * T1[a3 * n + a2] + s2[a2] * t2 + c3 * T3[a2 * n + a1]) / (base + L2[a2]);
-      acc += s2[a2] * E;
-    }
-    Gs[nn + i] = acc;
-  }
-  for (int i = tid; i < nn; i += nt) {  // G3[a2][a1] = sum_a3 s3[a3] E
-    int a2 = i / n, a1 = i - a2 * n;
-    double t3 = T3[i], c1 = s1[a1], c2 = s2[a2], base = lam + L1[a1] + L2[a2], acc = 0.0;
-    for (int a3 = 0; a3 < n; ++a3) {
-      double E = (c1 * T1[a3 * n + a2] + c2 * T2[a3 * n + a1] + s3[a3] * t3) / (base + L3[a3]);
-      acc += s3[a3] * E;
-    }
-    Gs[2 * nn + i] = acc;
-  }
-  __syncthreads();
-  // back: U_d[jb][ja] = sum S_b[jb][ab] S_a[ja][aa] G_d[ab][aa]
-  for (int d = 0; d < 3; ++d) {
-    const double* Sa = S[d == 0 ? 1 : 0];
-    const double* Sb = S[d == 2 ? 1 : 2];
-    const double* Gd = Gs + d * nn;
-    for (int i = tid; i < nn; i += nt) {
-      int ab = i / n, ja = i - ab * n;
-      double s = 0.0;
-      for (int aa = 0; aa < n; ++aa) s += Gd[ab * n + aa] * Sa[ja * n + aa];
-      X[i] = s;
-    }
-    __syncthreads();
-    double* U = FT + d * nn;
-    for (int i = tid; i < nn; i += nt) {
-      int jb = i / n, ja = i - jb * n;
-      double s = 0.0;
-      for (int ab = 0; ab < n; ++ab) s += Sb[jb * n + ab] * X[ab * n + ja];
-      U[i] = s;
-    }
-    __syncthreads();
-  }
-  // weight and add each unique star point once
-  for (int i = tid; i < 3 * nn; i += nt) {
-    int d = i / nn, rr = i - d * nn, A = rr / n, B = rr - A * n, j1, j2, j3;
-    if (d == 0) { j1 = c; j2 = B; j3 = A; }
-    else if (d == 1) { j2 = c; j1 = B; j3 = A; if (j1 == c) continue; }
-    else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
-    int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
-    if (!is_free(g, g1, g2, g3)) continue;
-    u[skel_index(g, g1, g2, g3)] += w1[j1] * w2[j2] * w3[j3] * FT[i];
   }
 }
 

@@ -39,10 +39,12 @@ struct PcgState {
 };
 
 // degree-specialised hot kernels (hot_kernels.cu)
-cudaError_t launch_elem_apply(const LevelGeom& g, const double* u, const double* etab, double lam, double* Y,
-                              const int* done, cudaStream_t st);
+// element operator Y_e = H_hat_e u_e of every element (etabP: padded table of 9 <= p <= 16, else unused)
+cudaError_t launch_elem_apply(const LevelGeom& g, const double* u, const double* etab, const double* etabP, double lam,
+                              double* Y, const int* done, cudaStream_t st);
+// one colour of the star smoother (stabP: padded star table of 9 <= p <= 16, else unused)
 cudaError_t launch_star(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c, long long nb, const double* r,
-                        double* u, const double* stab, const double* stabT, double lam, cudaStream_t st);
+                        double* u, const double* stab, const double* stabP, double lam, cudaStream_t st);
 cudaError_t launch_gather_resid(const LevelGeom& g, const double* Y, const double* F, double* out, const int* done,
                                 cudaStream_t st);
 size_t hot_smem(int p, int which);   // which: 0 element, 1 star
@@ -59,6 +61,11 @@ cudaError_t launch_elem16(const LevelGeom& g, const double* u, const double* eta
 int elem16_etp(int p);
 void elem16_table_row(int p, const double* et_row, double* out_row);
 cudaError_t elem16_set_smem_attr();
+// condensation (mode 0: Yc = H_BI H_II^-1 F_I on the face interiors) and interior recovery (mode 1:
+// u_I = H_II^-1 (F_I - H_IB u_hat) into ug) for 9 <= p <= 16 (cr16.cu), DMMA cube transforms
+cudaError_t launch_cr16(int mode, const LevelGeom& g, const double* Fg, const double* uh, const double* etabP, double lam,
+                        double* Yc, double* ug, cudaStream_t st);
+cudaError_t cr16_set_smem_attr();
 cudaError_t hot_set_smem_attr(int bytes);
 
 // p = 2 coarse operator tables (coarse_cg.cu): assembled 1-D lumped masses b_d[2k_d+1], assembled
@@ -102,8 +109,6 @@ __global__ void k_pcg_hmg_p2(HmgDev h, const double* b, double* xout, double* pv
 __global__ void k_build_coarse_ell(LevelGeom g, CoarseTabs ct, double lam, int* ellc, double* ella);
 __global__ void k_pcg_gv_ell_p2(long long n, const double* b, double* xout, double* vec, double* mbuf, const double* dinv,
                                 const int* ellc, const double* ella, double* part, PcgState* st, double rtol, int maxit);
-size_t elem_apply_smem(int p, int ET);
-size_t star_smem(int p, bool s_in_smem);
 size_t transfer_smem(int pf, int pc);
 size_t condense_smem(int p, int ET, bool cube_in_smem);
 size_t recover_smem(int p, int ET, bool cube_in_smem);
@@ -111,10 +116,6 @@ size_t recover_smem(int p, int ET, bool cube_in_smem);
 __global__ void k_skel_from_grid(LevelGeom g, const double* grid, double* skel);
 __global__ void k_skel_to_grid(LevelGeom g, const double* skel, double* grid);
 __global__ void k_weak_rhs(LevelGeom g, const double* b1, const double* b2, const double* b3, const double* f, double* F);
-__global__ void k_elem_apply(LevelGeom g, const double* u, const double* etab, double lam, double* Y, const int* done);
-__global__ void k_gather_resid(LevelGeom g, const double* Y, const double* F, double* out, const int* done);
-__global__ void k_star(LevelGeom g, int c1, int c2, int c3, int n1c, int n2c, const double* r, double* u,
-                       const double* stab, double lam, int s_in_smem);
 cudaError_t launch_restrict(const LevelGeom& gf, const LevelGeom& gc, const double* Jint, const double* rf, double* Z,
                             double* fc, double* uzero, int nt_local, size_t smem, int gather_blocks, cudaStream_t st);
 __global__ void k_dot_fused(const double* a, const double* b, long long n, double* part, unsigned* ticket, double* out);

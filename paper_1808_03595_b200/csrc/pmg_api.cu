@@ -38,7 +38,6 @@ struct DevLevel {
   LevelGeom g;
   double* etab = nullptr;
   double* stab = nullptr;
-  double* stabT = nullptr;
   double* stabP = nullptr;   // padded star table of k_star16 (9 <= p <= 16)
   double* etabP = nullptr;   // padded element table of k_elem16 (9 <= p <= 16)
   double* ectab = nullptr;   // element-centred smoother tables (opt.smoother == 1)
@@ -62,7 +61,6 @@ struct pmg_ctx {
   double* cube = nullptr;    // condense/recover cube scratch (large p)
   int cube_blocks = 0;
   bool cube_in_smem = true;
-  bool star_s_smem = true;
   double* part = nullptr;    // reduction partials (2 x kRedBlocks)
   double* dres = nullptr;    // device scalar results
   unsigned* ticket = nullptr;  // k_dot_fused's arrival counter (0 between launches)
@@ -92,7 +90,6 @@ struct pmg_ctx {
   long long launches = 0;
   int last_coarse_its = 0;
   long long coarse_its_total = 0;
-  bool ref_kernels = false;  // PMG_REFERENCE_KERNELS=1: runtime-p v1 kernels (A/B checks only)
   bool use_coop = false;     // coarse CG as one persistent cooperative kernel (p0 = 2)
   int coop_nb = 0;
   bool coop_reg = false;     // register-resident variant (one coarse unknown per thread)
@@ -120,8 +117,6 @@ struct pmg_ctx {
   long long launches_per_cycle = 0;
   double* hres = nullptr;    // pinned host scalar
   bool no_graph = false;     // PMG_NO_GRAPH=1
-  bool no_star16 = false;    // PMG_NO_STAR16=1: previous star kernel at 9 <= p <= 16 (A/B)
-  bool no_elem16 = false;    // PMG_NO_ELEM16=1: previous element kernel at 9 <= p <= 16 (A/B)
   // pmg_report phase times: solve-phase events and the coarse-solve bracket (recorded as external
   // event nodes inside the captured cycle graph), created at setup
   cudaEvent_t ev_ph[4] = {nullptr, nullptr, nullptr, nullptr};   // start, condensed, cycles done, recovered
@@ -203,19 +198,9 @@ pmg_status exchange(pmg_ctx* c, int l, double* x) {
 pmg_status residual_dev(pmg_ctx* c, int l, const double* u, const double* f, double* r, const int* done = nullptr) {
   const DevLevel& D = c->D[l];
   TimedRegion tr(c, 1, l == c->L);
-  if (c->ref_kernels) {
-    size_t sm = elem_apply_smem(D.g.p, D.g.ET);
-    k_elem_apply<<<(unsigned)D.g.nelem, kThreads, sm, c->st>>>(D.g, u, D.etab, c->lam, c->Y, done);
-  } else if (D.etabP && !c->no_elem16) {
-    launch_elem16(D.g, u, D.etabP, c->lam, c->Y, done, c->st);
-  } else {
-    launch_elem_apply(D.g, u, D.etab, c->lam, c->Y, done, c->st);
-  }
+  launch_elem_apply(D.g, u, D.etab, D.etabP, c->lam, c->Y, done, c->st);
   LAUNCH_CHECK(c);
-  if (c->ref_kernels)
-    k_gather_resid<<<grid_for(D.g.nskel), kThreads, 0, c->st>>>(D.g, c->Y, f, r, done);
-  else
-    launch_gather_resid(D.g, c->Y, f, r, done, c->st);
+  launch_gather_resid(D.g, c->Y, f, r, done, c->st);
   LAUNCH_CHECK(c);
   return PMG_OK;
 }
@@ -231,19 +216,13 @@ pmg_status smooth_dev(pmg_ctx* c, int l, const double* r, double* u) {
     }
     return PMG_OK;
   }
-  size_t sm = star_smem(g.p, c->star_s_smem);
   for (int col = 0; col < 8; ++col) {   // 8 vertex colours (parity), race-free
     // the z parity is that of the GLOBAL vertex plane, so a z-slab adds the colour corrections
     // of every point in the same order as one GPU (bitwise identical results)
     int c1 = col & 1, c2 = (col >> 1) & 1, c3 = ((col >> 2) & 1) ^ (g.zoff & 1);
     int n1 = (g.k1 - c1) / 2 + 1, n2 = (g.k2 - c2) / 2 + 1, n3 = (g.k3 - c3) / 2 + 1;
     long long nb = (long long)n1 * n2 * n3;
-    if (c->ref_kernels)
-      k_star<<<(unsigned)nb, kThreads, sm, c->st>>>(g, c1, c2, c3, n1, n2, r, u, D.stab, c->lam, c->star_s_smem ? 1 : 0);
-    else if (D.stabP && !c->no_star16)
-      launch_star16(g, c1, c2, c3, n1, n2, nb, r, u, D.stabP, c->lam, c->st);
-    else
-      launch_star(g, c1, c2, c3, n1, n2, nb, r, u, D.stab, D.stabT, c->lam, c->st);
+    launch_star(g, c1, c2, c3, n1, n2, nb, r, u, D.stab, D.stabP, c->lam, c->st);
     LAUNCH_CHECK(c);
   }
   return PMG_OK;
@@ -515,9 +494,13 @@ pmg_status vcycle_dev(pmg_ctx* c, double* u, const double* f, bool r_top_valid) 
 
 pmg_status condense_dev(pmg_ctx* c, const double* F, double* fhat) {
   const DevLevel& D = c->D[c->L];
-  size_t sm = condense_smem(D.g.p, D.g.ET, c->cube_in_smem);
-  int nb = c->cube_in_smem ? (int)std::min<long long>(D.g.nelem, 148LL * 8) : c->cube_blocks;
-  launch_condense_elem(nb, kThreads, sm, c->st, D.g, F, D.etab, c->lam, c->Y, c->cube_in_smem ? nullptr : c->cube);
+  if (D.etabP) {   // 9 <= p <= 16: DMMA cube transforms (cr16.cu)
+    launch_cr16(0, D.g, F, nullptr, D.etabP, c->lam, c->Y, nullptr, c->st);
+  } else {
+    size_t sm = condense_smem(D.g.p, D.g.ET, c->cube_in_smem);
+    int nb = c->cube_in_smem ? (int)std::min<long long>(D.g.nelem, 148LL * 8) : c->cube_blocks;
+    launch_condense_elem(nb, kThreads, sm, c->st, D.g, F, D.etab, c->lam, c->Y, c->cube_in_smem ? nullptr : c->cube);
+  }
   LAUNCH_CHECK(c);
   k_condense_gather<<<grid_for(D.g.nskel), kThreads, 0, c->st>>>(D.g, F, c->Y, fhat);
   LAUNCH_CHECK(c);
@@ -529,9 +512,13 @@ pmg_status recover_dev(pmg_ctx* c, const double* uhat, const double* F, double* 
   const long long ng = (long long)(D.g.k1 * D.g.p + 1) * (D.g.k2 * D.g.p + 1) * (D.g.k3 * D.g.p + 1);
   k_skel_to_grid<<<grid_for(ng), kThreads, 0, c->st>>>(D.g, uhat, ufull);
   LAUNCH_CHECK(c);
-  size_t sm = recover_smem(D.g.p, D.g.ET, c->cube_in_smem);
-  int nb = c->cube_in_smem ? (int)std::min<long long>(D.g.nelem, 148LL * 8) : c->cube_blocks;
-  launch_recover_elem(nb, kThreads, sm, c->st, D.g, F, uhat, D.etab, c->lam, ufull, c->cube_in_smem ? nullptr : c->cube);
+  if (D.etabP) {
+    launch_cr16(1, D.g, F, uhat, D.etabP, c->lam, nullptr, ufull, c->st);
+  } else {
+    size_t sm = recover_smem(D.g.p, D.g.ET, c->cube_in_smem);
+    int nb = c->cube_in_smem ? (int)std::min<long long>(D.g.nelem, 148LL * 8) : c->cube_blocks;
+    launch_recover_elem(nb, kThreads, sm, c->st, D.g, F, uhat, D.etab, c->lam, ufull, c->cube_in_smem ? nullptr : c->cube);
+  }
   LAUNCH_CHECK(c);
   return PMG_OK;
 }
@@ -702,7 +689,7 @@ pmg_status solve_dev(pmg_ctx* c, const double* F, double* ufull, double rtol, in
 void free_ctx(pmg_ctx* c) {
   if (!c) return;
   for (auto& D : c->D) {
-    cudaFree(D.etab); cudaFree(D.stab); cudaFree(D.stabT); cudaFree(D.stabP); cudaFree(D.etabP); cudaFree(D.ectab); cudaFree(D.Jint);
+    cudaFree(D.etab); cudaFree(D.stab); cudaFree(D.stabP); cudaFree(D.etabP); cudaFree(D.ectab); cudaFree(D.Jint);
     cudaFree(D.u); cudaFree(D.f); cudaFree(D.r);
   }
   cudaFree(c->ticket);
@@ -849,12 +836,12 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
     DevLevel& D = c->D[l];
     const HostLevel& Hl = c->H[l];
     D.g = Hl.g;
-    std::vector<double> et = Hl.etab, st = Hl.stab, stT = Hl.stabT;
+    std::vector<double> et = Hl.etab, st = Hl.stab;
     if (c->tr) {
       // the rank's slab: vertex planes zb .. z1, element layers zb .. z1-1 (one ghost layer
       // below); direction-3 rows of the element / star tables sliced to match
       LevelGeom& g = D.g;
-      const int k1 = g.k1, k2 = g.k2, V1 = g.V1, V2 = g.V2, n = g.n;
+      const int k1 = g.k1, k2 = g.k2, V1 = g.V1, V2 = g.V2;
       g.k3 = sp.z1 - sp.zb;
       g.V3 = g.k3 + 1;
       g.nrec = (long long)g.V1 * g.V2 * g.V3;
@@ -868,10 +855,8 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
       et.insert(et.end(), Hl.etab.begin() + (size_t)(k1 + k2 + sp.zb) * g.ET, Hl.etab.begin() + (size_t)(k1 + k2 + sp.z1) * g.ET);
       st.assign(Hl.stab.begin(), Hl.stab.begin() + (size_t)(V1 + V2) * g.ST);
       st.insert(st.end(), Hl.stab.begin() + (size_t)(V1 + V2 + sp.zb) * g.ST, Hl.stab.begin() + (size_t)(V1 + V2 + sp.z1 + 1) * g.ST);
-      stT.assign(Hl.stabT.begin(), Hl.stabT.begin() + (size_t)(V1 + V2) * n * n);
-      stT.insert(stT.end(), Hl.stabT.begin() + (size_t)(V1 + V2 + sp.zb) * n * n, Hl.stabT.begin() + (size_t)(V1 + V2 + sp.z1 + 1) * n * n);
     }
-    if ((s = upload(&D.etab, et)) || (s = upload(&D.stab, st)) || (s = upload(&D.stabT, stT))) { free_ctx(c); return s; }
+    if ((s = upload(&D.etab, et)) || (s = upload(&D.stab, st))) { free_ctx(c); return s; }
     if (D.g.p >= 9 && D.g.p <= 16) {   // k_star16's padded table: NP x NP S, then Lambda (pad 1), s, w (pad 0)
       const int n = D.g.n, NP = star16_np(D.g.p), STP = NP * NP + 3 * NP;
       const size_t rows = st.size() / D.g.ST;
@@ -903,21 +888,12 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
     cudaMemset(D.f, 0, D.g.nskel * sizeof(double));
     cudaMemset(D.r, 0, D.g.nskel * sizeof(double));
     Ylen = std::max<size_t>(Ylen, (size_t)D.g.nelem * D.g.YS);
-    max_elem = std::max(max_elem, elem_apply_smem(D.g.p, D.g.ET));
     if (l >= 1) {
       Zlen = std::max<size_t>(Zlen, (size_t)D.g.nrec * zs_of(deg[l - 1]));
       max_tr = std::max(max_tr, transfer_smem(D.g.p, deg[l - 1]));
     }
   }
   const LevelGeom& gt = c->D[L].g;
-  {
-    const char* env = std::getenv("PMG_REFERENCE_KERNELS");
-    c->ref_kernels = env && env[0] == '1';
-  }
-  // the v1 reference star kernel keeps S in shared memory when the top level allows it
-  c->star_s_smem = star_smem(p, true) <= (size_t)smem_optin;
-  if (c->ref_kernels)
-    for (int l = 0; l <= L; ++l) max_star = std::max(max_star, star_smem(c->D[l].g.p, c->star_s_smem));
   c->cube_in_smem = std::max(condense_smem(p, gt.ET, true), recover_smem(p, gt.ET, true)) <= (size_t)smem_optin;
   size_t max_cond = condense_smem(p, gt.ET, c->cube_in_smem), max_rec = recover_smem(p, gt.ET, c->cube_in_smem);
   Ylen = std::max<size_t>(Ylen, (size_t)gt.nelem * 6 * gt.m * gt.m);
@@ -983,8 +959,7 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   if (dalloc(&c->Fdev, c->n_grid) || dalloc(&c->Udev, c->n_grid)) { free_ctx(c); return fail(PMG_ENOMEM, "cudaMalloc failed (grid buffers)"); }
   // the attribute is per function, not per context: always allow the device maximum so that
   // several contexts with different degrees can coexist
-  cudaError_t e1 = cudaFuncSetAttribute(k_elem_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
-  cudaError_t e2 = cudaFuncSetAttribute(k_star, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  cudaError_t e1 = cudaSuccess, e2 = cudaSuccess;
   cudaError_t e3 = transfer_set_smem_attr(smem_optin);
   cudaError_t e4 = cudaSuccess;
   if (o.smoother == 1) {
@@ -993,15 +968,10 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   }
   cudaError_t e5 = condense_recover_set_smem_attr(smem_optin);
   cudaError_t e6 = cudaSuccess;
-  {
-    const char* e = std::getenv("PMG_NO_STAR16");
-    c->no_star16 = e && e[0] == '1';
-    e = std::getenv("PMG_NO_ELEM16");
-    c->no_elem16 = e && e[0] == '1';
-  }
   if (e6 == cudaSuccess) e6 = hot_set_smem_attr(smem_optin);
   if (e6 == cudaSuccess) e6 = star16_set_smem_attr();
   if (e6 == cudaSuccess) e6 = elem16_set_smem_attr();
+  if (e6 == cudaSuccess) e6 = cr16_set_smem_attr();
   if (e1 || e2 || e3 || e4 || e5 || e6) { free_ctx(c); return fail(PMG_ECUDA, "cudaFuncSetAttribute failed"); }
   // persistent cooperative coarse CG when the coarse degree is 2 and the device supports it
   {

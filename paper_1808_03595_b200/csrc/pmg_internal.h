@@ -80,7 +80,6 @@ struct HostLevel {
   LevelGeom g;
   std::vector<double> etab;      // (k1 + k2 + k3) * ET
   std::vector<double> stab;      // (V1 + V2 + V3) * ST
-  std::vector<double> stabT;     // (V1 + V2 + V3) * n^2: S^T of each star table row
   std::vector<double> ectab;     // (k1 + k2 + k3) * ec_table_stride(p) (element-centred smoother only)
   std::vector<double> Jint;      // (p - 1) x (p_c + 1): rows 1..p-1 of J (coarse -> this level)
   std::vector<double> coords[3];

@@ -210,7 +210,6 @@ std::string build_level(HostLevel& L, int p, const int k[3], const double* const
 
   // star tables
   L.stab.assign((size_t)(g.V1 + g.V2 + g.V3) * g.ST, 0.0);
-  L.stabT.assign((size_t)(g.V1 + g.V2 + g.V3) * n * n, 0.0);
   base = 0;
   for (int d = 0; d < 3; ++d)
     for (int v = 0; v <= k[d]; ++v, ++base) {
@@ -253,9 +252,6 @@ std::string build_level(HostLevel& L, int p, const int k[3], const double* const
         for (int b = 0; b < nc; ++b) lamv[cpl[b]] = lc[b];
       }
       for (int i = 0; i < n * n; ++i) T[i] = S[i];
-      double* TT = &L.stabT[base * n * n];
-      for (int j = 0; j < n; ++j)
-        for (int a = 0; a < n; ++a) TT[a * n + j] = S[j * n + a];
       for (int a = 0; a < n; ++a) T[n * n + a] = lamv[a];
       for (int a = 0; a < n; ++a) T[n * n + n + a] = S[c * n + a];
       for (int j = 0; j < n; ++j) {

@@ -124,8 +124,7 @@ __global__ void __launch_bounds__(128, 3)
   constexpr int N = K::N, NN = K::NN, C = K::C, M = K::M, MM = K::MM, NP = K::NP, LD = K::LD, MS = K::MS, NT = K::NT,
                 STP = K::STP, RS = K::RS;
   extern __shared__ double sm[];
-  const int bid = blockIdx.x, i1 = bid % n1c, rest = bid / n1c, i2 = rest % n2c, i3 = rest / n2c;
-  const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
+  const int v1 = c1 + 2 * (int)blockIdx.x, v2 = c2 + 2 * (int)blockIdx.y, v3 = c3 + 2 * (int)blockIdx.z;   // 3-D grid
   if (star_empty(g, v1, v2, v3)) return;
   if (v3 < g.own_lo) return;   // ghost star below the slab: computed by the lower rank
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -410,8 +409,8 @@ cudaError_t launch_star16(const LevelGeom& g, int c1, int c2, int c3, int n1c, i
   switch (g.p) {
 #define CASE(PP)                                                                                                     \
   case PP:                                                                                                           \
-    return launch_pdl(k_star16<PP>, dim3((unsigned)nb), dim3(Star16<PP>::NT), star16_smem<PP>(), st, g, c1, c2, c3, n1c, \
-                      n2c, r, u, stabP, lam);
+    return launch_pdl(k_star16<PP>, dim3((unsigned)n1c, (unsigned)n2c, (unsigned)(nb / ((long long)n1c * n2c))),     \
+                      dim3(Star16<PP>::NT), star16_smem<PP>(), st, g, c1, c2, c3, n1c, n2c, r, u, stabP, lam);
     CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
 #undef CASE
     default: return cudaErrorInvalidValue;

@@ -419,46 +419,6 @@ def test_degenerate_meshes(k, p):
     s.close()
 
 
-@pytest.mark.parametrize("name", ["k323_p4_lam1.7_stretched", "k333_p8_lam0", "k222_p6_lam2"])
-def test_kernel_variants_agree(name, monkeypatch):
-    """The alternative kernels kept for A/B measurements compute the same operators as the
-    defaults: star smoother variants (DFMA transforms, DMMA without prefetch, 128-thread prefetching
-    kernel at p <= 4), element-operator variants (DFMA, DMMA without the boundary cube), and the
-    runtime-degree reference kernels."""
-    import paper_1808_03595_b200 as pmg
-    P = pair(name)
-    case = P.case
-    rng = np.random.default_rng(4)
-    outs = {}
-    for label, env in [("default", {}), ("star1", {"PMG_STAR_VARIANT": "1"}), ("star2", {"PMG_STAR_VARIANT": "2"}),
-                       ("star3", {"PMG_STAR_VARIANT": "3"}), ("elem1", {"PMG_ELEM_VARIANT": "1"}),
-                       ("elem2", {"PMG_ELEM_VARIANT": "2"}), ("ref", {"PMG_REFERENCE_KERNELS": "1"})]:
-        for k in ("PMG_STAR_VARIANT", "PMG_ELEM_VARIANT", "PMG_REFERENCE_KERNELS"):
-            monkeypatch.delenv(k, raising=False)
-        for k, v in env.items():
-            monkeypatch.setenv(k, v)
-        s = pmg.Solver(case.k, case.widths, case.p, case.lam, coarse_rtol=1e-13)
-        res = []
-        for l in range(s.nlevels):
-            g = torch.from_numpy(np.random.default_rng(l).standard_normal(s.level_info(l)[2])).cuda()
-            x = s.new_skel(l)
-            s.skel_from_grid(l, g, x)
-            r = s.new_skel(l)
-            s.residual(l, x, None, r)
-            u = s.new_skel(l)
-            s.smooth(l, x, u)
-            torch.cuda.synchronize()
-            res.append((r.cpu().numpy(), u.cpu().numpy()))
-        outs[label] = res
-        s.close()
-    base = outs["default"]
-    for label, res in outs.items():
-        for (r, u), (r0, u0) in zip(res, base):
-            assert rel(r, r0) < 1e-12, (label, rel(r, r0))
-            assert rel(u, u0) < 1e-12, (label, rel(u, u0))
-    del rng
-
-
 def test_solve_host_and_report_paths():
     """pmg_solve_host (host buffers, pageable and pinned) equals the device solve bitwise; repeated
     solves are bitwise deterministic (graph replay); max_cycles too small returns PMG_ENOCONV with
@@ -488,29 +448,6 @@ def test_solve_host_and_report_paths():
     torch.cuda.synchronize()
     assert r3["status"] == pmg.PMG_ENOCONV and not r3["converged"] and r3["cycles"] == 1
     assert r3["r_final"] < r3["r0"] and float(u3.abs().max()) > 0
-
-
-@pytest.mark.parametrize("k,p", [((2, 3, 2), 17), ((2, 2, 2), 24), ((2, 2, 3), 32)])
-def test_high_degree_star_kernels_agree(k, p, monkeypatch):
-    """p > 16: the DMMA-transform star kernel (k_star_tm, default) and the DFMA-transform kernel
-    (k_star_t) compute the same smoother; oracle parity at p = 24 is in test_gpu_fullsize."""
-    import paper_1808_03595_b200 as pmg
-    case = pi.small_case(k, p, 0.4, stretch=1.3)
-    outs = []
-    for v in ("0", "1"):
-        monkeypatch.setenv("PMG_STAR_VARIANT", v)
-        s = pmg.Solver(case.k, case.widths, p, case.lam)
-        L = s.nlevels - 1
-        g = torch.from_numpy(np.random.default_rng(p).standard_normal(s.level_info(L)[2])).cuda()
-        r = s.new_skel(L)
-        s.skel_from_grid(L, g, r)
-        u = s.new_skel(L)
-        s.smooth(L, r, u)
-        torch.cuda.synchronize()
-        outs.append(u.cpu().numpy())
-        s.close()
-    assert rel(outs[0], outs[1]) < 1e-12
-
 
 
 NEUMANN_CASES = {

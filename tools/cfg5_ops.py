@@ -17,6 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=5)
 ap.add_argument("--p", type=int, default=None)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--solve", action="store_true", help="also one full solve (condense / recover kernels)")
 a = ap.parse_args()
 case = pi.config(a.config, p=a.p)
 s = pmg.Solver(case.k, case.widths, case.p, case.lam)
@@ -29,5 +30,10 @@ q = torch.zeros_like(r)
 for _ in range(a.reps):
     s.smooth(L, r, u)
     s.residual(L, u, f, q)
+if a.solve:
+    F = s.new_grid()
+    F.copy_(torch.randn_like(F))
+    ug = s.new_grid()
+    s.solve(F, ug, 1e-10)
 torch.cuda.synchronize()
 print("ok", case.name, n)
