@@ -67,17 +67,21 @@ __device__ __forceinline__ void cube_pass(const double* __restrict__ in, double*
   using K = CR16<P>;
   constexpr int M = K::M, LD = K::LD, RT = (K::CR + 7) / 8;
   const int r8 = lane >> 2, q4 = lane & 3;
+  double sb[4][2];   // the B fragments of S: the same for every row panel of the pass
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int k = 4 * kk + q4, jj = 8 * j + r8;
+      sb[kk][j] = TR ? S[k * LD + jj] : S[jj * LD + k];
+    }
   for (int mi = warp; mi < RT; mi += K::NW) {
     double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
-      const int k = 4 * kk + q4;
-      const double a = in[(8 * mi + r8) * LD + k];
+      const double a = in[(8 * mi + r8) * LD + 4 * kk + q4];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int jj = 8 * j + r8;
-        dmma_c(c[j][0], c[j][1], a, TR ? S[k * LD + jj] : S[jj * LD + k]);
-      }
+      for (int j = 0; j < 2; ++j) dmma_c(c[j][0], c[j][1], a, sb[kk][j]);
     }
     const int row = 8 * mi + r8;
     if (row < K::CR) {
@@ -149,9 +153,11 @@ __global__ void __launch_bounds__(256, 2)
   pdl_trigger();
   const long long N1 = (long long)g.k1 * P + 1, N2 = (long long)g.k2 * P + 1;
   // F_I -> C0[(i3 m + i2)][i1]
-  for (int i = tid; i < MM * M; i += NT) {
-    const int r = i / M, i1 = i - r * M, i3 = r / M, i2 = r - i3 * M;
-    cpa8c(&C0[r * LD + i1], Fg + (e1 * P + i1 + 1) + N1 * ((e2 * P + i2 + 1) + N2 * (long long)(e3 * P + i3 + 1)));
+  for (int r = tid; r < MM; r += NT) {   // one interior grid row (i3, i2) per thread
+    const int i3 = r / M, i2 = r - i3 * M;
+    const double* src = Fg + (e1 * P + 1) + N1 * ((e2 * P + i2 + 1) + N2 * (long long)(e3 * P + i3 + 1));
+#pragma unroll
+    for (int i1 = 0; i1 < M; ++i1) cpa8c(&C0[r * LD + i1], src + i1);
   }
   if (MODE == 1) {   // face interiors of u_hat -> Fa[f][A][B] (A slow, B fast tangential index)
     const long long V12 = (long long)g.V1 * g.V2;
@@ -199,19 +205,29 @@ __global__ void __launch_bounds__(256, 2)
   {
     const double *a10 = tb + MS + 16, *a11 = tb + MS + 32, *a20 = tb + TB + MS + 16, *a21 = tb + TB + MS + 32,
                  *a30 = tb + 2 * TB + MS + 16, *a31 = tb + 2 * TB + MS + 32;
-    for (int i = tid; i < MM * M; i += NT) {
-      const int r = i / M, b1 = i - r * M, b3 = r / M, b2 = r - b3 * M;
-      double v = C1[r * LD + b1];
+    for (int r = tid; r < MM; r += NT) {   // one row (b3, b2) per thread
+      const int b3 = r / M, b2 = r - b3 * M;
+      const double base = lam + L2[b2] + L3[b3];
+      double t0 = 0.0, t1 = 0.0, c2 = 0.0, c3 = 0.0, c4 = 0.0, c5 = 0.0;
       if (MODE == 1) {
-        double E = a10[b1] * Fa[0 * MS + b3 * LD + b2];
-        E = fma(a11[b1], Fa[1 * MS + b3 * LD + b2], E);
-        E = fma(a20[b2], Fa[2 * MS + b3 * LD + b1], E);
-        E = fma(a21[b2], Fa[3 * MS + b3 * LD + b1], E);
-        E = fma(a30[b3], Fa[4 * MS + b2 * LD + b1], E);
-        E = fma(a31[b3], Fa[5 * MS + b2 * LD + b1], E);
-        v -= E;
+        t0 = Fa[0 * MS + b3 * LD + b2];
+        t1 = Fa[1 * MS + b3 * LD + b2];
+        c2 = a20[b2]; c3 = a21[b2]; c4 = a30[b3]; c5 = a31[b3];
       }
-      C1[r * LD + b1] = v * rcp3c(lam + L1[b1] + L2[b2] + L3[b3]);
+#pragma unroll
+      for (int b1 = 0; b1 < M; ++b1) {
+        double v = C1[r * LD + b1];
+        if (MODE == 1) {
+          double E = a10[b1] * t0;
+          E = fma(a11[b1], t1, E);
+          E = fma(c2, Fa[2 * MS + b3 * LD + b1], E);
+          E = fma(c3, Fa[3 * MS + b3 * LD + b1], E);
+          E = fma(c4, Fa[4 * MS + b2 * LD + b1], E);
+          E = fma(c5, Fa[5 * MS + b2 * LD + b1], E);
+          v -= E;
+        }
+        C1[r * LD + b1] = v * rcp3c(base + L1[b1]);
+      }
     }
   }
   __syncthreads();
@@ -222,12 +238,11 @@ __global__ void __launch_bounds__(256, 2)
       double acc = 0.0;
       if (A < M && B < M) {
         const double* af = tb + d * TB + MS + (s ? 32 : 16);
-#pragma unroll 5
-        for (int t = 0; t < M; ++t) {
-          int b1, b2, b3;
-          if (d == 0) { b1 = t; b3 = A; b2 = B; } else if (d == 1) { b2 = t; b3 = A; b1 = B; } else { b3 = t; b2 = A; b1 = B; }
-          acc = fma(af[t], C1[(b3 * M + b2) * LD + b1], acc);
-        }
+        // V[b3][b2][b1] at C1[(b3 m + b2) LD + b1]: the line along the face normal
+        const double* v = C1 + (d == 0 ? (A * M + B) * LD : (d == 1 ? A * M * LD + B : A * LD + B));
+        const int st = d == 0 ? 1 : (d == 1 ? LD : M * LD);
+#pragma unroll
+        for (int t = 0; t < M; ++t) acc = fma(af[t], v[t * st], acc);
       }
       Fa[f * MS + A * LD + B] = acc;
     }
@@ -249,16 +264,45 @@ __global__ void __launch_bounds__(256, 2)
       Ye[i] = Fa[f * MS + A * LD + B];
     }
   } else {
-    // back transforms S along x1, x2, x3: C1 -> C0 -> C1 -> C0 ([i3][i2][i1] in C0), then store
+    // back transforms S along x1, x2, x3: C1 -> C0 -> C1 -> C0 ([i3][i2][i1] in C0), then store;
+    // meanwhile vertex record e of u_hat is staged in Fa (the T faces are dead)
+    {
+      const long long rb = (e1 + g.V1 * (long long)e2 + (long long)g.V1 * g.V2 * e3) * RS;
+      for (int i = tid; i < RS; i += NT) cpa8c(&Fa[i], uh + rb + i);
+      asm volatile("cp.async.commit_group;\n" ::);
+    }
     cube_pass<P, false>(C1, C0, S1, warp, lane);
     __syncthreads();
     cube_pass<P, false>(C0, C1, S2, warp, lane);
     __syncthreads();
     cube_pass<P, false>(C1, C0, S3, warp, lane);
+    asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();
-    for (int i = tid; i < MM * M; i += NT) {
-      const int r = i / M, i1 = i - r * M, i3 = r / M, i2 = r - i3 * M;
-      ug[(e1 * P + i1 + 1) + N1 * ((e2 * P + i2 + 1) + N2 * (long long)(e3 * P + i3 + 1))] = C0[r * LD + i1];
+    // the element's grid block t in [0, p)^3: interior points from C0, the points with some t_d = 0
+    // from vertex record e (its faces, edges and vertex are exactly those points; staged in Fa).  The
+    // planes t_d = p of the last element of a row belong to the next record: launch_skel_scatter_hi.
+    for (int r = tid; r < P * P; r += NT) {   // one grid row (t3, t2) of p points per thread
+      const int t3 = r / P, t2 = r - t3 * P;
+      double* dst = ug + (long long)e1 * P + N1 * ((e2 * P + t2) + N2 * (long long)(e3 * P + t3));
+      const double* Rec = Fa;   // record e, RS entries
+      if (t2 > 0 && t3 > 0) {
+        dst[0] = Rec[(t3 - 1) * M + (t2 - 1)];                           // face f1 interior
+        const double* row = C0 + ((t3 - 1) * M + (t2 - 1)) * LD;
+#pragma unroll
+        for (int t1 = 1; t1 < P; ++t1) dst[t1] = row[t1 - 1];
+      } else if (t2 == 0 && t3 == 0) {
+        dst[0] = Rec[3 * MM + 3 * M];                                    // vertex
+#pragma unroll
+        for (int t1 = 1; t1 < P; ++t1) dst[t1] = Rec[3 * MM + t1 - 1];   // edge e1
+      } else if (t2 == 0) {                                              // t3 > 0: edge e3, face f2
+        dst[0] = Rec[3 * MM + 2 * M + t3 - 1];
+#pragma unroll
+        for (int t1 = 1; t1 < P; ++t1) dst[t1] = Rec[MM + (t3 - 1) * M + t1 - 1];
+      } else {                                                           // t3 == 0, t2 > 0: edge e2, face f3
+        dst[0] = Rec[3 * MM + M + t2 - 1];
+#pragma unroll
+        for (int t1 = 1; t1 < P; ++t1) dst[t1] = Rec[2 * MM + (t2 - 1) * M + t1 - 1];
+      }
     }
   }
 }

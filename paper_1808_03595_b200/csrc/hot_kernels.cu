@@ -1282,8 +1282,8 @@ __global__ void __launch_bounds__(256) k_gather_resid_t(LevelGeom g, const doubl
 // ------------------------------------------------------------------------------------------
 // dispatch: one production kernel per degree range
 //   element operator: k_elem_pf (p <= 8), k_elem16 (9..16, elem16.cu), k_elem_apply_t (17..32)
-//   star smoother:    k_star_w (p <= 4 and >= star_w_min stars per colour), k_star_pf (p <= 8),
-//                     k_star16 (9..16, star16.cu), k_star_tm (17..32)
+//   star smoother:    k_star_w (p <= 4 and >= star_w_min stars per colour), k_star_pf (p <= 4),
+//                     k_star16 (5..16, star16.cu), k_star_tm (17..32)
 // ------------------------------------------------------------------------------------------
 // stars per colour from which k_star_w (warp per star, p <= 4) replaces k_star_pf; PMG_STAR_W_MIN
 // overrides the default (tests force the kernel onto small parity meshes with 0)
@@ -1308,8 +1308,10 @@ cudaError_t launch_elem_p(const LevelGeom& g, const double* u, const double* eta
 template <int P>
 cudaError_t launch_star_p(const LevelGeom& g, int c1, int c2, int c3, int n1c, int n2c, long long nb, const double* r,
                           double* u, const double* stab, const double* stabP, double lam, cudaStream_t st) {
-  if constexpr (P <= 8) {
-    if constexpr (P <= 4) {
+  if constexpr (P >= 5 && P <= 16) {
+    return launch_star16(g, c1, c2, c3, n1c, n2c, nb, r, u, stabP, lam, st);
+  } else if constexpr (P <= 4) {
+    {
       // warp per star pays off once a colour has many waves of 128-thread stars (large meshes);
       // for a few hundred stars the shorter per-star chain of k_star_pf wins (measured, config 2)
       if (nb >= star_w_min(4LL * 148 * StarPfCfg<P>::MINB))
@@ -1318,8 +1320,6 @@ cudaError_t launch_star_p(const LevelGeom& g, int c1, int c2, int c3, int n1c, i
     }
     return launch_pdl(k_star_pf<P>, dim3((unsigned)nb), dim3(StarPfCfg<P>::NT), star_pf_smem<P>(), st, g, c1, c2, c3, n1c,
                       n2c, r, u, stab, lam);
-  } else if constexpr (P <= 16) {
-    return launch_star16(g, c1, c2, c3, n1c, n2c, nb, r, u, stabP, lam, st);
   } else {
     return launch_pdl(k_star_tm<P>, dim3((unsigned)nb), dim3(StarTmCfg<P>::NT), star_tm_smem<P>(), st, g, c1, c2, c3, n1c,
                       n2c, r, u, stab, lam);
@@ -1375,7 +1375,7 @@ size_t hot_smem(int p, int which) {
   case P:                                                                                                    \
     if (which == 0) return P <= 8 ? elem_pf_smem<(P <= 8 ? P : 2)>() : (P > 16 ? elem_t_smem<P>() : 0);      \
     return P <= 4 ? std::max(star_pf_smem<(P <= 4 ? P : 2)>(), star_w_smem<(P <= 4 ? P : 2)>())            \
-                  : (P <= 8 ? star_pf_smem<(P <= 8 ? P : 2)>() : (P > 16 ? star_tm_smem<(P > 16 ? P : 17)>() : 0));
+                  : (P > 16 ? star_tm_smem<(P > 16 ? P : 17)>() : 0);
     PMG_DEGREES(CASE)
 #undef CASE
     default: return 0;
@@ -1389,8 +1389,8 @@ cudaError_t hot_set_smem_attr(int bytes) {
     cudaError_t a = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (a != cudaSuccess) e = a;                                                      \
   }
-#define CASE8(P) SET(k_elem_pf<P>) SET(k_star_pf<P>)
-#define CASE4(P) SET(k_star_w<P>)
+#define CASE8(P) SET(k_elem_pf<P>)
+#define CASE4(P) SET(k_star_w<P>) SET(k_star_pf<P>)
 #define CASE32(P) SET(k_elem_apply_t<P>) SET(k_star_tm<P>)
   CASE8(2) CASE8(3) CASE8(4) CASE8(5) CASE8(6) CASE8(7) CASE8(8)
   CASE4(2) CASE4(3) CASE4(4)

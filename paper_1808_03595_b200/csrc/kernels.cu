@@ -55,6 +55,63 @@ __global__ void k_skel_to_grid(LevelGeom g, const double* __restrict__ skel, dou
   }
 }
 
+// skeleton values -> their grid points only (the recovery writes every element interior): one block
+// per vertex record (3-D grid), the record's face interiors, edge interiors and vertex; entries of the
+// record that lie outside the box (faces / edges of records on the high box faces) are skipped
+template <int P>
+__global__ void __launch_bounds__(128) k_skel_scatter_t(LevelGeom g, const double* __restrict__ skel,
+                                                        double* __restrict__ grid, int o1, int o2, int o3) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int m = P - 1, mm = m * m, RS = 3 * mm + 3 * m + 1;
+  const int v1 = blockIdx.x + o1, v2 = blockIdx.y + o2, v3 = blockIdx.z + o3;   // record (offset grid)
+  const long long N1 = (long long)g.k1 * P + 1, N2 = (long long)g.k2 * P + 1;
+  const double* R = skel + (v1 + (long long)g.V1 * (v2 + (long long)g.V2 * v3)) * RS;
+  const long long g0 = (long long)v1 * P + N1 * ((long long)v2 * P + N2 * (long long)v3 * P);
+  const bool in1 = v1 < g.k1, in2 = v2 < g.k2, in3 = v3 < g.k3;
+  for (int l = threadIdx.x; l < mm; l += blockDim.x) {
+    const int a = l / m, b = l - a * m;   // a: slow, b: fast in-face index (record layout)
+    if (in2 && in3) grid[g0 + N1 * ((b + 1) + N2 * (long long)(a + 1))] = R[l];                 // f1: (t3, t2)
+    if (in1 && in3) grid[g0 + (b + 1) + N1 * N2 * (long long)(a + 1)] = R[mm + l];              // f2: (t3, t1)
+    if (in1 && in2) grid[g0 + (b + 1) + N1 * (long long)(a + 1)] = R[2 * mm + l];               // f3: (t2, t1)
+  }
+  for (int t = threadIdx.x; t < m; t += blockDim.x) {
+    if (in1) grid[g0 + t + 1] = R[3 * mm + t];
+    if (in2) grid[g0 + N1 * (t + 1)] = R[3 * mm + m + t];
+    if (in3) grid[g0 + N1 * N2 * (long long)(t + 1)] = R[3 * mm + 2 * m + t];
+  }
+  if (threadIdx.x == 0) grid[g0] = R[3 * mm + 3 * m];
+}
+
+cudaError_t launch_skel_scatter(const LevelGeom& g, const double* skel, double* grid, cudaStream_t st, bool hi_only) {
+  if (hi_only) {   // the records of the three high box planes (v_d = k_d)
+    cudaError_t e;
+    const LevelGeom* gp = &g;
+    auto one = [&](dim3 grd, int o1, int o2, int o3) -> cudaError_t {
+      switch (gp->p) {
+#define CASE(P) case P: return launch_pdl(k_skel_scatter_t<P>, grd, dim3(128), 0, st, g, skel, grid, o1, o2, o3);
+        CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14)
+        CASE(15) CASE(16) CASE(17) CASE(18) CASE(19) CASE(20) CASE(21) CASE(22) CASE(23) CASE(24) CASE(25) CASE(26)
+        CASE(27) CASE(28) CASE(29) CASE(30) CASE(31) CASE(32)
+#undef CASE
+        default: return cudaErrorInvalidValue;
+      }
+    };
+    if ((e = one(dim3(1, (unsigned)g.V2, (unsigned)g.V3), g.k1, 0, 0)) != cudaSuccess) return e;
+    if ((e = one(dim3((unsigned)g.V1, 1, (unsigned)g.V3), 0, g.k2, 0)) != cudaSuccess) return e;
+    return one(dim3((unsigned)g.V1, (unsigned)g.V2, 1), 0, 0, g.k3);
+  }
+  const dim3 grd((unsigned)g.V1, (unsigned)g.V2, (unsigned)g.V3);
+  switch (g.p) {
+#define CASE(P) case P: return launch_pdl(k_skel_scatter_t<P>, grd, dim3(128), 0, st, g, skel, grid, 0, 0, 0);
+    CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14)
+    CASE(15) CASE(16) CASE(17) CASE(18) CASE(19) CASE(20) CASE(21) CASE(22) CASE(23) CASE(24) CASE(25) CASE(26)
+    CASE(27) CASE(28) CASE(29) CASE(30) CASE(31) CASE(32)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 // F = b1[i1] b2[i2] b3[i3] f (assembled GLL-lumped mass is a tensor product of 1-D assembled masses)
 __global__ void k_weak_rhs(LevelGeom g, const double* __restrict__ b1, const double* __restrict__ b2,
                            const double* __restrict__ b3, const double* __restrict__ f, double* __restrict__ F) {

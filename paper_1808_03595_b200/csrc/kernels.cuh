@@ -115,6 +115,9 @@ size_t recover_smem(int p, int ET, bool cube_in_smem);
 
 __global__ void k_skel_from_grid(LevelGeom g, const double* grid, double* skel);
 __global__ void k_skel_to_grid(LevelGeom g, const double* skel, double* grid);
+// skeleton values onto their grid points only (element interiors untouched; used by the recovery);
+// hi_only: only the records of the three high box planes (v_d = k_d)
+cudaError_t launch_skel_scatter(const LevelGeom& g, const double* skel, double* grid, cudaStream_t st, bool hi_only);
 __global__ void k_weak_rhs(LevelGeom g, const double* b1, const double* b2, const double* b3, const double* f, double* F);
 cudaError_t launch_restrict(const LevelGeom& gf, const LevelGeom& gc, const double* Jint, const double* rf, double* Z,
                             double* fc, double* uzero, int nt_local, size_t smem, int gather_blocks, cudaStream_t st);

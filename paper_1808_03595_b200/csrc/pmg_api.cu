@@ -509,12 +509,16 @@ pmg_status condense_dev(pmg_ctx* c, const double* F, double* fhat) {
 
 pmg_status recover_dev(pmg_ctx* c, const double* uhat, const double* F, double* ufull) {
   const DevLevel& D = c->D[c->L];
-  const long long ng = (long long)(D.g.k1 * D.g.p + 1) * (D.g.k2 * D.g.p + 1) * (D.g.k3 * D.g.p + 1);
-  k_skel_to_grid<<<grid_for(ng), kThreads, 0, c->st>>>(D.g, uhat, ufull);
-  LAUNCH_CHECK(c);
   if (D.etabP) {
+    // 9 <= p <= 16: each element writes its grid block [0, p)^3 (interior and the skeleton points of its
+    // vertex record), the high box planes come from their records
     launch_cr16(1, D.g, F, uhat, D.etabP, c->lam, nullptr, ufull, c->st);
+    LAUNCH_CHECK(c);
+    launch_skel_scatter(D.g, uhat, ufull, c->st, true);
   } else {
+    // skeleton points from u_hat (non-free entries are zero), then every element interior
+    launch_skel_scatter(D.g, uhat, ufull, c->st, false);
+    LAUNCH_CHECK(c);
     size_t sm = recover_smem(D.g.p, D.g.ET, c->cube_in_smem);
     int nb = c->cube_in_smem ? (int)std::min<long long>(D.g.nelem, 148LL * 8) : c->cube_blocks;
     launch_recover_elem(nb, kThreads, sm, c->st, D.g, F, uhat, D.etab, c->lam, ufull, c->cube_in_smem ? nullptr : c->cube);
@@ -857,7 +861,7 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
       st.insert(st.end(), Hl.stab.begin() + (size_t)(V1 + V2 + sp.zb) * g.ST, Hl.stab.begin() + (size_t)(V1 + V2 + sp.z1 + 1) * g.ST);
     }
     if ((s = upload(&D.etab, et)) || (s = upload(&D.stab, st))) { free_ctx(c); return s; }
-    if (D.g.p >= 9 && D.g.p <= 16) {   // k_star16's padded table: NP x NP S, then Lambda (pad 1), s, w (pad 0)
+    if (D.g.p >= 5 && D.g.p <= 16) {   // k_star16's padded table: NP x NP S, then Lambda (pad 1), s, w (pad 0)
       const int n = D.g.n, NP = star16_np(D.g.p), STP = NP * NP + 3 * NP;
       const size_t rows = st.size() / D.g.ST;
       std::vector<double> sp(rows * STP, 0.0);
@@ -873,6 +877,8 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
         }
       }
       if ((s = upload(&D.stabP, sp))) { free_ctx(c); return s; }
+    }
+    if (D.g.p >= 9 && D.g.p <= 16) {
       const int ETP = elem16_etp(D.g.p);   // k_elem16's padded element table
       const size_t erows = et.size() / D.g.ET;
       std::vector<double> ep(erows * ETP, 0.0);

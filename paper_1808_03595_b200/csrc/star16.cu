@@ -57,10 +57,13 @@ __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %
 
 template <int P> struct Star16 {
   static constexpr int N = 2 * P - 1, NN = N * N, C = P - 1, M = P - 1, MM = M * M;
-  static constexpr int NP = (N + 7) / 8 * 8;          // 24 (p <= 12) or 32
+  static constexpr int NP = (N + 7) / 8 * 8;          // 16 (p <= 8), 24 (p <= 12) or 32
   static constexpr int LD = NP + 4;                    // = 4 or 12 mod 16: conflict-free fragment loads
   static constexpr int MS = NP * LD;
   static constexpr int NT = 128, NW = 4;
+  // core lane groups: GS lanes own a1 (16 for n_S <= 16, else the whole warp); NG groups per CTA
+  static constexpr int GS = NP <= 16 ? 16 : 32, NG = NW * (32 / GS);
+  static constexpr int MINB = NP <= 16 ? 5 : 3;       // CTAs per SM (registers / shared memory)
   static constexpr int STP = NP * NP + 3 * NP;         // padded star-table row
   static constexpr int RS = 3 * MM + 3 * M + 1;
   // shared memory (doubles): planes, S, X, vectors (Lambda, s, w per direction, NP each), 8 record
@@ -76,7 +79,9 @@ size_t star16_smem() { return sizeof(double) * Star16<P>::total; }
 template <int NP, int LD, bool TA, bool TB>
 __device__ __forceinline__ void gemm4(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ Cm,
                                       int warp, int lane) {
-  constexpr int T = NP / 8, BR = (T % 2 == 0) ? 2 : 1, BC = 2, JC = (T + BC - 1) / BC, NJ = (T / BR) * JC;
+  // tile blocks per job: 2 x 2 at n_S padded to 32 (4 jobs), 1 x 2 at 24 (6 jobs), 1 x 1 at 16 (4 jobs)
+  constexpr int T = NP / 8, BR = (T >= 4 && T % 2 == 0) ? 2 : 1, BC = T >= 3 ? 2 : 1, JC = (T + BC - 1) / BC,
+                NJ = (T / BR) * JC;
   const int r = lane >> 2, q = lane & 3;
   for (int job = warp; job < NJ; job += 4) {
     const int mi0 = (job / JC) * BR, ni0 = (job % JC) * BC;
@@ -117,7 +122,7 @@ __device__ __forceinline__ void gemm4(const double* __restrict__ A, const double
 }
 
 template <int P>
-__global__ void __launch_bounds__(128, 3)
+__global__ void __launch_bounds__(128, Star16<P>::MINB)
     k_star16(LevelGeom g, int c1, int c2, int c3, int n1c, int n2c, const double* __restrict__ r,
              double* __restrict__ u, const double* __restrict__ stabP, double lam) {
   using K = Star16<P>;
@@ -235,25 +240,26 @@ __global__ void __launch_bounds__(128, 3)
     gemm4<NP, LD, true, false>(Ssm + sA * MS, X, R + d * MS, warp, lane);
     __syncthreads();
   }
-  // ---- core: lanes own a1, each pass two a3 values (a, a + 4) of this warp
+  // ---- core: the GS lanes of a group own a1, each pass two a3 values (a, a + NG) of the group
   {
+    constexpr int GS = K::GS, NG = K::NG;
     const double *L1 = vec, *s1 = vec + NP, *L2 = vec + 3 * NP, *s2 = vec + 4 * NP, *L3 = vec + 6 * NP, *s3 = vec + 7 * NP;
     double* T1 = R;            // T1[a3][a2] -> G1[a3][a2]
     double* T2 = R + MS;       // T2[a3][a1] -> G2[a3][a1]
     const double* T3 = R + 2 * MS;   // T3[a2][a1]
-    const int a1 = lane;
+    const int a1 = lane & (GS - 1), grp = warp * (32 / GS) + lane / GS;
     const bool va = a1 < N;
     const int a1c = va ? a1 : 0;
     const double s1a = va ? s1[a1c] : 0.0, L1a = L1[a1c];
     double g3[N];
 #pragma unroll
     for (int a2 = 0; a2 < N; ++a2) g3[a2] = 0.0;
-    constexpr int PASSES = ((N + 3) / 4 + 1) / 2;
+    constexpr int PASSES = ((N + NG - 1) / NG + 1) / 2;
 #pragma unroll 1
     for (int it = 0; it < PASSES; ++it) {
-      const int a = warp + 8 * it, b = a + 4;
+      const int a = grp + 2 * NG * it, b = a + NG;
       const bool ta = a < N, tb = b < N;
-      const int ac = ta ? a : warp, bc = tb ? b : warp;   // invalid: a row this warp owns (no cross-warp race)
+      const int ac = ta ? a : grp, bc = tb ? b : grp;   // invalid: a row this group owns (no cross-group race)
       const double ona = (ta && va) ? 1.0 : 0.0, onb = (tb && va) ? 1.0 : 0.0;
       const double t2a = ona * T2[ac * LD + a1c], t2b = onb * T2[bc * LD + a1c];
       const double s3a = ona * s3[ac], s3b = onb * s3[bc];
@@ -286,10 +292,10 @@ __global__ void __launch_bounds__(128, 3)
             w[8 + j] = 0.0;
           }
         }
-        // reduce-scatter of the 16 values over the 32 lanes (sum over a1): lane l ends with the
-        // total of value l >> 1 (the lane pair l, l ^ 1 holds it twice)
+        // reduce-scatter of the 16 values over the GS lanes of the group (sum over a1): lane l of the
+        // group ends with the total of value l / (GS / 16) (GS = 32: the lane pair l, l ^ 1 holds it twice)
 #pragma unroll
-        for (int off = 16, half = 8; off >= 2; off >>= 1, half >>= 1) {
+        for (int off = GS / 2, half = 8; half >= 1; off >>= 1, half >>= 1) {
           const bool upper = (lane & off) != 0;
 #pragma unroll
           for (int j = 0; j < half; ++j) {
@@ -298,9 +304,10 @@ __global__ void __launch_bounds__(128, 3)
             w[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
           }
         }
-        const double tot = w[0] + __shfl_xor_sync(0xffffffffu, w[0], 1);
-        const int k = lane >> 1, a2 = 8 * ch + (k & 7);
-        if ((lane & 1) == 0 && a2 < N) {
+        double tot = w[0];
+        if constexpr (GS == 32) tot += __shfl_xor_sync(0xffffffffu, w[0], 1);
+        const int k = (GS == 32) ? (a1 >> 1) : a1, a2 = 8 * ch + (k & 7);
+        if ((GS == 16 || (lane & 1) == 0) && a2 < N) {
           if (k < 8) { if (ta) T1[a * LD + a2] = tot; }
           else if (tb) T1[b * LD + a2] = tot;
         }
@@ -310,10 +317,15 @@ __global__ void __launch_bounds__(128, 3)
         if (tb) T2[b * LD + a1] = g2b;
       }
     }
+    if constexpr (GS == 16) {   // the two groups of a warp share a1: add them first
+#pragma unroll
+      for (int a2 = 0; a2 < N; ++a2) g3[a2] += __shfl_xor_sync(0xffffffffu, g3[a2], 16);
+    }
     // G3 = sum over the four warps' partials, fixed order (w0 + w2) + (w1 + w3): T3's region and X
-    __syncthreads();   // every warp is done reading T3
+    __syncthreads();   // every group is done reading T3
     double* G3 = R + 2 * MS;
-    if (va) {
+    const bool wr = va && lane < GS;
+    if (wr) {
       if (warp == 0) {
 #pragma unroll
         for (int a2 = 0; a2 < N; ++a2) G3[a2 * LD + a1] = g3[a2];
@@ -323,7 +335,7 @@ __global__ void __launch_bounds__(128, 3)
       }
     }
     __syncthreads();
-    if (va) {
+    if (wr) {
       if (warp == 2) {
 #pragma unroll
         for (int a2 = 0; a2 < N; ++a2) G3[a2 * LD + a1] += g3[a2];
@@ -411,7 +423,7 @@ cudaError_t launch_star16(const LevelGeom& g, int c1, int c2, int c3, int n1c, i
   case PP:                                                                                                           \
     return launch_pdl(k_star16<PP>, dim3((unsigned)n1c, (unsigned)n2c, (unsigned)(nb / ((long long)n1c * n2c))),     \
                       dim3(Star16<PP>::NT), star16_smem<PP>(), st, g, c1, c2, c3, n1c, n2c, r, u, stabP, lam);
-    CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+    CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
 #undef CASE
     default: return cudaErrorInvalidValue;
   }
@@ -427,7 +439,7 @@ cudaError_t star16_set_smem_attr() {
                                          (int)star16_smem<PP>());                                  \
     if (a != cudaSuccess) e = a;                                                                   \
   }
-  CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+  CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
 #undef CASE
   return e;
 }
