@@ -63,6 +63,11 @@ typedef struct {
   int neumann;        /* homogeneous Neumann faces (bitmask: bit 2d / 2d+1 = low / high face of
                          direction d); every other face is homogeneous
                          Dirichlet.  Default 0 (all Dirichlet).  All six Neumann needs lambda > 0. */
+  int periodic;       /* periodic directions (bit d: direction d, "the ghost elements
+                         stay part of the domain"): k_d even and >= 2, no Neumann bit on d, one GPU (nranks = 1),
+                         vertex-star smoother, Jacobi-PCG coarse solver.  Grid vectors keep k_d p + 1 nodes along
+                         d; the last plane duplicates plane 0: its input values are ignored and the outputs
+                         (pmg_recover / pmg_solve / pmg_skel_to_grid) repeat plane 0 there.  Default 0. */
   int solver;         /* pmg_solve: 0 = multigrid fixpoint iteration (Alg. 4, "MG");
                          1 = Krylov-accelerated multigrid, inexact preconditioned CG with one V-cycle
                          from zero as preconditioner (Alg. 5; "kMG", with schedule 1 "kvMG") */

@@ -164,6 +164,9 @@ def lumped_mass_1d(mesh, d):
     b = np.zeros(mesh.N[d])
     for e in range(mesh.k[d]):
         b[e * p:(e + 1) * p + 1] += 0.5 * mesh.widths[d][e] * w
+    if mesh.is_periodic(d):   # node k_d p is node 0
+        b[0] += b[-1]
+        b[-1] = b[0]
     return b
 
 

@@ -5,6 +5,11 @@ H = sum_e Q_e H_e Q_e^T.  P:89-91: cuboidal elements with widths h_{i,e}.
 Homogeneous Dirichlet conditions on the whole box boundary (BASELINE configs).
 
 Global point (i1, i2, i3), 0 <= i_d <= k_d p, flat index g = i1 + N1 (i2 + N2 i3), x1 fastest.
+
+Periodic directions ("in the periodic case the ghost elements stay
+part of the domain, requiring no change in the operator"): the global index along d is taken
+modulo k_d p, so element k_d - 1 couples to the nodes of element 0; the grid keeps N_d = k_d p + 1
+nodes, and the last plane (i_d = k_d p) is a duplicate of plane 0 that carries no unknown.
 """
 import numpy as np
 
@@ -12,10 +17,18 @@ from .gll import gll
 
 
 class Mesh:
-    def __init__(self, k, widths, p, origin=(0.0, 0.0, 0.0), neumann=0):
+    def __init__(self, k, widths, p, origin=(0.0, 0.0, 0.0), neumann=0, periodic=0):
         """neumann: bit 2d / 2d+1 set = homogeneous Neumann on the low / high face of direction d
-        (SURVEY 8(f) NEXT-3); every other face is homogeneous Dirichlet."""
+        (SURVEY 8(f) NEXT-3); every other face is homogeneous Dirichlet.
+        periodic: bit d set = direction d is periodic (needs k_d >= 2, no Neumann bits on d)."""
         self.neumann = int(neumann)
+        self.periodic = int(periodic)
+        for d in range(3):
+            if self.periodic >> d & 1:
+                if self.neumann >> (2 * d) & 3:
+                    raise ValueError("a periodic direction has no Neumann faces")
+                if int(k[d]) < 2:
+                    raise ValueError("a periodic direction needs k_d >= 2")
         self.k = tuple(int(v) for v in k)
         self.p = int(p)
         if self.p < 1:
@@ -49,10 +62,42 @@ class Mesh:
         self.free_skel = self.free & self.skel    # condensed unknowns
         self._build_elements()
 
+    def is_periodic(self, d):
+        return bool(self.periodic >> d & 1)
+
+    def wrap(self, d, g):
+        """Global 1-D index along d as stored: modulo k_d p in a periodic direction."""
+        g = np.asarray(g)
+        return np.mod(g, self.k[d] * self.p) if self.is_periodic(d) else g
+
+    def xcoord(self, d, g):
+        """Coordinate of (possibly unwrapped) global 1-D index g: a periodic direction continues
+        with the period (the box length) beyond its ends."""
+        g = np.asarray(g)
+        if not self.is_periodic(d):
+            return self.coords[d][g]
+        n = self.k[d] * self.p
+        L = float(np.sum(self.widths[d]))
+        return self.coords[d][np.mod(g, n)] + L * np.floor_divide(g, n)
+
+    def fill_periodic(self, u):
+        """Copy plane 0 of every periodic direction into its duplicate last plane (grid output)."""
+        u = np.asarray(u, dtype=np.float64).reshape(self.N[2], self.N[1], self.N[0]).copy()
+        if self.is_periodic(0):
+            u[:, :, -1] = u[:, :, 0]
+        if self.is_periodic(1):
+            u[:, -1, :] = u[:, 0, :]
+        if self.is_periodic(2):
+            u[-1, :, :] = u[0, :, :]
+        return u.ravel()
+
     def free1d(self, d, g):
         """Global 1-D indices g along d that are unknowns: inside [0, N_d - 1] and not on a
-        Dirichlet end (a Neumann end point is an unknown)."""
+        Dirichlet end (a Neumann end point is an unknown); periodic: [0, N_d - 2] (the last index
+        duplicates index 0)."""
         g = np.asarray(g)
+        if self.is_periodic(d):
+            return (g >= 0) & (g < self.N[d] - 1)
         lo = bool(self.neumann >> (2 * d) & 1)
         hi = bool(self.neumann >> (2 * d + 1) & 1)
         return (g >= 0) & (g <= self.N[d] - 1) & ((g > 0) | lo) & ((g < self.N[d] - 1) | hi)
@@ -77,7 +122,8 @@ class Mesh:
         for e3 in range(self.k[2]):
             for e2 in range(self.k[1]):
                 for e1 in range(self.k[0]):
-                    elems.append(self.flat(e1 * p + t1, e2 * p + t2, e3 * p + t3))
+                    elems.append(self.flat(self.wrap(0, e1 * p + t1), self.wrap(1, e2 * p + t2),
+                                           self.wrap(2, e3 * p + t3)))
                     hs.append((self.widths[0][e1], self.widths[1][e2], self.widths[2][e3]))
         self.elem_idx = np.array(elems, dtype=np.int64)      # (n_e, (p+1)^3) global flat indices
         self.elem_h = np.array(hs, dtype=np.float64)          # (n_e, 3)

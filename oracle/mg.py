@@ -30,9 +30,12 @@ def level_degrees(p, p0=2):
 
 
 class Level:
-    def __init__(self, k, widths, p, lam, pw, neumann=0, smoother="star"):
-        """smoother: "star" (vertex stars, Alg. 2) or "element" (element-centred blocks, NEXT-4)."""
-        self.mesh = Mesh(k, widths, p, neumann=neumann)
+    def __init__(self, k, widths, p, lam, pw, neumann=0, smoother="star", periodic=0):
+        """smoother: "star" (vertex stars, Alg. 2) or "element" (element-centred blocks, NEXT-4).
+        periodic: bitmask of periodic directions (Mesh; NEXT-3)."""
+        self.mesh = Mesh(k, widths, p, neumann=neumann, periodic=periodic)
+        if periodic and smoother != "star":
+            raise ValueError("periodic directions: vertex-star smoother only")
         self.op = CondensedOperator(self.mesh, lam)
         if smoother not in ("star", "element"):
             raise ValueError("smoother must be 'star' or 'element'")
@@ -72,14 +75,14 @@ def pcg(level, b, rtol, maxit):
 
 class Hierarchy:
     def __init__(self, k, widths, p, lam, p0=2, pw=7, schedule=0, coarse_rtol=1e-4,
-                 coarse_maxit=10000, neumann=0, coarse_solver="auto", smoother="star"):
+                 coarse_maxit=10000, neumann=0, coarse_solver="auto", smoother="star", periodic=0):
         """neumann: face bitmask of homogeneous Neumann faces (Mesh; NEXT-3).
         coarse_solver: "jacobi" (Jacobi-PCG, reading R11), "hmg" (CG preconditioned by the
         h-multigrid V-cycle of oracle/hmg.py, reading R16) or "auto" (hmg iff more than 12288
         elements, some k_d halvable and lambda L_min^2 < 100 -- the rule the GPU library uses)."""
         self.degrees = level_degrees(p, p0)
         self.L = len(self.degrees) - 1
-        self.levels = [Level(k, widths, q, lam, pw, neumann, smoother if l > 0 else "star")
+        self.levels = [Level(k, widths, q, lam, pw, neumann, smoother if l > 0 else "star", periodic)
                        for l, q in enumerate(self.degrees)]
         self.transfers = [None] + [Transfer(self.levels[l - 1].mesh, self.levels[l].mesh)
                                    for l in range(1, self.L + 1)]
@@ -88,8 +91,10 @@ class Hierarchy:
         if coarse_solver == "auto":
             ne = int(np.prod(k))
             lmin = min(float(np.sum(w)) for w in widths)
-            coarse_solver = ("hmg" if (p0 == 2 and ne > 12288 and _hmg.coarsenable(k) and lam * lmin * lmin < 100.0)
-                             else "jacobi")
+            coarse_solver = ("hmg" if (p0 == 2 and ne > 12288 and _hmg.coarsenable(k) and lam * lmin * lmin < 100.0
+                                       and not periodic) else "jacobi")
+        if coarse_solver == "hmg" and periodic:
+            raise ValueError("the h-multigrid coarse solver does not support periodic directions")
         self.coarse_solver = coarse_solver
         self.hmg = _hmg.HMultigrid(k, widths, lam, neumann) if coarse_solver == "hmg" else None
         self.coarse_rtol = coarse_rtol
@@ -159,7 +164,7 @@ class Hierarchy:
             hist.append(rn)
             cycles += 1
         rho = (rn / r0) ** (1.0 / cycles) if cycles and r0 > 0 else 0.0
-        u_full = op.recover(u, F)
+        u_full = top.mesh.fill_periodic(op.recover(u, F))
         rep = dict(cycles=cycles, r0=r0, r_final=rn, rho=rho, history=hist,
                    converged=bool(rn <= rtol * r0), u_hat=u, f_hat=fhat)
         return u_full, rep
@@ -197,7 +202,7 @@ class Hierarchy:
             hist.append(rn)
             its += 1
         rho = (rn / r0) ** (1.0 / its) if its and r0 > 0 else 0.0
-        u_full = op.recover(u, F)
+        u_full = top.mesh.fill_periodic(op.recover(u, F))
         rep = dict(cycles=its, r0=r0, r_final=rn, rho=rho, history=hist,
                    converged=bool(rn <= rtol * r0), u_hat=u, f_hat=fhat)
         return u_full, rep

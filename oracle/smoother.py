@@ -41,7 +41,7 @@ def star_points(mesh, v):
     j3, j2, j1 = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
     j1, j2, j3 = j1.ravel(), j2.ravel(), j3.ravel()
     on_plane = (j1 == c) | (j2 == c) | (j3 == c)
-    G1, G2, G3 = g[0][j1], g[1][j2], g[2][j3]
+    G1, G2, G3 = mesh.wrap(0, g[0][j1]), mesh.wrap(1, g[1][j2]), mesh.wrap(2, g[2][j3])   # periodic: wrapped
     valid = mesh.free1d(0, G1) & mesh.free1d(1, G2) & mesh.free1d(2, G3)
     keep = on_plane & valid
     return mesh.flat(G1[keep], G2[keep], G3[keep]), (j1[keep], j2[keep], j3[keep])
@@ -57,19 +57,21 @@ def star_weights(mesh, v, loc, pw=7):
         g = star_index_range(mesh, v, d)[loc[d]]
         xv = mesh.coords[d][v[d] * p]
         e = np.where(g < v[d] * p, v[d] - 1, v[d])
-        e = np.clip(e, 0, mesh.k[d] - 1)
+        e = np.mod(e, mesh.k[d]) if mesh.is_periodic(d) else np.clip(e, 0, mesh.k[d] - 1)
         h = mesh.widths[d][e]
-        t = np.abs(mesh.coords[d][g] - xv) / h
+        t = np.abs(mesh.xcoord(d, g) - xv) / h
         W *= weight_poly(t, pw)
     return W
 
 
 def vertices(mesh):
-    """All mesh vertices ("the n_V vertices"), reading c-6: boundary vertices included."""
+    """All mesh vertices ("the n_V vertices"), reading c-6: boundary vertices included; in a
+    periodic direction vertex k_d is vertex 0."""
+    n = [mesh.k[d] + (0 if mesh.is_periodic(d) else 1) for d in range(3)]
     out = []
-    for v3 in range(mesh.k[2] + 1):
-        for v2 in range(mesh.k[1] + 1):
-            for v1 in range(mesh.k[0] + 1):
+    for v3 in range(n[2]):
+        for v2 in range(n[1]):
+            for v1 in range(n[0]):
                 out.append((v1, v2, v3))
     return out
 
@@ -77,9 +79,10 @@ def vertices(mesh):
 def block_elements(mesh, v):
     """Elements of the 2x2x2 block around vertex v that exist in the mesh."""
     out = []
-    for e3 in (v[2] - 1, v[2]):
-        for e2 in (v[1] - 1, v[1]):
-            for e1 in (v[0] - 1, v[0]):
+    w = lambda d, e: e % mesh.k[d] if mesh.is_periodic(d) else e
+    for e3 in (w(2, v[2] - 1), w(2, v[2])):
+        for e2 in (w(1, v[1] - 1), w(1, v[1])):
+            for e1 in (w(0, v[0] - 1), w(0, v[0])):
                 if 0 <= e1 < mesh.k[0] and 0 <= e2 < mesh.k[1] and 0 <= e3 < mesh.k[2]:
                     out.append(e1 + mesh.k[0] * (e2 + mesh.k[1] * e3))
     return out
@@ -116,6 +119,8 @@ def star_1d(mesh, v, d):
     M = np.zeros((n, n))
     K = np.zeros((n, n))
     for side, e in ((0, v[d] - 1), (1, v[d])):
+        if mesh.is_periodic(d):
+            e = e % mesh.k[d]
         if not (0 <= e < mesh.k[d]):
             continue
         Me, Ke = element_matrices_1d(p, mesh.widths[d][e])
@@ -129,7 +134,7 @@ def star_1d(mesh, v, d):
                 if 0 <= i < n:
                     K[j, i] += Ke[t, s]
             M[j, j] += Me[t, t]
-    g = star_index_range(mesh, v, d)
+    g = mesh.wrap(d, star_index_range(mesh, v, d))
     valid = mesh.free1d(d, g)
     return M, K, valid
 
@@ -195,7 +200,7 @@ def tpc_star_inverse(condop, v, r):
     (S1, L1), va1 = fd[0]
     (S2, L2), va2 = fd[1]
     (S3, L3), va3 = fd[2]
-    g = [star_index_range(mesh, v, d) for d in range(3)]
+    g = [mesh.wrap(d, star_index_range(mesh, v, d)) for d in range(3)]
     R = np.asarray(r)
 
     def val(i1, i2, i3, ok):
@@ -262,6 +267,9 @@ class StarSmoother:
         for v in vertices(mesh):
             key = []
             for d in range(3):
+                if mesh.is_periodic(d):
+                    key.append((mesh.widths[d][(v[d] - 1) % mesh.k[d]], mesh.widths[d][v[d]], "per"))
+                    continue
                 hl = mesh.widths[d][v[d] - 1] if v[d] >= 1 else None
                 hr = mesh.widths[d][v[d]] if v[d] < mesh.k[d] else None
                 key.append((hl, hr))

@@ -32,7 +32,8 @@ class PmgError(RuntimeError):
 
 class Options(ctypes.Structure):
     _fields_ = [("p0", ctypes.c_int), ("weight_degree", ctypes.c_int), ("schedule", ctypes.c_int),
-                ("neumann", ctypes.c_int), ("solver", ctypes.c_int), ("smoother", ctypes.c_int),
+                ("neumann", ctypes.c_int), ("periodic", ctypes.c_int), ("solver", ctypes.c_int),
+                ("smoother", ctypes.c_int),
                 ("coarse_rtol", ctypes.c_double), ("coarse_maxit", ctypes.c_int),
                 ("coarse_check", ctypes.c_int), ("coarse_solver", ctypes.c_int),
                 ("rank", ctypes.c_int), ("nranks", ctypes.c_int),
@@ -157,9 +158,10 @@ class Solver:
 
     def __init__(self, k, widths, p, lam, p0=2, schedule=0, coarse_rtol=1e-4, coarse_maxit=10000,
                  coarse_check=8, stream=None, rank=0, nranks=1, nccl_id=None, loopback=None, solver=0,
-                 neumann=0, coarse_solver=0, smoother=0):
+                 neumann=0, coarse_solver=0, smoother=0, periodic=0):
         """solver 0: MG fixpoint iteration (Alg. 4); 1: Krylov-accelerated MG (ipCG, Alg. 5).
         neumann: face bitmask of homogeneous Neumann faces (bit 2d / 2d+1: low / high face of d).
+        periodic: bitmask of periodic directions (bit d), k_d even.
         smoother 0: vertex stars (Alg. 2); 1: element-centred 3x3x3 blocks (NEXT-4)."""
         import numpy as np
         import torch
@@ -168,6 +170,7 @@ class Solver:
         o.rank, o.nranks = int(rank), int(nranks)
         o.solver = int(solver)
         o.neumann = int(neumann)
+        o.periodic = int(periodic)
         o.coarse_solver = int(coarse_solver)
         o.smoother = int(smoother)
         self._nccl_buf = None

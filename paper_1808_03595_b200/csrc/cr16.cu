@@ -161,10 +161,12 @@ __global__ void __launch_bounds__(256, 2)
   }
   if (MODE == 1) {   // face interiors of u_hat -> Fa[f][A][B] (A slow, B fast tangential index)
     const long long V12 = (long long)g.V1 * g.V2;
-    const long long rec0 = e1 + g.V1 * (long long)e2 + V12 * e3;
     for (int i = tid; i < 6 * MM; i += NT) {
       const int f = i / MM, l = i - f * MM, A = l / M, B = l - A * M, d = f >> 1, s = f & 1;
-      const long long rb = (rec0 + (d == 0 ? s : 0) + g.V1 * (long long)(d == 1 ? s : 0) + V12 * (d == 2 ? s : 0)) * RS;
+      // the face's record e + s e_d (periodic: the last element's high face is on record plane 0)
+      const int w1 = wrap_rec(e1 + (d == 0 ? s : 0), g.k1, g.per & 1), w2 = wrap_rec(e2 + (d == 1 ? s : 0), g.k2, g.per & 2),
+                w3 = wrap_rec(e3 + (d == 2 ? s : 0), g.k3, g.per & 4);
+      const long long rb = (w1 + g.V1 * (long long)w2 + V12 * w3) * RS;
       cpa8c(&Fa[f * MS + A * LD + B], uh + rb + d * MM + l);
     }
     // padding rows / columns of the face arrays (read by the face transforms against zero P entries)

@@ -143,7 +143,12 @@ __global__ void __launch_bounds__(128, 3)
   {
     const long long V12 = (long long)g.V1 * g.V2;
     const long long rec0 = e1 + g.V1 * (long long)e2 + V12 * e3;
-    auto recb = [&](int o1, int o2, int o3) { return (rec0 + o1 + g.V1 * (long long)o2 + V12 * o3) * RS; };
+    auto recb = [&](int o1, int o2, int o3) {   // record e + o (periodic: the last element wraps to 0)
+      if (!g.per) return (rec0 + o1 + g.V1 * (long long)o2 + V12 * o3) * RS;
+      const int w1 = wrap_rec(e1 + o1, g.k1, g.per & 1), w2 = wrap_rec(e2 + o2, g.k2, g.per & 2),
+                w3 = wrap_rec(e3 + o3, g.k3, g.per & 4);
+      return (w1 + g.V1 * (long long)w2 + V12 * w3) * RS;
+    };
 #pragma unroll
     for (int k = 0; k < (MM + NT - 1) / NT; ++k) {   // face interiors: thread = block position l
       const int l = tid + k * NT;

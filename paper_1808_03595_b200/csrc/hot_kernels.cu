@@ -111,7 +111,9 @@ __global__ void __launch_bounds__(ElemCfg<P>::NT) k_elem_apply_t(LevelGeom g, co
     if (d == 0) { t1 = s * P; t3 = A; t2 = B; }
     else if (d == 1) { t2 = s * P; t3 = A; t1 = B; }
     else { t3 = s * P; t2 = A; t1 = B; }
-    Uc[i] = __ldg(&u[skel_index_t<P>(g,e1 * P + t1, e2 * P + t2, e3 * P + t3)]);
+    int G1 = e1 * P + t1, G2 = e2 * P + t2, G3 = e3 * P + t3;
+    wrap_pt(g, G1, G2, G3);   // periodic: the last element's high faces are plane 0
+    Uc[i] = __ldg(&u[skel_index_t<P>(g, G1, G2, G3)]);
   }
   __syncthreads();
   // tangential directions of face f: a (fast) = x2 for d = 0 else x1; b (slow) = x3 for d < 2 else x2
@@ -455,7 +457,8 @@ __global__ void __launch_bounds__(StarPfCfg<P>::NT, StarPfCfg<P>::MINB)
   const long long V12 = (long long)g.V1 * g.V2;
   const long long rec0 = v1 + g.V1 * (long long)v2 + V12 * v3;
   // interior stars (the common case) touch only inside, free points: no per-point tests
-  const bool interior = v1 > 0 && v2 > 0 && v3 > 0 && v1 < g.k1 && v2 < g.k2 && v3 + g.zoff < g.K3;
+  const bool interior = ((v1 > 0 && v1 < g.k1) || (g.per & 1)) && ((v2 > 0 && v2 < g.k2) || (g.per & 2)) &&
+                        ((v3 > 0 && v3 + g.zoff < g.K3) || (g.per & 4));
   unsigned* map_s = reinterpret_cast<unsigned*>(sm + C::oMap);
   for (int i = tid; i < 3 * NN; i += NT) map_s[i] = __ldg(&kStarMap<P>.v[i]);
   // point of map entry e: record coordinate w_d = v_d - bit; free iff (w_d > 0 or t_d > 0) and
@@ -465,17 +468,18 @@ __global__ void __launch_bounds__(StarPfCfg<P>::NT, StarPfCfg<P>::MINB)
     const int W3 = w3 + g.zoff;
     // the point is G_d = w_d p + t_d (0 <= t_d < p), t_d == 0 iff bit 15 + d
     const bool z1 = e & (1u << 15), z2 = e & (1u << 16), z3 = e & (1u << 17);
-    return w1 >= 0 && w2 >= 0 && w3 >= 0 &&
-           (w1 > 0 || !z1 || (g.neu & 1)) && (w1 < g.k1 || (z1 && w1 == g.k1 && (g.neu & 2))) &&
-           (w2 > 0 || !z2 || (g.neu & 4)) && (w2 < g.k2 || (z2 && w2 == g.k2 && (g.neu & 8))) &&
-           (W3 > 0 || !z3 || (g.neu & 16)) && (W3 < g.K3 || (z3 && W3 == g.K3 && (g.neu & 32)));
+    return ((g.per & 1) || (w1 >= 0 && (w1 > 0 || !z1 || (g.neu & 1)) && (w1 < g.k1 || (z1 && w1 == g.k1 && (g.neu & 2))))) &&
+           ((g.per & 2) || (w2 >= 0 && (w2 > 0 || !z2 || (g.neu & 4)) && (w2 < g.k2 || (z2 && w2 == g.k2 && (g.neu & 8))))) &&
+           ((g.per & 4) || (w3 >= 0 && (W3 > 0 || !z3 || (g.neu & 16)) && (W3 < g.K3 || (z3 && W3 == g.K3 && (g.neu & 32)))));
   };
   // record base index of each of the 8 record-offset codes (-1: record outside the stored box)
   long long* s_base = reinterpret_cast<long long*>(sm + C::oBase);
   if (tid < 8) {
     const int b1 = tid & 1, b2 = (tid >> 1) & 1, b3 = (tid >> 2) & 1;
-    const bool ok = !((v1 == 0 && b1) || (v2 == 0 && b2) || (v3 == 0 && b3));
-    s_base[tid] = ok ? (rec0 - (b1 + g.V1 * (long long)b2 + V12 * b3)) * RS : -1LL;
+    const bool ok = !((v1 == 0 && b1 && !(g.per & 1)) || (v2 == 0 && b2 && !(g.per & 2)) || (v3 == 0 && b3 && !(g.per & 4)));
+    const int w1 = wrap_rec(v1 - b1, g.k1, g.per & 1), w2 = wrap_rec(v2 - b2, g.k2, g.per & 2),
+              w3 = wrap_rec(v3 - b3, g.k3, g.per & 4);   // periodic: record k-1 for v = 0
+    s_base[tid] = ok ? (w1 + g.V1 * (long long)w2 + V12 * w3) * RS : -1LL;
   }
   const size_t srow[3] = {row[0] * ST, row[1] * ST, row[2] * ST};
   __syncthreads();
@@ -705,12 +709,16 @@ __global__ void __launch_bounds__(ElemPfCfg<P>::NT, ElemPfCfg<P>::MINB)
     if (done && *done) return;   // (uniform per block; the issued cp.async only target this block's smem)
     constexpr int RS = 3 * MM + 3 * M + 1;
     const long long V12 = (long long)g.V1 * g.V2;
-    const long long rec0 = e1 + g.V1 * (long long)e2 + V12 * e3;
+    auto rb = [&](unsigned code) {   // record of the map code's +1 offsets (periodic: wrapped)
+      const int w1 = wrap_rec(e1 + (int)(code & 1u), g.k1, g.per & 1), w2 = wrap_rec(e2 + (int)((code >> 1) & 1u), g.k2, g.per & 2),
+                w3 = wrap_rec(e3 + (int)((code >> 2) & 1u), g.k3, g.per & 4);
+      return (w1 + g.V1 * (long long)w2 + V12 * w3) * RS;
+    };
     for (int o = tid; o < YS; o += NT) {
       int t1, t2, t3;
       ys_point<P>(o, t1, t2, t3);
       const unsigned m_ = map_s[o];
-      cp_async8(&cube[(t3 * Q + t2) * Q + t1], &u[(rec0 + rec_delta(m_, g.V1, V12)) * RS + (m_ & 0xFFFu)], true);
+      cp_async8(&cube[(t3 * Q + t2) * Q + t1], &u[rb((m_ >> 12) & 7u) + (m_ & 0xFFFu)], true);
     }
     cp_async_commit();
     for (int i = tid; i < M * MM; i += NT) {        // zero interior of the cube
@@ -921,7 +929,8 @@ __global__ void __launch_bounds__(256, 1) k_star_tm(LevelGeom g, int c1, int c2,
     const int d = i / NN, rr = i - d * NN, A = rr / N, B = rr - A * N;
     int j1, j2, j3;
     if (d == 0) { j1 = c; j2 = B; j3 = A; } else if (d == 1) { j2 = c; j1 = B; j3 = A; } else { j3 = c; j1 = B; j2 = A; }
-    const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
+    int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
+    wrap_pt(g, g1, g2, g3);
     const double val = inside(g, g1, g2, g3) ? __ldg(&r[skel_index_t<P>(g, g1, g2, g3)]) : 0.0;
     FT[d * MS + A * LD + B] = val * (1.0 / (double)(1 + (A == c) + (B == c)));   // inverse multiplicity
   }
@@ -1011,7 +1020,8 @@ __global__ void __launch_bounds__(256, 1) k_star_tm(LevelGeom g, int c1, int c2,
     if (d == 0) { j1 = c; j2 = B; j3 = A; }
     else if (d == 1) { j2 = c; j1 = B; j3 = A; if (j1 == c) continue; }
     else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
-    const int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
+    int g1 = o1 + j1, g2 = o2 + j2, g3 = o3 + j3;
+    wrap_pt(g, g1, g2, g3);
     if (!is_free(g, g1, g2, g3)) continue;
     u[skel_index_t<P>(g, g1, g2, g3)] += w1[j1] * w2[j2] * w3[j3] * Gs[d * MS + A * LD + B];
   }
@@ -1064,22 +1074,24 @@ __global__ void __launch_bounds__(128) k_star_w(LevelGeom g, int c1, int c2, int
   constexpr int RS = 3 * (P - 1) * (P - 1) + 3 * (P - 1) + 1;
   const long long V12 = (long long)g.V1 * g.V2;
   const long long rec0 = v1 + g.V1 * (long long)v2 + V12 * v3;
-  const bool interior = v1 > 0 && v2 > 0 && v3 > 0 && v1 < g.k1 && v2 < g.k2 && v3 + g.zoff < g.K3;
+  const bool interior = ((v1 > 0 && v1 < g.k1) || (g.per & 1)) && ((v2 > 0 && v2 < g.k2) || (g.per & 2)) &&
+                        ((v3 > 0 && v3 + g.zoff < g.K3) || (g.per & 4));
   auto pt_free = [&](unsigned e) {   // global test (w3 + zoff is the global record plane), Neumann faces free
     const int w1 = v1 - (int)((e >> 12) & 1u), w2 = v2 - (int)((e >> 13) & 1u), w3 = v3 - (int)((e >> 14) & 1u);
     const int W3 = w3 + g.zoff;
     // the point is G_d = w_d p + t_d (0 <= t_d < p), t_d == 0 iff bit 15 + d
     const bool z1 = e & (1u << 15), z2 = e & (1u << 16), z3 = e & (1u << 17);
-    return w1 >= 0 && w2 >= 0 && w3 >= 0 &&
-           (w1 > 0 || !z1 || (g.neu & 1)) && (w1 < g.k1 || (z1 && w1 == g.k1 && (g.neu & 2))) &&
-           (w2 > 0 || !z2 || (g.neu & 4)) && (w2 < g.k2 || (z2 && w2 == g.k2 && (g.neu & 8))) &&
-           (W3 > 0 || !z3 || (g.neu & 16)) && (W3 < g.K3 || (z3 && W3 == g.K3 && (g.neu & 32)));
+    return ((g.per & 1) || (w1 >= 0 && (w1 > 0 || !z1 || (g.neu & 1)) && (w1 < g.k1 || (z1 && w1 == g.k1 && (g.neu & 2))))) &&
+           ((g.per & 2) || (w2 >= 0 && (w2 > 0 || !z2 || (g.neu & 4)) && (w2 < g.k2 || (z2 && w2 == g.k2 && (g.neu & 8))))) &&
+           ((g.per & 4) || (w3 >= 0 && (W3 > 0 || !z3 || (g.neu & 16)) && (W3 < g.K3 || (z3 && W3 == g.K3 && (g.neu & 32)))));
   };
   long long* s_base = reinterpret_cast<long long*>(sm + C::oBase);
   if (lane < 8) {
     const int b1 = lane & 1, b2 = (lane >> 1) & 1, b3 = (lane >> 2) & 1;
-    const bool ok = !((v1 == 0 && b1) || (v2 == 0 && b2) || (v3 == 0 && b3));
-    s_base[lane] = ok ? (rec0 - (b1 + g.V1 * (long long)b2 + V12 * b3)) * RS : -1LL;
+    const bool ok = !((v1 == 0 && b1 && !(g.per & 1)) || (v2 == 0 && b2 && !(g.per & 2)) || (v3 == 0 && b3 && !(g.per & 4)));
+    const int w1 = wrap_rec(v1 - b1, g.k1, g.per & 1), w2 = wrap_rec(v2 - b2, g.k2, g.per & 2),
+              w3 = wrap_rec(v3 - b3, g.k3, g.per & 4);   // periodic: record k-1 for v = 0
+    s_base[lane] = ok ? (w1 + g.V1 * (long long)w2 + V12 * w3) * RS : -1LL;
   }
   const size_t srow[3] = {(size_t)v1 * ST, (size_t)(g.V1 + v2) * ST, (size_t)(g.V1 + g.V2 + v3) * ST};
   for (int i = lane; i < 3 * NN; i += 32) {
@@ -1229,6 +1241,9 @@ __global__ void __launch_bounds__(256) k_gather_resid_t(LevelGeom g, const doubl
     return ((size_t)a1 + (size_t)g.k1 * ((size_t)a2 + (size_t)g.k2 * a3)) * YS;
   };
   auto yat = [&](int a1, int a2, int a3, int off) -> double {   // 0 outside the box (Neumann faces)
+    a1 = wrap_rec(a1, g.k1, g.per & 1);   // periodic: element k - 1 precedes element 0
+    a2 = wrap_rec(a2, g.k2, g.per & 2);
+    a3 = wrap_rec(a3, g.k3, g.per & 4);
     return (a1 >= 0 && a2 >= 0 && a3 >= 0 && a1 < g.k1 && a2 < g.k2 && a3 < g.k3) ? Y[el(a1, a2, a3) + off] : 0.0;
   };
   for (int o = threadIdx.x; o < RS; o += blockDim.x) {

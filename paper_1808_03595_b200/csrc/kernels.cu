@@ -50,7 +50,9 @@ __global__ void k_skel_to_grid(LevelGeom g, const double* __restrict__ skel, dou
     int i2 = (int)(r % N2), i3 = (int)(r / N2);
     bool sk = (i1 % g.p == 0) || (i2 % g.p == 0) || (i3 % g.p == 0);
     double v = 0.0;
-    if (sk && is_free(g, i1, i2, i3)) v = skel[skel_index(g, i1, i2, i3)];
+    int w1 = i1, w2 = i2, w3 = i3;
+    wrap_pt(g, w1, w2, w3);   // periodic: the duplicate last plane shows plane 0
+    if (sk && is_free(g, w1, w2, w3)) v = skel[skel_index(g, w1, w2, w3)];
     grid[idx] = v;
   }
 }
@@ -66,7 +68,9 @@ __global__ void __launch_bounds__(128) k_skel_scatter_t(LevelGeom g, const doubl
   constexpr int m = P - 1, mm = m * m, RS = 3 * mm + 3 * m + 1;
   const int v1 = blockIdx.x + o1, v2 = blockIdx.y + o2, v3 = blockIdx.z + o3;   // record (offset grid)
   const long long N1 = (long long)g.k1 * P + 1, N2 = (long long)g.k2 * P + 1;
-  const double* R = skel + (v1 + (long long)g.V1 * (v2 + (long long)g.V2 * v3)) * RS;
+  const int r1 = ((g.per & 1) && v1 == g.k1) ? 0 : v1, r2 = ((g.per & 2) && v2 == g.k2) ? 0 : v2,
+            r3 = ((g.per & 4) && v3 == g.k3) ? 0 : v3;   // periodic: the duplicate plane shows plane 0
+  const double* R = skel + (r1 + (long long)g.V1 * (r2 + (long long)g.V2 * r3)) * RS;
   const long long g0 = (long long)v1 * P + N1 * ((long long)v2 * P + N2 * (long long)v3 * P);
   const bool in1 = v1 < g.k1, in2 = v2 < g.k2, in3 = v3 < g.k3;
   for (int l = threadIdx.x; l < mm; l += blockDim.x) {
@@ -192,13 +196,19 @@ __global__ void k_restrict_gather_t(LevelGeom gc, const double* __restrict__ Z, 
     if (is_free(gc, E.g1, E.g2, E.g3) && owned_plane(gc, E.v3)) {
       const int G[3] = {E.g1, E.g2, E.g3};
       const int K[3] = {gc.k1, gc.k2, gc.k3};
-      int cand[3][2], nc[3];
+      int cand[3][2], loc[3][2], nc[3];   // candidate records along d and the point's local coordinate there
       bool mult[3];
       for (int d = 0; d < 3; ++d) {
         mult[d] = (G[d] % pc) == 0;
         cand[d][0] = G[d] / pc;
+        loc[d][0] = G[d] - cand[d][0] * pc;
         nc[d] = 1;
-        if (mult[d] && cand[d][0] - 1 >= 0) { cand[d][1] = cand[d][0] - 1; nc[d] = 2; }
+        const bool per = (gc.per >> d) & 1;
+        if (mult[d] && (cand[d][0] - 1 >= 0 || per)) {   // periodic: plane 0 closes the last record
+          cand[d][1] = cand[d][0] - 1 >= 0 ? cand[d][0] - 1 : K[d] - 1;
+          loc[d][1] = pc;
+          nc[d] = 2;
+        }
         if (cand[d][0] > K[d]) nc[d] = 0;  // cannot happen for points inside the box
       }
       auto rec = [&](int w1, int w2, int w3) -> long long {
@@ -212,7 +222,7 @@ __global__ void k_restrict_gather_t(LevelGeom gc, const double* __restrict__ Z, 
           for (int ia = 0; ia < nc[da]; ++ia) {
             int w[3];
             w[d] = G[d] / pc; w[da] = cand[da][ia]; w[db] = cand[db][ib];
-            int be = G[db] - w[db] * pc, al = G[da] - w[da] * pc;
+            const int be = loc[db][ib], al = loc[da][ia];
             s += Z[rec(w[0], w[1], w[2]) + d * qc * qc + be * qc + al];
           }
       }
@@ -223,7 +233,7 @@ __global__ void k_restrict_gather_t(LevelGeom gc, const double* __restrict__ Z, 
         for (int i = 0; i < nc[d]; ++i) {
           int w[3];
           w[d] = cand[d][i]; w[da] = G[da] / pc; w[db] = G[db] / pc;
-          s += Z[rec(w[0], w[1], w[2]) + 3 * qc * qc + d * qc + (G[d] - w[d] * pc)];
+          s += Z[rec(w[0], w[1], w[2]) + 3 * qc * qc + d * qc + loc[d][i]];
         }
       }
       if (mult[0] && mult[1] && mult[2]) s += Z[rec(G[0] / pc, G[1] / pc, G[2] / pc) + ZS - 1];
@@ -251,6 +261,7 @@ __global__ void k_prolong_t(LevelGeom gf, LevelGeom gc, const double* __restrict
     int d = i / (qc * qc), rr = i - d * qc * qc, be = rr / qc, al = rr - be * qc;
     int G1 = v1 * pc, G2 = v2 * pc, G3 = v3 * pc;
     if (d == 0) { G3 += be; G2 += al; } else if (d == 1) { G3 += be; G1 += al; } else { G2 += be; G1 += al; }
+    wrap_pt(gc, G1, G2, G3);   // periodic: the closed face of the last record ends on plane 0
     C[i] = inside(gc, G1, G2, G3) ? uc[skel_index(gc, G1, G2, G3)] : 0.0;
   }
   for (int i = tid; i < 3 * qc + 1; i += nt) {
@@ -259,6 +270,7 @@ __global__ void k_prolong_t(LevelGeom gf, LevelGeom gc, const double* __restrict
       int d = i / qc, al = i - d * qc;
       if (d == 0) G1 += al; else if (d == 1) G2 += al; else G3 += al;
     }
+    wrap_pt(gc, G1, G2, G3);
     C[3 * qc * qc + i] = inside(gc, G1, G2, G3) ? uc[skel_index(gc, G1, G2, G3)] : 0.0;
   }
   __syncthreads();
@@ -429,6 +441,9 @@ __global__ void k_condense_gather(LevelGeom g, const double* __restrict__ Fg, co
         const int d = E.type, o = E.a * m + E.b;
         int w1 = E.v1, w2 = E.v2, w3 = E.v3;
         if (d == 0) w1 -= 1; else if (d == 1) w2 -= 1; else w3 -= 1;
+        w1 = wrap_rec(w1, g.k1, g.per & 1);   // periodic: element k - 1 precedes element 0
+        w2 = wrap_rec(w2, g.k2, g.per & 2);
+        w3 = wrap_rec(w3, g.k3, g.per & 4);
         const bool lo_in = w1 >= 0 && w2 >= 0 && w3 >= 0;                               // Neumann face: one side
         const bool hi_in = E.v1 < g.k1 && E.v2 < g.k2 && E.v3 < g.k3;
         size_t elo = lo_in ? (size_t)w1 + (size_t)g.k1 * ((size_t)w2 + (size_t)g.k2 * w3) : 0;
@@ -468,7 +483,9 @@ __global__ void __launch_bounds__(256) k_recover_elem(LevelGeom g, const double*
       int f = i / mm, r = i - f * mm, A = r / m, B = r - A * m, d = f >> 1, s = f & 1, t1, t2, t3;
       if (d == 0) { t1 = s * p; t3 = A + 1; t2 = B + 1; } else if (d == 1) { t2 = s * p; t3 = A + 1; t1 = B + 1; }
       else { t3 = s * p; t2 = A + 1; t1 = B + 1; }
-      Uf[i] = uh[skel_index(g, e1 * p + t1, e2 * p + t2, e3 * p + t3)];
+      int G1 = e1 * p + t1, G2 = e2 * p + t2, G3 = e3 * p + t3;
+      wrap_pt(g, G1, G2, G3);
+      Uf[i] = uh[skel_index(g, G1, G2, G3)];
     }
     __syncthreads();
     for (int f = 0; f < 6; ++f) {

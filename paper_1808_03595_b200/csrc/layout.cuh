@@ -50,18 +50,41 @@ __device__ __forceinline__ long long skel_index_t(const LevelGeom& g, int g1, in
   return rec * (3 * m * m + 3 * m + 1) + off;
 }
 
+// periodic directions: a global point index beyond either end (star / element neighbour accesses)
+// wrapped into [0, k_d p) (one GPU: z-periodic meshes are not split into slabs)
+__device__ __forceinline__ void wrap_pt(const LevelGeom& g, int& g1, int& g2, int& g3) {
+  if (g.per & 1) { const int n = g.k1 * g.p; g1 = g1 < 0 ? g1 + n : (g1 >= n ? g1 - n : g1); }
+  if (g.per & 2) { const int n = g.k2 * g.p; g2 = g2 < 0 ? g2 + n : (g2 >= n ? g2 - n : g2); }
+  if (g.per & 4) { const int n = g.k3 * g.p; g3 = g3 < 0 ? g3 + n : (g3 >= n ? g3 - n : g3); }
+}
+
 __device__ __forceinline__ bool inside(const LevelGeom& g, int g1, int g2, int g3) {
   return g1 >= 0 && g2 >= 0 && g3 >= 0 && g1 <= g.k1 * g.p && g2 <= g.k2 * g.p && g3 <= g.k3 * g.p;
 }
 // free unknown: strictly inside the GLOBAL box (g3 is local; the slab starts at vertex plane zoff)
-// Neumann faces (g.neu) keep their points as unknowns
+// Neumann faces (g.neu) keep their points as unknowns; in a periodic direction the last plane
+// (index k_d p) duplicates plane 0 and is not an unknown (callers wrap neighbour points first)
 __device__ __forceinline__ bool is_free(const LevelGeom& g, int g1, int g2, int g3) {
   const int G3 = g3 + g.zoff * g.p;
+  if (g.per) {
+    if ((g.per & 1) ? !(g1 >= 0 && g1 < g.k1 * g.p) : !free_1d(g1, g.k1 * g.p, g.neu & 1, (g.neu >> 1) & 1)) return false;
+    if ((g.per & 2) ? !(g2 >= 0 && g2 < g.k2 * g.p) : !free_1d(g2, g.k2 * g.p, (g.neu >> 2) & 1, (g.neu >> 3) & 1)) return false;
+    return (g.per & 4) ? (G3 >= 0 && G3 < g.K3 * g.p) : free_1d(G3, g.K3 * g.p, (g.neu >> 4) & 1, (g.neu >> 5) & 1);
+  }
   return free_1d(g1, g.k1 * g.p, g.neu & 1, (g.neu >> 1) & 1) && free_1d(g2, g.k2 * g.p, (g.neu >> 2) & 1, (g.neu >> 3) & 1) &&
          free_1d(G3, g.K3 * g.p, (g.neu >> 4) & 1, (g.neu >> 5) & 1);
 }
-// a box-corner star has no unknown iff the three faces meeting at the corner are Dirichlet
+// a box-corner star has no unknown iff the three faces meeting at the corner are Dirichlet (a
+// periodic direction has no corner); in a periodic direction the star at vertex k_d is the one at 0
 __device__ __forceinline__ bool star_empty(const LevelGeom& g, int v1, int v2, int v3) {
+  if (g.per) {
+    if (((g.per & 1) && v1 >= g.k1) || ((g.per & 2) && v2 >= g.k2) || ((g.per & 4) && v3 >= g.k3)) return true;
+    if (g.per & 7) {
+      const bool c1 = !(g.per & 1) && (v1 == 0 || v1 == g.k1), c2 = !(g.per & 2) && (v2 == 0 || v2 == g.k2),
+                 c3 = !(g.per & 4) && (v3 + g.zoff == 0 || v3 + g.zoff == g.K3);
+      if (!(c1 && c2 && c3)) return false;
+    }
+  }
   const int V3 = v3 + g.zoff;
   const bool c1 = v1 == 0 || v1 == g.k1, c2 = v2 == 0 || v2 == g.k2, c3 = V3 == 0 || V3 == g.K3;
   if (!(c1 && c2 && c3)) return false;

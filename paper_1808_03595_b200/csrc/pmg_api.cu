@@ -220,7 +220,10 @@ pmg_status smooth_dev(pmg_ctx* c, int l, const double* r, double* u) {
     // the z parity is that of the GLOBAL vertex plane, so a z-slab adds the colour corrections
     // of every point in the same order as one GPU (bitwise identical results)
     int c1 = col & 1, c2 = (col >> 1) & 1, c3 = ((col >> 2) & 1) ^ (g.zoff & 1);
-    int n1 = (g.k1 - c1) / 2 + 1, n2 = (g.k2 - c2) / 2 + 1, n3 = (g.k3 - c3) / 2 + 1;
+    // vertices c_d, c_d + 2, ... <= k_d; a periodic direction stops below k_d (vertex k_d is vertex 0)
+    int n1 = (g.per & 1) ? (g.k1 - c1 + 1) / 2 : (g.k1 - c1) / 2 + 1;
+    int n2 = (g.per & 2) ? (g.k2 - c2 + 1) / 2 : (g.k2 - c2) / 2 + 1;
+    int n3 = (g.per & 4) ? (g.k3 - c3 + 1) / 2 : (g.k3 - c3) / 2 + 1;
     long long nb = (long long)n1 * n2 * n3;
     launch_star(g, c1, c2, c3, n1, n2, nb, r, u, D.stab, D.stabP, c->lam, c->st);
     LAUNCH_CHECK(c);
@@ -749,6 +752,7 @@ void pmg_default_options(pmg_options* o) {
   o->schedule = 0;
   o->solver = 0;
   o->neumann = 0;
+  o->periodic = 0;
   o->coarse_rtol = 1e-4;
   o->coarse_maxit = 10000;
   o->coarse_check = 8;
@@ -793,6 +797,18 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   if (o.smoother != 0 && o.smoother != 1) return fail(PMG_EINVAL, "smoother must be 0 (vertex stars) or 1 (element-centred blocks)");
   if (o.smoother == 1 && o.nranks > 1) return fail(PMG_EINVAL, "the element-centred smoother runs on one GPU (nranks = 1)");
   if (o.smoother == 1 && p > 16) return fail(PMG_EINVAL, "the element-centred smoother supports p <= 16");
+  if (o.periodic < 0 || o.periodic > 7) return fail(PMG_EINVAL, "periodic is a 3-bit direction mask");
+  if (o.periodic) {
+    for (int d = 0; d < 3; ++d) {
+      if (!((o.periodic >> d) & 1)) continue;
+      if (n_e[d] < 2 || n_e[d] % 2) return fail(PMG_EINVAL, "a periodic direction needs an even k_d >= 2 (8 star colours)");
+      if ((o.neumann >> (2 * d)) & 3) return fail(PMG_EINVAL, "a periodic direction has no Neumann faces");
+    }
+    if (o.nranks > 1) return fail(PMG_EINVAL, "periodic directions run on one GPU (nranks = 1)");
+    if (o.smoother == 1) return fail(PMG_EINVAL, "periodic directions: vertex-star smoother only");
+    if (o.coarse_solver == 2) return fail(PMG_EINVAL, "periodic directions: Jacobi-PCG coarse solver only");
+    if (o.periodic == 7 && o.neumann == 0 && lambda == 0.0) return fail(PMG_EINVAL, "fully periodic Poisson (lambda = 0) is singular");
+  }
 
   pmg_ctx* c = new (std::nothrow) pmg_ctx();
   if (!c) return fail(PMG_ENOMEM, "host allocation failed");
@@ -814,7 +830,7 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   c->H.resize(L + 1);
   c->D.resize(L + 1);
   for (int l = 0; l <= L; ++l) {
-    std::string err = build_level(c->H[l], deg[l], n_e, widths, lambda, o.weight_degree, o.neumann);
+    std::string err = build_level(c->H[l], deg[l], n_e, widths, lambda, o.weight_degree, o.neumann, o.periodic);
     if (!err.empty()) { free_ctx(c); return fail(PMG_EINVAL, err); }
     if (l >= 1) build_interp(c->H[l], deg[l - 1]);
     if (o.smoother == 1) {   // every level (pmg_smooth may be called on any level)
@@ -959,6 +975,10 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
     std::vector<double> b(kd * p + 1, 0.0);
     for (int e = 0; e < kd; ++e)
       for (int t = 0; t <= p; ++t) b[e * p + t] += 0.5 * widths[d][e] * ww[t];
+    if ((o.periodic >> d) & 1) {   // node k_d p is node 0
+      b[0] += b[kd * p];
+      b[kd * p] = b[0];
+    }
     if ((s = upload(&c->bm[d], b))) { free_ctx(c); return s; }
   }
   c->n_grid = (long long)(n_e[0] * p + 1) * (n_e[1] * p + 1) * ((sp.z1 - sp.z0) * p + 1);
@@ -986,7 +1006,8 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_coop_p2, kThreads, 0);
     const char* env = std::getenv("PMG_COARSE_MULTIKERNEL");
-    if (coop && per_sm > 0 && c->D[0].g.p == 2 && !(env && env[0] == '1')) {
+    // periodic meshes take the multi-kernel Jacobi-PCG (its operator is the wrapped element operator)
+    if (coop && per_sm > 0 && c->D[0].g.p == 2 && !(env && env[0] == '1') && !o.periodic) {
       long long want = (c->g0g.nskel + kThreads - 1) / kThreads;
       long long cap = std::min<long long>((long long)per_sm * nsm, 1344);
       c->coop_nb = (int)std::max<long long>(1, std::min(want, cap));

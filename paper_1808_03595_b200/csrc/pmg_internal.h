@@ -34,7 +34,15 @@ struct LevelGeom {
   // homogeneous Neumann faces (NEXT-3): bit 2d / 2d+1 = low / high face of direction d;
   // every other face is homogeneous Dirichlet
   int neu;
+  // periodic directions (NEXT-3): bit d.  Global indices along d are taken modulo k_d p:
+  // record plane k_d duplicates plane 0 and holds no unknown; neighbour accesses wrap (wrap_pt).
+  int per;
 };
+
+// the record coordinate w (possibly -1 or k) of a periodic direction, wrapped into [0, k)
+PMG_HD inline int wrap_rec(int w, int k, bool periodic) {
+  return periodic ? (w < 0 ? w + k : (w >= k ? w - k : w)) : w;
+}
 
 // is global 1-D index G (0 <= G <= n_el p) an unknown along a direction with the given end flags?
 PMG_HD inline bool free_1d(int G, int n_el_p, bool neu_lo, bool neu_hi) {
@@ -87,7 +95,7 @@ struct HostLevel {
 
 // Host setup; returns an empty string on success, else an error message.
 std::string build_level(HostLevel& L, int p, const int k[3], const double* const widths[3],
-                        double lambda, int weight_degree, int neumann = 0);
+                        double lambda, int weight_degree, int neumann = 0, int periodic = 0);
 std::string build_interp(HostLevel& fine, int p_coarse);
 // element-centred block tables (fills L.ectab; L built by build_level with the same k, widths)
 std::string build_ec_tables(HostLevel& L, const int k[3], const double* const widths[3], int neumann);

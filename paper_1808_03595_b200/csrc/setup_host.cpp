@@ -143,7 +143,7 @@ static double weight7(double t) {
 }
 
 std::string build_level(HostLevel& L, int p, const int k[3], const double* const widths[3],
-                        double lambda, int weight_degree, int neumann) {
+                        double lambda, int weight_degree, int neumann, int periodic) {
   (void)lambda;
   if (weight_degree != 7) return "only weight_degree = 7 is implemented (P:316)";
   if (p < 2 || p > 32) return "degree p must be in [2, 32]";
@@ -162,6 +162,7 @@ std::string build_level(HostLevel& L, int p, const int k[3], const double* const
   g.nelem = (long long)k[0] * k[1] * k[2];
   g.zoff = 0; g.K3 = k[2]; g.own_lo = 0; g.own_hi = g.V3;
   g.neu = neumann;
+  g.per = periodic;
 
   std::vector<double> xi, wq;
   gll(p, xi, wq);
@@ -215,8 +216,10 @@ std::string build_level(HostLevel& L, int p, const int k[3], const double* const
     for (int v = 0; v <= k[d]; ++v, ++base) {
       double* T = &L.stab[base * g.ST];
       std::vector<double> M(n, 0.0), K(n * n, 0.0);
+      const bool per = (periodic >> d) & 1;
       for (int side = 0; side < 2; ++side) {
         int e = v - 1 + side;
+        if (per) e = ((e % k[d]) + k[d]) % k[d];   // periodic: the line wraps (vertex k_d is vertex 0)
         if (e < 0 || e >= k[d]) continue;
         double h = widths[d][e];
         for (int t = 0; t <= p; ++t) {
@@ -232,7 +235,7 @@ std::string build_level(HostLevel& L, int p, const int k[3], const double* const
       std::vector<int> cpl;
       for (int j = 0; j < n; ++j) {
         long long gg = (long long)(v - 1) * p + 1 + j;   // unknowns of the star line (Dirichlet ends padded)
-        if (free_1d((int)gg, k[d] * p, (neumann >> (2 * d)) & 1, (neumann >> (2 * d + 1)) & 1)) cpl.push_back(j);
+        if (per || free_1d((int)gg, k[d] * p, (neumann >> (2 * d)) & 1, (neumann >> (2 * d + 1)) & 1)) cpl.push_back(j);
       }
       int nc = (int)cpl.size();
       std::vector<double> S(n * n, 0.0), lamv(n, 1.0);
@@ -467,9 +470,12 @@ std::string coarse_diag(const HostLevel& L, double lambda, std::vector<double>& 
                 v -= Ma * Ma * Mb * Mb * sum;
               }
               int g1 = e1 * p + t1, g2 = e2 * p + t2, g3 = e3 * p + t3;
-              bool fr = free_1d(g1, g.k1 * p, g.neu & 1, (g.neu >> 1) & 1) &&
-                        free_1d(g2, g.k2 * p, (g.neu >> 2) & 1, (g.neu >> 3) & 1) &&
-                        free_1d(g3, g.k3 * p, (g.neu >> 4) & 1, (g.neu >> 5) & 1);
+              if (g.per & 1) g1 %= g.k1 * p;   // periodic: the last element's high faces are plane 0
+              if (g.per & 2) g2 %= g.k2 * p;
+              if (g.per & 4) g3 %= g.k3 * p;
+              bool fr = ((g.per & 1) || free_1d(g1, g.k1 * p, g.neu & 1, (g.neu >> 1) & 1)) &&
+                        ((g.per & 2) || free_1d(g2, g.k2 * p, (g.neu >> 2) & 1, (g.neu >> 3) & 1)) &&
+                        ((g.per & 4) || free_1d(g3, g.k3 * p, (g.neu >> 4) & 1, (g.neu >> 5) & 1));
               if (fr) diag[host_skel_index(g, g1, g2, g3)] += v;
             }
       }

@@ -141,7 +141,6 @@ __global__ void __launch_bounds__(128, Star16<P>::MINB)
   long long* fb = reinterpret_cast<long long*>(sm + K::oFb);
   long long* lb = reinterpret_cast<long long*>(sm + K::oLb);
   const long long V12 = (long long)g.V1 * g.V2;
-  const long long rec0 = v1 + g.V1 * (long long)v2 + V12 * v3;
   // ---- setup tables (before the dependency wait): S_d padded NP x NP, then Lambda, s, w
   {
     auto row = [&](int d) -> size_t {   // star-table row of the vertex line along direction d
@@ -160,8 +159,10 @@ __global__ void __launch_bounds__(128, Star16<P>::MINB)
   }
   if (tid < 8) {   // record (v - b) for offset bits b = (b1, b2, b3); -1 if outside the stored box
     const int b1 = tid & 1, b2 = (tid >> 1) & 1, b3 = (tid >> 2) & 1;
-    const bool ok = !((v1 == 0 && b1) || (v2 == 0 && b2) || (v3 == 0 && b3));
-    base[tid] = ok ? (rec0 - (b1 + g.V1 * (long long)b2 + V12 * b3)) * RS : -1LL;
+    const bool ok = !((v1 == 0 && b1 && !(g.per & 1)) || (v2 == 0 && b2 && !(g.per & 2)) || (v3 == 0 && b3 && !(g.per & 4)));
+    const int w1 = wrap_rec(v1 - b1, g.k1, g.per & 1), w2 = wrap_rec(v2 - b2, g.k2, g.per & 2),
+              w3 = wrap_rec(v3 - b3, g.k3, g.per & 4);   // periodic: record k - 1 for v = 0
+    base[tid] = ok ? (w1 + g.V1 * (long long)w2 + V12 * w3) * RS : -1LL;
   }
   __syncthreads();
   if (tid < 12) {   // face block f = 4 d + 2 qa + qb: interior of face d of the record on side (qa, qb)

@@ -53,15 +53,15 @@ def close(a, b, tol):
 class Pair:
     """Oracle hierarchy + GPU solver for the same problem."""
 
-    def __init__(self, k, p, lam, stretch, coarse_rtol=1e-13, schedule=0, neumann=0):
+    def __init__(self, k, p, lam, stretch, coarse_rtol=1e-13, schedule=0, neumann=0, periodic=0):
         from oracle import mg
         import paper_1808_03595_b200 as pmg
         case = pi.small_case(k, p, lam, stretch=stretch)
         self.case = case
         self.orc = mg.Hierarchy(case.k, case.widths, p, lam, coarse_rtol=coarse_rtol, schedule=schedule,
-                                neumann=neumann)
+                                neumann=neumann, periodic=periodic)
         self.gpu = pmg.Solver(case.k, case.widths, p, lam, coarse_rtol=coarse_rtol, schedule=schedule,
-                              neumann=neumann)
+                              neumann=neumann, periodic=periodic)
         assert self.gpu.nlevels == len(self.orc.levels)
         self.rng = np.random.default_rng(11)
 
@@ -646,3 +646,162 @@ def test_warp_star_kernel_forced_parity(name, monkeypatch):
         torch.cuda.synchronize()
         assert close(g.cpu().numpy(), sm.apply(r), OP_TOL), l
     s.close()
+
+
+# periodic directions: every kernel family (k_star_pf / k_star_w at
+# p <= 4, k_star16 at 5..16, k_star_tm above; k_elem_pf, k_elem16, k_elem_apply_t; transfers;
+# condensation / recovery) on wrapped meshes
+PERIODIC_CASES = {
+    "k423_p4_per_x": dict(k=(4, 2, 3), p=4, lam=0.3, stretch=1.3, periodic=0b001),
+    "k324_p8_per_yz": dict(k=(3, 2, 4), p=8, lam=0.0, stretch=None, periodic=0b110),
+    "k224_p16_per_xyz": dict(k=(2, 2, 4), p=16, lam=1.1, stretch=None, periodic=0b111),
+    "k422_p12_per_x_neu_z": dict(k=(4, 2, 2), p=12, lam=0.5, stretch=1.2, periodic=0b001, neumann=0b110000),
+    "k243_p3_per_y": dict(k=(2, 4, 3), p=3, lam=0.0, stretch=None, periodic=0b010),
+    "k222_p20_per_x": dict(k=(2, 2, 2), p=20, lam=0.7, stretch=None, periodic=0b001),
+}
+_PPAIRS = {}
+
+
+def ppair(name):
+    if name not in _PPAIRS:
+        _PPAIRS[name] = Pair(**PERIODIC_CASES[name])
+    return _PPAIRS[name]
+
+
+@pytest.mark.parametrize("name", list(PERIODIC_CASES))
+def test_periodic_operators_parity(name):
+    """Residual, smoother, restriction, prolongation on every level, condensation / recovery and the
+    V-cycle against the oracle's wrapped operators (per-operator tolerance)."""
+    P = ppair(name)
+    L = P.gpu.nlevels - 1
+    for l in range(L + 1):
+        orc = P.orc.levels[l]
+        u, f = P.rand_skel(l), P.rand_skel(l)
+        r = P.gpu.new_skel(l)
+        P.gpu.residual(l, P.to_skel(l, u), P.to_skel(l, f), r)
+        assert close(P.to_grid(l, r), orc.mesh.fill_periodic(orc.op.residual(u, f)), OP_TOL), l
+        du = P.gpu.new_skel(l)
+        P.gpu.smooth(l, P.to_skel(l, f), du)
+        assert close(P.to_grid(l, du), orc.mesh.fill_periodic(orc.smoother.apply(f)), OP_TOL), l
+        if l >= 1:
+            T = P.orc.transfers[l]
+            fc = P.gpu.new_skel(l - 1)
+            P.gpu.restrict(l, P.to_skel(l, f), fc)
+            assert close(P.to_grid(l - 1, fc), P.orc.levels[l - 1].mesh.fill_periodic(T.restrict(f)), OP_TOL), l
+            uc = P.rand_skel(l - 1)
+            uf = P.gpu.new_skel(l)
+            P.gpu.prolong(l, P.to_skel(l - 1, uc), uf)
+            assert close(P.to_grid(l, uf), orc.mesh.fill_periodic(T.prolong(uc)), OP_TOL), l
+    m = P.mesh(L)
+    op = P.orc.levels[L].op
+    F = P.rng.standard_normal(m.ntot) * m.free
+    Fd = torch.from_numpy(F).cuda()
+    fh = P.gpu.new_skel(L)
+    P.gpu.condense(Fd, fh)
+    assert close(P.to_grid(L, fh), m.fill_periodic(op.condense(F)), OP_TOL)
+    uh = P.rand_skel(L)
+    ug = P.gpu.new_grid()
+    P.gpu.recover(P.to_skel(L, uh), Fd, ug)
+    torch.cuda.synchronize()
+    assert close(ug.cpu().numpy(), m.fill_periodic(op.recover(uh, F)), OP_TOL)
+    f = P.rand_skel(L)
+    u = P.gpu.new_skel(L)
+    P.gpu.vcycle(u, P.to_skel(L, f))
+    assert close(P.to_grid(L, u), m.fill_periodic(P.orc.vcycle(np.zeros_like(f), f)), OP_TOL)
+
+
+@pytest.mark.parametrize("name", list(PERIODIC_CASES))
+def test_periodic_solve_parity(name):
+    from oracle import condensed
+    P = ppair(name)
+    L = P.gpu.nlevels - 1
+    m = P.mesh(L)
+    F = condensed.weak_rhs(m, pi.uniform_pm1(5, np.arange(m.ntot)))
+    u_orc, rep_o = P.orc.solve(F, 1e-10)
+    ug = P.gpu.new_grid()
+    rep = P.gpu.solve(torch.from_numpy(F).cuda(), ug, 1e-10)
+    torch.cuda.synchronize()
+    assert rep["converged"] and rep["cycles"] == rep_o["cycles"], (rep["cycles"], rep_o["cycles"])
+    assert close(ug.cpu().numpy(), u_orc, SOLVE_TOL)
+
+
+@pytest.mark.parametrize("per", [0b001, 0b111])
+def test_periodic_manufactured_on_gpu(per):
+    """lambda = 1, f = 4 u: u = cos x cos y cos z fully periodic on (0, 2 pi)^3, or u = cos x sin y sin z
+    periodic in x with Dirichlet y, z faces on (0, 2 pi) x (0, pi)^2; 4 x 2 x 2 elements, p = 8: the
+    GPU solve reproduces u to spectral accuracy, duplicate planes included."""
+    import math
+    import paper_1808_03595_b200 as pmg
+    k = (4, 2, 2)
+    Lb = (2 * math.pi,) * 3 if per == 0b111 else (2 * math.pi, math.pi, math.pi)
+    s = pmg.Solver(k, pi.uniform_widths(k, Lb), 8, 1.0, periodic=per)
+    L = s.nlevels - 1
+    x = [s.grid_coords(L, d) for d in range(3)]
+    X3, X2, X1 = np.meshgrid(x[2], x[1], x[0], indexing="ij")
+    ue = (np.cos(X1) * ((np.cos(X2) * np.cos(X3)) if per == 0b111 else (np.sin(X2) * np.sin(X3)))).ravel()
+    F = s.new_grid()
+    s.weak_rhs(torch.from_numpy(4.0 * ue).cuda(), F)
+    u = s.new_grid()
+    rep = s.solve(F, u, 1e-12)
+    torch.cuda.synchronize()
+    assert rep["converged"]
+    assert np.abs(u.cpu().numpy() - ue).max() < 1e-5
+    s.close()
+
+
+def test_periodic_translation_invariance_on_gpu():
+    """Uniform elements, periodic in x: the GPU solution of the right-hand side shifted by one element
+    along x is the shifted solution."""
+    import paper_1808_03595_b200 as pmg
+    k, p = (6, 2, 3), 8
+    s = pmg.Solver(k, pi.uniform_widths(k, (1.0, 0.7, 0.9)), p, 0.3, periodic=0b001, coarse_rtol=1e-13)
+    N = (k[0] * p + 1, k[1] * p + 1, k[2] * p + 1)
+    g = np.random.default_rng(5).uniform(-1, 1, (N[2], N[1], N[0] - 1))
+
+    def solve(gg):
+        f = np.concatenate([gg, gg[:, :, :1]], axis=2).ravel()
+        F = s.new_grid()
+        s.weak_rhs(torch.from_numpy(f).cuda(), F)
+        u = s.new_grid()
+        rep = s.solve(F, u, 1e-12)
+        torch.cuda.synchronize()
+        return u.cpu().numpy().reshape(N[2], N[1], N[0])[:, :, :N[0] - 1], rep
+    u1, r1 = solve(g)
+    u2, r2 = solve(np.roll(g, p, axis=2))
+    assert r1["cycles"] == r2["cycles"]
+    a = np.roll(u1, p, axis=2)
+    assert np.abs(a - u2).max() <= 1e-10 * np.abs(a).max()
+    s.close()
+
+
+def test_periodic_warp_star_kernel_forced(monkeypatch):
+    import paper_1808_03595_b200 as pmg
+    monkeypatch.setenv("PMG_STAR_W_MIN", "0")
+    P = ppair("k423_p4_per_x")
+    case = P.case
+    s = pmg.Solver(case.k, case.widths, case.p, case.lam, periodic=0b001)
+    for l in range(s.nlevels):
+        r = P.rand_skel(l)
+        rs = s.new_skel(l)
+        s.skel_from_grid(l, torch.from_numpy(r).cuda(), rs)
+        du = s.new_skel(l)
+        s.smooth(l, rs, du)
+        g = s.new_grid(l)
+        s.skel_to_grid(l, du, g)
+        torch.cuda.synchronize()
+        assert close(g.cpu().numpy(), P.orc.levels[l].mesh.fill_periodic(P.orc.levels[l].smoother.apply(r)), OP_TOL), l
+    s.close()
+
+
+def test_periodic_invalid_options():
+    import paper_1808_03595_b200 as pmg
+    case = pi.small_case((3, 2, 2), 4, 0.5)
+    with pytest.raises(pmg.PmgError):
+        pmg.Solver(case.k, case.widths, 4, 0.5, periodic=0b001)             # odd k_1
+    case = pi.small_case((2, 2, 2), 4, 0.0)
+    with pytest.raises(pmg.PmgError):
+        pmg.Solver(case.k, case.widths, 4, 0.0, periodic=0b111)             # singular fully periodic Poisson
+    with pytest.raises(pmg.PmgError):
+        pmg.Solver(case.k, case.widths, 4, 1.0, periodic=0b001, neumann=0b000001)
+    with pytest.raises(pmg.PmgError):
+        pmg.Solver(case.k, case.widths, 4, 1.0, periodic=0b001, smoother=1)
