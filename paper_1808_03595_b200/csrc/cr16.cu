@@ -234,19 +234,29 @@ __global__ void __launch_bounds__(256, 2)
   }
   __syncthreads();
   if (MODE == 0) {
-    // G_f[A][B] = sum_{b_d} a_f[b_d] V (into Fa, zero padded), then Yc_f = P_b^T G_f P_a
-    for (int i = tid; i < 6 * 256; i += NT) {
-      const int f = i >> 8, l = i & 255, A = l >> 4, B = l & 15, d = f >> 1, s = f & 1;
-      double acc = 0.0;
+    // G_f[A][B] = sum_{b_d} a_f[b_d] V (into Fa, zero padded), then Yc_f = P_b^T G_f P_a; one (A, B)
+    // per thread for all six faces (six independent accumulation chains)
+    {
+      const int A = tid >> 4, B = tid & 15;
+      double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       if (A < M && B < M) {
-        const double* af = tb + d * TB + MS + (s ? 32 : 16);
-        // V[b3][b2][b1] at C1[(b3 m + b2) LD + b1]: the line along the face normal
-        const double* v = C1 + (d == 0 ? (A * M + B) * LD : (d == 1 ? A * M * LD + B : A * LD + B));
-        const int st = d == 0 ? 1 : (d == 1 ? LD : M * LD);
+        const double *a10 = tb + MS + 16, *a11 = tb + MS + 32, *a20 = tb + TB + MS + 16, *a21 = tb + TB + MS + 32,
+                     *a30 = tb + 2 * TB + MS + 16, *a31 = tb + 2 * TB + MS + 32;
 #pragma unroll
-        for (int t = 0; t < M; ++t) acc = fma(af[t], v[t * st], acc);
+        for (int t = 0; t < M; ++t) {
+          const double v0 = C1[(A * M + B) * LD + t];   // faces normal to x1: (b3, b2) = (A, B), b1 = t
+          const double v1 = C1[(A * M + t) * LD + B];   // normal to x2: (b3, b1) = (A, B), b2 = t
+          const double v2 = C1[(t * M + A) * LD + B];   // normal to x3: (b2, b1) = (A, B), b3 = t
+          acc[0] = fma(a10[t], v0, acc[0]);
+          acc[1] = fma(a11[t], v0, acc[1]);
+          acc[2] = fma(a20[t], v1, acc[2]);
+          acc[3] = fma(a21[t], v1, acc[3]);
+          acc[4] = fma(a30[t], v2, acc[4]);
+          acc[5] = fma(a31[t], v2, acc[5]);
+        }
       }
-      Fa[f * MS + A * LD + B] = acc;
+#pragma unroll
+      for (int f = 0; f < 6; ++f) Fa[f * MS + A * LD + B] = acc[f];
     }
     __syncthreads();
     double* X = C0;
@@ -261,9 +271,10 @@ __global__ void __launch_bounds__(256, 2)
     }
     __syncthreads();
     double* Ye = Yc + (size_t)e * 6 * MM;
-    for (int i = tid; i < 6 * MM; i += NT) {
-      const int f = i / MM, l = i - f * MM, A = l / M, B = l - A * M;
-      Ye[i] = Fa[f * MS + A * LD + B];
+    for (int l = tid; l < MM; l += NT) {   // block position l for all six faces
+      const int A = l / M, B = l - A * M;
+#pragma unroll
+      for (int f = 0; f < 6; ++f) Ye[f * MM + l] = Fa[f * MS + A * LD + B];
     }
   } else {
     // back transforms S along x1, x2, x3: C1 -> C0 -> C1 -> C0 ([i3][i2][i1] in C0), then store;

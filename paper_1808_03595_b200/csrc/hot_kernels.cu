@@ -1237,15 +1237,20 @@ __global__ void __launch_bounds__(256) k_gather_resid_t(LevelGeom g, const doubl
   const int v1 = blockIdx.x, v2 = blockIdx.y, v3 = blockIdx.z;
   const long long rec = v1 + (long long)g.V1 * (v2 + (long long)g.V2 * v3);
   const bool own = owned_plane(g, v3);
-  auto el = [&](int a1, int a2, int a3) -> size_t {
-    return ((size_t)a1 + (size_t)g.k1 * ((size_t)a2 + (size_t)g.k2 * a3)) * YS;
-  };
-  auto yat = [&](int a1, int a2, int a3, int off) -> double {   // 0 outside the box (Neumann faces)
-    a1 = wrap_rec(a1, g.k1, g.per & 1);   // periodic: element k - 1 precedes element 0
+  // Y offsets of the (up to) 8 elements around vertex v: bit d of c set = element v_d along d, clear =
+  // element v_d - 1 (periodic: wrapped); -1 outside the box (Neumann faces have one side)
+  __shared__ long long eb[8];
+  if (threadIdx.x < 8) {
+    const int c = threadIdx.x;
+    int a1 = v1 - 1 + (c & 1), a2 = v2 - 1 + ((c >> 1) & 1), a3 = v3 - 1 + ((c >> 2) & 1);
+    a1 = wrap_rec(a1, g.k1, g.per & 1);
     a2 = wrap_rec(a2, g.k2, g.per & 2);
     a3 = wrap_rec(a3, g.k3, g.per & 4);
-    return (a1 >= 0 && a2 >= 0 && a3 >= 0 && a1 < g.k1 && a2 < g.k2 && a3 < g.k3) ? Y[el(a1, a2, a3) + off] : 0.0;
-  };
+    const bool in = a1 >= 0 && a2 >= 0 && a3 >= 0 && a1 < g.k1 && a2 < g.k2 && a3 < g.k3;
+    eb[c] = in ? ((long long)a1 + (long long)g.k1 * ((long long)a2 + (long long)g.k2 * a3)) * YS : -1LL;
+  }
+  __syncthreads();
+  auto yat = [&](int c, int off) -> double { const long long b_ = eb[c]; return b_ >= 0 ? Y[b_ + off] : 0.0; };
   for (int o = threadIdx.x; o < RS; o += blockDim.x) {
     int t1 = 0, t2 = 0, t3 = 0, type, a = 0, b = 0;
     if (o < 3 * mm) {
@@ -1264,28 +1269,22 @@ __global__ void __launch_bounds__(256) k_gather_resid_t(LevelGeom g, const doubl
     double r = 0.0;
     if (own && is_free(g, v1 * P + t1, v2 * P + t2, v3 * P + t3)) {
       double s_ = 0.0;
-      if (type < 3) {
+      if (type < 3) {            // face normal to d: the element below along d (its high face) and v's
         const int d = type, oo = a * m + b;
-        int w1 = v1, w2 = v2, w3 = v3;
-        if (d == 0) w1 -= 1; else if (d == 1) w2 -= 1; else w3 -= 1;
-        s_ = yat(w1, w2, w3, (2 * d + 1) * mm + oo) + yat(v1, v2, v3, (2 * d) * mm + oo);
-      } else if (type < 6) {
-        const int d = type - 3;
+        s_ = yat(7 & ~(1 << d), (2 * d + 1) * mm + oo) + yat(7, (2 * d) * mm + oo);
+      } else if (type < 6) {     // edge along d: the four elements around it
+        const int d = type - 3, da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2;
         for (int bB = 0; bB < 2; ++bB)
           for (int bA = 0; bA < 2; ++bA) {
-            int a1 = v1, a2 = v2, a3 = v3;
-            if (d == 0) { a2 += bA - 1; a3 += bB - 1; }
-            else if (d == 1) { a1 += bA - 1; a3 += bB - 1; }
-            else { a1 += bA - 1; a2 += bB - 1; }
             const int qe = 4 * d + (1 - bA) + 2 * (1 - bB);
-            s_ += yat(a1, a2, a3, 6 * mm + qe * m + a);
+            s_ += yat((1 << d) | (bA << da) | (bB << db), 6 * mm + qe * m + a);
           }
-      } else {
+      } else {                   // vertex: the eight elements
         for (int c3 = 0; c3 < 2; ++c3)
           for (int c2 = 0; c2 < 2; ++c2)
             for (int c1 = 0; c1 < 2; ++c1) {
               const int qv = (1 - c1) + 2 * (1 - c2) + 4 * (1 - c3);
-              s_ += yat(v1 - 1 + c1, v2 - 1 + c2, v3 - 1 + c3, 6 * mm + 12 * m + qv);
+              s_ += yat(c1 | (c2 << 1) | (c3 << 2), 6 * mm + 12 * m + qv);
             }
       }
       r = F ? F[rec * RS + o] - s_ : s_;

@@ -24,6 +24,8 @@ KEYS = {
     "launch__block_size": "block",
     "smsp__cycles_active.avg": "smsp_active_cycles",
     "sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active": "dmma_pipe_pct",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active": "fp64_inst_pct",
+    "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active": "dmma_inst_pct",
 }
 
 
