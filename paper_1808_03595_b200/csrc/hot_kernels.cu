@@ -18,6 +18,14 @@
 
 namespace pmg {
 
+// 1/x by rcp.approx and one cubic Newton step r (1 + e + e^2), e = 1 - x r (error e^3)
+__device__ __forceinline__ double rcp_c3(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
+
 __device__ __forceinline__ double rcp_nr(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
@@ -884,8 +892,9 @@ __global__ void __launch_bounds__(ElemPfCfg<P>::NT, ElemPfCfg<P>::MINB)
 // per two fragment loads.
 // ------------------------------------------------------------------------------------------
 template <int P> struct StarTmCfg {
-  static constexpr int N = 2 * P - 1, NN = N * N, C = P - 1, NP = 64, LD = 68, MS = NP * LD;
-  static constexpr int NT = 256, NW = 8, TPP = (NP / 8) * (NP / 8);
+  // n_S padded to a multiple of 8 (40 ... 64), leading dimension = 4 mod 8 (conflict-free fragments)
+  static constexpr int N = 2 * P - 1, NN = N * N, C = P - 1, NP = (N + 7) / 8 * 8, LD = NP + 4, MS = NP * LD;
+  static constexpr int NT = 256, NW = 8, TB = NP / 8, TPP = TB * TB;
   static constexpr int oFT = 0, oG = 3 * MS, oVec = 6 * MS, total = oVec + 9 * N;
 };
 
@@ -938,7 +947,7 @@ __global__ void __launch_bounds__(256, 1) k_star_tm(LevelGeom g, int c1, int c2,
   auto sget = [](const double* Sd, int row, int col) { return (row < N && col < N) ? __ldg(&Sd[row * N + col]) : 0.0; };
   // forward A: X_d = F_d S_a  (X into G's space)
   for (int job = warp; job < 3 * TPP; job += C::NW) {
-    const int d = job / TPP, t = job - d * TPP, mi = t >> 3, ni = t & 7;
+    const int d = job / TPP, t = job - d * TPP, mi = t / C::TB, ni = t - mi * C::TB;
     const double* Fd = FT + d * MS;
     const double* Sa = S[d == 0 ? 1 : 0];
     dmma_tile_fn<NP>([&](int i, int k) { return Fd[i * LD + k]; }, [&](int k, int j) { return sget(Sa, k, j); },
@@ -947,7 +956,7 @@ __global__ void __launch_bounds__(256, 1) k_star_tm(LevelGeom g, int c1, int c2,
   __syncthreads();
   // forward B: T_d = S_b^T X_d  (into FT)
   for (int job = warp; job < 3 * TPP; job += C::NW) {
-    const int d = job / TPP, t = job - d * TPP, mi = t >> 3, ni = t & 7;
+    const int d = job / TPP, t = job - d * TPP, mi = t / C::TB, ni = t - mi * C::TB;
     const double* Xd = Gs + d * MS;
     const double* Sb = S[d == 2 ? 1 : 2];
     dmma_tile_fn<NP>([&](int i, int k) { return sget(Sb, k, i); }, [&](int k, int j) { return Xd[k * LD + j]; },
@@ -969,7 +978,7 @@ __global__ void __launch_bounds__(256, 1) k_star_tm(LevelGeom g, int c1, int c2,
           double E = s1[a1] * t1;
           E = fma(x2, T2[a3 * LD + a1], E);
           E = fma(x3, T3[a2 * LD + a1], E);
-          acc = fma(s1[a1], E * rcp_nr(base + L1[a1]), acc);
+          acc = fma(s1[a1], E * rcp_c3(base + L1[a1]), acc);
         }
       } else if (pass == 1) {   // G2[a3][a1] = sum_a2 s2[a2] E
         const int a3 = hi, a1 = lo;
@@ -979,7 +988,7 @@ __global__ void __launch_bounds__(256, 1) k_star_tm(LevelGeom g, int c1, int c2,
           double E = x1 * T1[a3 * LD + a2];
           E = fma(s2[a2], t2, E);
           E = fma(x3, T3[a2 * LD + a1], E);
-          acc = fma(s2[a2], E * rcp_nr(base + L2[a2]), acc);
+          acc = fma(s2[a2], E * rcp_c3(base + L2[a2]), acc);
         }
       } else {                  // G3[a2][a1] = sum_a3 s3[a3] E
         const int a2 = hi, a1 = lo;
@@ -989,7 +998,7 @@ __global__ void __launch_bounds__(256, 1) k_star_tm(LevelGeom g, int c1, int c2,
           double E = x1 * T1[a3 * LD + a2];
           E = fma(x2, T2[a3 * LD + a1], E);
           E = fma(s3[a3], t3, E);
-          acc = fma(s3[a3], E * rcp_nr(base + L3[a3]), acc);
+          acc = fma(s3[a3], E * rcp_c3(base + L3[a3]), acc);
         }
       }
       Gs[pass * MS + hi * LD + lo] = acc;
@@ -998,7 +1007,7 @@ __global__ void __launch_bounds__(256, 1) k_star_tm(LevelGeom g, int c1, int c2,
   __syncthreads();
   // back A: X_d = G_d S_a^T  (into FT) ; back B: U_d = S_b X_d  (into G)
   for (int job = warp; job < 3 * TPP; job += C::NW) {
-    const int d = job / TPP, t = job - d * TPP, mi = t >> 3, ni = t & 7;
+    const int d = job / TPP, t = job - d * TPP, mi = t / C::TB, ni = t - mi * C::TB;
     const double* Gd = Gs + d * MS;
     const double* Sa = S[d == 0 ? 1 : 0];
     dmma_tile_fn<NP>([&](int i, int k) { return Gd[i * LD + k]; }, [&](int k, int j) { return sget(Sa, j, k); },
@@ -1006,7 +1015,7 @@ __global__ void __launch_bounds__(256, 1) k_star_tm(LevelGeom g, int c1, int c2,
   }
   __syncthreads();
   for (int job = warp; job < 3 * TPP; job += C::NW) {
-    const int d = job / TPP, t = job - d * TPP, mi = t >> 3, ni = t & 7;
+    const int d = job / TPP, t = job - d * TPP, mi = t / C::TB, ni = t - mi * C::TB;
     const double* Xd = FT + d * MS;
     const double* Sb = S[d == 2 ? 1 : 2];
     dmma_tile_fn<NP>([&](int i, int k) { return sget(Sb, i, k); }, [&](int k, int j) { return Xd[k * LD + j]; },
