@@ -200,6 +200,29 @@ __device__ __forceinline__ double apply_entry(const LevelGeom& g, const CoarseTa
   return q;
 }
 
+// Read-only accessor for the standalone residual (the vector is not written in the kernel: L1 path)
+struct RoAcc {
+  const double* p;
+  __device__ __forceinline__ double operator()(long long i) const {
+    const double v = __ldg(&p[i < 0 ? 0 : i]);
+    return i < 0 ? 0.0 : v;
+  }
+};
+
+// Condensed residual at p = 2 (one GPU, not periodic): r = f - H_hat u (f = NULL: H_hat u) on free entries, 0 elsewhere,
+// one thread per skeleton entry with the line stencil + element corrections above (no element
+// workspace; the p = 2 element kernel ran 27 points per CTA).
+__global__ void __launch_bounds__(256) k_resid_p2(LevelGeom g, CoarseTabs ct, const double* __restrict__ u,
+                                                 const double* __restrict__ f, double* __restrict__ r, double lam) {
+  const long long n = g.nskel;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const Entry E = decode2(g, i);
+    if (!is_free(g, E.g1, E.g2, E.g3)) { r[i] = 0.0; continue; }
+    const double hu = apply_entry(g, ct, RoAcc{u}, i, lam);
+    r[i] = f ? f[i] - hu : hu;   // f = NULL: the operator application H_hat u
+  }
+}
+
 // The same row of H_hat written out once: q[idx] = sum_k a[k] p[jx[k]] with the 13 line-stencil
 // entries first and the 12 face-centre entries of the (up to two) adjacent elements after them.
 // Unused slots point at idx itself with a zero coefficient (a harmless load).  The row never changes
@@ -590,158 +613,371 @@ __global__ void __launch_bounds__(256) k_pcg_gv_ell_p2(long long n, const double
 
 // ------------------------------------------------------------------------------------------
 // CG on the coarse system with the h-multigrid V-cycle as preconditioner (reading R16,
-// oracle/hmg.py): one cooperative launch; every step of the V-cycle is a grid-stride loop over the
-// level's unknowns followed by a grid barrier; the coarsest level (a few hundred unknowns) is
-// smoothed by block 0 alone with block barriers.  Damped Jacobi (omega = 0.6), two sweeps before and
-// after the coarse correction, 40 sweeps on the coarsest level -- the oracle's constants.
+// oracle/hmg.py), matrix-free on the p = 2 GRID layout of every h-level.
+//
+// Every h-level is a p = 2 mesh; its vectors are (2k_1+1)(2k_2+1)(2k_3+1) grid arrays, x1 fastest,
+// with the element centres (all three indices odd) and the non-free points held at zero.  The
+// condensed operator at p = 2 (see the header of this file) is evaluated on the fly:
+//   q_i = lam B1 B2 B3 v_i + sum_d (B_a B_b) sum_{o=-2..2} K_d[G_d][o] v_{i + o s_d}
+//         - sum_{elements e with i a face centre of e} H_{c,i} (H_cB v_B) / H_cc,
+// the 1-D assembled lumped masses B_d and stiffness rows K_d per grid index, and per direction and
+// element index the centre row of the element's 1-D matrices (m = M[1], K[1][0], K[1][2], K[1][1]):
+//   H_{c, face d low}  = K_d[1][0] m_a m_b,   H_{c, face d high} = K_d[1][2] m_a m_b,
+//   H_cc = lam m1 m2 m3 + K_1[1][1] m2 m3 + m1 K_2[1][1] m3 + m1 m2 K_3[1][1].
+// An operator application reads one vector (stencil neighbours from L1 / L2) and writes one: about
+// 16 B per point instead of the 300 B of an assembled 25-entry ELL row.  The transfers are
+// tensor-product 1-D tables: prolongation = the coarse element's quadratic at the fine node with the
+// centre value replaced by its harmonic extension -H_cB u_B / H_cc; restriction = its exact
+// transpose (a gather of <= 7 fine nodes per direction, plus the centre gathers redistributed to the
+// face centres).
 // ------------------------------------------------------------------------------------------
+// experiment builds (-DPMG_HMG_TRACE): block 0 stamps %globaltimer at every grid barrier of the
+// h-multigrid CG (first 8192 barriers of a launch) -> pmg_debug_hmg_trace
+#ifdef PMG_HMG_TRACE
+__device__ unsigned long long g_hmg_trace[2 * 8192];
+__device__ int g_hmg_ntrace;
+#define HSYNC(tag)                                                                            \
+  do {                                                                                        \
+    grid.sync();                                                                              \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && g_hmg_ntrace < 8192) {                         \
+      unsigned long long t_;                                                                  \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                 \
+      g_hmg_trace[2 * g_hmg_ntrace] = t_;                                                     \
+      g_hmg_trace[2 * g_hmg_ntrace + 1] = (tag);                                              \
+      g_hmg_ntrace++;                                                                         \
+    }                                                                                         \
+  } while (0)
+#else
+#define HSYNC(tag) grid.sync()
+#endif
+
 namespace {
 constexpr double kHmgOmega = 0.6;
 constexpr int kHmgNu = 2, kHmgCoarsest = 40;
 
-__device__ __forceinline__ double ell_row(const double* __restrict__ val, const int* __restrict__ col, long long n,
-                                          long long i, const double* __restrict__ v) {
+// the 4-entry element row e of a per-direction table (two 16-byte read-only loads)
+__device__ __forceinline__ double4 ld_row4(const double* t, int e) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(t) + 2 * e);
+  const double2 b = __ldg(reinterpret_cast<const double2*>(t) + 2 * e + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+
+__device__ __forceinline__ void hg_decode(const HGridLev& L, long long i, int& g1, int& g2, int& g3) {
+  const unsigned u = (unsigned)i, t = u / (unsigned)L.N1;
+  g1 = (int)(u - t * (unsigned)L.N1);
+  g3 = (int)(t / (unsigned)L.N2);
+  g2 = (int)(t - (unsigned)g3 * (unsigned)L.N2);
+}
+
+__device__ __forceinline__ bool hg_free(const HGridLev& L, int g1, int g2, int g3) {
+  if (g1 & g2 & g3 & 1) return false;   // element centre: condensed out
+  return free_1d(g1, L.N1 - 1, L.neu & 1, (L.neu >> 1) & 1) && free_1d(g2, L.N2 - 1, (L.neu >> 2) & 1, (L.neu >> 3) & 1) &&
+         free_1d(g3, L.N3 - 1, (L.neu >> 4) & 1, (L.neu >> 5) & 1);
+}
+
+// plain vector (written inside the kernel: plain loads, ordered by the grid barriers)
+struct HV {
+  const double* p;
+  __device__ __forceinline__ double operator()(long long j) const { return p[j]; }
+};
+// omega D^-1 f: the first damped-Jacobi sweep from zero, evaluated where the second sweep reads it
+struct HW {
+  const double *d, *f;
+  __device__ __forceinline__ double operator()(long long j) const { return kHmgOmega * d[j] * f[j]; }
+};
+
+// (H_cB v_B) / H_cc of the element with centre grid index ic and element indices (e1, e2, e3)
+template <class Acc>
+__device__ __forceinline__ double hg_centre(const HGridLev& L, const Acc& v, long long ic, int e1, int e2, int e3,
+                                            double lam, double4 E1, double4 E2, double4 E3) {
+  const long long s2 = L.N1, s3 = (long long)L.N1 * L.N2;
+  const double m23 = E2.x * E3.x, m13 = E1.x * E3.x, m12 = E1.x * E2.x;
+  double s = m23 * fma(E1.y, v(ic - 1), E1.z * v(ic + 1));
+  s = fma(m13, fma(E2.y, v(ic - s2), E2.z * v(ic + s2)), s);
+  s = fma(m12, fma(E3.y, v(ic - s3), E3.z * v(ic + s3)), s);
+  const double hcc = fma(lam * E1.x, m23, fma(E1.w, m23, fma(E2.w, m13, E3.w * m12)));
+  return s / hcc;
+}
+
+// (H_hat v)_i at a free grid point i = (g1, g2, g3); v is zero at centres and non-free points
+template <class Acc>
+__device__ __forceinline__ double hg_apply(const HGridLev& L, const Acc& v, long long i, int g1, int g2, int g3,
+                                           double lam) {
+  const int G[3] = {g1, g2, g3};
+  const int N[3] = {L.N1, L.N2, L.N3};
+  const long long s[3] = {1, L.N1, (long long)L.N1 * L.N2};
+  const double B1 = __ldg(&L.b[0][g1]), B2 = __ldg(&L.b[1][g2]), B3 = __ldg(&L.b[2][g3]);
+  const double Bab[3] = {B2 * B3, B1 * B3, B1 * B2};
+  const double v0 = v(i);
+  double q = lam * B1 * Bab[0] * v0;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double* Kr = L.K[d] + 5 * G[d];
+    double acc = __ldg(&Kr[2]) * v0;
+    if (G[d] >= 2) acc = fma(__ldg(&Kr[0]), v(i - 2 * s[d]), acc);
+    if (G[d] >= 1) acc = fma(__ldg(&Kr[1]), v(i - s[d]), acc);
+    if (G[d] + 1 < N[d]) acc = fma(__ldg(&Kr[3]), v(i + s[d]), acc);
+    if (G[d] + 2 < N[d]) acc = fma(__ldg(&Kr[4]), v(i + 2 * s[d]), acc);
+    q = fma(Bab[d], acc, q);
+  }
+  if ((g1 & 1) + (g2 & 1) + (g3 & 1) == 2) {   // face centre: the (up to two) element corrections
+    const int d = (g1 & 1) == 0 ? 0 : ((g2 & 1) == 0 ? 1 : 2);
+    const int Gd = d == 0 ? g1 : (d == 1 ? g2 : g3);
+    const int kd = d == 0 ? L.k1 : (d == 1 ? L.k2 : L.k3);
+    const long long sd = d == 0 ? 1 : (d == 1 ? s[1] : s[2]);
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {   // 0: the element above (i its low face), 1: below
+      const int ed = (Gd >> 1) - side;
+      if (ed < 0 || ed >= kd) continue;
+      const int e1 = d == 0 ? ed : (g1 - 1) >> 1, e2 = d == 1 ? ed : (g2 - 1) >> 1, e3 = d == 2 ? ed : (g3 - 1) >> 1;
+      const double4 E1 = ld_row4(L.E[0], e1);
+      const double4 E2 = ld_row4(L.E[1], e2);
+      const double4 E3 = ld_row4(L.E[2], e3);
+      const long long ic = side ? i - sd : i + sd;
+      const double V = hg_centre(L, v, ic, e1, e2, e3, lam, E1, E2, E3);
+      const double kf = d == 0 ? (side ? E1.z : E1.y) : (d == 1 ? (side ? E2.z : E2.y) : (side ? E3.z : E3.y));
+      const double mab = d == 0 ? E2.x * E3.x : (d == 1 ? E1.x * E3.x : E1.x * E2.x);
+      q = fma(-kf * mab, V, q);
+    }
+  }
+  return q;
+}
+
+// prolongation into fine point (g1, g2, g3) of level F from the coarse level C vector xc
+__device__ __forceinline__ double hg_prolong(const HGridLev& F, const HGridLev& C, const double* xc, int g1, int g2,
+                                             int g3, double lam) {
+  const int ec1 = __ldg(&F.pe[0][g1]), ec2 = __ldg(&F.pe[1][g2]), ec3 = __ldg(&F.pe[2][g3]);
+  const long long cs2 = C.N1, cs3 = (long long)C.N1 * C.N2;
+  const long long cb = 2 * ec1 + cs2 * (2 * ec2) + cs3 * (2 * ec3);
+  double w1[3], w2[3], w3[3];
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    w1[t] = __ldg(&F.pw[0][3 * g1 + t]);
+    w2[t] = __ldg(&F.pw[1][3 * g2 + t]);
+    w3[t] = __ldg(&F.pw[2][3 * g3 + t]);
+  }
+  // centre value: harmonic extension of the coarse element's skeleton values
+  const double4 E1 = ld_row4(C.E[0], ec1);
+  const double4 E2 = ld_row4(C.E[1], ec2);
+  const double4 E3 = ld_row4(C.E[2], ec3);
+  const long long ic = cb + 1 + cs2 + cs3;
+  const double uc = -hg_centre(C, HV{xc}, ic, ec1, ec2, ec3, lam, E1, E2, E3);
   double s = 0.0;
 #pragma unroll
-  for (int k = 0; k < kRowLen; ++k) s = fma(__ldg(&val[k * n + i]), __ldcg(&v[__ldg(&col[k * n + i])]), s);
-  return s;
-}
-
-// one CSR row reduced by a whole warp: lane j takes entries j, j + 32, ... in order, then a fixed
-// xor tree (deterministic); every lane returns the row value.  The transfer rows are up to ~125
-// long (restriction), too long for one thread's dependent load chain.
-__device__ __forceinline__ double csr_row_warp(const int* __restrict__ ptr, const int* __restrict__ col,
-                                               const double* __restrict__ val, long long i,
-                                               const double* __restrict__ v, int lane) {
-  double s = 0.0;
-  const int k1 = __ldg(&ptr[i + 1]);
-  for (int k = __ldg(&ptr[i]) + lane; k < k1; k += 32) s = fma(__ldg(&val[k]), __ldcg(&v[__ldg(&col[k])]), s);
+  for (int c = 0; c < 3; ++c) {
+    double sb = 0.0;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    for (int b = 0; b < 3; ++b) {
+      double sa = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double u = (a == 1 && b == 1 && c == 1) ? uc : xc[cb + a + cs2 * b + cs3 * c];
+        sa = fma(w1[a], u, sa);
+      }
+      sb = fma(w2[b], sa, sb);
+    }
+    s = fma(w3[c], sb, s);
+  }
   return s;
 }
 
-// one CSR row by one thread (the prolongation rows: at most 26 entries, one coarse element's
-// skeleton; a warp per row would leave most lanes idle and serialise the rows)
-__device__ __forceinline__ double csr_row_thread(const int* __restrict__ ptr, const int* __restrict__ col,
-                                                 const double* __restrict__ val, long long i,
-                                                 const double* __restrict__ v) {
+// Restriction R = P^T from level F to level C, tensor-product form in three passes (barriers between):
+//   T1 = (R_1 x I x I) r_f,  T2 = (I x R_2 x I) T1,  T3 = (I x I x R_3) T2  (the transposed 1-D
+// interpolations, <= 7 fine nodes per coarse node), then f_c = E^T T3: a free coarse face centre adds
+// -H_cf / H_cc times T3 at the centres of its (up to two) elements (the transposed harmonic extension).
+__device__ __forceinline__ double hg_dot7(const double* __restrict__ w, int n, const double* v, long long stride) {
   double s = 0.0;
-  const int k1 = __ldg(&ptr[i + 1]);
-  for (int k = __ldg(&ptr[i]); k < k1; ++k) s = fma(__ldg(&val[k]), __ldcg(&v[__ldg(&col[k])]), s);
+#pragma unroll
+  for (int a = 0; a < 7; ++a)
+    if (a < n) s = fma(__ldg(&w[a]), v[a * stride], s);
   return s;
 }
 
-// z = V-cycle(f_0) into h.x[0]; h.f[0] holds the right-hand side.  With rz_part set, the block's
+__device__ __forceinline__ double hg_t3(const HGridLev& F, const HGridLev& C, int J1, int J2, int J3) {
+  const long long plane = (long long)C.N1 * C.N2;
+  const int c0 = __ldg(&F.r0[2][J3]), nc = __ldg(&F.rn[2][J3]);
+  return hg_dot7(F.rw[2] + 7 * J3, nc, F.t2 + J1 + (long long)C.N1 * J2 + plane * c0, plane);
+}
+
+__device__ __forceinline__ double hg_restrict(const HGridLev& F, const HGridLev& C, int J1, int J2, int J3, double lam) {
+  double s = hg_t3(F, C, J1, J2, J3);
+  if ((J1 & 1) + (J2 & 1) + (J3 & 1) == 2) {   // coarse face centre: the centres' harmonic-extension share
+    const int d = (J1 & 1) == 0 ? 0 : ((J2 & 1) == 0 ? 1 : 2);
+    const int Jd = d == 0 ? J1 : (d == 1 ? J2 : J3);
+    const int kd = d == 0 ? C.k1 : (d == 1 ? C.k2 : C.k3);
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const int ed = (Jd >> 1) - side;
+      if (ed < 0 || ed >= kd) continue;
+      const int e1 = d == 0 ? ed : (J1 - 1) >> 1, e2 = d == 1 ? ed : (J2 - 1) >> 1, e3 = d == 2 ? ed : (J3 - 1) >> 1;
+      const double4 E1 = ld_row4(C.E[0], e1);
+      const double4 E2 = ld_row4(C.E[1], e2);
+      const double4 E3 = ld_row4(C.E[2], e3);
+      const double m23 = E2.x * E3.x, m13 = E1.x * E3.x, m12 = E1.x * E2.x;
+      const double hcc = fma(lam * E1.x, m23, fma(E1.w, m23, fma(E2.w, m13, E3.w * m12)));
+      const double kf = d == 0 ? (side ? E1.z : E1.y) : (d == 1 ? (side ? E2.z : E2.y) : (side ? E3.z : E3.y));
+      const double mab = d == 0 ? m23 : (d == 1 ? m13 : m12);
+      s = fma(-(kf * mab) / hcc, hg_t3(F, C, 2 * e1 + 1, 2 * e2 + 1, 2 * e3 + 1), s);
+    }
+  }
+  return s;
+}
+
+// z = V-cycle(f_0) into h.L[0].x; h.L[0].f holds the right-hand side.  With rz_part set, the block's
 // partial of f_0 . z (the CG's r.z) is formed in the last level-0 sweep and published before the
 // V-cycle's final barrier, which then doubles as the CG's reduction barrier.
-__device__ void hmg_vcycle(const HmgDev& h, cg::grid_group& grid, long long t0, long long T,
-                           double* red = nullptr, double* rz_part = nullptr) {
-  const int L = h.nlev - 1;
-  for (int l = 0; l < L; ++l) {
-    const long long n = h.n[l];
-    double *x = h.x[l], *r = h.r[l];
-    const double *f = h.f[l], *di = h.dinv[l];
+__device__ void hg_vcycle(const HmgGridDev& h, cg::grid_group& grid, long long t0, long long T, double lam,
+                          double* red, double* rz_part) {
+  const int Lc = h.nlev - 1;
+  for (int l = 0; l < Lc; ++l) {
+    const HGridLev& L = h.L[l];
+    const long long n = L.n;
     // the two pre-sweeps from zero in one pass: x1 = omega D^-1 f is local, so
     // x2_i = x1_i + omega d_i (f_i - sum_j A_ij x1_j) gathers omega d_j f_j directly
     static_assert(kHmgNu == 2, "the fused sweeps below are written for nu = 2");
     for (long long i = t0; i < n; i += T) {
-      const double* val = h.Aval[l];
-      const int* col = h.Acol[l];
-      double ax = 0.0;
-#pragma unroll
-      for (int k = 0; k < kRowLen; ++k) {
-        const int j = __ldg(&col[k * n + i]);
-        ax = fma(__ldg(&val[k * n + i]), kHmgOmega * __ldg(&di[j]) * __ldcg(&f[j]), ax);
+      int g1, g2, g3;
+      hg_decode(L, i, g1, g2, g3);
+      double xi = 0.0;
+      if (hg_free(L, g1, g2, g3)) {
+        const double wd = kHmgOmega * __ldg(&L.dinv[i]), fi = L.f[i];
+        xi = fma(wd, fi - hg_apply(L, HW{L.dinv, L.f}, i, g1, g2, g3, lam), wd * fi);
       }
-      const double x1 = kHmgOmega * di[i] * f[i];
-      x[i] = fma(kHmgOmega * di[i], f[i] - ax, x1);
+      L.x[i] = xi;
     }
-    grid.sync();
-    for (long long i = t0; i < n; i += T) r[i] = f[i] - ell_row(h.Aval[l], h.Acol[l], n, i, x);
-    grid.sync();
-    const long long nc = h.n[l + 1];
-    for (long long i = t0 >> 5; i < nc; i += T >> 5) {
-      const double v = csr_row_warp(h.Rptr[l], h.Rcol[l], h.Rval[l], i, r, (int)(t0 & 31));
-      if ((t0 & 31) == 0) h.f[l + 1][i] = v;
+    HSYNC(1 + 100 * l);
+    for (long long i = t0; i < n; i += T) {
+      int g1, g2, g3;
+      hg_decode(L, i, g1, g2, g3);
+      L.r[i] = hg_free(L, g1, g2, g3) ? L.f[i] - hg_apply(L, HV{L.x}, i, g1, g2, g3, lam) : 0.0;
     }
-    grid.sync();
+    HSYNC(2 + 100 * l);
+    const HGridLev& C = h.L[l + 1];
+    {   // T1[J1, G2, G3] = sum_a R_1(J1, a) r[a, G2, G3]
+      const long long n1 = (long long)C.N1 * L.N2 * L.N3;
+      for (long long j = t0; j < n1; j += T) {
+        const unsigned row = (unsigned)j / (unsigned)C.N1, J1 = (unsigned)j - row * (unsigned)C.N1;
+        L.t1[j] = hg_dot7(L.rw[0] + 7 * J1, __ldg(&L.rn[0][J1]), L.r + (long long)L.N1 * row + __ldg(&L.r0[0][J1]), 1);
+      }
+    }
+    HSYNC(12 + 100 * l);
+    {   // T2[J1, J2, G3] = sum_b R_2(J2, b) T1[J1, b, G3]
+      const long long n2 = (long long)C.N1 * C.N2 * L.N3;
+      for (long long j = t0; j < n2; j += T) {
+        const unsigned t = (unsigned)j / (unsigned)C.N1, J1 = (unsigned)j - t * (unsigned)C.N1;
+        const unsigned G3 = t / (unsigned)C.N2, J2 = t - G3 * (unsigned)C.N2;
+        L.t2[j] = hg_dot7(L.rw[1] + 7 * J2, __ldg(&L.rn[1][J2]),
+                          L.t1 + J1 + (long long)C.N1 * (__ldg(&L.r0[1][J2]) + (long long)L.N2 * G3), C.N1);
+      }
+    }
+    HSYNC(13 + 100 * l);
+    for (long long j = t0; j < C.n; j += T) {
+      int J1, J2, J3;
+      hg_decode(C, j, J1, J2, J3);
+      C.f[j] = hg_free(C, J1, J2, J3) ? hg_restrict(L, C, J1, J2, J3, lam) : 0.0;
+    }
+    HSYNC(3 + 100 * l);
   }
+  const HGridLev& LC = h.L[Lc];
   if (h.ncf > 0) {                       // coarsest level: x = A^-1 f (dense inverse, warp per row)
     const int lane = (int)(t0 & 31);
     for (long long i = t0 >> 5; i < h.ncf; i += T >> 5) {
       const double* row = h.cinv + i * (long long)h.ncf;
       double s = 0.0;
-      for (int j = lane; j < h.ncf; j += 32) s = fma(__ldg(&row[j]), __ldcg(&h.f[L][__ldg(&h.cidx[j])]), s);
+      for (int j = lane; j < h.ncf; j += 32) s = fma(__ldg(&row[j]), LC.f[__ldg(&h.cidx[j])], s);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) h.x[L][__ldg(&h.cidx[i])] = s;
+      if (lane == 0) LC.x[__ldg(&h.cidx[i])] = s;
     }
   } else if (blockIdx.x == 0) {          // large coarsest level: block 0, Jacobi sweeps, block barriers
-    const long long n = h.n[L];
-    double *x = h.x[L], *r = h.r[L];
-    const double *f = h.f[L], *di = h.dinv[L];
-    for (long long i = threadIdx.x; i < n; i += blockDim.x) x[i] = kHmgOmega * di[i] * f[i];
+    const long long n = LC.n;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) LC.x[i] = kHmgOmega * __ldg(&LC.dinv[i]) * LC.f[i];
     __syncthreads();
-    for (int s = 1; s < kHmgCoarsest; ++s) {
-      for (long long i = threadIdx.x; i < n; i += blockDim.x) r[i] = f[i] - ell_row(h.Aval[L], h.Acol[L], n, i, x);
+    for (int sw = 1; sw < kHmgCoarsest; ++sw) {
+      for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+        int g1, g2, g3;
+        hg_decode(LC, i, g1, g2, g3);
+        LC.r[i] = hg_free(LC, g1, g2, g3) ? LC.f[i] - hg_apply(LC, HV{LC.x}, i, g1, g2, g3, lam) : 0.0;
+      }
       __syncthreads();
-      for (long long i = threadIdx.x; i < n; i += blockDim.x) x[i] = fma(kHmgOmega * di[i], r[i], x[i]);
+      for (long long i = threadIdx.x; i < n; i += blockDim.x) LC.x[i] = fma(kHmgOmega * __ldg(&LC.dinv[i]), LC.r[i], LC.x[i]);
       __syncthreads();
     }
   }
-  grid.sync();
-  for (int l = L - 1; l >= 0; --l) {
-    const long long n = h.n[l];
-    double *x = h.x[l], *r = h.r[l];
-    const double *f = h.f[l], *di = h.dinv[l];
-    for (long long i = t0; i < n; i += T) x[i] += csr_row_thread(h.Pptr[l], h.Pcol[l], h.Pval[l], i, h.x[l + 1]);
-    grid.sync();
+  HSYNC(4);
+  for (int l = Lc - 1; l >= 0; --l) {
+    const HGridLev& L = h.L[l];
+    const HGridLev& C = h.L[l + 1];
+    const long long n = L.n;
+    for (long long i = t0; i < n; i += T) {
+      int g1, g2, g3;
+      hg_decode(L, i, g1, g2, g3);
+      if (hg_free(L, g1, g2, g3)) L.x[i] += hg_prolong(L, C, C.x, g1, g2, g3, lam);
+    }
+    HSYNC(5 + 100 * l);
     // two post-sweeps, each one pass, ping-pong x -> r -> x (r is free here)
-    for (long long i = t0; i < n; i += T) r[i] = fma(kHmgOmega * di[i], f[i] - ell_row(h.Aval[l], h.Acol[l], n, i, x), x[i]);
-    grid.sync();
+    for (long long i = t0; i < n; i += T) {
+      int g1, g2, g3;
+      hg_decode(L, i, g1, g2, g3);
+      double ri = 0.0;
+      if (hg_free(L, g1, g2, g3))
+        ri = fma(kHmgOmega * __ldg(&L.dinv[i]), L.f[i] - hg_apply(L, HV{L.x}, i, g1, g2, g3, lam), L.x[i]);
+      L.r[i] = ri;
+    }
+    HSYNC(6 + 100 * l);
     double srz = 0.0;
     for (long long i = t0; i < n; i += T) {
-      const double xi = fma(kHmgOmega * di[i], f[i] - ell_row(h.Aval[l], h.Acol[l], n, i, r), r[i]);
-      x[i] = xi;
-      srz = fma(f[i], xi, srz);
+      int g1, g2, g3;
+      hg_decode(L, i, g1, g2, g3);
+      double xi = 0.0;
+      if (hg_free(L, g1, g2, g3)) {
+        const double fi = L.f[i];
+        xi = fma(kHmgOmega * __ldg(&L.dinv[i]), fi - hg_apply(L, HV{L.r}, i, g1, g2, g3, lam), L.r[i]);
+        srz = fma(fi, xi, srz);
+      }
+      L.x[i] = xi;
     }
     if (l == 0 && rz_part) block_reduce3(srz, srz, srz, red, blockIdx.x, rz_part, rz_part, rz_part);
-    grid.sync();
+    HSYNC(7 + 100 * l);
   }
-  if (L == 0 && rz_part) {   // a single h-level (the dense solve alone): r.z after it
-    const long long n = h.n[0];
+  if (Lc == 0 && rz_part) {   // a single h-level (the dense solve alone): r.z after it
+    const HGridLev& L = h.L[0];
     double srz = 0.0;
-    for (long long i = t0; i < n; i += T) srz = fma(h.f[0][i], __ldcg(&h.x[0][i]), srz);
+    for (long long i = t0; i < L.n; i += T) srz = fma(L.f[i], L.x[i], srz);
     block_reduce3(srz, srz, srz, red, blockIdx.x, rz_part, rz_part, rz_part);
-    grid.sync();
+    HSYNC(8);
   }
 }
 }  // namespace
 
 // Standard PCG (as mg.pcg / hmg.pcg_hmg): x = 0, r = b, z = M^-1 r, p = z; q = A p, alpha = r.z / p.q,
 // x += alpha p, r -= alpha q, stop at ||r|| <= rtol ||b||, z = M^-1 r, beta = r.z_new / r.z, p = z + beta p.
-// r lives in h.f[0] (the V-cycle's right-hand side), z in h.x[0].
-__global__ void __launch_bounds__(256) k_pcg_hmg_p2(HmgDev h, const double* __restrict__ b, double* __restrict__ xout,
-                                                   double* __restrict__ pv, double* __restrict__ q,
-                                                   double* __restrict__ part, PcgState* st, double rtol, int maxit) {
+// b and xout are skeleton-record vectors of the p0 = 2 level (geometry h.g0); inside, r lives in
+// h.L[0].f (the V-cycle's right-hand side), z in h.L[0].x, x / p / q in the grid arrays X / pv / q.
+__global__ void __launch_bounds__(256, 3) k_pcg_hmg_p2(HmgGridDev h, const double* __restrict__ b, double* __restrict__ xout,
+                                                   double* __restrict__ X, double* __restrict__ pv,
+                                                   double* __restrict__ q, double lam, double* __restrict__ part,
+                                                   PcgState* st, double rtol, int maxit) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[96];
   const int nb = gridDim.x;
-  const long long n = h.n[0];
+  const HGridLev& L0 = h.L[0];
+  const long long n = L0.n;
   const long long T = (long long)gridDim.x * blockDim.x, t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  double* R = h.f[0];
-  double* Z = h.x[0];
+  double* R = L0.f;
+  double* Z = L0.x;
   double *pa = part, *pb = part + nb, *pc = part + 2 * nb;
   double sb = 0.0;
-  for (long long i = t0; i < n; i += T) {
-    const double bi = b[i];
-    xout[i] = 0.0;
+  for (long long i = t0; i < n; i += T) {   // record layout -> grid layout (free points only)
+    int g1, g2, g3;
+    hg_decode(L0, i, g1, g2, g3);
+    const double bi = hg_free(L0, g1, g2, g3) ? b[sidx2(h.g0, g1, g2, g3)] : 0.0;
+    X[i] = 0.0;
     R[i] = bi;
     sb = fma(bi, bi, sb);
   }
   block_reduce3(sb, 0.0, 0.0, red, blockIdx.x, pa, pb, pc);
-  grid.sync();
+  HSYNC(9);
   double bb, d1, d2;
   grid_totals3(pa, pb, pc, nb, red, bb, d1, d2);
   int its = 0, breakdown = 0;
@@ -751,55 +987,53 @@ __global__ void __launch_bounds__(256) k_pcg_hmg_p2(HmgDev h, const double* __re
     // Two grid barriers per iteration besides the V-cycle's: with p_new = z + beta p,
     // q_new = H z + beta q_old, so the direction, the operator application (z is complete after
     // the V-cycle) and p.q share one phase; r.z is reduced inside the V-cycle's last sweep
-    hmg_vcycle(h, grid, t0, T, red, pc);
+    hg_vcycle(h, grid, t0, T, lam, red, pc);
     double rz, pq;
     grid_totals3(pc, pc, pc, nb, red, rz, d1, d2);
-    {
-      double spq = 0.0;
-      for (long long i = t0; i < n; i += T) {
-        const double zi = Z[i];
-        const double qi = ell_row(h.Aval[0], h.Acol[0], n, i, Z);
-        pv[i] = zi;
-        q[i] = qi;
-        spq = fma(zi, qi, spq);
-      }
-      block_reduce3(spq, spq, spq, red, blockIdx.x, pa, pa, pa);
-      grid.sync();
-      grid_totals3(pa, pa, pa, nb, red, pq, d1, d2);
-    }
+    double beta = 0.0;
     for (;;) {
-      if (!(pq > 0.0)) { breakdown = 1; break; }
-      const double alpha = rz / pq;
-      double srr = 0.0;
-      for (long long i = t0; i < n; i += T) {
-        xout[i] = fma(alpha, pv[i], xout[i]);
-        const double ri = fma(-alpha, q[i], R[i]);
-        R[i] = ri;
-        srr = fma(ri, ri, srr);
-      }
-      block_reduce3(srr, srr, srr, red, blockIdx.x, pb, pb, pb);
-      grid.sync();
-      double rr;
-      grid_totals3(pb, pb, pb, nb, red, rr, d1, d2);
-      ++its;
-      if (sqrt(rr) <= rtol * sqrt(bb) || its >= maxit) break;
-      hmg_vcycle(h, grid, t0, T, red, pc);
-      double rzn;
-      grid_totals3(pc, pc, pc, nb, red, rzn, d1, d2);
-      const double beta = rzn / rz;
-      rz = rzn;
       double spq = 0.0;
       for (long long i = t0; i < n; i += T) {
-        const double pvi = fma(beta, pv[i], Z[i]);
-        const double qi = fma(beta, q[i], ell_row(h.Aval[0], h.Acol[0], n, i, Z));
+        int g1, g2, g3;
+        hg_decode(L0, i, g1, g2, g3);
+        const double hz = hg_free(L0, g1, g2, g3) ? hg_apply(L0, HV{Z}, i, g1, g2, g3, lam) : 0.0;
+        const double pvi = its == 0 ? Z[i] : fma(beta, pv[i], Z[i]);
+        const double qi = its == 0 ? hz : fma(beta, q[i], hz);
         pv[i] = pvi;
         q[i] = qi;
         spq = fma(pvi, qi, spq);
       }
       block_reduce3(spq, spq, spq, red, blockIdx.x, pa, pa, pa);
-      grid.sync();
+      HSYNC(10);
       grid_totals3(pa, pa, pa, nb, red, pq, d1, d2);
+      if (!(pq > 0.0)) { breakdown = 1; break; }
+      const double alpha = rz / pq;
+      double srr = 0.0;
+      for (long long i = t0; i < n; i += T) {
+        X[i] = fma(alpha, pv[i], X[i]);
+        const double ri = fma(-alpha, q[i], R[i]);
+        R[i] = ri;
+        srr = fma(ri, ri, srr);
+      }
+      block_reduce3(srr, srr, srr, red, blockIdx.x, pb, pb, pb);
+      HSYNC(11);
+      double rr;
+      grid_totals3(pb, pb, pb, nb, red, rr, d1, d2);
+      ++its;
+      if (sqrt(rr) <= rtol * sqrt(bb) || its >= maxit) break;
+      hg_vcycle(h, grid, t0, T, lam, red, pc);
+      double rzn;
+      grid_totals3(pc, pc, pc, nb, red, rzn, d1, d2);
+      beta = rzn / rz;
+      rz = rzn;
     }
+  }
+  // grid layout -> record layout (every record entry written; outside the box / non-free: 0)
+  const long long nrec = h.g0.nskel;
+  for (long long j = t0; j < nrec; j += T) {
+    const Entry E = decode2(h.g0, j);
+    const bool in = E.g1 <= 2 * h.g0.k1 && E.g2 <= 2 * h.g0.k2 && E.g3 <= 2 * h.g0.k3;
+    xout[j] = in ? X[E.g1 + L0.N1 * ((long long)E.g2 + (long long)L0.N2 * E.g3)] : 0.0;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->its = its;
@@ -893,4 +1127,17 @@ __global__ void __launch_bounds__(256) k_pcg_coop_p2(LevelGeom g, CoarseTabs ct,
   }
 }
 
+
+#ifdef PMG_HMG_TRACE
+// copy the barrier trace (pairs: globaltimer ns, tag) to host memory and reset it; returns the count
+extern "C" int pmg_debug_hmg_trace(unsigned long long* out, int cap) {
+  int n = 0;
+  cudaMemcpyFromSymbol(&n, g_hmg_ntrace, sizeof(int));
+  n = n < cap ? n : cap;
+  cudaMemcpyFromSymbol(out, g_hmg_trace, sizeof(unsigned long long) * 2 * n);
+  const int z = 0;
+  cudaMemcpyToSymbol(g_hmg_ntrace, &z, sizeof(int));
+  return n;
+}
+#endif
 }  // namespace pmg

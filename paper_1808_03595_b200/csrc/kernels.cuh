@@ -81,31 +81,37 @@ __global__ void k_pcg_coop_reg_p2(LevelGeom g, CoarseTabs ct, const double* b, d
                                   const double* dinv, double lam, double* part, PcgState* st, double rtol, int maxit);
 __global__ void k_pcg_gv_p2(LevelGeom g, CoarseTabs ct, const double* b, double* xout, double* mbuf,
                             const double* dinv, double lam, double* part, PcgState* st, double rtol, int maxit);
-// h-multigrid preconditioned coarse CG (reading R16): level 0 is the p0 = 2 coarse system, level
-// l + 1 has half the elements per direction; ELL rows per level, CSR transfers P_l (l <- l+1) and
-// R_l = P_l^T; per-level work vectors x, f, r.
+// h-multigrid preconditioned coarse CG (reading R16): level 0 is the p0 = 2
+// coarse system, level l + 1 the element-merged mesh; every level in p = 2 GRID layout
+// (N_d = 2 k_d + 1 points per direction, x1 fastest; centres and non-free points held at 0).
 constexpr int kMaxHLevels = 8;
-struct HmgDev {
-  int nlev;
-  long long n[kMaxHLevels];
-  const double* Aval[kMaxHLevels];
-  const int* Acol[kMaxHLevels];
-  const double* dinv[kMaxHLevels];
-  double* x[kMaxHLevels];
-  double* f[kMaxHLevels];
-  double* r[kMaxHLevels];
-  const int* Pptr[kMaxHLevels];
-  const int* Pcol[kMaxHLevels];
-  const double* Pval[kMaxHLevels];
-  const int* Rptr[kMaxHLevels];
-  const int* Rcol[kMaxHLevels];
-  const double* Rval[kMaxHLevels];
-  int ncf;                 // coarsest level solved exactly: its free unknowns (0: Jacobi sweeps instead)
-  const int* cidx;         // their skeleton indices
-  const double* cinv;      // dense inverse (ncf x ncf, row-major) of the coarsest condensed operator
+struct HGridLev {
+  int k1, k2, k3, N1, N2, N3, neu;
+  long long n;                  // N1 N2 N3
+  const double* b[3];           // assembled 1-D lumped mass per grid index
+  const double* K[3];           // assembled 1-D stiffness, 5 entries (offsets -2..2) per grid index
+  const double* E[3];           // per element index: {M[1], K[1][0], K[1][2], K[1][1]} (double4)
+  const double* dinv;           // 1 / diag(H_hat) on free points, else 0 (grid)
+  double *x, *f, *r;            // work vectors (grid)
+  // transfer to level l + 1 (unused on the coarsest level)
+  const int* pe[3];             // per fine grid index: coarse element
+  const double* pw[3];          // per fine grid index: the 3 quadratic weights of that element's nodes
+  const int* r0[3];             // per coarse grid index: first fine index with a nonzero weight
+  const int* rn[3];             // ... and the count (<= 7)
+  const double* rw[3];          // ... and the weights (7 per coarse index)
+  double *t1, *t2;              // restriction scratch: N1c N2 N3 and N1c N2c N3 (this level's N2, N3)
 };
-__global__ void k_pcg_hmg_p2(HmgDev h, const double* b, double* xout, double* pv, double* q, double* part, PcgState* st,
-                             double rtol, int maxit);
+struct HmgGridDev {
+  int nlev;
+  HGridLev L[kMaxHLevels];
+  int ncf;                      // coarsest level solved exactly: its free unknowns (0: Jacobi sweeps instead)
+  const int* cidx;              // their grid indices
+  const double* cinv;           // dense inverse (ncf x ncf, row-major) of the coarsest condensed operator
+  LevelGeom g0;                 // record geometry of level 0 (the CG's b / x layout)
+};
+__global__ void k_pcg_hmg_p2(HmgGridDev h, const double* b, double* xout, double* X, double* pv, double* q, double lam,
+                             double* part, PcgState* st, double rtol, int maxit);
+__global__ void k_resid_p2(LevelGeom g, CoarseTabs ct, const double* u, const double* f, double* r, double lam);
 __global__ void k_build_coarse_ell(LevelGeom g, CoarseTabs ct, double lam, int* ellc, double* ella);
 __global__ void k_pcg_gv_ell_p2(long long n, const double* b, double* xout, double* vec, double* mbuf, const double* dinv,
                                 const int* ellc, const double* ella, double* part, PcgState* st, double rtol, int maxit);

@@ -106,10 +106,10 @@ struct pmg_ctx {
   // h-multigrid preconditioned coarse CG (reading R16)
   bool use_hmg = false;
   int hmg_nb = 0;
-  HmgDev hmg{};
+  HmgGridDev hmg{};
   std::vector<HostLevel> hhost;      // h-levels 1.. (level 0 is H[0])
   std::vector<void*> hmg_allocs;     // device buffers owned by the h-hierarchy
-  double *hpv = nullptr, *hq = nullptr;
+  double *hpv = nullptr, *hq = nullptr, *hX = nullptr;   // h-multigrid CG grid vectors p, q, x
   double* ellv = nullptr;    // 8 n0 CG vectors
   double* ctab[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // CoarseTabs storage
   double* cV = nullptr;      // (unused)
@@ -198,6 +198,12 @@ pmg_status exchange(pmg_ctx* c, int l, double* x) {
 pmg_status residual_dev(pmg_ctx* c, int l, const double* u, const double* f, double* r, const int* done = nullptr) {
   const DevLevel& D = c->D[l];
   TimedRegion tr(c, 1, l == c->L);
+  if (D.g.p == 2 && l == 0 && c->ctab[0] && !c->tr && !D.g.per && !done) {   // p = 2: direct stencil form
+    CoarseTabs ct{c->ctab[0], c->ctab[1], c->ctab[2], c->ctab[3], c->ctab[4], c->ctab[5], c->ctab[6]};
+    k_resid_p2<<<grid_for(D.g.nskel), kThreads, 0, c->st>>>(D.g, ct, u, f, r, c->lam);
+    LAUNCH_CHECK(c);
+    return PMG_OK;
+  }
   launch_elem_apply(D.g, u, D.etab, D.etabP, c->lam, c->Y, done, c->st);
   LAUNCH_CHECK(c);
   launch_gather_resid(D.g, c->Y, f, r, done, c->st);
@@ -307,7 +313,7 @@ pmg_status pcg_dev(pmg_ctx* c, const double* b, double* x) {
     void* args_reg[] = {&g0, &ct, (void*)&b, &x, &c->cz, (void*)&dinv, &lam, &part, &st, &rtol, &maxit};
     void* args_gv[] = {&g0, &ct, (void*)&b, &x, &c->cgm, (void*)&dinv, &lam, &part, &st, &rtol, &maxit};
     if (c->use_hmg) {   // CG preconditioned by the h-multigrid V-cycle (reading R16)
-      void* args_h[] = {&c->hmg, (void*)&b, &x, &c->hpv, &c->hq, &part, &st, &rtol, &maxit};
+      void* args_h[] = {&c->hmg, (void*)&b, &x, &c->hX, &c->hpv, &c->hq, &lam, &part, &st, &rtol, &maxit};
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(c->hmg_nb);
       cfg.blockDim = dim3(kThreads);
@@ -703,7 +709,7 @@ void free_ctx(pmg_ctx* c) {
   cudaFree(c->Y); cudaFree(c->Z); cudaFree(c->cube); cudaFree(c->part); cudaFree(c->dres); cudaFree(c->pcg);
   cudaFree(c->cgm); cudaFree(c->ella); cudaFree(c->ellv);
   for (void* a : c->hmg_allocs) cudaFree(a);
-  cudaFree(c->hpv); cudaFree(c->hq);
+  cudaFree(c->hpv); cudaFree(c->hq); cudaFree(c->hX);
   cudaFree(c->cx); cudaFree(c->cr); cudaFree(c->cz); cudaFree(c->cp); cudaFree(c->cq); cudaFree(c->dinv);
   for (int d = 0; d < 3; ++d) cudaFree(c->bm[d]);
   cudaFree(c->Fdev); cudaFree(c->Udev);
@@ -1140,8 +1146,9 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
         hl.push_back(&c->hhost.back());
         for (int d = 0; d < 3; ++d) kl[d] = kn[d];
       }
-      HmgDev& h = c->hmg;
+      HmgGridDev& h = c->hmg;
       h.nlev = (int)hl.size();
+      h.g0 = c->g0g;
       bool ok = true;
       auto dal = [&](double** ptr, size_t cnt) {
         if (!ok || dalloc(ptr, cnt) != cudaSuccess) { ok = false; return; }
@@ -1160,59 +1167,93 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
         if (ok) cudaMemcpy(p_, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice);
         return reinterpret_cast<const int*>(p_);
       };
+      // p = 2 record entry -> (g1, g2, g3) (parities of the record offset, as decode2 on the device)
+      auto rec_point = [](const LevelGeom& g, long long idx, int* G) {
+        const long long rec = idx / 7;
+        const int o = (int)(idx - rec * 7);
+        const long long r2 = rec / g.V1;
+        G[0] = 2 * (int)(rec - r2 * g.V1) + ((0x0E >> o) & 1);
+        G[1] = 2 * (int)(r2 % g.V2) + ((0x15 >> o) & 1);
+        G[2] = 2 * (int)(r2 / g.V2) + ((0x23 >> o) & 1);
+      };
       for (int l = 0; l < h.nlev && ok; ++l) {
         const HostLevel& HL = *hl[l];
-        const long long n = HL.g.nskel;
-        h.n[l] = n;
-        std::vector<double> tabs[7];
+        const LevelGeom& g = HL.g;
+        HGridLev& L = h.L[l];
+        L.k1 = g.k1; L.k2 = g.k2; L.k3 = g.k3;
+        L.N1 = 2 * g.k1 + 1; L.N2 = 2 * g.k2 + 1; L.N3 = 2 * g.k3 + 1;
+        L.neu = o.neumann;
+        L.n = (long long)L.N1 * L.N2 * L.N3;
+        std::vector<double> tabs[7], E[3];
         coarse_tables(HL, lambda, tabs);
-        const double* ct_d[7];
-        for (int i = 0; i < 7; ++i) ct_d[i] = up_d(tabs[i]);
-        double *val = nullptr, *colblk = nullptr;
-        dal(&val, 25 * n);
-        dal(&colblk, (25 * n + 1) / 2);
-        if (!ok) break;
-        CoarseTabs ct{ct_d[0], ct_d[1], ct_d[2], ct_d[3], ct_d[4], ct_d[5], ct_d[6]};
-        k_build_coarse_ell<<<grid_for(n), kThreads>>>(HL.g, ct, lambda, reinterpret_cast<int*>(colblk), val);
-        h.Aval[l] = val;
-        h.Acol[l] = reinterpret_cast<const int*>(colblk);
-        std::vector<double> dg, di;
+        hgrid_elem_rows(HL, E);
+        for (int d = 0; d < 3; ++d) {
+          L.b[d] = up_d(tabs[d]);
+          L.K[d] = up_d(tabs[3 + d]);
+          L.E[d] = up_d(E[d]);
+        }
+        // 1 / diag(H_hat) from the record-layout diagonal, scattered to the grid
+        std::vector<double> dg, di((size_t)L.n, 0.0);
         coarse_diag(HL, lambda, dg);
-        di.resize(dg.size());
-        for (size_t i = 0; i < dg.size(); ++i) di[i] = dg[i] != 0.0 ? 1.0 / dg[i] : 0.0;
-        h.dinv[l] = up_d(di);
-        dal(&h.x[l], n);
-        dal(&h.f[l], n);
-        dal(&h.r[l], n);
+        for (long long i = 0; i < g.nskel; ++i) {
+          if (dg[i] == 0.0) continue;
+          int G[3];
+          rec_point(g, i, G);
+          if (G[0] < L.N1 && G[1] < L.N2 && G[2] < L.N3) di[G[0] + L.N1 * ((long long)G[1] + (long long)L.N2 * G[2])] = 1.0 / dg[i];
+        }
+        L.dinv = up_d(di);
+        dal(&L.x, L.n);
+        dal(&L.f, L.n);
+        dal(&L.r, L.n);
         if (l + 1 < h.nlev) {
-          std::vector<int> Pp, Pc, Rp, Rc;
-          std::vector<double> Pv, Rv;
-          std::string err = build_h_transfer(HL, *hl[l + 1], lambda, o.neumann, Pp, Pc, Pv, Rp, Rc, Rv);
-          if (!err.empty()) { free_ctx(c); return fail(PMG_EINVAL, err); }
-          h.Pptr[l] = up_i(Pp); h.Pcol[l] = up_i(Pc); h.Pval[l] = up_d(Pv);
-          h.Rptr[l] = up_i(Rp); h.Rcol[l] = up_i(Rc); h.Rval[l] = up_d(Rv);
+          const LevelGeom& gc = hl[l + 1]->g;
+          const int kf[3] = {g.k1, g.k2, g.k3}, kc[3] = {gc.k1, gc.k2, gc.k3};
+          for (int d = 0; d < 3; ++d) {
+            std::vector<int> pe, r0, rn;
+            std::vector<double> pw, rw;
+            std::string err = build_h_transfer_1d(kf[d], wl[d][l].data(), kc[d], wl[d][l + 1].data(), pe, pw, r0, rn, rw);
+            if (!err.empty()) { free_ctx(c); return fail(PMG_EINVAL, err); }
+            L.pe[d] = up_i(pe); L.pw[d] = up_d(pw);
+            L.r0[d] = up_i(r0); L.rn[d] = up_i(rn); L.rw[d] = up_d(rw);
+          }
+          dal(&L.t1, (size_t)(2 * gc.k1 + 1) * L.N2 * L.N3);
+          dal(&L.t2, (size_t)(2 * gc.k1 + 1) * (2 * gc.k2 + 1) * L.N3);
         }
       }
       if (ok) {
-        const long long n0h = h.n[0];
-        if (dalloc(&c->hpv, n0h) != cudaSuccess || dalloc(&c->hq, n0h) != cudaSuccess) ok = false;
+        const long long n0h = h.L[0].n;
+        if (dalloc(&c->hpv, n0h) != cudaSuccess || dalloc(&c->hq, n0h) != cudaSuccess ||
+            dalloc(&c->hX, n0h) != cudaSuccess)
+          ok = false;
       }
       // coarsest level: dense inverse over its free unknowns (<= 1500, as the oracle), assembled
-      // from the ELL rows; Cholesky-based inversion on the host
+      // from its ELL rows (built on the device in record layout); Cholesky-based inversion on the host
       h.ncf = 0;
       if (ok) {
         const int Lc = h.nlev - 1;
-        const long long n = h.n[Lc];
-        std::vector<double> val(25 * n), dinvL(n);
+        const HostLevel& HL = *hl[Lc];
+        const long long n = HL.g.nskel;
+        std::vector<double> tabs[7];
+        coarse_tables(HL, lambda, tabs);
+        double* ctd[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+        double *val_d = nullptr, *col_d = nullptr;
+        for (int i = 0; i < 7; ++i) ctd[i] = const_cast<double*>(up_d(tabs[i]));
+        dal(&val_d, 25 * n);
+        dal(&col_d, (25 * n + 1) / 2);
+        std::vector<double> val(25 * n), dg;
         std::vector<int> col(25 * n);
-        cudaDeviceSynchronize();
-        cudaMemcpy(val.data(), h.Aval[Lc], val.size() * sizeof(double), cudaMemcpyDeviceToHost);
-        cudaMemcpy(col.data(), h.Acol[Lc], col.size() * sizeof(int), cudaMemcpyDeviceToHost);
-        cudaMemcpy(dinvL.data(), h.dinv[Lc], n * sizeof(double), cudaMemcpyDeviceToHost);
+        if (ok) {
+          CoarseTabs ct{ctd[0], ctd[1], ctd[2], ctd[3], ctd[4], ctd[5], ctd[6]};
+          k_build_coarse_ell<<<grid_for(n), kThreads>>>(HL.g, ct, lambda, reinterpret_cast<int*>(col_d), val_d);
+          cudaDeviceSynchronize();
+          cudaMemcpy(val.data(), val_d, val.size() * sizeof(double), cudaMemcpyDeviceToHost);
+          cudaMemcpy(col.data(), col_d, col.size() * sizeof(int), cudaMemcpyDeviceToHost);
+        }
+        coarse_diag(HL, lambda, dg);
         std::vector<int> fidx, pos(n, -1);
-        for (long long i = 0; i < n; ++i) if (dinvL[i] != 0.0) { pos[i] = (int)fidx.size(); fidx.push_back((int)i); }
+        for (long long i = 0; i < n; ++i) if (dg[i] != 0.0) { pos[i] = (int)fidx.size(); fidx.push_back((int)i); }
         const int nf = (int)fidx.size();
-        if (nf > 0 && nf <= 1500) {
+        if (ok && nf > 0 && nf <= 1500) {
           std::vector<double> A((size_t)nf * nf, 0.0);
           for (int a = 0; a < nf; ++a)
             for (int kx = 0; kx < 25; ++kx) {
@@ -1248,8 +1289,16 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
               }
               for (int i = 0; i < nf; ++i) inv[(size_t)i * nf + cidx_] = y[i];
             }
+            // record indices -> grid indices of the coarsest level
+            const HGridLev& LC = h.L[Lc];
+            std::vector<int> gidx(nf);
+            for (int a = 0; a < nf; ++a) {
+              int G[3];
+              rec_point(HL.g, fidx[a], G);
+              gidx[a] = (int)(G[0] + LC.N1 * ((long long)G[1] + (long long)LC.N2 * G[2]));
+            }
             h.cinv = up_d(inv);
-            h.cidx = up_i(fidx);
+            h.cidx = up_i(gidx);
             if (ok) h.ncf = nf;
           }
         }
@@ -1261,7 +1310,7 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
         return fail(PMG_ENOMEM, "h-multigrid coarse solver: allocation / setup failed");
       }
       c->hmg_nb = (int)std::min<long long>((long long)per_sm_h * nsm_dev(dev),
-                                           std::max<long long>(1, (h.n[0] + kThreads - 1) / kThreads));
+                                           std::max<long long>(1, (h.L[0].n + kThreads - 1) / kThreads));
       c->hmg_nb = std::min(c->hmg_nb, 2048);
       c->use_hmg = true;
     }

@@ -105,10 +105,11 @@ std::string coarse_diag(const HostLevel& L, double lambda, std::vector<double>& 
 std::string coarse_tables(const HostLevel& L, double lambda, std::vector<double> tabs[7]);
 // 1-D GLL nodes and weights (p >= 1)
 void gll(int p, std::vector<double>& x, std::vector<double>& w);
-// h-multigrid transfer between two p = 2 levels (k_fine = 2 k_coarse): CSR P (fine <- coarse) and
-// R = P^T over skeleton entries (reading R16)
-std::string build_h_transfer(const HostLevel& fine, const HostLevel& coarse, double lambda, int neumann,
-                             std::vector<int>& Pptr, std::vector<int>& Pcol, std::vector<double>& Pval,
-                             std::vector<int>& Rptr, std::vector<int>& Rcol, std::vector<double>& Rval);
+// h-multigrid (reading R16) p = 2 grid-layout tables: per direction the element centre rows
+// {M[1], K[1][0], K[1][2], K[1][1]}, and the 1-D transfer tables between a fine and a coarse line
+std::string hgrid_elem_rows(const HostLevel& L, std::vector<double> E[3]);
+std::string build_h_transfer_1d(int kf, const double* wf, int kc, const double* wc, std::vector<int>& pe,
+                                std::vector<double>& pw, std::vector<int>& r0, std::vector<int>& rn,
+                                std::vector<double>& rw);
 
 }  // namespace pmg

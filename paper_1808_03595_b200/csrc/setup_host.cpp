@@ -486,98 +486,78 @@ std::string coarse_diag(const HostLevel& L, double lambda, std::vector<double>& 
 
 namespace pmg {
 
-// h-multigrid transfer of the p = 2 coarse level (reading R16, oracle/hmg.py::h_prolongation):
-// P = fine free skeleton <- coarse free skeleton; a fine point takes the coarse element's tensor
-// quadratic (GLL nodes -1, 0, 1) at its position, with the coarse element's centre value replaced by
-// its harmonic extension -H_cB u_B / H_cc (static-condensation recovery with zero load).
-// CSR over fine skeleton entries; R = P^T is built by transposition.
-std::string build_h_transfer(const HostLevel& fine, const HostLevel& coarse, double lambda, const int neumann,
-                             std::vector<int>& Pptr, std::vector<int>& Pcol, std::vector<double>& Pval,
-                             std::vector<int>& Rptr, std::vector<int>& Rcol, std::vector<double>& Rval) {
-  const LevelGeom& gf = fine.g;
-  const LevelGeom& gc = coarse.g;
-  if (gf.p != 2 || gc.p != 2) return "h-transfer needs p = 2 levels";
-  const int kf[3] = {gf.k1, gf.k2, gf.k3}, kc[3] = {gc.k1, gc.k2, gc.k3};
-  auto freep = [&](int G, int d, int kel) {
-    return free_1d(G, kel * 2, (neumann >> (2 * d)) & 1, (neumann >> (2 * d + 1)) & 1);
-  };
-  auto quad = [](double xi, double* l) {
-    l[0] = 0.5 * xi * (xi - 1.0);
-    l[1] = 1.0 - xi * xi;
-    l[2] = 0.5 * xi * (xi + 1.0);
-  };
-  std::vector<double> xi2, w2;
-  gll(2, xi2, w2);
-  std::vector<double> Kh = ref_stiffness(2, xi2, w2);
-  std::vector<std::vector<int>> rows((size_t)gf.nskel);
-  std::vector<std::vector<double>> vals((size_t)gf.nskel);
-  const int N[3] = {2 * kf[0], 2 * kf[1], 2 * kf[2]};
-  for (int G3 = 0; G3 <= N[2]; ++G3)
-    for (int G2 = 0; G2 <= N[1]; ++G2)
-      for (int G1 = 0; G1 <= N[0]; ++G1) {
-        const int G[3] = {G1, G2, G3};
-        if ((G1 & 1) && (G2 & 1) && (G3 & 1)) continue;            // element centre: not skeleton
-        if (!(freep(G1, 0, kf[0]) && freep(G2, 1, kf[1]) && freep(G3, 2, kf[2]))) continue;
-        const long long fi = host_skel_index(gf, G1, G2, G3);
-        int ec[3];
-        double l[3][3], M[3][3], K[3][9];
-        for (int d = 0; d < 3; ++d) {
-          const int ratio = kf[d] / kc[d];                                  // 2: merged, 1: kept
-          ec[d] = std::min(G[d] / (2 * ratio), kc[d] - 1);
-          const double xa = coarse.coords[d][2 * ec[d]], xb = coarse.coords[d][2 * ec[d] + 2];
-          quad(2.0 * (fine.coords[d][G[d]] - xa) / (xb - xa) - 1.0, l[d]);
-          const double h = xb - xa;
-          for (int t = 0; t < 3; ++t) M[d][t] = 0.5 * h * w2[t];
-          for (int t = 0; t < 9; ++t) K[d][t] = (2.0 / h) * Kh[t];
-        }
-        // centre row of the coarse element operator (lumped mass: couples only along one line)
-        auto Hc = [&](int s1, int s2, int s3) {
-          const int s[3] = {s1, s2, s3};
-          double v = 0.0;
-          const int nd = (s1 != 1) + (s2 != 1) + (s3 != 1);
-          if (nd == 0) v += lambda * M[0][1] * M[1][1] * M[2][1];
-          for (int d = 0; d < 3; ++d) {
-            bool others = true;
-            for (int e = 0; e < 3; ++e) if (e != d && s[e] != 1) others = false;
-            if (!others) continue;
-            const int da = (d == 0) ? 1 : 0, db = (d == 2) ? 1 : 2;
-            v += K[d][1 * 3 + s[d]] * M[da][1] * M[db][1];
-          }
-          return v;
-        };
-        const double wc = l[0][1] * l[1][1] * l[2][1], hcc = Hc(1, 1, 1);
-        for (int s3 = 0; s3 < 3; ++s3)
-          for (int s2 = 0; s2 < 3; ++s2)
-            for (int s1 = 0; s1 < 3; ++s1) {
-              if (s1 == 1 && s2 == 1 && s3 == 1) continue;
-              const double w = l[0][s1] * l[1][s2] * l[2][s3] + wc * (-Hc(s1, s2, s3) / hcc);
-              if (w == 0.0) continue;
-              const int C1 = 2 * ec[0] + s1, C2 = 2 * ec[1] + s2, C3 = 2 * ec[2] + s3;
-              if (!(freep(C1, 0, kc[0]) && freep(C2, 1, kc[1]) && freep(C3, 2, kc[2]))) continue;
-              rows[fi].push_back((int)host_skel_index(gc, C1, C2, C3));
-              vals[fi].push_back(w);
-            }
-      }
-  Pptr.assign((size_t)gf.nskel + 1, 0);
-  for (long long i = 0; i < gf.nskel; ++i) Pptr[i + 1] = Pptr[i] + (int)rows[i].size();
-  Pcol.resize(Pptr.back());
-  Pval.resize(Pptr.back());
-  for (long long i = 0; i < gf.nskel; ++i)
-    for (size_t k = 0; k < rows[i].size(); ++k) { Pcol[Pptr[i] + k] = rows[i][k]; Pval[Pptr[i] + k] = vals[i][k]; }
-  // R = P^T (rows in increasing fine index within each coarse row: deterministic sums)
-  Rptr.assign((size_t)gc.nskel + 1, 0);
-  for (int c : Pcol) Rptr[c + 1]++;
-  for (long long i = 0; i < gc.nskel; ++i) Rptr[i + 1] += Rptr[i];
-  Rcol.resize(Pcol.size());
-  Rval.resize(Pcol.size());
-  std::vector<int> fill(Rptr.begin(), Rptr.end() - 1);
-  for (long long i = 0; i < gf.nskel; ++i)
-    for (int k = Pptr[i]; k < Pptr[i + 1]; ++k) {
-      const int c = Pcol[k];
-      Rcol[fill[c]] = (int)i;
-      Rval[fill[c]] = Pval[k];
-      fill[c]++;
+// h-multigrid level tables (reading R16), p = 2 GRID layout.
+// Per direction d and element index e: the centre row of the element's 1-D matrices,
+// {M[1], K[1][0], K[1][2], K[1][1]} (physical: M = h/2 w, K = 2/h K_hat).
+std::string hgrid_elem_rows(const HostLevel& L, std::vector<double> E[3]) {
+  const LevelGeom& g = L.g;
+  if (g.p != 2) return "h-level tables need p = 2";
+  const int k[3] = {g.k1, g.k2, g.k3};
+  size_t base = 0;
+  for (int d = 0; d < 3; ++d) {
+    E[d].assign((size_t)4 * k[d], 0.0);
+    for (int e = 0; e < k[d]; ++e) {
+      const double* T = &L.etab[(base + e) * g.ET];
+      E[d][4 * e + 0] = T[et_M(2) + 1];
+      E[d][4 * e + 1] = T[et_K(2) + 3 + 0];
+      E[d][4 * e + 2] = T[et_K(2) + 3 + 2];
+      E[d][4 * e + 3] = T[et_K(2) + 3 + 1];
     }
+    base += k[d];
+  }
+  return "";
+}
+
+// 1-D h-transfer tables of one direction between a fine p = 2 line of kf elements (widths wf) and
+// the coarse line of kc elements (kf = 2 kc: merged pairs, widths wc[e] = wf[2e] + wf[2e+1];
+// kf = kc: kept).  Fine node G lies in coarse element ec = min(G / (2 kf / kc), kc - 1) at local
+// position x (sums of fine widths from the element's left end); its weights are the quadratic
+// Lagrange basis on the coarse element's GLL nodes {-1, 0, 1} at xi = 2 x / wc[ec] - 1
+// (oracle/hmg.py::h_prolongation).  Restriction rows: for coarse node J the contiguous fine range
+// with a nonzero weight W(G, J) (<= 7 nodes), weights in order (exact transpose).
+std::string build_h_transfer_1d(int kf, const double* wf, int kc, const double* wc, std::vector<int>& pe,
+                                std::vector<double>& pw, std::vector<int>& r0, std::vector<int>& rn,
+                                std::vector<double>& rw) {
+  if (!(kf == kc || kf == 2 * kc)) return "h-transfer: k_fine must be k_coarse or 2 k_coarse";
+  const int ratio = kf / kc, nf = 2 * kf + 1, nc = 2 * kc + 1;
+  pe.assign(nf, 0);
+  pw.assign((size_t)3 * nf, 0.0);
+  for (int G = 0; G < nf; ++G) {
+    const int ec = std::min(G / (2 * ratio), kc - 1);
+    const int t = G - 2 * ratio * ec;
+    double x;
+    if (ratio == 2) {
+      const double h1 = wf[2 * ec], h2 = wf[2 * ec + 1];
+      const double pos[5] = {0.0, 0.5 * h1, h1, h1 + 0.5 * h2, h1 + h2};
+      x = pos[t];
+    } else {
+      const double h = wf[ec];
+      const double pos[3] = {0.0, 0.5 * h, h};
+      x = pos[t];
+    }
+    const double xi = 2.0 * x / wc[ec] - 1.0;
+    pe[G] = ec;
+    pw[3 * G + 0] = 0.5 * xi * (xi - 1.0);
+    pw[3 * G + 1] = 1.0 - xi * xi;
+    pw[3 * G + 2] = 0.5 * xi * (xi + 1.0);
+  }
+  r0.assign(nc, 0);
+  rn.assign(nc, 0);
+  rw.assign((size_t)7 * nc, 0.0);
+  auto W = [&](int G, int J) {
+    const int t = J - 2 * pe[G];
+    return (t >= 0 && t <= 2) ? pw[3 * G + t] : 0.0;
+  };
+  for (int J = 0; J < nc; ++J) {
+    int lo = -1, hi = -1;
+    for (int G = 0; G < nf; ++G)
+      if (W(G, J) != 0.0) { if (lo < 0) lo = G; hi = G; }
+    if (lo < 0) continue;
+    if (hi - lo + 1 > 7) return "h-transfer: restriction row longer than 7";
+    r0[J] = lo;
+    rn[J] = hi - lo + 1;
+    for (int G = lo; G <= hi; ++G) rw[(size_t)7 * J + (G - lo)] = W(G, J);
+  }
   return "";
 }
 

@@ -546,6 +546,9 @@ HMG_CASES = {   # coarse levels above the 1500-unknown dense limit: at least two
     "k888_p4_lam0.6": dict(k=(8, 8, 8), p=4, lam=0.6, stretch=1.3, neumann=0),
     "k1688_p2_lam0": dict(k=(16, 8, 8), p=2, lam=0.0, stretch=None, neumann=0),        # L = 0: CG only
     "k884_p4_neu": dict(k=(8, 8, 4), p=4, lam=0.9, stretch=None, neumann=0b110011),
+    # four h-levels (16x16x8 -> 8x8x4 -> 4x4x2 -> 2x2x2, semi-coarsening in x3), stretched widths
+    "k16168_p2_stretch": dict(k=(16, 16, 8), p=2, lam=0.3, stretch=1.2, neumann=0),
+    "k16816_p2_neu": dict(k=(16, 8, 16), p=2, lam=0.0, stretch=1.1, neumann=0b000011),
 }
 
 
