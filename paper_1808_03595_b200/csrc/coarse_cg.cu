@@ -633,6 +633,9 @@ __global__ void __launch_bounds__(256) k_pcg_gv_ell_p2(long long n, const double
 // ------------------------------------------------------------------------------------------
 // experiment builds (-DPMG_HMG_TRACE): block 0 stamps %globaltimer at every grid barrier of the
 // h-multigrid CG (first 8192 barriers of a launch) -> pmg_debug_hmg_trace
+#ifndef PMG_HMG_MINB
+#define PMG_HMG_MINB 2   // blocks per SM of k_pcg_hmg_p2 (register cap 128)
+#endif
 #ifdef PMG_HMG_TRACE
 __device__ unsigned long long g_hmg_trace[2 * 8192];
 __device__ int g_hmg_ntrace;
@@ -675,22 +678,51 @@ __device__ __forceinline__ bool hg_free(const HGridLev& L, int g1, int g2, int g
          free_1d(g3, L.N3 - 1, (L.neu >> 4) & 1, (L.neu >> 5) & 1);
 }
 
+// Point pairs: the grid sweeps below give each thread the two x1-neighbours P0 = (2j, g2, g3) and
+// P1 = (2j + 1, g2, g3) (P1 absent at j = k1).  Both share the x1-line loads, the x2 / x3 tables and
+// the coarse element of the transfers, and the point types of a pair depend on (g2, g3) only, so
+// the lanes of a warp (consecutive j) take the same branch.
+struct HPair {
+  int i0;            // grid index of P0 (h-level grids have < 2^31 points)
+  int j, g2, g3;
+  bool h1, f0, f1;   // P1 exists; P0 / P1 are free unknowns
+};
+
+__device__ __forceinline__ HPair hg_pair(const HGridLev& L, long long ip) {
+  HPair P;
+  const unsigned np1 = (unsigned)L.k1 + 1u;
+  const unsigned u = (unsigned)ip, row = u / np1;
+  P.j = (int)(u - row * np1);
+  P.g3 = (int)(row / (unsigned)L.N2);
+  P.g2 = (int)(row - (unsigned)P.g3 * (unsigned)L.N2);
+  P.i0 = 2 * P.j + L.N1 * (int)row;
+  const int G1 = 2 * P.j;
+  P.h1 = G1 + 1 < L.N1;
+  const bool f23 = free_1d(P.g2, L.N2 - 1, (L.neu >> 2) & 1, (L.neu >> 3) & 1) &&
+                   free_1d(P.g3, L.N3 - 1, (L.neu >> 4) & 1, (L.neu >> 5) & 1);
+  P.f0 = f23 && free_1d(G1, L.N1 - 1, L.neu & 1, (L.neu >> 1) & 1);
+  P.f1 = f23 && P.h1 && !((P.g2 & 1) && (P.g3 & 1));   // odd x1 index: interior along x1; (o, o, o) is a centre
+  return P;
+}
+
+__device__ __forceinline__ long long hg_npairs(const HGridLev& L) { return (long long)(L.k1 + 1) * L.N2 * L.N3; }
+
 // plain vector (written inside the kernel: plain loads, ordered by the grid barriers)
 struct HV {
   const double* p;
-  __device__ __forceinline__ double operator()(long long j) const { return p[j]; }
+  __device__ __forceinline__ double operator()(int j) const { return p[j]; }
 };
 // omega D^-1 f: the first damped-Jacobi sweep from zero, evaluated where the second sweep reads it
 struct HW {
   const double *d, *f;
-  __device__ __forceinline__ double operator()(long long j) const { return kHmgOmega * d[j] * f[j]; }
+  __device__ __forceinline__ double operator()(int j) const { return kHmgOmega * __ldg(&d[j]) * f[j]; }
 };
 
-// (H_cB v_B) / H_cc of the element with centre grid index ic and element indices (e1, e2, e3)
+// (H_cB v_B) / H_cc of the element with centre grid index ic
 template <class Acc>
-__device__ __forceinline__ double hg_centre(const HGridLev& L, const Acc& v, long long ic, int e1, int e2, int e3,
-                                            double lam, double4 E1, double4 E2, double4 E3) {
-  const long long s2 = L.N1, s3 = (long long)L.N1 * L.N2;
+__device__ __forceinline__ double hg_centre(const HGridLev& L, const Acc& v, int ic, double lam, double4 E1,
+                                            double4 E2, double4 E3) {
+  const int s2 = L.N1, s3 = L.N1 * L.N2;
   const double m23 = E2.x * E3.x, m13 = E1.x * E3.x, m12 = E1.x * E2.x;
   double s = m23 * fma(E1.y, v(ic - 1), E1.z * v(ic + 1));
   s = fma(m13, fma(E2.y, v(ic - s2), E2.z * v(ic + s2)), s);
@@ -699,86 +731,148 @@ __device__ __forceinline__ double hg_centre(const HGridLev& L, const Acc& v, lon
   return s / hcc;
 }
 
-// (H_hat v)_i at a free grid point i = (g1, g2, g3); v is zero at centres and non-free points
+// (H_hat v) at the pair's points (values at non-free points are meaningless; callers mask);
+// v is zero at centres and non-free points.  Every load of the pair -- the x1 line, the x2 / x3 lines
+// of both points, the tables and the six neighbours of the (up to two) element centres next to
+// the pair's face centre -- is issued up front with out-of-range indices clamped to i0 (a harmless
+// load whose coefficient is zero), so an application costs one memory round trip, not three.
 template <class Acc>
-__device__ __forceinline__ double hg_apply(const HGridLev& L, const Acc& v, long long i, int g1, int g2, int g3,
-                                           double lam) {
-  const int G[3] = {g1, g2, g3};
-  const int N[3] = {L.N1, L.N2, L.N3};
-  const long long s[3] = {1, L.N1, (long long)L.N1 * L.N2};
-  const double B1 = __ldg(&L.b[0][g1]), B2 = __ldg(&L.b[1][g2]), B3 = __ldg(&L.b[2][g3]);
-  const double Bab[3] = {B2 * B3, B1 * B3, B1 * B2};
-  const double v0 = v(i);
-  double q = lam * B1 * Bab[0] * v0;
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const double* Kr = L.K[d] + 5 * G[d];
-    double acc = __ldg(&Kr[2]) * v0;
-    if (G[d] >= 2) acc = fma(__ldg(&Kr[0]), v(i - 2 * s[d]), acc);
-    if (G[d] >= 1) acc = fma(__ldg(&Kr[1]), v(i - s[d]), acc);
-    if (G[d] + 1 < N[d]) acc = fma(__ldg(&Kr[3]), v(i + s[d]), acc);
-    if (G[d] + 2 < N[d]) acc = fma(__ldg(&Kr[4]), v(i + 2 * s[d]), acc);
-    q = fma(Bab[d], acc, q);
+__device__ __forceinline__ void hg_apply2(const HGridLev& L, const Acc& v, const HPair& P, double lam, double& q0,
+                                          double& q1) {
+  const int i0 = P.i0, s2 = L.N1, s3 = L.N1 * L.N2;
+  const int G1 = 2 * P.j, g2 = P.g2, g3 = P.g3;
+  const bool lo = P.j >= 1, h1 = P.h1, h2 = G1 + 2 < L.N1;
+  auto cl = [&](bool ok, int k) { return ok ? k : i0; };
+  auto cz = [](bool ok, double x) { return ok ? x : 0.0; };
+  // ---- loads ----
+  const double va = v(cl(lo, i0 - 2)), vb = v(cl(lo, i0 - 1)), vc = v(i0), vd = v(cl(h1, i0 + 1)), ve = v(cl(h2, i0 + 2));
+  const bool y0 = g2 >= 2, y1 = g2 >= 1, y3 = g2 + 1 < L.N2, y4 = g2 + 2 < L.N2;
+  const bool z0 = g3 >= 2, z1 = g3 >= 1, z3 = g3 + 1 < L.N3, z4 = g3 + 2 < L.N3;
+  const double a20 = v(cl(y0, i0 - 2 * s2)), a21 = v(cl(y1, i0 - s2)), a23 = v(cl(y3, i0 + s2)), a24 = v(cl(y4, i0 + 2 * s2));
+  const double a30 = v(cl(z0, i0 - 2 * s3)), a31 = v(cl(z1, i0 - s3)), a33 = v(cl(z3, i0 + s3)), a34 = v(cl(z4, i0 + 2 * s3));
+  const int i1 = cl(h1, i0 + 1);
+  const double b20 = v(cl(h1 && y0, i1 - 2 * s2)), b21 = v(cl(h1 && y1, i1 - s2)), b23 = v(cl(h1 && y3, i1 + s2)),
+               b24 = v(cl(h1 && y4, i1 + 2 * s2));
+  const double b30 = v(cl(h1 && z0, i1 - 2 * s3)), b31 = v(cl(h1 && z1, i1 - s3)), b33 = v(cl(h1 && z3, i1 + s3)),
+               b34 = v(cl(h1 && z4, i1 + 2 * s3));
+  // face centre of the pair: kind 1 = P0 (even, odd, odd) normal to x1; 2 = P1 (odd, odd, even) normal to
+  // x3; 3 = P1 (odd, even, odd) normal to x2; 0 = none.  Side 0: the element above, 1: below.
+  const bool o2 = g2 & 1, o3 = g3 & 1;
+  const int kind = (o2 && o3) ? 1 : ((o2 && h1) ? 2 : ((o3 && h1) ? 3 : 0));
+  const int ea = kind == 1 ? (g2 - 1) >> 1 : P.j < L.k1 ? P.j : 0;           // x1 element (kinds 2, 3)
+  const int Gd = kind == 1 ? G1 : (kind == 2 ? g3 : g2);
+  const int kd = kind == 1 ? L.k1 : (kind == 2 ? L.k3 : L.k2);
+  const int sd = kind == 1 ? 1 : (kind == 2 ? s3 : s2);
+  const int fc = kind == 1 ? i0 : i1;                                   // the face centre
+  const bool ok0 = kind != 0 && (Gd >> 1) < kd, ok1 = kind != 0 && (Gd >> 1) >= 1;
+  const int ed0 = ok0 ? (Gd >> 1) : 0, ed1 = ok1 ? (Gd >> 1) - 1 : 0;
+  // tangential element rows: kind 1: x2 and x3; kind 2: x1 and x2; kind 3: x1 and x3
+  const double4 Ta = kind == 1 ? ld_row4(L.E[1], (g2 - 1) >> 1) : ld_row4(L.E[0], ea);
+  const double4 Tb = kind == 2 ? ld_row4(L.E[1], o2 ? (g2 - 1) >> 1 : 0)
+                               : ld_row4(L.E[2], o3 ? (g3 - 1) >> 1 : 0);
+  const double* Ed = L.E[kind == 1 ? 0 : (kind == 2 ? 2 : 1)];
+  const double4 N0 = ld_row4(Ed, ed0), N1 = ld_row4(Ed, ed1);
+  const int c0 = cl(ok0, fc + sd), c1 = cl(ok1, fc - sd);
+  const double u0m1 = v(cl(ok0, c0 - 1)), u0p1 = v(cl(ok0, c0 + 1)), u0m2 = v(cl(ok0, c0 - s2)), u0p2 = v(cl(ok0, c0 + s2)),
+               u0m3 = v(cl(ok0, c0 - s3)), u0p3 = v(cl(ok0, c0 + s3));
+  const double u1m1 = v(cl(ok1, c1 - 1)), u1p1 = v(cl(ok1, c1 + 1)), u1m2 = v(cl(ok1, c1 - s2)), u1p2 = v(cl(ok1, c1 + s2)),
+               u1m3 = v(cl(ok1, c1 - s3)), u1p3 = v(cl(ok1, c1 + s3));
+  const double B2 = __ldg(&L.b[1][g2]), B3 = __ldg(&L.b[2][g3]), B1a = __ldg(&L.b[0][G1]);
+  const double B1b = h1 ? __ldg(&L.b[0][G1 + 1]) : 0.0;
+  const double* K1a = L.K[0] + 5 * G1;
+  const double* K1b = L.K[0] + 5 * (h1 ? G1 + 1 : G1);
+  const double* K2r = L.K[1] + 5 * g2;
+  const double* K3r = L.K[2] + 5 * g3;
+  // ---- arithmetic ----
+  const double B23 = B2 * B3;
+  double x1 = __ldg(&K1a[2]) * vc;
+  x1 = fma(__ldg(&K1a[0]), cz(lo, va), x1);
+  x1 = fma(__ldg(&K1a[1]), cz(lo, vb), x1);
+  x1 = fma(__ldg(&K1a[3]), cz(h1, vd), x1);
+  x1 = fma(__ldg(&K1a[4]), cz(h2, ve), x1);
+  const double k20 = __ldg(&K2r[0]), k21 = __ldg(&K2r[1]), k22 = __ldg(&K2r[2]), k23 = __ldg(&K2r[3]), k24 = __ldg(&K2r[4]);
+  const double k30 = __ldg(&K3r[0]), k31 = __ldg(&K3r[1]), k32 = __ldg(&K3r[2]), k33 = __ldg(&K3r[3]), k34 = __ldg(&K3r[4]);
+  auto line = [&](double c, double m2, double m1, double p1, double p2, double k0, double k1, double k2, double k3,
+                  double k4, bool e0, bool e1, bool e3, bool e4) {
+    double acc = k2 * c;
+    acc = fma(k0, cz(e0, m2), acc);
+    acc = fma(k1, cz(e1, m1), acc);
+    acc = fma(k3, cz(e3, p1), acc);
+    acc = fma(k4, cz(e4, p2), acc);
+    return acc;
+  };
+  q0 = lam * B1a * B23 * vc;
+  q0 = fma(B23, x1, q0);
+  q0 = fma(B1a * B3, line(vc, a20, a21, a23, a24, k20, k21, k22, k23, k24, y0, y1, y3, y4), q0);
+  q0 = fma(B1a * B2, line(vc, a30, a31, a33, a34, k30, k31, k32, k33, k34, z0, z1, z3, z4), q0);
+  const double vdd = cz(h1, vd);
+  double y1s = __ldg(&K1b[2]) * vdd;
+  y1s = fma(__ldg(&K1b[1]), vc, y1s);
+  y1s = fma(__ldg(&K1b[3]), cz(h2, ve), y1s);
+  q1 = lam * B1b * B23 * vdd;
+  q1 = fma(B23, y1s, q1);
+  q1 = fma(B1b * B3, line(vdd, b20, b21, b23, b24, k20, k21, k22, k23, k24, h1 && y0, h1 && y1, h1 && y3, h1 && y4), q1);
+  q1 = fma(B1b * B2, line(vdd, b30, b31, b33, b34, k30, k31, k32, k33, k34, h1 && z0, h1 && z1, h1 && z3, h1 && z4), q1);
+  if (kind != 0) {
+    // element rows in direction order (E1, E2, E3) for the two sides
+    auto corr = [&](const double4& Nn, double um1, double up1, double um2, double up2, double um3, double up3, int side) {
+      const double4 E1 = kind == 1 ? Nn : Ta;
+      const double4 E2 = kind == 1 ? Ta : (kind == 2 ? Tb : Nn);
+      const double4 E3 = kind == 1 ? Tb : (kind == 2 ? Nn : Tb);
+      const double m23 = E2.x * E3.x, m13 = E1.x * E3.x, m12 = E1.x * E2.x;
+      double s = m23 * fma(E1.y, um1, E1.z * up1);
+      s = fma(m13, fma(E2.y, um2, E2.z * up2), s);
+      s = fma(m12, fma(E3.y, um3, E3.z * up3), s);
+      const double hcc = fma(lam * E1.x, m23, fma(E1.w, m23, fma(E2.w, m13, E3.w * m12)));
+      const double mab = kind == 1 ? m23 : (kind == 2 ? m12 : m13);
+      return (side ? Nn.z : Nn.y) * mab * (s / hcc);
+    };
+    double c = 0.0;
+    if (ok0) c += corr(N0, u0m1, u0p1, u0m2, u0p2, u0m3, u0p3, 0);
+    if (ok1) c += corr(N1, u1m1, u1p1, u1m2, u1p2, u1m3, u1p3, 1);
+    if (kind == 1) q0 -= c; else q1 -= c;
   }
-  if ((g1 & 1) + (g2 & 1) + (g3 & 1) == 2) {   // face centre: the (up to two) element corrections
-    const int d = (g1 & 1) == 0 ? 0 : ((g2 & 1) == 0 ? 1 : 2);
-    const int Gd = d == 0 ? g1 : (d == 1 ? g2 : g3);
-    const int kd = d == 0 ? L.k1 : (d == 1 ? L.k2 : L.k3);
-    const long long sd = d == 0 ? 1 : (d == 1 ? s[1] : s[2]);
-#pragma unroll
-    for (int side = 0; side < 2; ++side) {   // 0: the element above (i its low face), 1: below
-      const int ed = (Gd >> 1) - side;
-      if (ed < 0 || ed >= kd) continue;
-      const int e1 = d == 0 ? ed : (g1 - 1) >> 1, e2 = d == 1 ? ed : (g2 - 1) >> 1, e3 = d == 2 ? ed : (g3 - 1) >> 1;
-      const double4 E1 = ld_row4(L.E[0], e1);
-      const double4 E2 = ld_row4(L.E[1], e2);
-      const double4 E3 = ld_row4(L.E[2], e3);
-      const long long ic = side ? i - sd : i + sd;
-      const double V = hg_centre(L, v, ic, e1, e2, e3, lam, E1, E2, E3);
-      const double kf = d == 0 ? (side ? E1.z : E1.y) : (d == 1 ? (side ? E2.z : E2.y) : (side ? E3.z : E3.y));
-      const double mab = d == 0 ? E2.x * E3.x : (d == 1 ? E1.x * E3.x : E1.x * E2.x);
-      q = fma(-kf * mab, V, q);
-    }
-  }
-  return q;
 }
 
-// prolongation into fine point (g1, g2, g3) of level F from the coarse level C vector xc
-__device__ __forceinline__ double hg_prolong(const HGridLev& F, const HGridLev& C, const double* xc, int g1, int g2,
-                                             int g3, double lam) {
-  const int ec1 = __ldg(&F.pe[0][g1]), ec2 = __ldg(&F.pe[1][g2]), ec3 = __ldg(&F.pe[2][g3]);
-  const long long cs2 = C.N1, cs3 = (long long)C.N1 * C.N2;
-  const long long cb = 2 * ec1 + cs2 * (2 * ec2) + cs3 * (2 * ec3);
-  double w1[3], w2[3], w3[3];
+// prolongation into the pair's points of level F from the coarse level C vector xc: the coarse
+// element's quadratic with the centre value replaced by its harmonic extension -H_cB u_B / H_cc
+// (both points lie in the same coarse element)
+__device__ __forceinline__ void hg_prolong2(const HGridLev& F, const HGridLev& C, const double* xc, const HPair& P,
+                                            double lam, double& s0, double& s1) {
+  const int G1 = 2 * P.j;
+  const int ec1 = __ldg(&F.pe[0][G1]), ec2 = __ldg(&F.pe[1][P.g2]), ec3 = __ldg(&F.pe[2][P.g3]);
+  const int cs2 = C.N1, cs3 = C.N1 * C.N2;
+  const int cb = 2 * ec1 + cs2 * (2 * ec2) + cs3 * (2 * ec3);
+  double wa[3], wb[3], w2[3], w3[3];
 #pragma unroll
   for (int t = 0; t < 3; ++t) {
-    w1[t] = __ldg(&F.pw[0][3 * g1 + t]);
-    w2[t] = __ldg(&F.pw[1][3 * g2 + t]);
-    w3[t] = __ldg(&F.pw[2][3 * g3 + t]);
+    wa[t] = __ldg(&F.pw[0][3 * G1 + t]);
+    wb[t] = P.h1 ? __ldg(&F.pw[0][3 * G1 + 3 + t]) : 0.0;
+    w2[t] = __ldg(&F.pw[1][3 * P.g2 + t]);
+    w3[t] = __ldg(&F.pw[2][3 * P.g3 + t]);
   }
-  // centre value: harmonic extension of the coarse element's skeleton values
-  const double4 E1 = ld_row4(C.E[0], ec1);
-  const double4 E2 = ld_row4(C.E[1], ec2);
-  const double4 E3 = ld_row4(C.E[2], ec3);
-  const long long ic = cb + 1 + cs2 + cs3;
-  const double uc = -hg_centre(C, HV{xc}, ic, ec1, ec2, ec3, lam, E1, E2, E3);
-  double s = 0.0;
+  const double4 E1 = ld_row4(C.E[0], ec1), E2 = ld_row4(C.E[1], ec2), E3 = ld_row4(C.E[2], ec3);
+  const double uc = -hg_centre(C, HV{xc}, cb + 1 + cs2 + cs3, lam, E1, E2, E3);
+  s0 = 0.0;
+  s1 = 0.0;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    double sb = 0.0;
+    double t0 = 0.0, t1 = 0.0;
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      double sa = 0.0;
+      double sa = 0.0, sb = 0.0;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         const double u = (a == 1 && b == 1 && c == 1) ? uc : xc[cb + a + cs2 * b + cs3 * c];
-        sa = fma(w1[a], u, sa);
+        sa = fma(wa[a], u, sa);
+        sb = fma(wb[a], u, sb);
       }
-      sb = fma(w2[b], sa, sb);
+      t0 = fma(w2[b], sa, t0);
+      t1 = fma(w2[b], sb, t1);
     }
-    s = fma(w3[c], sb, s);
+    s0 = fma(w3[c], t0, s0);
+    s1 = fma(w3[c], t1, s1);
   }
-  return s;
 }
 
 // Restriction R = P^T from level F to level C, tensor-product form in three passes (barriers between):
@@ -831,25 +925,30 @@ __device__ void hg_vcycle(const HmgGridDev& h, cg::grid_group& grid, long long t
   const int Lc = h.nlev - 1;
   for (int l = 0; l < Lc; ++l) {
     const HGridLev& L = h.L[l];
-    const long long n = L.n;
+    const long long np = hg_npairs(L);
     // the two pre-sweeps from zero in one pass: x1 = omega D^-1 f is local, so
     // x2_i = x1_i + omega d_i (f_i - sum_j A_ij x1_j) gathers omega d_j f_j directly
     static_assert(kHmgNu == 2, "the fused sweeps below are written for nu = 2");
-    for (long long i = t0; i < n; i += T) {
-      int g1, g2, g3;
-      hg_decode(L, i, g1, g2, g3);
-      double xi = 0.0;
-      if (hg_free(L, g1, g2, g3)) {
-        const double wd = kHmgOmega * __ldg(&L.dinv[i]), fi = L.f[i];
-        xi = fma(wd, fi - hg_apply(L, HW{L.dinv, L.f}, i, g1, g2, g3, lam), wd * fi);
+    for (long long ip = t0; ip < np; ip += T) {
+      const HPair P = hg_pair(L, ip);
+      double a0, a1;
+      hg_apply2(L, HW{L.dinv, L.f}, P, lam, a0, a1);
+      {
+        const double wd = kHmgOmega * __ldg(&L.dinv[P.i0]), fi = L.f[P.i0];
+        L.x[P.i0] = P.f0 ? fma(wd, fi - a0, wd * fi) : 0.0;
       }
-      L.x[i] = xi;
+      if (P.h1) {
+        const double wd = kHmgOmega * __ldg(&L.dinv[P.i0 + 1]), fi = L.f[P.i0 + 1];
+        L.x[P.i0 + 1] = P.f1 ? fma(wd, fi - a1, wd * fi) : 0.0;
+      }
     }
     HSYNC(1 + 100 * l);
-    for (long long i = t0; i < n; i += T) {
-      int g1, g2, g3;
-      hg_decode(L, i, g1, g2, g3);
-      L.r[i] = hg_free(L, g1, g2, g3) ? L.f[i] - hg_apply(L, HV{L.x}, i, g1, g2, g3, lam) : 0.0;
+    for (long long ip = t0; ip < np; ip += T) {
+      const HPair P = hg_pair(L, ip);
+      double a0, a1;
+      hg_apply2(L, HV{L.x}, P, lam, a0, a1);
+      L.r[P.i0] = P.f0 ? L.f[P.i0] - a0 : 0.0;
+      if (P.h1) L.r[P.i0 + 1] = P.f1 ? L.f[P.i0 + 1] - a1 : 0.0;
     }
     HSYNC(2 + 100 * l);
     const HGridLev& C = h.L[l + 1];
@@ -890,17 +989,19 @@ __device__ void hg_vcycle(const HmgGridDev& h, cg::grid_group& grid, long long t
       if (lane == 0) LC.x[__ldg(&h.cidx[i])] = s;
     }
   } else if (blockIdx.x == 0) {          // large coarsest level: block 0, Jacobi sweeps, block barriers
-    const long long n = LC.n;
-    for (long long i = threadIdx.x; i < n; i += blockDim.x) LC.x[i] = kHmgOmega * __ldg(&LC.dinv[i]) * LC.f[i];
+    const long long np = hg_npairs(LC);
+    for (long long i = threadIdx.x; i < LC.n; i += blockDim.x) LC.x[i] = kHmgOmega * __ldg(&LC.dinv[i]) * LC.f[i];
     __syncthreads();
     for (int sw = 1; sw < kHmgCoarsest; ++sw) {
-      for (long long i = threadIdx.x; i < n; i += blockDim.x) {
-        int g1, g2, g3;
-        hg_decode(LC, i, g1, g2, g3);
-        LC.r[i] = hg_free(LC, g1, g2, g3) ? LC.f[i] - hg_apply(LC, HV{LC.x}, i, g1, g2, g3, lam) : 0.0;
+      for (long long ip = threadIdx.x; ip < np; ip += blockDim.x) {
+        const HPair P = hg_pair(LC, ip);
+        double a0, a1;
+        hg_apply2(LC, HV{LC.x}, P, lam, a0, a1);
+        LC.r[P.i0] = P.f0 ? LC.f[P.i0] - a0 : 0.0;
+        if (P.h1) LC.r[P.i0 + 1] = P.f1 ? LC.f[P.i0 + 1] - a1 : 0.0;
       }
       __syncthreads();
-      for (long long i = threadIdx.x; i < n; i += blockDim.x) LC.x[i] = fma(kHmgOmega * __ldg(&LC.dinv[i]), LC.r[i], LC.x[i]);
+      for (long long i = threadIdx.x; i < LC.n; i += blockDim.x) LC.x[i] = fma(kHmgOmega * __ldg(&LC.dinv[i]), LC.r[i], LC.x[i]);
       __syncthreads();
     }
   }
@@ -908,34 +1009,43 @@ __device__ void hg_vcycle(const HmgGridDev& h, cg::grid_group& grid, long long t
   for (int l = Lc - 1; l >= 0; --l) {
     const HGridLev& L = h.L[l];
     const HGridLev& C = h.L[l + 1];
-    const long long n = L.n;
-    for (long long i = t0; i < n; i += T) {
-      int g1, g2, g3;
-      hg_decode(L, i, g1, g2, g3);
-      if (hg_free(L, g1, g2, g3)) L.x[i] += hg_prolong(L, C, C.x, g1, g2, g3, lam);
+    const long long np = hg_npairs(L);
+    for (long long ip = t0; ip < np; ip += T) {
+      const HPair P = hg_pair(L, ip);
+      if (!(P.f0 || P.f1)) continue;
+      double s0, s1;
+      hg_prolong2(L, C, C.x, P, lam, s0, s1);
+      if (P.f0) L.x[P.i0] += s0;
+      if (P.f1) L.x[P.i0 + 1] += s1;
     }
     HSYNC(5 + 100 * l);
     // two post-sweeps, each one pass, ping-pong x -> r -> x (r is free here)
-    for (long long i = t0; i < n; i += T) {
-      int g1, g2, g3;
-      hg_decode(L, i, g1, g2, g3);
-      double ri = 0.0;
-      if (hg_free(L, g1, g2, g3))
-        ri = fma(kHmgOmega * __ldg(&L.dinv[i]), L.f[i] - hg_apply(L, HV{L.x}, i, g1, g2, g3, lam), L.x[i]);
-      L.r[i] = ri;
+    for (long long ip = t0; ip < np; ip += T) {
+      const HPair P = hg_pair(L, ip);
+      double a0, a1;
+      hg_apply2(L, HV{L.x}, P, lam, a0, a1);
+      L.r[P.i0] = P.f0 ? fma(kHmgOmega * __ldg(&L.dinv[P.i0]), L.f[P.i0] - a0, L.x[P.i0]) : 0.0;
+      if (P.h1) L.r[P.i0 + 1] = P.f1 ? fma(kHmgOmega * __ldg(&L.dinv[P.i0 + 1]), L.f[P.i0 + 1] - a1, L.x[P.i0 + 1]) : 0.0;
     }
     HSYNC(6 + 100 * l);
     double srz = 0.0;
-    for (long long i = t0; i < n; i += T) {
-      int g1, g2, g3;
-      hg_decode(L, i, g1, g2, g3);
-      double xi = 0.0;
-      if (hg_free(L, g1, g2, g3)) {
-        const double fi = L.f[i];
-        xi = fma(kHmgOmega * __ldg(&L.dinv[i]), fi - hg_apply(L, HV{L.r}, i, g1, g2, g3, lam), L.r[i]);
-        srz = fma(fi, xi, srz);
+    for (long long ip = t0; ip < np; ip += T) {
+      const HPair P = hg_pair(L, ip);
+      double a0, a1;
+      hg_apply2(L, HV{L.r}, P, lam, a0, a1);
+      double x0 = 0.0, x1 = 0.0;
+      if (P.f0) {
+        const double fi = L.f[P.i0];
+        x0 = fma(kHmgOmega * __ldg(&L.dinv[P.i0]), fi - a0, L.r[P.i0]);
+        srz = fma(fi, x0, srz);
       }
-      L.x[i] = xi;
+      if (P.f1) {
+        const double fi = L.f[P.i0 + 1];
+        x1 = fma(kHmgOmega * __ldg(&L.dinv[P.i0 + 1]), fi - a1, L.r[P.i0 + 1]);
+        srz = fma(fi, x1, srz);
+      }
+      L.x[P.i0] = x0;
+      if (P.h1) L.x[P.i0 + 1] = x1;
     }
     if (l == 0 && rz_part) block_reduce3(srz, srz, srz, red, blockIdx.x, rz_part, rz_part, rz_part);
     HSYNC(7 + 100 * l);
@@ -954,7 +1064,7 @@ __device__ void hg_vcycle(const HmgGridDev& h, cg::grid_group& grid, long long t
 // x += alpha p, r -= alpha q, stop at ||r|| <= rtol ||b||, z = M^-1 r, beta = r.z_new / r.z, p = z + beta p.
 // b and xout are skeleton-record vectors of the p0 = 2 level (geometry h.g0); inside, r lives in
 // h.L[0].f (the V-cycle's right-hand side), z in h.L[0].x, x / p / q in the grid arrays X / pv / q.
-__global__ void __launch_bounds__(256, 3) k_pcg_hmg_p2(HmgGridDev h, const double* __restrict__ b, double* __restrict__ xout,
+__global__ void __launch_bounds__(256, PMG_HMG_MINB) k_pcg_hmg_p2(HmgGridDev h, const double* __restrict__ b, double* __restrict__ xout,
                                                    double* __restrict__ X, double* __restrict__ pv,
                                                    double* __restrict__ q, double lam, double* __restrict__ part,
                                                    PcgState* st, double rtol, int maxit) {
@@ -962,7 +1072,7 @@ __global__ void __launch_bounds__(256, 3) k_pcg_hmg_p2(HmgGridDev h, const doubl
   __shared__ double red[96];
   const int nb = gridDim.x;
   const HGridLev& L0 = h.L[0];
-  const long long n = L0.n;
+  const long long n = L0.n, np = hg_npairs(L0);
   const long long T = (long long)gridDim.x * blockDim.x, t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   double* R = L0.f;
   double* Z = L0.x;
@@ -993,15 +1103,21 @@ __global__ void __launch_bounds__(256, 3) k_pcg_hmg_p2(HmgGridDev h, const doubl
     double beta = 0.0;
     for (;;) {
       double spq = 0.0;
-      for (long long i = t0; i < n; i += T) {
-        int g1, g2, g3;
-        hg_decode(L0, i, g1, g2, g3);
-        const double hz = hg_free(L0, g1, g2, g3) ? hg_apply(L0, HV{Z}, i, g1, g2, g3, lam) : 0.0;
-        const double pvi = its == 0 ? Z[i] : fma(beta, pv[i], Z[i]);
-        const double qi = its == 0 ? hz : fma(beta, q[i], hz);
-        pv[i] = pvi;
-        q[i] = qi;
-        spq = fma(pvi, qi, spq);
+      for (long long ip = t0; ip < np; ip += T) {
+        const HPair P = hg_pair(L0, ip);
+        double a0, a1;
+        hg_apply2(L0, HV{Z}, P, lam, a0, a1);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          if (k == 1 && !P.h1) break;
+          const long long i = P.i0 + k;
+          const double hz = (k ? P.f1 : P.f0) ? (k ? a1 : a0) : 0.0;
+          const double pvi = its == 0 ? Z[i] : fma(beta, pv[i], Z[i]);
+          const double qi = its == 0 ? hz : fma(beta, q[i], hz);
+          pv[i] = pvi;
+          q[i] = qi;
+          spq = fma(pvi, qi, spq);
+        }
       }
       block_reduce3(spq, spq, spq, red, blockIdx.x, pa, pa, pa);
       HSYNC(10);
@@ -1009,11 +1125,21 @@ __global__ void __launch_bounds__(256, 3) k_pcg_hmg_p2(HmgGridDev h, const doubl
       if (!(pq > 0.0)) { breakdown = 1; break; }
       const double alpha = rz / pq;
       double srr = 0.0;
-      for (long long i = t0; i < n; i += T) {
-        X[i] = fma(alpha, pv[i], X[i]);
-        const double ri = fma(-alpha, q[i], R[i]);
-        R[i] = ri;
-        srr = fma(ri, ri, srr);
+      for (long long i = t0; i < n; i += 4 * T) {   // four points per thread in flight
+        double xv[4], pvv[4], qv[4], rv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const long long ik = i + k * T < n ? i + k * T : i;
+          xv[k] = X[ik]; pvv[k] = pv[ik]; qv[k] = q[ik]; rv[k] = R[ik];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (i + k * T >= n) break;
+          X[i + k * T] = fma(alpha, pvv[k], xv[k]);
+          const double ri = fma(-alpha, qv[k], rv[k]);
+          R[i + k * T] = ri;
+          srr = fma(ri, ri, srr);
+        }
       }
       block_reduce3(srr, srr, srr, red, blockIdx.x, pb, pb, pb);
       HSYNC(11);

@@ -1005,6 +1005,31 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
   if (e6 == cudaSuccess) e6 = elem16_set_smem_attr();
   if (e6 == cudaSuccess) e6 = cr16_set_smem_attr();
   if (e1 || e2 || e3 || e4 || e5 || e6) { free_ctx(c); return fail(PMG_ECUDA, "cudaFuncSetAttribute failed"); }
+  // the h-multigrid coarse solver (below) is chosen from the mesh alone: when it will run, the
+  // ELL rows of the Jacobi-PCG (and their L2 set-aside, which slows every other streaming kernel)
+  // are not built
+  auto hmg_choice = [&](bool& want, bool& coarsenable0) {
+    const LevelGeom& g0 = c->g0g;
+    const int k0[3] = {g0.k1, g0.k2, g0.k3};
+    auto halvable = [](int kd) { return kd % 2 == 0 && kd / 2 >= 2; };
+    coarsenable0 = halvable(k0[0]) || halvable(k0[1]) || halvable(k0[2]);
+    const long long ne0 = (long long)k0[0] * k0[1] * k0[2];
+    // automatic choice: a large coarse system whose Jacobi-PCG iteration count grows with the mesh,
+    // i.e. not mass dominated: lambda L_min^2 < 100 (L_min the shortest box edge; config 4's
+    // lambda = 100 on (0, 2 pi) converges in ~45 Jacobi-PCG iterations and stays on Jacobi)
+    double Lmin = 1e300;
+    for (int d = 0; d < 3; ++d) {
+      double Ld = 0.0;
+      for (int e = 0; e < n_e[d]; ++e) Ld += widths[d][e];
+      Lmin = std::min(Lmin, Ld);
+    }
+    const bool grid_fits = (long long)(2 * k0[0] + 1) * (2 * k0[1] + 1) * (2 * k0[2] + 1) < (1LL << 31);   // int grid indices
+    want = c->D[0].g.p == 2 && !o.periodic && grid_fits &&
+           (o.coarse_solver == 2 ||
+            (o.coarse_solver == 0 && ne0 > 12288 && coarsenable0 && lambda * Lmin * Lmin < 100.0));
+  };
+  bool hmg_want = false, hmg_coarsenable = false;
+  hmg_choice(hmg_want, hmg_coarsenable);
   // persistent cooperative coarse CG when the coarse degree is 2 and the device supports it
   {
     int coop = 0, nsm = 0, per_sm = 0;
@@ -1047,7 +1072,7 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
         int per_sm_ell = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_ell, k_pcg_gv_ell_p2, kThreads, 0);
         const char* le = std::getenv("PMG_COARSE_ELL");
-        if (!c->coop_gv && !(le && le[0] == '0') && per_sm_ell > 0) {
+        if (!c->coop_gv && !hmg_want && !(le && le[0] == '0') && per_sm_ell > 0) {
           const long long n0e = c->g0g.nskel;
           if (dalloc(&c->ella, 25 * n0e + (25 * n0e + 1) / 2) == cudaSuccess &&
               dalloc(&c->ellv, 8 * n0e) == cudaSuccess && (c->cgm || dalloc(&c->cgm, 2 * n0e) == cudaSuccess)) {
@@ -1096,20 +1121,8 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
     const int k0[3] = {g0.k1, g0.k2, g0.k3};
     auto halvable = [](int kd) { return kd % 2 == 0 && kd / 2 >= 2; };
     auto coarsenable = [&](const int* k) { return halvable(k[0]) || halvable(k[1]) || halvable(k[2]); };
-    const long long ne0 = (long long)k0[0] * k0[1] * k0[2];
-    // automatic choice: a large coarse system whose Jacobi-PCG iteration count grows with the mesh,
-    // i.e. not mass dominated: lambda L_min^2 < 100 (L_min the shortest box edge; config 4's
-    // lambda = 100 on (0, 2 pi) converges in ~45 Jacobi-PCG iterations and stays on Jacobi)
-    double Lmin = 1e300;
-    for (int d = 0; d < 3; ++d) {
-      double Ld = 0.0;
-      for (int e = 0; e < n_e[d]; ++e) Ld += widths[d][e];
-      Lmin = std::min(Lmin, Ld);
-    }
-    const bool want = c->use_coop && c->D[0].g.p == 2 &&
-                      (o.coarse_solver == 2 ||
-                       (o.coarse_solver == 0 && ne0 > 12288 && coarsenable(k0) && lambda * Lmin * Lmin < 100.0));
-    if (o.coarse_solver == 2 && !(c->use_coop && coarsenable(k0))) {
+    const bool want = c->use_coop && hmg_want;
+    if (o.coarse_solver == 2 && !(c->use_coop && hmg_coarsenable)) {
       free_ctx(c);
       return fail(PMG_EINVAL, "coarse_solver = 2 needs p0 = 2 and some k_d even with k_d / 2 >= 2");
     }

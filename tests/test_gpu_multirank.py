@@ -185,6 +185,12 @@ def test_operators_and_vcycle_bitwise(name, nr):
             want = ref[key].reshape(-1, P)[sl["zb"]:sl["z1"] + 1]
             got = val.reshape(-1, P)
             # every local plane, ghosts included, is refreshed after each call
+            if key == ("res", 0) or (key == "vcycle" and L == 0):
+                # one GPU evaluates the p0 = 2 residual with the direct line-stencil kernel (k_resid_p2),
+                # z-slabs with the element kernel: the same operator, another summation order (at L = 0
+                # the V-cycle starts from that residual)
+                assert np.allclose(got, want, rtol=0, atol=1e-13 * np.abs(want).max()), (key, sl)
+                continue
             assert np.array_equal(got, want), (key, sl, np.abs(got - want).max())
 
 
@@ -237,7 +243,10 @@ def test_nccl_transport_single_rank(name, solver):
     rep2 = s.solve(torch.from_numpy(F_np).cuda(), u, 1e-10)      # graph replay
     torch.cuda.synchronize()
     assert rep["cycles"] == rep1["cycles"] == rep2["cycles"]
-    assert torch.equal(u, u1)
+    if case.p == 2:   # one GPU: the p0 = 2 stopping residual by k_resid_p2 (another summation order)
+        assert (u - u1).abs().max().item() <= 1e-13 * u1.abs().max().item()
+    else:
+        assert torch.equal(u, u1)
     s.close()
 
 
