@@ -1081,9 +1081,11 @@ pmg_status pmg_setup(pmg_ctx** out, const int n_e[3], const double* const widths
             int maxp = 0, maxwin = 0;
             cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
             cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-            const char* np_ = std::getenv("PMG_NO_L2PERSIST");
+            // opt-in (PMG_L2PERSIST=1): the set-aside speeds the coarse CG up but slows every other
+            // streaming kernel of the solve more (config 4: 61.8 vs 60.4 ms per solve)
+            const char* np_ = std::getenv("PMG_L2PERSIST");
             const size_t rows = sizeof(double) * (size_t)(25 * n0e + (25 * n0e + 1) / 2);
-            if (maxp > 0 && maxwin > 0 && !(np_ && np_[0] == '1')) {
+            if (maxp > 0 && maxwin > 0 && np_ && np_[0] == '1') {
               size_t cur = 0;
               cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
               const size_t want = std::min<size_t>((size_t)maxp, rows);
