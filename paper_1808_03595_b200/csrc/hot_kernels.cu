@@ -652,13 +652,15 @@ __global__ void __launch_bounds__(StarPfCfg<P>::NT, StarPfCfg<P>::MINB)
 //     swapped indices.
 // ------------------------------------------------------------------------------------------
 template <int P> struct ElemPfCfg {
-  static constexpr int M = P - 1, Q = P + 1, MM = M * M, QQ = Q * Q, QQQ = Q * QQ, MP = 8, LD = 12, MS = MP * LD;
+  // p <= 4: direct m x m face transforms, tight m x m arrays; p > 4: 8 x 8 DMMA tiles (leading dim 12)
+  static constexpr int M = P - 1, Q = P + 1, MM = M * M, QQ = Q * Q, QQQ = Q * QQ, MP = 8, LD = (P <= 4) ? M : 12,
+                       MS = (P <= 4) ? MM : MP * LD, NPP = (P <= 4) ? 0 : 3 * MS;
   // p = 2: 26 outputs per element -- two warps per element (measured: 8 % faster on 2 M elements;
   // at p = 3, 4 the 128-thread block is as fast or faster)
   static constexpr int NT = (P <= 2) ? 64 : 128, NW = NT / 32, MINB = (P <= 2) ? 16 : 8;
   static constexpr int ET = (P - 1) + 2 * (P - 1) * (P - 1) + 2 * (P - 1) + (P + 1) + (P + 1) * (P + 1);
   static constexpr int YS = 6 * MM + 12 * M + 8;
-  static constexpr int oCube = 0, oTab = QQQ, oPp = oTab + 3 * ET, oA = oPp + 3 * MS, oT = oA + 6 * MS,
+  static constexpr int oCube = 0, oTab = QQQ, oPp = oTab + 3 * ET, oA = oPp + NPP, oT = oA + 6 * MS,
                        oG = oT + 6 * MS, oInv = oG + 6 * MS, oMap = oInv + MM * M, total = oMap + (YS + 1) / 2;
 };
 
@@ -733,23 +735,49 @@ __global__ void __launch_bounds__(ElemPfCfg<P>::NT, ElemPfCfg<P>::MINB)
       const int a3 = i / MM, rr = i - a3 * MM, a2 = rr / M, a1 = rr - a2 * M;
       cube[((a3 + 1) * Q + a2 + 1) * Q + a1 + 1] = 0.0;
     }
-    for (int i = tid; i < 6 * MS; i += NT) G[i] = 0.0;
+    if constexpr (P > 4)
+      for (int i = tid; i < 6 * MS; i += NT) G[i] = 0.0;
     cp_async_wait<0>();
     __syncthreads();
   }
   const double* Lv[3] = {tb + et_lam(P), tb + ET + et_lam(P), tb + 2 * ET + et_lam(P)};
+  // the face interior value (A, B) of face f in the zero-interior cube
+  auto face_pt = [&](int f, int A, int B) {
+    const int d = f >> 1, sd = (f & 1) * P;
+    return (d == 0) ? ((A + 1) * Q + B + 1) * Q + sd : ((d == 1) ? ((A + 1) * Q + sd) * Q + B + 1 : (sd * Q + A + 1) * Q + B + 1);
+  };
+  if constexpr (P <= 4) {
+    // m <= 3: the face transforms as direct m x m products from the table rows (the padded 8 x 8
+    // DMMA tiles of p > 4 would be > 85 % zeros, and their staging made the kernel shared-memory bound)
+    for (int i = tid; i < 6 * MM; i += NT) {        // X_f[A][ba] = sum_B U_f[A][B] P_a[ba][B]  (into T)
+      const int f = i / MM, r = i - f * MM, A = r / M, ba = r - A * M, d = f >> 1, da = (d == 0) ? 1 : 0;
+      const double* Pa = tb + da * ET + et_P(P) + ba * M;
+      double x = 0.0;
+#pragma unroll
+      for (int B = 0; B < M; ++B) x = fma(cube[face_pt(f, A, B)], Pa[B], x);
+      T[f * MS + A * LD + ba] = x;
+    }
+    for (int i = tid; i < MM * M; i += NT) {        // 1/D over the interior eigen-triples
+      const int b3 = i / MM, rr = i - b3 * MM, b2 = rr / M, b1 = rr - b2 * M;
+      invD[i] = rcp_nr(lam + Lv[0][b1] + Lv[1][b2] + Lv[2][b3]);
+    }
+    __syncthreads();
+    for (int i = tid; i < 6 * MM; i += NT) {        // T_f[bb][ba] = sum_A P_b[bb][A] X_f[A][ba]  (into Ab)
+      const int f = i / MM, r = i - f * MM, bb = r / M, ba = r - bb * M, d = f >> 1, db = (d == 2) ? 1 : 2;
+      const double* Pb = tb + db * ET + et_P(P) + bb * M;
+      double t = 0.0;
+#pragma unroll
+      for (int A = 0; A < M; ++A) t = fma(Pb[A], T[f * MS + A * LD + ba], t);
+      Ab[f * MS + bb * LD + ba] = t;
+    }
+  } else {
   for (int i = tid; i < 3 * MP * MP; i += NT) {     // padded P_d[b][i]
     const int d = i / (MP * MP), rr = i - d * MP * MP, A = rr / MP, B = rr - A * MP;
     Pp[d * MS + A * LD + B] = (A < M && B < M) ? tb[d * ET + et_P(P) + A * M + B] : 0.0;
   }
   for (int i = tid; i < 6 * MP * MP; i += NT) {     // padded face interiors from the cube
-    const int f = i / (MP * MP), rr = i - f * MP * MP, A = rr / MP, B = rr - A * MP, d = f >> 1, sd = (f & 1) * P;
-    double v = 0.0;
-    if (A < M && B < M) {
-      const int t = (d == 0) ? ((A + 1) * Q + B + 1) * Q + sd : ((d == 1) ? ((A + 1) * Q + sd) * Q + B + 1 : (sd * Q + A + 1) * Q + B + 1);
-      v = cube[t];
-    }
-    Ab[f * MS + A * LD + B] = v;
+    const int f = i / (MP * MP), rr = i - f * MP * MP, A = rr / MP, B = rr - A * MP;
+    Ab[f * MS + A * LD + B] = (A < M && B < M) ? cube[face_pt(f, A, B)] : 0.0;
   }
   for (int i = tid; i < MM * M; i += NT) {          // 1/D over the interior eigen-triples
     const int b3 = i / MM, rr = i - b3 * MM, b2 = rr / M, b1 = rr - b2 * M;
@@ -764,6 +792,7 @@ __global__ void __launch_bounds__(ElemPfCfg<P>::NT, ElemPfCfg<P>::MINB)
   for (int f = warp; f < 6; f += C::NW) {            // forward B: T_f = P_b X_f  (into Ab)
     const int d = f >> 1, db = (d == 2) ? 1 : 2;
     dmma_tile_t<MP, LD, false, false>(Pp + db * MS, T + f * MS, Ab + f * MS, 0, 0, lane);
+  }
   }
   __syncthreads();
   {
@@ -829,6 +858,25 @@ __global__ void __launch_bounds__(ElemPfCfg<P>::NT, ElemPfCfg<P>::MINB)
     }
   }
   __syncthreads();
+  if constexpr (P <= 4) {
+    for (int i = tid; i < 6 * MM; i += NT) {        // X_f[bb][B] = sum_ba G_f[bb][ba] P_a[ba][B]  (into T)
+      const int f = i / MM, r = i - f * MM, bb = r / M, B = r - bb * M, d = f >> 1, da = (d == 0) ? 1 : 0;
+      const double* Pa = tb + da * ET + et_P(P) + B;
+      double x = 0.0;
+#pragma unroll
+      for (int ba = 0; ba < M; ++ba) x = fma(G[f * MS + bb * LD + ba], Pa[ba * M], x);
+      T[f * MS + bb * LD + B] = x;
+    }
+    __syncthreads();
+    for (int i = tid; i < 6 * MM; i += NT) {        // C_f[A][B] = sum_bb P_b[bb][A] X_f[bb][B]  (into G)
+      const int f = i / MM, r = i - f * MM, A = r / M, B = r - A * M, d = f >> 1, db = (d == 2) ? 1 : 2;
+      const double* Pb = tb + db * ET + et_P(P) + A;
+      double c = 0.0;
+#pragma unroll
+      for (int bb = 0; bb < M; ++bb) c = fma(Pb[bb * M], T[f * MS + bb * LD + B], c);
+      G[f * MS + A * LD + B] = c;
+    }
+  } else {
   for (int f = warp; f < 6; f += C::NW) {            // back A: X_f = G_f P_a   (into T)
     const int d = f >> 1, da = (d == 0) ? 1 : 0;
     dmma_tile_t<MP, LD, false, false>(G + f * MS, Pp + da * MS, T + f * MS, 0, 0, lane);
@@ -837,6 +885,7 @@ __global__ void __launch_bounds__(ElemPfCfg<P>::NT, ElemPfCfg<P>::MINB)
   for (int f = warp; f < 6; f += C::NW) {            // back B: C_f = P_b^T X_f  (into G)
     const int d = f >> 1, db = (d == 2) ? 1 : 2;
     dmma_tile_t<MP, LD, true, false>(Pp + db * MS, T + f * MS, G + f * MS, 0, 0, lane);
+  }
   }
   __syncthreads();
   const double *M1 = tb + et_M(P), *M2 = tb + ET + et_M(P), *M3 = tb + 2 * ET + et_M(P);
