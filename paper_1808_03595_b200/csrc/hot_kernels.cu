@@ -655,9 +655,8 @@ template <int P> struct ElemPfCfg {
   // p <= 4: direct m x m face transforms, tight m x m arrays; p > 4: 8 x 8 DMMA tiles (leading dim 12)
   static constexpr int M = P - 1, Q = P + 1, MM = M * M, QQ = Q * Q, QQQ = Q * QQ, MP = 8, LD = (P <= 4) ? M : 12,
                        MS = (P <= 4) ? MM : MP * LD, NPP = (P <= 4) ? 0 : 3 * MS;
-  // p = 2: 26 outputs per element -- two warps per element (measured: 8 % faster on 2 M elements;
-  // at p = 3, 4 the 128-thread block is as fast or faster)
-  static constexpr int NT = (P <= 2) ? 64 : 128, NW = NT / 32, MINB = (P <= 2) ? 16 : 8;
+  // p <= 4: two warps per element (with the direct transforms: p = 4 residual 1.12 -> 1.00 ms)
+  static constexpr int NT = (P <= 4) ? 64 : 128, NW = NT / 32, MINB = (NT == 64) ? 16 : 8;
   static constexpr int ET = (P - 1) + 2 * (P - 1) * (P - 1) + 2 * (P - 1) + (P + 1) + (P + 1) * (P + 1);
   static constexpr int YS = 6 * MM + 12 * M + 8;
   static constexpr int oCube = 0, oTab = QQQ, oPp = oTab + 3 * ET, oA = oPp + NPP, oT = oA + 6 * MS,
@@ -1284,6 +1283,12 @@ __global__ void __launch_bounds__(128) k_star_w(LevelGeom g, int c1, int c2, int
 // one thread per record slot.  Same sums in the same order as k_gather_resid (kernels.cu):
 // r = F - sum over the elements sharing the point of their outputs Y.
 // ------------------------------------------------------------------------------------------
+template <int P> struct GatherCfg {
+  static constexpr int RS = 3 * (P - 1) * (P - 1) + 3 * (P - 1) + 1;
+  static constexpr int R = RS >= 128 ? 1 : 256 / RS;                        // records per block
+  static constexpr int NT = R > 1 ? 256 : (RS < 64 ? 64 : (RS < 128 ? 128 : 256));
+};
+
 template <int P>
 __global__ void __launch_bounds__(256) k_gather_resid_t(LevelGeom g, const double* __restrict__ Y,
                                                         const double* __restrict__ F, double* __restrict__ out,
@@ -1292,24 +1297,32 @@ __global__ void __launch_bounds__(256) k_gather_resid_t(LevelGeom g, const doubl
   pdl_trigger();
   if (done && *done) return;
   constexpr int m = P - 1, mm = m * m, RS = 3 * mm + 3 * m + 1, YS = 6 * mm + 12 * m + 8;
-  const int v1 = blockIdx.x, v2 = blockIdx.y, v3 = blockIdx.z;
-  const long long rec = v1 + (long long)g.V1 * (v2 + (long long)g.V2 * v3);
+  // R consecutive records along x1 per block (low degrees: a record has only 7 ... 127 slots); their
+  // R x RS slots are one contiguous range of the skeleton vector
+  constexpr int R = GatherCfg<P>::R;
+  const int v2 = blockIdx.y, v3 = blockIdx.z, v1b = blockIdx.x * R;
   const bool own = owned_plane(g, v3);
   // Y offsets of the (up to) 8 elements around vertex v: bit d of c set = element v_d along d, clear =
   // element v_d - 1 (periodic: wrapped); -1 outside the box (Neumann faces have one side)
-  __shared__ long long eb[8];
-  if (threadIdx.x < 8) {
-    const int c = threadIdx.x;
+  __shared__ long long ebs[R][8];
+  for (int i = threadIdx.x; i < 8 * R; i += blockDim.x) {
+    const int c = i & 7, v1 = v1b + (i >> 3);
     int a1 = v1 - 1 + (c & 1), a2 = v2 - 1 + ((c >> 1) & 1), a3 = v3 - 1 + ((c >> 2) & 1);
     a1 = wrap_rec(a1, g.k1, g.per & 1);
     a2 = wrap_rec(a2, g.k2, g.per & 2);
     a3 = wrap_rec(a3, g.k3, g.per & 4);
     const bool in = a1 >= 0 && a2 >= 0 && a3 >= 0 && a1 < g.k1 && a2 < g.k2 && a3 < g.k3;
-    eb[c] = in ? ((long long)a1 + (long long)g.k1 * ((long long)a2 + (long long)g.k2 * a3)) * YS : -1LL;
+    ebs[i >> 3][c] = in ? ((long long)a1 + (long long)g.k1 * ((long long)a2 + (long long)g.k2 * a3)) * YS : -1LL;
   }
   __syncthreads();
+  const long long rec0 = v1b + (long long)g.V1 * (v2 + (long long)g.V2 * v3);
+  const int nrec = min(R, g.V1 - v1b);
+  for (int j = threadIdx.x; j < nrec * RS; j += blockDim.x) {
+  const int ri = j / RS, o = j - ri * RS, v1 = v1b + ri;
+  const long long rec = rec0 + ri;
+  const long long* eb = ebs[ri];
   auto yat = [&](int c, int off) -> double { const long long b_ = eb[c]; return b_ >= 0 ? Y[b_ + off] : 0.0; };
-  for (int o = threadIdx.x; o < RS; o += blockDim.x) {
+  {
     int t1 = 0, t2 = 0, t3 = 0, type, a = 0, b = 0;
     if (o < 3 * mm) {
       type = o / mm;
@@ -1348,6 +1361,7 @@ __global__ void __launch_bounds__(256) k_gather_resid_t(LevelGeom g, const doubl
       r = F ? F[rec * RS + o] - s_ : s_;
     }
     out[rec * RS + o] = r;
+  }
   }
 }
 
@@ -1414,13 +1428,12 @@ cudaError_t launch_elem_apply(const LevelGeom& g, const double* u, const double*
 
 cudaError_t launch_gather_resid(const LevelGeom& g, const double* Y, const double* F, double* out, const int* done,
                                 cudaStream_t st) {
-  const dim3 grid((unsigned)g.V1, (unsigned)g.V2, (unsigned)g.V3);
   switch (g.p) {
 #define CASE(P)                                                                                     \
   case P: {                                                                                         \
-    constexpr int RS = 3 * (P - 1) * (P - 1) + 3 * (P - 1) + 1;                                     \
-    const int nt = RS < 64 ? 64 : (RS < 128 ? 128 : 256);                                           \
-    return launch_pdl(k_gather_resid_t<P>, grid, dim3(nt), 0, st, g, Y, F, out, done);              \
+    constexpr int R = GatherCfg<P>::R;                                                              \
+    const dim3 grid((unsigned)((g.V1 + R - 1) / R), (unsigned)g.V2, (unsigned)g.V3);                \
+    return launch_pdl(k_gather_resid_t<P>, grid, dim3(GatherCfg<P>::NT), 0, st, g, Y, F, out, done); \
   }
     PMG_DEGREES(CASE)
 #undef CASE
