@@ -665,6 +665,15 @@ __device__ __forceinline__ double4 ld_row4(const double* t, int e) {
   return make_double4(a.x, a.y, b.x, b.y);
 }
 
+// 1 / x from the hardware approximation and one cubic Newton step (error e^3 of the ~2^-23
+// approximation: below double rounding); replaces the FP64 division sequence in the stencils
+__device__ __forceinline__ double hg_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
+
 __device__ __forceinline__ void hg_decode(const HGridLev& L, long long i, int& g1, int& g2, int& g3) {
   const unsigned u = (unsigned)i, t = u / (unsigned)L.N1;
   g1 = (int)(u - t * (unsigned)L.N1);
@@ -728,7 +737,7 @@ __device__ __forceinline__ double hg_centre(const HGridLev& L, const Acc& v, int
   s = fma(m13, fma(E2.y, v(ic - s2), E2.z * v(ic + s2)), s);
   s = fma(m12, fma(E3.y, v(ic - s3), E3.z * v(ic + s3)), s);
   const double hcc = fma(lam * E1.x, m23, fma(E1.w, m23, fma(E2.w, m13, E3.w * m12)));
-  return s / hcc;
+  return s * hg_rcp(hcc);
 }
 
 // (H_hat v) at the pair's points (values at non-free points are meaningless; callers mask);
@@ -825,7 +834,7 @@ __device__ __forceinline__ void hg_apply2(const HGridLev& L, const Acc& v, const
       s = fma(m12, fma(E3.y, um3, E3.z * up3), s);
       const double hcc = fma(lam * E1.x, m23, fma(E1.w, m23, fma(E2.w, m13, E3.w * m12)));
       const double mab = kind == 1 ? m23 : (kind == 2 ? m12 : m13);
-      return (side ? Nn.z : Nn.y) * mab * (s / hcc);
+      return (side ? Nn.z : Nn.y) * mab * (s * hg_rcp(hcc));
     };
     double c = 0.0;
     if (ok0) c += corr(N0, u0m1, u0p1, u0m2, u0p2, u0m3, u0p3, 0);
@@ -911,7 +920,7 @@ __device__ __forceinline__ double hg_restrict(const HGridLev& F, const HGridLev&
       const double hcc = fma(lam * E1.x, m23, fma(E1.w, m23, fma(E2.w, m13, E3.w * m12)));
       const double kf = d == 0 ? (side ? E1.z : E1.y) : (d == 1 ? (side ? E2.z : E2.y) : (side ? E3.z : E3.y));
       const double mab = d == 0 ? m23 : (d == 1 ? m13 : m12);
-      s = fma(-(kf * mab) / hcc, hg_t3(F, C, 2 * e1 + 1, 2 * e2 + 1, 2 * e3 + 1), s);
+      s = fma(-(kf * mab) * hg_rcp(hcc), hg_t3(F, C, 2 * e1 + 1, 2 * e2 + 1, 2 * e3 + 1), s);
     }
   }
   return s;
