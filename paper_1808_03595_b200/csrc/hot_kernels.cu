@@ -327,7 +327,7 @@ constexpr unsigned rec_slot(int m, int t1, int t2, int t3) {
 
 template <int P> struct StarMap { unsigned v[3 * (2 * P - 1) * (2 * P - 1)]; };
 // star plane d, position (A, B) of the (2p-1)^2 plane (A slow), relative to the star's vertex record
-template <int P> constexpr StarMap<P> make_star_map() {
+template <int P> __host__ __device__ constexpr StarMap<P> make_star_map() {
   StarMap<P> s{};
   constexpr int N = 2 * P - 1, NN = N * N, c = P - 1, m = P - 1;
   for (int i = 0; i < 3 * NN; ++i) {
@@ -1279,6 +1279,153 @@ __global__ void __launch_bounds__(128) k_star_w(LevelGeom g, int c1, int c2, int
 }
 
 // ------------------------------------------------------------------------------------------
+// star smoother at p = 2 (n_S = 3: 27-point stars, 19 skeleton points): one THREAD per star.  The
+// same arithmetic as k_star_w (Alg. 1 + Alg. 2, reading R19): the three 3 x 3 planes
+// through the vertex with the inverse multiplicity on the two lines through it, the
+// forward transforms T_d = S_slow^T F_d S_fast, the fused core over the 27 eigen-triples
+// V = E / (lambda + L1 + L2 + L3), the back transforms and the weighted scatter-add -- all in
+// registers, with the compile-time point map folded into immediates.  A warp per 27-point star
+// (k_star_w) left most lanes idle: the p = 2 sweep ran at 1.6 % of the HBM bound.
+// ------------------------------------------------------------------------------------------
+#ifndef PMG_STARP2_MINB
+#define PMG_STARP2_MINB 3   // 168 registers, small spills: 0.83 -> 0.75 ms per sweep at 128^3 elements
+#endif
+__global__ void __launch_bounds__(128, PMG_STARP2_MINB) k_star_p2(LevelGeom g, int c1, int c2, int c3, int n1c, int n2c, long long nstars,
+                                                const double* __restrict__ r, double* __restrict__ u,
+                                                const double* __restrict__ stab, double lam) {
+  constexpr int P = 2, N = 3, NN = 9, c = 1, RS = 7;
+  constexpr StarMap<P> map = make_star_map<P>();
+  pdl_wait();
+  pdl_trigger();
+  const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (b >= nstars) return;
+  const int i1 = (int)(b % n1c), rest = (int)(b / n1c), i2 = rest % n2c, i3 = rest / n2c;
+  const int v1 = c1 + 2 * i1, v2 = c2 + 2 * i2, v3 = c3 + 2 * i3;
+  if (star_empty(g, v1, v2, v3)) return;
+  if (v3 < g.own_lo) return;
+  const long long V12 = (long long)g.V1 * g.V2;
+  const bool interior = ((v1 > 0 && v1 < g.k1) || (g.per & 1)) && ((v2 > 0 && v2 < g.k2) || (g.per & 2)) &&
+                        ((v3 > 0 && v3 + g.zoff < g.K3) || (g.per & 4));
+  auto pt_free = [&](unsigned e) {   // as k_star_w
+    const int w1 = v1 - (int)((e >> 12) & 1u), w2 = v2 - (int)((e >> 13) & 1u), w3 = v3 - (int)((e >> 14) & 1u);
+    const int W3 = w3 + g.zoff;
+    const bool z1 = e & (1u << 15), z2 = e & (1u << 16), z3 = e & (1u << 17);
+    return ((g.per & 1) || (w1 >= 0 && (w1 > 0 || !z1 || (g.neu & 1)) && (w1 < g.k1 || (z1 && w1 == g.k1 && (g.neu & 2))))) &&
+           ((g.per & 2) || (w2 >= 0 && (w2 > 0 || !z2 || (g.neu & 4)) && (w2 < g.k2 || (z2 && w2 == g.k2 && (g.neu & 8))))) &&
+           ((g.per & 4) || (w3 >= 0 && (W3 > 0 || !z3 || (g.neu & 16)) && (W3 < g.K3 || (z3 && W3 == g.K3 && (g.neu & 32)))));
+  };
+  long long base[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int b1 = q & 1, b2 = (q >> 1) & 1, b3 = (q >> 2) & 1;
+    const bool ok = !((v1 == 0 && b1 && !(g.per & 1)) || (v2 == 0 && b2 && !(g.per & 2)) || (v3 == 0 && b3 && !(g.per & 4)));
+    const int w1 = wrap_rec(v1 - b1, g.k1, g.per & 1), w2 = wrap_rec(v2 - b2, g.k2, g.per & 2),
+              w3 = wrap_rec(v3 - b3, g.k3, g.per & 4);
+    base[q] = ok ? (w1 + g.V1 * (long long)w2 + V12 * w3) * RS : -1LL;
+  }
+  const double* St[3] = {stab + (size_t)v1 * g.ST, stab + (size_t)(g.V1 + v2) * g.ST, stab + (size_t)(g.V1 + g.V2 + v3) * g.ST};
+  // gather the three planes (inverse multiplicity on the lines through the vertex)
+  double F[3][NN];
+#pragma unroll
+  for (int i = 0; i < 3 * NN; ++i) {
+    const int d = i / NN, A = (i % NN) / N, B = i % N;
+    const unsigned e = map.v[i];
+    const long long bb = base[(e >> 12) & 7u];
+    const double x = bb >= 0 ? __ldg(&r[bb + (e & 0xFFFu)]) : 0.0;
+    F[d][A * N + B] = x * (1.0 / (double)(1 + (A == c) + (B == c)));
+  }
+  // forward transforms: T_d[a][b] = sum_{A,B} S_slow[A][a] F_d[A][B] S_fast[B][b]
+  // (plane 0: A = j3, B = j2; plane 1: A = j3, B = j1; plane 2: A = j2, B = j1)
+  double T[3][NN];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double* Sf = St[d == 0 ? 1 : 0];
+    const double* Ss = St[d == 2 ? 1 : 2];
+    double X[NN];
+#pragma unroll
+    for (int A = 0; A < N; ++A)
+#pragma unroll
+      for (int bq = 0; bq < N; ++bq) {
+        double x = 0.0;
+#pragma unroll
+        for (int B = 0; B < N; ++B) x = fma(F[d][A * N + B], __ldg(&Sf[B * N + bq]), x);
+        X[A * N + bq] = x;
+      }
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+      for (int bq = 0; bq < N; ++bq) {
+        double t = 0.0;
+#pragma unroll
+        for (int A = 0; A < N; ++A) t = fma(__ldg(&Ss[A * N + a]), X[A * N + bq], t);
+        T[d][a * N + bq] = t;
+      }
+  }
+  // core over the eigen-triples: T1 = T[0][a3][a2], T2 = T[1][a3][a1], T3 = T[2][a2][a1]
+  double Lm[3][N], sv[3][N];
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      Lm[d][a] = __ldg(&St[d][NN + a]);
+      sv[d][a] = __ldg(&St[d][NN + N + a]);
+    }
+  double G[3][NN];
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int k = 0; k < NN; ++k) G[d][k] = 0.0;
+#pragma unroll
+  for (int a3 = 0; a3 < N; ++a3)
+#pragma unroll
+    for (int a2 = 0; a2 < N; ++a2)
+#pragma unroll
+      for (int a1 = 0; a1 < N; ++a1) {
+        double E = sv[0][a1] * T[0][a3 * N + a2];
+        E = fma(sv[1][a2], T[1][a3 * N + a1], E);
+        E = fma(sv[2][a3], T[2][a2 * N + a1], E);
+        const double V = E * rcp_nr(lam + Lm[0][a1] + Lm[1][a2] + Lm[2][a3]);
+        G[0][a3 * N + a2] = fma(sv[0][a1], V, G[0][a3 * N + a2]);
+        G[1][a3 * N + a1] = fma(sv[1][a2], V, G[1][a3 * N + a1]);
+        G[2][a2 * N + a1] = fma(sv[2][a3], V, G[2][a2 * N + a1]);
+      }
+  // back transforms U_d[A][B] = sum_{a,b} S_slow[A][a] G_d[a][b] S_fast[B][b], weighted scatter-add
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double* Sf = St[d == 0 ? 1 : 0];
+    const double* Ss = St[d == 2 ? 1 : 2];
+    double X[NN];
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+      for (int B = 0; B < N; ++B) {
+        double x = 0.0;
+#pragma unroll
+        for (int bq = 0; bq < N; ++bq) x = fma(G[d][a * N + bq], __ldg(&Sf[B * N + bq]), x);
+        X[a * N + B] = x;
+      }
+#pragma unroll
+    for (int A = 0; A < N; ++A)
+#pragma unroll
+      for (int B = 0; B < N; ++B) {
+        int j1, j2, j3;
+        if (d == 0) { j1 = c; j2 = B; j3 = A; }
+        else if (d == 1) { j2 = c; j1 = B; j3 = A; if (j1 == c) continue; }
+        else { j3 = c; j1 = B; j2 = A; if (j1 == c || j2 == c) continue; }
+        const unsigned e = map.v[d * NN + A * N + B];
+        const long long bb = base[(e >> 12) & 7u];
+        if (bb < 0 || !(interior || pt_free(e))) continue;
+        double uu = 0.0;
+#pragma unroll
+        for (int a = 0; a < N; ++a) uu = fma(__ldg(&Ss[A * N + a]), X[a * N + B], uu);
+        const double w = __ldg(&St[0][NN + 2 * N + j1]) * __ldg(&St[1][NN + 2 * N + j2]) * __ldg(&St[2][NN + 2 * N + j3]);
+        double* dst = &u[bb + (e & 0xFFFu)];
+        *dst = fma(w, uu, *dst);
+      }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // residual gather, degree-templated: one block per vertex record (3-D grid, no index division),
 // one thread per record slot.  Same sums in the same order as k_gather_resid (kernels.cu):
 // r = F - sum over the elements sharing the point of their outputs Y.
@@ -1396,6 +1543,9 @@ cudaError_t launch_star_p(const LevelGeom& g, int c1, int c2, int c3, int n1c, i
                           double* u, const double* stab, const double* stabP, double lam, cudaStream_t st) {
   if constexpr (P >= 5 && P <= 16) {
     return launch_star16(g, c1, c2, c3, n1c, n2c, nb, r, u, stabP, lam, st);
+  } else if constexpr (P == 2) {
+    return launch_pdl(k_star_p2, dim3((unsigned)((nb + 127) / 128)), dim3(128), 0, st, g, c1, c2, c3, n1c, n2c, nb, r, u,
+                      stab, lam);
   } else if constexpr (P <= 4) {
     {
       // warp per star pays off once a colour has many waves of 128-thread stars (large meshes);
