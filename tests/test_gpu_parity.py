@@ -584,6 +584,31 @@ def test_hmg_coarse_solver_parity(name):
     s.close()
 
 
+def test_hmg_recurrence_true_residual():
+    """The h-multigrid CG updates q = H z + beta q by recurrence (one operator application per
+    iteration), so its recursive residual can drift from f - H x.  On a 32 x 32 x 16-element p = 2
+    mesh (L = 0: the V-cycle is the coarse CG alone, four h-levels) solved to 1e-12, the TRUE residual
+    recomputed by the residual kernel must still be below 1e-10 of ||f||."""
+    import paper_1808_03595_b200 as pmg
+    k = (32, 32, 16)
+    case = pi.small_case(k, 2, 0.0, stretch=1.1)
+    s = pmg.Solver(case.k, case.widths, 2, 0.0, coarse_rtol=1e-12, coarse_solver=2)
+    L = s.nlevels - 1
+    assert L == 0
+    n = s.level_info(0)[2]
+    g = s.new_grid(0)
+    g.copy_(torch.from_numpy(np.random.default_rng(5).standard_normal(n)))
+    f = s.new_skel(0)
+    s.skel_from_grid(0, g, f)
+    u = s.new_skel(0)
+    s.vcycle(u, f)
+    r = s.new_skel(0)
+    s.residual(0, u, f, r)
+    torch.cuda.synchronize()
+    assert torch.linalg.norm(r).item() <= 1e-10 * torch.linalg.norm(f).item()
+    s.close()
+
+
 def test_hmg_auto_on_large_mesh_matches_jacobi():
     """32^3 elements at p = 4 (coarse 32^3 at p0 = 2, 226 k unknowns): the automatic choice takes the
     h-multigrid coarse CG; the solve agrees with the Jacobi-PCG one and needs far fewer coarse
