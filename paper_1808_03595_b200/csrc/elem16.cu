@@ -383,18 +383,24 @@ __global__ void __launch_bounds__(128, 3)
         const double* Uf = Uc + f * FS;
         const double* Kd = Kt(d);
         double z = X[f * MS + A * LDT + B];
-        z = fma(Kt(da)[ta * LDT], Uf[tbb * LDT], z);                     // t = 0 term along a
         z = fma(Kt(db)[tbb * LDT], Uf[ta], z);                           // t = 0 term along b
         z = fma(Kd[td * LDT], Uc[(2 * d) * FS + tbb * LDT + ta], z);     // normal line: the two faces
         z = fma(Kd[td * LDT + P], Uc[(2 * d + 1) * FS + tbb * LDT + ta], z);
         z = fma(lam, Uf[tbb * LDT + ta], z);
-        Ye[f * MM + l] = Mv(d)[td] * Mv(da)[ta] * Mv(db)[tbb] * z - T[f * MS + A * LDT + B];
+        // t = 0 term along a after the M_a[ta] scaling: M_a[ta] K~_a[ta][0] = K_a[ta][0] = K_a[0][ta]
+        // = M_a[0] K~_a[0][ta] (K symmetric), read along the row: lanes of consecutive ta hit
+        // consecutive banks instead of a column at stride LDT
+        const double za = fma(Mv(da)[0] * Kt(da)[ta], Uf[tbb * LDT], Mv(da)[ta] * z);
+        Ye[f * MM + l] = Mv(d)[td] * Mv(db)[tbb] * za - T[f * MS + A * LDT + B];
       }
     }
   }
   // a boundary line along d through (t1, t2, t3) lies in a face whose normal n != d has t_n in {0, p}:
   // in that face's closed array it is a row (d the fast direction) or a column
-  auto line = [&](int d, int t1, int t2, int t3) -> double {
+  // TR: the line of the point's own edge direction d, whose K~ row t_d varies over the lanes: summed
+  // as sum_t K~_d[t][t_d] M_d[t] u(t) = M_d[t_d] sum_t K~_d[t_d][t] u(t) (K symmetric), the row read
+  // along consecutive t_d (no stride-LDT bank conflicts)
+  auto line = [&](int d, int t1, int t2, int t3, auto TR) -> double {
     int n;
     if (d != 0 && (t1 == 0 || t1 == P)) n = 0;
     else if (d != 1 && (t2 == 0 || t2 == P)) n = 1;
@@ -405,19 +411,28 @@ __global__ void __launch_bounds__(128, 3)
     const double* Uf = Uc + (2 * n + (tn == P ? 1 : 0)) * FS;
     const double* ptr = (d == fa) ? Uf + tbb * LDT : Uf + ta;
     const int st = (d == fa) ? 1 : LDT;
-    const double* Kr = Kt(d) + (d == 0 ? t1 : (d == 1 ? t2 : t3)) * LDT;
+    const int td = d == 0 ? t1 : (d == 1 ? t2 : t3);
     double z = 0.0;
+    if constexpr (decltype(TR)::value) {
+      const double* Kc = Kt(d) + td;
+      const double* Md = Mv(d);
 #pragma unroll
-    for (int t = 0; t <= P; ++t) z = fma(Kr[t], ptr[t * st], z);
+      for (int t = 0; t <= P; ++t) z = fma(Kc[t * LDT], Md[t] * ptr[t * st], z);
+    } else {
+      const double* Kr = Kt(d) + td * LDT;
+#pragma unroll
+      for (int t = 0; t <= P; ++t) z = fma(Kr[t], ptr[t * st], z);
+    }
     return z;
   };
   for (int o = 6 * MM + tid; o < YS; o += NT) {
-    int t1, t2, t3;
+    int t1, t2, t3, de = -1;
     if (o < 6 * MM + 12 * M) {
       const int r = o - 6 * MM, qe = r / M, i = r - qe * M, d = qe >> 2, sA = qe & 1, sB = (qe >> 1) & 1;
       if (d == 0) { t1 = i + 1; t2 = sA * P; t3 = sB * P; }
       else if (d == 1) { t2 = i + 1; t1 = sA * P; t3 = sB * P; }
       else { t3 = i + 1; t1 = sA * P; t2 = sB * P; }
+      de = d;
     } else {
       const int qv = o - 6 * MM - 12 * M;
       t1 = (qv & 1) * P; t2 = ((qv >> 1) & 1) * P; t3 = ((qv >> 2) & 1) * P;
@@ -427,10 +442,19 @@ __global__ void __launch_bounds__(128, 3)
     const int tn = n == 0 ? t1 : (n == 1 ? t2 : t3);
     const int ta = n == 0 ? t2 : t1, tbb = n == 2 ? t2 : t3;
     double z = lam * Uc[(2 * n + (tn == P ? 1 : 0)) * FS + tbb * LDT + ta];
-    z += line(0, t1, t2, t3);
-    z += line(1, t1, t2, t3);
-    z += line(2, t1, t2, t3);
-    Ye[o] = Mv(0)[t1] * Mv(1)[t2] * Mv(2)[t3] * z;
+    if (de < 0) {   // vertex: every K~ row index is 0 or p
+      z += line(0, t1, t2, t3, FF{});
+      z += line(1, t1, t2, t3, FF{});
+      z += line(2, t1, t2, t3, FF{});
+      Ye[o] = Mv(0)[t1] * Mv(1)[t2] * Mv(2)[t3] * z;
+    } else {        // edge along de: Y = M_a M_b (M_de[t_de] (lam u + two cross lines) + own line)
+      const int da = de == 0 ? 1 : 0, db = de == 2 ? 1 : 2;
+      const int tde = de == 0 ? t1 : (de == 1 ? t2 : t3);
+      z += line(da, t1, t2, t3, FF{});
+      z += line(db, t1, t2, t3, FF{});
+      const double ze = fma(Mv(de)[tde], z, line(de, t1, t2, t3, TT{}));
+      Ye[o] = Mv(da)[da == 0 ? t1 : t2] * Mv(db)[db == 1 ? t2 : t3] * ze;
+    }
   }
 }
 
