@@ -25,3 +25,14 @@ run((2, 2, 2), 13, 0.7, smoother=1)
 run((2, 2, 1), 16, 0.7, smoother=1)
 run((3, 3, 3), 4, 0.2, solver=1, neumann=0b100101)
 run((8, 8, 4), 4, 0.0, coarse_solver=2)
+# round 2 kernels: p = 9..16 star / element / condensation (k_star16, k_elem16, k_cr16), p = 17..32
+# (k_star_tm, k_elem_apply_t), p = 2 thread-per-star, periodic faces, the grid-layout h-multigrid at p = 2
+run((2, 3, 2), 12, 0.0)
+run((2, 2, 2), 9, 0.4)
+run((2, 2, 2), 24, 0.0)
+run((4, 4, 4), 2, 0.3)
+run((4, 2, 4), 6, 0.0, periodic=0b101)
+run((2, 2, 2), 12, 0.5, periodic=0b010)
+run((8, 8, 8), 2, 0.0, coarse_solver=2)
+os.environ["PMG_STAR_W_MIN"] = "0"
+run((3, 3, 3), 4, 0.0)
