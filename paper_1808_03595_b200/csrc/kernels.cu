@@ -135,8 +135,20 @@ __global__ void k_weak_rhs(LevelGeom g, const double* __restrict__ b1, const dou
 // ------------------------------------------------------------------------------------------
 size_t transfer_smem(int pf, int pc) {
   int mf = pf - 1, qc = pc + 1;
-  return sizeof(double) * (size_t)(3 * qc * qc + 3 * qc + 1 + mf * qc + mf * qc + mf * mf + qc * mf);
+  size_t rt = (size_t)(3 * qc * qc + 3 * qc + 1 + mf * qc + mf * qc + mf * mf + qc * mf);
+  // register-tiled kernels (pf <= 16): closed coarse record (even length), J padded to even rows, X of 3 faces
+  size_t tl = (size_t)(3 * qc * qc + 3 * qc + 2 + mf * (qc + 1) + 3 * qc * mf + 3 * mf * mf);
+  return sizeof(double) * (rt > tl ? rt : tl);
 }
+
+// register-tiled face transforms of the transfer kernels (compile-time degrees, p_f <= 16): a thread
+// owns one row (or column) of a face in registers and reads J as broadcast 16-byte shared loads, one
+// load per two FMAs instead of two loads per FMA; every output is summed in the same order as in
+// the plain loops, so the results are bitwise the same
+template <int PF_, int PC_> struct TransferTile {
+  static constexpr bool on = PF_ > 0 && PF_ <= 16;
+  static constexpr int MF = PF_ > 0 ? PF_ - 1 : 1, QC = PC_ + 1, QP = (QC + 1) & ~1;
+};
 
 // Z[v] = [3 closed coarse faces qc x qc][3 closed coarse edges qc][vertex]
 // PF_ / PC_ > 0: degrees known at compile time (unrolled loops, constant divisions); 0: runtime
@@ -145,12 +157,76 @@ __global__ void k_restrict_local_t(LevelGeom gf, int pc_rt, const double* __rest
                                    const double* __restrict__ rf, double* __restrict__ Z) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double smt[];
+  double* sm = smt;
+  using TT = TransferTile<PF_, PC_>;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if constexpr (TT::on) {
+    constexpr int MF = TT::MF, QC = TT::QC, QP = TT::QP, ZSc = 3 * QC * QC + 3 * QC + 1;
+    double* Jp = sm;                // MF x QP (rows padded to an even length)
+    double* X3 = Jp + MF * QP;      // 3 x MF x QC
+    double* F3 = X3 + 3 * MF * QC;  // the record's 3 face interiors (contiguous in the record)
+    for (int i = tid; i < MF * QP; i += nt) {
+      const int ia = i / QP, al = i - ia * QP;
+      Jp[i] = al < QC ? Jint[ia * QC + al] : 0.0;
+    }
+    const long long rec = blockIdx.x;
+    const double* R = rf + rec * gf.RS;
+    double* Zr = Z + rec * ZSc;
+    for (int i = tid; i < 3 * MF * MF; i += nt) F3[i] = R[i];
+    __syncthreads();
+    for (int row = tid; row < 3 * MF; row += nt) {   // X[d][ib][:] = sum_ia F_d[ib][ia] J[ia][:]
+      const double* F = F3 + row * MF;               // row = d * MF + ib
+      double x[QP];
+#pragma unroll
+      for (int al = 0; al < QP; ++al) x[al] = 0.0;
+#pragma unroll 3
+      for (int ia = 0; ia < MF; ++ia) {
+        const double fv = F[ia];
+#pragma unroll
+        for (int a2 = 0; a2 < QP / 2; ++a2) {
+          const double2 j = *reinterpret_cast<const double2*>(Jp + ia * QP + 2 * a2);
+          x[2 * a2] = fma(fv, j.x, x[2 * a2]);
+          x[2 * a2 + 1] = fma(fv, j.y, x[2 * a2 + 1]);
+        }
+      }
+#pragma unroll
+      for (int al = 0; al < QC; ++al) X3[row * QC + al] = x[al];
+    }
+    __syncthreads();
+    for (int c = tid; c < 3 * QC; c += nt) {         // Z[d][:][al] = sum_ib J[ib][:] X[d][ib][al]
+      const int d = c / QC, al = c - d * QC;
+      double z[QP];
+#pragma unroll
+      for (int be = 0; be < QP; ++be) z[be] = 0.0;
+#pragma unroll 3
+      for (int ib = 0; ib < MF; ++ib) {
+        const double xv = X3[(d * MF + ib) * QC + al];
+#pragma unroll
+        for (int b2 = 0; b2 < QP / 2; ++b2) {
+          const double2 j = *reinterpret_cast<const double2*>(Jp + ib * QP + 2 * b2);
+          z[2 * b2] = fma(j.x, xv, z[2 * b2]);
+          z[2 * b2 + 1] = fma(j.y, xv, z[2 * b2 + 1]);
+        }
+      }
+#pragma unroll
+      for (int be = 0; be < QC; ++be) Zr[d * QC * QC + be * QC + al] = z[be];
+    }
+    for (int i = tid; i < 3 * QC; i += nt) {
+      const int d = i / QC, al = i - d * QC;
+      const double* E = R + off_edge(MF, d);
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < MF; ++t) s += Jp[t * QP + al] * E[t];
+      Zr[3 * QC * QC + i] = s;
+    }
+    if (tid == 0) Zr[ZSc - 1] = R[off_vert(MF)];
+    return;
+  }
   const int pc = PC_ > 0 ? PC_ : pc_rt;
   const int mf = PF_ > 0 ? PF_ - 1 : gf.m, qc = pc + 1, ZS = 3 * qc * qc + 3 * qc + 1;
   double* J = sm;             // mf x qc
   double* X = J + mf * qc;    // mf x qc
-  const int tid = threadIdx.x, nt = blockDim.x;
   for (int i = tid; i < mf * qc; i += nt) J[i] = Jint[i];
   __syncthreads();
   const long long rec = blockIdx.x;
@@ -248,15 +324,22 @@ __global__ void k_prolong_t(LevelGeom gf, LevelGeom gc, const double* __restrict
                             const double* __restrict__ uc, double* __restrict__ uf) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double smt[];
+  double* sm = smt;
+  using TT = TransferTile<PF_, PC_>;
   const int pf = PF_ > 0 ? PF_ : gf.p, mf = pf - 1, pc = PC_ > 0 ? PC_ : gc.p, qc = pc + 1;
   double* C = sm;                      // 3 qc^2 closed faces, 3 qc closed edges, 1 vertex
-  double* J = C + 3 * qc * qc + 3 * qc + 1;  // mf x qc
-  double* X = J + mf * qc;             // qc x mf
+  // tiled: J rows padded to an even length on a 16-byte boundary (Jld = QP), else mf x qc
+  const int Jld = TT::on ? TT::QP : qc;
+  double* J = C + (TT::on ? ((3 * qc * qc + 3 * qc + 2) & ~1) : 3 * qc * qc + 3 * qc + 1);
+  double* X = J + mf * Jld;            // qc x mf (tiled: 3 faces)
   const int tid = threadIdx.x, nt = blockDim.x;
   const long long rec = blockIdx.x;
   const int v1 = (int)(rec % gf.V1), v2 = (int)((rec / gf.V1) % gf.V2), v3 = (int)(rec / ((long long)gf.V1 * gf.V2));
-  for (int i = tid; i < mf * qc; i += nt) J[i] = Jint[i];
+  for (int i = tid; i < mf * Jld; i += nt) {
+    const int ia = i / Jld, al = i - ia * Jld;
+    J[i] = al < qc ? Jint[ia * qc + al] : 0.0;
+  }
   for (int i = tid; i < 3 * qc * qc; i += nt) {
     int d = i / (qc * qc), rr = i - d * qc * qc, be = rr / qc, al = rr - be * qc;
     int G1 = v1 * pc, G2 = v2 * pc, G3 = v3 * pc;
@@ -275,6 +358,63 @@ __global__ void k_prolong_t(LevelGeom gf, LevelGeom gc, const double* __restrict
   }
   __syncthreads();
   double* Ur = uf + rec * gf.RS;
+  if constexpr (TT::on) {
+    constexpr int MF = TT::MF, QC = TT::QC, QP = TT::QP;
+    for (int row = tid; row < 3 * QC; row += nt) {   // X[d][be][:] = sum_al C_d[be][al] J[:][al]
+      const double* Cr = C + row * QC;               // row = d * QC + be
+      double cr[QC];
+#pragma unroll
+      for (int al = 0; al < QC; ++al) cr[al] = Cr[al];
+#pragma unroll 3
+      for (int ia = 0; ia < MF; ++ia) {
+        double sx = 0.0;
+#pragma unroll
+        for (int a2 = 0; a2 < QP / 2; ++a2) {
+          const double2 j = *reinterpret_cast<const double2*>(J + ia * QP + 2 * a2);
+          sx = fma(cr[2 * a2], j.x, sx);
+          if (2 * a2 + 1 < QC) sx = fma(cr[2 * a2 + 1 < QC ? 2 * a2 + 1 : 0], j.y, sx);
+        }
+        X[row * MF + ia] = sx;
+      }
+    }
+    __syncthreads();
+    for (int c = tid; c < 3 * MF; c += nt) {         // F_d[:][ia] = sum_be J[:][be] X[d][be][ia]
+      const int d = c / MF, ia = c - d * MF;
+      double xc[QC];
+#pragma unroll
+      for (int be = 0; be < QC; ++be) xc[be] = X[(d * QC + be) * MF + ia];
+      int g1 = v1 * PF_, g2 = v2 * PF_, g3 = v3 * PF_;
+      if (d == 0) g2 += ia + 1; else g1 += ia + 1;
+#pragma unroll 3
+      for (int ib = 0; ib < MF; ++ib) {
+        double sf = 0.0;
+#pragma unroll
+        for (int b2 = 0; b2 < QP / 2; ++b2) {
+          const double2 j = *reinterpret_cast<const double2*>(J + ib * QP + 2 * b2);
+          sf = fma(j.x, xc[2 * b2], sf);
+          if (2 * b2 + 1 < QC) sf = fma(j.y, xc[2 * b2 + 1 < QC ? 2 * b2 + 1 : 0], sf);
+        }
+        const int h1 = g1, h2 = d == 2 ? g2 + ib + 1 : g2, h3 = d == 2 ? g3 : g3 + ib + 1;
+        if (is_free(gf, h1, h2, h3)) Ur[off_face(MF, d) + ib * MF + ia] += sf;
+      }
+    }
+    for (int i = tid; i < 3 * MF + 1; i += nt) {
+      int g1 = v1 * PF_, g2 = v2 * PF_, g3 = v3 * PF_;
+      double s;
+      if (i < 3 * MF) {
+        const int d = i / MF, t = i - d * MF;
+        const double* Ce = C + 3 * QC * QC + d * QC;
+        s = 0.0;
+#pragma unroll
+        for (int al = 0; al < QC; ++al) s += J[t * QP + al] * Ce[al];
+        if (d == 0) g1 += t + 1; else if (d == 1) g2 += t + 1; else g3 += t + 1;
+      } else {
+        s = C[3 * QC * QC + 3 * QC];
+      }
+      if (is_free(gf, g1, g2, g3)) Ur[off_edge(MF, 0) + i] += s;   // edges then vertex are contiguous
+    }
+    return;
+  }
   for (int d = 0; d < 3; ++d) {
     const double* Cd = C + d * qc * qc;
     for (int i = tid; i < qc * mf; i += nt) {  // X[be][ia] = sum_al C[be][al] J[ia][al]
