@@ -137,7 +137,7 @@ size_t transfer_smem(int pf, int pc) {
   int mf = pf - 1, qc = pc + 1;
   size_t rt = (size_t)(3 * qc * qc + 3 * qc + 1 + mf * qc + mf * qc + mf * mf + qc * mf);
   // register-tiled kernels (pf <= 16): closed coarse record (even length), J padded to even rows, X of 3 faces
-  size_t tl = (size_t)(3 * qc * qc + 3 * qc + 2 + mf * (qc + 1) + 3 * qc * mf + 3 * mf * mf);
+  size_t tl = (size_t)(3 * qc * qc + 3 * qc + 2 + mf * (qc + 1) + 3 * qc * mf + 3 * mf * mf + 3 * mf + 2);
   return sizeof(double) * (rt > tl ? rt : tl);
 }
 
@@ -356,10 +356,16 @@ __global__ void k_prolong_t(LevelGeom gf, LevelGeom gc, const double* __restrict
     wrap_pt(gc, G1, G2, G3);
     C[3 * qc * qc + i] = inside(gc, G1, G2, G3) ? uc[skel_index(gc, G1, G2, G3)] : 0.0;
   }
-  __syncthreads();
   double* Ur = uf + rec * gf.RS;
+  if constexpr (TT::on) {   // the fine record is staged, updated in shared memory and written back whole (coalesced)
+    constexpr int MF = TT::MF, QC = TT::QC, RSc = 3 * MF * MF + 3 * MF + 1;
+    double* Us = X + 3 * QC * MF;
+    for (int i = tid; i < RSc; i += nt) Us[i] = Ur[i];
+  }
+  __syncthreads();
   if constexpr (TT::on) {
-    constexpr int MF = TT::MF, QC = TT::QC, QP = TT::QP;
+    constexpr int MF = TT::MF, QC = TT::QC, QP = TT::QP, RSc = 3 * MF * MF + 3 * MF + 1;
+    double* Us = X + 3 * QC * MF;
     for (int row = tid; row < 3 * QC; row += nt) {   // X[d][be][:] = sum_al C_d[be][al] J[:][al]
       const double* Cr = C + row * QC;               // row = d * QC + be
       double cr[QC];
@@ -395,7 +401,7 @@ __global__ void k_prolong_t(LevelGeom gf, LevelGeom gc, const double* __restrict
           if (2 * b2 + 1 < QC) sf = fma(j.y, xc[2 * b2 + 1 < QC ? 2 * b2 + 1 : 0], sf);
         }
         const int h1 = g1, h2 = d == 2 ? g2 + ib + 1 : g2, h3 = d == 2 ? g3 : g3 + ib + 1;
-        if (is_free(gf, h1, h2, h3)) Ur[off_face(MF, d) + ib * MF + ia] += sf;
+        if (is_free(gf, h1, h2, h3)) Us[off_face(MF, d) + ib * MF + ia] += sf;
       }
     }
     for (int i = tid; i < 3 * MF + 1; i += nt) {
@@ -411,8 +417,10 @@ __global__ void k_prolong_t(LevelGeom gf, LevelGeom gc, const double* __restrict
       } else {
         s = C[3 * QC * QC + 3 * QC];
       }
-      if (is_free(gf, g1, g2, g3)) Ur[off_edge(MF, 0) + i] += s;   // edges then vertex are contiguous
+      if (is_free(gf, g1, g2, g3)) Us[off_edge(MF, 0) + i] += s;   // edges then vertex are contiguous
     }
+    __syncthreads();
+    for (int i = tid; i < RSc; i += nt) Ur[i] = Us[i];
     return;
   }
   for (int d = 0; d < 3; ++d) {
