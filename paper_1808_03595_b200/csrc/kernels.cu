@@ -267,7 +267,9 @@ __global__ void k_restrict_gather_t(LevelGeom gc, const double* __restrict__ Z, 
   const int pc = PC_ > 0 ? PC_ : gc.p, qc = pc + 1, ZS = 3 * qc * qc + 3 * qc + 1;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < gc.nskel;
        idx += (long long)gridDim.x * blockDim.x) {
-    Entry E = decode_entry(gc, idx);
+    Entry E;
+    if (PC_ > 1 && gc.nskel < (1ll << 31)) E = decode_entry_t<(PC_ > 1 ? PC_ : 2)>(gc, (unsigned)idx);
+    else E = decode_entry(gc, idx);
     double s = 0.0;
     if (is_free(gc, E.g1, E.g2, E.g3) && owned_plane(gc, E.v3)) {
       const int G[3] = {E.g1, E.g2, E.g3};
@@ -345,7 +347,10 @@ __global__ void k_prolong_t(LevelGeom gf, LevelGeom gc, const double* __restrict
     int G1 = v1 * pc, G2 = v2 * pc, G3 = v3 * pc;
     if (d == 0) { G3 += be; G2 += al; } else if (d == 1) { G3 += be; G1 += al; } else { G2 += be; G1 += al; }
     wrap_pt(gc, G1, G2, G3);   // periodic: the closed face of the last record ends on plane 0
-    C[i] = inside(gc, G1, G2, G3) ? uc[skel_index(gc, G1, G2, G3)] : 0.0;
+    long long ci;
+    if constexpr (PC_ > 0) ci = skel_index_t<(PC_ > 0 ? PC_ : 1)>(gc, G1, G2, G3);
+    else ci = skel_index(gc, G1, G2, G3);
+    C[i] = inside(gc, G1, G2, G3) ? uc[ci] : 0.0;
   }
   for (int i = tid; i < 3 * qc + 1; i += nt) {
     int G1 = v1 * pc, G2 = v2 * pc, G3 = v3 * pc;
@@ -354,7 +359,10 @@ __global__ void k_prolong_t(LevelGeom gf, LevelGeom gc, const double* __restrict
       if (d == 0) G1 += al; else if (d == 1) G2 += al; else G3 += al;
     }
     wrap_pt(gc, G1, G2, G3);
-    C[3 * qc * qc + i] = inside(gc, G1, G2, G3) ? uc[skel_index(gc, G1, G2, G3)] : 0.0;
+    long long ci;
+    if constexpr (PC_ > 0) ci = skel_index_t<(PC_ > 0 ? PC_ : 1)>(gc, G1, G2, G3);
+    else ci = skel_index(gc, G1, G2, G3);
+    C[3 * qc * qc + i] = inside(gc, G1, G2, G3) ? uc[ci] : 0.0;
   }
   double* Ur = uf + rec * gf.RS;
   if constexpr (TT::on) {   // the fine record is staged, updated in shared memory and written back whole (coalesced)

@@ -130,4 +130,38 @@ __device__ __forceinline__ Entry decode_entry(const LevelGeom& g, long long idx)
   return E;
 }
 
+// decode_entry with the degree known at compile time and a vector shorter than 2^31 entries:
+// 32-bit arithmetic, divisions by RS, m^2 and m become multiply-shifts
+template <int P>
+__device__ __forceinline__ Entry decode_entry_t(const LevelGeom& g, unsigned idx) {
+  constexpr int m = P - 1, mm = m * m;
+  constexpr unsigned RS = 3 * mm + 3 * m + 1;
+  Entry E;
+  const unsigned rec = idx / RS;
+  const int o = (int)(idx - rec * RS);
+  const unsigned r2 = rec / (unsigned)g.V1;
+  E.v1 = (int)(rec - r2 * (unsigned)g.V1);
+  E.v3 = (int)(r2 / (unsigned)g.V2);
+  E.v2 = (int)(r2 - (unsigned)E.v3 * (unsigned)g.V2);
+  E.g1 = E.v1 * P; E.g2 = E.v2 * P; E.g3 = E.v3 * P;
+  E.a = 0; E.b = 0;
+  if (o < 3 * mm) {
+    E.type = o / (mm > 0 ? mm : 1);
+    const int r = o - E.type * mm;
+    E.a = r / m; E.b = r - E.a * m;
+    if (E.type == 0) { E.g3 += E.a + 1; E.g2 += E.b + 1; }
+    else if (E.type == 1) { E.g3 += E.a + 1; E.g1 += E.b + 1; }
+    else { E.g2 += E.a + 1; E.g1 += E.b + 1; }
+  } else if (o < 3 * mm + 3 * m) {
+    const int r = o - 3 * mm;
+    const int d = r / m;
+    E.type = 3 + d;
+    E.a = r - d * m;
+    if (d == 0) E.g1 += E.a + 1; else if (d == 1) E.g2 += E.a + 1; else E.g3 += E.a + 1;
+  } else {
+    E.type = 6;
+  }
+  return E;
+}
+
 }  // namespace pmg
