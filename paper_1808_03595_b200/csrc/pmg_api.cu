@@ -241,7 +241,10 @@ int zs_of(int pc) { int qc = pc + 1; return 3 * qc * qc + 3 * qc + 1; }
 
 // per-record transfer kernels do O(p^3) work on O(p^2) data: size the block to the face
 // (p <= 16: the register-tiled transforms have 3 (p - 1) row threads per record)
-int transfer_threads(int pf) { return pf <= 8 ? 32 : (pf <= 16 ? 64 : 256); }
+#ifndef PMG_TR_NT8
+#define PMG_TR_NT8 32
+#endif
+int transfer_threads(int pf) { return pf <= 8 ? PMG_TR_NT8 : (pf <= 16 ? 64 : 256); }
 
 pmg_status restrict_dev(pmg_ctx* c, int l, const double* rf, double* fc, double* uzero = nullptr) {
   const DevLevel& F = c->D[l];
